@@ -1,0 +1,192 @@
+/*
+ * hyteg_b200.h -- C ABI of the B200-native P1 macro-face multigrid hot path.
+ *
+ * Drop-in boundary for the reference's (arXiv 1805.10167, "hytegrid") matrix-
+ * free multigrid path. Plain C types only: opaque handles, host pointers and
+ * sizes. Every entry point returns a status (0 = ok) and leaves a message for
+ * hyb_last_error(); each status mirrors the reference's exception class:
+ *
+ *   HYB_INVALID_ARGUMENT  std::invalid_argument  (kind / domain / BC mismatch, aliasing)
+ *   HYB_OUT_OF_RANGE      std::out_of_range      (levels)
+ *   HYB_RUNTIME_ERROR     std::runtime_error     (zero diagonal, coarse CG divergence)
+ *   HYB_LOGIC_ERROR       std::logic_error       (exchange protocol errors)
+ *   HYB_CUDA_ERROR / HYB_NCCL_ERROR              (device / collective failures)
+ *
+ * Semantics: operations are stream-ordered on the domain's CUDA stream; every
+ * call that returns host data (download, dot, norms, solve) synchronises, so
+ * results are visible exactly as after the reference's synchronous calls.
+ * Ghost layers are refreshed by the operations that read them (apply, smooth,
+ * transfers), as in the reference.
+ *
+ * Reference paths below are relative to /root/reference/proj.
+ */
+#ifndef HYTEG_B200_H
+#define HYTEG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum hyb_status {
+    HYB_OK = 0,
+    HYB_INVALID_ARGUMENT = 1,
+    HYB_OUT_OF_RANGE = 2,
+    HYB_RUNTIME_ERROR = 3,
+    HYB_LOGIC_ERROR = 4,
+    HYB_CUDA_ERROR = 5,
+    HYB_NCCL_ERROR = 6,
+    HYB_INTERNAL_ERROR = 7
+};
+
+/* DoF flags (include/hytegrid/field.hpp:14-21) */
+enum hyb_flag { HYB_INNER = 1, HYB_DIRICHLET = 2, HYB_NEUMANN = 4, HYB_ALL_FLAGS = 7 };
+/* forms (include/hytegrid/elements.hpp:17-25; P1 LAPLACE and MASS) */
+enum hyb_form { HYB_LAPLACE = 0, HYB_MASS = 1 };
+enum hyb_smoother { HYB_SMOOTH_JACOBI = 0 };
+enum hyb_partitioner { HYB_PARTITION_ROUND_ROBIN = 0, HYB_PARTITION_GREEDY_EDGECUT = 1 };
+
+typedef struct hyb_domain hyb_domain;       /* DistributedDomain + Controller */
+typedef struct hyb_function hyb_function;   /* ScalarFunction (P1)            */
+typedef struct hyb_operator hyb_operator;   /* StencilOperator (P1)           */
+typedef struct hyb_hierarchy hyb_hierarchy; /* GridHierarchy                  */
+
+/* Thread-local message of the last failed call. */
+const char* hyb_last_error(void);
+int hyb_abi_version(void);
+
+/* ---- setup helpers --------------------------------------------------------
+ * hyb_meshgen: src/meshgen.cpp:50-141 (meshgen::unit_triangle .. annulus).
+ *   kind "unit_triangle" | "unit_square" | "unit_square_reversed" |
+ *   "square_ring8" | "channel" (nx, ny, width, height) |
+ *   "annulus" (segments, layers, r_inner, r_outer). Writes NUL-terminated
+ *   mesh text into out (cap bytes); *len = text length (call with cap = 0 to
+ *   size the buffer).
+ * hyb_mesh_perturb: moves marker-0 vertices by U[-frac,frac] x shortest
+ *   incident edge (seeded), rejects inverted triangles.
+ * hyb_mesh_counts: build_setup_graph (src/mesh.cpp:97-263) counts.
+ * hyb_partition: partition_round_robin / partition_greedy_edgecut
+ *   (src/balancing.cpp:19-137); out[#primitives] = rank by primitive ID.
+ */
+int hyb_meshgen(const char* kind, const double* params, int nparams, char* out, int64_t cap, int64_t* len);
+int hyb_mesh_perturb(const char* mesh_text, double frac, uint64_t seed, char* out, int64_t cap, int64_t* len);
+int hyb_mesh_counts(const char* mesh_text, int64_t* nv, int64_t* ne, int64_t* nf);
+int hyb_partition(const char* mesh_text, int ranks, int partitioner, int weight_level, int32_t* out);
+/* host-only stencil assembly (assemble_stencils, src/operators.cpp:342-352):
+ * same layout as hyb_operator_stencil; no device needed */
+int hyb_stencil_host(const char* mesh_text, int form, int level, uint64_t primitive_id, double* out, int cap,
+                     int* len);
+
+/* ---- domain ---------------------------------------------------------------
+ * Replaces DistributedDomain(setup, assignment, ranks) + Controller
+ * (include/hytegrid/primitives.hpp:61-100, communication.hpp:40-56).
+ * assignment: rank per primitive ID (NULL: all rank 0). local_ranks: the
+ * logical ranks this process drives on `device` -- all of them reproduces the
+ * reference's P-ranks-in-one-process model (co-resident ranks exchange
+ * through device copies); one rank per process plus hyb_domain_connect_nccl
+ * runs the same exchange over NCCL.
+ */
+int hyb_domain_create(const char* mesh_text, int world_ranks, const int32_t* assignment, const int32_t* local_ranks,
+                      int n_local, int device, hyb_domain** out);
+int hyb_domain_destroy(hyb_domain* d);
+int hyb_nccl_unique_id(char out[128]);
+int hyb_domain_connect_nccl(hyb_domain* d, const char id[128], int rank);
+/* owned DoFs of the whole domain / of this process at `level` */
+int hyb_domain_owned_count(hyb_domain* d, int level, int64_t* total, int64_t* local);
+/* bytes of one function arena at `level` (storage incl. ghosts/padding) */
+int hyb_domain_arena_bytes(hyb_domain* d, int level, int64_t* bytes);
+int hyb_domain_synchronize(hyb_domain* d);
+/* CUDA-event timing of the hot kernels on the domain stream:
+ * names "apply", "residual", "jacobi", "restrict", "prolongate", "prolongate_add" */
+int hyb_domain_profile(hyb_domain* d, int enable);
+int hyb_domain_timer(hyb_domain* d, const char* name, double* total_ms, int64_t* count);
+int hyb_domain_timer_reset(hyb_domain* d);
+/* CUDA events on the domain stream (16 slots) and elapsed ms between two */
+int hyb_domain_event_record(hyb_domain* d, int slot);
+int hyb_domain_event_elapsed(hyb_domain* d, int a, int b, double* ms);
+/* kernels launched by this library so far (process-wide) */
+int hyb_kernel_launches(int64_t* count);
+/* coordinates (x, y interleaved) of owned DoFs: for_each_owned_coord
+ * (src/layout.cpp:239-282); global_order 1: whole domain in ID order */
+int hyb_owned_coords(hyb_domain* d, int level, int global_order, double* xy, int64_t n);
+
+/* ---- functions ------------------------------------------------------------
+ * ScalarFunction(name, domain, P1, min, max, bc) (include/hytegrid/function.hpp:19-20);
+ * bc: marker -> flag pairs, unmapped non-zero markers are DIRICHLET
+ * (field.hpp:29-34). Storage is zero-initialised.
+ * upload / download: owned DoFs in GlobalDoFMap order (primitives by ID, each
+ * in for_each_owned order; numbering.hpp:41-43) -- global_order 1 for the
+ * whole domain, 0 for this process's primitives only; upload writes only
+ * DoFs whose flag is in mask.
+ */
+int hyb_function_create(hyb_domain* d, const char* name, int min_level, int max_level, const int32_t* bc_markers,
+                        const uint8_t* bc_flags, int n_bc, hyb_function** out);
+int hyb_function_destroy(hyb_function* f);
+int hyb_function_upload(hyb_function* f, int level, const double* host, int64_t n, int global_order, uint8_t mask);
+int hyb_function_download(hyb_function* f, int level, double* host, int64_t n, int global_order);
+int hyb_function_flags(hyb_function* f, int level, uint8_t* flags, int64_t n, int global_order);
+/* interpolate(f, const, level, mask) (function.hpp:55-56) */
+int hyb_interpolate_const(hyb_function* f, double value, int level, uint8_t mask);
+/* device counter-based U[lo,hi] keyed on (seed, stream, DoF identity) */
+int hyb_interpolate_random(hyb_function* f, int level, uint64_t seed, uint64_t stream, double lo, double hi,
+                           uint8_t mask);
+/* sync / sync_all (function.hpp:79-81): full schedule V->E, E->F, F->E, E->V */
+int hyb_sync(hyb_function* f, int level);
+
+/* ---- operators ------------------------------------------------------------
+ * StencilOperator(domain, form, P1, min, max, bc) (operators.hpp:76-88).
+ * Stencil readback for tests: face 7 terms W NW S C N SE E + diag; edge up to
+ * 7 terms + diag; vertex 1 + #edges terms + diag.
+ */
+int hyb_operator_create(hyb_domain* d, int form, int min_level, int max_level, const int32_t* bc_markers,
+                        const uint8_t* bc_flags, int n_bc, hyb_operator** out);
+int hyb_operator_destroy(hyb_operator* A);
+int hyb_operator_stencil(hyb_operator* A, int level, uint64_t primitive_id, double* out, int cap, int* len);
+
+/* apply(A, ctl, src, dst, level, mask)            operators.hpp:108-109 */
+int hyb_apply(hyb_operator* A, hyb_function* src, hyb_function* dst, int level, uint8_t mask);
+/* r := rhs - A x (apply + assign(1, rhs, -1, r, r), solvers.cpp:418-419), fused */
+int hyb_residual(hyb_operator* A, hyb_function* rhs, hyb_function* x, hyb_function* r, int level);
+/* smooth_jacobi(A, ctl, rhs, x, omega, level)     operators.hpp:113-114 */
+int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level);
+/* diagonal(A, d, level)                           operators.hpp:125 */
+int hyb_diagonal(hyb_operator* A, hyb_function* d, int level);
+/* prolongate(ctl, coarse, fine, coarse_level, mask) solvers.hpp:26-27 */
+int hyb_prolongate(hyb_function* coarse, hyb_function* fine, int coarse_level, uint8_t mask);
+/* prolongate + add_scaled(fine, 1, .) fused (solvers.cpp:424-425) */
+int hyb_prolongate_add(hyb_function* coarse, hyb_function* fine, int coarse_level, uint8_t mask);
+/* restrict_to_coarse(ctl, fine, coarse, coarse_level, mask) solvers.hpp:32-33 */
+int hyb_restrict(hyb_function* fine, hyb_function* coarse, int coarse_level, uint8_t mask);
+/* assign / add_scaled / dot / norm2 / max_abs     function.hpp:60-74 */
+int hyb_assign(double alpha, hyb_function* x1, double beta, hyb_function* x2, hyb_function* dst, int level,
+               uint8_t mask);
+int hyb_add_scaled(hyb_function* dst, double gamma, hyb_function* y, int level, uint8_t mask);
+int hyb_dot(hyb_function* a, hyb_function* b, int level, double* out);
+int hyb_norm2(hyb_function* a, int level, double* out);
+int hyb_max_abs(hyb_function* a, int level, double* out);
+
+/* ---- multigrid driver -----------------------------------------------------
+ * GridHierarchy(domain, ctl, form, min, max, bc) (solvers.hpp:81-102) with a
+ * selectable smoother (weighted Jacobi, omega) and a device-resident coarse
+ * CG (tolerance, max iterations; < 0 = #coarse DoFs + 100 as the reference).
+ */
+int hyb_hierarchy_create(hyb_domain* d, int form, int min_level, int max_level, const int32_t* bc_markers,
+                         const uint8_t* bc_flags, int n_bc, int smoother, double omega, double coarse_tol,
+                         int coarse_max_iter, hyb_hierarchy** out);
+int hyb_hierarchy_destroy(hyb_hierarchy* h);
+int hyb_hierarchy_vcycle(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, int nu_pre, int nu_post);
+int hyb_hierarchy_residual_norm(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, double* out);
+/* residuals[0..*n_out): ||rhs - A x|| before each cycle and after the last */
+int hyb_hierarchy_solve(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, double tol, int max_cycles,
+                        int nu_pre, int nu_post, double* residuals, int* n_out, int* converged);
+
+/* ---- pinned host memory (end-to-end transfers) ---- */
+int hyb_host_alloc(int64_t bytes, void** out);
+int hyb_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HYTEG_B200_H */

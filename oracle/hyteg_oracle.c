@@ -1,0 +1,940 @@
+/*
+ * TEST INFRASTRUCTURE ONLY -- see hyteg_oracle.h.
+ *
+ * Plain-C restatement of the reference hot path. Every function cites the
+ * reference code it restates (paths relative to /root/reference/proj). Built
+ * with -ffp-contract=off: products and sums round separately, as in the
+ * reference's baseline x86-64 Release build.
+ */
+#include "hyteg_oracle.h"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { F_INNER = 1, F_DIRICHLET = 2, F_NEUMANN = 4 };
+
+static char g_err[512];
+const char* og_last_error(void) { return g_err; }
+static int fail(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return 1;
+}
+
+typedef struct { double x, y; } V2;
+static V2 v_sub(V2 a, V2 b) { V2 r = {a.x - b.x, a.y - b.y}; return r; }
+static V2 v_add(V2 a, V2 b) { V2 r = {a.x + b.x, a.y + b.y}; return r; }
+static V2 v_scl(double s, V2 a) { V2 r = {s * a.x, s * a.y}; return r; }
+static double v_cross(V2 a, V2 b) { return a.x * b.y - a.y * b.x; }
+static double v_dot(V2 a, V2 b) { return a.x * b.x + a.y * b.y; }
+
+typedef struct {
+    V2 p;
+    int marker, ne, nf;
+    int e[32];      /* incident edge IDs, ascending */
+    int f[32];      /* incident face IDs, ascending */
+    int corner[32]; /* local corner index in face f[i] */
+    int flank[32][2];
+} OV;
+typedef struct {
+    int v[2], marker, nf;
+    int f[2], slot[2], al[2];
+} OE;
+typedef struct {
+    int v[3], e[3], al[3];
+    V2 c[3];
+} OF;
+
+typedef struct {
+    long base, dk;
+    double coeff;
+} ETerm;
+
+struct og_session {
+    int nv, ne, nf, np;
+    OV* V;
+    OE* E;
+    OF* F;
+    int lmin, lmax, nfun;
+    int nbc, bcm[32];
+    unsigned char bcf[32];
+    int64_t** off;   /* [lvl][id] arena offset */
+    int64_t* asize;  /* [lvl] arena size */
+    double*** val;   /* [fun][lvl] arena */
+    double** fst;    /* [lvl][fi*8] face terms W NW S C N SE E + diag */
+    ETerm** est;     /* [lvl][ei*7] */
+    int** ent;       /* [lvl][ei] number of edge terms */
+    double** ediag;  /* [lvl][ei] */
+    double** vst;    /* [lvl] flat: per vertex 1+ne terms + diag */
+    int64_t* vcoff;  /* per vertex offset in vst */
+};
+
+/* ------------------------------------------------------------------ mesh
+ * parse_mesh (src/mesh.cpp:22-83) and build_setup_graph (src/mesh.cpp:97-263) */
+static const int kSlotCorner[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+static const int kCornerSlots[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+
+static int next_line(const char** p, char* buf, size_t cap) {
+    while (**p) {
+        const char* s = *p;
+        const char* e = strchr(s, '\n');
+        size_t len = e ? (size_t)(e - s) : strlen(s);
+        *p = e ? e + 1 : s + len;
+        if (len >= cap) len = cap - 1;
+        memcpy(buf, s, len);
+        buf[len] = 0;
+        char* h = strchr(buf, '#');
+        if (h) *h = 0;
+        for (char* q = buf; *q; ++q)
+            if (*q != ' ' && *q != '\t' && *q != '\r') return 1;
+    }
+    return 0;
+}
+
+typedef struct { int a, b, t; } Pair;
+static int pair_cmp(const void* x, const void* y) {
+    const Pair* p = x;
+    const Pair* q = y;
+    if (p->a != q->a) return p->a < q->a ? -1 : 1;
+    if (p->b != q->b) return p->b < q->b ? -1 : 1;
+    return p->t < q->t ? -1 : (p->t > q->t);
+}
+
+static int build_graph(og_session* s, const char* text) {
+    const char* p = text;
+    char line[512];
+    long nv, nt;
+    if (!next_line(&p, line, sizeof line) || sscanf(line, "%ld %ld", &nv, &nt) != 2) return fail("bad header");
+    V2* pos = calloc((size_t)nv + 1, sizeof(V2));
+    int* mk = calloc((size_t)nv + 1, sizeof(int));
+    int (*tri)[3] = calloc((size_t)nt + 1, sizeof *tri);
+    for (long i = 0; i < nv; ++i) {
+        if (!next_line(&p, line, sizeof line) || sscanf(line, "%lf %lf %d", &pos[i].x, &pos[i].y, &mk[i]) != 3)
+            return fail("bad vertex line");
+    }
+    for (long i = 0; i < nt; ++i) {
+        int r;
+        if (!next_line(&p, line, sizeof line) || sscanf(line, "%d %d %d %d", &tri[i][0], &tri[i][1], &tri[i][2], &r) != 4)
+            return fail("bad triangle line");
+        const double a2 = v_cross(v_sub(pos[tri[i][1]], pos[tri[i][0]]), v_sub(pos[tri[i][2]], pos[tri[i][0]]));
+        if (a2 == 0.0) return fail("degenerate triangle");
+        if (a2 < 0.0) { int t = tri[i][1]; tri[i][1] = tri[i][2]; tri[i][2] = t; }
+    }
+    /* edges: sorted vertex pairs, lexicographic order fixes IDs */
+    Pair* pr = malloc(sizeof(Pair) * (size_t)(3 * nt + 1));
+    for (long i = 0; i < nt; ++i)
+        for (int sl = 0; sl < 3; ++sl) {
+            int a = tri[i][kSlotCorner[sl][0]], b = tri[i][kSlotCorner[sl][1]];
+            Pair q = {a < b ? a : b, a < b ? b : a, (int)i};
+            pr[3 * i + sl] = q;
+        }
+    qsort(pr, (size_t)(3 * nt), sizeof(Pair), pair_cmp);
+    int ne = 0;
+    for (long i = 0; i < 3 * nt; ++i)
+        if (i == 0 || pr[i].a != pr[i - 1].a || pr[i].b != pr[i - 1].b) ++ne;
+    s->nv = (int)nv;
+    s->ne = ne;
+    s->nf = (int)nt;
+    s->np = s->nv + s->ne + s->nf;
+    s->V = calloc((size_t)nv + 1, sizeof(OV));
+    s->E = calloc((size_t)ne + 1, sizeof(OE));
+    s->F = calloc((size_t)nt + 1, sizeof(OF));
+    const int EB = (int)nv, FB = (int)nv + ne;
+    int ei = -1;
+    for (long i = 0; i < 3 * nt; ++i) {
+        if (i == 0 || pr[i].a != pr[i - 1].a || pr[i].b != pr[i - 1].b) {
+            ++ei;
+            s->E[ei].v[0] = pr[i].a;
+            s->E[ei].v[1] = pr[i].b;
+        }
+        OE* e = &s->E[ei];
+        if (e->nf >= 2) return fail("non-manifold mesh");
+        e->f[e->nf++] = FB + pr[i].t; /* triangles ascending within a pair */
+    }
+    for (long i = 0; i < nt; ++i) {
+        OF* f = &s->F[i];
+        for (int k = 0; k < 3; ++k) {
+            f->v[k] = tri[i][k];
+            f->c[k] = pos[tri[i][k]];
+        }
+        for (int sl = 0; sl < 3; ++sl) {
+            int a = tri[i][kSlotCorner[sl][0]], b = tri[i][kSlotCorner[sl][1]];
+            int lo = a < b ? a : b, hi = a < b ? b : a;
+            for (int j = 0; j < ne; ++j) /* small meshes only: linear search is fine */
+                if (s->E[j].v[0] == lo && s->E[j].v[1] == hi) { f->e[sl] = EB + j; break; }
+            f->al[sl] = a < b;
+        }
+    }
+    for (int j = 0; j < ne; ++j) {
+        OE* e = &s->E[j];
+        const int ma = mk[e->v[0]], mb = mk[e->v[1]];
+        e->marker = (e->nf == 1 && ma != 0 && mb != 0) ? (ma > mb ? ma : mb) : 0;
+        for (int q = 0; q < e->nf; ++q) {
+            const OF* f = &s->F[e->f[q] - FB];
+            for (int sl = 0; sl < 3; ++sl)
+                if (f->e[sl] == EB + j) { e->slot[q] = sl; e->al[q] = f->al[sl]; }
+        }
+    }
+    for (long v = 0; v < nv; ++v) { s->V[v].p = pos[v]; s->V[v].marker = mk[v]; }
+    for (int j = 0; j < ne; ++j)
+        for (int end = 0; end < 2; ++end) {
+            OV* v = &s->V[s->E[j].v[end]];
+            if (v->ne >= 32) return fail("vertex degree > 32");
+            v->e[v->ne++] = EB + j;
+        }
+    for (long i = 0; i < nt; ++i)
+        for (int k = 0; k < 3; ++k) {
+            OV* v = &s->V[s->F[i].v[k]];
+            if (v->nf >= 32) return fail("vertex degree > 32");
+            v->f[v->nf] = FB + (int)i;
+            v->corner[v->nf] = k;
+            v->flank[v->nf][0] = s->F[i].e[kCornerSlots[k][0]];
+            v->flank[v->nf][1] = s->F[i].e[kCornerSlots[k][1]];
+            v->nf++;
+        }
+    free(pos);
+    free(mk);
+    free(tri);
+    free(pr);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ flags
+ * BoundaryConditions::flag_for (include/hytegrid/field.hpp:29-34); P1 owned
+ * flags are uniform per primitive (src/field.cpp:15-120) */
+static int flag_for(const og_session* s, int marker) {
+    if (marker == 0) return F_INNER;
+    for (int i = 0; i < s->nbc; ++i)
+        if (s->bcm[i] == marker) return s->bcf[i];
+    return F_DIRICHLET;
+}
+static int kind_of(const og_session* s, int id) { return id < s->nv ? 0 : id < s->nv + s->ne ? 1 : 2; }
+static int owned_flag(const og_session* s, int id) {
+    switch (kind_of(s, id)) {
+    case 0: return flag_for(s, s->V[id].marker);
+    case 1: return flag_for(s, s->E[id - s->nv].marker);
+    default: return F_INNER;
+    }
+}
+
+/* ------------------------------------------------------------------ layout
+ * ROW_MAJOR index (include/hytegrid/indexing.hpp:73-79), border walks
+ * (src/indexing.cpp:61-72), storage sizes (src/layout.cpp:66-138) */
+static int64_t fidx(int W, int c, int r) { return (int64_t)r * W - (int64_t)r * (r - 1) / 2 + c; }
+static void border_dof(int W, int slot, int off, int k, int* c, int* r) {
+    if (slot == 0) { *c = k; *r = off; }
+    else if (slot == 1) { *c = off; *r = k; }
+    else { *c = (W - 1 - off) - k; *r = k; }
+}
+static double* arena(og_session* s, int f, int level) { return s->val[f][level - s->lmin]; }
+static double* prim(og_session* s, int f, int level, int id) {
+    return arena(s, f, level) + s->off[level - s->lmin][id];
+}
+
+/* ------------------------------------------------------------------ stencils
+ * local_stiffness P1 LAPLACE (src/elements.cpp:17-48), assemble_face /
+ * assemble_edge / assemble_vertex (src/operators.cpp:95-263) */
+typedef struct { double m[3][3]; } M3;
+static M3 elem(V2 t0, V2 t1, V2 t2) {
+    V2 u1 = v_sub(t1, t0), u2 = v_sub(t2, t0);
+    double det = v_cross(u1, u2);
+    double area = fabs(det) / 2.0;
+    V2 g[3];
+    g[1].x = u2.y / det; g[1].y = -u2.x / det;
+    g[2].x = -u1.y / det; g[2].y = u1.x / det;
+    g[0].x = -g[1].x - g[2].x; g[0].y = -g[1].y - g[2].y;
+    M3 m;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j <= i; ++j) { m.m[i][j] = area * v_dot(g[i], g[j]); m.m[j][i] = m.m[i][j]; }
+    return m;
+}
+static void cell_mats(const V2 c[3], int level, M3* up, M3* down) {
+    const double inv = 1.0 / (double)(1 << level);
+    V2 u = v_scl(inv, v_sub(c[1], c[0])), v = v_scl(inv, v_sub(c[2], c[0])), z = {0, 0};
+    *up = elem(z, u, v);
+    *down = elem(u, v, v_add(u, v));
+}
+static const int UPD[3][2] = {{0, 0}, {1, 0}, {0, 1}};
+static const int DND[3][2] = {{1, 0}, {0, 1}, {1, 1}};
+typedef struct { int up, c, r; } Cell;
+static void vcells(int c, int r, Cell out[6]) {
+    Cell t[6] = {{1, c, r}, {1, c - 1, r}, {1, c, r - 1}, {0, c - 1, r}, {0, c, r - 1}, {0, c - 1, r - 1}};
+    memcpy(out, t, sizeof t);
+}
+static int inside(Cell t, int n) { return t.c >= 0 && t.r >= 0 && t.c + t.r <= (t.up ? n - 1 : n - 2); }
+static int irecv_of(Cell t, int c, int r) {
+    const int (*d)[2] = t.up ? UPD : DND;
+    int ir = -1;
+    for (int i = 0; i < 3; ++i)
+        if (t.c + d[i][0] == c && t.r + d[i][1] == r) ir = i;
+    return ir;
+}
+
+static void face_stencil(const OF* f, int level, double out[8]) {
+    static const int order[7][2] = {{-1, 0}, {-1, 1}, {0, -1}, {0, 0}, {0, 1}, {1, -1}, {1, 0}};
+    M3 up, dn;
+    cell_mats(f->c, level, &up, &dn);
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    Cell cs[6];
+    vcells(0, 0, cs);
+    for (int q = 0; q < 6; ++q) {
+        const M3* M = cs[q].up ? &up : &dn;
+        const int (*d)[2] = cs[q].up ? UPD : DND;
+        const int ir = irecv_of(cs[q], 0, 0);
+        for (int j = 0; j < 3; ++j) {
+            const int dc = cs[q].c + d[j][0], dr = cs[q].r + d[j][1];
+            for (int k = 0; k < 7; ++k)
+                if (order[k][0] == dc && order[k][1] == dr) acc[k] += M->m[ir][j];
+        }
+    }
+    for (int k = 0; k < 7; ++k) out[k] = acc[k];
+    out[7] = acc[3];
+}
+
+static int eterm_cmp(const void* a, const void* b) {
+    const ETerm* p = a;
+    const ETerm* q = b;
+    if (p->base != q->base) return p->base < q->base ? -1 : 1;
+    return p->dk < q->dk ? -1 : (p->dk > q->dk);
+}
+
+static int edge_stencil(og_session* s, const OE* e, int level, ETerm out[7], double* diag) {
+    const int n = 1 << level, W = n + 1;
+    int nt = 0;
+    if (n < 2) { *diag = 0; return 0; }
+    for (int fi = 0; fi < e->nf; ++fi) {
+        const OF* f = &s->F[e->f[fi] - s->nv - s->ne];
+        M3 up, dn;
+        cell_mats(f->c, level, &up, &dn);
+        const int slot = e->slot[fi], al = e->al[fi];
+        const int w0 = al ? 1 : n - 1;
+        int rc, rr;
+        border_dof(W, slot, 0, w0, &rc, &rr);
+        const long halo = (long)(n + 1) + (long)fi * (2 * n + 1);
+        Cell cs[6];
+        vcells(rc, rr, cs);
+        for (int q = 0; q < 6; ++q) {
+            if (!inside(cs[q], n)) continue;
+            const M3* M = cs[q].up ? &up : &dn;
+            const int (*d)[2] = cs[q].up ? UPD : DND;
+            const int ir = irecv_of(cs[q], rc, rr);
+            for (int j = 0; j < 3; ++j) {
+                const int c = cs[q].c + d[j][0], r = cs[q].r + d[j][1];
+                const int o = slot == 0 ? r : slot == 1 ? c : n - (c + r);
+                const int w = slot == 0 ? c : r;
+                long base, entry;
+                if (o == 0) { base = 0; entry = al ? w : n - w; }
+                else { base = halo + W; entry = al ? w : (W - o - 1) - w; }
+                const long dk = entry - 1;
+                int k;
+                for (k = 0; k < nt; ++k)
+                    if (out[k].base == base && out[k].dk == dk) break;
+                if (k == nt) {
+                    if (nt == 7) { fail("edge stencil too large"); return -1; }
+                    out[nt].base = base; out[nt].dk = dk; out[nt].coeff = 0.0; ++nt;
+                }
+                out[k].coeff += M->m[ir][j];
+            }
+        }
+    }
+    qsort(out, (size_t)nt, sizeof(ETerm), eterm_cmp);
+    *diag = 0;
+    for (int k = 0; k < nt; ++k)
+        if (out[k].base == 0 && out[k].dk == 0) *diag = out[k].coeff;
+    return nt;
+}
+
+static void vertex_stencil(og_session* s, int vid, int level, double* out) {
+    const OV* v = &s->V[vid];
+    const int n = 1 << level;
+    for (int i = 0; i <= v->ne; ++i) out[i] = 0.0;
+    for (int q = 0; q < v->nf; ++q) {
+        const OF* f = &s->F[v->f[q] - s->nv - s->ne];
+        M3 up, dn;
+        cell_mats(f->c, level, &up, &dn);
+        const int ci = v->corner[q];
+        const int cc = ci == 1 ? n - 1 : 0, cr = ci == 2 ? n - 1 : 0;
+        for (int j = 0; j < 3; ++j) {
+            const double coeff = up.m[ci][j];
+            if (j == ci) { out[0] += coeff; continue; }
+            const int c = cc + UPD[j][0], r = cr + UPD[j][1];
+            int pick = -1;
+            for (int t = 0; t < 2; ++t) {
+                const int sl = kCornerSlots[ci][t];
+                const int o = sl == 0 ? r : sl == 1 ? c : n - (c + r);
+                if (o == 0) { pick = sl; break; }
+            }
+            const int eid = v->flank[q][pick == kCornerSlots[ci][0] ? 0 : 1];
+            for (int k = 0; k < v->ne; ++k)
+                if (v->e[k] == eid) { out[1 + k] += coeff; break; }
+        }
+    }
+    out[v->ne + 1] = out[0];
+}
+
+/* ------------------------------------------------------------------ session */
+og_session* og_create(const char* mesh_text, int min_level, int max_level, const int* bc_markers,
+                      const unsigned char* bc_flags, int nbc, int nfuncs) {
+    og_session* s = calloc(1, sizeof *s);
+    if (build_graph(s, mesh_text)) { free(s); return NULL; }
+    s->lmin = min_level;
+    s->lmax = max_level;
+    s->nfun = nfuncs;
+    s->nbc = nbc < 32 ? nbc : 32;
+    for (int i = 0; i < s->nbc; ++i) { s->bcm[i] = bc_markers[i]; s->bcf[i] = bc_flags[i]; }
+    const int nl = max_level - min_level + 1;
+    s->off = calloc((size_t)nl, sizeof(int64_t*));
+    s->asize = calloc((size_t)nl, sizeof(int64_t));
+    s->fst = calloc((size_t)nl, sizeof(double*));
+    s->est = calloc((size_t)nl, sizeof(ETerm*));
+    s->ent = calloc((size_t)nl, sizeof(int*));
+    s->ediag = calloc((size_t)nl, sizeof(double*));
+    s->vst = calloc((size_t)nl, sizeof(double*));
+    s->vcoff = calloc((size_t)s->nv + 1, sizeof(int64_t));
+    int64_t vc = 0;
+    for (int v = 0; v < s->nv; ++v) { s->vcoff[v] = vc; vc += 2 + s->V[v].ne; }
+    for (int L = min_level; L <= max_level; ++L) {
+        const int li = L - min_level, n = 1 << L, W = n + 1;
+        s->off[li] = calloc((size_t)s->np, sizeof(int64_t));
+        int64_t pos = 0;
+        for (int id = 0; id < s->np; ++id) {
+            s->off[li][id] = pos;
+            switch (kind_of(s, id)) {
+            case 0: pos += 1 + s->V[id].ne; break;
+            case 1: pos += (n + 1) + (int64_t)s->E[id - s->nv].nf * (2 * n + 1); break;
+            default: pos += (int64_t)W * (W + 1) / 2; break;
+            }
+        }
+        s->asize[li] = pos;
+        s->fst[li] = calloc((size_t)s->nf * 8 + 1, sizeof(double));
+        for (int i = 0; i < s->nf; ++i) face_stencil(&s->F[i], L, s->fst[li] + 8 * i);
+        s->est[li] = calloc((size_t)s->ne * 7 + 1, sizeof(ETerm));
+        s->ent[li] = calloc((size_t)s->ne + 1, sizeof(int));
+        s->ediag[li] = calloc((size_t)s->ne + 1, sizeof(double));
+        for (int i = 0; i < s->ne; ++i) {
+            int nt = edge_stencil(s, &s->E[i], L, s->est[li] + 7 * i, &s->ediag[li][i]);
+            if (nt < 0) return NULL;
+            s->ent[li][i] = nt;
+        }
+        s->vst[li] = calloc((size_t)vc + 1, sizeof(double));
+        for (int v = 0; v < s->nv; ++v) vertex_stencil(s, v, L, s->vst[li] + s->vcoff[v]);
+    }
+    s->val = calloc((size_t)nfuncs, sizeof(double**));
+    for (int f = 0; f < nfuncs; ++f) {
+        s->val[f] = calloc((size_t)nl, sizeof(double*));
+        for (int li = 0; li < nl; ++li) s->val[f][li] = calloc((size_t)s->asize[li] + 1, sizeof(double));
+    }
+    return s;
+}
+
+void og_destroy(og_session* s) {
+    if (!s) return;
+    const int nl = s->lmax - s->lmin + 1;
+    for (int f = 0; f < s->nfun; ++f) {
+        for (int li = 0; li < nl; ++li) free(s->val[f][li]);
+        free(s->val[f]);
+    }
+    for (int li = 0; li < nl; ++li) {
+        free(s->off[li]); free(s->fst[li]); free(s->est[li]); free(s->ent[li]); free(s->ediag[li]); free(s->vst[li]);
+    }
+    free(s->val); free(s->off); free(s->asize); free(s->fst); free(s->est); free(s->ent); free(s->ediag);
+    free(s->vst); free(s->vcoff); free(s->V); free(s->E); free(s->F); free(s);
+}
+
+static int check(og_session* s, int f, int level) {
+    if (f < 0 || f >= s->nfun) return fail("bad function index %d", f);
+    if (level < s->lmin || level > s->lmax) return fail("level %d outside [%d, %d]", level, s->lmin, s->lmax);
+    return 0;
+}
+
+/* owned traversal: for_each_owned (src/layout.cpp:176-237) -- vertex slot 0;
+ * edge 1..n-1; face r = 1..n-2, c = 1..n-1-r. Calls fn(slot) in order. */
+#define FOR_OWNED(s, id, level, SLOT, BODY)                                          \
+    do {                                                                             \
+        const int n_ = 1 << (level), W_ = n_ + 1;                                    \
+        const int k_ = kind_of(s, id);                                               \
+        if (k_ == 0) { const int64_t SLOT = 0; BODY; }                               \
+        else if (k_ == 1) { for (int64_t SLOT = 1; SLOT <= n_ - 1; ++SLOT) { BODY; } } \
+        else {                                                                       \
+            for (int r_ = 1; r_ <= n_ - 2; ++r_)                                     \
+                for (int c_ = 1; c_ + r_ <= n_ - 1; ++c_) {                          \
+                    const int64_t SLOT = fidx(W_, c_, r_);                           \
+                    BODY;                                                            \
+                }                                                                    \
+        }                                                                            \
+    } while (0)
+
+int64_t og_owned(og_session* s, int level) {
+    const int64_t n = (int64_t)1 << level;
+    return s->nv + (int64_t)s->ne * (n - 1) + (int64_t)s->nf * ((n - 1) * (n - 2) / 2);
+}
+
+static int move(og_session* s, int f, int level, double* v, int to_field) {
+    if (check(s, f, level)) return 1;
+    int64_t pos = 0;
+    for (int id = 0; id < s->np; ++id) {
+        double* p = prim(s, f, level, id);
+        FOR_OWNED(s, id, level, slot, { if (to_field) p[slot] = v[pos]; else v[pos] = p[slot]; ++pos; });
+    }
+    return 0;
+}
+int og_set(og_session* s, int f, int level, const double* v) { return move(s, f, level, (double*)v, 1); }
+int og_get(og_session* s, int f, int level, double* v) { return move(s, f, level, v, 0); }
+
+int og_flags(og_session* s, int level, unsigned char* out) {
+    int64_t pos = 0;
+    for (int id = 0; id < s->np; ++id) {
+        const int fl = owned_flag(s, id);
+        FOR_OWNED(s, id, level, slot, { (void)slot; out[pos++] = (unsigned char)fl; });
+    }
+    return 0;
+}
+
+int og_stencil(og_session* s, int64_t id, int level, double* out, int* len) {
+    if (level < s->lmin || level > s->lmax || id < 0 || id >= s->np) return fail("no stencil");
+    const int li = level - s->lmin;
+    int n = 0;
+    switch (kind_of(s, (int)id)) {
+    case 0: {
+        const int ne = s->V[id].ne;
+        for (int i = 0; i <= ne + 1; ++i) out[n++] = s->vst[li][s->vcoff[id] + i];
+        break;
+    }
+    case 1: {
+        const int ei = (int)id - s->nv;
+        for (int i = 0; i < s->ent[li][ei]; ++i) out[n++] = s->est[li][7 * ei + i].coeff;
+        out[n++] = s->ediag[li][ei];
+        break;
+    }
+    default:
+        for (int i = 0; i < 8; ++i) out[n++] = s->fst[li][8 * (id - s->nv - s->ne) + i];
+    }
+    *len = n;
+    return 0;
+}
+
+/* keyed U[lo,hi] of the device generator (paper_1805_10167_b200/csrc/kernels.cu) */
+static uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+int og_keyed_uniform(og_session* s, int level, uint64_t seed, uint64_t stream, double lo, double hi, double* out) {
+    const uint64_t sk = mix64(mix64(seed) ^ (stream * 0xD1B54A32D192ED03ull));
+    const int n = 1 << level;
+    int64_t pos = 0;
+    for (int id = 0; id < s->np; ++id) {
+        const int k = kind_of(s, id);
+        if (k == 0) {
+            uint64_t h = mix64(sk ^ mix64((uint64_t)id << 40));
+            out[pos++] = lo + (hi - lo) * ((double)(h >> 11) * 0x1p-53);
+        } else if (k == 1) {
+            for (int q = 1; q <= n - 1; ++q) {
+                uint64_t h = mix64(sk ^ mix64(((uint64_t)id << 40) ^ ((uint64_t)q << 20)));
+                out[pos++] = lo + (hi - lo) * ((double)(h >> 11) * 0x1p-53);
+            }
+        } else {
+            for (int r = 1; r <= n - 2; ++r)
+                for (int c = 1; c + r <= n - 1; ++c) {
+                    uint64_t h = mix64(sk ^ mix64(((uint64_t)id << 40) ^ ((uint64_t)c << 20) ^ (uint64_t)r));
+                    out[pos++] = lo + (hi - lo) * ((double)(h >> 11) * 0x1p-53);
+                }
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ sync
+ * full_sync_schedule V->E, E->F, F->E, E->V (src/communication.cpp:54-62)
+ * with FieldPackInfo pack/unpack (src/communication.cpp:272-403); one rank,
+ * every pair is a local_copy (pack + unpack, :64-72). */
+int og_sync(og_session* s, int f, int level) {
+    if (check(s, f, level)) return 1;
+    const int n = 1 << level, W = n + 1;
+    const int EB = s->nv, FB = s->nv + s->ne;
+    for (int j = 0; j < s->ne; ++j) { /* V->E: line ends = vertex values */
+        double* L = prim(s, f, level, EB + j);
+        L[0] = prim(s, f, level, s->E[j].v[0])[0];
+        L[n] = prim(s, f, level, s->E[j].v[1])[0];
+    }
+    for (int i = 0; i < s->nf; ++i) { /* E->F: edge line onto the face border */
+        double* fv = prim(s, f, level, FB + i);
+        for (int sl = 0; sl < 3; ++sl) {
+            const double* L = prim(s, f, level, s->F[i].e[sl]);
+            for (int k = 0; k < W; ++k) {
+                int c, r;
+                border_dof(W, sl, 0, s->F[i].al[sl] ? k : W - 1 - k, &c, &r);
+                fv[fidx(W, c, r)] = L[k];
+            }
+        }
+    }
+    for (int j = 0; j < s->ne; ++j) { /* F->E: halo rows 0 and 1, edge order */
+        double* ev = prim(s, f, level, EB + j);
+        const OE* e = &s->E[j];
+        for (int q = 0; q < e->nf; ++q) {
+            const double* fv = prim(s, f, level, e->f[q]);
+            int64_t pos = (n + 1) + (int64_t)q * (2 * n + 1);
+            for (int off = 0; off < 2; ++off) {
+                const int len = W - off;
+                for (int k = 0; k < len; ++k) {
+                    int c, r;
+                    border_dof(W, e->slot[q], off, e->al[q] ? k : len - 1 - k, &c, &r);
+                    ev[pos++] = fv[fidx(W, c, r)];
+                }
+            }
+        }
+    }
+    for (int v = 0; v < s->nv; ++v) { /* E->V: first interior line value */
+        double* vv = prim(s, f, level, v);
+        for (int q = 0; q < s->V[v].ne; ++q) {
+            const int eid = s->V[v].e[q];
+            const double* L = prim(s, f, level, eid);
+            vv[1 + q] = L[s->E[eid - EB].v[0] == v ? 1 : n - 1];
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ rows
+ * visit_rows (src/operators.cpp:270-320): per owned row, the stencil terms in
+ * table order starting from acc = 0. */
+static double row_acc(og_session* s, int level, int id, int64_t slot, const double* x, int c, int r) {
+    const int li = level - s->lmin, n = 1 << level, W = n + 1;
+    double acc = 0;
+    switch (kind_of(s, id)) {
+    case 0: {
+        const double* st = s->vst[li] + s->vcoff[id];
+        for (int j = 0; j <= s->V[id].ne; ++j) acc += st[j] * x[j];
+        break;
+    }
+    case 1: {
+        const int ei = id - s->nv;
+        for (int t = 0; t < s->ent[li][ei]; ++t) {
+            const ETerm* e = &s->est[li][7 * ei + t];
+            acc += e->coeff * x[e->base + slot + e->dk];
+        }
+        break;
+    }
+    default: {
+        static const int o[7][2] = {{-1, 0}, {-1, 1}, {0, -1}, {0, 0}, {0, 1}, {1, -1}, {1, 0}};
+        const double* st = s->fst[li] + 8 * (id - s->nv - s->ne);
+        for (int t = 0; t < 7; ++t) acc += st[t] * x[fidx(W, c + o[t][0], r + o[t][1])];
+    }
+    }
+    return acc;
+}
+static double row_diag(og_session* s, int level, int id) {
+    const int li = level - s->lmin;
+    switch (kind_of(s, id)) {
+    case 0: return s->vst[li][s->vcoff[id] + s->V[id].ne + 1];
+    case 1: return s->ediag[li][id - s->nv];
+    default: return s->fst[li][8 * (id - s->nv - s->ne) + 7];
+    }
+}
+
+/* iterate rows of one primitive in owned order, giving (slot, c, r) */
+#define FOR_ROWS(s, id, level, SLOT, C, R, BODY)                                       \
+    do {                                                                               \
+        const int n_ = 1 << (level), W_ = n_ + 1;                                      \
+        const int k_ = kind_of(s, id);                                                 \
+        if (k_ == 0) { const int64_t SLOT = 0; const int C = 0, R = 0; BODY; }         \
+        else if (k_ == 1) {                                                            \
+            for (int64_t SLOT = 1; SLOT <= n_ - 1; ++SLOT) { const int C = 0, R = 0; BODY; } \
+        } else {                                                                       \
+            for (int R = 1; R <= n_ - 2; ++R)                                          \
+                for (int C = 1; C + R <= n_ - 1; ++C) {                                \
+                    const int64_t SLOT = fidx(W_, C, R);                               \
+                    BODY;                                                              \
+                }                                                                      \
+        }                                                                              \
+    } while (0)
+
+/* apply (src/operators.cpp:379-419) */
+int og_apply(og_session* s, int src, int dst, int level, int mask) {
+    if (check(s, src, level) || check(s, dst, level)) return 1;
+    if (src == dst) return fail("apply: src and dst must be distinct functions");
+    og_sync(s, src, level);
+    for (int phase = 0; phase < 3; ++phase)
+        for (int id = 0; id < s->np; ++id) {
+            if (kind_of(s, id) != phase) continue;
+            const double* sv = prim(s, src, level, id);
+            double* dv = prim(s, dst, level, id);
+            const int fl = owned_flag(s, id);
+            FOR_ROWS(s, id, level, slot, c, r, {
+                if (!(fl & mask)) continue;
+                if (fl & F_DIRICHLET) { dv[slot] = sv[slot]; continue; }
+                dv[slot] = row_acc(s, level, id, slot, sv, c, r);
+            });
+        }
+    return 0;
+}
+
+/* assign / add_scaled (src/function.cpp:156-190) */
+int og_assign(og_session* s, double alpha, int x1, double beta, int x2, int dst, int level, int mask) {
+    if (check(s, x1, level) || check(s, x2, level) || check(s, dst, level)) return 1;
+    for (int id = 0; id < s->np; ++id) {
+        const double* a = prim(s, x1, level, id);
+        const double* b = prim(s, x2, level, id);
+        double* o = prim(s, dst, level, id);
+        const int fl = owned_flag(s, id);
+        if (!(fl & mask)) continue;
+        FOR_OWNED(s, id, level, slot, { o[slot] = alpha * a[slot] + beta * b[slot]; });
+    }
+    return 0;
+}
+int og_add_scaled(og_session* s, int dst, double gamma, int y, int level, int mask) {
+    if (check(s, y, level) || check(s, dst, level)) return 1;
+    for (int id = 0; id < s->np; ++id) {
+        const double* a = prim(s, y, level, id);
+        double* o = prim(s, dst, level, id);
+        if (!(owned_flag(s, id) & mask)) continue;
+        FOR_OWNED(s, id, level, slot, { o[slot] += gamma * a[slot]; });
+    }
+    return 0;
+}
+
+/* residual composed as GridHierarchy does (src/solvers.cpp:418-419) */
+int og_residual(og_session* s, int rhs, int x, int r, int level) {
+    if (og_apply(s, x, r, level, 7)) return 1;
+    return og_assign(s, 1.0, rhs, -1.0, r, r, level, 7);
+}
+
+/* smooth (src/operators.cpp:423-470): sync x, phases V/E/F, DIRICHLET rows
+ * skipped, upd = x + omega*(rhs - acc)/diag; Jacobi defers writes per primitive */
+static int smooth(og_session* s, int rhs, int x, double omega, int level, int jacobi) {
+    if (check(s, rhs, level) || check(s, x, level)) return 1;
+    if (rhs == x) return fail("smooth: rhs and x must be distinct functions");
+    og_sync(s, x, level);
+    const int n = 1 << level;
+    double* pending = malloc(sizeof(double) * (size_t)((int64_t)(n + 1) * (n + 2) / 2 + 64));
+    for (int phase = 0; phase < 3; ++phase)
+        for (int id = 0; id < s->np; ++id) {
+            if (kind_of(s, id) != phase) continue;
+            const double* rv = prim(s, rhs, level, id);
+            double* xv = prim(s, x, level, id);
+            const int fl = owned_flag(s, id);
+            if (fl & F_DIRICHLET) continue;
+            const double diag = row_diag(s, level, id);
+            int64_t np_ = 0;
+            int bad = 0;
+            FOR_ROWS(s, id, level, slot, c, r, {
+                if (diag == 0.0) { bad = 1; continue; }
+                const double acc = row_acc(s, level, id, slot, xv, c, r);
+                const double upd = xv[slot] + omega * (rv[slot] - acc) / diag;
+                if (jacobi) pending[np_++] = upd;
+                else xv[slot] = upd;
+            });
+            if (bad) { free(pending); return fail("smooth: zero diagonal entry"); }
+            if (jacobi) {
+                int64_t q = 0;
+                FOR_OWNED(s, id, level, slot, { xv[slot] = pending[q++]; });
+            }
+        }
+    free(pending);
+    return 0;
+}
+int og_jacobi(og_session* s, int rhs, int x, double omega, int level) { return smooth(s, rhs, x, omega, level, 1); }
+int og_gs(og_session* s, int rhs, int x, int level) { return smooth(s, rhs, x, 1.0, level, 0); }
+
+/* restrict_to_coarse (src/solvers.cpp:131-204) */
+int og_restrict(og_session* s, int fine, int coarse, int lc, int mask) {
+    if (check(s, fine, lc + 1) || check(s, coarse, lc)) return 1;
+    og_sync(s, fine, lc + 1);
+    const int nc = 1 << lc, wc = nc + 1, nfn = 2 * nc, wf = nfn + 1;
+    for (int id = 0; id < s->np; ++id) {
+        const double* fv = prim(s, fine, lc + 1, id);
+        double* cv = prim(s, coarse, lc, id);
+        if (!(owned_flag(s, id) & mask)) continue;
+        switch (kind_of(s, id)) {
+        case 0: {
+            double acc = fv[0];
+            for (int q = 0; q < s->V[id].ne; ++q) acc += 0.5 * fv[1 + q];
+            cv[0] = acc;
+            break;
+        }
+        case 1: {
+            const OE* e = &s->E[id - s->nv];
+            for (int k = 1; k < nc; ++k) {
+                double acc = fv[2 * k] + 0.5 * (fv[2 * k - 1] + fv[2 * k + 1]);
+                for (int q = 0; q < e->nf; ++q) {
+                    const int64_t base = (nfn + 1) + (int64_t)q * (2 * nfn + 1) + (nfn + 1);
+                    acc += 0.5 * (fv[base + 2 * k - 1] + fv[base + 2 * k]);
+                }
+                cv[k] = acc;
+            }
+            break;
+        }
+        default:
+            for (int row = 1; row < nc; ++row)
+                for (int col = 1; col + row <= nc - 1; ++col) {
+                    const int fc = 2 * col, fr = 2 * row;
+#define FV(cc, rr) fv[fidx(wf, (cc), (rr))]
+                    cv[fidx(wc, col, row)] =
+                        FV(fc, fr) + 0.5 * (FV(fc - 1, fr) + FV(fc + 1, fr) + FV(fc, fr - 1) + FV(fc, fr + 1) +
+                                            FV(fc + 1, fr - 1) + FV(fc - 1, fr + 1));
+#undef FV
+                }
+        }
+    }
+    return 0;
+}
+
+/* prolongate (src/solvers.cpp:71-129) */
+int og_prolongate(og_session* s, int coarse, int fine, int lc, int mask) {
+    if (check(s, fine, lc + 1) || check(s, coarse, lc)) return 1;
+    og_sync(s, coarse, lc);
+    const int nc = 1 << lc, wc = nc + 1, wf = 2 * nc + 1;
+    for (int id = 0; id < s->np; ++id) {
+        const double* cv = prim(s, coarse, lc, id);
+        double* fv = prim(s, fine, lc + 1, id);
+        if (!(owned_flag(s, id) & mask)) continue;
+        switch (kind_of(s, id)) {
+        case 0: fv[0] = cv[0]; break;
+        case 1:
+            for (int k = 1; k < 2 * nc; ++k)
+                fv[k] = (k % 2 == 0) ? cv[k / 2] : 0.5 * (cv[(k - 1) / 2] + cv[(k + 1) / 2]);
+            break;
+        default:
+            for (int row = 1; row < 2 * nc; ++row)
+                for (int col = 1; col + row <= 2 * nc - 1; ++col) {
+#define CV(cc, rr) cv[fidx(wc, (cc), (rr))]
+                    double v;
+                    if (col % 2 == 0 && row % 2 == 0) v = CV(col / 2, row / 2);
+                    else if (row % 2 == 0) v = 0.5 * (CV((col - 1) / 2, row / 2) + CV((col + 1) / 2, row / 2));
+                    else if (col % 2 == 0) v = 0.5 * (CV(col / 2, (row - 1) / 2) + CV(col / 2, (row + 1) / 2));
+                    else v = 0.5 * (CV((col + 1) / 2, (row - 1) / 2) + CV((col - 1) / 2, (row + 1) / 2));
+#undef CV
+                    fv[fidx(wf, col, row)] = v;
+                }
+        }
+    }
+    return 0;
+}
+
+/* dot: per-primitive sequential partial, pairwise fold over ID order
+ * (src/function.cpp:38-51, 59-110, 192-206) */
+static double combine_tree(double* v, int64_t len) {
+    if (len == 0) return 0.0;
+    while (len > 1) {
+        int64_t m = 0;
+        for (int64_t i = 0; i + 1 < len; i += 2) v[m++] = v[i] + v[i + 1];
+        if (len % 2) v[m++] = v[len - 1];
+        len = m;
+    }
+    return v[0];
+}
+int og_dot(og_session* s, int a, int b, int level, double* out) {
+    if (check(s, a, level) || check(s, b, level)) return 1;
+    double* part = malloc(sizeof(double) * (size_t)(s->np + 1));
+    for (int id = 0; id < s->np; ++id) {
+        const double* x = prim(s, a, level, id);
+        const double* y = prim(s, b, level, id);
+        double acc = 0.0;
+        FOR_OWNED(s, id, level, slot, { acc += x[slot] * y[slot]; });
+        part[id] = acc;
+    }
+    *out = combine_tree(part, s->np);
+    free(part);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ V-cycle
+ * GridHierarchy::cycle (src/solvers.cpp:406-428) with smooth_jacobi(omega),
+ * coarse_correct (:430-442) by cg_solve's recurrence (:226-259) with the
+ * operator applied matrix-free (DIRICHLET rows identity on a vector that is
+ * zero there, which is the constrained matrix of :322-352). Functions
+ * nfun-5 .. nfun-3 serve as the hierarchy's r, b, e and nfun-2, nfun-1 as
+ * matvec scratch; CG works on flat owned vectors in GlobalDoFMap order. */
+static double flat_dot(const double* a, const double* b, int64_t n) {
+    double acc = 0;
+    for (int64_t i = 0; i < n; ++i) acc += a[i] * b[i];
+    return acc;
+}
+
+typedef struct {
+    og_session* s;
+    int R, B, E, P, AP, lmin, nu1, nu2;
+    double omega, tol;
+} Cyc;
+
+static int matvec(Cyc* c, const double* v, double* out) {
+    og_set(c->s, c->P, c->lmin, v);
+    if (og_apply(c->s, c->P, c->AP, c->lmin, 7)) return 1;
+    return og_get(c->s, c->AP, c->lmin, out);
+}
+
+static int coarse(Cyc* c, int rhs, int x) {
+    og_session* s = c->s;
+    const int L = c->lmin;
+    if (og_residual(s, rhs, x, c->R, L)) return 1;
+    const int64_t n = og_owned(s, L);
+    double* b = malloc(sizeof(double) * (size_t)(5 * n + 5));
+    double *e = b + n, *r = e + n, *p = r + n, *ap = p + n;
+    og_get(s, c->R, L, b);
+    const int max_iter = (int)n + 100;
+    const double target = c->tol * sqrt(flat_dot(b, b, n));
+    for (int64_t i = 0; i < n; ++i) { e[i] = 0.0; r[i] = b[i]; p[i] = r[i]; }
+    double rs = flat_dot(r, r, n);
+    double res = sqrt(rs);
+    int it = 0;
+    while (it < max_iter && res > target) {
+        if (matvec(c, p, ap)) { free(b); return 1; }
+        const double pap = flat_dot(p, ap, n);
+        if (pap <= 0.0) break;
+        const double alpha = rs / pap;
+        for (int64_t i = 0; i < n; ++i) { e[i] += alpha * p[i]; r[i] -= alpha * ap[i]; }
+        const double rs_new = flat_dot(r, r, n);
+        const double beta = rs_new / rs;
+        for (int64_t i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
+        rs = rs_new;
+        ++it;
+        res = sqrt(rs);
+    }
+    if (matvec(c, e, ap)) { free(b); return 1; }
+    double t = 0;
+    for (int64_t i = 0; i < n; ++i) { const double d = b[i] - ap[i]; t += d * d; }
+    if (!(sqrt(t) <= target)) { free(b); return fail("vcycle: coarse CG did not converge"); }
+    og_set(s, c->R, L, e);
+    free(b);
+    return og_add_scaled(s, x, 1.0, c->R, L, F_INNER | F_NEUMANN);
+}
+
+static int cycle(Cyc* c, int rhs, int x, int L) {
+    og_session* s = c->s;
+    if (og_assign(s, 1.0, rhs, 0.0, rhs, x, L, F_DIRICHLET)) return 1;
+    if (L == c->lmin) return coarse(c, rhs, x);
+    for (int i = 0; i < c->nu1; ++i)
+        if (og_jacobi(s, rhs, x, c->omega, L)) return 1;
+    if (og_residual(s, rhs, x, c->R, L)) return 1;
+    if (og_restrict(s, c->R, c->B, L - 1, 7)) return 1;
+    og_assign(s, 0.0, c->B, 0.0, c->B, c->B, L - 1, F_DIRICHLET); /* interpolate(b, 0, DIRICHLET) */
+    og_assign(s, 0.0, c->E, 0.0, c->E, c->E, L - 1, 7);           /* interpolate(e, 0) */
+    if (cycle(c, c->B, c->E, L - 1)) return 1;
+    if (og_prolongate(s, c->E, c->R, L - 1, F_INNER | F_NEUMANN)) return 1;
+    if (og_add_scaled(s, x, 1.0, c->R, L, F_INNER | F_NEUMANN)) return 1;
+    for (int i = 0; i < c->nu2; ++i)
+        if (og_jacobi(s, rhs, x, c->omega, L)) return 1;
+    return 0;
+}
+
+int og_vcycle_jacobi(og_session* s, int rhs, int x, int level, int nu1, int nu2, double omega, double coarse_tol,
+                     int ncycles, double* residuals) {
+    if (s->nfun < 7) return fail("vcycle needs nfuncs >= 7 (last five are scratch)");
+    Cyc c = {s, s->nfun - 5, s->nfun - 4, s->nfun - 3, s->nfun - 2, s->nfun - 1, s->lmin, nu1, nu2, omega,
+             coarse_tol};
+    double d;
+    if (og_residual(s, rhs, x, c.R, level) || og_dot(s, c.R, c.R, level, &d)) return 1;
+    residuals[0] = sqrt(d);
+    for (int k = 0; k < ncycles; ++k) {
+        if (cycle(&c, rhs, x, level)) return 1;
+        if (og_residual(s, rhs, x, c.R, level) || og_dot(s, c.R, c.R, level, &d)) return 1;
+        residuals[k + 1] = sqrt(d);
+    }
+    return 0;
+}

@@ -1,0 +1,384 @@
+// TEST INFRASTRUCTURE ONLY -- never part of the product path.
+//
+// Plain-C adapter around the UNMODIFIED reference library (compiled from
+// /root/reference/proj/src/*.cpp by oracle/Makefile with
+// -Dhytegrid=hytegrid_ref, output only under oracle/_ref/). Used by tests/
+// to pin the C restatement (oracle/hyteg_oracle.c), to generate the golden
+// fixtures in tests/golden/, and by bench.py --impl reference as the CPU
+// baseline. Values cross this boundary as owned-DoF vectors in GlobalDoFMap
+// order (primitives by ID, each in for_each_owned order), filled per
+// primitive so no global std::map is built.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "hytegrid/balancing.hpp"
+#include "hytegrid/function.hpp"
+#include "hytegrid/meshgen.hpp"
+#include "hytegrid/numbering.hpp"
+#include "hytegrid/operators.hpp"
+#include "hytegrid/solvers.hpp"
+
+using namespace hytegrid;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F> int guard(F&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return 4;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 7;
+    }
+}
+
+struct Session {
+    SetupGraph setup;
+    std::unique_ptr<DistributedDomain> dom;
+    std::unique_ptr<Controller> ctl;
+    BoundaryConditions bc;
+    int min_level = 0, max_level = 0;
+    std::vector<std::unique_ptr<ScalarFunction>> f;
+    std::unique_ptr<StencilOperator> A;
+    // composed V-cycle scratch (GridHierarchy's r_, b_, e_)
+    std::unique_ptr<ScalarFunction> r, b, e;
+};
+
+std::vector<PrimitiveID> ids_sorted(const DistributedDomain& dom) {
+    std::vector<PrimitiveID> ids;
+    for (int r = 0; r < dom.ranks(); ++r)
+        for (const auto& [id, p] : dom.graph(r).local) ids.push_back(id);
+    std::sort(ids.begin(), ids.end());
+    return ids;
+}
+
+void move_owned(Session& s, int fi, int level, double* data, bool to_field) {
+    ScalarFunction& fn = *s.f.at(size_t(fi));
+    size_t pos = 0;
+    for (const PrimitiveID id : ids_sorted(*s.dom)) {
+        const Primitive& p = s.dom->primitive(id);
+        auto& vals = fn.values(id, level);
+        for_each_owned(FunctionKind::P1, p.kind, p.info, level, fn.layout(), [&](std::size_t slot) {
+            if (to_field) vals[slot] = data[pos];
+            else data[pos] = vals[slot];
+            ++pos;
+        });
+    }
+}
+
+const std::uint8_t kSmooth = flag_bit(DoFFlag::INNER) | flag_bit(DoFFlag::NEUMANN);
+const std::uint8_t kDir = flag_bit(DoFFlag::DIRICHLET);
+
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_meshgen(const char* kind, const double* p, char* out, int64_t cap, int64_t* len) {
+    return guard([&] {
+        const std::string k(kind);
+        std::string t;
+        if (k == "unit_triangle") t = meshgen::unit_triangle();
+        else if (k == "unit_square") t = meshgen::unit_square();
+        else if (k == "unit_square_reversed") t = meshgen::unit_square_reversed();
+        else if (k == "square_ring8") t = meshgen::square_ring8();
+        else if (k == "channel") t = meshgen::channel(int(p[0]), int(p[1]), p[2], p[3]);
+        else if (k == "annulus") t = meshgen::annulus(int(p[0]), int(p[1]), p[2], p[3]);
+        else throw std::invalid_argument("unknown mesh kind");
+        *len = int64_t(t.size());
+        if (cap > int64_t(t.size())) std::memcpy(out, t.c_str(), t.size() + 1);
+    });
+}
+
+// rank per primitive ID from the reference partitioners (src/balancing.cpp)
+int ref_partition(const char* mesh, int ranks, int partitioner, int weight_level, int* out) {
+    return guard([&] {
+        const SetupGraph setup = build_setup_graph(parse_mesh_string(mesh));
+        const Assignment a = partitioner == 1
+                                 ? partition_greedy_edgecut(setup, weighted_graph(setup, FunctionKind::P1, weight_level),
+                                                            ranks)
+                                 : partition_round_robin(setup, ranks);
+        for (const auto& [id, r] : a) out[id.value] = r;
+    });
+}
+
+// partitioner: 0 round robin, 1 greedy edge cut (weights at weight_level)
+int ref_create(const char* mesh, int ranks, int partitioner, int weight_level, int min_level, int max_level,
+               const int* bc_markers, const uint8_t* bc_flags, int nbc, int nfuncs, void** out) {
+    return guard([&] {
+        auto s = std::make_unique<Session>();
+        s->setup = build_setup_graph(parse_mesh_string(mesh));
+        const Assignment a = partitioner == 1
+                                 ? partition_greedy_edgecut(s->setup,
+                                                            weighted_graph(s->setup, FunctionKind::P1, weight_level),
+                                                            ranks)
+                                 : partition_round_robin(s->setup, ranks);
+        s->dom = std::make_unique<DistributedDomain>(s->setup, a, ranks);
+        s->ctl = std::make_unique<Controller>(*s->dom);
+        for (int i = 0; i < nbc; ++i) s->bc.marker_flag[bc_markers[i]] = DoFFlag(bc_flags[i]);
+        s->min_level = min_level;
+        s->max_level = max_level;
+        for (int i = 0; i < nfuncs; ++i) {
+            s->f.push_back(std::make_unique<ScalarFunction>("f" + std::to_string(i), *s->dom, FunctionKind::P1,
+                                                            min_level, max_level, s->bc));
+            register_function(*s->ctl, *s->f.back());
+        }
+        s->A = std::make_unique<StencilOperator>(*s->dom, Form::LAPLACE, FunctionKind::P1, min_level, max_level, s->bc);
+        *out = s.release();
+    });
+}
+
+void ref_destroy(void* s) { delete static_cast<Session*>(s); }
+
+int64_t ref_owned(void* sp, int level) {
+    Session& s = *static_cast<Session*>(sp);
+    int64_t n = 0;
+    for (const PrimitiveID id : ids_sorted(*s.dom)) {
+        const Primitive& p = s.dom->primitive(id);
+        for_each_owned(FunctionKind::P1, p.kind, p.info, level, row_major_layout(), [&](std::size_t) { ++n; });
+    }
+    return n;
+}
+
+int ref_set(void* s, int fi, int level, const double* data) {
+    return guard([&] { move_owned(*static_cast<Session*>(s), fi, level, const_cast<double*>(data), true); });
+}
+int ref_get(void* s, int fi, int level, double* data) {
+    return guard([&] { move_owned(*static_cast<Session*>(s), fi, level, data, false); });
+}
+int ref_flags(void* sp, int fi, int level, uint8_t* out) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        size_t pos = 0;
+        for (const PrimitiveID id : ids_sorted(*s.dom)) {
+            const Primitive& p = s.dom->primitive(id);
+            const auto& fl = s.f.at(size_t(fi))->flags(id, level);
+            for_each_owned(FunctionKind::P1, p.kind, p.info, level, row_major_layout(),
+                           [&](std::size_t slot) { out[pos++] = fl[slot]; });
+        }
+    });
+}
+// owned DoF coordinates (for_each_owned_coord), x/y interleaved
+int ref_coords(void* sp, int level, double* xy) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        size_t pos = 0;
+        for (const PrimitiveID id : ids_sorted(*s.dom)) {
+            const Primitive& p = s.dom->primitive(id);
+            for_each_owned_coord(FunctionKind::P1, p.kind, p.info, level, row_major_layout(),
+                                 [&](std::size_t, double x, double y) {
+                                     xy[2 * pos] = x;
+                                     xy[2 * pos + 1] = y;
+                                     ++pos;
+                                 });
+        }
+    });
+}
+
+int ref_sync(void* sp, int fi, int level) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        sync_all(*s.ctl, *s.f.at(size_t(fi)), level);
+    });
+}
+
+int ref_apply(void* sp, int src, int dst, int level, uint8_t mask) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        apply(*s.A, *s.ctl, *s.f.at(size_t(src)), *s.f.at(size_t(dst)), level, mask);
+    });
+}
+
+// r = rhs - A x, composed exactly as GridHierarchy (src/solvers.cpp:418-419)
+int ref_residual(void* sp, int rhs, int x, int r, int level) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        apply(*s.A, *s.ctl, *s.f.at(size_t(x)), *s.f.at(size_t(r)), level);
+        assign(1.0, *s.f.at(size_t(rhs)), -1.0, *s.f.at(size_t(r)), *s.f.at(size_t(r)), level);
+    });
+}
+
+int ref_jacobi(void* sp, int rhs, int x, double omega, int level) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        smooth_jacobi(*s.A, *s.ctl, *s.f.at(size_t(rhs)), *s.f.at(size_t(x)), omega, level);
+    });
+}
+
+int ref_gs(void* sp, int rhs, int x, int level) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        smooth_gs(*s.A, *s.ctl, *s.f.at(size_t(rhs)), *s.f.at(size_t(x)), level);
+    });
+}
+
+int ref_restrict(void* sp, int fine, int coarse, int lc, uint8_t mask) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        restrict_to_coarse(*s.ctl, *s.f.at(size_t(fine)), *s.f.at(size_t(coarse)), lc, mask);
+    });
+}
+
+int ref_prolongate(void* sp, int coarse, int fine, int lc, uint8_t mask) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        prolongate(*s.ctl, *s.f.at(size_t(coarse)), *s.f.at(size_t(fine)), lc, mask);
+    });
+}
+
+int ref_assign(void* sp, double alpha, int x1, double beta, int x2, int dst, int level, uint8_t mask) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        assign(alpha, *s.f.at(size_t(x1)), beta, *s.f.at(size_t(x2)), *s.f.at(size_t(dst)), level, mask);
+    });
+}
+
+int ref_add_scaled(void* sp, int dst, double gamma, int y, int level, uint8_t mask) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        add_scaled(*s.f.at(size_t(dst)), gamma, *s.f.at(size_t(y)), level, mask);
+    });
+}
+
+int ref_dot(void* sp, int a, int b, int level, double* out) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        *out = dot(*s.f.at(size_t(a)), *s.f.at(size_t(b)), level);
+    });
+}
+
+// stencil readback in the reference's table order; face: 7 terms + diag;
+// edge: line terms + diag; vertex: terms + diag
+int ref_stencil(void* sp, uint64_t id, int level, double* out, int* len) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        const StencilTable& t = s.A->table(PrimitiveID{id}, level);
+        int n = 0;
+        const Primitive& p = s.dom->primitive(PrimitiveID{id});
+        if (p.kind == PrimitiveKind::FACE) {
+            for (const auto& e : t.face.at(DoFGroup::VERTEX)) out[n++] = e.coeff;
+            out[n++] = t.face_diag.at(DoFGroup::VERTEX);
+        } else if (p.kind == PrimitiveKind::EDGE) {
+            for (const auto& e : t.edge_line) out[n++] = e.coeff;
+            out[n++] = t.edge_line_diag;
+        } else {
+            for (const auto& e : t.vertex) out[n++] = e.coeff;
+            out[n++] = t.vertex_diag;
+        }
+        *len = n;
+    });
+}
+
+// Composed Jacobi V-cycle oracle: GridHierarchy::cycle
+// (src/solvers.cpp:406-428) line by line with smooth_jacobi(omega) in place of
+// smooth_gs, any min level (>= 0), coarse CG (cg_solve) to coarse_tol on the
+// constrained assembled min-level matrix. residuals[0..ncycles] as in
+// GridHierarchy::solve (src/solvers.cpp:451-465) with tol = 0.
+namespace {
+struct Composed {
+    Session& s;
+    int min_level;
+    int nu1, nu2;
+    double omega, tol;
+    GlobalDoFMap cmap;
+    std::vector<uint8_t> cflags;
+    SparseMatrix cA;
+    Composed(Session& s_, int minl, int a, int b, double w, double t)
+        : s(s_), min_level(minl), nu1(a), nu2(b), omega(w), tol(t),
+          cmap(*s_.dom, FunctionKind::P1, minl), cflags(cmap.gather_flags(*s_.r)),
+          cA(assemble_global_sparse(*s_.A, minl, cmap)) {
+        std::vector<double> zero(cA.rows(), 0.0);
+        constrain_dirichlet(cA, zero, cflags);
+    }
+    void coarse(ScalarFunction& rhs, ScalarFunction& x) {
+        const int L = min_level;
+        apply(*s.A, *s.ctl, x, *s.r, L);
+        assign(1.0, rhs, -1.0, *s.r, *s.r, L);
+        const std::vector<double> b = cmap.gather(*s.r);
+        std::vector<double> e(b.size(), 0.0);
+        const SolveReport rep = cg_solve(cA, b, e, tol, static_cast<int>(b.size()) + 100);
+        if (!rep.converged) throw std::runtime_error("vcycle: coarse CG did not converge\n" + rep.history());
+        cmap.scatter(e, *s.r);
+        add_scaled(x, 1.0, *s.r, L, kSmooth);
+    }
+    void cycle(ScalarFunction& rhs, ScalarFunction& x, int L) {
+        assign(1.0, rhs, 0.0, rhs, x, L, kDir);
+        if (L == min_level) {
+            coarse(rhs, x);
+            return;
+        }
+        for (int i = 0; i < nu1; ++i) smooth_jacobi(*s.A, *s.ctl, rhs, x, omega, L);
+        apply(*s.A, *s.ctl, x, *s.r, L);
+        assign(1.0, rhs, -1.0, *s.r, *s.r, L);
+        restrict_to_coarse(*s.ctl, *s.r, *s.b, L - 1);
+        interpolate(*s.b, [](double, double) { return 0.0; }, L - 1, kDir);
+        interpolate(*s.e, [](double, double) { return 0.0; }, L - 1);
+        cycle(*s.b, *s.e, L - 1);
+        prolongate(*s.ctl, *s.e, *s.r, L - 1, kSmooth);
+        add_scaled(x, 1.0, *s.r, L, kSmooth);
+        for (int i = 0; i < nu2; ++i) smooth_jacobi(*s.A, *s.ctl, rhs, x, omega, L);
+    }
+    double resnorm(ScalarFunction& rhs, ScalarFunction& x, int L) {
+        apply(*s.A, *s.ctl, x, *s.r, L);
+        assign(1.0, rhs, -1.0, *s.r, *s.r, L);
+        return norm2(*s.r, L);
+    }
+};
+} // namespace
+
+int ref_vcycle_jacobi(void* sp, int rhs, int x, int level, int nu1, int nu2, double omega, double coarse_tol,
+                      int ncycles, double* residuals) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        if (!s.r) {
+            s.r = std::make_unique<ScalarFunction>("mg.r", *s.dom, FunctionKind::P1, s.min_level, s.max_level, s.bc);
+            s.b = std::make_unique<ScalarFunction>("mg.b", *s.dom, FunctionKind::P1, s.min_level, s.max_level, s.bc);
+            s.e = std::make_unique<ScalarFunction>("mg.e", *s.dom, FunctionKind::P1, s.min_level, s.max_level, s.bc);
+            register_function(*s.ctl, *s.r);
+            register_function(*s.ctl, *s.b);
+            register_function(*s.ctl, *s.e);
+        }
+        Composed c(s, s.min_level, nu1, nu2, omega, coarse_tol);
+        ScalarFunction& R = *s.f.at(size_t(rhs));
+        ScalarFunction& X = *s.f.at(size_t(x));
+        residuals[0] = c.resnorm(R, X, level);
+        for (int k = 0; k < ncycles; ++k) {
+            c.cycle(R, X, level);
+            residuals[k + 1] = c.resnorm(R, X, level);
+        }
+    });
+}
+
+// the reference's own GridHierarchy (hybrid Gauss-Seidel, min level >= 1)
+int ref_gridhierarchy_solve(void* sp, int rhs, int x, int level, double tol, int max_cycles, int nu1, int nu2,
+                            double* residuals, int* n_out) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        GridHierarchy mg(*s.dom, *s.ctl, Form::LAPLACE, s.min_level, s.max_level, s.bc);
+        const SolveReport rep =
+            mg.solve(*s.f.at(size_t(rhs)), *s.f.at(size_t(x)), level, tol, max_cycles, nu1, nu2);
+        for (size_t i = 0; i < rep.residuals.size(); ++i) residuals[i] = rep.residuals[i];
+        *n_out = int(rep.residuals.size());
+    });
+}
+
+} // extern "C"

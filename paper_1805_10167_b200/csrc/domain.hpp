@@ -1,0 +1,258 @@
+// Device-resident runtime for the P1 macro-face multigrid hot path.
+//
+// Mirrors the reference's runtime objects (include/hytegrid/primitives.hpp,
+// function.hpp, operators.hpp, solvers.hpp):
+//   Domain    ~ DistributedDomain + Controller: the macro-primitive graph, the
+//               rank assignment, this process's primitives (one or several
+//               logical ranks), per-level device tables and ghost-exchange
+//               plans; the transport is an in-process device copy between
+//               co-resident logical ranks or NCCL between processes.
+//   Function  ~ ScalarFunction: one HBM arena per level, per-primitive flags.
+//   Operator  ~ StencilOperator (P1, LAPLACE/MASS): per-level coefficients.
+//   Hierarchy ~ GridHierarchy: V-cycle driver with device coarse CG.
+#pragma once
+
+#include <array>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "setup.hpp"
+
+namespace hyb {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define HYB_CUDA(call) ::hyb::cuda_check((call), #call)
+
+/// Owning device allocation.
+class DevMem {
+  public:
+    DevMem() = default;
+    explicit DevMem(size_t bytes);
+    ~DevMem();
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    DevMem(DevMem&& o) noexcept : p_(o.p_), bytes_(o.bytes_) { o.p_ = nullptr; o.bytes_ = 0; }
+    DevMem& operator=(DevMem&& o) noexcept;
+    template <class T> T* as() const { return static_cast<T*>(p_); }
+    size_t bytes() const { return bytes_; }
+    void swap(DevMem& o) noexcept { std::swap(p_, o.p_); std::swap(bytes_, o.bytes_); }
+
+  private:
+    void* p_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+template <class T> DevMem upload_vec(const std::vector<T>& v, cudaStream_t st);
+
+enum Direction : int { V2E = 0, E2F = 1, F2E = 2, E2V = 3 };
+
+struct ExchangeDir {
+    DevMem pack;   // arena -> send staging (remote and co-resident-rank pairs)
+    int npack = 0;
+    DevMem local;  // receive staging -> arena, plus same-rank arena -> arena copies
+    int nlocal = 0;
+    struct Block {
+        int src_rank, dst_rank;
+        int64_t send_off, recv_off, count;
+    };
+    std::vector<Block> inproc;  // co-resident ranks: send block -> recv block
+    std::vector<Block> sends;   // to a remote process
+    std::vector<Block> recvs;   // from a remote process
+};
+
+struct LevelGeom {
+    LevelTables t; // geometry part (coefficient pointers left null)
+    DevMem rowoff, edge_off, edge_nf, vtx_off, vtx_ne, vtx_coef_off, face_gid, edge_gid, vtx_gid;
+    std::vector<int64_t> h_rowoff, h_edge_off, h_vtx_off;
+    ExchangeDir dir[4];
+    int64_t send_size = 0, recv_size = 0;
+};
+
+class Domain;
+
+class Function {
+  public:
+    Function(Domain& d, std::string name, int min_level, int max_level, BoundaryMap bc);
+    Domain& domain() const { return *dom_; }
+    const std::string& name() const { return name_; }
+    int min_level() const { return min_; }
+    int max_level() const { return max_; }
+    const BoundaryMap& bc() const { return bc_; }
+    double* data(int level) const;
+    DevMem& arena(int level);
+    FlagTables flags() const { return {edge_flag_.as<uint8_t>(), vtx_flag_.as<uint8_t>()}; }
+    void check_level(int level, const char* op) const;
+
+  private:
+    Domain* dom_;
+    std::string name_;
+    int min_, max_;
+    BoundaryMap bc_;
+    std::vector<DevMem> arenas_;
+    DevMem edge_flag_, vtx_flag_;
+};
+
+class Operator {
+  public:
+    Operator(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc);
+    Domain& domain() const { return *dom_; }
+    int min_level() const { return min_; }
+    int max_level() const { return max_; }
+    const BoundaryMap& bc() const { return bc_; }
+    Form form() const { return form_; }
+    /// geometry + this operator's coefficients for `level`
+    LevelTables tables(int level) const;
+    /// host copies (tests): face [nfaces][8], edge [nedges][8], vertex flat
+    const std::vector<double>& host_face_coef(int level) const { return lv_.at(size_t(level - min_)).hf; }
+    const std::vector<double>& host_edge_coef(int level) const { return lv_.at(size_t(level - min_)).he; }
+    const std::vector<double>& host_vtx_coef(int level) const { return lv_.at(size_t(level - min_)).hv; }
+
+  private:
+    struct Lv {
+        DevMem face, edge, vtx;
+        std::vector<double> hf, he, hv;
+    };
+    Domain* dom_;
+    Form form_;
+    int min_, max_;
+    BoundaryMap bc_;
+    std::vector<Lv> lv_;
+};
+
+struct KernelTimer {
+    std::string name;
+    cudaEvent_t start, stop;
+};
+
+class Domain {
+  public:
+    /// local_ranks: the logical ranks this process drives (all on `device`).
+    Domain(const std::string& mesh_text, int world_ranks, const std::vector<int>& assignment,
+           const std::vector<int>& local_ranks, int device);
+    ~Domain();
+
+    const MacroGraph& graph() const { return g_; }
+    int world() const { return world_; }
+    const std::vector<int>& local_ranks() const { return local_ranks_; }
+    bool is_local_rank(int r) const;
+    const std::vector<int>& rank_of() const { return rank_of_; }
+    cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
+
+    // local primitives (global IDs, ID order) and reverse maps (-1 = not local)
+    const std::vector<uint64_t>& local_faces() const { return lfaces_; }
+    const std::vector<uint64_t>& local_edges() const { return ledges_; }
+    const std::vector<uint64_t>& local_verts() const { return lverts_; }
+    int local_index(uint64_t gid) const { return lidx_[size_t(gid)]; }
+
+    LevelGeom& level(int L);
+    int64_t owned_total(int L) const;  // all primitives of the graph
+    int64_t owned_local(int L);        // this process's primitives
+
+    // NCCL (multi-process); unique id is 128 bytes
+    static void nccl_unique_id(char out[128]);
+    void connect_nccl(const char id[128], int rank);
+    bool multi_process() const { return nccl_comm_ != nullptr; }
+
+    // ghost exchange of one function, full schedule V->E, E->F, F->E, E->V
+    void sync(Function& f, int level);
+
+    // scratch
+    DevMem& jacobi_scratch(int level);
+    double* staging(int64_t doubles);
+    double* partials(int64_t doubles);
+    double* scalar_out() { return scalars_.as<double>(); }
+
+    // in-process all-reduce of a per-primitive vector (sum) across processes
+    void allreduce_sum(double* dev, int64_t n);
+
+    // profiling of named kernels (CUDA events on the domain stream)
+    bool profiling = false;
+    void timer_begin(const char* name);
+    void timer_end();
+    void timer_query(const std::string& name, double* total_ms, int64_t* count);
+    void timer_reset();
+
+    void synchronize();
+
+    // stream events for device-side timing of host-driven regions
+    void event_record(int slot);
+    float event_elapsed(int a, int b);
+
+  private:
+    cudaEvent_t events_[16] = {};
+    void build_exchange(LevelGeom& lg, int L);
+
+    MacroGraph g_;
+    int world_;
+    std::vector<int> rank_of_;
+    std::vector<int> local_ranks_;
+    int device_;
+    cudaStream_t stream_ = nullptr;
+    std::vector<uint64_t> lfaces_, ledges_, lverts_;
+    std::vector<int> lidx_;
+    std::map<int, std::unique_ptr<LevelGeom>> levels_;
+    std::map<int, DevMem> jacobi_;
+    DevMem staging_, partials_, scalars_, sendbuf_, recvbuf_;
+    void* nccl_comm_ = nullptr;
+    std::vector<KernelTimer> pending_;
+    std::map<std::string, std::pair<double, int64_t>> timers_;
+};
+
+// ---- operations (reference signatures, include/hytegrid/operators.hpp:108-125,
+//      solvers.hpp:26-33, function.hpp:55-81) ----
+void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t mask);
+void residual(const Operator& A, Function& rhs, Function& x, Function& r, int level);
+void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level);
+void diagonal(const Operator& A, Function& d, int level);
+void prolongate(Function& coarse, Function& fine, int coarse_level, uint8_t mask, bool add);
+void restrict_to_coarse(Function& fine, Function& coarse, int coarse_level, uint8_t mask);
+void assign(double alpha, Function& x1, double beta, Function& x2, Function& dst, int level, uint8_t mask);
+void add_scaled(Function& dst, double gamma, Function& y, int level, uint8_t mask);
+void fill_const(Function& f, double value, int level, uint8_t mask);
+void fill_random(Function& f, int level, uint64_t seed, uint64_t stream, double lo, double hi, uint8_t mask);
+double dot(Function& a, Function& b, int level);
+double max_abs(Function& a, int level);
+void upload(Function& f, int level, const double* host, int64_t n, bool global_order, uint8_t mask);
+void download(Function& f, int level, double* host, int64_t n, bool global_order);
+
+enum Smoother : int { SMOOTH_JACOBI = 0 };
+
+class Hierarchy {
+  public:
+    Hierarchy(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc, int smoother, double omega,
+              double coarse_tol, int coarse_max_iter);
+    const Operator& op() const { return a_; }
+    void vcycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post);
+    double residual_norm(Function& rhs, Function& x, int level);
+    /// residual history; returns number of cycles run
+    std::vector<double> solve(Function& rhs, Function& x, int level, double tol, int max_cycles, int nu_pre,
+                              int nu_post, bool* converged);
+    int last_coarse_iterations = 0;
+
+  private:
+    void cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post);
+    void coarse_correct(Function& rhs, Function& x);
+    void smooth(Function& rhs, Function& x, int level);
+
+    Domain* dom_;
+    Operator a_;
+    Function r_, b_, e_;
+    Function cx_, cr_, cp_, cap_;
+    int smoother_;
+    double omega_;
+    double coarse_tol_;
+    int coarse_max_iter_;
+};
+
+} // namespace hyb

@@ -1,0 +1,754 @@
+// sm_100a kernels for the P1 macro-face multigrid hot path.
+//
+// Every kernel is HBM-bound (fp64, 0.8 flop/B); no tensor cores. Arithmetic
+// follows the reference's term order with separately rounded products and
+// sums (compiled with -fmad=false), so stencil rows, Jacobi updates and
+// transfers are bitwise the reference's:
+//   face / edge / vertex rows       reference src/operators.cpp:270-320, 403-417
+//   Jacobi update                   reference src/operators.cpp:461
+//   prolongation / restriction      reference src/solvers.cpp:71-204
+//   assign / add_scaled             reference src/function.cpp:156-190
+//   ghost copies                    reference src/communication.cpp:272-403
+#include "kernels.hpp"
+
+#include <atomic>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace hyb {
+
+namespace {
+
+constexpr uint8_t F_INNER = 1, F_DIRICHLET = 2;
+
+std::atomic<int64_t> g_launches{0};
+
+inline void check_launch(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA launch failed (") + what + "): " + cudaGetErrorString(e));
+}
+
+__device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double shfl_down1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+// ---------------------------------------------------------------------------
+// K1: face stencil (apply / residual / Jacobi) over face interiors.
+//
+// CTA = 4 independent warps; a warp owns 64 consecutive columns (2 per lane,
+// 16-byte loads) of one face and marches up a band of rows with a 3-row
+// register window; c-1 / c+1 neighbours come from warp shuffles, the two
+// columns beyond the warp from one predicated load per row (lanes 0 / 31).
+// Rows are prefetched FS_PF ahead so each lane keeps several 16-byte loads
+// in flight (HBM latency hiding without shared memory).
+// ---------------------------------------------------------------------------
+constexpr int FS_WARPS = 4;
+constexpr int FS_COLS = 64;
+constexpr int FS_RB = 64;
+constexpr int FS_PF = 4;
+
+template <int MODE>
+__global__ void __launch_bounds__(FS_WARPS * 32) k_face_stencil(LevelTables t, const double* __restrict__ x,
+                                                                const double* __restrict__ b,
+                                                                double* __restrict__ y, double omega) {
+    const int n = t.n, W = t.W;
+    const int face = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c0 = (blockIdx.x * FS_WARPS + warp) * FS_COLS;
+    int r_lo = blockIdx.y * FS_RB;
+    if (r_lo < 1) r_lo = 1;
+    int r_hi = (blockIdx.y + 1) * FS_RB; // exclusive
+    if (r_hi > n - 1) r_hi = n - 1;     // interior rows r <= n-2
+    const int cmin = c0 < 1 ? 1 : c0;
+    if (r_hi > n - cmin) r_hi = n - cmin; // first column stays interior: r <= n-1-cmin
+    if (r_lo >= r_hi) return;           // warp-uniform
+
+    const int64_t base = int64_t(face) * t.face_stride;
+    const double* __restrict__ xf = x + base;
+    const double* __restrict__ bf = b + base;
+    double* __restrict__ yf = y + base;
+    const int64_t* __restrict__ ro = t.rowoff;
+    const double* co = t.face_coef + size_t(face) * 8;
+    const double cW = co[0], cNW = co[1], cS = co[2], cC = co[3], cN = co[4], cSE = co[5], cE = co[6], dg = co[7];
+
+    const int c = c0 + 2 * lane;
+    const bool edge_lane = (lane == 0 && c0 > 0) || lane == 31;
+    const int ce = lane == 0 ? c0 - 1 : c0 + FS_COLS;
+
+    // x row q: (c, c+1) pair and this lane's out-of-warp neighbour column
+    auto ldx = [&](int q, double2& v, double& ex) {
+        v = make_double2(0.0, 0.0);
+        ex = 0.0;
+        if (q <= r_hi) {
+            const int len = W - q;
+            const double* row = xf + ro[q];
+            if (c < len) v = __ldg(reinterpret_cast<const double2*>(row + c));
+            if (edge_lane && ce < len) ex = __ldg(row + ce);
+        }
+    };
+    auto ldb = [&](int q, double2& v) {
+        v = make_double2(0.0, 0.0);
+        if (MODE != ST_APPLY && q < r_hi) {
+            const int len = W - q;
+            if (c < len) v = __ldg(reinterpret_cast<const double2*>(bf + ro[q] + c));
+        }
+    };
+
+    double2 xm, x0;
+    double exm, ex0;
+    ldx(r_lo - 1, xm, exm);
+    ldx(r_lo, x0, ex0);
+    double2 q[FS_PF], qb[FS_PF];
+    double qe[FS_PF];
+#pragma unroll
+    for (int u = 0; u < FS_PF; ++u) {
+        ldx(r_lo + 1 + u, q[u], qe[u]);
+        ldb(r_lo + u, qb[u]);
+    }
+    double l0 = shfl_up1(x0.y);
+    double rm = shfl_down1(xm.x);
+    double r0 = shfl_down1(x0.x);
+    if (lane == 0) l0 = ex0;
+    if (lane == 31) { rm = exm; r0 = ex0; }
+
+    for (int r = r_lo; r < r_hi; r += FS_PF) {
+#pragma unroll
+        for (int u = 0; u < FS_PF; ++u) {
+            const int rr = r + u;
+            const double2 xp = q[u];
+            const double exp_ = qe[u];
+            const double2 bb = qb[u];
+            ldx(rr + 1 + FS_PF, q[u], qe[u]);
+            ldb(rr + FS_PF, qb[u]);
+            double lp = shfl_up1(xp.y);
+            double rp = shfl_down1(xp.x);
+            if (lane == 0) lp = exp_;
+            if (lane == 31) rp = exp_;
+            if (rr < r_hi) {
+                const int last = n - 1 - rr; // last interior column of this row
+                const bool v0 = c >= 1 && c <= last;
+                const bool v1 = c + 1 <= last;
+                // reference term order: W NW S C N SE E, accumulation from 0
+                double a0 = 0.0;
+                a0 += cW * l0;
+                a0 += cNW * lp;
+                a0 += cS * xm.x;
+                a0 += cC * x0.x;
+                a0 += cN * xp.x;
+                a0 += cSE * xm.y;
+                a0 += cE * x0.y;
+                double a1 = 0.0;
+                a1 += cW * x0.x;
+                a1 += cNW * xp.x;
+                a1 += cS * xm.y;
+                a1 += cC * x0.y;
+                a1 += cN * xp.y;
+                a1 += cSE * rm;
+                a1 += cE * r0;
+                double o0 = a0, o1 = a1;
+                if (MODE == ST_RESIDUAL) {
+                    o0 = bb.x - a0;
+                    o1 = bb.y - a1;
+                } else if (MODE == ST_JACOBI) {
+                    o0 = x0.x + omega * (bb.x - a0) / dg;
+                    o1 = x0.y + omega * (bb.y - a1) / dg;
+                }
+                double* yrow = yf + ro[rr];
+                if (v0 && v1) {
+                    *reinterpret_cast<double2*>(yrow + c) = make_double2(o0, o1);
+                } else {
+                    if (v0) yrow[c] = o0;
+                    if (v1) yrow[c + 1] = o1;
+                }
+            }
+            xm = x0;
+            rm = r0;
+            x0 = xp;
+            l0 = lp;
+            r0 = rp;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2/K3: edge line rows and vertex rows, one launch. Flags are per primitive
+// (SURVEY F6): a masked-out primitive is skipped, a DIRICHLET row is the
+// identity (apply), b - x (residual) or kept (Jacobi).
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl, const double* __restrict__ x,
+                                                    const double* __restrict__ b, double* __restrict__ y,
+                                                    double omega, uint8_t mask, int kblocks) {
+    const int n = t.n;
+    const int eblocks = t.nedges * kblocks;
+    if (int(blockIdx.x) < eblocks) {
+        const int e = blockIdx.x / kblocks;
+        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+        if (k > n - 1) return;
+        const uint8_t f = fl.edge_flag[e];
+        if (!(f & mask)) return;
+        const int64_t off = t.edge_off[e];
+        const double* L = x + off;
+        if (f & F_DIRICHLET) {
+            y[off + k] = MODE == ST_RESIDUAL ? b[off + k] - L[k] : L[k];
+            return;
+        }
+        const double* co = t.edge_coef + size_t(e) * 8;
+        const double* H0 = L + (n + 1);
+        double acc = 0.0;
+        acc += co[0] * L[k - 1];
+        acc += co[1] * L[k];
+        acc += co[2] * L[k + 1];
+        acc += co[3] * H0[k - 1];
+        acc += co[4] * H0[k];
+        if (t.edge_nf[e] == 2) {
+            const double* H1 = H0 + n;
+            acc += co[5] * H1[k - 1];
+            acc += co[6] * H1[k];
+        }
+        double o = acc;
+        if (MODE == ST_RESIDUAL) o = b[off + k] - acc;
+        else if (MODE == ST_JACOBI) o = L[k] + omega * (b[off + k] - acc) / co[7];
+        y[off + k] = o;
+        return;
+    }
+    const int v = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+    if (v >= t.nverts) return;
+    const uint8_t f = fl.vtx_flag[v];
+    if (!(f & mask)) return;
+    const int64_t off = t.vtx_off[v];
+    if (f & F_DIRICHLET) {
+        y[off] = MODE == ST_RESIDUAL ? b[off] - x[off] : x[off];
+        return;
+    }
+    const int ne = t.vtx_ne[v];
+    const double* co = t.vtx_coef + t.vtx_coef_off[v];
+    double acc = 0.0;
+    for (int j = 0; j <= ne; ++j) acc += co[j] * x[off + j];
+    double o = acc;
+    if (MODE == ST_RESIDUAL) o = b[off] - acc;
+    else if (MODE == ST_JACOBI) o = x[off] + omega * (b[off] - acc) / co[ne + 1];
+    y[off] = o;
+}
+
+// ---------------------------------------------------------------------------
+// K11: ghost copies, one warp per walk segment.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t seg_addr(int64_t base, uint16_t mode, int k, int count, int W,
+                                            const int64_t* __restrict__ ro) {
+    const int w = (mode & SEG_REV) ? count - 1 - k : k;
+    if (!(mode & SEG_FACE)) return base + w;
+    const int off = (mode & SEG_OFF1) ? 1 : 0;
+    const int slot = (mode >> SEG_SLOT_SHIFT) & 3;
+    int c, r;
+    if (slot == 0) { c = w; r = off; }
+    else if (slot == 1) { c = off; r = w; }
+    else { c = W - 1 - off - w; r = w; }
+    return base + ro[r] + c;
+}
+
+__global__ void __launch_bounds__(256) k_copy_segments(const CopySeg* __restrict__ segs, int nseg, LevelTables t,
+                                                       double* arena, double* sendbuf, double* recvbuf) {
+    const int s = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s >= nseg) return;
+    const CopySeg g = segs[s];
+    double* bufs[3] = {arena, sendbuf, recvbuf};
+    const double* src = bufs[g.src_mode & SEG_BUF_MASK];
+    double* dst = bufs[g.dst_mode & SEG_BUF_MASK];
+    for (int k = lane; k < g.count; k += 32)
+        dst[seg_addr(g.dst, g.dst_mode, k, g.count, t.W, t.rowoff)] =
+            src[seg_addr(g.src, g.src_mode, k, g.count, t.W, t.rowoff)];
+}
+
+// ---------------------------------------------------------------------------
+// Face row iteration helper for the O(DoF) face kernels below:
+// grid (column blocks of 128, bands of FR_RB rows, faces).
+// ---------------------------------------------------------------------------
+constexpr int FR_RB = 16;
+
+inline dim3 face_row_grid(int n_cols, int n_rows, int nfaces) {
+    return dim3(unsigned((n_cols + 127) / 128), unsigned((n_rows + FR_RB - 1) / FR_RB), unsigned(nfaces));
+}
+
+// ---------------------------------------------------------------------------
+// K8: prolongation (optionally fused with the add into the fine iterate).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_prolongate_faces(LevelTables tc, LevelTables tf, const double* __restrict__ xc,
+                                                          double* __restrict__ xf, int add) {
+    const int nf = tf.n;
+    const int col = 1 + blockIdx.x * 128 + threadIdx.x;
+    const double* cv = xc + int64_t(blockIdx.z) * tc.face_stride;
+    double* fv = xf + int64_t(blockIdx.z) * tf.face_stride;
+    const int r0 = 1 + blockIdx.y * FR_RB;
+    for (int row = r0; row < r0 + FR_RB && row <= nf - 2; ++row) {
+        if (col > nf - 1 - row) break;
+        const int64_t* cr = tc.rowoff;
+        double v;
+        if (col % 2 == 0 && row % 2 == 0) v = cv[cr[row / 2] + col / 2];
+        else if (row % 2 == 0) v = 0.5 * (cv[cr[row / 2] + (col - 1) / 2] + cv[cr[row / 2] + (col + 1) / 2]);
+        else if (col % 2 == 0) v = 0.5 * (cv[cr[(row - 1) / 2] + col / 2] + cv[cr[(row + 1) / 2] + col / 2]);
+        else v = 0.5 * (cv[cr[(row - 1) / 2] + (col + 1) / 2] + cv[cr[(row + 1) / 2] + (col - 1) / 2]);
+        double* p = fv + tf.rowoff[row] + col;
+        *p = add ? *p + v : v;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_prolongate_ev(LevelTables tc, LevelTables tf, FlagTables ff,
+                                                       const double* __restrict__ xc, double* __restrict__ xf,
+                                                       uint8_t mask, int add, int kblocks) {
+    const int nf = tf.n;
+    const int eblocks = tf.nedges * kblocks;
+    if (int(blockIdx.x) < eblocks) {
+        const int e = blockIdx.x / kblocks;
+        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+        if (k > nf - 1 || !(ff.edge_flag[e] & mask)) return;
+        const double* cl = xc + tc.edge_off[e];
+        const double v = (k % 2 == 0) ? cl[k / 2] : 0.5 * (cl[(k - 1) / 2] + cl[(k + 1) / 2]);
+        double* p = xf + tf.edge_off[e] + k;
+        *p = add ? *p + v : v;
+        return;
+    }
+    const int vtx = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+    if (vtx >= tf.nverts || !(ff.vtx_flag[vtx] & mask)) return;
+    const double v = xc[tc.vtx_off[vtx]];
+    double* p = xf + tf.vtx_off[vtx];
+    *p = add ? *p + v : v;
+}
+
+// ---------------------------------------------------------------------------
+// K7: restriction (exact transpose of the prolongation).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_restrict_faces(LevelTables tc, LevelTables tf, const double* __restrict__ xf,
+                                                        double* __restrict__ xc) {
+    const int nc = tc.n;
+    const int col = 1 + blockIdx.x * 128 + threadIdx.x;
+    const double* fv = xf + int64_t(blockIdx.z) * tf.face_stride;
+    double* cv = xc + int64_t(blockIdx.z) * tc.face_stride;
+    const int r0 = 1 + blockIdx.y * FR_RB;
+    const int64_t* fr_ = tf.rowoff;
+    for (int row = r0; row < r0 + FR_RB && row <= nc - 2; ++row) {
+        if (col > nc - 1 - row) break;
+        const int fc = 2 * col, fr = 2 * row;
+        const double* rm = fv + fr_[fr - 1];
+        const double* r0p = fv + fr_[fr];
+        const double* rp = fv + fr_[fr + 1];
+        cv[tc.rowoff[row] + col] =
+            r0p[fc] + 0.5 * (r0p[fc - 1] + r0p[fc + 1] + rm[fc] + rp[fc] + rm[fc + 1] + rp[fc - 1]);
+    }
+}
+
+__global__ void __launch_bounds__(128) k_restrict_ev(LevelTables tc, LevelTables tf, FlagTables cf,
+                                                     const double* __restrict__ xf, double* __restrict__ xc,
+                                                     uint8_t mask, int kblocks) {
+    const int nc = tc.n, nfn = tf.n;
+    const int eblocks = tc.nedges * kblocks;
+    if (int(blockIdx.x) < eblocks) {
+        const int e = blockIdx.x / kblocks;
+        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+        if (k > nc - 1 || !(cf.edge_flag[e] & mask)) return;
+        const double* fl = xf + tf.edge_off[e];
+        double acc = fl[2 * k] + 0.5 * (fl[2 * k - 1] + fl[2 * k + 1]);
+        const int nfc = tf.edge_nf[e];
+        for (int j = 0; j < nfc; ++j) {
+            const double* h = fl + (nfn + 1) + int64_t(j) * nfn;
+            acc += 0.5 * (h[2 * k - 1] + h[2 * k]);
+        }
+        xc[tc.edge_off[e] + k] = acc;
+        return;
+    }
+    const int v = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+    if (v >= tc.nverts || !(cf.vtx_flag[v] & mask)) return;
+    const double* fv = xf + tf.vtx_off[v];
+    double acc = fv[0];
+    const int ne = tf.vtx_ne[v];
+    for (int j = 1; j <= ne; ++j) acc += 0.5 * fv[j];
+    xc[tc.vtx_off[v]] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// K9: BLAS-1. Faces are streamed as one flat block (interior, border ghosts
+// and padding alike: ghosts are refreshed by the next sync before any read,
+// so only owned results matter); edges / vertices honour per-primitive flags.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double blas_op(int op, double alpha, double a, double beta, double b, double d) {
+    if (op == 0) return alpha * a + beta * b;
+    if (op == 1) return d + alpha * a;
+    return alpha;
+}
+
+__global__ void __launch_bounds__(256) k_blas1_faces(int op, int64_t n2, double alpha, const double2* __restrict__ x1,
+                                                     double beta, const double2* __restrict__ x2, double2* dst) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
+        const double2 a = op != 2 ? x1[i] : make_double2(0, 0);
+        const double2 b = op == 0 ? x2[i] : make_double2(0, 0);
+        const double2 d = op == 1 ? dst[i] : make_double2(0, 0);
+        dst[i] = make_double2(blas_op(op, alpha, a.x, beta, b.x, d.x), blas_op(op, alpha, a.y, beta, b.y, d.y));
+    }
+}
+
+__global__ void __launch_bounds__(128) k_blas1_ev(int op, LevelTables t, FlagTables fl, double alpha,
+                                                  const double* __restrict__ x1, double beta,
+                                                  const double* __restrict__ x2, double* dst, uint8_t mask,
+                                                  int kblocks) {
+    const int n = t.n;
+    const int eblocks = t.nedges * kblocks;
+    int64_t i;
+    if (int(blockIdx.x) < eblocks) {
+        const int e = blockIdx.x / kblocks;
+        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+        if (k > n - 1 || !(fl.edge_flag[e] & mask)) return;
+        i = t.edge_off[e] + k;
+    } else {
+        const int v = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+        if (v >= t.nverts || !(fl.vtx_flag[v] & mask)) return;
+        i = t.vtx_off[v];
+    }
+    dst[i] = blas_op(op, alpha, op != 2 ? x1[i] : 0.0, beta, op == 0 ? x2[i] : 0.0, op == 1 ? dst[i] : 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// K13: counter-based uniform values keyed on canonical DoF identity:
+// face (id, c, r), edge (id, k), vertex (id) -- partition independent.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double key_uniform(uint64_t sk, uint64_t id, uint64_t c, uint64_t r, double lo,
+                                              double hi) {
+    const uint64_t key = (id << 40) ^ (c << 20) ^ r;
+    const uint64_t h = mix64(sk ^ mix64(key));
+    const double u = double(h >> 11) * 0x1p-53; // [0, 1)
+    return lo + (hi - lo) * u;
+}
+
+__global__ void __launch_bounds__(128) k_random_faces(LevelTables t, uint64_t sk, double lo, double hi, double* dst) {
+    const int n = t.n;
+    const int col = 1 + blockIdx.x * 128 + threadIdx.x;
+    const uint64_t id = t.face_gid[blockIdx.z];
+    double* fv = dst + int64_t(blockIdx.z) * t.face_stride;
+    const int r0 = 1 + blockIdx.y * FR_RB;
+    for (int row = r0; row < r0 + FR_RB && row <= n - 2; ++row) {
+        if (col > n - 1 - row) break;
+        fv[t.rowoff[row] + col] = key_uniform(sk, id, uint64_t(col), uint64_t(row), lo, hi);
+    }
+}
+
+__global__ void __launch_bounds__(128) k_random_ev(LevelTables t, FlagTables fl, uint64_t sk, double lo, double hi,
+                                                   double* dst, uint8_t mask, int kblocks) {
+    const int n = t.n;
+    const int eblocks = t.nedges * kblocks;
+    if (int(blockIdx.x) < eblocks) {
+        const int e = blockIdx.x / kblocks;
+        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+        if (k > n - 1 || !(fl.edge_flag[e] & mask)) return;
+        dst[t.edge_off[e] + k] = key_uniform(sk, t.edge_gid[e], uint64_t(k), 0, lo, hi);
+        return;
+    }
+    const int v = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+    if (v >= t.nverts || !(fl.vtx_flag[v] & mask)) return;
+    dst[t.vtx_off[v]] = key_uniform(sk, t.vtx_gid[v], 0, 0, lo, hi);
+}
+
+// ---------------------------------------------------------------------------
+// Packed owned order (reference for_each_owned, src/layout.cpp:176-237):
+// local vertices, then edges k = 1..n-1, then faces r = 1..n-2, c = 1..n-1-r.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t face_packed_row(int n, int r) {
+    // rows 1..r-1 have lengths n-2, n-3, ..., n-r
+    return int64_t(r - 1) * (n - 1) - int64_t(r) * (r - 1) / 2;
+}
+
+__global__ void __launch_bounds__(128) k_pack_faces(LevelTables t, const double* __restrict__ src,
+                                                    double* __restrict__ dst, int to_arena, uint8_t mask) {
+    const int n = t.n;
+    const int col = 1 + blockIdx.x * 128 + threadIdx.x;
+    if (!(mask & F_INNER)) return;
+    const int64_t per_face = int64_t(n - 1) * (n - 2) / 2;
+    const int64_t pbase = int64_t(t.nverts) + int64_t(t.nedges) * (n - 1) + int64_t(blockIdx.z) * per_face;
+    const int64_t abase = int64_t(blockIdx.z) * t.face_stride;
+    const int r0 = 1 + blockIdx.y * FR_RB;
+    for (int row = r0; row < r0 + FR_RB && row <= n - 2; ++row) {
+        if (col > n - 1 - row) break;
+        const int64_t pi = pbase + face_packed_row(n, row) + (col - 1);
+        const int64_t ai = abase + t.rowoff[row] + col;
+        if (to_arena) dst[ai] = src[pi];
+        else dst[pi] = src[ai];
+    }
+}
+
+__global__ void __launch_bounds__(128) k_pack_ev(LevelTables t, FlagTables fl, const double* __restrict__ src,
+                                                 double* __restrict__ dst, int to_arena, uint8_t mask, int kblocks) {
+    const int n = t.n;
+    const int eblocks = t.nedges * kblocks;
+    int64_t pi, ai;
+    if (int(blockIdx.x) < eblocks) {
+        const int e = blockIdx.x / kblocks;
+        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+        if (k > n - 1) return;
+        if (to_arena && !(fl.edge_flag[e] & mask)) return;
+        pi = int64_t(t.nverts) + int64_t(e) * (n - 1) + (k - 1);
+        ai = t.edge_off[e] + k;
+    } else {
+        const int v = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+        if (v >= t.nverts) return;
+        if (to_arena && !(fl.vtx_flag[v] & mask)) return;
+        pi = v;
+        ai = t.vtx_off[v];
+    }
+    if (to_arena) dst[ai] = src[pi];
+    else dst[pi] = src[ai];
+}
+
+// ---------------------------------------------------------------------------
+// K10: per-primitive partials. Faces: one CTA per (face, band of PB rows),
+// fixed-shape tree inside the CTA, bands folded in order per face, so the
+// partial of a face is independent of the partitioning.
+// ---------------------------------------------------------------------------
+constexpr int PB = 32;
+
+template <int OP>
+__device__ __forceinline__ double red2(double a, double b) {
+    return OP == 0 ? a + b : fmax(a, b);
+}
+
+template <int OP>
+__device__ double block_reduce_256(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (int(threadIdx.x) < s) sh[threadIdx.x] = red2<OP>(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    return sh[0];
+}
+
+template <int OP>
+__global__ void __launch_bounds__(256) k_partials_faces(LevelTables t, const double* __restrict__ x1,
+                                                        const double* __restrict__ x2, double* scratch, int bands) {
+    __shared__ double sh[256];
+    const int n = t.n;
+    const double* a = x1 + int64_t(blockIdx.y) * t.face_stride;
+    const double* b = x2 + int64_t(blockIdx.y) * t.face_stride;
+    double s = 0.0;
+    const int r0 = 1 + blockIdx.x * PB;
+    for (int row = r0; row < r0 + PB && row <= n - 2; ++row) {
+        const int64_t ro = t.rowoff[row];
+        for (int col = 1 + threadIdx.x; col <= n - 1 - row; col += 256) {
+            const double va = a[ro + col];
+            s = OP == 0 ? s + va * b[ro + col] : fmax(s, fabs(va));
+        }
+    }
+    const double tot = block_reduce_256<OP>(s, sh);
+    if (threadIdx.x == 0) scratch[int64_t(blockIdx.y) * bands + blockIdx.x] = tot;
+}
+
+template <int OP>
+__global__ void k_partials_finish(LevelTables t, const double* __restrict__ x1, const double* __restrict__ x2,
+                                  const double* scratch, int bands, double* part) {
+    // thread per face (fold bands), then per edge / vertex
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = t.n;
+    if (i < t.nfaces) {
+        double s = 0.0;
+        for (int j = 0; j < bands; ++j) s = red2<OP>(s, scratch[int64_t(i) * bands + j]);
+        part[t.face_gid[i]] = s;
+        return;
+    }
+    int j = i - t.nfaces;
+    if (j < t.nedges) {
+        const double* a = x1 + t.edge_off[j];
+        const double* b = x2 + t.edge_off[j];
+        double s = 0.0;
+        for (int k = 1; k <= n - 1; ++k) s = OP == 0 ? s + a[k] * b[k] : fmax(s, fabs(a[k]));
+        part[t.edge_gid[j]] = s;
+        return;
+    }
+    j -= t.nedges;
+    if (j < t.nverts) {
+        const double va = x1[t.vtx_off[j]];
+        part[t.vtx_gid[j]] = OP == 0 ? 0.0 + va * x2[t.vtx_off[j]] : fmax(0.0, fabs(va));
+    }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(1024) k_combine_tree(double* v, int64_t len, double* out) {
+    // pairwise fold in list order, odd tail carried (reference
+    // src/function.cpp:38-51); ping-pong between v[0..len) and v[len..2len)
+    double* src = v;
+    double* dst = v + len;
+    int64_t m = len;
+    if (m == 0) {
+        if (threadIdx.x == 0) *out = 0.0;
+        return;
+    }
+    while (m > 1) {
+        const int64_t half = m / 2;
+        for (int64_t i = threadIdx.x; i < half; i += blockDim.x) dst[i] = red2<OP>(src[2 * i], src[2 * i + 1]);
+        if ((m & 1) && threadIdx.x == 0) dst[half] = src[m - 1];
+        __syncthreads();
+        m = half + (m & 1);
+        double* tmp = src;
+        src = dst;
+        dst = tmp;
+    }
+    if (threadIdx.x == 0) *out = src[0];
+}
+
+inline int kblocks_for(int n) { return n - 1 > 0 ? (n - 1 + 127) / 128 : 0; }
+
+} // namespace
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+int64_t kernel_launch_count() { return g_launches.load(); }
+
+void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const double* x, const double* b, double* y,
+                    double omega, uint8_t mask, cudaStream_t st, int parts) {
+    // faces: interior DoFs are INNER; only present for n >= 3
+    if ((parts & 1) && (mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
+        const dim3 grid(unsigned((t.n - 1 + FS_WARPS * FS_COLS - 1) / (FS_WARPS * FS_COLS)),
+                        unsigned((t.n - 1 + FS_RB - 1) / FS_RB), unsigned(t.nfaces));
+        switch (mode) {
+        case ST_APPLY: k_face_stencil<ST_APPLY><<<grid, FS_WARPS * 32, 0, st>>>(t, x, b, y, omega); break;
+        case ST_RESIDUAL: k_face_stencil<ST_RESIDUAL><<<grid, FS_WARPS * 32, 0, st>>>(t, x, b, y, omega); break;
+        default: k_face_stencil<ST_JACOBI><<<grid, FS_WARPS * 32, 0, st>>>(t, x, b, y, omega); break;
+        }
+        check_launch("face stencil");
+    }
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    if ((parts & 2) && blocks > 0) {
+        switch (mode) {
+        case ST_APPLY: k_ev_stencil<ST_APPLY><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb); break;
+        case ST_RESIDUAL: k_ev_stencil<ST_RESIDUAL><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb); break;
+        default: k_ev_stencil<ST_JACOBI><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb); break;
+        }
+        check_launch("edge/vertex stencil");
+    }
+}
+
+void launch_copy_segments(const CopySeg* segs, int nseg, const LevelTables& t, double* arena, double* sendbuf,
+                          double* recvbuf, cudaStream_t st) {
+    if (nseg <= 0) return;
+    k_copy_segments<<<(nseg + 7) / 8, 256, 0, st>>>(segs, nseg, t, arena, sendbuf, recvbuf);
+    check_launch("copy segments");
+}
+
+void launch_prolongate(const LevelTables& tc, const LevelTables& tf, const FlagTables& ff, const double* xc,
+                       double* xf, uint8_t mask, bool add, cudaStream_t st) {
+    if ((mask & F_INNER) && tf.nfaces > 0 && tf.n >= 3) {
+        k_prolongate_faces<<<face_row_grid(tf.n - 2, tf.n - 2, tf.nfaces), 128, 0, st>>>(tc, tf, xc, xf, add);
+        check_launch("prolongate faces");
+    }
+    const int kb = kblocks_for(tf.n);
+    const int blocks = tf.nedges * kb + (tf.nverts + 127) / 128;
+    if (blocks > 0) {
+        k_prolongate_ev<<<blocks, 128, 0, st>>>(tc, tf, ff, xc, xf, mask, add ? 1 : 0, kb);
+        check_launch("prolongate edges/vertices");
+    }
+}
+
+void launch_restrict(const LevelTables& tc, const LevelTables& tf, const FlagTables& cf, const double* xf, double* xc,
+                     uint8_t mask, cudaStream_t st) {
+    if ((mask & F_INNER) && tc.nfaces > 0 && tc.n >= 3) {
+        k_restrict_faces<<<face_row_grid(tc.n - 2, tc.n - 2, tc.nfaces), 128, 0, st>>>(tc, tf, xf, xc);
+        check_launch("restrict faces");
+    }
+    const int kb = kblocks_for(tc.n);
+    const int blocks = tc.nedges * kb + (tc.nverts + 127) / 128;
+    if (blocks > 0) {
+        k_restrict_ev<<<blocks, 128, 0, st>>>(tc, tf, cf, xf, xc, mask, kb);
+        check_launch("restrict edges/vertices");
+    }
+}
+
+void launch_blas1(int op, const LevelTables& t, const FlagTables& fl, double alpha, const double* x1, double beta,
+                  const double* x2, double* dst, uint8_t mask, cudaStream_t st) {
+    if ((mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
+        const int64_t n2 = t.faces_size / 2;
+        const int64_t want = (n2 + 255) / 256;
+        const int grid = int(want < 148 * 16 ? want : 148 * 16);
+        k_blas1_faces<<<grid, 256, 0, st>>>(op, n2, alpha, reinterpret_cast<const double2*>(x1), beta,
+                                            reinterpret_cast<const double2*>(x2), reinterpret_cast<double2*>(dst));
+        check_launch("blas1 faces");
+    }
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    if (blocks > 0) {
+        k_blas1_ev<<<blocks, 128, 0, st>>>(op, t, fl, alpha, x1, beta, x2, dst, mask, kb);
+        check_launch("blas1 edges/vertices");
+    }
+}
+
+void launch_random(const LevelTables& t, const FlagTables& fl, uint64_t seed, uint64_t stream, double lo, double hi,
+                   double* dst, uint8_t mask, cudaStream_t st) {
+    const uint64_t sk = mix64(mix64(seed) ^ (stream * 0xD1B54A32D192ED03ull));
+    if ((mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
+        k_random_faces<<<face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st>>>(t, sk, lo, hi, dst);
+        check_launch("random faces");
+    }
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    if (blocks > 0) {
+        k_random_ev<<<blocks, 128, 0, st>>>(t, fl, sk, lo, hi, dst, mask, kb);
+        check_launch("random edges/vertices");
+    }
+}
+
+void launch_scatter_owned(const LevelTables& t, const FlagTables& fl, const double* packed, double* arena,
+                          uint8_t mask, cudaStream_t st) {
+    if (t.nfaces > 0 && t.n >= 3) {
+        k_pack_faces<<<face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st>>>(t, packed, arena, 1, mask);
+        check_launch("scatter faces");
+    }
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    if (blocks > 0) {
+        k_pack_ev<<<blocks, 128, 0, st>>>(t, fl, packed, arena, 1, mask, kb);
+        check_launch("scatter edges/vertices");
+    }
+}
+
+void launch_gather_owned(const LevelTables& t, const double* arena, double* packed, cudaStream_t st) {
+    if (t.nfaces > 0 && t.n >= 3) {
+        k_pack_faces<<<face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st>>>(t, arena, packed, 0, 0xff);
+        check_launch("gather faces");
+    }
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    if (blocks > 0) {
+        k_pack_ev<<<blocks, 128, 0, st>>>(t, FlagTables{}, arena, packed, 0, 0xff, kb);
+        check_launch("gather edges/vertices");
+    }
+}
+
+void launch_partials(int op, const LevelTables& t, const double* x1, const double* x2, double* part, double* scratch,
+                     cudaStream_t st) {
+    const int bands = t.n >= 3 ? (t.n - 2 + PB - 1) / PB : 0;
+    if (t.nfaces > 0 && bands > 0) {
+        const dim3 grid(unsigned(bands), unsigned(t.nfaces));
+        if (op == 0) k_partials_faces<0><<<grid, 256, 0, st>>>(t, x1, x2, scratch, bands);
+        else k_partials_faces<1><<<grid, 256, 0, st>>>(t, x1, x2, scratch, bands);
+        check_launch("partials faces");
+    }
+    const int total = t.nfaces + t.nedges + t.nverts;
+    if (total > 0) {
+        if (op == 0) k_partials_finish<0><<<(total + 127) / 128, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
+        else k_partials_finish<1><<<(total + 127) / 128, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
+        check_launch("partials finish");
+    }
+}
+
+void launch_combine_tree(int op, double* v, int64_t len, double* out, cudaStream_t st) {
+    if (op == 0) k_combine_tree<0><<<1, 1024, 0, st>>>(v, len, out);
+    else k_combine_tree<1><<<1, 1024, 0, st>>>(v, len, out);
+    check_launch("combine tree");
+}
+
+} // namespace hyb

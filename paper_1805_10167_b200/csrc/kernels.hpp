@@ -1,0 +1,100 @@
+// Device kernel interface for the P1 macro-face multigrid hot path (sm_100a).
+//
+// HBM layout of one (function, level) arena, all primitives local to this
+// process, 256-byte aligned blocks:
+//   [ faces : nfaces x face_stride doubles, padded row-major closed triangle ]
+//   [ edges : per edge  line(n+1) | halo row 1 of face 0 (n) | of face 1 (n) ]
+//   [ verts : per vertex own | one ghost per incident edge (ID order)      ]
+// Face row r (r = 0..n, length W-r, W = n+1) starts at rowoff[r], a multiple
+// of 4 doubles (32 B) so row loads are sector aligned and 16-byte vectorisable.
+// The reference stores the same DoFs in per-primitive std::vectors
+// (reference src/layout.cpp:38-138); halo row 0 is not stored because no P1
+// kernel reads it (reference src/operators.cpp:136-137, src/solvers.cpp:167-170).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hyb {
+
+/// Per-level stencil/transfer tables for all local primitives (device ptrs).
+struct LevelTables {
+    int level = 0, n = 1, W = 2;
+    int nfaces = 0, nedges = 0, nverts = 0;
+    int64_t face_stride = 0;          // doubles per face
+    int64_t faces_size = 0;           // nfaces * face_stride
+    int64_t arena_size = 0;           // total doubles
+    const int64_t* rowoff = nullptr;  // [W+1]
+    const double* face_coef = nullptr;  // [nfaces][8]: 7 terms + diag
+    const int64_t* edge_off = nullptr;  // [nedges]
+    const int8_t* edge_nf = nullptr;    // [nedges]
+    const double* edge_coef = nullptr;  // [nedges][8]: up to 7 terms + diag
+    const int64_t* vtx_off = nullptr;   // [nverts]
+    const int32_t* vtx_ne = nullptr;    // [nverts]
+    const int64_t* vtx_coef_off = nullptr; // [nverts] into vtx_coef
+    const double* vtx_coef = nullptr;      // own + per edge, then diag
+    const uint64_t* face_gid = nullptr; // global primitive IDs
+    const uint64_t* edge_gid = nullptr;
+    const uint64_t* vtx_gid = nullptr;
+    // packed owned order of local primitives: vertices, edges, faces by ID
+    int64_t owned_local = 0;
+};
+
+/// Per-function flags of the owned line / vertex DoFs (face interiors are
+/// always INNER, reference src/field.cpp:20-33).
+struct FlagTables {
+    const uint8_t* edge_flag = nullptr;
+    const uint8_t* vtx_flag = nullptr;
+};
+
+/// One contiguous ghost copy (a walk of `count` DoFs). Buffers: 0 arena,
+/// 1 send staging, 2 receive staging. Face walks address border rows:
+/// slot 0 (k, off), slot 1 (off, k), slot 2 (W-1-off-k, k); reversed walks
+/// run k -> count-1-k (reference src/indexing.cpp:61-83).
+struct CopySeg {
+    int64_t src;
+    int64_t dst;
+    int32_t count;
+    uint16_t src_mode;
+    uint16_t dst_mode;
+};
+enum : uint16_t {
+    SEG_BUF_MASK = 3,
+    SEG_FACE = 4,   // face walk addressing
+    SEG_SLOT_SHIFT = 3, // 2 bits
+    SEG_OFF1 = 32,  // row at distance 1 from the border
+    SEG_REV = 64,   // reversed walk
+};
+
+enum StencilMode : int { ST_APPLY = 0, ST_RESIDUAL = 1, ST_JACOBI = 2 };
+
+// ---- launchers (all asynchronous on `st`) ----
+// parts: 1 = face interiors (K1), 2 = edge lines + vertices (K2/K3), 3 = both
+void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const double* x, const double* b,
+                    double* y, double omega, uint8_t mask, cudaStream_t st, int parts = 3);
+/// number of kernels launched by this library so far (process-wide)
+int64_t kernel_launch_count();
+void launch_copy_segments(const CopySeg* segs, int nseg, const LevelTables& t, double* arena, double* sendbuf,
+                          double* recvbuf, cudaStream_t st);
+void launch_prolongate(const LevelTables& coarse, const LevelTables& fine, const FlagTables& fine_flags,
+                       const double* xc, double* xf, uint8_t mask, bool add, cudaStream_t st);
+void launch_restrict(const LevelTables& coarse, const LevelTables& fine, const FlagTables& coarse_flags,
+                     const double* xf, double* xc, uint8_t mask, cudaStream_t st);
+// dst := alpha*x1 + beta*x2 (op 0), dst += alpha*x1 (op 1), dst := alpha (op 2)
+void launch_blas1(int op, const LevelTables& t, const FlagTables& fl, double alpha, const double* x1, double beta,
+                  const double* x2, double* dst, uint8_t mask, cudaStream_t st);
+// counter-based U[lo,hi] keyed on (seed, stream, canonical DoF key)
+void launch_random(const LevelTables& t, const FlagTables& fl, uint64_t seed, uint64_t stream, double lo, double hi,
+                   double* dst, uint8_t mask, cudaStream_t st);
+// packed owned order <-> arena (local primitives); mask only for scatter
+void launch_scatter_owned(const LevelTables& t, const FlagTables& fl, const double* packed, double* arena,
+                          uint8_t mask, cudaStream_t st);
+void launch_gather_owned(const LevelTables& t, const double* arena, double* packed, cudaStream_t st);
+// per-primitive partials of sum(x1*x2) (op 0) or max|x1| (op 1) into
+// part[global id]; scratch >= nfaces * bands doubles
+void launch_partials(int op, const LevelTables& t, const double* x1, const double* x2, double* part,
+                     double* scratch, cudaStream_t st);
+// fixed pairwise fold (op 0 sum, op 1 max) of v[0..len) -> out[0]; v is clobbered
+void launch_combine_tree(int op, double* v, int64_t len, double* out, cudaStream_t st);
+
+} // namespace hyb

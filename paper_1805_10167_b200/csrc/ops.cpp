@@ -1,0 +1,389 @@
+// Operations on device-resident functions, with the reference's argument
+// checks and exception types (reference src/operators.cpp:322-505,
+// src/solvers.cpp:22-204, 385-465, src/function.cpp:11-241).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "domain.hpp"
+
+namespace hyb {
+
+namespace {
+
+constexpr uint8_t kSmoothMask = INNER | NEUMANN;
+constexpr uint8_t kDirichletMask = DIRICHLET;
+
+void check_op_function(const Operator& A, const Function& f, int level, const char* what, bool check_bc) {
+    if (&f.domain() != &A.domain()) throw InvalidArgument(std::string(what) + ": function lives on a different domain");
+    if (level < f.min_level() || level > f.max_level() || level < A.min_level() || level > A.max_level())
+        throw OutOfRange(std::string(what) + ": level " + std::to_string(level) + " outside the allocated range");
+    if (check_bc && !(f.bc() == A.bc()))
+        throw InvalidArgument(std::string(what) + ": boundary conditions differ from the operator's");
+}
+
+void check_pair(const char* op, const Function& a, const Function& b, int level) {
+    a.check_level(level, op);
+    b.check_level(level, op);
+    if (&a.domain() != &b.domain())
+        throw InvalidArgument(std::string(op) + ": '" + a.name() + "' and '" + b.name() + "' live on different domains");
+}
+
+void check_transfer(const Function& coarse, const Function& fine, int lc, const char* what) {
+    if (&coarse.domain() != &fine.domain())
+        throw InvalidArgument(std::string(what) + ": functions live on different domains");
+    if (lc < coarse.min_level() || lc > coarse.max_level() || lc + 1 < fine.min_level() || lc + 1 > fine.max_level())
+        throw OutOfRange(std::string(what) + ": level pair (" + std::to_string(lc) + ", " + std::to_string(lc + 1) +
+                         ") outside the functions' level ranges");
+}
+
+// zero diagonal on a row that a smoother would update -> runtime_error
+// (reference src/operators.cpp:457-458)
+void check_diagonals(const Operator& A, const Function& x, int level, const char* what) {
+    Domain& d = A.domain();
+    const MacroGraph& g = d.graph();
+    const int n = 1 << level;
+    const auto& hf = A.host_face_coef(level);
+    if (n >= 3)
+        for (size_t i = 0; i < d.local_faces().size(); ++i)
+            if (hf[i * 8 + 7] == 0.0) throw RuntimeError(std::string(what) + ": zero diagonal entry");
+    const auto& he = A.host_edge_coef(level);
+    if (n >= 2)
+        for (size_t i = 0; i < d.local_edges().size(); ++i)
+            if (!(x.bc().flag_for(g.edges[g.edge_index(d.local_edges()[i])].marker) & DIRICHLET) && he[i * 8 + 7] == 0.0)
+                throw RuntimeError(std::string(what) + ": zero diagonal entry");
+    const auto& hv = A.host_vtx_coef(level);
+    size_t pos = 0;
+    for (uint64_t id : d.local_verts()) {
+        const MacroVertex& v = g.vertices[id];
+        pos += 1 + v.edges.size();
+        if (!(x.bc().flag_for(v.marker) & DIRICHLET) && hv[pos] == 0.0)
+            throw RuntimeError(std::string(what) + ": zero diagonal entry");
+        pos += 1;
+    }
+}
+
+} // namespace
+
+void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t mask) {
+    check_op_function(A, src, level, "apply", false);
+    check_op_function(A, dst, level, "apply", true);
+    if (&src == &dst) throw InvalidArgument("apply: src and dst must be distinct functions");
+    Domain& d = A.domain();
+    d.sync(src, level); // full schedule first (reference src/operators.cpp:390)
+    const LevelTables t = A.tables(level);
+    launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, mask, d.stream(), 2);
+    d.timer_begin("apply");
+    launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, mask, d.stream(), 1);
+    d.timer_end();
+}
+
+void residual(const Operator& A, Function& rhs, Function& x, Function& r, int level) {
+    check_op_function(A, rhs, level, "residual", false);
+    check_op_function(A, x, level, "residual", false);
+    check_op_function(A, r, level, "residual", true);
+    if (&x == &r || &rhs == &r) throw InvalidArgument("residual: r must be distinct from x and rhs");
+    Domain& d = A.domain();
+    d.sync(x, level);
+    const LevelTables t = A.tables(level);
+    launch_stencil(ST_RESIDUAL, t, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
+                   d.stream(), 2);
+    d.timer_begin("residual");
+    launch_stencil(ST_RESIDUAL, t, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
+                   d.stream(), 1);
+    d.timer_end();
+}
+
+void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level) {
+    check_op_function(A, rhs, level, "smooth_jacobi", true);
+    check_op_function(A, x, level, "smooth_jacobi", true);
+    if (&rhs == &x) throw InvalidArgument("smooth_jacobi: rhs and x must be distinct functions");
+    check_diagonals(A, x, level, "smooth_jacobi");
+    Domain& d = A.domain();
+    d.sync(x, level);
+    DevMem& next = d.jacobi_scratch(level);
+    // pending write-back of the reference (src/operators.cpp:435-468) is a
+    // second buffer here: read x, write x', swap.
+    const LevelTables t = A.tables(level);
+    launch_stencil(ST_JACOBI, t, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
+                   d.stream(), 2);
+    d.timer_begin("jacobi");
+    launch_stencil(ST_JACOBI, t, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
+                   d.stream(), 1);
+    d.timer_end();
+    x.arena(level).swap(next);
+}
+
+void diagonal(const Operator& A, Function& dst, int level) {
+    check_op_function(A, dst, level, "diagonal", true);
+    Domain& d = A.domain();
+    const MacroGraph& g = d.graph();
+    const int n = 1 << level;
+    std::vector<double> packed(size_t(d.owned_local(level)));
+    size_t pos = 0;
+    const auto& hv = A.host_vtx_coef(level);
+    size_t cpos = 0;
+    for (uint64_t id : d.local_verts()) {
+        const MacroVertex& v = g.vertices[id];
+        const double diag = hv[cpos + 1 + v.edges.size()];
+        cpos += 2 + v.edges.size();
+        packed[pos++] = (dst.bc().flag_for(v.marker) & DIRICHLET) ? 1.0 : diag;
+    }
+    const auto& he = A.host_edge_coef(level);
+    for (size_t i = 0; i < d.local_edges().size(); ++i) {
+        const bool dir = dst.bc().flag_for(g.edges[g.edge_index(d.local_edges()[i])].marker) & DIRICHLET;
+        for (int k = 1; k <= n - 1; ++k) packed[pos++] = dir ? 1.0 : he[i * 8 + 7];
+    }
+    const auto& hf = A.host_face_coef(level);
+    const size_t per_face = size_t(n - 1) * size_t(std::max(n - 2, 0)) / 2;
+    for (size_t i = 0; i < d.local_faces().size(); ++i)
+        for (size_t k = 0; k < per_face; ++k) packed[pos++] = hf[i * 8 + 7];
+    upload(dst, level, packed.data(), int64_t(packed.size()), false, ALL_FLAGS);
+}
+
+void prolongate(Function& coarse, Function& fine, int lc, uint8_t mask, bool add) {
+    check_transfer(coarse, fine, lc, "prolongate");
+    Domain& d = fine.domain();
+    d.sync(coarse, lc);
+    d.timer_begin(add ? "prolongate_add" : "prolongate");
+    launch_prolongate(d.level(lc).t, d.level(lc + 1).t, fine.flags(), coarse.data(lc), fine.data(lc + 1), mask, add,
+                      d.stream());
+    d.timer_end();
+}
+
+void restrict_to_coarse(Function& fine, Function& coarse, int lc, uint8_t mask) {
+    check_transfer(coarse, fine, lc, "restrict_to_coarse");
+    Domain& d = fine.domain();
+    d.sync(fine, lc + 1);
+    d.timer_begin("restrict");
+    launch_restrict(d.level(lc).t, d.level(lc + 1).t, coarse.flags(), fine.data(lc + 1), coarse.data(lc), mask,
+                    d.stream());
+    d.timer_end();
+}
+
+void assign(double alpha, Function& x1, double beta, Function& x2, Function& dst, int level, uint8_t mask) {
+    check_pair("assign", x1, x2, level);
+    check_pair("assign", x1, dst, level);
+    Domain& d = dst.domain();
+    launch_blas1(0, d.level(level).t, dst.flags(), alpha, x1.data(level), beta, x2.data(level), dst.data(level), mask,
+                 d.stream());
+}
+
+void add_scaled(Function& dst, double gamma, Function& y, int level, uint8_t mask) {
+    check_pair("add_scaled", dst, y, level);
+    Domain& d = dst.domain();
+    launch_blas1(1, d.level(level).t, dst.flags(), gamma, y.data(level), 0.0, y.data(level), dst.data(level), mask,
+                 d.stream());
+}
+
+void fill_const(Function& f, double value, int level, uint8_t mask) {
+    f.check_level(level, "interpolate");
+    Domain& d = f.domain();
+    launch_blas1(2, d.level(level).t, f.flags(), value, f.data(level), 0.0, f.data(level), f.data(level), mask,
+                 d.stream());
+}
+
+void fill_random(Function& f, int level, uint64_t seed, uint64_t stream, double lo, double hi, uint8_t mask) {
+    f.check_level(level, "interpolate");
+    Domain& d = f.domain();
+    launch_random(d.level(level).t, f.flags(), seed, stream, lo, hi, f.data(level), mask, d.stream());
+}
+
+namespace {
+double reduce(int op, Function& a, Function& b, int level) {
+    Domain& d = a.domain();
+    const LevelTables& t = d.level(level).t;
+    const int64_t np = int64_t(d.graph().size());
+    const int bands = t.n >= 3 ? (t.n - 2 + 31) / 32 : 0;
+    double* buf = d.partials(2 * np + int64_t(t.nfaces) * bands + 1);
+    double* part = buf;
+    double* scratch = buf + 2 * np;
+    HYB_CUDA(cudaMemsetAsync(part, 0, size_t(np) * 8, d.stream()));
+    launch_partials(op, t, a.data(level), b.data(level), part, scratch, d.stream());
+    d.allreduce_sum(part, np); // one non-zero entry per primitive: exact
+    launch_combine_tree(op, part, np, d.scalar_out(), d.stream());
+    double out = 0.0;
+    HYB_CUDA(cudaMemcpyAsync(&out, d.scalar_out(), 8, cudaMemcpyDeviceToHost, d.stream()));
+    HYB_CUDA(cudaStreamSynchronize(d.stream()));
+    return out;
+}
+} // namespace
+
+double dot(Function& a, Function& b, int level) {
+    check_pair("dot", a, b, level);
+    return reduce(0, a, b, level);
+}
+
+double max_abs(Function& a, int level) {
+    a.check_level(level, "max_abs");
+    return reduce(1, a, a, level);
+}
+
+// ---------------------------------------------------------------- host <-> device
+namespace {
+// owned position of a local primitive's first DoF in the global ordering
+struct GlobalOrder {
+    int64_t nv, ne, n, per_face;
+    int64_t vertex(uint64_t id) const { return int64_t(id); }
+    int64_t edge(size_t ei) const { return nv + int64_t(ei) * (n - 1); }
+    int64_t face(size_t fi) const { return nv + ne * (n - 1) + int64_t(fi) * per_face; }
+};
+
+bool all_local(const Domain& d) {
+    return d.local_faces().size() == d.graph().nf() && d.local_edges().size() == d.graph().ne() &&
+           d.local_verts().size() == d.graph().nv();
+}
+
+// copies between the global vector and the local packed vector
+void global_local(Domain& d, int level, const double* src, double* dst, bool to_local) {
+    const MacroGraph& g = d.graph();
+    const int64_t n = int64_t(1) << level;
+    const GlobalOrder go{int64_t(g.nv()), int64_t(g.ne()), n, (n - 1) * (n - 2) / 2};
+    int64_t pos = 0;
+    auto mv = [&](int64_t gpos, int64_t len) {
+        if (len <= 0) return;
+        if (to_local) std::memcpy(dst + pos, src + gpos, size_t(len) * 8);
+        else std::memcpy(dst + gpos, src + pos, size_t(len) * 8);
+        pos += len;
+    };
+    for (uint64_t id : d.local_verts()) mv(go.vertex(id), 1);
+    for (uint64_t id : d.local_edges()) mv(go.edge(g.edge_index(id)), n - 1);
+    for (uint64_t id : d.local_faces()) mv(go.face(g.face_index(id)), go.per_face);
+}
+} // namespace
+
+void upload(Function& f, int level, const double* host, int64_t n, bool global_order, uint8_t mask) {
+    f.check_level(level, "upload");
+    Domain& d = f.domain();
+    const LevelTables& t = d.level(level).t;
+    const int64_t want = global_order ? d.owned_total(level) : t.owned_local;
+    if (n != want)
+        throw InvalidArgument("upload: vector has " + std::to_string(n) + " entries, expected " + std::to_string(want));
+    double* stage = d.staging(t.owned_local);
+    if (!global_order || all_local(d)) {
+        HYB_CUDA(cudaMemcpyAsync(stage, host, size_t(t.owned_local) * 8, cudaMemcpyHostToDevice, d.stream()));
+    } else {
+        std::vector<double> tmp(size_t(t.owned_local));
+        global_local(d, level, host, tmp.data(), true);
+        HYB_CUDA(cudaMemcpyAsync(stage, tmp.data(), tmp.size() * 8, cudaMemcpyHostToDevice, d.stream()));
+        HYB_CUDA(cudaStreamSynchronize(d.stream()));
+    }
+    launch_scatter_owned(t, f.flags(), stage, f.data(level), mask, d.stream());
+}
+
+void download(Function& f, int level, double* host, int64_t n, bool global_order) {
+    f.check_level(level, "download");
+    Domain& d = f.domain();
+    const LevelTables& t = d.level(level).t;
+    const int64_t want = global_order ? d.owned_total(level) : t.owned_local;
+    if (n != want)
+        throw InvalidArgument("download: vector has " + std::to_string(n) + " entries, expected " + std::to_string(want));
+    double* stage = d.staging(t.owned_local);
+    launch_gather_owned(t, f.data(level), stage, d.stream());
+    if (!global_order || all_local(d)) {
+        HYB_CUDA(cudaMemcpyAsync(host, stage, size_t(t.owned_local) * 8, cudaMemcpyDeviceToHost, d.stream()));
+        HYB_CUDA(cudaStreamSynchronize(d.stream()));
+    } else {
+        std::vector<double> tmp(size_t(t.owned_local));
+        HYB_CUDA(cudaMemcpyAsync(tmp.data(), stage, tmp.size() * 8, cudaMemcpyDeviceToHost, d.stream()));
+        HYB_CUDA(cudaStreamSynchronize(d.stream()));
+        global_local(d, level, tmp.data(), host, false);
+    }
+}
+
+// ---------------------------------------------------------------- Hierarchy
+Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc, int smoother, double omega,
+                     double coarse_tol, int coarse_max_iter)
+    : dom_(&d), a_(d, form, min_level, max_level, bc), r_(d, "mg.r", min_level, max_level, bc),
+      b_(d, "mg.b", min_level, max_level, bc), e_(d, "mg.e", min_level, max_level, bc),
+      cx_(d, "cg.x", min_level, min_level, bc), cr_(d, "cg.r", min_level, min_level, bc),
+      cp_(d, "cg.p", min_level, min_level, bc), cap_(d, "cg.ap", min_level, min_level, bc), smoother_(smoother),
+      omega_(omega), coarse_tol_(coarse_tol), coarse_max_iter_(coarse_max_iter) {
+    if (min_level < 0 || min_level > max_level)
+        throw InvalidArgument("GridHierarchy: need 0 <= min_level <= max_level");
+    if (smoother != SMOOTH_JACOBI) throw InvalidArgument("GridHierarchy: unknown smoother");
+    if (coarse_max_iter_ < 0) coarse_max_iter_ = int(d.owned_total(min_level)) + 100;
+}
+
+void Hierarchy::smooth(Function& rhs, Function& x, int level) { smooth_jacobi(a_, rhs, x, omega_, level); }
+
+void Hierarchy::vcycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
+    if (level < a_.min_level() || level > a_.max_level())
+        throw OutOfRange("vcycle: level " + std::to_string(level) + " outside [" + std::to_string(a_.min_level()) +
+                         ", " + std::to_string(a_.max_level()) + "]");
+    if (nu_pre < 0 || nu_post < 0) throw InvalidArgument("vcycle: negative smoothing count");
+    cycle(rhs, x, level, nu_pre, nu_post);
+}
+
+// reference src/solvers.cpp:406-428 with the smoother of the configuration
+void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
+    assign(1.0, rhs, 0.0, rhs, x, level, kDirichletMask);
+    if (level == a_.min_level()) {
+        coarse_correct(rhs, x);
+        return;
+    }
+    for (int i = 0; i < nu_pre; ++i) smooth(rhs, x, level);
+    residual(a_, rhs, x, r_, level);
+    restrict_to_coarse(r_, b_, level - 1, ALL_FLAGS);
+    fill_const(b_, 0.0, level - 1, kDirichletMask);
+    fill_const(e_, 0.0, level - 1, ALL_FLAGS);
+    cycle(b_, e_, level - 1, nu_pre, nu_post);
+    // prolongate(e -> r) + add_scaled(x, 1, r) on the smooth mask, fused
+    prolongate(e_, x, level - 1, kSmoothMask, true);
+    for (int i = 0; i < nu_post; ++i) smooth(rhs, x, level);
+}
+
+// reference src/solvers.cpp:430-442 + cg_solve :226-259, matrix-free on device
+void Hierarchy::coarse_correct(Function& rhs, Function& x) {
+    const int L = a_.min_level();
+    residual(a_, rhs, x, r_, L);
+    fill_const(cx_, 0.0, L, ALL_FLAGS);
+    assign(1.0, r_, 0.0, r_, cr_, L, ALL_FLAGS);
+    assign(1.0, cr_, 0.0, cr_, cp_, L, ALL_FLAGS);
+    const double target = coarse_tol_ * std::sqrt(dot(r_, r_, L));
+    double rs = dot(cr_, cr_, L);
+    int it = 0;
+    while (it < coarse_max_iter_ && std::sqrt(rs) > target) {
+        apply(a_, cp_, cap_, L, ALL_FLAGS);
+        const double pap = dot(cp_, cap_, L);
+        if (pap <= 0.0) break; // non-positive curvature: breakdown
+        const double alpha = rs / pap;
+        add_scaled(cx_, alpha, cp_, L, ALL_FLAGS);
+        add_scaled(cr_, -alpha, cap_, L, ALL_FLAGS);
+        const double rs_new = dot(cr_, cr_, L);
+        const double beta = rs_new / rs;
+        assign(1.0, cr_, beta, cp_, cp_, L, ALL_FLAGS);
+        rs = rs_new;
+        ++it;
+    }
+    last_coarse_iterations = it;
+    residual(a_, r_, cx_, cap_, L); // true residual of the returned iterate
+    const double true_res = std::sqrt(dot(cap_, cap_, L));
+    if (!(true_res <= target)) throw RuntimeError("vcycle: coarse CG did not converge");
+    add_scaled(x, 1.0, cx_, L, kSmoothMask);
+}
+
+double Hierarchy::residual_norm(Function& rhs, Function& x, int level) {
+    residual(a_, rhs, x, r_, level);
+    return std::sqrt(dot(r_, r_, level));
+}
+
+std::vector<double> Hierarchy::solve(Function& rhs, Function& x, int level, double tol, int max_cycles, int nu_pre,
+                                     int nu_post, bool* converged) {
+    if (level < a_.min_level() || level > a_.max_level())
+        throw OutOfRange("solve: level " + std::to_string(level) + " outside the hierarchy");
+    if (nu_pre < 0 || nu_post < 0) throw InvalidArgument("solve: negative smoothing count");
+    std::vector<double> res{residual_norm(rhs, x, level)};
+    const double r0 = res.front();
+    const double target = r0 > 0.0 ? tol * r0 : tol;
+    int it = 0;
+    while (it < max_cycles && res.back() > target) {
+        cycle(rhs, x, level, nu_pre, nu_post);
+        ++it;
+        res.push_back(residual_norm(rhs, x, level));
+    }
+    if (converged) *converged = res.back() <= target;
+    return res;
+}
+
+} // namespace hyb

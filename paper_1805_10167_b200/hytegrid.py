@@ -1,0 +1,443 @@
+"""Reference-shaped host API over the B200 C ABI.
+
+Mirrors the reference's public C++ API for the multigrid hot path
+(/root/reference/proj/include/hytegrid/{primitives,function,operators,
+solvers}.hpp): same names, argument meaning and error classes, so code written
+against ``hytegrid`` ports line by line. Differences, all forced by device
+residency:
+
+* values live in HBM; ``ScalarFunction.values(id, level)`` is replaced by
+  ``upload`` / ``download`` of owned DoFs in GlobalDoFMap order
+  (numbering.hpp:41-43);
+* ``interpolate`` with a Python callable evaluates it on the host at the
+  owned DoF coordinates (bitwise the reference's for_each_owned_coord) and
+  uploads the masked values; ``interpolate_random`` and constants run on the
+  device;
+* ``Controller`` carries no state: ghost-exchange plans belong to the domain,
+  and ``register_function`` is accepted for source compatibility.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import (CudaError, HybError, HybRuntimeError, InvalidArgument, LogicError, NcclError,  # noqa: F401
+                   OutOfRange, check, lib)
+
+INNER = 1
+DIRICHLET = 2
+NEUMANN = 4
+ALL_DOF_FLAGS = 7
+SMOOTH_MASK = INNER | NEUMANN
+
+LAPLACE = 0
+MASS = 1
+
+SMOOTHERS = {"jacobi": 0}
+
+
+def _pd(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _text_call(fn, *args) -> str:
+    n = C.c_int64(0)
+    check(fn(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(fn(*args, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+class meshgen:
+    """Fixture meshes in the reference mesh-file format (src/meshgen.cpp)."""
+
+    @staticmethod
+    def _gen(kind: str, *params: float) -> str:
+        arr = (C.c_double * max(len(params), 1))(*params)
+        return _text_call(lib.hyb_meshgen, kind.encode(), arr, len(params))
+
+    @staticmethod
+    def unit_triangle() -> str:
+        return meshgen._gen("unit_triangle")
+
+    @staticmethod
+    def unit_square() -> str:
+        return meshgen._gen("unit_square")
+
+    @staticmethod
+    def unit_square_reversed() -> str:
+        return meshgen._gen("unit_square_reversed")
+
+    @staticmethod
+    def square_ring8() -> str:
+        return meshgen._gen("square_ring8")
+
+    @staticmethod
+    def channel(nx: int, ny: int, width: float = 1.0, height: float = 1.0) -> str:
+        return meshgen._gen("channel", nx, ny, width, height)
+
+    @staticmethod
+    def annulus(segments: int, layers: int, r_inner: float, r_outer: float) -> str:
+        return meshgen._gen("annulus", segments, layers, r_inner, r_outer)
+
+    @staticmethod
+    def perturb(mesh_text: str, frac: float, seed: int) -> str:
+        return _text_call(lib.hyb_mesh_perturb, mesh_text.encode(), frac, seed)
+
+
+def mesh_counts(mesh_text: str) -> tuple[int, int, int]:
+    nv, ne, nf = C.c_int64(), C.c_int64(), C.c_int64()
+    check(lib.hyb_mesh_counts(mesh_text.encode(), C.byref(nv), C.byref(ne), C.byref(nf)))
+    return nv.value, ne.value, nf.value
+
+
+def _partition(mesh_text: str, ranks: int, kind: int, level: int) -> np.ndarray:
+    out = np.zeros(sum(mesh_counts(mesh_text)), dtype=np.int32)
+    check(lib.hyb_partition(mesh_text.encode(), ranks, kind, level, out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+
+
+def partition_round_robin(mesh_text: str, ranks: int) -> np.ndarray:
+    return _partition(mesh_text, ranks, 0, 0)
+
+
+def partition_greedy_edgecut(mesh_text: str, ranks: int, weight_level: int) -> np.ndarray:
+    return _partition(mesh_text, ranks, 1, weight_level)
+
+
+def stencil_host(mesh_text: str, level: int, primitive_id: int, form: int = 0) -> np.ndarray:
+    """Stencil of one primitive assembled on the host (no device needed)."""
+    out = np.zeros(64)
+    n = C.c_int()
+    check(lib.hyb_stencil_host(mesh_text.encode(), form, level, primitive_id, _pd(out), 64, C.byref(n)))
+    return out[: n.value].copy()
+
+
+def _bc_arrays(bc: dict | None):
+    bc = bc or {}
+    markers = (C.c_int32 * max(len(bc), 1))(*[int(k) for k in bc])
+    flags = (C.c_uint8 * max(len(bc), 1))(*[int(v) for v in bc.values()])
+    return markers, flags, len(bc)
+
+
+class DistributedDomain:
+    """Macro-primitive graph distributed over ``ranks`` logical ranks.
+
+    ``local_ranks`` (default: all) are driven by this process on ``device``;
+    co-resident ranks exchange ghosts through device copies, remote ranks
+    (one per process) through NCCL after ``connect_nccl``.
+    """
+
+    def __init__(self, mesh_text: str, ranks: int = 1, assignment=None, local_ranks=None, device: int = 0):
+        self.mesh_text = mesh_text
+        self.ranks = ranks
+        self.counts = mesh_counts(mesh_text)
+        if assignment is None:
+            assignment = partition_round_robin(mesh_text, ranks)
+        self.assignment = np.ascontiguousarray(assignment, dtype=np.int32)
+        lr = list(range(ranks)) if local_ranks is None else list(local_ranks)
+        lr_arr = (C.c_int32 * len(lr))(*lr)
+        h = C.c_void_p()
+        check(lib.hyb_domain_create(mesh_text.encode(), ranks, self.assignment.ctypes.data_as(C.POINTER(C.c_int32)),
+                                    lr_arr, len(lr), device, C.byref(h)))
+        self._h = h
+        self.local_ranks = lr
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.hyb_domain_destroy(self._h)
+            self._h = None
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib.hyb_nccl_unique_id(buf))
+        return buf.raw
+
+    def connect_nccl(self, uid: bytes, rank: int) -> None:
+        check(lib.hyb_domain_connect_nccl(self._h, uid, rank))
+
+    def owned_count(self, level: int) -> tuple[int, int]:
+        t, l_ = C.c_int64(), C.c_int64()
+        check(lib.hyb_domain_owned_count(self._h, level, C.byref(t), C.byref(l_)))
+        return t.value, l_.value
+
+    def arena_bytes(self, level: int) -> int:
+        b = C.c_int64()
+        check(lib.hyb_domain_arena_bytes(self._h, level, C.byref(b)))
+        return b.value
+
+    def coords(self, level: int, global_order: bool = True) -> np.ndarray:
+        n = self.owned_count(level)[0 if global_order else 1]
+        xy = np.zeros((n, 2))
+        check(lib.hyb_owned_coords(self._h, level, int(global_order), _pd(xy), n))
+        return xy
+
+    def synchronize(self) -> None:
+        check(lib.hyb_domain_synchronize(self._h))
+
+    def profile(self, enable: bool = True) -> None:
+        check(lib.hyb_domain_profile(self._h, int(enable)))
+
+    def timer(self, name: str) -> tuple[float, int]:
+        ms, cnt = C.c_double(), C.c_int64()
+        check(lib.hyb_domain_timer(self._h, name.encode(), C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
+    def timer_reset(self) -> None:
+        check(lib.hyb_domain_timer_reset(self._h))
+
+    def event_record(self, slot: int) -> None:
+        check(lib.hyb_domain_event_record(self._h, slot))
+
+    def event_elapsed(self, a: int, b: int) -> float:
+        ms = C.c_double()
+        check(lib.hyb_domain_event_elapsed(self._h, a, b, C.byref(ms)))
+        return ms.value
+
+
+def kernel_launches() -> int:
+    n = C.c_int64()
+    check(lib.hyb_kernel_launches(C.byref(n)))
+    return n.value
+
+
+class Controller:
+    """Stateless stand-in for hytegrid::Controller (exchange plans live in the domain)."""
+
+    def __init__(self, domain: DistributedDomain):
+        self.domain = domain
+
+
+def register_function(ctl: Controller, f: "ScalarFunction") -> None:  # noqa: ARG001 - API parity
+    return None
+
+
+class ScalarFunction:
+    """P1 grid function: one HBM arena per level (zero-initialised)."""
+
+    def __init__(self, name: str, domain: DistributedDomain, min_level: int, max_level: int, bc: dict | None = None):
+        self.name = name
+        self.domain = domain
+        self.min_level = min_level
+        self.max_level = max_level
+        self.bc = dict(bc or {})
+        m, f, n = _bc_arrays(self.bc)
+        h = C.c_void_p()
+        check(lib.hyb_function_create(domain._h, name.encode(), min_level, max_level, m, f, n, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.hyb_function_destroy(self._h)
+            self._h = None
+
+    def _n(self, level: int, global_order: bool) -> int:
+        return self.domain.owned_count(level)[0 if global_order else 1]
+
+    def upload(self, level: int, values, global_order: bool = True, mask: int = ALL_DOF_FLAGS) -> None:
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        check(lib.hyb_function_upload(self._h, level, _pd(v), v.size, int(global_order), mask))
+
+    def download(self, level: int, global_order: bool = True, out: np.ndarray | None = None) -> np.ndarray:
+        n = self._n(level, global_order)
+        if out is None:
+            out = np.empty(n)
+        check(lib.hyb_function_download(self._h, level, _pd(out), n, int(global_order)))
+        return out
+
+    def flags(self, level: int, global_order: bool = True) -> np.ndarray:
+        n = self._n(level, global_order)
+        out = np.zeros(n, dtype=np.uint8)
+        check(lib.hyb_function_flags(self._h, level, out.ctypes.data_as(C.POINTER(C.c_uint8)), n,
+                                     int(global_order)))
+        return out
+
+
+class StencilOperator:
+    """Constant-coefficient P1 operator (LAPLACE or MASS), stencils per level."""
+
+    def __init__(self, domain: DistributedDomain, form: int = LAPLACE, min_level: int = 0, max_level: int = 0,
+                 bc: dict | None = None):
+        self.domain = domain
+        self.form = form
+        self.min_level = min_level
+        self.max_level = max_level
+        self.bc = dict(bc or {})
+        m, f, n = _bc_arrays(self.bc)
+        h = C.c_void_p()
+        check(lib.hyb_operator_create(domain._h, form, min_level, max_level, m, f, n, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.hyb_operator_destroy(self._h)
+            self._h = None
+
+    def stencil(self, level: int, primitive_id: int) -> np.ndarray:
+        out = np.zeros(64)
+        n = C.c_int()
+        check(lib.hyb_operator_stencil(self._h, level, primitive_id, _pd(out), 64, C.byref(n)))
+        return out[: n.value].copy()
+
+
+# ---------------------------------------------------------------- operations
+def interpolate(f: ScalarFunction, expr, level: int, flag_mask: int = ALL_DOF_FLAGS) -> None:
+    """Owned DoFs with flag in mask := expr(x, y) (or a constant)."""
+    if callable(expr):
+        xy = f.domain.coords(level, global_order=False)
+        vals = np.asarray(expr(xy[:, 0], xy[:, 1]), dtype=np.float64)
+        if vals.shape != (xy.shape[0],):
+            vals = np.array([expr(x, y) for x, y in xy], dtype=np.float64)
+        f.upload(level, vals, global_order=False, mask=flag_mask)
+    else:
+        check(lib.hyb_interpolate_const(f._h, float(expr), level, flag_mask))
+
+
+def interpolate_random(f: ScalarFunction, level: int, seed: int, stream: int = 0, lo: float = -1.0, hi: float = 1.0,
+                       flag_mask: int = ALL_DOF_FLAGS) -> None:
+    check(lib.hyb_interpolate_random(f._h, level, seed, stream, lo, hi, flag_mask))
+
+
+def sync_all(ctl: Controller, f: ScalarFunction, level: int) -> None:  # noqa: ARG001
+    check(lib.hyb_sync(f._h, level))
+
+
+def apply(A: StencilOperator, ctl: Controller, src: ScalarFunction, dst: ScalarFunction, level: int,  # noqa: ARG001
+          flag_mask: int = ALL_DOF_FLAGS) -> None:
+    check(lib.hyb_apply(A._h, src._h, dst._h, level, flag_mask))
+
+
+def residual(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: ScalarFunction,  # noqa: ARG001
+             r: ScalarFunction, level: int) -> None:
+    check(lib.hyb_residual(A._h, rhs._h, x._h, r._h, level))
+
+
+def smooth_jacobi(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: ScalarFunction,  # noqa: ARG001
+                  omega: float, level: int) -> None:
+    check(lib.hyb_smooth_jacobi(A._h, rhs._h, x._h, omega, level))
+
+
+def diagonal(A: StencilOperator, d: ScalarFunction, level: int) -> None:
+    check(lib.hyb_diagonal(A._h, d._h, level))
+
+
+def prolongate(ctl: Controller, coarse: ScalarFunction, fine: ScalarFunction, coarse_level: int,  # noqa: ARG001
+               flag_mask: int = ALL_DOF_FLAGS) -> None:
+    check(lib.hyb_prolongate(coarse._h, fine._h, coarse_level, flag_mask))
+
+
+def prolongate_add(ctl: Controller, coarse: ScalarFunction, fine: ScalarFunction, coarse_level: int,  # noqa: ARG001
+                   flag_mask: int = ALL_DOF_FLAGS) -> None:
+    check(lib.hyb_prolongate_add(coarse._h, fine._h, coarse_level, flag_mask))
+
+
+def restrict_to_coarse(ctl: Controller, fine: ScalarFunction, coarse: ScalarFunction, coarse_level: int,  # noqa
+                       flag_mask: int = ALL_DOF_FLAGS) -> None:
+    check(lib.hyb_restrict(fine._h, coarse._h, coarse_level, flag_mask))
+
+
+def assign(alpha: float, x1: ScalarFunction, beta: float, x2: ScalarFunction, dst: ScalarFunction, level: int,
+           flag_mask: int = ALL_DOF_FLAGS) -> None:
+    check(lib.hyb_assign(alpha, x1._h, beta, x2._h, dst._h, level, flag_mask))
+
+
+def add_scaled(dst: ScalarFunction, gamma: float, y: ScalarFunction, level: int,
+               flag_mask: int = ALL_DOF_FLAGS) -> None:
+    check(lib.hyb_add_scaled(dst._h, gamma, y._h, level, flag_mask))
+
+
+def dot(a: ScalarFunction, b: ScalarFunction, level: int) -> float:
+    out = C.c_double()
+    check(lib.hyb_dot(a._h, b._h, level, C.byref(out)))
+    return out.value
+
+
+def norm2(a: ScalarFunction, level: int) -> float:
+    out = C.c_double()
+    check(lib.hyb_norm2(a._h, level, C.byref(out)))
+    return out.value
+
+
+def max_abs(a: ScalarFunction, level: int) -> float:
+    out = C.c_double()
+    check(lib.hyb_max_abs(a._h, level, C.byref(out)))
+    return out.value
+
+
+@dataclass
+class SolveReport:
+    """reference include/hytegrid/solvers.hpp:42-50"""
+    converged: bool = False
+    iterations: int = 0
+    residuals: list = field(default_factory=list)
+
+    def history(self) -> str:
+        lines = []
+        for k, r in enumerate(self.residuals):
+            if k == 0:
+                lines.append(f"cycle {k} residual {r:.6e}")
+            else:
+                prev = self.residuals[k - 1]
+                f = r / prev if prev > 0 else 0.0
+                lines.append(f"cycle {k} residual {r:.6e} factor {f:.4f}")
+        return "\n".join(lines) + "\n"
+
+
+class GridHierarchy:
+    """V-cycle multigrid (reference GridHierarchy, solvers.hpp:81-102).
+
+    smoother 'jacobi' with weight omega; coarse level solved on the device by
+    CG to coarse_tol (reference default 1e-12, max_iter #DoFs + 100).
+    """
+
+    def __init__(self, domain: DistributedDomain, ctl: Controller, form: int, min_level: int, max_level: int,  # noqa
+                 bc: dict | None = None, smoother: str = "jacobi", omega: float = 2.0 / 3.0,
+                 coarse_tol: float = 1e-12, coarse_max_iter: int = -1):
+        self.domain = domain
+        self.min_level = min_level
+        self.max_level = max_level
+        m, f, n = _bc_arrays(bc)
+        h = C.c_void_p()
+        check(lib.hyb_hierarchy_create(domain._h, form, min_level, max_level, m, f, n, SMOOTHERS[smoother], omega,
+                                       coarse_tol, coarse_max_iter, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.hyb_hierarchy_destroy(self._h)
+            self._h = None
+
+    def vcycle(self, rhs: ScalarFunction, x: ScalarFunction, level: int, nu_pre: int = 2, nu_post: int = 2) -> None:
+        check(lib.hyb_hierarchy_vcycle(self._h, rhs._h, x._h, level, nu_pre, nu_post))
+
+    def residual_norm(self, rhs: ScalarFunction, x: ScalarFunction, level: int) -> float:
+        out = C.c_double()
+        check(lib.hyb_hierarchy_residual_norm(self._h, rhs._h, x._h, level, C.byref(out)))
+        return out.value
+
+    def solve(self, rhs: ScalarFunction, x: ScalarFunction, level: int, tol: float, max_cycles: int,
+              nu_pre: int = 2, nu_post: int = 2) -> SolveReport:
+        res = np.zeros(max_cycles + 1)
+        n = C.c_int()
+        conv = C.c_int()
+        check(lib.hyb_hierarchy_solve(self._h, rhs._h, x._h, level, tol, max_cycles, nu_pre, nu_post, _pd(res),
+                                      C.byref(n), C.byref(conv)))
+        return SolveReport(bool(conv.value), n.value - 1, list(res[: n.value]))
+
+
+class PinnedBuffer:
+    """Page-locked host memory (for end-to-end H2D/D2H timing)."""
+
+    def __init__(self, n_doubles: int):
+        p = C.c_void_p()
+        check(lib.hyb_host_alloc(n_doubles * 8, C.byref(p)))
+        self._p = p
+        self.array = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=(n_doubles,))
+
+    def __del__(self):
+        if getattr(self, "_p", None):
+            lib.hyb_host_free(self._p)
+            self._p = None
