@@ -15,7 +15,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC -Xptxa
 CXXFLAGS := -O2 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -I$(CUDA)/include
 LDFLAGS  := -shared -static-libstdc++ -static-libgcc -Wl,--exclude-libs,ALL -L$(CUDA)/lib64 -lcudart_static -ldl -lpthread -lrt
 
-HDRS := $(wildcard $(CSRC)/*.hpp) include/hyteg_b200.h
+HDRS := $(wildcard $(CSRC)/*.hpp) $(wildcard $(CSRC)/*.cuh) include/hyteg_b200.h
 OBJS := $(BUILD)/kernels.o $(BUILD)/setup.o $(BUILD)/domain.o $(BUILD)/ops.o $(BUILD)/capi.o
 
 .PHONY: all lib oracle clean

@@ -1,0 +1,190 @@
+// K1: face stencil (apply / residual / Jacobi) over macro-face interiors.
+// Included by kernels.cu.
+//
+// One CTA = one (face, 256-column block, band of FS_RB rows). A producer warp
+// streams the band's row segments HBM -> shared memory with 1-D bulk copies
+// (cp.async.bulk, the TMA engine) into an FS_S-stage ring guarded by
+// mbarriers (full: bytes landed; empty: all consumer warps done). Four
+// consumer warps own 2 columns per lane and march up the band with a 3-row
+// register window (rows r-1, r from registers, row r+1 from the stage), so
+// x is read from HBM once per band (+2 halo rows, L2 hits) and the loads in
+// flight are bounded by shared memory, not registers.
+//
+// Row term order W NW S C N SE E from acc = 0, separately rounded (built with
+// -fmad=false): bitwise the reference's face row (src/operators.cpp:308-316,
+// 403-417) and Jacobi update (:461).
+#pragma once
+
+constexpr int FS_CWARPS = 4;                 // consumer warps
+constexpr int FS_THREADS = (FS_CWARPS + 1) * 32;
+constexpr int FS_COLS = FS_CWARPS * 64;      // 256 columns per CTA
+constexpr int FS_XW = FS_COLS + 4;           // staged x columns [c0-2, c0+FS_COLS+2)
+constexpr int FS_RB = 64;                    // rows per band
+constexpr int FS_S = 8;                      // pipeline stages
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int MODE> struct FaceSmem {
+    double x[FS_S][FS_XW];
+    double b[MODE == ST_APPLY ? 1 : FS_S][FS_COLS];
+    uint64_t full[FS_S];
+    uint64_t empty[FS_S];
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, const double* __restrict__ x,
+                                                                 const double* __restrict__ b,
+                                                                 double* __restrict__ y, double omega) {
+    __shared__ __align__(128) FaceSmem<MODE> sm;
+    const int n = t.n, W = t.W;
+    const int face = blockIdx.z;
+    const int c0 = blockIdx.x * FS_COLS;
+    int r_lo = blockIdx.y * FS_RB;
+    if (r_lo < 1) r_lo = 1;
+    int r_hi = (blockIdx.y + 1) * FS_RB; // exclusive
+    if (r_hi > n - 1) r_hi = n - 1;     // interior rows r <= n-2
+    const int cmin = c0 < 1 ? 1 : c0;
+    if (r_hi > n - cmin) r_hi = n - cmin; // first column of the block stays interior
+    if (r_lo >= r_hi) return;           // CTA-uniform, before any barrier use
+    const int nrows = r_hi - r_lo;      // computed rows
+    const int nstage = nrows + 2;       // x rows r_lo-1 .. r_hi
+
+    const int64_t base = int64_t(face) * t.face_stride;
+    const int64_t* __restrict__ ro = t.rowoff;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < FS_S; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], FS_CWARPS);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == FS_CWARPS) {
+        // ---------------- producer: one lane issues the bulk copies
+        if (lane == 0) {
+            const double* xf = x + base;
+            const double* bf = b + base;
+            for (int i = 0; i < nstage; ++i) {
+                const int s = i % FS_S;
+                mbar_wait(&sm.empty[s], ((i / FS_S) & 1) ^ 1);
+                const int q = r_lo - 1 + i; // x row of this stage
+                const int plen = (W - q + 3) & ~3; // padded row length
+                const int xs = c0 - 2 < 0 ? 0 : c0 - 2;
+                const int xe = c0 - 2 + FS_XW < plen ? c0 - 2 + FS_XW : plen;
+                const uint32_t bx = xe > xs ? uint32_t(xe - xs) * 8u : 0u;
+                uint32_t bb = 0;
+                int be = 0;
+                if (MODE != ST_APPLY && i >= 2) { // b row q-1 pairs with x row q
+                    const int pb = (W - (q - 1) + 3) & ~3;
+                    be = c0 + FS_COLS < pb ? c0 + FS_COLS : pb;
+                    bb = be > c0 ? uint32_t(be - c0) * 8u : 0u;
+                }
+                mbar_arrive_expect_tx(&sm.full[s], bx + bb);
+                if (bx) bulk_g2s(&sm.x[s][xs - (c0 - 2)], xf + ro[q] + xs, bx, &sm.full[s]);
+                if (MODE != ST_APPLY && bb) bulk_g2s(&sm.b[s][0], bf + ro[q - 1] + c0, bb, &sm.full[s]);
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: lane owns columns c, c+1
+    const int tid = threadIdx.x; // 0 .. 127
+    const int c = c0 + 2 * tid;
+    const int k = 2 + 2 * tid; // smem index of column c
+    const double* co = t.face_coef + size_t(face) * 8;
+    const double cW = co[0], cNW = co[1], cS = co[2], cC = co[3], cN = co[4], cSE = co[5], cE = co[6], dg = co[7];
+    double* __restrict__ yf = y + base;
+
+    // window: rows r-1 (m*) and r (z*) at columns c-1, c, c+1, c+2
+    double ml = 0, m0 = 0, m1 = 0, mr = 0, zl = 0, z0 = 0, z1 = 0, zr = 0;
+    for (int i = 0; i < nstage; ++i) {
+        const int s = i % FS_S;
+        mbar_wait(&sm.full[s], (i / FS_S) & 1);
+        const double* sx = sm.x[s];
+        const double2 pl2 = *reinterpret_cast<const double2*>(sx + k - 2);
+        const double2 pc2 = *reinterpret_cast<const double2*>(sx + k);
+        const double2 pr2 = *reinterpret_cast<const double2*>(sx + k + 2);
+        double2 bb = make_double2(0.0, 0.0);
+        if (MODE != ST_APPLY && i >= 2) bb = *reinterpret_cast<const double2*>(&sm.b[s][2 * tid]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        const double pl = pl2.y, p0 = pc2.x, p1 = pc2.y, pr = pr2.x;
+        if (i >= 2) {
+            const int r = r_lo + i - 2;
+            const int last = n - 1 - r; // last interior column of row r
+            const bool v0 = c >= 1 && c <= last;
+            const bool v1 = c + 1 <= last;
+            if (v0 || v1) {
+                double a0 = 0.0;
+                a0 += cW * zl;
+                a0 += cNW * pl;
+                a0 += cS * m0;
+                a0 += cC * z0;
+                a0 += cN * p0;
+                a0 += cSE * m1;
+                a0 += cE * z1;
+                double a1 = 0.0;
+                a1 += cW * z0;
+                a1 += cNW * p0;
+                a1 += cS * m1;
+                a1 += cC * z1;
+                a1 += cN * p1;
+                a1 += cSE * mr;
+                a1 += cE * zr;
+                double o0 = a0, o1 = a1;
+                if (MODE == ST_RESIDUAL) {
+                    o0 = bb.x - a0;
+                    o1 = bb.y - a1;
+                } else if (MODE == ST_JACOBI) {
+                    o0 = z0 + omega * (bb.x - a0) / dg;
+                    o1 = z1 + omega * (bb.y - a1) / dg;
+                }
+                double* yrow = yf + ro[r];
+                if (v0 && v1) {
+                    __stcs(reinterpret_cast<double2*>(yrow + c), make_double2(o0, o1));
+                } else {
+                    if (v0) yrow[c] = o0;
+                    if (v1) yrow[c + 1] = o1;
+                }
+            }
+        }
+        ml = zl; m0 = z0; m1 = z1; mr = zr;
+        zl = pl; z0 = p0; z1 = p1; zr = pr;
+    }
+    (void)ml;
+}
+
+inline dim3 face_stencil_grid(const LevelTables& t) {
+    return dim3(unsigned((t.n - 1 + FS_COLS - 1) / FS_COLS), unsigned((t.n - 1 + FS_RB - 1) / FS_RB),
+                unsigned(t.nfaces));
+}

@@ -34,142 +34,7 @@ __device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xf
 __device__ __forceinline__ double shfl_down1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
 // ---------------------------------------------------------------------------
-// K1: face stencil (apply / residual / Jacobi) over face interiors.
-//
-// CTA = 4 independent warps; a warp owns 64 consecutive columns (2 per lane,
-// 16-byte loads) of one face and marches up a band of rows with a 3-row
-// register window; c-1 / c+1 neighbours come from warp shuffles, the two
-// columns beyond the warp from one predicated load per row (lanes 0 / 31).
-// Rows are prefetched FS_PF ahead so each lane keeps several 16-byte loads
-// in flight (HBM latency hiding without shared memory).
-// ---------------------------------------------------------------------------
-constexpr int FS_WARPS = 4;
-constexpr int FS_COLS = 64;
-constexpr int FS_RB = 64;
-constexpr int FS_PF = 4;
-
-template <int MODE>
-__global__ void __launch_bounds__(FS_WARPS * 32) k_face_stencil(LevelTables t, const double* __restrict__ x,
-                                                                const double* __restrict__ b,
-                                                                double* __restrict__ y, double omega) {
-    const int n = t.n, W = t.W;
-    const int face = blockIdx.z;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c0 = (blockIdx.x * FS_WARPS + warp) * FS_COLS;
-    int r_lo = blockIdx.y * FS_RB;
-    if (r_lo < 1) r_lo = 1;
-    int r_hi = (blockIdx.y + 1) * FS_RB; // exclusive
-    if (r_hi > n - 1) r_hi = n - 1;     // interior rows r <= n-2
-    const int cmin = c0 < 1 ? 1 : c0;
-    if (r_hi > n - cmin) r_hi = n - cmin; // first column stays interior: r <= n-1-cmin
-    if (r_lo >= r_hi) return;           // warp-uniform
-
-    const int64_t base = int64_t(face) * t.face_stride;
-    const double* __restrict__ xf = x + base;
-    const double* __restrict__ bf = b + base;
-    double* __restrict__ yf = y + base;
-    const int64_t* __restrict__ ro = t.rowoff;
-    const double* co = t.face_coef + size_t(face) * 8;
-    const double cW = co[0], cNW = co[1], cS = co[2], cC = co[3], cN = co[4], cSE = co[5], cE = co[6], dg = co[7];
-
-    const int c = c0 + 2 * lane;
-    const bool edge_lane = (lane == 0 && c0 > 0) || lane == 31;
-    const int ce = lane == 0 ? c0 - 1 : c0 + FS_COLS;
-
-    // x row q: (c, c+1) pair and this lane's out-of-warp neighbour column
-    auto ldx = [&](int q, double2& v, double& ex) {
-        v = make_double2(0.0, 0.0);
-        ex = 0.0;
-        if (q <= r_hi) {
-            const int len = W - q;
-            const double* row = xf + ro[q];
-            if (c < len) v = __ldg(reinterpret_cast<const double2*>(row + c));
-            if (edge_lane && ce < len) ex = __ldg(row + ce);
-        }
-    };
-    auto ldb = [&](int q, double2& v) {
-        v = make_double2(0.0, 0.0);
-        if (MODE != ST_APPLY && q < r_hi) {
-            const int len = W - q;
-            if (c < len) v = __ldg(reinterpret_cast<const double2*>(bf + ro[q] + c));
-        }
-    };
-
-    double2 xm, x0;
-    double exm, ex0;
-    ldx(r_lo - 1, xm, exm);
-    ldx(r_lo, x0, ex0);
-    double2 q[FS_PF], qb[FS_PF];
-    double qe[FS_PF];
-#pragma unroll
-    for (int u = 0; u < FS_PF; ++u) {
-        ldx(r_lo + 1 + u, q[u], qe[u]);
-        ldb(r_lo + u, qb[u]);
-    }
-    double l0 = shfl_up1(x0.y);
-    double rm = shfl_down1(xm.x);
-    double r0 = shfl_down1(x0.x);
-    if (lane == 0) l0 = ex0;
-    if (lane == 31) { rm = exm; r0 = ex0; }
-
-    for (int r = r_lo; r < r_hi; r += FS_PF) {
-#pragma unroll
-        for (int u = 0; u < FS_PF; ++u) {
-            const int rr = r + u;
-            const double2 xp = q[u];
-            const double exp_ = qe[u];
-            const double2 bb = qb[u];
-            ldx(rr + 1 + FS_PF, q[u], qe[u]);
-            ldb(rr + FS_PF, qb[u]);
-            double lp = shfl_up1(xp.y);
-            double rp = shfl_down1(xp.x);
-            if (lane == 0) lp = exp_;
-            if (lane == 31) rp = exp_;
-            if (rr < r_hi) {
-                const int last = n - 1 - rr; // last interior column of this row
-                const bool v0 = c >= 1 && c <= last;
-                const bool v1 = c + 1 <= last;
-                // reference term order: W NW S C N SE E, accumulation from 0
-                double a0 = 0.0;
-                a0 += cW * l0;
-                a0 += cNW * lp;
-                a0 += cS * xm.x;
-                a0 += cC * x0.x;
-                a0 += cN * xp.x;
-                a0 += cSE * xm.y;
-                a0 += cE * x0.y;
-                double a1 = 0.0;
-                a1 += cW * x0.x;
-                a1 += cNW * xp.x;
-                a1 += cS * xm.y;
-                a1 += cC * x0.y;
-                a1 += cN * xp.y;
-                a1 += cSE * rm;
-                a1 += cE * r0;
-                double o0 = a0, o1 = a1;
-                if (MODE == ST_RESIDUAL) {
-                    o0 = bb.x - a0;
-                    o1 = bb.y - a1;
-                } else if (MODE == ST_JACOBI) {
-                    o0 = x0.x + omega * (bb.x - a0) / dg;
-                    o1 = x0.y + omega * (bb.y - a1) / dg;
-                }
-                double* yrow = yf + ro[rr];
-                if (v0 && v1) {
-                    *reinterpret_cast<double2*>(yrow + c) = make_double2(o0, o1);
-                } else {
-                    if (v0) yrow[c] = o0;
-                    if (v1) yrow[c + 1] = o1;
-                }
-            }
-            xm = x0;
-            rm = r0;
-            x0 = xp;
-            l0 = lp;
-            r0 = rp;
-        }
-    }
-}
+#include "face_stencil.cuh"
 
 // ---------------------------------------------------------------------------
 // K2/K3: edge line rows and vertex rows, one launch. Flags are per primitive
@@ -612,12 +477,11 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
                     double omega, uint8_t mask, cudaStream_t st, int parts) {
     // faces: interior DoFs are INNER; only present for n >= 3
     if ((parts & 1) && (mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
-        const dim3 grid(unsigned((t.n - 1 + FS_WARPS * FS_COLS - 1) / (FS_WARPS * FS_COLS)),
-                        unsigned((t.n - 1 + FS_RB - 1) / FS_RB), unsigned(t.nfaces));
+        const dim3 grid = face_stencil_grid(t);
         switch (mode) {
-        case ST_APPLY: k_face_stencil<ST_APPLY><<<grid, FS_WARPS * 32, 0, st>>>(t, x, b, y, omega); break;
-        case ST_RESIDUAL: k_face_stencil<ST_RESIDUAL><<<grid, FS_WARPS * 32, 0, st>>>(t, x, b, y, omega); break;
-        default: k_face_stencil<ST_JACOBI><<<grid, FS_WARPS * 32, 0, st>>>(t, x, b, y, omega); break;
+        case ST_APPLY: k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega); break;
+        case ST_RESIDUAL: k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega); break;
+        default: k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega); break;
         }
         check_launch("face stencil");
     }
