@@ -78,6 +78,23 @@ int hyb_partition(const char* mesh_text, int ranks, int partitioner, int weight_
 int hyb_stencil_host(const char* mesh_text, int form, int level, uint64_t primitive_id, double* out, int cap,
                      int* len);
 
+/* ---- host-only plans (no device) ------------------------------------------
+ * The arena layout and one-round ghost-exchange plan one process derives for
+ * `level` (the device runtime uses exactly these), for multi-process checks on
+ * CPUs. sizes[0..7] = arena slots, owned DoFs here, local gathers, all gathers,
+ * packed sends, #co-resident blocks, #send blocks, #receive blocks.
+ * which: 0 arena slot of each local owned DoF (packed order), 1 its global
+ * index, 2 gather destinations, 3 gather sources (first nlocal), 4 packed
+ * sources, 5 owner global index of each gather destination, 6/7/8 co-resident
+ * / send / receive blocks as 5 int64 (src rank, dst rank, send off, recv off,
+ * count). */
+typedef struct hyb_plan hyb_plan;
+int hyb_plan_create(const char* mesh_text, int world_ranks, const int32_t* assignment, const int32_t* local_ranks,
+                    int n_local, int level, hyb_plan** out);
+int hyb_plan_destroy(hyb_plan* p);
+int hyb_plan_sizes(hyb_plan* p, int64_t sizes[8]);
+int hyb_plan_array(hyb_plan* p, int which, int64_t* out, int64_t cap, int64_t* len);
+
 /* ---- domain ---------------------------------------------------------------
  * Replaces DistributedDomain(setup, assignment, ranks) + Controller
  * (include/hytegrid/primitives.hpp:61-100, communication.hpp:40-56).

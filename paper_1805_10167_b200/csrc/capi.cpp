@@ -19,6 +19,13 @@ struct hyb_operator {
 struct hyb_hierarchy {
     std::unique_ptr<hyb::Hierarchy> h;
 };
+struct hyb_plan {
+    hyb::MacroGraph g;
+    hyb::Placement p;
+    hyb::HostLayout lay;
+    hyb::HostExchange x;
+    int level = 0;
+};
 
 namespace {
 
@@ -173,6 +180,69 @@ int hyb_stencil_host(const char* mesh_text, int form, int level, uint64_t id, do
         if (len) *len = int(v.size());
         if (cap < int(v.size())) throw hyb::InvalidArgument("hyb_stencil_host: buffer too small");
         for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+    });
+}
+
+int hyb_plan_create(const char* mesh_text, int world_ranks, const int32_t* assignment, const int32_t* local_ranks,
+                    int n_local, int level, hyb_plan** out) {
+    return guarded([&] {
+        need(mesh_text, "hyb_plan_create");
+        auto h = std::make_unique<hyb_plan>();
+        h->g = hyb::build_macro_graph(hyb::parse_mesh_text(mesh_text));
+        std::vector<int> a(h->g.size(), 0), lr;
+        if (assignment)
+            for (size_t i = 0; i < a.size(); ++i) a[i] = assignment[i];
+        for (int i = 0; i < n_local; ++i) lr.push_back(local_ranks[i]);
+        if (lr.empty()) throw hyb::InvalidArgument("hyb_plan_create: no local ranks");
+        for (int r : a)
+            if (r < 0 || r >= world_ranks) throw hyb::InvalidArgument("hyb_plan_create: rank out of range");
+        if (level < 0 || level > 20) throw hyb::OutOfRange("hyb_plan_create: level");
+        h->level = level;
+        h->p = hyb::place(h->g, a, lr);
+        h->lay = hyb::plan_layout(h->g, h->p, level);
+        h->x = hyb::plan_exchange(h->g, a, lr, h->p, h->lay);
+        *out = h.release();
+    });
+}
+
+int hyb_plan_destroy(hyb_plan* p) {
+    return guarded([&] { delete p; });
+}
+
+int hyb_plan_sizes(hyb_plan* p, int64_t sizes[8]) {
+    return guarded([&] {
+        need(p, "hyb_plan_sizes");
+        const int64_t v[8] = {p->lay.arena_size, p->lay.owned_local, p->x.nlocal, int64_t(p->x.dst.size()),
+                              int64_t(p->x.pack.size()), int64_t(p->x.inproc.size()), int64_t(p->x.sends.size()),
+                              int64_t(p->x.recvs.size())};
+        for (int i = 0; i < 8; ++i) sizes[i] = v[i];
+    });
+}
+
+int hyb_plan_array(hyb_plan* p, int which, int64_t* out, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        need(p, "hyb_plan_array");
+        std::vector<int64_t> v;
+        auto blocks = [&](const std::vector<hyb::ExBlock>& bs) {
+            for (const auto& b : bs) v.insert(v.end(), {b.src_rank, b.dst_rank, b.send_off, b.recv_off, b.count});
+        };
+        switch (which) {
+        case 0: v = hyb::owned_positions(p->g, p->p, p->lay); break;
+        case 1: v = hyb::owned_global_index(p->g, p->p, p->level); break;
+        case 2: v = p->x.dst; break;
+        case 3: v = p->x.src; break;
+        case 4: v = p->x.pack; break;
+        case 5: v = p->x.owner_gidx; break;
+        case 6: blocks(p->x.inproc); break;
+        case 7: blocks(p->x.sends); break;
+        case 8: blocks(p->x.recvs); break;
+        default: throw hyb::InvalidArgument("hyb_plan_array: unknown array");
+        }
+        if (len) *len = int64_t(v.size());
+        if (out) {
+            if (cap < int64_t(v.size())) throw hyb::InvalidArgument("hyb_plan_array: buffer too small");
+            std::copy(v.begin(), v.end(), out);
+        }
     });
 }
 

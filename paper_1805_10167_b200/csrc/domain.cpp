@@ -42,6 +42,9 @@ template <class T> DevMem upload_vec(const std::vector<T>& v, cudaStream_t st) {
 }
 template DevMem upload_vec(const std::vector<double>&, cudaStream_t);
 template DevMem upload_vec(const std::vector<int64_t>&, cudaStream_t);
+template DevMem upload_vec(const std::vector<uint64_t>&, cudaStream_t);
+template DevMem upload_vec(const std::vector<int32_t>&, cudaStream_t);
+template DevMem upload_vec(const std::vector<int8_t>&, cudaStream_t);
 
 // ---------------------------------------------------------------- NCCL (dlopen)
 namespace {
@@ -108,15 +111,7 @@ Domain::Domain(const std::string& mesh_text, int world_ranks, const std::vector<
     rank_of_ = assignment;
     HYB_CUDA(cudaSetDevice(device_));
     HYB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    lidx_.assign(g_.size(), -1);
-    for (uint64_t id = 0; id < g_.size(); ++id) {
-        if (!is_local_rank(rank_of_[id])) continue;
-        switch (g_.kind_of(id)) {
-        case VERTEX: lidx_[id] = int(lverts_.size()); lverts_.push_back(id); break;
-        case EDGE: lidx_[id] = int(ledges_.size()); ledges_.push_back(id); break;
-        case FACE: lidx_[id] = int(lfaces_.size()); lfaces_.push_back(id); break;
-        }
-    }
+    place_ = place(g_, rank_of_, local_ranks_);
     scalars_ = DevMem(64 * sizeof(double));
 }
 
@@ -172,68 +167,30 @@ LevelGeom& Domain::level(int L) {
     if (it != levels_.end()) return *it->second;
     if (L < 0 || L > 20) throw OutOfRange("level " + std::to_string(L) + " unsupported");
     auto lg = std::make_unique<LevelGeom>();
+    const HostLayout lay = plan_layout(g_, place_, L);
     LevelTables& t = lg->t;
-    const int n = 1 << L, W = n + 1;
     t.level = L;
-    t.n = n;
-    t.W = W;
-    t.nfaces = int(lfaces_.size());
-    t.nedges = int(ledges_.size());
-    t.nverts = int(lverts_.size());
-    // padded closed triangle: row r holds W-r values, rows start on 32 B
-    lg->h_rowoff.resize(size_t(W) + 1);
-    int64_t off = 0;
-    for (int r = 0; r <= W; ++r) {
-        lg->h_rowoff[size_t(r)] = off;
-        if (r < W) off += round_up(W - r, 4);
-    }
-    t.face_stride = round_up(off, 32);
-    t.faces_size = t.face_stride * t.nfaces;
-    int64_t pos = t.faces_size;
-    std::vector<int8_t> enf;
-    for (uint64_t id : ledges_) {
-        const MacroEdge& e = g_.edges[g_.edge_index(id)];
-        lg->h_edge_off.push_back(pos);
-        enf.push_back(int8_t(e.faces.size()));
-        pos += round_up((n + 1) + int64_t(e.faces.size()) * n, 4);
-    }
-    pos = round_up(pos, 32);
-    std::vector<int32_t> vne;
-    std::vector<int64_t> vco; // vertex coefficients: own + one per edge + diag
-    int64_t cpos = 0;
-    for (uint64_t id : lverts_) {
-        const MacroVertex& v = g_.vertices[id];
-        lg->h_vtx_off.push_back(pos);
-        vne.push_back(int32_t(v.edges.size()));
-        vco.push_back(cpos);
-        pos += 1 + int64_t(v.edges.size());
-        cpos += 2 + int64_t(v.edges.size());
-    }
-    t.arena_size = round_up(std::max<int64_t>(pos, 32), 32);
-    t.owned_local = int64_t(t.nverts) + int64_t(t.nedges) * (n - 1) + int64_t(t.nfaces) * ((n - 1) * (n - 2) / 2);
-
-    lg->rowoff = upload_vec(lg->h_rowoff, stream_);
-    lg->edge_off = upload_vec(lg->h_edge_off, stream_);
-    {
-        DevMem m(std::max<size_t>(enf.size(), 1));
-        if (!enf.empty()) HYB_CUDA(cudaMemcpy(m.as<void>(), enf.data(), enf.size(), cudaMemcpyHostToDevice));
-        lg->edge_nf = std::move(m);
-    }
-    lg->vtx_off = upload_vec(lg->h_vtx_off, stream_);
-    lg->vtx_coef_off = upload_vec(vco, stream_);
-    {
-        DevMem m(std::max<size_t>(vne.size(), 1) * 4);
-        if (!vne.empty()) HYB_CUDA(cudaMemcpy(m.as<void>(), vne.data(), vne.size() * 4, cudaMemcpyHostToDevice));
-        lg->vtx_ne = std::move(m);
-    }
-    auto up_ids = [&](const std::vector<uint64_t>& v) {
-        DevMem m(std::max<size_t>(v.size(), 1) * 8);
-        if (!v.empty()) HYB_CUDA(cudaMemcpy(m.as<void>(), v.data(), v.size() * 8, cudaMemcpyHostToDevice));
-        return m;
-    };
-    lg->face_gid = up_ids(lfaces_);
-    lg->edge_gid = up_ids(ledges_);
-    lg->vtx_gid = up_ids(lverts_);
+    t.n = lay.n;
+    t.W = lay.W;
+    t.nfaces = int(place_.faces.size());
+    t.nedges = int(place_.edges.size());
+    t.nverts = int(place_.verts.size());
+    t.face_stride = lay.face_stride;
+    t.faces_size = lay.faces_size;
+    t.arena_size = lay.arena_size;
+    t.owned_local = lay.owned_local;
+    lg->h_rowoff = lay.rowoff;
+    lg->h_edge_off = lay.edge_off;
+    lg->h_vtx_off = lay.vtx_off;
+    lg->rowoff = upload_vec(lay.rowoff, stream_);
+    lg->edge_off = upload_vec(lay.edge_off, stream_);
+    lg->edge_nf = upload_vec(lay.edge_nf, stream_);
+    lg->vtx_off = upload_vec(lay.vtx_off, stream_);
+    lg->vtx_coef_off = upload_vec(lay.vtx_coef_off, stream_);
+    lg->vtx_ne = upload_vec(lay.vtx_ne, stream_);
+    lg->face_gid = upload_vec(place_.faces, stream_);
+    lg->edge_gid = upload_vec(place_.edges, stream_);
+    lg->vtx_gid = upload_vec(place_.verts, stream_);
     t.rowoff = lg->rowoff.as<int64_t>();
     t.edge_off = lg->edge_off.as<int64_t>();
     t.edge_nf = lg->edge_nf.as<int8_t>();
@@ -243,167 +200,22 @@ LevelGeom& Domain::level(int L) {
     t.face_gid = lg->face_gid.as<uint64_t>();
     t.edge_gid = lg->edge_gid.as<uint64_t>();
     t.vtx_gid = lg->vtx_gid.as<uint64_t>();
-    build_exchange(*lg, L);
+    build_exchange(*lg, lay);
     auto& ref = *lg;
     levels_[L] = std::move(lg);
     return ref;
 }
 
-// Ghost-exchange plan for one level (reference src/communication.cpp:54-403).
-// Pairs (sender, receiver) are enumerated in receiver-ID, then sender order;
-// every process derives the same order from the global graph, so a packed
-// block between two ranks needs no tags.
-void Domain::build_exchange(LevelGeom& lg, int L) {
-    const int n = 1 << L;
-    const LevelTables& t = lg.t;
-    struct Piece {
-        int64_t base;
-        uint16_t mode;
-    };
-    struct Pair {
-        uint64_t snd, rcv;
-        Piece src, dst;
-        int count;
-    };
-    auto face_piece = [&](uint64_t fid, int slot, bool off1, bool rev) {
-        const int fi = lidx_[fid];
-        uint16_t m = uint16_t(SEG_FACE | (slot << SEG_SLOT_SHIFT));
-        if (off1) m |= SEG_OFF1;
-        if (rev) m |= SEG_REV;
-        return Piece{fi >= 0 ? int64_t(fi) * t.face_stride : -1, m};
-    };
-    auto edge_at = [&](uint64_t eid, int64_t k) {
-        const int ei = lidx_[eid];
-        return Piece{ei >= 0 ? lg.h_edge_off[size_t(ei)] + k : -1, 0};
-    };
-    auto vtx_at = [&](uint64_t vid, int64_t k) {
-        const int vi = lidx_[vid];
-        return Piece{vi >= 0 ? lg.h_vtx_off[size_t(vi)] + k : -1, 0};
-    };
-
-    for (int d = 0; d < 4; ++d) {
-        std::vector<Pair> pairs;
-        switch (d) {
-        case V2E:
-            for (size_t ei = 0; ei < g_.ne(); ++ei) {
-                const uint64_t eid = g_.edge_id(ei);
-                const MacroEdge& e = g_.edges[ei];
-                for (int end = 0; end < 2; ++end)
-                    pairs.push_back({e.v[size_t(end)], eid, vtx_at(e.v[size_t(end)], 0), edge_at(eid, end ? n : 0), 1});
-            }
-            break;
-        case E2F:
-            for (size_t fi = 0; fi < g_.nf(); ++fi) {
-                const uint64_t fid = g_.face_id(fi);
-                const MacroFace& f = g_.faces[fi];
-                for (int s = 0; s < 3; ++s)
-                    pairs.push_back({f.e[size_t(s)], fid, edge_at(f.e[size_t(s)], 0),
-                                     face_piece(fid, s, false, !f.aligned[size_t(s)]), n + 1});
-            }
-            break;
-        case F2E:
-            for (size_t ei = 0; ei < g_.ne(); ++ei) {
-                const uint64_t eid = g_.edge_id(ei);
-                const MacroEdge& e = g_.edges[ei];
-                for (size_t j = 0; j < e.faces.size(); ++j) {
-                    const FaceSide& fs = e.faces[j];
-                    pairs.push_back({fs.face, eid, face_piece(fs.face, fs.slot, true, !fs.aligned),
-                                     edge_at(eid, (n + 1) + int64_t(j) * n), n});
-                }
-            }
-            break;
-        case E2V:
-            for (size_t vi = 0; vi < g_.nv(); ++vi) {
-                const MacroVertex& v = g_.vertices[vi];
-                for (size_t j = 0; j < v.edges.size(); ++j) {
-                    const MacroEdge& e = g_.edges[g_.edge_index(v.edges[j])];
-                    const int end = e.v[0] == vi ? 0 : 1;
-                    pairs.push_back({v.edges[j], uint64_t(vi), edge_at(v.edges[j], end == 0 ? 1 : n - 1),
-                                     vtx_at(vi, 1 + int64_t(j)), 1});
-                }
-            }
-            break;
-        }
-        // block sizes between distinct ranks touching this process
-        std::map<std::pair<int, int>, int64_t> block;
-        for (const Pair& p : pairs) {
-            const int rs = rank_of_[p.snd], rq = rank_of_[p.rcv];
-            if (rs == rq || !(is_local_rank(rs) || is_local_rank(rq))) continue;
-            block[{rs, rq}] += p.count;
-        }
-        std::map<std::pair<int, int>, int64_t> send_off, recv_off;
-        int64_t so = 0, ro = 0;
-        for (const auto& [k, cnt] : block)
-            if (is_local_rank(k.first)) { send_off[k] = so; so += cnt; }
-        for (const auto& [k, cnt] : block)
-            if (is_local_rank(k.second)) { recv_off[k] = ro; ro += cnt; }
-        ExchangeDir& X = lg.dir[d];
-        for (const auto& [k, cnt] : block) {
-            const bool sl = is_local_rank(k.first), rl = is_local_rank(k.second);
-            ExchangeDir::Block b{k.first, k.second, sl ? send_off[k] : -1, rl ? recv_off[k] : -1, cnt};
-            if (sl && rl) X.inproc.push_back(b);
-            else if (sl) X.sends.push_back(b);
-            else X.recvs.push_back(b);
-        }
-        lg.send_size = std::max(lg.send_size, so);
-        lg.recv_size = std::max(lg.recv_size, ro);
-        std::vector<CopySeg> pack, local;
-        std::map<std::pair<int, int>, int64_t> cursor;
-        for (const Pair& p : pairs) {
-            const int rs = rank_of_[p.snd], rq = rank_of_[p.rcv];
-            const bool sl = is_local_rank(rs), rl = is_local_rank(rq);
-            if (rs == rq) {
-                if (sl) local.push_back({p.src.base, p.dst.base, p.count, p.src.mode, p.dst.mode});
-                continue;
-            }
-            if (!(sl || rl)) continue;
-            const int64_t pos = cursor[{rs, rq}];
-            cursor[{rs, rq}] += p.count;
-            if (sl) pack.push_back({p.src.base, send_off[{rs, rq}] + pos, p.count, p.src.mode, uint16_t(1)});
-            if (rl) local.push_back({recv_off[{rs, rq}] + pos, p.dst.base, p.count, uint16_t(2), p.dst.mode});
-        }
-        X.npack = int(pack.size());
-        X.nlocal = int(local.size());
-        auto up_segs = [&](const std::vector<CopySeg>& v) {
-            DevMem m(std::max<size_t>(v.size(), 1) * sizeof(CopySeg));
-            if (!v.empty())
-                HYB_CUDA(cudaMemcpy(m.as<void>(), v.data(), v.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
-            return m;
-        };
-        X.pack = up_segs(pack);
-        X.local = up_segs(local);
-    }
-    if (int64_t(sendbuf_.bytes() / 8) < lg.send_size) sendbuf_ = DevMem(size_t(lg.send_size) * 8);
-    if (int64_t(recvbuf_.bytes() / 8) < lg.recv_size) recvbuf_ = DevMem(size_t(lg.recv_size) * 8);
-}
-
-void Domain::sync(Function& f, int level_) {
-    f.check_level(level_, "sync");
-    LevelGeom& lg = level(level_);
-    double* arena = f.data(level_);
-    double* sb = sendbuf_.as<double>();
-    double* rb = recvbuf_.as<double>();
-    for (int d = 0; d < 4; ++d) {
-        ExchangeDir& X = lg.dir[d];
-        launch_copy_segments(X.pack.as<CopySeg>(), X.npack, lg.t, arena, sb, rb, stream_);
-        for (const auto& b : X.inproc)
-            HYB_CUDA(cudaMemcpyAsync(rb + b.recv_off, sb + b.send_off, size_t(b.count) * 8, cudaMemcpyDeviceToDevice,
-                                     stream_));
-        if (!X.sends.empty() || !X.recvs.empty()) {
-            if (!nccl_comm_) throw LogicError("sync: remote ranks present but NCCL is not connected");
-            auto& api = nccl();
-            auto comm = static_cast<ncclComm_t>(nccl_comm_);
-            nccl_check(api.GroupStart(), "ncclGroupStart");
-            for (const auto& b : X.sends)
-                nccl_check(api.Send(sb + b.send_off, size_t(b.count), ncclFloat64, b.dst_rank, comm, stream_),
-                           "ncclSend");
-            for (const auto& b : X.recvs)
-                nccl_check(api.Recv(rb + b.recv_off, size_t(b.count), ncclFloat64, b.src_rank, comm, stream_),
-                           "ncclRecv");
-            nccl_check(api.GroupEnd(), "ncclGroupEnd");
-        }
-        launch_copy_segments(X.local.as<CopySeg>(), X.nlocal, lg.t, arena, sb, rb, stream_);
-    }
+void nccl_group_exchange(void* comm_, cudaStream_t st, double* sb, double* rb, const std::vector<ExBlock>& sends,
+                         const std::vector<ExBlock>& recvs) {
+    auto& api = nccl();
+    auto comm = static_cast<ncclComm_t>(comm_);
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (const auto& b : sends)
+        nccl_check(api.Send(sb + b.send_off, size_t(b.count), ncclFloat64, b.dst_rank, comm, st), "ncclSend");
+    for (const auto& b : recvs)
+        nccl_check(api.Recv(rb + b.recv_off, size_t(b.count), ncclFloat64, b.src_rank, comm, st), "ncclRecv");
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
 }
 
 DevMem& Domain::jacobi_scratch(int L) {

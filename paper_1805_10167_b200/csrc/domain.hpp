@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "kernels.hpp"
+#include "plan.hpp"
 #include "setup.hpp"
 
 namespace hyb {
@@ -54,29 +55,24 @@ class DevMem {
 
 template <class T> DevMem upload_vec(const std::vector<T>& v, cudaStream_t st);
 
-enum Direction : int { V2E = 0, E2F = 1, F2E = 2, E2V = 3 };
-
-struct ExchangeDir {
-    DevMem pack;   // arena -> send staging (remote and co-resident-rank pairs)
-    int npack = 0;
-    DevMem local;  // receive staging -> arena, plus same-rank arena -> arena copies
-    int nlocal = 0;
-    struct Block {
-        int src_rank, dst_rank;
-        int64_t send_off, recv_off, count;
-    };
-    std::vector<Block> inproc;  // co-resident ranks: send block -> recv block
-    std::vector<Block> sends;   // to a remote process
-    std::vector<Block> recvs;   // from a remote process
+/// One-round ghost refresh plan of a level (see Domain::build_exchange).
+struct Exchange {
+    DevMem dst, src;  // ghost slot <- owner slot (same rank), then ghost slot <- receive staging
+    DevMem pack;      // owner slots packed for other ranks, in block order
+    int64_t nlocal = 0, ntotal = 0, npack = 0;
+    std::vector<ExBlock> inproc;  // co-resident ranks: send block -> recv block (device copy)
+    std::vector<ExBlock> sends;   // to a remote process (NCCL)
+    std::vector<ExBlock> recvs;   // from a remote process (NCCL)
 };
 
 struct LevelGeom {
     LevelTables t; // geometry part (coefficient pointers left null)
     DevMem rowoff, edge_off, edge_nf, vtx_off, vtx_ne, vtx_coef_off, face_gid, edge_gid, vtx_gid;
     std::vector<int64_t> h_rowoff, h_edge_off, h_vtx_off;
-    ExchangeDir dir[4];
+    Exchange xch;
     int64_t send_size = 0, recv_size = 0;
 };
+
 
 class Domain;
 
@@ -150,10 +146,10 @@ class Domain {
     int device() const { return device_; }
 
     // local primitives (global IDs, ID order) and reverse maps (-1 = not local)
-    const std::vector<uint64_t>& local_faces() const { return lfaces_; }
-    const std::vector<uint64_t>& local_edges() const { return ledges_; }
-    const std::vector<uint64_t>& local_verts() const { return lverts_; }
-    int local_index(uint64_t gid) const { return lidx_[size_t(gid)]; }
+    const std::vector<uint64_t>& local_faces() const { return place_.faces; }
+    const std::vector<uint64_t>& local_edges() const { return place_.edges; }
+    const std::vector<uint64_t>& local_verts() const { return place_.verts; }
+    int local_index(uint64_t gid) const { return place_.lidx[size_t(gid)]; }
 
     LevelGeom& level(int L);
     int64_t owned_total(int L) const;  // all primitives of the graph
@@ -189,9 +185,11 @@ class Domain {
     void event_record(int slot);
     float event_elapsed(int a, int b);
 
+    const Placement& placement() const { return place_; }
+
   private:
     cudaEvent_t events_[16] = {};
-    void build_exchange(LevelGeom& lg, int L);
+    void build_exchange(LevelGeom& lg, const HostLayout& lay);
 
     MacroGraph g_;
     int world_;
@@ -199,8 +197,7 @@ class Domain {
     std::vector<int> local_ranks_;
     int device_;
     cudaStream_t stream_ = nullptr;
-    std::vector<uint64_t> lfaces_, ledges_, lverts_;
-    std::vector<int> lidx_;
+    Placement place_;
     std::map<int, std::unique_ptr<LevelGeom>> levels_;
     std::map<int, DevMem> jacobi_;
     DevMem staging_, partials_, scalars_, sendbuf_, recvbuf_;

@@ -98,33 +98,30 @@ __global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl
 }
 
 // ---------------------------------------------------------------------------
-// K11: ghost copies, one warp per walk segment.
+// K11: ghost refresh. Every ghost slot (face border rows, edge line ends and
+// halo row 1, vertex edge ghosts) is resolved at plan time to the storage of
+// the DoF's owner, so the reference's four relay directions
+// (src/communication.cpp:54-62) collapse into one gather: the state after
+// it is the reference's post-sync_all state, every copy equal to its owner.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int64_t seg_addr(int64_t base, uint16_t mode, int k, int count, int W,
-                                            const int64_t* __restrict__ ro) {
-    const int w = (mode & SEG_REV) ? count - 1 - k : k;
-    if (!(mode & SEG_FACE)) return base + w;
-    const int off = (mode & SEG_OFF1) ? 1 : 0;
-    const int slot = (mode >> SEG_SLOT_SHIFT) & 3;
-    int c, r;
-    if (slot == 0) { c = w; r = off; }
-    else if (slot == 1) { c = off; r = w; }
-    else { c = W - 1 - off - w; r = w; }
-    return base + ro[r] + c;
+__global__ void __launch_bounds__(256) k_ghost_gather(const int64_t* __restrict__ dst,
+                                                      const int64_t* __restrict__ src, int64_t nlocal,
+                                                      int64_t ntotal, double* arena,
+                                                      const double* __restrict__ recv) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < ntotal;
+         i += int64_t(gridDim.x) * blockDim.x)
+        arena[dst[i]] = i < nlocal ? arena[src[i]] : recv[i - nlocal];
 }
 
-__global__ void __launch_bounds__(256) k_copy_segments(const CopySeg* __restrict__ segs, int nseg, LevelTables t,
-                                                       double* arena, double* sendbuf, double* recvbuf) {
-    const int s = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (s >= nseg) return;
-    const CopySeg g = segs[s];
-    double* bufs[3] = {arena, sendbuf, recvbuf};
-    const double* src = bufs[g.src_mode & SEG_BUF_MASK];
-    double* dst = bufs[g.dst_mode & SEG_BUF_MASK];
-    for (int k = lane; k < g.count; k += 32)
-        dst[seg_addr(g.dst, g.dst_mode, k, g.count, t.W, t.rowoff)] =
-            src[seg_addr(g.src, g.src_mode, k, g.count, t.W, t.rowoff)];
+__global__ void __launch_bounds__(256) k_ghost_pack(const int64_t* __restrict__ src, int64_t n,
+                                                    const double* __restrict__ arena, double* __restrict__ send) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        send[i] = arena[src[i]];
+}
+
+inline int grid_for(int64_t n, int per_block = 256, int cap = 148 * 16) {
+    const int64_t b = (n + per_block - 1) / per_block;
+    return int(b < cap ? (b > 0 ? b : 1) : cap);
 }
 
 // ---------------------------------------------------------------------------
@@ -497,11 +494,17 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
     }
 }
 
-void launch_copy_segments(const CopySeg* segs, int nseg, const LevelTables& t, double* arena, double* sendbuf,
-                          double* recvbuf, cudaStream_t st) {
-    if (nseg <= 0) return;
-    k_copy_segments<<<(nseg + 7) / 8, 256, 0, st>>>(segs, nseg, t, arena, sendbuf, recvbuf);
-    check_launch("copy segments");
+void launch_ghost_gather(const int64_t* dst, const int64_t* src, int64_t nlocal, int64_t ntotal, double* arena,
+                         const double* recv, cudaStream_t st) {
+    if (ntotal <= 0) return;
+    k_ghost_gather<<<grid_for(ntotal), 256, 0, st>>>(dst, src, nlocal, ntotal, arena, recv);
+    check_launch("ghost gather");
+}
+
+void launch_ghost_pack(const int64_t* src, int64_t n, const double* arena, double* send, cudaStream_t st) {
+    if (n <= 0) return;
+    k_ghost_pack<<<grid_for(n), 256, 0, st>>>(src, n, arena, send);
+    check_launch("ghost pack");
 }
 
 void launch_prolongate(const LevelTables& tc, const LevelTables& tf, const FlagTables& ff, const double* xc,

@@ -47,25 +47,6 @@ struct FlagTables {
     const uint8_t* vtx_flag = nullptr;
 };
 
-/// One contiguous ghost copy (a walk of `count` DoFs). Buffers: 0 arena,
-/// 1 send staging, 2 receive staging. Face walks address border rows:
-/// slot 0 (k, off), slot 1 (off, k), slot 2 (W-1-off-k, k); reversed walks
-/// run k -> count-1-k (reference src/indexing.cpp:61-83).
-struct CopySeg {
-    int64_t src;
-    int64_t dst;
-    int32_t count;
-    uint16_t src_mode;
-    uint16_t dst_mode;
-};
-enum : uint16_t {
-    SEG_BUF_MASK = 3,
-    SEG_FACE = 4,   // face walk addressing
-    SEG_SLOT_SHIFT = 3, // 2 bits
-    SEG_OFF1 = 32,  // row at distance 1 from the border
-    SEG_REV = 64,   // reversed walk
-};
-
 enum StencilMode : int { ST_APPLY = 0, ST_RESIDUAL = 1, ST_JACOBI = 2 };
 
 // ---- launchers (all asynchronous on `st`) ----
@@ -74,8 +55,12 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
                     double* y, double omega, uint8_t mask, cudaStream_t st, int parts = 3);
 /// number of kernels launched by this library so far (process-wide)
 int64_t kernel_launch_count();
-void launch_copy_segments(const CopySeg* segs, int nseg, const LevelTables& t, double* arena, double* sendbuf,
-                          double* recvbuf, cudaStream_t st);
+/// Ghost refresh, one pass: arena[dst[i]] = arena[src[i]] for i < nlocal
+/// (owner on this process), arena[dst[i]] = recv[i - nlocal] for the rest.
+void launch_ghost_gather(const int64_t* dst, const int64_t* src, int64_t nlocal, int64_t ntotal, double* arena,
+                         const double* recv, cudaStream_t st);
+/// send[i] = arena[src[i]] (owned values other processes hold ghosts of)
+void launch_ghost_pack(const int64_t* src, int64_t n, const double* arena, double* send, cudaStream_t st);
 void launch_prolongate(const LevelTables& coarse, const LevelTables& fine, const FlagTables& fine_flags,
                        const double* xc, double* xf, uint8_t mask, bool add, cudaStream_t st);
 void launch_restrict(const LevelTables& coarse, const LevelTables& fine, const FlagTables& coarse_flags,

@@ -115,6 +115,41 @@ def stencil_host(mesh_text: str, level: int, primitive_id: int, form: int = 0) -
     return out[: n.value].copy()
 
 
+class ExchangePlan:
+    """Host-only view of the layout and one-round ghost-exchange plan that a
+    process driving ``local_ranks`` builds for ``level`` (no device needed)."""
+
+    ARRAYS = {"owned_slots": 0, "owned_global": 1, "gather_dst": 2, "gather_src": 3, "pack_src": 4,
+              "owner_global": 5, "inproc": 6, "sends": 7, "recvs": 8}
+
+    def __init__(self, mesh_text: str, ranks: int, assignment, local_ranks, level: int):
+        a = np.ascontiguousarray(assignment, dtype=np.int32)
+        lr = (C.c_int32 * len(local_ranks))(*local_ranks)
+        h = C.c_void_p()
+        check(lib.hyb_plan_create(mesh_text.encode(), ranks, a.ctypes.data_as(C.POINTER(C.c_int32)), lr,
+                                  len(local_ranks), level, C.byref(h)))
+        self._h = h
+        s = (C.c_int64 * 8)()
+        check(lib.hyb_plan_sizes(h, s))
+        (self.arena_size, self.owned_local, self.nlocal, self.ntotal, self.npack, self.n_inproc, self.n_sends,
+         self.n_recvs) = list(s)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.hyb_plan_destroy(self._h)
+            self._h = None
+
+    def array(self, name: str) -> np.ndarray:
+        which = self.ARRAYS[name]
+        n = C.c_int64()
+        check(lib.hyb_plan_array(self._h, which, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.int64)
+        check(lib.hyb_plan_array(self._h, which, out.ctypes.data_as(C.POINTER(C.c_int64)), n.value, C.byref(n)))
+        if which >= 6:
+            out = out.reshape(-1, 5)
+        return out
+
+
 def _bc_arrays(bc: dict | None):
     bc = bc or {}
     markers = (C.c_int32 * max(len(bc), 1))(*[int(k) for k in bc])
