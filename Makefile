@@ -13,10 +13,10 @@ LIB      := $(PKG)/libhyteg_b200.so
 # in the reference's baseline x86-64 build (bitwise parity).
 NVFLAGS  := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC -Xptxas -v
 CXXFLAGS := -O2 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -I$(CUDA)/include
-LDFLAGS  := -shared -static-libstdc++ -static-libgcc -Wl,--exclude-libs,ALL -L$(CUDA)/lib64 -lcudart_static -ldl -lpthread -lrt
+LDFLAGS  := -shared -Wl,--no-undefined -static-libstdc++ -static-libgcc -Wl,--exclude-libs,ALL -L$(CUDA)/lib64 -lcudart_static -ldl -lpthread -lrt
 
 HDRS := $(wildcard $(CSRC)/*.hpp) $(wildcard $(CSRC)/*.cuh) include/hyteg_b200.h
-OBJS := $(BUILD)/kernels.o $(BUILD)/setup.o $(BUILD)/domain.o $(BUILD)/exchange.o $(BUILD)/plan.o $(BUILD)/ops.o $(BUILD)/capi.o
+OBJS := $(BUILD)/kernels.o $(BUILD)/setup.o $(BUILD)/domain.o $(BUILD)/exchange.o $(BUILD)/plan.o $(BUILD)/coarse.o $(BUILD)/ops.o $(BUILD)/capi.o
 
 .PHONY: all lib oracle clean
 all: lib oracle

@@ -45,6 +45,7 @@ template DevMem upload_vec(const std::vector<int64_t>&, cudaStream_t);
 template DevMem upload_vec(const std::vector<uint64_t>&, cudaStream_t);
 template DevMem upload_vec(const std::vector<int32_t>&, cudaStream_t);
 template DevMem upload_vec(const std::vector<int8_t>&, cudaStream_t);
+template DevMem upload_vec(const std::vector<uint8_t>&, cudaStream_t);
 
 // ---------------------------------------------------------------- NCCL (dlopen)
 namespace {

@@ -241,15 +241,23 @@ class Hierarchy {
     void cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post);
     void coarse_correct(Function& rhs, Function& x);
     void smooth(Function& rhs, Function& x, int level);
+    void check_coarse(); // throws if the last coarse solve did not converge
 
     Domain* dom_;
     Operator a_;
     Function r_, b_, e_;
-    Function cx_, cr_, cp_, cap_;
     int smoother_;
     double omega_;
     double coarse_tol_;
     int coarse_max_iter_;
+    // min-level system, replicated on every rank (see coarse.hpp)
+    struct Coarse {
+        int64_t n = 0, nloc = 0;
+        DevMem rowptr, col, val;  // constrained CSR
+        DevMem gidx, pos, flag;   // this process's owned min-level DoFs
+        DevMem vec;               // b, x, r, p, ap (n each)
+        DevMem status;            // CoarseStatus
+    } coarse_;
 };
 
 } // namespace hyb

@@ -135,27 +135,9 @@ inline dim3 face_row_grid(int n_cols, int n_rows, int nfaces) {
 }
 
 // ---------------------------------------------------------------------------
-// K8: prolongation (optionally fused with the add into the fine iterate).
+// K7/K8 face transfers: transfer.cuh
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_prolongate_faces(LevelTables tc, LevelTables tf, const double* __restrict__ xc,
-                                                          double* __restrict__ xf, int add) {
-    const int nf = tf.n;
-    const int col = 1 + blockIdx.x * 128 + threadIdx.x;
-    const double* cv = xc + int64_t(blockIdx.z) * tc.face_stride;
-    double* fv = xf + int64_t(blockIdx.z) * tf.face_stride;
-    const int r0 = 1 + blockIdx.y * FR_RB;
-    for (int row = r0; row < r0 + FR_RB && row <= nf - 2; ++row) {
-        if (col > nf - 1 - row) break;
-        const int64_t* cr = tc.rowoff;
-        double v;
-        if (col % 2 == 0 && row % 2 == 0) v = cv[cr[row / 2] + col / 2];
-        else if (row % 2 == 0) v = 0.5 * (cv[cr[row / 2] + (col - 1) / 2] + cv[cr[row / 2] + (col + 1) / 2]);
-        else if (col % 2 == 0) v = 0.5 * (cv[cr[(row - 1) / 2] + col / 2] + cv[cr[(row + 1) / 2] + col / 2]);
-        else v = 0.5 * (cv[cr[(row - 1) / 2] + (col + 1) / 2] + cv[cr[(row + 1) / 2] + (col - 1) / 2]);
-        double* p = fv + tf.rowoff[row] + col;
-        *p = add ? *p + v : v;
-    }
-}
+#include "transfer.cuh"
 
 __global__ void __launch_bounds__(128) k_prolongate_ev(LevelTables tc, LevelTables tf, FlagTables ff,
                                                        const double* __restrict__ xc, double* __restrict__ xf,
@@ -182,25 +164,6 @@ __global__ void __launch_bounds__(128) k_prolongate_ev(LevelTables tc, LevelTabl
 // ---------------------------------------------------------------------------
 // K7: restriction (exact transpose of the prolongation).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_restrict_faces(LevelTables tc, LevelTables tf, const double* __restrict__ xf,
-                                                        double* __restrict__ xc) {
-    const int nc = tc.n;
-    const int col = 1 + blockIdx.x * 128 + threadIdx.x;
-    const double* fv = xf + int64_t(blockIdx.z) * tf.face_stride;
-    double* cv = xc + int64_t(blockIdx.z) * tc.face_stride;
-    const int r0 = 1 + blockIdx.y * FR_RB;
-    const int64_t* fr_ = tf.rowoff;
-    for (int row = r0; row < r0 + FR_RB && row <= nc - 2; ++row) {
-        if (col > nc - 1 - row) break;
-        const int fc = 2 * col, fr = 2 * row;
-        const double* rm = fv + fr_[fr - 1];
-        const double* r0p = fv + fr_[fr];
-        const double* rp = fv + fr_[fr + 1];
-        cv[tc.rowoff[row] + col] =
-            r0p[fc] + 0.5 * (r0p[fc - 1] + r0p[fc + 1] + rm[fc] + rp[fc] + rm[fc + 1] + rp[fc - 1]);
-    }
-}
-
 __global__ void __launch_bounds__(128) k_restrict_ev(LevelTables tc, LevelTables tf, FlagTables cf,
                                                      const double* __restrict__ xf, double* __restrict__ xc,
                                                      uint8_t mask, int kblocks) {
@@ -510,7 +473,7 @@ void launch_ghost_pack(const int64_t* src, int64_t n, const double* arena, doubl
 void launch_prolongate(const LevelTables& tc, const LevelTables& tf, const FlagTables& ff, const double* xc,
                        double* xf, uint8_t mask, bool add, cudaStream_t st) {
     if ((mask & F_INNER) && tf.nfaces > 0 && tf.n >= 3) {
-        k_prolongate_faces<<<face_row_grid(tf.n - 2, tf.n - 2, tf.nfaces), 128, 0, st>>>(tc, tf, xc, xf, add);
+        k_prolongate_faces<<<transfer_grid(tc.n, tf.nfaces), TR_WARPS * 32, 0, st>>>(tc, tf, xc, xf, add);
         check_launch("prolongate faces");
     }
     const int kb = kblocks_for(tf.n);
@@ -524,7 +487,7 @@ void launch_prolongate(const LevelTables& tc, const LevelTables& tf, const FlagT
 void launch_restrict(const LevelTables& tc, const LevelTables& tf, const FlagTables& cf, const double* xf, double* xc,
                      uint8_t mask, cudaStream_t st) {
     if ((mask & F_INNER) && tc.nfaces > 0 && tc.n >= 3) {
-        k_restrict_faces<<<face_row_grid(tc.n - 2, tc.n - 2, tc.nfaces), 128, 0, st>>>(tc, tf, xf, xc);
+        k_restrict_faces<<<transfer_grid(tc.n, tc.nfaces), TR_WARPS * 32, 0, st>>>(tc, tf, xf, xc);
         check_launch("restrict faces");
     }
     const int kb = kblocks_for(tc.n);
@@ -616,6 +579,132 @@ void launch_combine_tree(int op, double* v, int64_t len, double* out, cudaStream
     if (op == 0) k_combine_tree<0><<<1, 1024, 0, st>>>(v, len, out);
     else k_combine_tree<1><<<1, 1024, 0, st>>>(v, len, out);
     check_launch("combine tree");
+}
+
+} // namespace hyb
+
+// ===========================================================================
+// coarse-grid solve
+// ===========================================================================
+namespace hyb {
+namespace {
+
+__global__ void k_coarse_gather(int64_t nloc, const int64_t* __restrict__ gidx, const int64_t* __restrict__ pos,
+                                const double* __restrict__ arena, double* __restrict__ glob) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nloc; i += int64_t(gridDim.x) * blockDim.x)
+        glob[gidx[i]] = arena[pos[i]];
+}
+
+__global__ void k_coarse_scatter_add(int64_t nloc, const int64_t* __restrict__ gidx, const int64_t* __restrict__ pos,
+                                     const uint8_t* __restrict__ flag, uint8_t mask,
+                                     const double* __restrict__ glob, double* __restrict__ arena) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nloc; i += int64_t(gridDim.x) * blockDim.x)
+        if (flag[i] & mask) arena[pos[i]] += 1.0 * glob[gidx[i]];
+}
+
+constexpr int CG_THREADS = 1024;
+
+// fixed-shape block reduction: per-thread strided partial, warp tree, warp-0 tree
+__device__ double cg_dot(const double* __restrict__ u, const double* __restrict__ v, int64_t n, double* red) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) s += u[i] * v[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = s;
+    __syncthreads();
+    if (w == 0) {
+        double t = red[l];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+        if (l == 0) red[32] = t;
+    }
+    __syncthreads();
+    const double out = red[32];
+    __syncthreads();
+    return out;
+}
+
+__device__ void cg_spmv(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                        const double* __restrict__ val, const double* __restrict__ u, double* __restrict__ out,
+                        int64_t n) {
+    for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) {
+        double acc = 0.0; // row entries in column order (reference SparseMatrix::multiply)
+        for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) acc += val[k] * u[col[k]];
+        out[i] = acc;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(CG_THREADS) k_coarse_cg(int64_t n, const int32_t* __restrict__ rowptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ b, double* x, double* r,
+                                                          double* p, double* ap, double tol, int max_iter,
+                                                          CoarseStatus* st) {
+    __shared__ double red[33];
+    for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) {
+        x[i] = 0.0;
+        r[i] = b[i]; // b - A * 0
+        p[i] = b[i];
+    }
+    __syncthreads();
+    const double target = tol * sqrt(cg_dot(b, b, n, red));
+    double rs = cg_dot(r, r, n, red);
+    int it = 0, breakdown = 0;
+    while (it < max_iter && sqrt(rs) > target) {
+        cg_spmv(rowptr, col, val, p, ap, n);
+        const double pap = cg_dot(p, ap, n, red);
+        if (pap <= 0.0) {
+            breakdown = 1;
+            break;
+        }
+        const double alpha = rs / pap;
+        for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) {
+            x[i] += alpha * p[i];
+            r[i] -= alpha * ap[i];
+        }
+        __syncthreads();
+        const double rs_new = cg_dot(r, r, n, red);
+        const double beta = rs_new / rs;
+        for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) p[i] = r[i] + beta * p[i];
+        __syncthreads();
+        rs = rs_new;
+        ++it;
+    }
+    // true residual of the returned iterate (reference finish_report)
+    cg_spmv(rowptr, col, val, x, ap, n);
+    for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) ap[i] = b[i] - ap[i];
+    __syncthreads();
+    const double res = sqrt(cg_dot(ap, ap, n, red));
+    if (threadIdx.x == 0) {
+        st->iterations = it;
+        st->breakdown = breakdown;
+        st->converged = res <= target ? 1 : 0;
+        st->target = target;
+        st->residual = res;
+    }
+}
+
+} // namespace
+
+void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos, const double* arena, double* glob,
+                          cudaStream_t st) {
+    if (nloc <= 0) return;
+    k_coarse_gather<<<grid_for(nloc), 256, 0, st>>>(nloc, gidx, pos, arena, glob);
+    check_launch("coarse gather");
+}
+
+void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* b,
+                      double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
+                      cudaStream_t stream) {
+    k_coarse_cg<<<1, CG_THREADS, 0, stream>>>(n, rowptr, col, val, b, x, r, p, ap, tol, max_iter, st);
+    check_launch("coarse cg");
+}
+
+void launch_coarse_scatter_add(int64_t nloc, const int64_t* gidx, const int64_t* pos, const uint8_t* flag,
+                               uint8_t mask, const double* glob, double* arena, cudaStream_t st) {
+    if (nloc <= 0) return;
+    k_coarse_scatter_add<<<grid_for(nloc), 256, 0, st>>>(nloc, gidx, pos, flag, mask, glob, arena);
+    check_launch("coarse scatter");
 }
 
 } // namespace hyb

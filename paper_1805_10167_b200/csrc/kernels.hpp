@@ -82,4 +82,25 @@ void launch_partials(int op, const LevelTables& t, const double* x1, const doubl
 // fixed pairwise fold (op 0 sum, op 1 max) of v[0..len) -> out[0]; v is clobbered
 void launch_combine_tree(int op, double* v, int64_t len, double* out, cudaStream_t st);
 
+// ---- coarse-grid solve (device-resident, replicated per rank) ----
+struct CoarseStatus {
+    int iterations;
+    int converged;
+    int breakdown;
+    int pad;
+    double target;
+    double residual;
+};
+// glob[gidx[i]] = arena[pos[i]]   (glob zeroed by the caller)
+void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos, const double* arena, double* glob,
+                          cudaStream_t st);
+// CG on the assembled constrained CSR system, one CTA (reference cg_solve,
+// src/solvers.cpp:226-259): x := A^-1 b to tol * ||b||, status written to st
+void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* b,
+                      double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
+                      cudaStream_t stream);
+// arena[pos[i]] += glob[gidx[i]] where flag[i] & mask
+void launch_coarse_scatter_add(int64_t nloc, const int64_t* gidx, const int64_t* pos, const uint8_t* flag,
+                               uint8_t mask, const double* glob, double* arena, cudaStream_t st);
+
 } // namespace hyb

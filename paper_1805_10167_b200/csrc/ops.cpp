@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "coarse.hpp"
 #include "domain.hpp"
 
 namespace hyb {
@@ -295,14 +296,30 @@ void download(Function& f, int level, double* host, int64_t n, bool global_order
 Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc, int smoother, double omega,
                      double coarse_tol, int coarse_max_iter)
     : dom_(&d), a_(d, form, min_level, max_level, bc), r_(d, "mg.r", min_level, max_level, bc),
-      b_(d, "mg.b", min_level, max_level, bc), e_(d, "mg.e", min_level, max_level, bc),
-      cx_(d, "cg.x", min_level, min_level, bc), cr_(d, "cg.r", min_level, min_level, bc),
-      cp_(d, "cg.p", min_level, min_level, bc), cap_(d, "cg.ap", min_level, min_level, bc), smoother_(smoother),
+      b_(d, "mg.b", min_level, max_level, bc), e_(d, "mg.e", min_level, max_level, bc), smoother_(smoother),
       omega_(omega), coarse_tol_(coarse_tol), coarse_max_iter_(coarse_max_iter) {
     if (min_level < 0 || min_level > max_level)
         throw InvalidArgument("GridHierarchy: need 0 <= min_level <= max_level");
     if (smoother != SMOOTH_JACOBI) throw InvalidArgument("GridHierarchy: unknown smoother");
-    if (coarse_max_iter_ < 0) coarse_max_iter_ = int(d.owned_total(min_level)) + 100;
+    // min-level system: every rank holds the whole (small) constrained matrix
+    const HostCsr csr = assemble_constrained(d.graph(), form, min_level, bc);
+    if (coarse_max_iter_ < 0) coarse_max_iter_ = int(csr.n) + 100; // reference src/solvers.cpp:437
+    const HostLayout lay = plan_layout(d.graph(), d.placement(), min_level);
+    const std::vector<int64_t> gidx = owned_global_index(d.graph(), d.placement(), min_level);
+    const std::vector<int64_t> pos = owned_positions(d.graph(), d.placement(), lay);
+    std::vector<uint8_t> fl(gidx.size());
+    for (size_t i = 0; i < gidx.size(); ++i) fl[i] = csr.flag[size_t(gidx[i])];
+    coarse_.n = csr.n;
+    coarse_.nloc = int64_t(gidx.size());
+    coarse_.rowptr = upload_vec(csr.rowptr, d.stream());
+    coarse_.col = upload_vec(csr.col, d.stream());
+    coarse_.val = upload_vec(csr.val, d.stream());
+    coarse_.gidx = upload_vec(gidx, d.stream());
+    coarse_.pos = upload_vec(pos, d.stream());
+    coarse_.flag = upload_vec(fl, d.stream());
+    coarse_.vec = DevMem(size_t(5 * std::max<int64_t>(csr.n, 1)) * 8);
+    coarse_.status = DevMem(sizeof(CoarseStatus));
+    HYB_CUDA(cudaMemsetAsync(coarse_.status.as<void>(), 0, sizeof(CoarseStatus), d.stream()));
 }
 
 void Hierarchy::smooth(Function& rhs, Function& x, int level) { smooth_jacobi(a_, rhs, x, omega_, level); }
@@ -313,6 +330,7 @@ void Hierarchy::vcycle(Function& rhs, Function& x, int level, int nu_pre, int nu
                          ", " + std::to_string(a_.max_level()) + "]");
     if (nu_pre < 0 || nu_post < 0) throw InvalidArgument("vcycle: negative smoothing count");
     cycle(rhs, x, level, nu_pre, nu_post);
+    check_coarse();
 }
 
 // reference src/solvers.cpp:406-428 with the smoother of the configuration
@@ -333,34 +351,39 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
     for (int i = 0; i < nu_post; ++i) smooth(rhs, x, level);
 }
 
-// reference src/solvers.cpp:430-442 + cg_solve :226-259, matrix-free on device
+// reference src/solvers.cpp:430-442: residual, gather into the global coarse
+// vector (one allreduce across processes), CG on the assembled constrained
+// matrix (cg_solve :226-259) on the device, scatter-add on the smooth mask.
+// No host synchronisation: convergence is checked after the cycle.
 void Hierarchy::coarse_correct(Function& rhs, Function& x) {
     const int L = a_.min_level();
+    Domain& d = *dom_;
     residual(a_, rhs, x, r_, L);
-    fill_const(cx_, 0.0, L, ALL_FLAGS);
-    assign(1.0, r_, 0.0, r_, cr_, L, ALL_FLAGS);
-    assign(1.0, cr_, 0.0, cr_, cp_, L, ALL_FLAGS);
-    const double target = coarse_tol_ * std::sqrt(dot(r_, r_, L));
-    double rs = dot(cr_, cr_, L);
-    int it = 0;
-    while (it < coarse_max_iter_ && std::sqrt(rs) > target) {
-        apply(a_, cp_, cap_, L, ALL_FLAGS);
-        const double pap = dot(cp_, cap_, L);
-        if (pap <= 0.0) break; // non-positive curvature: breakdown
-        const double alpha = rs / pap;
-        add_scaled(cx_, alpha, cp_, L, ALL_FLAGS);
-        add_scaled(cr_, -alpha, cap_, L, ALL_FLAGS);
-        const double rs_new = dot(cr_, cr_, L);
-        const double beta = rs_new / rs;
-        assign(1.0, cr_, beta, cp_, cp_, L, ALL_FLAGS);
-        rs = rs_new;
-        ++it;
-    }
-    last_coarse_iterations = it;
-    residual(a_, r_, cx_, cap_, L); // true residual of the returned iterate
-    const double true_res = std::sqrt(dot(cap_, cap_, L));
-    if (!(true_res <= target)) throw RuntimeError("vcycle: coarse CG did not converge");
-    add_scaled(x, 1.0, cx_, L, kSmoothMask);
+    const int64_t n = coarse_.n;
+    double* b = coarse_.vec.as<double>();
+    double* cx = b + n;
+    HYB_CUDA(cudaMemsetAsync(b, 0, size_t(n) * 8, d.stream()));
+    launch_coarse_gather(coarse_.nloc, coarse_.gidx.as<int64_t>(), coarse_.pos.as<int64_t>(), r_.data(L), b,
+                         d.stream());
+    d.allreduce_sum(b, n); // one owner per entry: exact
+    d.timer_begin("coarse_cg");
+    launch_coarse_cg(n, coarse_.rowptr.as<int32_t>(), coarse_.col.as<int32_t>(), coarse_.val.as<double>(), b, cx,
+                     b + 2 * n, b + 3 * n, b + 4 * n, coarse_tol_, coarse_max_iter_,
+                     coarse_.status.as<CoarseStatus>(), d.stream());
+    d.timer_end();
+    launch_coarse_scatter_add(coarse_.nloc, coarse_.gidx.as<int64_t>(), coarse_.pos.as<int64_t>(),
+                              coarse_.flag.as<uint8_t>(), kSmoothMask, cx, x.data(L), d.stream());
+}
+
+void Hierarchy::check_coarse() {
+    CoarseStatus st{};
+    HYB_CUDA(cudaMemcpyAsync(&st, coarse_.status.as<void>(), sizeof st, cudaMemcpyDeviceToHost, dom_->stream()));
+    HYB_CUDA(cudaStreamSynchronize(dom_->stream()));
+    last_coarse_iterations = st.iterations;
+    if (!st.converged)
+        throw RuntimeError("vcycle: coarse CG did not converge (" + std::to_string(st.iterations) +
+                           " iterations, residual " + std::to_string(st.residual) + ", target " +
+                           std::to_string(st.target) + ")");
 }
 
 double Hierarchy::residual_norm(Function& rhs, Function& x, int level) {
@@ -379,6 +402,7 @@ std::vector<double> Hierarchy::solve(Function& rhs, Function& x, int level, doub
     int it = 0;
     while (it < max_cycles && res.back() > target) {
         cycle(rhs, x, level, nu_pre, nu_post);
+        check_coarse();
         ++it;
         res.push_back(residual_norm(rhs, x, level));
     }
