@@ -193,6 +193,9 @@ int hyb_hierarchy_create(hyb_domain* d, int form, int min_level, int max_level, 
                          int coarse_max_iter, hyb_hierarchy** out);
 int hyb_hierarchy_destroy(hyb_hierarchy* h);
 int hyb_hierarchy_vcycle(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, int nu_pre, int nu_post);
+/* CUDA-graph replay of V-cycles (default on; needs an even nu_pre + nu_post):
+ * enable < 0 leaves the setting unchanged; *replays = graph launches so far */
+int hyb_hierarchy_graphs(hyb_hierarchy* h, int enable, int64_t* replays);
 int hyb_hierarchy_residual_norm(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, double* out);
 /* residuals[0..*n_out): ||rhs - A x|| before each cycle and after the last */
 int hyb_hierarchy_solve(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, double tol, int max_cycles,

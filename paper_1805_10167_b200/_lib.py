@@ -116,6 +116,7 @@ _SIGS = {
     "hyb_hierarchy_create": (_i, [_p, _i, _i, _i, _pi32, _pu8, _i, _i, _d, _d, _i, C.POINTER(_p)]),
     "hyb_hierarchy_destroy": (_i, [_p]),
     "hyb_hierarchy_vcycle": (_i, [_p, _p, _p, _i, _i, _i]),
+    "hyb_hierarchy_graphs": (_i, [_p, _i, _pi64]),
     "hyb_hierarchy_residual_norm": (_i, [_p, _p, _p, _i, _pd]),
     "hyb_hierarchy_solve": (_i, [_p, _p, _p, _i, _d, _i, _i, _i, _pd, C.POINTER(_i), C.POINTER(_i)]),
     "hyb_host_alloc": (_i, [_i64, C.POINTER(_p)]),

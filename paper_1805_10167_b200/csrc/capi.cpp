@@ -642,6 +642,14 @@ int hyb_hierarchy_vcycle(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, i
     });
 }
 
+int hyb_hierarchy_graphs(hyb_hierarchy* h, int enable, int64_t* replays) {
+    return guarded([&] {
+        need(h, "hyb_hierarchy_graphs");
+        if (enable >= 0) h->h->use_graphs = enable != 0;
+        if (replays) *replays = h->h->graph_replays;
+    });
+}
+
 int hyb_hierarchy_residual_norm(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, double* out) {
     return guarded([&] {
         need(h, "hyb_hierarchy_residual_norm");

@@ -60,6 +60,7 @@ struct Exchange {
     DevMem dst, src;  // ghost slot <- owner slot (same rank), then ghost slot <- receive staging
     DevMem pack;      // owner slots packed for other ranks, in block order
     int64_t nlocal = 0, ntotal = 0, npack = 0;
+    bool idx32 = false; // dst/src stored as int32 (arena < 2^31 slots)
     std::vector<ExBlock> inproc;  // co-resident ranks: send block -> recv block (device copy)
     std::vector<ExBlock> sends;   // to a remote process (NCCL)
     std::vector<ExBlock> recvs;   // from a remote process (NCCL)
@@ -242,7 +243,28 @@ class Hierarchy {
     void coarse_correct(Function& rhs, Function& x);
     void smooth(Function& rhs, Function& x, int level);
     void check_coarse(); // throws if the last coarse solve did not converge
+    void run_cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post);
+    std::vector<const void*> graph_key(Function& rhs, Function& x, int level, int nu_pre, int nu_post);
 
+    // CUDA-graph replay of whole V-cycles: a cycle with an even number of
+    // Jacobi sweeps per level leaves every arena where it found it, so the
+    // captured kernel/NCCL sequence can be replayed while the pointers match.
+  public:
+    bool use_graphs = true;
+    int64_t graph_replays = 0;
+
+  private:
+    struct CycleGraph {
+        std::vector<const void*> key;
+        cudaGraphExec_t exec = nullptr;
+    };
+    std::vector<CycleGraph> graphs_;
+    std::vector<std::vector<const void*>> warm_;
+
+  public:
+    ~Hierarchy();
+
+  private:
     Domain* dom_;
     Operator a_;
     Function r_, b_, e_;

@@ -12,8 +12,14 @@ void Domain::build_exchange(LevelGeom& lg, const HostLayout& lay) {
     X.nlocal = h.nlocal;
     X.ntotal = int64_t(h.dst.size());
     X.npack = int64_t(h.pack.size());
-    X.dst = upload_vec(h.dst, stream_);
-    X.src = upload_vec(h.src, stream_);
+    X.idx32 = lay.arena_size < (int64_t(1) << 31);
+    if (X.idx32) { // halves the index traffic of every ghost refresh
+        X.dst = upload_vec(std::vector<int32_t>(h.dst.begin(), h.dst.end()), stream_);
+        X.src = upload_vec(std::vector<int32_t>(h.src.begin(), h.src.end()), stream_);
+    } else {
+        X.dst = upload_vec(h.dst, stream_);
+        X.src = upload_vec(h.src, stream_);
+    }
     X.pack = upload_vec(h.pack, stream_);
     X.inproc = std::move(h.inproc);
     X.sends = std::move(h.sends);
@@ -44,7 +50,7 @@ void Domain::sync(Function& f, int L) {
         if (!nccl_comm_) throw LogicError("sync: remote ranks present but NCCL is not connected");
         nccl_group_exchange(nccl_comm_, stream_, sb, rb, X.sends, X.recvs);
     }
-    launch_ghost_gather(X.dst.as<int64_t>(), X.src.as<int64_t>(), X.nlocal, X.ntotal, arena, rb, stream_);
+    launch_ghost_gather(X.dst.as<void>(), X.src.as<void>(), X.idx32, X.nlocal, X.ntotal, arena, rb, stream_);
 }
 
 } // namespace hyb

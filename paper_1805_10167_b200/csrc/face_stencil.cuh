@@ -1,7 +1,7 @@
 // K1: face stencil (apply / residual / Jacobi) over macro-face interiors.
 // Included by kernels.cu.
 //
-// One CTA = one (face, 256-column block, band of FS_RB rows). A producer warp
+// One CTA = one (face, 256-column block, band of rows). A producer warp
 // streams the band's row segments HBM -> shared memory with 1-D bulk copies
 // (cp.async.bulk, the TMA engine) into an FS_S-stage ring guarded by
 // mbarriers (full: bytes landed; empty: all consumer warps done). Four
@@ -19,7 +19,19 @@ constexpr int FS_CWARPS = 4;                 // consumer warps
 constexpr int FS_THREADS = (FS_CWARPS + 1) * 32;
 constexpr int FS_COLS = FS_CWARPS * 64;      // 256 columns per CTA
 constexpr int FS_XW = FS_COLS + 4;           // staged x columns [c0-2, c0+FS_COLS+2)
-constexpr int FS_RB = 64;                    // rows per band
+// rows per band: long bands amortise the 2 halo rows at fine levels, short
+// ones give coarse levels enough CTAs (the row march is latency-bound there)
+__host__ __device__ __forceinline__ int fs_band(int n) { return n >= 1024 ? 64 : (n >= 512 ? 32 : (n >= 128 ? 16 : 8)); }
+
+// Correctly rounded a / d from y = RN(1/d) (Markstein: q = RN(a y),
+// r = a - d q exactly by FMA, RN(q + r y) = RN(a / d) barring
+// under/overflow): the Jacobi row's division by its per-face constant
+// diagonal in 3 FP64 ops instead of a full IEEE division per DoF.
+__device__ __forceinline__ double div_by(double a, double d, double y) {
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-d, q, a);
+    return __fma_rn(r, y, q);
+}
 constexpr int FS_S = 8;                      // pipeline stages
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -66,9 +78,10 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     const int n = t.n, W = t.W;
     const int face = blockIdx.z;
     const int c0 = blockIdx.x * FS_COLS;
-    int r_lo = blockIdx.y * FS_RB;
+    const int rb = fs_band(t.n);
+    int r_lo = blockIdx.y * rb;
     if (r_lo < 1) r_lo = 1;
-    int r_hi = (blockIdx.y + 1) * FS_RB; // exclusive
+    int r_hi = (blockIdx.y + 1) * rb; // exclusive
     if (r_hi > n - 1) r_hi = n - 1;     // interior rows r <= n-2
     const int cmin = c0 < 1 ? 1 : c0;
     if (r_hi > n - cmin) r_hi = n - cmin; // first column of the block stays interior
@@ -123,6 +136,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     const int k = 2 + 2 * tid; // smem index of column c
     const double* co = t.face_coef + size_t(face) * 8;
     const double cW = co[0], cNW = co[1], cS = co[2], cC = co[3], cN = co[4], cSE = co[5], cE = co[6], dg = co[7];
+    const double rdg = 1.0 / dg;
     double* __restrict__ yf = y + base;
 
     // window: rows r-1 (m*) and r (z*) at columns c-1, c, c+1, c+2
@@ -166,8 +180,8 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                     o0 = bb.x - a0;
                     o1 = bb.y - a1;
                 } else if (MODE == ST_JACOBI) {
-                    o0 = z0 + omega * (bb.x - a0) / dg;
-                    o1 = z1 + omega * (bb.y - a1) / dg;
+                    o0 = z0 + div_by(omega * (bb.x - a0), dg, rdg); // x + omega*(b - Ax)/diag
+                    o1 = z1 + div_by(omega * (bb.y - a1), dg, rdg);
                 }
                 double* yrow = yf + ro[r];
                 if (v0 && v1) {
@@ -185,6 +199,6 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
 }
 
 inline dim3 face_stencil_grid(const LevelTables& t) {
-    return dim3(unsigned((t.n - 1 + FS_COLS - 1) / FS_COLS), unsigned((t.n - 1 + FS_RB - 1) / FS_RB),
+    return dim3(unsigned((t.n - 1 + FS_COLS - 1) / FS_COLS), unsigned((t.n - 1 + fs_band(t.n) - 1) / fs_band(t.n)),
                 unsigned(t.nfaces));
 }

@@ -104,9 +104,9 @@ __global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl
 // (src/communication.cpp:54-62) collapse into one gather: the state after
 // it is the reference's post-sync_all state, every copy equal to its owner.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_ghost_gather(const int64_t* __restrict__ dst,
-                                                      const int64_t* __restrict__ src, int64_t nlocal,
-                                                      int64_t ntotal, double* arena,
+template <class I>
+__global__ void __launch_bounds__(256) k_ghost_gather(const I* __restrict__ dst, const I* __restrict__ src,
+                                                      int64_t nlocal, int64_t ntotal, double* arena,
                                                       const double* __restrict__ recv) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < ntotal;
          i += int64_t(gridDim.x) * blockDim.x)
@@ -352,51 +352,74 @@ __device__ double block_reduce_256(double v, double* sh) {
     return sh[0];
 }
 
+template <int OP> __device__ __forceinline__ double term(double a, double b) {
+    return OP == 0 ? a * b : fabs(a);
+}
+
+template <int OP> __device__ __forceinline__ double warp_fold(double v) {
+    for (int o = 16; o > 0; o >>= 1) v = red2<OP>(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Faces: CTA = 8 warps over one band of PB rows; warp w takes rows w, w+8, ...;
+// a lane accumulates the 16-byte pairs at its columns (even and odd slots in
+// separate registers, interior columns only). The shape of every sum depends
+// only on the face, so partials are bitwise partition invariant.
 template <int OP>
 __global__ void __launch_bounds__(256) k_partials_faces(LevelTables t, const double* __restrict__ x1,
                                                         const double* __restrict__ x2, double* scratch, int bands) {
     __shared__ double sh[256];
     const int n = t.n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double* a = x1 + int64_t(blockIdx.y) * t.face_stride;
     const double* b = x2 + int64_t(blockIdx.y) * t.face_stride;
-    double s = 0.0;
+    double s0 = 0.0, s1 = 0.0;
     const int r0 = 1 + blockIdx.x * PB;
-    for (int row = r0; row < r0 + PB && row <= n - 2; ++row) {
+    for (int row = r0 + warp; row < r0 + PB && row <= n - 2; row += 8) {
         const int64_t ro = t.rowoff[row];
-        for (int col = 1 + threadIdx.x; col <= n - 1 - row; col += 256) {
-            const double va = a[ro + col];
-            s = OP == 0 ? s + va * b[ro + col] : fmax(s, fabs(va));
+        const int last = n - 1 - row;
+        for (int col = 2 * lane; col <= last; col += 64) {
+            const double2 va = __ldg(reinterpret_cast<const double2*>(a + ro + col));
+            const double2 vb = OP == 0 ? __ldg(reinterpret_cast<const double2*>(b + ro + col)) : va;
+            if (col >= 1) s0 = red2<OP>(s0, term<OP>(va.x, vb.x));
+            if (col + 1 <= last) s1 = red2<OP>(s1, term<OP>(va.y, vb.y));
         }
     }
-    const double tot = block_reduce_256<OP>(s, sh);
+    const double tot = block_reduce_256<OP>(red2<OP>(s0, s1), sh);
     if (threadIdx.x == 0) scratch[int64_t(blockIdx.y) * bands + blockIdx.x] = tot;
 }
 
+// faces: fold the bands in order (one thread per face); edges: one warp per
+// edge over k = 1..n-1 with a fixed shuffle tree; vertices: one thread each
 template <int OP>
 __global__ void k_partials_finish(LevelTables t, const double* __restrict__ x1, const double* __restrict__ x2,
                                   const double* scratch, int bands, double* part) {
-    // thread per face (fold bands), then per edge / vertex
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = t.n;
-    if (i < t.nfaces) {
-        double s = 0.0;
-        for (int j = 0; j < bands; ++j) s = red2<OP>(s, scratch[int64_t(i) * bands + j]);
-        part[t.face_gid[i]] = s;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nfw = (t.nfaces + 31) / 32; // warps spent on faces
+    if (gw < nfw) {
+        const int i = gw * 32 + lane;
+        if (i < t.nfaces) {
+            double s = 0.0;
+            for (int j = 0; j < bands; ++j) s = red2<OP>(s, scratch[int64_t(i) * bands + j]);
+            part[t.face_gid[i]] = s;
+        }
         return;
     }
-    int j = i - t.nfaces;
-    if (j < t.nedges) {
-        const double* a = x1 + t.edge_off[j];
-        const double* b = x2 + t.edge_off[j];
+    const int e = gw - nfw;
+    if (e < t.nedges) {
+        const double* a = x1 + t.edge_off[e];
+        const double* b = x2 + t.edge_off[e];
         double s = 0.0;
-        for (int k = 1; k <= n - 1; ++k) s = OP == 0 ? s + a[k] * b[k] : fmax(s, fabs(a[k]));
-        part[t.edge_gid[j]] = s;
+        for (int k = 1 + lane; k <= n - 1; k += 32) s = red2<OP>(s, term<OP>(a[k], b[k]));
+        s = warp_fold<OP>(s);
+        if (lane == 0) part[t.edge_gid[e]] = s;
         return;
     }
-    j -= t.nedges;
-    if (j < t.nverts) {
-        const double va = x1[t.vtx_off[j]];
-        part[t.vtx_gid[j]] = OP == 0 ? 0.0 + va * x2[t.vtx_off[j]] : fmax(0.0, fabs(va));
+    const int v = (gw - nfw - t.nedges) * 32 + lane;
+    if (v >= 0 && v < t.nverts) {
+        const double va = x1[t.vtx_off[v]];
+        part[t.vtx_gid[v]] = red2<OP>(0.0, term<OP>(va, x2[t.vtx_off[v]]));
     }
 }
 
@@ -457,10 +480,17 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
     }
 }
 
-void launch_ghost_gather(const int64_t* dst, const int64_t* src, int64_t nlocal, int64_t ntotal, double* arena,
+void launch_ghost_gather(const void* dst, const void* src, bool idx32, int64_t nlocal, int64_t ntotal, double* arena,
                          const double* recv, cudaStream_t st) {
     if (ntotal <= 0) return;
-    k_ghost_gather<<<grid_for(ntotal), 256, 0, st>>>(dst, src, nlocal, ntotal, arena, recv);
+    if (idx32)
+        k_ghost_gather<int32_t><<<grid_for(ntotal), 256, 0, st>>>(static_cast<const int32_t*>(dst),
+                                                                   static_cast<const int32_t*>(src), nlocal, ntotal,
+                                                                   arena, recv);
+    else
+        k_ghost_gather<int64_t><<<grid_for(ntotal), 256, 0, st>>>(static_cast<const int64_t*>(dst),
+                                                                   static_cast<const int64_t*>(src), nlocal, ntotal,
+                                                                   arena, recv);
     check_launch("ghost gather");
 }
 
@@ -567,10 +597,11 @@ void launch_partials(int op, const LevelTables& t, const double* x1, const doubl
         else k_partials_faces<1><<<grid, 256, 0, st>>>(t, x1, x2, scratch, bands);
         check_launch("partials faces");
     }
-    const int total = t.nfaces + t.nedges + t.nverts;
-    if (total > 0) {
-        if (op == 0) k_partials_finish<0><<<(total + 127) / 128, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
-        else k_partials_finish<1><<<(total + 127) / 128, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
+    const int warps = (t.nfaces + 31) / 32 + t.nedges + (t.nverts + 31) / 32;
+    if (warps > 0) {
+        const int blocks = (warps + 3) / 4;
+        if (op == 0) k_partials_finish<0><<<blocks, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
+        else k_partials_finish<1><<<blocks, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
         check_launch("partials finish");
     }
 }
@@ -637,10 +668,22 @@ __device__ void cg_spmv(const int32_t* __restrict__ rowptr, const int32_t* __res
 __global__ void __launch_bounds__(CG_THREADS) k_coarse_cg(int64_t n, const int32_t* __restrict__ rowptr,
                                                           const int32_t* __restrict__ col,
                                                           const double* __restrict__ val,
-                                                          const double* __restrict__ b, double* x, double* r,
+                                                          const double* __restrict__ bg, double* xg, double* r,
                                                           double* p, double* ap, double tol, int max_iter,
-                                                          CoarseStatus* st) {
+                                                          CoarseStatus* st, int in_smem) {
     __shared__ double red[33];
+    extern __shared__ double dsm[]; // small systems: all five vectors on chip
+    const double* b = bg;
+    double* x = xg;
+    if (in_smem) {
+        double* sb = dsm;
+        x = dsm + n;
+        r = dsm + 2 * n;
+        p = dsm + 3 * n;
+        ap = dsm + 4 * n;
+        for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) sb[i] = bg[i];
+        b = sb;
+    }
     for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) {
         x[i] = 0.0;
         r[i] = b[i]; // b - A * 0
@@ -675,6 +718,8 @@ __global__ void __launch_bounds__(CG_THREADS) k_coarse_cg(int64_t n, const int32
     for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) ap[i] = b[i] - ap[i];
     __syncthreads();
     const double res = sqrt(cg_dot(ap, ap, n, red));
+    if (in_smem)
+        for (int64_t i = threadIdx.x; i < n; i += CG_THREADS) xg[i] = x[i];
     if (threadIdx.x == 0) {
         st->iterations = it;
         st->breakdown = breakdown;
@@ -696,7 +741,17 @@ void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos,
 void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* b,
                       double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
                       cudaStream_t stream) {
-    k_coarse_cg<<<1, CG_THREADS, 0, stream>>>(n, rowptr, col, val, b, x, r, p, ap, tol, max_iter, st);
+    const size_t smem = size_t(5 * n) * sizeof(double);
+    const bool in_smem = smem <= 200 * 1024;
+    if (in_smem) {
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr_set = true;
+        }
+    }
+    k_coarse_cg<<<1, CG_THREADS, in_smem ? smem : 0, stream>>>(n, rowptr, col, val, b, x, r, p, ap, tol, max_iter, st,
+                                                               in_smem ? 1 : 0);
     check_launch("coarse cg");
 }
 

@@ -57,7 +57,8 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
 int64_t kernel_launch_count();
 /// Ghost refresh, one pass: arena[dst[i]] = arena[src[i]] for i < nlocal
 /// (owner on this process), arena[dst[i]] = recv[i - nlocal] for the rest.
-void launch_ghost_gather(const int64_t* dst, const int64_t* src, int64_t nlocal, int64_t ntotal, double* arena,
+/// dst/src are int32 (idx32, arenas below 2^31 slots) or int64 arrays.
+void launch_ghost_gather(const void* dst, const void* src, bool idx32, int64_t nlocal, int64_t ntotal, double* arena,
                          const double* recv, cudaStream_t st);
 /// send[i] = arena[src[i]] (owned values other processes hold ghosts of)
 void launch_ghost_pack(const int64_t* src, int64_t n, const double* arena, double* send, cudaStream_t st);

@@ -329,7 +329,72 @@ void Hierarchy::vcycle(Function& rhs, Function& x, int level, int nu_pre, int nu
         throw OutOfRange("vcycle: level " + std::to_string(level) + " outside [" + std::to_string(a_.min_level()) +
                          ", " + std::to_string(a_.max_level()) + "]");
     if (nu_pre < 0 || nu_post < 0) throw InvalidArgument("vcycle: negative smoothing count");
-    cycle(rhs, x, level, nu_pre, nu_post);
+    run_cycle(rhs, x, level, nu_pre, nu_post);
+}
+
+Hierarchy::~Hierarchy() {
+    for (auto& g : graphs_)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+}
+
+std::vector<const void*> Hierarchy::graph_key(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
+    std::vector<const void*> k{&rhs, &x, rhs.data(level), x.data(level), reinterpret_cast<const void*>(intptr_t(level)),
+                               reinterpret_cast<const void*>(intptr_t(nu_pre)),
+                               reinterpret_cast<const void*>(intptr_t(nu_post))};
+    for (int l = a_.min_level(); l <= level; ++l) {
+        k.push_back(r_.data(l));
+        k.push_back(b_.data(l));
+        k.push_back(e_.data(l));
+        if (l > a_.min_level()) k.push_back(dom_->jacobi_scratch(l).as<void>());
+    }
+    return k;
+}
+
+// One cycle, replayed from a CUDA graph when possible: the first call with a
+// given argument/arena state runs eagerly (allocations, plans), the second
+// captures the whole cycle (kernels, copies, NCCL) and later calls replay it.
+void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
+    Domain& d = *dom_;
+    if (!use_graphs || (nu_pre + nu_post) % 2 != 0 || d.profiling) {
+        cycle(rhs, x, level, nu_pre, nu_post);
+        check_coarse();
+        return;
+    }
+    const std::vector<const void*> key = graph_key(rhs, x, level, nu_pre, nu_post);
+    for (const auto& g : graphs_)
+        if (g.key == key) {
+            HYB_CUDA(cudaGraphLaunch(g.exec, d.stream()));
+            ++graph_replays;
+            check_coarse();
+            return;
+        }
+    if (std::find(warm_.begin(), warm_.end(), key) == warm_.end()) {
+        cycle(rhs, x, level, nu_pre, nu_post);
+        check_coarse();
+        warm_.push_back(key);
+        return;
+    }
+    cudaGraph_t graph = nullptr;
+    HYB_CUDA(cudaStreamBeginCapture(d.stream(), cudaStreamCaptureModeThreadLocal));
+    try {
+        cycle(rhs, x, level, nu_pre, nu_post);
+    } catch (...) {
+        cudaStreamEndCapture(d.stream(), &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    HYB_CUDA(cudaStreamEndCapture(d.stream(), &graph));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    HYB_CUDA(ie);
+    if (graph_key(rhs, x, level, nu_pre, nu_post) != key) { // capture ran no kernels, only host bookkeeping
+        cudaGraphExecDestroy(exec);
+        throw LogicError("vcycle: arena state not restored by the captured cycle");
+    }
+    graphs_.push_back({key, exec});
+    HYB_CUDA(cudaGraphLaunch(exec, d.stream()));
+    ++graph_replays;
     check_coarse();
 }
 
@@ -401,8 +466,7 @@ std::vector<double> Hierarchy::solve(Function& rhs, Function& x, int level, doub
     const double target = r0 > 0.0 ? tol * r0 : tol;
     int it = 0;
     while (it < max_cycles && res.back() > target) {
-        cycle(rhs, x, level, nu_pre, nu_post);
-        check_coarse();
+        run_cycle(rhs, x, level, nu_pre, nu_post);
         ++it;
         res.push_back(residual_norm(rhs, x, level));
     }

@@ -5,79 +5,85 @@
 // marches a band of coarse rows; fine columns 2c, 2c+1 are read/written as one
 // aligned 16-byte pair, the c+1 / 2c-1 neighbours come from warp shuffles
 // (lane 31 / lane 0 load the one value beyond the warp). Every fine row and
-// every coarse row is touched once per band: HBM streams at full width.
+// every coarse row is touched once per band, and the next row's loads are
+// issued before the current row is stored, so two rows of loads are in flight
+// per warp.
 //
 // Arithmetic is the reference's, term by term (src/solvers.cpp:106-124,
 // 184-200).
 #pragma once
 
 constexpr int TR_WARPS = 4;
-constexpr int TR_RB = 32; // coarse rows per band
+__host__ __device__ __forceinline__ int tr_band(int nc) { return nc >= 256 ? 32 : (nc >= 64 ? 16 : 8); }
 
 inline dim3 transfer_grid(int nc, int nfaces) {
-    return dim3(unsigned((nc + TR_WARPS * 32) / (TR_WARPS * 32)), unsigned((nc + TR_RB) / TR_RB), unsigned(nfaces));
+    return dim3(unsigned((nc + TR_WARPS * 32) / (TR_WARPS * 32)), unsigned((nc + tr_band(nc)) / tr_band(nc)),
+                unsigned(nfaces));
 }
 
 // fine := P coarse (add = 0) or fine += P coarse (add = 1) on fine face interiors
 __global__ void __launch_bounds__(TR_WARPS * 32) k_prolongate_faces(LevelTables tc, LevelTables tf,
-                                                                    const double* __restrict__ xc,
-                                                                    double* __restrict__ xf, int add) {
+                                                                    const double* __restrict__ xc, double* xf,
+                                                                    int add) {
     const int nc = tc.n, nf = tf.n;
     const int lane = threadIdx.x & 31;
     const int cw = (blockIdx.x * TR_WARPS + (threadIdx.x >> 5)) * 32; // first coarse column of the warp
     const int c = cw + lane;
-    const int r_lo = blockIdx.y * TR_RB;
-    int r_hi = r_lo + TR_RB;
+    const int rb = tr_band(nc);
+    const int r_lo = blockIdx.y * rb;
+    int r_hi = r_lo + rb;
     if (r_hi > nc) r_hi = nc; // coarse rows 0..nc-1 feed fine rows 1..nf-2
     if (cw > nc - 1 - r_lo || r_lo >= r_hi) return; // warp-uniform: no fine output here
     const double* cv = xc + int64_t(blockIdx.z) * tc.face_stride;
     double* fv = xf + int64_t(blockIdx.z) * tf.face_stride;
     const int64_t* __restrict__ cro = tc.rowoff;
     const int64_t* __restrict__ fro = tf.rowoff;
+    const int fc = 2 * c;
     // coarse value at (col, row) if it exists in the closed triangle, else 0
     auto cload = [&](int col, int row) { return col + row <= nc ? __ldg(cv + cro[row] + col) : 0.0; };
-    double a0 = cload(c, r_lo);                   // C(c, r)
-    double e0 = lane == 31 ? cload(cw + 32, r_lo) : 0.0;
-    double a1v = __shfl_down_sync(0xffffffffu, a0, 1);
-    double b0 = lane == 31 ? e0 : a1v;            // C(c+1, r)
+    auto fload = [&](int row) { // current fine pair (add mode), row must be an interior fine row
+        return (add && row >= 1 && row <= nf - 2 && fc <= nf - 1 - row) ? *reinterpret_cast<const double2*>(fv + fro[row] + fc)
+                                                                       : make_double2(0.0, 0.0);
+    };
+    const double a_own = cload(c, r_lo);
+    const double a_ext = lane == 31 ? cload(cw + 32, r_lo) : 0.0;
+    double nx = cload(c, r_lo + 1);
+    double nxe = lane == 31 ? cload(cw + 32, r_lo + 1) : 0.0;
+    double2 f0 = fload(2 * r_lo), f1 = fload(2 * r_lo + 1);
+    double a0 = a_own;
+    const double a_sh = __shfl_down_sync(0xffffffffu, a_own, 1);
+    double b0 = lane == 31 ? a_ext : a_sh;
     for (int r = r_lo; r < r_hi; ++r) {
-        const double n0 = cload(c, r + 1);        // C(c, r+1)
-        const double en = lane == 31 ? cload(cw + 32, r + 1) : 0.0;
+        const double n0 = nx, ne = nxe;
+        const double2 g0 = f0, g1 = f1;
+        if (r + 1 < r_hi) { // issue the next row's loads first
+            nx = cload(c, r + 2);
+            nxe = lane == 31 ? cload(cw + 32, r + 2) : 0.0;
+            f0 = fload(2 * r + 2);
+            f1 = fload(2 * r + 3);
+        }
         const double sn = __shfl_down_sync(0xffffffffu, n0, 1);
-        const double n1 = lane == 31 ? en : sn;   // C(c+1, r+1)
-        const int fc = 2 * c;
-        // fine row 2r: (2c) copy, (2c+1) row midpoint
+        const double n1 = lane == 31 ? ne : sn; // C(c+1, r+1)
         const int fr0 = 2 * r, fr1 = 2 * r + 1;
-        if (fr0 >= 1 && fr0 <= nf - 2) {
+        if (fr0 >= 1 && fr0 <= nf - 2) { // fine row 2r: (2c) copy, (2c+1) row midpoint
             const int last = nf - 1 - fr0;
             const double v0 = a0, v1 = 0.5 * (a0 + b0);
             double* p = fv + fro[fr0] + fc;
-            const bool ok0 = fc >= 1 && fc <= last, ok1 = fc + 1 >= 1 && fc + 1 <= last;
+            const bool ok0 = fc >= 1 && fc <= last, ok1 = fc + 1 <= last;
             if (ok0 && ok1) {
-                double2 o = make_double2(v0, v1);
-                if (add) {
-                    const double2 cur = *reinterpret_cast<const double2*>(p);
-                    o = make_double2(cur.x + v0, cur.y + v1);
-                }
-                *reinterpret_cast<double2*>(p) = o;
+                *reinterpret_cast<double2*>(p) = add ? make_double2(g0.x + v0, g0.y + v1) : make_double2(v0, v1);
             } else {
                 if (ok0) p[0] = add ? p[0] + v0 : v0;
                 if (ok1) p[1] = add ? p[1] + v1 : v1;
             }
         }
-        // fine row 2r+1: (2c) column midpoint, (2c+1) diagonal midpoint
-        if (fr1 <= nf - 2) {
+        if (fr1 <= nf - 2) { // fine row 2r+1: (2c) column midpoint, (2c+1) diagonal midpoint
             const int last = nf - 1 - fr1;
             const double v0 = 0.5 * (a0 + n0), v1 = 0.5 * (b0 + n0);
             double* p = fv + fro[fr1] + fc;
             const bool ok0 = fc >= 1 && fc <= last, ok1 = fc + 1 <= last;
             if (ok0 && ok1) {
-                double2 o = make_double2(v0, v1);
-                if (add) {
-                    const double2 cur = *reinterpret_cast<const double2*>(p);
-                    o = make_double2(cur.x + v0, cur.y + v1);
-                }
-                *reinterpret_cast<double2*>(p) = o;
+                *reinterpret_cast<double2*>(p) = add ? make_double2(g1.x + v0, g1.y + v1) : make_double2(v0, v1);
             } else {
                 if (ok0) p[0] = add ? p[0] + v0 : v0;
                 if (ok1) p[1] = add ? p[1] + v1 : v1;
@@ -96,9 +102,10 @@ __global__ void __launch_bounds__(TR_WARPS * 32) k_restrict_faces(LevelTables tc
     const int lane = threadIdx.x & 31;
     const int cw = (blockIdx.x * TR_WARPS + (threadIdx.x >> 5)) * 32;
     const int c = cw + lane;
-    int r_lo = blockIdx.y * TR_RB;
+    const int rb = tr_band(nc);
+    int r_lo = blockIdx.y * rb;
     if (r_lo < 1) r_lo = 1;
-    int r_hi = (blockIdx.y + 1) * TR_RB;
+    int r_hi = (blockIdx.y + 1) * rb;
     if (r_hi > nc - 1) r_hi = nc - 1; // coarse interior rows 1..nc-2
     const int cmin = cw < 1 ? 1 : cw;
     if (r_hi > nc - cmin) r_hi = nc - cmin;
@@ -108,28 +115,31 @@ __global__ void __launch_bounds__(TR_WARPS * 32) k_restrict_faces(LevelTables tc
     const int64_t* __restrict__ cro = tc.rowoff;
     const int64_t* __restrict__ fro = tf.rowoff;
     const int fc = 2 * c;
-    // fine pair (2c, 2c+1) of row q and the value at 2c-1 (left lane / own load)
-    auto fload = [&](int q, double2& v, double& left) {
-        const int len = nf + 1 - q;
-        v = fc < len ? __ldg(reinterpret_cast<const double2*>(fv + fro[q] + fc)) : make_double2(0.0, 0.0);
-        const double from_left = __shfl_up_sync(0xffffffffu, v.y, 1);
-        left = from_left;
-        if (lane == 0) left = (fc >= 1 && fc - 1 < len) ? __ldg(fv + fro[q] + fc - 1) : 0.0;
+    // raw loads of fine row q: pair (2c, 2c+1); lane 0 also the value at 2c-1
+    auto fpair = [&](int q) {
+        return fc < nf + 1 - q ? __ldg(reinterpret_cast<const double2*>(fv + fro[q] + fc)) : make_double2(0.0, 0.0);
     };
-    double2 s;       // fine row 2r-1
-    double sl;
-    fload(2 * r_lo - 1, s, sl);
+    auto fleft = [&](int q) { return (lane == 0 && fc >= 1 && fc - 1 < nf + 1 - q) ? __ldg(fv + fro[q] + fc - 1) : 0.0; };
+    auto left_of = [&](const double2& v, double own) { // value at 2c-1 from the left lane
+        const double l = __shfl_up_sync(0xffffffffu, v.y, 1);
+        return lane == 0 ? own : l;
+    };
+    double2 s = fpair(2 * r_lo - 1); // fine row 2r-1
+    double2 m = fpair(2 * r_lo), p = fpair(2 * r_lo + 1);
+    double ml_raw = fleft(2 * r_lo), pl_raw = fleft(2 * r_lo + 1);
     for (int r = r_lo; r < r_hi; ++r) {
-        double2 m, p;
-        double ml, pl;
-        fload(2 * r, m, ml);
-        fload(2 * r + 1, p, pl);
-        if (c >= 1 && c <= nc - 1 - r) {
-            // f(2c,2r) + 0.5*(W + E + S + N + SE + NW), left to right
-            cv[cro[r] + c] = m.x + 0.5 * (ml + m.y + s.x + p.x + s.y + pl);
+        const double2 cm = m, cp = p;
+        const double cml = ml_raw, cpl = pl_raw;
+        if (r + 1 < r_hi) { // next coarse row's fine rows 2r+2, 2r+3
+            m = fpair(2 * r + 2);
+            p = fpair(2 * r + 3);
+            ml_raw = fleft(2 * r + 2);
+            pl_raw = fleft(2 * r + 3);
         }
-        s = p;
-        sl = pl;
+        const double W = left_of(cm, cml), NW = left_of(cp, cpl);
+        if (c >= 1 && c <= nc - 1 - r)
+            // f(2c,2r) + 0.5*(W + E + S + N + SE + NW), left to right
+            cv[cro[r] + c] = cm.x + 0.5 * (W + cm.y + s.x + cp.x + s.y + NW);
+        s = cp;
     }
-    (void)sl;
 }

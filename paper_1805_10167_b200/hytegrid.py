@@ -448,6 +448,12 @@ class GridHierarchy:
     def vcycle(self, rhs: ScalarFunction, x: ScalarFunction, level: int, nu_pre: int = 2, nu_post: int = 2) -> None:
         check(lib.hyb_hierarchy_vcycle(self._h, rhs._h, x._h, level, nu_pre, nu_post))
 
+    def use_graphs(self, enable: bool | None = None) -> int:
+        """Toggle CUDA-graph replay of V-cycles; returns graph launches so far."""
+        n = C.c_int64()
+        check(lib.hyb_hierarchy_graphs(self._h, -1 if enable is None else int(enable), C.byref(n)))
+        return n.value
+
     def residual_norm(self, rhs: ScalarFunction, x: ScalarFunction, level: int) -> float:
         out = C.c_double()
         check(lib.hyb_hierarchy_residual_norm(self._h, rhs._h, x._h, level, C.byref(out)))

@@ -334,3 +334,23 @@ def test_cfg2_full_size_properties():
     flags = y.flags(L)
     yv = y.download(L)
     assert np.max(np.abs(yv[flags == H.INNER])) <= 1e-12 * (1 << L) ** 0
+
+
+def test_graph_replayed_vcycles_bitwise_equal_eager():
+    """CUDA-graph replay of the V-cycle is the same computation as eager launches."""
+    mesh = H.meshgen.channel(4, 4)
+    L = 6
+    out = []
+    for graphs in (False, True):
+        dom = H.DistributedDomain(mesh, 2)
+        ctl = H.Controller(dom)
+        mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L)
+        mg.use_graphs(graphs)
+        rhs = H.ScalarFunction("rhs", dom, 0, L)
+        x = H.ScalarFunction("x", dom, 0, L)
+        H.interpolate_random(rhs, L, seed=5, flag_mask=H.INNER)
+        rep = mg.solve(rhs, x, L, 0.0, 6)
+        out.append((x.download(L), rep.residuals, mg.use_graphs()))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+    assert out[0][2] == 0 and out[1][2] >= 4
