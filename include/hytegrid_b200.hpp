@@ -1,0 +1,275 @@
+// hytegrid_b200.hpp -- C++ drop-in for the reference's multigrid hot-path API
+// (arXiv 1805.10167 "hytegrid", /root/reference/proj/include/hytegrid/*.hpp),
+// header-only over the C ABI in hyteg_b200.h. Same names, argument order and
+// exception types as the reference:
+//
+//   reference                                   here
+//   DistributedDomain(setup, assignment, P)     DistributedDomain(mesh_text, P[, assignment])
+//   Controller(domain), register_function       Controller(domain), register_function (no-ops)
+//   ScalarFunction(name, dom, P1, min, max, bc) ScalarFunction(name, dom, min, max, bc)
+//   StencilOperator(dom, form, P1, min, max, bc) StencilOperator(dom, form, min, max, bc)
+//   apply / smooth_jacobi / diagonal            same (operators.hpp:108-125)
+//   prolongate / restrict_to_coarse             same (solvers.hpp:26-33)
+//   assign / add_scaled / dot / norm2 / max_abs same (function.hpp:60-74)
+//   interpolate(f, expr, level, mask)           same; expr evaluated on the host at the
+//                                               reference's DoF coordinates, then uploaded
+//   sync_all(ctl, f, level)                     same
+//   GridHierarchy(dom, ctl, form, min, max, bc) same + smoother weight / coarse tolerance
+//   f.values(id, level)                         f.download(level) / f.upload(level, v)
+//                                               (GlobalDoFMap order, numbering.hpp:41-43)
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hyteg_b200.h"
+
+namespace hytegrid_b200 {
+
+enum class DoFFlag : std::uint8_t { INNER = 1, DIRICHLET = 2, NEUMANN = 4 };
+constexpr std::uint8_t ALL_DOF_FLAGS = 7;
+inline std::uint8_t flag_bit(DoFFlag f) { return static_cast<std::uint8_t>(f); }
+enum class Form : int { LAPLACE = HYB_LAPLACE, MASS = HYB_MASS };
+
+struct BoundaryConditions {
+    std::map<int, DoFFlag> marker_flag;
+};
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(int status) {
+    if (status == HYB_OK) return;
+    const std::string msg = hyb_last_error();
+    switch (status) {
+    case HYB_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case HYB_OUT_OF_RANGE: throw std::out_of_range(msg);
+    case HYB_RUNTIME_ERROR: throw std::runtime_error(msg);
+    case HYB_LOGIC_ERROR: throw std::logic_error(msg);
+    default: throw CudaError(msg);
+    }
+}
+
+namespace meshgen {
+inline std::string gen(const char* kind, std::vector<double> p = {}) {
+    int64_t len = 0;
+    check(hyb_meshgen(kind, p.data(), int(p.size()), nullptr, 0, &len));
+    std::string s(size_t(len) + 1, '\0');
+    check(hyb_meshgen(kind, p.data(), int(p.size()), s.data(), len + 1, &len));
+    s.resize(size_t(len));
+    return s;
+}
+inline std::string unit_triangle() { return gen("unit_triangle"); }
+inline std::string unit_square() { return gen("unit_square"); }
+inline std::string unit_square_reversed() { return gen("unit_square_reversed"); }
+inline std::string square_ring8() { return gen("square_ring8"); }
+inline std::string channel(int nx, int ny, double w = 1.0, double h = 1.0) { return gen("channel", {double(nx), double(ny), w, h}); }
+inline std::string annulus(int seg, int layers, double ri, double ro) {
+    return gen("annulus", {double(seg), double(layers), ri, ro});
+}
+} // namespace meshgen
+
+class DistributedDomain {
+  public:
+    /// P logical ranks, all driven by this process (the reference's model);
+    /// assignment empty = partition_round_robin.
+    DistributedDomain(const std::string& mesh_text, int ranks = 1, std::vector<int32_t> assignment = {},
+                      int device = 0) {
+        int64_t nv, ne, nf;
+        check(hyb_mesh_counts(mesh_text.c_str(), &nv, &ne, &nf));
+        if (assignment.empty()) {
+            assignment.resize(size_t(nv + ne + nf));
+            check(hyb_partition(mesh_text.c_str(), ranks, HYB_PARTITION_ROUND_ROBIN, 0, assignment.data()));
+        }
+        std::vector<int32_t> local(static_cast<size_t>(ranks));
+        for (int r = 0; r < ranks; ++r) local[size_t(r)] = r;
+        check(hyb_domain_create(mesh_text.c_str(), ranks, assignment.data(), local.data(), ranks, device, &h_));
+    }
+    ~DistributedDomain() { hyb_domain_destroy(h_); }
+    DistributedDomain(const DistributedDomain&) = delete;
+    DistributedDomain& operator=(const DistributedDomain&) = delete;
+    hyb_domain* handle() const { return h_; }
+    int64_t owned(int level) const {
+        int64_t t = 0;
+        check(hyb_domain_owned_count(h_, level, &t, nullptr));
+        return t;
+    }
+    std::vector<double> coords(int level) const {
+        std::vector<double> xy(size_t(2 * owned(level)));
+        check(hyb_owned_coords(h_, level, 1, xy.data(), owned(level)));
+        return xy;
+    }
+
+  private:
+    hyb_domain* h_ = nullptr;
+};
+
+class ScalarFunction;
+
+class Controller {
+  public:
+    explicit Controller(DistributedDomain& d) : domain_(&d) {}
+    DistributedDomain& domain() { return *domain_; }
+
+  private:
+    DistributedDomain* domain_;
+};
+
+namespace detail {
+inline void bc_arrays(const BoundaryConditions& bc, std::vector<int32_t>& m, std::vector<uint8_t>& f) {
+    for (const auto& [k, v] : bc.marker_flag) {
+        m.push_back(k);
+        f.push_back(static_cast<uint8_t>(v));
+    }
+}
+} // namespace detail
+
+class ScalarFunction {
+  public:
+    ScalarFunction(const std::string& name, DistributedDomain& d, int min_level, int max_level,
+                   BoundaryConditions bc = {})
+        : dom_(&d) {
+        std::vector<int32_t> m;
+        std::vector<uint8_t> f;
+        detail::bc_arrays(bc, m, f);
+        check(hyb_function_create(d.handle(), name.c_str(), min_level, max_level, m.data(), f.data(), int(m.size()),
+                                  &h_));
+    }
+    ~ScalarFunction() { hyb_function_destroy(h_); }
+    ScalarFunction(const ScalarFunction&) = delete;
+    ScalarFunction& operator=(const ScalarFunction&) = delete;
+    hyb_function* handle() const { return h_; }
+    DistributedDomain& domain() const { return *dom_; }
+    std::vector<double> download(int level) const {
+        std::vector<double> v(size_t(dom_->owned(level)));
+        check(hyb_function_download(h_, level, v.data(), int64_t(v.size()), 1));
+        return v;
+    }
+    void upload(int level, const std::vector<double>& v, std::uint8_t mask = ALL_DOF_FLAGS) {
+        check(hyb_function_upload(h_, level, v.data(), int64_t(v.size()), 1, mask));
+    }
+
+  private:
+    DistributedDomain* dom_;
+    hyb_function* h_ = nullptr;
+};
+
+inline void register_function(Controller&, const ScalarFunction&) {}
+
+class StencilOperator {
+  public:
+    StencilOperator(DistributedDomain& d, Form form, int min_level, int max_level, BoundaryConditions bc = {}) {
+        std::vector<int32_t> m;
+        std::vector<uint8_t> f;
+        detail::bc_arrays(bc, m, f);
+        check(hyb_operator_create(d.handle(), int(form), min_level, max_level, m.data(), f.data(), int(m.size()), &h_));
+    }
+    ~StencilOperator() { hyb_operator_destroy(h_); }
+    StencilOperator(const StencilOperator&) = delete;
+    StencilOperator& operator=(const StencilOperator&) = delete;
+    hyb_operator* handle() const { return h_; }
+
+  private:
+    hyb_operator* h_ = nullptr;
+};
+
+inline void interpolate(ScalarFunction& f, const std::function<double(double, double)>& expr, int level,
+                        std::uint8_t mask = ALL_DOF_FLAGS) {
+    const std::vector<double> xy = f.domain().coords(level);
+    std::vector<double> v(xy.size() / 2);
+    for (size_t i = 0; i < v.size(); ++i) v[i] = expr(xy[2 * i], xy[2 * i + 1]);
+    f.upload(level, v, mask);
+}
+inline void sync_all(Controller&, const ScalarFunction& f, int level) { check(hyb_sync(f.handle(), level)); }
+inline void apply(const StencilOperator& A, Controller&, const ScalarFunction& src, ScalarFunction& dst, int level,
+                  std::uint8_t mask = ALL_DOF_FLAGS) {
+    check(hyb_apply(A.handle(), src.handle(), dst.handle(), level, mask));
+}
+inline void smooth_jacobi(const StencilOperator& A, Controller&, const ScalarFunction& rhs, ScalarFunction& x,
+                          double omega, int level) {
+    check(hyb_smooth_jacobi(A.handle(), rhs.handle(), x.handle(), omega, level));
+}
+inline void diagonal(const StencilOperator& A, ScalarFunction& d, int level) {
+    check(hyb_diagonal(A.handle(), d.handle(), level));
+}
+inline void prolongate(Controller&, const ScalarFunction& coarse, ScalarFunction& fine, int coarse_level,
+                       std::uint8_t mask = ALL_DOF_FLAGS) {
+    check(hyb_prolongate(coarse.handle(), fine.handle(), coarse_level, mask));
+}
+inline void restrict_to_coarse(Controller&, const ScalarFunction& fine, ScalarFunction& coarse, int coarse_level,
+                               std::uint8_t mask = ALL_DOF_FLAGS) {
+    check(hyb_restrict(fine.handle(), coarse.handle(), coarse_level, mask));
+}
+inline void assign(double alpha, const ScalarFunction& x1, double beta, const ScalarFunction& x2, ScalarFunction& dst,
+                   int level, std::uint8_t mask = ALL_DOF_FLAGS) {
+    check(hyb_assign(alpha, x1.handle(), beta, x2.handle(), dst.handle(), level, mask));
+}
+inline void add_scaled(ScalarFunction& dst, double gamma, const ScalarFunction& y, int level,
+                       std::uint8_t mask = ALL_DOF_FLAGS) {
+    check(hyb_add_scaled(dst.handle(), gamma, y.handle(), level, mask));
+}
+inline double dot(const ScalarFunction& a, const ScalarFunction& b, int level) {
+    double out = 0;
+    check(hyb_dot(a.handle(), b.handle(), level, &out));
+    return out;
+}
+inline double norm2(const ScalarFunction& a, int level) { return std::sqrt(dot(a, a, level)); }
+inline double max_abs(const ScalarFunction& a, int level) {
+    double out = 0;
+    check(hyb_max_abs(a.handle(), level, &out));
+    return out;
+}
+
+struct SolveReport {
+    bool converged = false;
+    int iterations = 0;
+    std::vector<double> residuals;
+};
+
+class GridHierarchy {
+  public:
+    GridHierarchy(DistributedDomain& d, Controller&, Form form, int min_level, int max_level,
+                  BoundaryConditions bc = {}, double omega = 2.0 / 3.0, double coarse_tol = 1e-12)
+        : max_(max_level) {
+        std::vector<int32_t> m;
+        std::vector<uint8_t> f;
+        detail::bc_arrays(bc, m, f);
+        check(hyb_hierarchy_create(d.handle(), int(form), min_level, max_level, m.data(), f.data(), int(m.size()),
+                                   HYB_SMOOTH_JACOBI, omega, coarse_tol, -1, &h_));
+    }
+    ~GridHierarchy() { hyb_hierarchy_destroy(h_); }
+    GridHierarchy(const GridHierarchy&) = delete;
+    GridHierarchy& operator=(const GridHierarchy&) = delete;
+    void vcycle(const ScalarFunction& rhs, ScalarFunction& x, int level, int nu_pre = 2, int nu_post = 2) {
+        check(hyb_hierarchy_vcycle(h_, rhs.handle(), x.handle(), level, nu_pre, nu_post));
+    }
+    double residual_norm(const ScalarFunction& rhs, const ScalarFunction& x, int level) {
+        double out = 0;
+        check(hyb_hierarchy_residual_norm(h_, rhs.handle(), x.handle(), level, &out));
+        return out;
+    }
+    SolveReport solve(const ScalarFunction& rhs, ScalarFunction& x, int level, double tol, int max_cycles,
+                      int nu_pre = 2, int nu_post = 2) {
+        SolveReport rep;
+        rep.residuals.resize(size_t(max_cycles) + 1);
+        int n = 0, conv = 0;
+        check(hyb_hierarchy_solve(h_, rhs.handle(), x.handle(), level, tol, max_cycles, nu_pre, nu_post,
+                                  rep.residuals.data(), &n, &conv));
+        rep.residuals.resize(size_t(n));
+        rep.iterations = n - 1;
+        rep.converged = conv != 0;
+        return rep;
+    }
+
+  private:
+    hyb_hierarchy* h_ = nullptr;
+    int max_;
+};
+
+} // namespace hytegrid_b200
