@@ -167,6 +167,10 @@ int hyb_apply(hyb_operator* A, hyb_function* src, hyb_function* dst, int level, 
 int hyb_residual(hyb_operator* A, hyb_function* rhs, hyb_function* x, hyb_function* r, int level);
 /* smooth_jacobi(A, ctl, rhs, x, omega, level)     operators.hpp:113-114 */
 int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level);
+/* smooth_gs(A, ctl, rhs, x, level): hybrid Gauss-Seidel, lexicographic inside
+ * each primitive, halos frozen after the initial sync (operators.hpp:120-121);
+ * bitwise the reference's (wavefront over t = c + 2r on faces) */
+int hyb_smooth_gs(hyb_operator* A, hyb_function* rhs, hyb_function* x, int level);
 /* diagonal(A, d, level)                           operators.hpp:125 */
 int hyb_diagonal(hyb_operator* A, hyb_function* d, int level);
 /* prolongate(ctl, coarse, fine, coarse_level, mask) solvers.hpp:26-27 */

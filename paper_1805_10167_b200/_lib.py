@@ -6,6 +6,7 @@ raises, there is no fallback.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 import re
@@ -104,6 +105,7 @@ _SIGS = {
     "hyb_apply": (_i, [_p, _p, _p, _i, _u8]),
     "hyb_residual": (_i, [_p, _p, _p, _p, _i]),
     "hyb_smooth_jacobi": (_i, [_p, _p, _p, _d, _i]),
+    "hyb_smooth_gs": (_i, [_p, _p, _p, _i]),
     "hyb_diagonal": (_i, [_p, _p, _i]),
     "hyb_prolongate": (_i, [_p, _p, _i, _u8]),
     "hyb_prolongate_add": (_i, [_p, _p, _i, _u8]),
@@ -127,6 +129,20 @@ for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)
     _fn.restype = _res
     _fn.argtypes = _args
+
+
+_state = {"alive": True}
+
+
+@atexit.register
+def _mark_shutdown() -> None:
+    # handles still alive at interpreter exit are left to process teardown:
+    # destroying them while the CUDA runtime shuts down is unsafe
+    _state["alive"] = False
+
+
+def alive() -> bool:
+    return _state["alive"]
 
 
 def check(status: int) -> None:

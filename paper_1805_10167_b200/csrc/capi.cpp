@@ -535,6 +535,15 @@ int hyb_residual(hyb_operator* A, hyb_function* rhs, hyb_function* x, hyb_functi
     });
 }
 
+int hyb_smooth_gs(hyb_operator* A, hyb_function* rhs, hyb_function* x, int level) {
+    return guarded([&] {
+        need(A, "hyb_smooth_gs");
+        need(rhs, "hyb_smooth_gs");
+        need(x, "hyb_smooth_gs");
+        hyb::smooth_gs(*A->a, *rhs->f, *x->f, level);
+    });
+}
+
 int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level) {
     return guarded([&] {
         need(A, "hyb_smooth_jacobi");

@@ -112,6 +112,9 @@ Domain::Domain(const std::string& mesh_text, int world_ranks, const std::vector<
     rank_of_ = assignment;
     HYB_CUDA(cudaSetDevice(device_));
     HYB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    HYB_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+    HYB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    HYB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     place_ = place(g_, rank_of_, local_ranks_);
     scalars_ = DevMem(64 * sizeof(double));
 }
@@ -124,6 +127,9 @@ Domain::~Domain() {
     for (auto& e : events_)
         if (e) cudaEventDestroy(e);
     if (nccl_comm_) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (aux_) cudaStreamDestroy(aux_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -279,6 +285,60 @@ void Domain::timer_reset() {
 }
 
 void Domain::synchronize() { HYB_CUDA(cudaStreamSynchronize(stream_)); }
+
+void Domain::fork() {
+    HYB_CUDA(cudaEventRecord(ev_fork_, stream_));
+    HYB_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+}
+
+void Domain::join() {
+    HYB_CUDA(cudaEventRecord(ev_join_, aux_));
+    HYB_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+}
+
+Domain::GsPlan& Domain::gs_plan(int L) {
+    auto it = gs_.find(L);
+    if (it != gs_.end()) return it->second;
+    GsPlan p;
+    const int n = 1 << L;
+    if (n >= 3 && !place_.faces.empty()) {
+        // tiles in skewed coordinates (t = c + 2r, r): t in [T I, T I + T),
+        // r in [1 + R J, 1 + R J + R); interior points have 2r+1 <= t <= n-1+r
+        const int T = GS_TILE_COLS, R = GS_TILE_ROWS;
+        p.ni = (2 * n) / T + 1;
+        p.nj = (n - 2 + R - 1) / R;
+        auto exists = [&](int i, int j) {
+            if (i < 0 || j < 0 || i >= p.ni || j >= p.nj) return false;
+            for (int r = 1 + R * j; r < 1 + R * (j + 1) && r <= n - 2; ++r)
+                if (std::max(T * i, 2 * r + 1) <= std::min(T * i + T - 1, n - 1 + r)) return true;
+            return false;
+        };
+        struct Tile {
+            int w, face, i, j, has;
+        };
+        std::vector<std::pair<int, int>> cells;
+        for (int j = 0; j < p.nj; ++j)
+            for (int i = 0; i < p.ni; ++i)
+                if (exists(i, j)) cells.push_back({i, j});
+        std::vector<Tile> order;
+        for (int f = 0; f < int(place_.faces.size()); ++f)
+            for (const auto& [i, j] : cells)
+                order.push_back({i + j, f, i, j,
+                                 (exists(i - 1, j) ? 1 : 0) | (exists(i, j - 1) ? 2 : 0) | (exists(i - 1, j - 1) ? 4 : 0)});
+        // dependencies (W, S, SW) have a smaller i + j: dequeued earlier
+        std::sort(order.begin(), order.end(), [](const Tile& a, const Tile& b) {
+            return a.w != b.w ? a.w < b.w : (a.face != b.face ? a.face < b.face : a.i < b.i);
+        });
+        std::vector<int32_t> flat;
+        for (const Tile& t : order) flat.insert(flat.end(), {t.face, t.i, t.j, t.has});
+        p.ntiles = int(order.size());
+        p.tiles = upload_vec(flat, stream_);
+        p.nflags = int64_t(place_.faces.size()) * p.ni * p.nj;
+        p.flags = DevMem(size_t(std::max<int64_t>(p.nflags, 1)) * 4);
+        p.counter = DevMem(16);
+    }
+    return gs_[L] = std::move(p);
+}
 
 void Domain::event_record(int slot) {
     if (slot < 0 || slot >= 16) throw OutOfRange("event slot " + std::to_string(slot));

@@ -188,7 +188,24 @@ class Domain {
 
     const Placement& placement() const { return place_; }
 
+    /// Gauss-Seidel face-tile queue of a level: tiles (face, i, j) ordered by
+    /// wavefront, plus per-tile done flags and the queue counter.
+    struct GsPlan {
+        DevMem tiles, flags, counter;
+        int ntiles = 0, ni = 0, nj = 0;
+        int64_t nflags = 0;
+    };
+    GsPlan& gs_plan(int L);
+
+    /// side stream for work independent of the main stream's next kernel
+    cudaStream_t aux_stream() const { return aux_; }
+    void fork(); // aux stream waits for the main stream
+    void join(); // main stream waits for the aux stream
+
   private:
+    std::map<int, GsPlan> gs_;
+    cudaStream_t aux_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     cudaEvent_t events_[16] = {};
     void build_exchange(LevelGeom& lg, const HostLayout& lay);
 
@@ -212,6 +229,7 @@ class Domain {
 void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t mask);
 void residual(const Operator& A, Function& rhs, Function& x, Function& r, int level);
 void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level);
+void smooth_gs(const Operator& A, Function& rhs, Function& x, int level);
 void diagonal(const Operator& A, Function& d, int level);
 void prolongate(Function& coarse, Function& fine, int coarse_level, uint8_t mask, bool add);
 void restrict_to_coarse(Function& fine, Function& coarse, int coarse_level, uint8_t mask);
@@ -224,7 +242,7 @@ double max_abs(Function& a, int level);
 void upload(Function& f, int level, const double* host, int64_t n, bool global_order, uint8_t mask);
 void download(Function& f, int level, double* host, int64_t n, bool global_order);
 
-enum Smoother : int { SMOOTH_JACOBI = 0 };
+enum Smoother : int { SMOOTH_JACOBI = 0, SMOOTH_GS = 1 };
 
 class Hierarchy {
   public:

@@ -1,0 +1,160 @@
+// Hybrid Gauss-Seidel (reference smooth_gs, src/operators.cpp:423-482):
+// inside every primitive the owned DoFs update in place in lattice order, halo
+// copies stay frozen at their state after the sweep's initial sync. Included
+// by kernels.cu.
+//
+// Faces. Row-major lexicographic order makes x(c, r) depend on the updated
+// W (c-1, r), S (c, r-1), SE (c+1, r-1) and on the old E, N, NW values, so in
+// the skewed coordinates t = c + 2r every dependency has t' < t and r' <= r:
+// points of one t are independent, and each sees exactly the operands it sees
+// in the reference -- results are bitwise the reference's. Tiles are
+// rectangles in (t, r): tile (I, J) = t in [32 I, 32 I + 32), r in
+// [1 + 32 J, 33 + 32 J) (parallelograms in (c, r)); a tile depends only on its
+// W (I-1, J) and S (I, J-1) tiles. One warp owns a tile, lane q owns row
+// r0 + q, and 32 steps over t update up to 32 points each, from a skewed
+// shared-memory copy of the tile plus halo (row r stored from c = 32 I - 2r - 2).
+// Warps take tiles from a global queue ordered by I + J and wait on the done
+// flags of the two predecessors, dequeued earlier, hence running or done: no
+// deadlock. Tile loads bypass L1 (__ldcg): neighbour tiles are written on other
+// SMs.
+#pragma once
+
+constexpr int GS_T = 32;           // t-width of a tile (steps)
+constexpr int GS_R = 32;           // rows per tile (one per lane)
+constexpr int GS_WARPS = 2;        // independent warps per CTA
+constexpr int GS_K = GS_T + 4;     // staged columns per row: kk in [-2, 34)
+constexpr int GS_XS = GS_K + 2;    // padded smem row strides (doubles)
+constexpr int GS_BS = GS_T + 2;
+
+__device__ __forceinline__ void wait_flag(const int* f) {
+    while (*reinterpret_cast<const volatile int*>(f) == 0) __nanosleep(32);
+}
+
+// 16-byte global -> shared copy through L2 (.cg), `bytes` valid, rest zeroed
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const double* __restrict__ b, double* x,
+                                                            const int4* __restrict__ tiles, int ntiles, int ni,
+                                                            int nj, int* flags, int* counter) {
+    // lane = row: padded row strides (16-byte aligned for cp.async) keep the
+    // per-step column reads of 32 different rows at 2-way bank conflicts
+    __shared__ __align__(16) double s_x[GS_WARPS][GS_R + 2][GS_XS];
+    __shared__ __align__(16) double s_b[GS_WARPS][GS_R][GS_BS];
+    const int n = t.n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double(*sx)[GS_XS] = s_x[warp];
+    double(*sb)[GS_BS] = s_b[warp];
+    const int64_t* __restrict__ ro = t.rowoff;
+    for (;;) {
+        int idx = 0;
+        if (lane == 0) idx = atomicAdd(counter, 1);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= ntiles) break;
+        const int4 tl = tiles[idx];
+        // has: bits 0/1/2 = the W (I-1, J), S (I, J-1), SW (I-1, J-1) tiles hold points;
+        // a point's dependencies (t-1, t-2 in rows r, r-1) lie in exactly those
+        const int face = tl.x, ti = tl.y, tj = tl.z, has = tl.w;
+        int* fflags = flags + int64_t(face) * ni * nj;
+        if (lane == 0) {
+            if (has & 1) wait_flag(fflags + tj * ni + (ti - 1));
+            if (has & 2) wait_flag(fflags + (tj - 1) * ni + ti);
+            if (has & 4) wait_flag(fflags + (tj - 1) * ni + (ti - 1));
+            __threadfence();
+        }
+        __syncwarp();
+        const int t0 = ti * GS_T, r0 = 1 + tj * GS_R;
+        const double* xf = x + int64_t(face) * t.face_stride;
+        const double* bf = b + int64_t(face) * t.face_stride;
+        // stage rows r0-1 .. r0+32 (row r holds c = t0 - 2r + kk, kk in
+        // [-2, 34)) and the tile's b with 16-byte cp.async.cg copies (L2 only,
+        // all in flight at once, zero-fill outside the closed triangle)
+        for (int e = lane; e < (GS_R + 2) * (GS_K / 2); e += 32) {
+            const int q = e / (GS_K / 2), o = 2 * (e % (GS_K / 2));
+            const int r = r0 - 1 + q, c = t0 - 2 * r + o - 2; // c is even: 16-byte aligned
+            const int len = r <= n ? n - r : -1;              // last column of row r
+            const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
+            cp_async16(&sx[q][o], bytes ? xf + ro[r] + c : xf, bytes);
+        }
+        for (int e = lane; e < GS_R * (GS_T / 2); e += 32) {
+            const int q = e / (GS_T / 2), o = 2 * (e % (GS_T / 2));
+            const int r = r0 + q, c = t0 - 2 * r + o;
+            const int len = r <= n ? n - r : -1;
+            const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
+            cp_async16(&sb[q][o], bytes ? bf + ro[r] + c : bf, bytes);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        const double* co = t.face_coef + size_t(face) * 8;
+        const double cW = co[0], cNW = co[1], cS = co[2], cC = co[3], cN = co[4], cSE = co[5], cE = co[6], dg = co[7];
+        const double rdg = 1.0 / dg;
+        const int q = lane + 1, r = r0 + lane; // this lane's row
+        for (int kk = 0; kk < GS_T; ++kk) {
+            const int c = t0 + kk - 2 * r;
+            if (r <= n - 2 && c >= 1 && c + r <= n - 1) {
+                const int k = kk + 2; // staged column of (c, r)
+                double acc = 0.0;     // reference term order, in-place operands
+                acc += cW * sx[q][k - 1];
+                acc += cNW * sx[q + 1][k + 1];
+                acc += cS * sx[q - 1][k - 2];
+                acc += cC * sx[q][k];
+                acc += cN * sx[q + 1][k + 2];
+                acc += cSE * sx[q - 1][k - 1];
+                acc += cE * sx[q][k + 1];
+                sx[q][k] = sx[q][k] + div_by(sb[lane][kk] - acc, dg, rdg);
+            }
+            __syncwarp();
+        }
+        double* xw = x + int64_t(face) * t.face_stride;
+        for (int qq = 0; qq < GS_R; ++qq) { // write back row by row (coalesced)
+            const int rr = r0 + qq, c = t0 - 2 * rr + lane;
+            if (rr <= n - 2 && c >= 1 && c + rr <= n - 1) __stcg(xw + ro[rr] + c, sx[qq + 1][lane + 2]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicExch(fflags + tj * ni + ti, 1);
+        }
+    }
+}
+
+// edges: one thread walks its line k = 1..n-1 in place; vertices: one thread
+__global__ void __launch_bounds__(128) k_gs_ev(LevelTables t, FlagTables fl, const double* __restrict__ b,
+                                               double* x) {
+    const int n = t.n;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < t.nedges) {
+        if (fl.edge_flag[i] & 2) return; // DIRICHLET rows are skipped
+        const int64_t off = t.edge_off[i];
+        double* L = x + off;
+        const double* H0 = L + (n + 1);
+        const double* H1 = H0 + n;
+        const double* co = t.edge_coef + size_t(i) * 8;
+        const bool two = t.edge_nf[i] == 2;
+        for (int k = 1; k <= n - 1; ++k) {
+            double acc = 0.0;
+            acc += co[0] * L[k - 1];
+            acc += co[1] * L[k];
+            acc += co[2] * L[k + 1];
+            acc += co[3] * H0[k - 1];
+            acc += co[4] * H0[k];
+            if (two) {
+                acc += co[5] * H1[k - 1];
+                acc += co[6] * H1[k];
+            }
+            L[k] = L[k] + 1.0 * (b[off + k] - acc) / co[7];
+        }
+        return;
+    }
+    const int v = i - t.nedges;
+    if (v >= t.nverts || (fl.vtx_flag[v] & 2)) return;
+    const int64_t off = t.vtx_off[v];
+    const int ne = t.vtx_ne[v];
+    const double* co = t.vtx_coef + t.vtx_coef_off[v];
+    double acc = 0.0;
+    for (int j = 0; j <= ne; ++j) acc += co[j] * x[off + j];
+    x[off] = x[off] + 1.0 * (b[off] - acc) / co[ne + 1];
+}

@@ -138,6 +138,7 @@ inline dim3 face_row_grid(int n_cols, int n_rows, int nfaces) {
 // K7/K8 face transfers: transfer.cuh
 // ---------------------------------------------------------------------------
 #include "transfer.cuh"
+#include "gauss_seidel.cuh"
 
 __global__ void __launch_bounds__(128) k_prolongate_ev(LevelTables tc, LevelTables tf, FlagTables ff,
                                                        const double* __restrict__ xc, double* __restrict__ xf,
@@ -512,6 +513,22 @@ void launch_prolongate(const LevelTables& tc, const LevelTables& tf, const FlagT
         k_prolongate_ev<<<blocks, 128, 0, st>>>(tc, tf, ff, xc, xf, mask, add ? 1 : 0, kb);
         check_launch("prolongate edges/vertices");
     }
+}
+
+void launch_gs_faces(const LevelTables& t, const double* b, double* x, const int4* tiles, int ntiles, int ni, int nj,
+                     int* flags, int* counter, cudaStream_t st) {
+    if (ntiles <= 0) return;
+    int blocks = (ntiles + GS_WARPS - 1) / GS_WARPS;
+    if (blocks > 148 * 8) blocks = 148 * 8; // warps pull tiles from the queue
+    k_gs_faces<<<blocks, GS_WARPS * 32, 0, st>>>(t, b, x, tiles, ntiles, ni, nj, flags, counter);
+    check_launch("gauss-seidel faces");
+}
+
+void launch_gs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st) {
+    const int total = t.nedges + t.nverts;
+    if (total <= 0) return;
+    k_gs_ev<<<(total + 127) / 128, 128, 0, st>>>(t, fl, b, x);
+    check_launch("gauss-seidel edges/vertices");
 }
 
 void launch_restrict(const LevelTables& tc, const LevelTables& tf, const FlagTables& cf, const double* xf, double* xc,

@@ -66,6 +66,14 @@ void launch_prolongate(const LevelTables& coarse, const LevelTables& fine, const
                        const double* xc, double* xf, uint8_t mask, bool add, cudaStream_t st);
 void launch_restrict(const LevelTables& coarse, const LevelTables& fine, const FlagTables& coarse_flags,
                      const double* xf, double* xc, uint8_t mask, cudaStream_t st);
+// hybrid Gauss-Seidel: face tiles (face, I, J, dependency bits) over skewed
+// coordinates (t = c + 2r in GS_TILE_COLS-wide slabs, rows in GS_TILE_ROWS),
+// queue ordered by I + J; per-tile done flags and the queue counter zeroed by
+// the caller; edges/vertices in their own kernel
+constexpr int GS_TILE_COLS = 32, GS_TILE_ROWS = 32;
+void launch_gs_faces(const LevelTables& t, const double* b, double* x, const int4* tiles, int ntiles, int ni, int nj,
+                     int* flags, int* counter, cudaStream_t st);
+void launch_gs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st);
 // dst := alpha*x1 + beta*x2 (op 0), dst += alpha*x1 (op 1), dst := alpha (op 2)
 void launch_blas1(int op, const LevelTables& t, const FlagTables& fl, double alpha, const double* x1, double beta,
                   const double* x2, double* dst, uint8_t mask, cudaStream_t st);

@@ -115,6 +115,32 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
     x.arena(level).swap(next);
 }
 
+// hybrid Gauss-Seidel (reference smooth_gs, src/operators.cpp:423-482): one
+// sync, then every primitive in place in lattice order with frozen halos;
+// faces (wavefront tiles) and edges/vertices are independent, so the latter
+// run on the side stream concurrently.
+void smooth_gs(const Operator& A, Function& rhs, Function& x, int level) {
+    check_op_function(A, rhs, level, "smooth_gs", true);
+    check_op_function(A, x, level, "smooth_gs", true);
+    if (&rhs == &x) throw InvalidArgument("smooth_gs: rhs and x must be distinct functions");
+    check_diagonals(A, x, level, "smooth_gs");
+    Domain& d = A.domain();
+    d.sync(x, level);
+    const LevelTables t = A.tables(level);
+    Domain::GsPlan& gp = d.gs_plan(level);
+    d.fork();
+    launch_gs_ev(t, x.flags(), rhs.data(level), x.data(level), d.aux_stream());
+    if (gp.ntiles > 0) {
+        HYB_CUDA(cudaMemsetAsync(gp.flags.as<void>(), 0, size_t(gp.nflags) * 4, d.stream()));
+        HYB_CUDA(cudaMemsetAsync(gp.counter.as<void>(), 0, 16, d.stream()));
+        d.timer_begin("gauss_seidel");
+        launch_gs_faces(t, rhs.data(level), x.data(level), gp.tiles.as<int4>(), gp.ntiles, gp.ni, gp.nj,
+                        gp.flags.as<int>(), gp.counter.as<int>(), d.stream());
+        d.timer_end();
+    }
+    d.join();
+}
+
 void diagonal(const Operator& A, Function& dst, int level) {
     check_op_function(A, dst, level, "diagonal", true);
     Domain& d = A.domain();
@@ -300,7 +326,7 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
       omega_(omega), coarse_tol_(coarse_tol), coarse_max_iter_(coarse_max_iter) {
     if (min_level < 0 || min_level > max_level)
         throw InvalidArgument("GridHierarchy: need 0 <= min_level <= max_level");
-    if (smoother != SMOOTH_JACOBI) throw InvalidArgument("GridHierarchy: unknown smoother");
+    if (smoother != SMOOTH_JACOBI && smoother != SMOOTH_GS) throw InvalidArgument("GridHierarchy: unknown smoother");
     // min-level system: every rank holds the whole (small) constrained matrix
     const HostCsr csr = assemble_constrained(d.graph(), form, min_level, bc);
     if (coarse_max_iter_ < 0) coarse_max_iter_ = int(csr.n) + 100; // reference src/solvers.cpp:437
@@ -322,7 +348,10 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
     HYB_CUDA(cudaMemsetAsync(coarse_.status.as<void>(), 0, sizeof(CoarseStatus), d.stream()));
 }
 
-void Hierarchy::smooth(Function& rhs, Function& x, int level) { smooth_jacobi(a_, rhs, x, omega_, level); }
+void Hierarchy::smooth(Function& rhs, Function& x, int level) {
+    if (smoother_ == SMOOTH_GS) smooth_gs(a_, rhs, x, level); // the reference's own choice (solvers.cpp:417, 427)
+    else smooth_jacobi(a_, rhs, x, omega_, level);
+}
 
 void Hierarchy::vcycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
     if (level < a_.min_level() || level > a_.max_level())
@@ -355,7 +384,8 @@ std::vector<const void*> Hierarchy::graph_key(Function& rhs, Function& x, int le
 // captures the whole cycle (kernels, copies, NCCL) and later calls replay it.
 void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
     Domain& d = *dom_;
-    if (!use_graphs || (nu_pre + nu_post) % 2 != 0 || d.profiling) {
+    const bool swaps_restore = smoother_ != SMOOTH_JACOBI || (nu_pre + nu_post) % 2 == 0; // GS works in place
+    if (!use_graphs || !swaps_restore || d.profiling) {
         cycle(rhs, x, level, nu_pre, nu_post);
         check_coarse();
         return;

@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from ._lib import (CudaError, HybError, HybRuntimeError, InvalidArgument, LogicError, NcclError,  # noqa: F401
-                   OutOfRange, check, lib)
+                   OutOfRange, alive, check, lib)
 
 INNER = 1
 DIRICHLET = 2
@@ -35,7 +35,7 @@ SMOOTH_MASK = INNER | NEUMANN
 LAPLACE = 0
 MASS = 1
 
-SMOOTHERS = {"jacobi": 0}
+SMOOTHERS = {"jacobi": 0, "gs": 1}
 
 
 def _pd(a: np.ndarray):
@@ -135,7 +135,7 @@ class ExchangePlan:
          self.n_recvs) = list(s)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and alive():
             lib.hyb_plan_destroy(self._h)
             self._h = None
 
@@ -181,7 +181,7 @@ class DistributedDomain:
         self.local_ranks = lr
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and alive():
             lib.hyb_domain_destroy(self._h)
             self._h = None
 
@@ -265,7 +265,7 @@ class ScalarFunction:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and alive():
             lib.hyb_function_destroy(self._h)
             self._h = None
 
@@ -307,7 +307,7 @@ class StencilOperator:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and alive():
             lib.hyb_operator_destroy(self._h)
             self._h = None
 
@@ -348,6 +348,12 @@ def apply(A: StencilOperator, ctl: Controller, src: ScalarFunction, dst: ScalarF
 def residual(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: ScalarFunction,  # noqa: ARG001
              r: ScalarFunction, level: int) -> None:
     check(lib.hyb_residual(A._h, rhs._h, x._h, r._h, level))
+
+
+def smooth_gs(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: ScalarFunction,  # noqa: ARG001
+              level: int) -> None:
+    """Hybrid Gauss-Seidel (reference smooth_gs), bitwise the reference's."""
+    check(lib.hyb_smooth_gs(A._h, rhs._h, x._h, level))
 
 
 def smooth_jacobi(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: ScalarFunction,  # noqa: ARG001
@@ -441,7 +447,7 @@ class GridHierarchy:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and alive():
             lib.hyb_hierarchy_destroy(self._h)
             self._h = None
 
@@ -479,6 +485,6 @@ class PinnedBuffer:
         self.array = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=(n_doubles,))
 
     def __del__(self):
-        if getattr(self, "_p", None):
+        if getattr(self, "_p", None) and alive():
             lib.hyb_host_free(self._p)
             self._p = None
