@@ -44,7 +44,7 @@ enum hyb_status {
 enum hyb_flag { HYB_INNER = 1, HYB_DIRICHLET = 2, HYB_NEUMANN = 4, HYB_ALL_FLAGS = 7 };
 /* forms (include/hytegrid/elements.hpp:17-25; P1 LAPLACE and MASS) */
 enum hyb_form { HYB_LAPLACE = 0, HYB_MASS = 1 };
-enum hyb_smoother { HYB_SMOOTH_JACOBI = 0 };
+enum hyb_smoother { HYB_SMOOTH_JACOBI = 0, HYB_SMOOTH_GS = 1, HYB_SMOOTH_COLORED_GS = 2 };
 enum hyb_partitioner { HYB_PARTITION_ROUND_ROBIN = 0, HYB_PARTITION_GREEDY_EDGECUT = 1 };
 
 typedef struct hyb_domain hyb_domain;       /* DistributedDomain + Controller */
@@ -171,6 +171,10 @@ int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, doubl
  * each primitive, halos frozen after the initial sync (operators.hpp:120-121);
  * bitwise the reference's (wavefront over t = c + 2r on faces) */
 int hyb_smooth_gs(hyb_operator* A, hyb_function* rhs, hyb_function* x, int level);
+/* coloured hybrid Gauss-Seidel (configuration 3; the reference has none):
+ * smooth_gs's structure with faces swept in colours (c + 2r) mod 3 = 0, 1, 2
+ * and edge lines odd k then even k (oracle: og_cgs in oracle/hyteg_oracle.c) */
+int hyb_smooth_cgs(hyb_operator* A, hyb_function* rhs, hyb_function* x, int level);
 /* diagonal(A, d, level)                           operators.hpp:125 */
 int hyb_diagonal(hyb_operator* A, hyb_function* d, int level);
 /* prolongate(ctl, coarse, fine, coarse_level, mask) solvers.hpp:26-27 */

@@ -723,6 +723,22 @@ static int smooth(og_session* s, int rhs, int x, double omega, int level, int ja
             const double diag = row_diag(s, level, id);
             int64_t np_ = 0;
             int bad = 0;
+            if (jacobi == 2) {
+                /* coloured GS (no reference counterpart): same row update, in place,
+                 * faces in colours (c + 2r) mod 3 = 0, 1, 2, edge lines odd k then
+                 * even k; each class is an independent set, so the in-class order
+                 * does not matter */
+                const int k_ = kind_of(s, id);
+                const int ncol = k_ == 2 ? 3 : (k_ == 1 ? 2 : 1);
+                for (int col = 0; col < ncol; ++col)
+                    FOR_ROWS(s, id, level, slot, c, r, {
+                        if (k_ == 2 && (c + 2 * r) % 3 != col) continue;
+                        if (k_ == 1 && (int)(slot % 2) != 1 - col) continue;
+                        if (diag == 0.0) { bad = 1; continue; }
+                        const double acc = row_acc(s, level, id, slot, xv, c, r);
+                        xv[slot] = xv[slot] + omega * (rv[slot] - acc) / diag;
+                    });
+            } else
             FOR_ROWS(s, id, level, slot, c, r, {
                 if (diag == 0.0) { bad = 1; continue; }
                 const double acc = row_acc(s, level, id, slot, xv, c, r);
@@ -731,7 +747,7 @@ static int smooth(og_session* s, int rhs, int x, double omega, int level, int ja
                 else xv[slot] = upd;
             });
             if (bad) { free(pending); return fail("smooth: zero diagonal entry"); }
-            if (jacobi) {
+            if (jacobi == 1) {
                 int64_t q = 0;
                 FOR_OWNED(s, id, level, slot, { xv[slot] = pending[q++]; });
             }
@@ -741,6 +757,7 @@ static int smooth(og_session* s, int rhs, int x, double omega, int level, int ja
 }
 int og_jacobi(og_session* s, int rhs, int x, double omega, int level) { return smooth(s, rhs, x, omega, level, 1); }
 int og_gs(og_session* s, int rhs, int x, int level) { return smooth(s, rhs, x, 1.0, level, 0); }
+int og_cgs(og_session* s, int rhs, int x, int level) { return smooth(s, rhs, x, 1.0, level, 2); }
 
 /* restrict_to_coarse (src/solvers.cpp:131-204) */
 int og_restrict(og_session* s, int fine, int coarse, int lc, int mask) {
@@ -861,7 +878,13 @@ typedef struct {
     og_session* s;
     int R, B, E, P, AP, lmin, nu1, nu2;
     double omega, tol;
+    int smoother; /* 0 weighted Jacobi, 1 hybrid GS, 2 coloured GS */
 } Cyc;
+
+static int cyc_smooth(Cyc* c, int rhs, int x, int L) {
+    return c->smoother == 1 ? og_gs(c->s, rhs, x, L)
+                            : (c->smoother == 2 ? og_cgs(c->s, rhs, x, L) : og_jacobi(c->s, rhs, x, c->omega, L));
+}
 
 static int matvec(Cyc* c, const double* v, double* out) {
     og_set(c->s, c->P, c->lmin, v);
@@ -910,7 +933,7 @@ static int cycle(Cyc* c, int rhs, int x, int L) {
     if (og_assign(s, 1.0, rhs, 0.0, rhs, x, L, F_DIRICHLET)) return 1;
     if (L == c->lmin) return coarse(c, rhs, x);
     for (int i = 0; i < c->nu1; ++i)
-        if (og_jacobi(s, rhs, x, c->omega, L)) return 1;
+        if (cyc_smooth(c, rhs, x, L)) return 1;
     if (og_residual(s, rhs, x, c->R, L)) return 1;
     if (og_restrict(s, c->R, c->B, L - 1, 7)) return 1;
     og_assign(s, 0.0, c->B, 0.0, c->B, c->B, L - 1, F_DIRICHLET); /* interpolate(b, 0, DIRICHLET) */
@@ -919,15 +942,15 @@ static int cycle(Cyc* c, int rhs, int x, int L) {
     if (og_prolongate(s, c->E, c->R, L - 1, F_INNER | F_NEUMANN)) return 1;
     if (og_add_scaled(s, x, 1.0, c->R, L, F_INNER | F_NEUMANN)) return 1;
     for (int i = 0; i < c->nu2; ++i)
-        if (og_jacobi(s, rhs, x, c->omega, L)) return 1;
+        if (cyc_smooth(c, rhs, x, L)) return 1;
     return 0;
 }
 
-int og_vcycle_jacobi(og_session* s, int rhs, int x, int level, int nu1, int nu2, double omega, double coarse_tol,
-                     int ncycles, double* residuals) {
+int og_vcycle(og_session* s, int rhs, int x, int level, int smoother, int nu1, int nu2, double omega,
+              double coarse_tol, int ncycles, double* residuals) {
     if (s->nfun < 7) return fail("vcycle needs nfuncs >= 7 (last five are scratch)");
     Cyc c = {s, s->nfun - 5, s->nfun - 4, s->nfun - 3, s->nfun - 2, s->nfun - 1, s->lmin, nu1, nu2, omega,
-             coarse_tol};
+             coarse_tol, smoother};
     double d;
     if (og_residual(s, rhs, x, c.R, level) || og_dot(s, c.R, c.R, level, &d)) return 1;
     residuals[0] = sqrt(d);
@@ -937,4 +960,9 @@ int og_vcycle_jacobi(og_session* s, int rhs, int x, int level, int nu1, int nu2,
         residuals[k + 1] = sqrt(d);
     }
     return 0;
+}
+
+int og_vcycle_jacobi(og_session* s, int rhs, int x, int level, int nu1, int nu2, double omega, double coarse_tol,
+                     int ncycles, double* residuals) {
+    return og_vcycle(s, rhs, x, level, 0, nu1, nu2, omega, coarse_tol, ncycles, residuals);
 }

@@ -36,11 +36,16 @@ int og_apply(og_session* s, int src, int dst, int level, int mask);
 int og_residual(og_session* s, int rhs, int x, int r, int level);
 int og_jacobi(og_session* s, int rhs, int x, double omega, int level);
 int og_gs(og_session* s, int rhs, int x, int level);
+/* coloured hybrid GS: faces by (c + 2r) mod 3, edges odd then even k (no reference counterpart) */
+int og_cgs(og_session* s, int rhs, int x, int level);
 int og_restrict(og_session* s, int fine, int coarse, int lc, int mask);
 int og_prolongate(og_session* s, int coarse, int fine, int lc, int mask);
 int og_assign(og_session* s, double alpha, int x1, double beta, int x2, int dst, int level, int mask);
 int og_add_scaled(og_session* s, int dst, double gamma, int y, int level, int mask);
 int og_dot(og_session* s, int a, int b, int level, double* out);
+/* smoother 0 weighted Jacobi (omega), 1 hybrid GS, 2 coloured GS */
+int og_vcycle(og_session* s, int rhs, int x, int level, int smoother, int nu1, int nu2, double omega,
+              double coarse_tol, int ncycles, double* residuals);
 int og_vcycle_jacobi(og_session* s, int rhs, int x, int level, int nu1, int nu2, double omega, double coarse_tol,
                      int ncycles, double* residuals);
 

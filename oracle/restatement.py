@@ -38,6 +38,8 @@ def lib():
             "og_residual": (i, [p, i, i, i, i]),
             "og_jacobi": (i, [p, i, i, d, i]),
             "og_gs": (i, [p, i, i, i]),
+            "og_cgs": (i, [p, i, i, i]),
+            "og_vcycle": (i, [p, i, i, i, i, i, i, d, d, i, pd]),
             "og_restrict": (i, [p, i, i, i, i]),
             "og_prolongate": (i, [p, i, i, i, i]),
             "og_assign": (i, [p, d, i, d, i, i, i, i]),
@@ -120,6 +122,14 @@ class Session:
 
     def gs(self, rhs, x, level):
         _ck(lib().og_gs(self.h, rhs, x, level))
+
+    def cgs(self, rhs, x, level):
+        _ck(lib().og_cgs(self.h, rhs, x, level))
+
+    def vcycle(self, rhs, x, level, smoother, nu1, nu2, omega, coarse_tol, ncycles):
+        res = np.zeros(ncycles + 1)
+        _ck(lib().og_vcycle(self.h, rhs, x, level, smoother, nu1, nu2, omega, coarse_tol, ncycles, _pd(res)))
+        return res
 
     def restrict(self, fine, coarse, lc, mask=7):
         _ck(lib().og_restrict(self.h, fine, coarse, lc, mask))

@@ -106,6 +106,7 @@ _SIGS = {
     "hyb_residual": (_i, [_p, _p, _p, _p, _i]),
     "hyb_smooth_jacobi": (_i, [_p, _p, _p, _d, _i]),
     "hyb_smooth_gs": (_i, [_p, _p, _p, _i]),
+    "hyb_smooth_cgs": (_i, [_p, _p, _p, _i]),
     "hyb_diagonal": (_i, [_p, _p, _i]),
     "hyb_prolongate": (_i, [_p, _p, _i, _u8]),
     "hyb_prolongate_add": (_i, [_p, _p, _i, _u8]),

@@ -544,6 +544,15 @@ int hyb_smooth_gs(hyb_operator* A, hyb_function* rhs, hyb_function* x, int level
     });
 }
 
+int hyb_smooth_cgs(hyb_operator* A, hyb_function* rhs, hyb_function* x, int level) {
+    return guarded([&] {
+        need(A, "hyb_smooth_cgs");
+        need(rhs, "hyb_smooth_cgs");
+        need(x, "hyb_smooth_cgs");
+        hyb::smooth_cgs(*A->a, *rhs->f, *x->f, level);
+    });
+}
+
 int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level) {
     return guarded([&] {
         need(A, "hyb_smooth_jacobi");

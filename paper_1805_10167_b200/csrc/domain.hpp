@@ -230,6 +230,7 @@ void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t m
 void residual(const Operator& A, Function& rhs, Function& x, Function& r, int level);
 void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level);
 void smooth_gs(const Operator& A, Function& rhs, Function& x, int level);
+void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level);
 void diagonal(const Operator& A, Function& d, int level);
 void prolongate(Function& coarse, Function& fine, int coarse_level, uint8_t mask, bool add);
 void restrict_to_coarse(Function& fine, Function& coarse, int coarse_level, uint8_t mask);
@@ -242,7 +243,7 @@ double max_abs(Function& a, int level);
 void upload(Function& f, int level, const double* host, int64_t n, bool global_order, uint8_t mask);
 void download(Function& f, int level, double* host, int64_t n, bool global_order);
 
-enum Smoother : int { SMOOTH_JACOBI = 0, SMOOTH_GS = 1 };
+enum Smoother : int { SMOOTH_JACOBI = 0, SMOOTH_GS = 1, SMOOTH_CGS = 2 };
 
 class Hierarchy {
   public:

@@ -121,6 +121,65 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
     }
 }
 
+// ---------------------------------------------------------------------------
+// Coloured hybrid Gauss-Seidel (configuration 3; absent from the reference):
+// the reference's smooth() structure -- one sync, frozen halos, DIRICHLET rows
+// skipped, upd = x + (b - Ax)/diag -- with a colour order inside primitives:
+// face points by (c + 2r) mod 3 = 0, 1, 2 (every 7-point neighbour differs by
+// +-1 or +-2, so each class is an independent set; red-black is not, the
+// stencil graph has triangles), edge lines odd k then even k. Restated in
+// oracle/hyteg_oracle.c (og_cgs).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_cgs_faces(LevelTables t, const double* __restrict__ b, double* x,
+                                                   int color) {
+    const int n = t.n;
+    const int r = 1 + blockIdx.y;
+    if (r > n - 2) return;
+    const int cs = ((color - 2 * r) % 3 + 3) % 3; // first column of this colour (c >= 0)
+    const int c = cs + 3 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (c < 1 || c > n - 1 - r) return;
+    const int64_t base = int64_t(blockIdx.z) * t.face_stride;
+    double* xf = x + base;
+    const int64_t* ro = t.rowoff;
+    const double* rm = xf + ro[r - 1];
+    double* r0 = xf + ro[r];
+    const double* rp = xf + ro[r + 1];
+    const double* co = t.face_coef + size_t(blockIdx.z) * 8;
+    double acc = 0.0;
+    acc += co[0] * r0[c - 1];
+    acc += co[1] * rp[c - 1];
+    acc += co[2] * rm[c];
+    acc += co[3] * r0[c];
+    acc += co[4] * rp[c];
+    acc += co[5] * rm[c + 1];
+    acc += co[6] * r0[c + 1];
+    r0[c] = r0[c] + div_by(b[base + ro[r] + c] - acc, co[7], 1.0 / co[7]);
+}
+
+// edges: colour 1 = odd k, colour 0 = even k, one thread per line DoF
+__global__ void __launch_bounds__(128) k_cgs_edges(LevelTables t, FlagTables fl, const double* __restrict__ b,
+                                                   double* x, int parity, int kblocks) {
+    const int n = t.n;
+    const int e = blockIdx.x / kblocks;
+    const int k = 2 * ((blockIdx.x % kblocks) * blockDim.x + threadIdx.x) + parity;
+    if (e >= t.nedges || k < 1 || k > n - 1 || (fl.edge_flag[e] & 2)) return;
+    const int64_t off = t.edge_off[e];
+    double* L = x + off;
+    const double* H0 = L + (n + 1);
+    const double* co = t.edge_coef + size_t(e) * 8;
+    double acc = 0.0;
+    acc += co[0] * L[k - 1];
+    acc += co[1] * L[k];
+    acc += co[2] * L[k + 1];
+    acc += co[3] * H0[k - 1];
+    acc += co[4] * H0[k];
+    if (t.edge_nf[e] == 2) {
+        acc += co[5] * H0[n + k - 1];
+        acc += co[6] * H0[n + k];
+    }
+    L[k] = L[k] + 1.0 * (b[off + k] - acc) / co[7];
+}
+
 // edges: one thread walks its line k = 1..n-1 in place; vertices: one thread
 __global__ void __launch_bounds__(128) k_gs_ev(LevelTables t, FlagTables fl, const double* __restrict__ b,
                                                double* x) {

@@ -524,6 +524,30 @@ void launch_gs_faces(const LevelTables& t, const double* b, double* x, const int
     check_launch("gauss-seidel faces");
 }
 
+void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
+    if (t.nfaces <= 0 || t.n < 3) return;
+    for (int color = 0; color < 3; ++color) {
+        const dim3 grid(unsigned(((t.n - 1) / 3 + 1 + 127) / 128), unsigned(t.n - 2), unsigned(t.nfaces));
+        k_cgs_faces<<<grid, 128, 0, st>>>(t, b, x, color);
+        check_launch("coloured gauss-seidel faces");
+    }
+}
+
+void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st) {
+    LevelTables tv = t; // vertices: the sequential GS kernel with no edges
+    tv.nedges = 0;
+    if (t.nverts > 0) {
+        k_gs_ev<<<(t.nverts + 127) / 128, 128, 0, st>>>(tv, fl, b, x);
+        check_launch("coloured gauss-seidel vertices");
+    }
+    const int kb = t.n - 1 > 0 ? (t.n / 2 + 127) / 128 : 0;
+    if (t.nedges > 0 && kb > 0)
+        for (int parity = 1; parity >= 0; --parity) { // odd k first, then even k
+            k_cgs_edges<<<t.nedges * kb, 128, 0, st>>>(t, fl, b, x, parity, kb);
+            check_launch("coloured gauss-seidel edges");
+        }
+}
+
 void launch_gs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st) {
     const int total = t.nedges + t.nverts;
     if (total <= 0) return;

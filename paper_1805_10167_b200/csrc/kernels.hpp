@@ -74,6 +74,10 @@ constexpr int GS_TILE_COLS = 32, GS_TILE_ROWS = 32;
 void launch_gs_faces(const LevelTables& t, const double* b, double* x, const int4* tiles, int ntiles, int ni, int nj,
                      int* flags, int* counter, cudaStream_t st);
 void launch_gs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st);
+// coloured hybrid Gauss-Seidel: faces in colours (c + 2r) mod 3, edge lines
+// odd/even k, vertices as in launch_gs_ev
+void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st);
+void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st);
 // dst := alpha*x1 + beta*x2 (op 0), dst += alpha*x1 (op 1), dst := alpha (op 2)
 void launch_blas1(int op, const LevelTables& t, const FlagTables& fl, double alpha, const double* x1, double beta,
                   const double* x2, double* dst, uint8_t mask, cudaStream_t st);

@@ -141,6 +141,23 @@ void smooth_gs(const Operator& A, Function& rhs, Function& x, int level) {
     d.join();
 }
 
+// coloured hybrid Gauss-Seidel (configuration 3, see gauss_seidel.cuh)
+void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level) {
+    check_op_function(A, rhs, level, "smooth_cgs", true);
+    check_op_function(A, x, level, "smooth_cgs", true);
+    if (&rhs == &x) throw InvalidArgument("smooth_cgs: rhs and x must be distinct functions");
+    check_diagonals(A, x, level, "smooth_cgs");
+    Domain& d = A.domain();
+    d.sync(x, level);
+    const LevelTables t = A.tables(level);
+    d.fork();
+    launch_cgs_ev(t, x.flags(), rhs.data(level), x.data(level), d.aux_stream());
+    d.timer_begin("coloured_gs");
+    launch_cgs_faces(t, rhs.data(level), x.data(level), d.stream());
+    d.timer_end();
+    d.join();
+}
+
 void diagonal(const Operator& A, Function& dst, int level) {
     check_op_function(A, dst, level, "diagonal", true);
     Domain& d = A.domain();
@@ -326,7 +343,8 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
       omega_(omega), coarse_tol_(coarse_tol), coarse_max_iter_(coarse_max_iter) {
     if (min_level < 0 || min_level > max_level)
         throw InvalidArgument("GridHierarchy: need 0 <= min_level <= max_level");
-    if (smoother != SMOOTH_JACOBI && smoother != SMOOTH_GS) throw InvalidArgument("GridHierarchy: unknown smoother");
+    if (smoother != SMOOTH_JACOBI && smoother != SMOOTH_GS && smoother != SMOOTH_CGS)
+        throw InvalidArgument("GridHierarchy: unknown smoother");
     // min-level system: every rank holds the whole (small) constrained matrix
     const HostCsr csr = assemble_constrained(d.graph(), form, min_level, bc);
     if (coarse_max_iter_ < 0) coarse_max_iter_ = int(csr.n) + 100; // reference src/solvers.cpp:437
@@ -350,6 +368,7 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
 
 void Hierarchy::smooth(Function& rhs, Function& x, int level) {
     if (smoother_ == SMOOTH_GS) smooth_gs(a_, rhs, x, level); // the reference's own choice (solvers.cpp:417, 427)
+    else if (smoother_ == SMOOTH_CGS) smooth_cgs(a_, rhs, x, level);
     else smooth_jacobi(a_, rhs, x, omega_, level);
 }
 

@@ -35,7 +35,7 @@ SMOOTH_MASK = INNER | NEUMANN
 LAPLACE = 0
 MASS = 1
 
-SMOOTHERS = {"jacobi": 0, "gs": 1}
+SMOOTHERS = {"jacobi": 0, "gs": 1, "colored_gs": 2}
 
 
 def _pd(a: np.ndarray):
@@ -354,6 +354,12 @@ def smooth_gs(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: Scala
               level: int) -> None:
     """Hybrid Gauss-Seidel (reference smooth_gs), bitwise the reference's."""
     check(lib.hyb_smooth_gs(A._h, rhs._h, x._h, level))
+
+
+def smooth_colored_gs(A: StencilOperator, ctl: Controller, rhs: ScalarFunction,  # noqa: ARG001
+                      x: ScalarFunction, level: int) -> None:
+    """Coloured hybrid Gauss-Seidel: faces by (c + 2r) mod 3, edges odd/even k."""
+    check(lib.hyb_smooth_cgs(A._h, rhs._h, x._h, level))
 
 
 def smooth_jacobi(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: ScalarFunction,  # noqa: ARG001
