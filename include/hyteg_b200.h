@@ -208,6 +208,22 @@ int hyb_hierarchy_residual_norm(hyb_hierarchy* h, hyb_function* rhs, hyb_functio
 /* residuals[0..*n_out): ||rhs - A x|| before each cycle and after the last */
 int hyb_hierarchy_solve(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, double tol, int max_cycles,
                         int nu_pre, int nu_post, double* residuals, int* n_out, int* converged);
+/* Full multigrid (no reference counterpart; configuration 4): rhs is given at
+ * `level` and overwritten below it by restriction (DIRICHLET rows zeroed); x
+ * is solved level by level from min_level (one cycle there, then prolongation
+ * + cycles_per_level cycles per finer level), then cycled at `level` until
+ * ||r|| <= tol * ||r(x = 0)||. rhs and x must cover [min_level, level].
+ * residuals: [0] = ||r(x = 0)||, [1] after the FMG sweep, then one per cycle
+ * (capacity >= max_cycles + 2). */
+int hyb_hierarchy_fmg(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, int cycles_per_level,
+                      int nu_pre, int nu_post, double tol, int max_cycles, double* residuals, int* n_out,
+                      int* converged);
+/* CG (the recurrence of cg_solve, src/solvers.cpp:226-259) preconditioned by
+ * one V(nu_pre, nu_post) cycle from zero (configuration 5). x starts at 0;
+ * stops after max_iter iterations or at ||r|| <= tol * ||r0||. residuals has
+ * capacity max_iter + 1. rhs and x need only `level`. */
+int hyb_hierarchy_pcg(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, int max_iter, int nu_pre,
+                      int nu_post, double tol, double* residuals, int* n_out, int* converged);
 
 /* ---- pinned host memory (end-to-end transfers) ---- */
 int hyb_host_alloc(int64_t bytes, void** out);

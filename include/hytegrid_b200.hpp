@@ -266,6 +266,32 @@ class GridHierarchy {
         rep.converged = conv != 0;
         return rep;
     }
+    /// full multigrid (rhs coarser levels are overwritten), see hyb_hierarchy_fmg
+    SolveReport fmg(ScalarFunction& rhs, ScalarFunction& x, int level, double tol, int max_cycles, int nu_pre = 2,
+                    int nu_post = 2, int cycles_per_level = 1) {
+        SolveReport rep;
+        rep.residuals.resize(size_t(max_cycles) + 2);
+        int n = 0, conv = 0;
+        check(hyb_hierarchy_fmg(h_, rhs.handle(), x.handle(), level, cycles_per_level, nu_pre, nu_post, tol,
+                                max_cycles, rep.residuals.data(), &n, &conv));
+        rep.residuals.resize(size_t(n));
+        rep.iterations = n - 2;
+        rep.converged = conv != 0;
+        return rep;
+    }
+    /// V-cycle preconditioned CG from x = 0, see hyb_hierarchy_pcg
+    SolveReport pcg(const ScalarFunction& rhs, ScalarFunction& x, int level, int max_iter, double tol = 0.0,
+                    int nu_pre = 1, int nu_post = 1) {
+        SolveReport rep;
+        rep.residuals.resize(size_t(max_iter) + 1);
+        int n = 0, conv = 0;
+        check(hyb_hierarchy_pcg(h_, rhs.handle(), x.handle(), level, max_iter, nu_pre, nu_post, tol,
+                                rep.residuals.data(), &n, &conv));
+        rep.residuals.resize(size_t(n));
+        rep.iterations = n - 1;
+        rep.converged = conv != 0;
+        return rep;
+    }
 
   private:
     hyb_hierarchy* h_ = nullptr;

@@ -966,3 +966,91 @@ int og_vcycle_jacobi(og_session* s, int rhs, int x, int level, int nu1, int nu2,
                      int ncycles, double* residuals) {
     return og_vcycle(s, rhs, x, level, 0, nu1, nu2, omega, coarse_tol, ncycles, residuals);
 }
+
+/* ------------------------------------------------------------------ FMG
+ * Full multigrid (configuration 4; the reference has none, FMG is a SPEC
+ * non-goal): the level hierarchy of rhs by restriction (DIRICHLET rows zeroed
+ * as the V-cycle does for corrections), the min-level solve by one cycle, then
+ * per finer level: x := P x_coarse on the smooth mask and `per_level` cycles;
+ * then cycles at `level` until ||r|| <= tol ||r(x = 0)||. residuals[0] is
+ * ||r(x = 0)||, [1] after the FMG sweep, then one per cycle; *n_out entries. */
+static double resnorm(Cyc* c, int rhs, int x, int L) {
+    double d = 0;
+    og_residual(c->s, rhs, x, c->R, L);
+    og_dot(c->s, c->R, c->R, L, &d);
+    return sqrt(d);
+}
+
+int og_fmg(og_session* s, int rhs, int x, int level, int smoother, int nu1, int nu2, double omega, double coarse_tol,
+           int per_level, double tol, int max_cycles, double* residuals, int* n_out) {
+    if (s->nfun < 7) return fail("fmg needs nfuncs >= 7 (last five are scratch)");
+    Cyc c = {s, s->nfun - 5, s->nfun - 4, s->nfun - 3, s->nfun - 2, s->nfun - 1, s->lmin, nu1, nu2, omega,
+             coarse_tol, smoother};
+    for (int l = level; l > s->lmin; --l) {
+        if (og_restrict(s, rhs, rhs, l - 1, 7)) return 1;
+        og_assign(s, 0.0, rhs, 0.0, rhs, rhs, l - 1, F_DIRICHLET);
+    }
+    og_assign(s, 0.0, x, 0.0, x, x, level, 7);
+    const double r0 = resnorm(&c, rhs, x, level);
+    int k = 0;
+    residuals[k++] = r0;
+    og_assign(s, 0.0, x, 0.0, x, x, s->lmin, 7);
+    if (cycle(&c, rhs, x, s->lmin)) return 1;
+    for (int l = s->lmin + 1; l <= level; ++l) {
+        og_assign(s, 0.0, x, 0.0, x, x, l, 7);
+        if (og_prolongate(s, x, x, l - 1, F_INNER | F_NEUMANN)) return 1;
+        for (int i = 0; i < per_level; ++i)
+            if (cycle(&c, rhs, x, l)) return 1;
+    }
+    residuals[k++] = resnorm(&c, rhs, x, level);
+    const double target = tol * r0;
+    for (int it = 0; it < max_cycles && residuals[k - 1] > target; ++it) {
+        if (cycle(&c, rhs, x, level)) return 1;
+        residuals[k++] = resnorm(&c, rhs, x, level);
+    }
+    *n_out = k;
+    return 0;
+}
+
+/* ------------------------------------------------------------------ PCG
+ * Configuration 5: cg_solve's recurrence (src/solvers.cpp:226-259) with the
+ * matrix replaced by apply, vec_dot by dot, and z = one V(nu1, nu2) cycle on
+ * A z = r from z = 0 as the preconditioner (symmetric for Jacobi pre/post
+ * smoothing with R = P^T). Scratch: functions nfun-9 .. nfun-6 hold r, z, p,
+ * Ap, the last five are the cycle's. residuals[k] = ||r_k||, k = 0..iters. */
+int og_pcg(og_session* s, int rhs, int x, int level, int nu1, int nu2, double omega, double coarse_tol, int iters,
+           double* residuals) {
+    if (s->nfun < 11) return fail("pcg needs nfuncs >= 11 (last nine are scratch)");
+    Cyc c = {s, s->nfun - 5, s->nfun - 4, s->nfun - 3, s->nfun - 2, s->nfun - 1, s->lmin, nu1, nu2, omega,
+             coarse_tol, 0};
+    const int PR = s->nfun - 9, PZ = s->nfun - 8, PP = s->nfun - 7, PAP = s->nfun - 6;
+    double d;
+    og_assign(s, 0.0, x, 0.0, x, x, level, 7);
+    og_residual(s, rhs, x, PR, level);
+    og_dot(s, PR, PR, level, &d);
+    residuals[0] = sqrt(d);
+    og_assign(s, 0.0, PZ, 0.0, PZ, PZ, level, 7);
+    if (cycle(&c, PR, PZ, level)) return 1;
+    og_assign(s, 1.0, PZ, 0.0, PZ, PP, level, 7);
+    double rz;
+    og_dot(s, PR, PZ, level, &rz);
+    for (int k = 0; k < iters; ++k) {
+        og_apply(s, PP, PAP, level, 7);
+        double pap;
+        og_dot(s, PP, PAP, level, &pap);
+        if (pap <= 0.0) return fail("pcg: non-positive curvature");
+        const double alpha = rz / pap;
+        og_add_scaled(s, x, alpha, PP, level, 7);
+        og_add_scaled(s, PR, -alpha, PAP, level, 7);
+        og_assign(s, 0.0, PZ, 0.0, PZ, PZ, level, 7);
+        if (cycle(&c, PR, PZ, level)) return 1;
+        double rz_new;
+        og_dot(s, PR, PZ, level, &rz_new);
+        const double beta = rz_new / rz;
+        og_assign(s, 1.0, PZ, beta, PP, PP, level, 7);
+        rz = rz_new;
+        og_dot(s, PR, PR, level, &d);
+        residuals[k + 1] = sqrt(d);
+    }
+    return 0;
+}

@@ -48,6 +48,12 @@ int og_vcycle(og_session* s, int rhs, int x, int level, int smoother, int nu1, i
               double coarse_tol, int ncycles, double* residuals);
 int og_vcycle_jacobi(og_session* s, int rhs, int x, int level, int nu1, int nu2, double omega, double coarse_tol,
                      int ncycles, double* residuals);
+/* full multigrid then V-cycles to tol * ||r(x=0)|| (configuration 4) */
+int og_fmg(og_session* s, int rhs, int x, int level, int smoother, int nu1, int nu2, double omega, double coarse_tol,
+           int per_level, double tol, int max_cycles, double* residuals, int* n_out);
+/* CG preconditioned by one V(nu1, nu2) Jacobi cycle (configuration 5) */
+int og_pcg(og_session* s, int rhs, int x, int level, int nu1, int nu2, double omega, double coarse_tol, int iters,
+           double* residuals);
 
 #ifdef __cplusplus
 }

@@ -39,6 +39,8 @@ def lib():
             "og_jacobi": (i, [p, i, i, d, i]),
             "og_gs": (i, [p, i, i, i]),
             "og_cgs": (i, [p, i, i, i]),
+            "og_fmg": (i, [p, i, i, i, i, i, i, d, d, i, d, i, pd, C.POINTER(C.c_int)]),
+            "og_pcg": (i, [p, i, i, i, i, i, d, d, i, pd]),
             "og_vcycle": (i, [p, i, i, i, i, i, i, d, d, i, pd]),
             "og_restrict": (i, [p, i, i, i, i]),
             "og_prolongate": (i, [p, i, i, i, i]),
@@ -129,6 +131,18 @@ class Session:
     def vcycle(self, rhs, x, level, smoother, nu1, nu2, omega, coarse_tol, ncycles):
         res = np.zeros(ncycles + 1)
         _ck(lib().og_vcycle(self.h, rhs, x, level, smoother, nu1, nu2, omega, coarse_tol, ncycles, _pd(res)))
+        return res
+
+    def fmg(self, rhs, x, level, smoother, nu1, nu2, omega, coarse_tol, per_level, tol, max_cycles):
+        res = np.zeros(max_cycles + 2)
+        n = C.c_int()
+        _ck(lib().og_fmg(self.h, rhs, x, level, smoother, nu1, nu2, omega, coarse_tol, per_level, tol, max_cycles,
+                         _pd(res), C.byref(n)))
+        return res[: n.value]
+
+    def pcg(self, rhs, x, level, nu1, nu2, omega, coarse_tol, iters):
+        res = np.zeros(iters + 1)
+        _ck(lib().og_pcg(self.h, rhs, x, level, nu1, nu2, omega, coarse_tol, iters, _pd(res)))
         return res
 
     def restrict(self, fine, coarse, lc, mask=7):

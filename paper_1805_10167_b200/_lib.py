@@ -122,6 +122,8 @@ _SIGS = {
     "hyb_hierarchy_graphs": (_i, [_p, _i, _pi64]),
     "hyb_hierarchy_residual_norm": (_i, [_p, _p, _p, _i, _pd]),
     "hyb_hierarchy_solve": (_i, [_p, _p, _p, _i, _d, _i, _i, _i, _pd, C.POINTER(_i), C.POINTER(_i)]),
+    "hyb_hierarchy_fmg": (_i, [_p, _p, _p, _i, _i, _i, _i, _d, _i, _pd, C.POINTER(_i), C.POINTER(_i)]),
+    "hyb_hierarchy_pcg": (_i, [_p, _p, _p, _i, _i, _i, _i, _d, _pd, C.POINTER(_i), C.POINTER(_i)]),
     "hyb_host_alloc": (_i, [_i64, C.POINTER(_p)]),
     "hyb_host_free": (_i, [_p]),
 }

@@ -687,6 +687,36 @@ int hyb_hierarchy_solve(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, in
     });
 }
 
+int hyb_hierarchy_fmg(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, int cycles_per_level,
+                      int nu_pre, int nu_post, double tol, int max_cycles, double* residuals, int* n_out,
+                      int* converged) {
+    return guarded([&] {
+        need(h, "hyb_hierarchy_fmg");
+        need(rhs, "hyb_hierarchy_fmg");
+        need(x, "hyb_hierarchy_fmg");
+        bool conv = false;
+        const auto res =
+            h->h->fmg(*rhs->f, *x->f, level, cycles_per_level, nu_pre, nu_post, tol, max_cycles, &conv);
+        for (size_t i = 0; i < res.size(); ++i) residuals[i] = res[i];
+        if (n_out) *n_out = int(res.size());
+        if (converged) *converged = conv ? 1 : 0;
+    });
+}
+
+int hyb_hierarchy_pcg(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, int max_iter, int nu_pre,
+                      int nu_post, double tol, double* residuals, int* n_out, int* converged) {
+    return guarded([&] {
+        need(h, "hyb_hierarchy_pcg");
+        need(rhs, "hyb_hierarchy_pcg");
+        need(x, "hyb_hierarchy_pcg");
+        bool conv = false;
+        const auto res = h->h->pcg(*rhs->f, *x->f, level, max_iter, nu_pre, nu_post, tol, &conv);
+        for (size_t i = 0; i < res.size(); ++i) residuals[i] = res[i];
+        if (n_out) *n_out = int(res.size());
+        if (converged) *converged = conv ? 1 : 0;
+    });
+}
+
 int hyb_host_alloc(int64_t bytes, void** out) {
     return guarded([&] { HYB_CUDA(cudaMallocHost(out, size_t(std::max<int64_t>(bytes, 1)))); });
 }

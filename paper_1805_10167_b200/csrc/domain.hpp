@@ -255,6 +255,12 @@ class Hierarchy {
     /// residual history; returns number of cycles run
     std::vector<double> solve(Function& rhs, Function& x, int level, double tol, int max_cycles, int nu_pre,
                               int nu_post, bool* converged);
+    /// full multigrid, then cycles to tol * ||r(x = 0)|| (see hyb_hierarchy_fmg)
+    std::vector<double> fmg(Function& rhs, Function& x, int level, int per_level, int nu_pre, int nu_post, double tol,
+                            int max_cycles, bool* converged);
+    /// CG preconditioned by one V(nu_pre, nu_post) cycle (see hyb_hierarchy_pcg)
+    std::vector<double> pcg(Function& rhs, Function& x, int level, int max_iter, int nu_pre, int nu_post, double tol,
+                            bool* converged);
     int last_coarse_iterations = 0;
 
   private:
@@ -286,7 +292,8 @@ class Hierarchy {
   private:
     Domain* dom_;
     Operator a_;
-    Function r_, b_, e_;
+    Function r_, b_, e_; // b_, e_ (coarse rhs/correction) stop one level below max
+    std::unique_ptr<Function> pcg_r_, pcg_z_, pcg_p_; // PCG vectors at one level (Ap lives in r_)
     int smoother_;
     double omega_;
     double coarse_tol_;

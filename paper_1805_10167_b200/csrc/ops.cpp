@@ -339,7 +339,8 @@ void download(Function& f, int level, double* host, int64_t n, bool global_order
 Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc, int smoother, double omega,
                      double coarse_tol, int coarse_max_iter)
     : dom_(&d), a_(d, form, min_level, max_level, bc), r_(d, "mg.r", min_level, max_level, bc),
-      b_(d, "mg.b", min_level, max_level, bc), e_(d, "mg.e", min_level, max_level, bc), smoother_(smoother),
+      b_(d, "mg.b", min_level, std::max(min_level, max_level - 1), bc),
+      e_(d, "mg.e", min_level, std::max(min_level, max_level - 1), bc), smoother_(smoother),
       omega_(omega), coarse_tol_(coarse_tol), coarse_max_iter_(coarse_max_iter) {
     if (min_level < 0 || min_level > max_level)
         throw InvalidArgument("GridHierarchy: need 0 <= min_level <= max_level");
@@ -391,8 +392,10 @@ std::vector<const void*> Hierarchy::graph_key(Function& rhs, Function& x, int le
                                reinterpret_cast<const void*>(intptr_t(nu_post))};
     for (int l = a_.min_level(); l <= level; ++l) {
         k.push_back(r_.data(l));
-        k.push_back(b_.data(l));
-        k.push_back(e_.data(l));
+        if (l < level) {
+            k.push_back(b_.data(l));
+            k.push_back(e_.data(l));
+        }
         if (l > a_.min_level()) k.push_back(dom_->jacobi_scratch(l).as<void>());
     }
     return k;
@@ -518,6 +521,90 @@ std::vector<double> Hierarchy::solve(Function& rhs, Function& x, int level, doub
         run_cycle(rhs, x, level, nu_pre, nu_post);
         ++it;
         res.push_back(residual_norm(rhs, x, level));
+    }
+    if (converged) *converged = res.back() <= target;
+    return res;
+}
+
+// Full multigrid (configuration 4; no reference counterpart). Restatement:
+// oracle/hyteg_oracle.c og_fmg.
+std::vector<double> Hierarchy::fmg(Function& rhs, Function& x, int level, int per_level, int nu_pre, int nu_post,
+                                   double tol, int max_cycles, bool* converged) {
+    const int lmin = a_.min_level();
+    if (level < lmin || level > a_.max_level()) throw OutOfRange("fmg: level " + std::to_string(level) + " outside the hierarchy");
+    if (nu_pre < 0 || nu_post < 0 || per_level < 0 || max_cycles < 0)
+        throw InvalidArgument("fmg: negative smoothing or cycle count");
+    for (Function* f : {&rhs, &x}) {
+        f->check_level(lmin, "fmg");
+        f->check_level(level, "fmg");
+    }
+    if (&rhs == &x) throw InvalidArgument("fmg: rhs and x must be distinct functions");
+    for (int l = level; l > lmin; --l) {
+        restrict_to_coarse(rhs, rhs, l - 1, ALL_FLAGS);
+        fill_const(rhs, 0.0, l - 1, kDirichletMask);
+    }
+    fill_const(x, 0.0, level, ALL_FLAGS);
+    std::vector<double> res{residual_norm(rhs, x, level)};
+    const double target = tol * res.front();
+    fill_const(x, 0.0, lmin, ALL_FLAGS);
+    run_cycle(rhs, x, lmin, nu_pre, nu_post);
+    for (int l = lmin + 1; l <= level; ++l) {
+        fill_const(x, 0.0, l, ALL_FLAGS);
+        prolongate(x, x, l - 1, kSmoothMask, false);
+        for (int i = 0; i < per_level; ++i) run_cycle(rhs, x, l, nu_pre, nu_post);
+    }
+    res.push_back(residual_norm(rhs, x, level));
+    for (int it = 0; it < max_cycles && res.back() > target; ++it) {
+        run_cycle(rhs, x, level, nu_pre, nu_post);
+        res.push_back(residual_norm(rhs, x, level));
+    }
+    if (converged) *converged = res.back() <= target;
+    return res;
+}
+
+// CG preconditioned by one V-cycle from zero (configuration 5): cg_solve's
+// recurrence (reference src/solvers.cpp:226-259) with apply / dot on the
+// device. Ap is held in the hierarchy's finest residual r_, which the cycle
+// only needs after Ap has been consumed. Restatement: og_pcg.
+std::vector<double> Hierarchy::pcg(Function& rhs, Function& x, int level, int max_iter, int nu_pre, int nu_post,
+                                   double tol, bool* converged) {
+    if (level < a_.min_level() || level > a_.max_level())
+        throw OutOfRange("pcg: level " + std::to_string(level) + " outside the hierarchy");
+    if (nu_pre < 0 || nu_post < 0 || max_iter < 0) throw InvalidArgument("pcg: negative smoothing or iteration count");
+    if (&rhs == &x) throw InvalidArgument("pcg: rhs and x must be distinct functions");
+    rhs.check_level(level, "pcg");
+    x.check_level(level, "pcg");
+    Domain& d = *dom_;
+    if (!pcg_r_ || pcg_r_->min_level() != level) {
+        pcg_r_.reset();
+        pcg_z_.reset();
+        pcg_p_.reset();
+        pcg_r_ = std::make_unique<Function>(d, "pcg.r", level, level, a_.bc());
+        pcg_z_ = std::make_unique<Function>(d, "pcg.z", level, level, a_.bc());
+        pcg_p_ = std::make_unique<Function>(d, "pcg.p", level, level, a_.bc());
+    }
+    Function &r = *pcg_r_, &z = *pcg_z_, &p = *pcg_p_, &ap = r_;
+    fill_const(x, 0.0, level, ALL_FLAGS);
+    residual(a_, rhs, x, r, level);
+    std::vector<double> res{std::sqrt(dot(r, r, level))};
+    const double target = tol * res.front();
+    fill_const(z, 0.0, level, ALL_FLAGS);
+    run_cycle(r, z, level, nu_pre, nu_post);
+    assign(1.0, z, 0.0, z, p, level, ALL_FLAGS);
+    double rz = dot(r, z, level);
+    for (int k = 0; k < max_iter && res.back() > target; ++k) {
+        apply(a_, p, ap, level, ALL_FLAGS);
+        const double pap = dot(p, ap, level);
+        if (!(pap > 0.0)) throw RuntimeError("pcg: non-positive curvature p.Ap = " + std::to_string(pap));
+        const double alpha = rz / pap;
+        add_scaled(x, alpha, p, level, ALL_FLAGS);
+        add_scaled(r, -alpha, ap, level, ALL_FLAGS);
+        fill_const(z, 0.0, level, ALL_FLAGS);
+        run_cycle(r, z, level, nu_pre, nu_post);
+        const double rz_new = dot(r, z, level);
+        assign(1.0, z, rz_new / rz, p, p, level, ALL_FLAGS);
+        rz = rz_new;
+        res.push_back(std::sqrt(dot(r, r, level)));
     }
     if (converged) *converged = res.back() <= target;
     return res;

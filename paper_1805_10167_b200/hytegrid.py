@@ -480,6 +480,31 @@ class GridHierarchy:
                                       C.byref(n), C.byref(conv)))
         return SolveReport(bool(conv.value), n.value - 1, list(res[: n.value]))
 
+    def fmg(self, rhs: ScalarFunction, x: ScalarFunction, level: int, tol: float, max_cycles: int,
+            nu_pre: int = 2, nu_post: int = 2, cycles_per_level: int = 1) -> SolveReport:
+        """Full multigrid then V-cycles to tol * ||r(x = 0)|| (no reference
+        counterpart; configuration 4). rhs is given at `level`; its coarser
+        levels are overwritten by restriction. residuals[0] = ||r(x = 0)||,
+        [1] after the FMG sweep, then one per cycle; iterations counts the
+        cycles after the sweep."""
+        res = np.zeros(max_cycles + 2)
+        n = C.c_int()
+        conv = C.c_int()
+        check(lib.hyb_hierarchy_fmg(self._h, rhs._h, x._h, level, cycles_per_level, nu_pre, nu_post, tol, max_cycles,
+                                    _pd(res), C.byref(n), C.byref(conv)))
+        return SolveReport(bool(conv.value), n.value - 2, list(res[: n.value]))
+
+    def pcg(self, rhs: ScalarFunction, x: ScalarFunction, level: int, max_iter: int, tol: float = 0.0,
+            nu_pre: int = 1, nu_post: int = 1) -> SolveReport:
+        """CG preconditioned by one V(nu_pre, nu_post) cycle (configuration 5);
+        x starts at zero. residuals[k] = ||r_k||."""
+        res = np.zeros(max_iter + 1)
+        n = C.c_int()
+        conv = C.c_int()
+        check(lib.hyb_hierarchy_pcg(self._h, rhs._h, x._h, level, max_iter, nu_pre, nu_post, tol, _pd(res),
+                                    C.byref(n), C.byref(conv)))
+        return SolveReport(bool(conv.value), n.value - 1, list(res[: n.value]))
+
 
 class PinnedBuffer:
     """Page-locked host memory (for end-to-end H2D/D2H timing)."""

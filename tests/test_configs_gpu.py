@@ -5,7 +5,13 @@ Gauss-Seidel (the reference has no coloured GS; the checker is the C
 restatement oracle/hyteg_oracle.c og_cgs, whose plain GS branch is pinned
 bitwise to the reference). Reduced sizes against the oracle, bitwise per sweep
 and 1e-8 per cycle; the full size (level 9, 1.07 G DoFs) through convergence
-properties."""
+properties.
+
+config 4 -- full multigrid (og_fmg) and config 5 -- V(1,1)-preconditioned CG
+(og_pcg): neither exists in the reference; both are compositions of the pinned
+primitives (restrict, prolongate, cycle, apply, dot) restated in the C oracle.
+Residual histories within 1e-8 relative at reduced sizes; full-size shares
+through convergence properties."""
 import numpy as np
 import pytest
 
@@ -61,6 +67,133 @@ def test_cfg3_reduced_vcycle_history():
     mine = np.array(rep.residuals)
     assert np.max(np.abs(mine - ref) / ref) <= 1e-8, (mine, ref)
     assert mine[-1] / mine[0] < 0.05
+
+
+def cfg4_rhs(dom, mesh, L):
+    """sin(pi x) sin(pi y) + U[-1e-3, 1e-3] (seed 3), global order"""
+    xy = dom.coords(L)
+    return np.sin(np.pi * xy[:, 0]) * np.sin(np.pi * xy[:, 1]) + keyed_uniform(mesh, L, seed=3, lo=-1e-3, hi=1e-3)
+
+
+@pytest.mark.parametrize("ranks", [1, 2])
+def test_cfg4_fmg_vs_restatement(ranks):
+    """Config 4 shape at reduced size: square 4 x 4 cells (32 faces), levels
+    2 -> 6, FMG with V(2,2) weighted Jacobi, then cycles to 1e-10."""
+    mesh = H.meshgen.channel(4, 4)
+    lmin, L = 2, 6
+    dom = H.DistributedDomain(mesh, ranks)
+    ctl = H.Controller(dom)
+    rhs = H.ScalarFunction("rhs", dom, lmin, L)
+    x = H.ScalarFunction("x", dom, lmin, L)
+    b = cfg4_rhs(dom, mesh, L)
+    rhs.upload(L, b)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, lmin, L, smoother="jacobi", coarse_tol=1e-12)
+    rep = mg.fmg(rhs, x, L, 1e-10, 40)
+    o = O.Session(mesh, lmin, L, 7)
+    o.set(0, L, b)
+    ref = o.fmg(0, 1, L, 0, 2, 2, 2.0 / 3.0, 1e-12, 1, 1e-10, 40)
+    mine = np.array(rep.residuals)
+    assert rep.converged and len(mine) == len(ref), (mine, ref)
+    assert np.max(np.abs(mine - ref) / ref) <= 1e-8, (mine, ref)
+    # the FMG sweep alone reaches discretisation-level accuracy
+    assert mine[1] / mine[0] < 0.1
+    # restricted rhs on a coarse level agrees too (DIRICHLET rows zeroed)
+    o.set(0, L, b)
+    for lc in range(L - 1, lmin - 1, -1):
+        o.restrict(0, 0, lc)
+        o.assign(0.0, 0, 0.0, 0, 0, lc, H.DIRICHLET)
+    assert np.array_equal(rhs.download(lmin), o.get(0, lmin))
+    np.testing.assert_allclose(x.download(L), o.get(1, L), rtol=0, atol=1e-9 * np.abs(o.get(1, L)).max())
+
+
+@pytest.mark.parametrize("ranks", [1, 3])
+def test_cfg5_pcg_vs_restatement(ranks):
+    """Config 5 shape at reduced size: channel 4 x 8 (64 faces), level 6,
+    CG preconditioned by one V(1,1) Jacobi cycle, 12 iterations."""
+    mesh = H.meshgen.channel(4, 8)
+    L = 6
+    dom = H.DistributedDomain(mesh, ranks)
+    ctl = H.Controller(dom)
+    rhs = H.ScalarFunction("rhs", dom, L, L)
+    x = H.ScalarFunction("x", dom, L, L)
+    b = keyed_uniform(mesh, L, seed=4)
+    b[rhs.flags(L) != H.INNER] = 0.0
+    rhs.upload(L, b)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="jacobi", coarse_tol=1e-12)
+    rep = mg.pcg(rhs, x, L, 12)
+    o = O.Session(mesh, 0, L, 11)
+    o.set(0, L, b)
+    ref = o.pcg(0, 1, L, 1, 1, 2.0 / 3.0, 1e-12, 12)
+    mine = np.array(rep.residuals)
+    assert len(mine) == 13
+    assert np.max(np.abs(mine - ref) / ref) <= 1e-8, (mine, ref)
+    assert mine[-1] / mine[0] < 1e-7, mine
+    # x solves A x = b to the final residual
+    r = H.ScalarFunction("r", dom, L, L)
+    A = H.StencilOperator(dom, H.LAPLACE, L, L)
+    H.residual(A, ctl, rhs, x, r, L)
+    assert abs(H.norm2(r, L) - mine[-1]) <= 1e-6 * mine[-1]
+
+
+def test_pcg_graph_replay_matches_eager():
+    """PCG's preconditioner cycles replay from a CUDA graph after two eager
+    runs; the residual history is bitwise the eager one."""
+    mesh = H.meshgen.channel(4, 4)
+    L = 5
+    dom = H.DistributedDomain(mesh, 1)
+    ctl = H.Controller(dom)
+    rhs = H.ScalarFunction("rhs", dom, L, L)
+    x = H.ScalarFunction("x", dom, L, L)
+    H.interpolate_random(rhs, L, seed=4, flag_mask=H.INNER)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L)
+    mg.use_graphs(False)
+    eager = mg.pcg(rhs, x, L, 10).residuals
+    mg.use_graphs(True)
+    graphed = mg.pcg(rhs, x, L, 10).residuals
+    assert mg.use_graphs() > 0
+    assert graphed == eager
+
+
+@pytest.mark.slow
+def test_cfg4_full_mesh():
+    """Config 4 mesh (64 x 64 cells, 8192 faces), levels 2 -> 9 on one GPU
+    (level 11 needs ~100 GB per GPU at 8 GPUs): FMG then cycles to 1e-10."""
+    mesh = H.meshgen.channel(64, 64)
+    lmin, L = 2, 9
+    dom = H.DistributedDomain(mesh, 1)
+    ctl = H.Controller(dom)
+    rhs = H.ScalarFunction("rhs", dom, lmin, L)
+    x = H.ScalarFunction("x", dom, lmin, L)
+    H.interpolate(rhs, lambda px, py: np.sin(np.pi * px) * np.sin(np.pi * py), L)
+    noise = H.ScalarFunction("noise", dom, L, L)
+    H.interpolate_random(noise, L, seed=3, lo=-1e-3, hi=1e-3)
+    H.add_scaled(rhs, 1.0, noise, L)
+    del noise
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, lmin, L, smoother="jacobi")
+    rep = mg.fmg(rhs, x, L, 1e-10, 40)
+    res = np.array(rep.residuals)
+    assert rep.converged, res
+    assert res[1] / res[0] < 0.1, res
+    assert np.all(res[2:] < res[1:-1]), res
+
+
+@pytest.mark.slow
+def test_cfg5_one_gpu_share():
+    """Config 5 per-GPU share: 1024 faces at level 11 (level 12 needs ~69 GB
+    per vector), 50 PCG iterations preconditioned by V(1,1)."""
+    mesh = H.meshgen.channel(16, 32)
+    L = 11
+    dom = H.DistributedDomain(mesh, 1)
+    ctl = H.Controller(dom)
+    rhs = H.ScalarFunction("rhs", dom, L, L)
+    x = H.ScalarFunction("x", dom, L, L)
+    H.interpolate_random(rhs, L, seed=4, flag_mask=H.INNER)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="jacobi")
+    rep = mg.pcg(rhs, x, L, 50)
+    res = np.array(rep.residuals)
+    assert len(res) == 51
+    assert res[10] / res[0] < 1e-6, res
+    assert np.all(np.isfinite(res))
 
 
 @pytest.mark.slow

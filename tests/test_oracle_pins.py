@@ -123,3 +123,26 @@ def test_restatement_matches_reference_live(mesh_kind, level):
         o.prolongate(2, 3, level - 1)
         assert np.array_equal(r.get(3, level), o.get(3, level))
         assert r.dot(0, 1, level) == o.dot(0, 1, level)
+
+
+def test_restatement_fmg_and_pcg_converge():
+    """og_fmg / og_pcg have no reference counterpart: they compose the pinned
+    primitives. Sanity: FMG reaches discretisation accuracy in one sweep and
+    then converges monotonically; PCG's recurrence residual equals the true
+    residual of its x."""
+    from paper_1805_10167_b200 import hytegrid as H
+    mesh = H.meshgen.channel(4, 4)
+    o = O.Session(mesh, 2, 6, 11)
+    o.set(0, 6, keyed_uniform(mesh, 6, seed=3, lo=-1e-3, hi=1e-3) + 1.0)
+    fl = o.flags(6)
+    b = o.get(0, 6)
+    b[fl != 1] = 0.0
+    o.set(0, 6, b)
+    res = o.fmg(0, 1, 6, 0, 2, 2, 2.0 / 3.0, 1e-12, 1, 1e-10, 40)
+    assert res[1] / res[0] < 0.1 and res[-1] <= 1e-10 * res[0]
+    assert np.all(res[2:] < res[1:-1])
+    o.set(0, 6, b)
+    res = o.pcg(0, 1, 6, 1, 1, 2.0 / 3.0, 1e-12, 10)
+    assert res[-1] / res[0] < 1e-6
+    o.residual(0, 1, 2, 6)
+    assert abs(np.sqrt(o.dot(2, 2, 6)) - res[-1]) <= 1e-6 * res[-1]
