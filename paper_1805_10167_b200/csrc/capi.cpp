@@ -7,16 +7,23 @@
 #include "../../include/hyteg_b200.h"
 #include "domain.hpp"
 
+// Objects built on a domain share ownership of it: destroying the domain
+// handle first (any order is legal, e.g. a garbage collector finalising a
+// cycle) releases the Domain only with its last function/operator/hierarchy.
+// `keep` is declared first so it is destroyed after the object using it.
 struct hyb_domain {
-    std::unique_ptr<hyb::Domain> d;
+    std::shared_ptr<hyb::Domain> d;
 };
 struct hyb_function {
+    std::shared_ptr<hyb::Domain> keep;
     std::unique_ptr<hyb::Function> f;
 };
 struct hyb_operator {
+    std::shared_ptr<hyb::Domain> keep;
     std::unique_ptr<hyb::Operator> a;
 };
 struct hyb_hierarchy {
+    std::shared_ptr<hyb::Domain> keep;
     std::unique_ptr<hyb::Hierarchy> h;
 };
 struct hyb_plan {
@@ -260,7 +267,7 @@ int hyb_domain_create(const char* mesh_text, int world_ranks, const int32_t* ass
         else
             for (int r = 0; r < world_ranks; ++r) lr.push_back(r);
         auto h = std::make_unique<hyb_domain>();
-        h->d = std::make_unique<hyb::Domain>(mesh_text, world_ranks, a, lr, device);
+        h->d = std::make_shared<hyb::Domain>(mesh_text, world_ranks, a, lr, device);
         *out = h.release();
     });
 }
@@ -388,6 +395,7 @@ int hyb_function_create(hyb_domain* d, const char* name, int min_level, int max_
     return guarded([&] {
         need(d, "hyb_function_create");
         auto h = std::make_unique<hyb_function>();
+        h->keep = d->d;
         h->f = std::make_unique<hyb::Function>(*d->d, name ? name : "f", min_level, max_level,
                                                make_bc(bc_markers, bc_flags, n_bc));
         *out = h.release();
@@ -467,6 +475,7 @@ int hyb_operator_create(hyb_domain* d, int form, int min_level, int max_level, c
         need(d, "hyb_operator_create");
         if (form != HYB_LAPLACE && form != HYB_MASS) throw hyb::InvalidArgument("StencilOperator: unsupported form");
         auto h = std::make_unique<hyb_operator>();
+        h->keep = d->d;
         h->a = std::make_unique<hyb::Operator>(*d->d, hyb::Form(form), min_level, max_level,
                                                make_bc(bc_markers, bc_flags, n_bc));
         *out = h.release();
@@ -640,6 +649,7 @@ int hyb_hierarchy_create(hyb_domain* d, int form, int min_level, int max_level, 
     return guarded([&] {
         need(d, "hyb_hierarchy_create");
         auto h = std::make_unique<hyb_hierarchy>();
+        h->keep = d->d;
         h->h = std::make_unique<hyb::Hierarchy>(*d->d, hyb::Form(form), min_level, max_level,
                                                 make_bc(bc_markers, bc_flags, n_bc), smoother, omega, coarse_tol,
                                                 coarse_max_iter);
