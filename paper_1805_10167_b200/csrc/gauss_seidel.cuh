@@ -130,30 +130,106 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
 // stencil graph has triangles), edge lines odd k then even k. Restated in
 // oracle/hyteg_oracle.c (og_cgs).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_cgs_faces(LevelTables t, const double* __restrict__ b, double* x,
-                                                   int color) {
-    const int n = t.n;
-    const int r = 1 + blockIdx.y;
-    if (r > n - 2) return;
-    const int cs = ((color - 2 * r) % 3 + 3) % 3; // first column of this colour (c >= 0)
-    const int c = cs + 3 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (c < 1 || c > n - 1 - r) return;
-    const int64_t base = int64_t(blockIdx.z) * t.face_stride;
-    double* xf = x + base;
-    const int64_t* ro = t.rowoff;
+// Coloured face sweep, all three colours in ONE streaming pass per face.
+// A colour class has no neighbour of its own colour (the seven stencil offsets
+// change c + 2r by +-1 or +-2), so colour k at row r depends only on the other
+// colours in rows r-1..r+1. One CTA walks its face downwards in blocks of K
+// rows; step j runs
+//     C0 on rows [j, j+K)  ->  C1 on rows [j-1, j+K-1)  ->  C2 on rows [j-2, j+K-2)
+// with a CTA barrier between phases. Every update then sees exactly the
+// values of the three full-face passes (C0 reads old C1/C2, C1 new C0 / old C2,
+// C2 new C0/C1), so the result is bitwise the 3-pass sweep (og_cgs), while the
+// K+3-row window of x and b stays in L1/L2 between the phases; the next
+// block's rows are prefetched into L2 by one bulk prefetch per array. K = 8
+// balances barrier count against the L2 footprint of ~600 resident faces
+// (K = 16 re-reads rows from HBM, K <= 4 is barrier-bound). A variant staging
+// whole rows in shared memory by TMA (colours skewed two rows apart, one
+// barrier per row) moved exactly the algorithmic bytes but was issue-bound on
+// its per-row overhead and ran slower; see DESIGN.md.
+constexpr int CGS_WARPS = 8;
+
+__device__ __forceinline__ void cgs_point_loads(const double* rm, const double* r0, const double* rp,
+                                                const double* br, int c, double (&v)[8]) {
+    v[0] = r0[c - 1];
+    v[1] = rp[c - 1];
+    v[2] = rm[c];
+    v[3] = r0[c];
+    v[4] = rp[c];
+    v[5] = rm[c + 1];
+    v[6] = r0[c + 1];
+    v[7] = __ldg(br + c);
+}
+
+__device__ __forceinline__ double cgs_point_update(const double (&v)[8], const double (&co)[8], double rd) {
+    double acc = 0.0; // reference term order W NW S C N SE E
+    acc += co[0] * v[0];
+    acc += co[1] * v[1];
+    acc += co[2] * v[2];
+    acc += co[3] * v[3];
+    acc += co[4] * v[4];
+    acc += co[5] * v[5];
+    acc += co[6] * v[6];
+    return v[3] + div_by(v[7] - acc, co[7], rd);
+}
+
+// one warp, one row, one colour: two points per lane per iteration with all
+// loads issued before the stores (points of one colour are independent)
+__device__ __forceinline__ void cgs_row(double* __restrict__ xf, const double* __restrict__ bf,
+                                        const int64_t* __restrict__ ro, int n, int r, int colour, const double (&co)[8],
+                                        double rd, int lane) {
     const double* rm = xf + ro[r - 1];
     double* r0 = xf + ro[r];
     const double* rp = xf + ro[r + 1];
-    const double* co = t.face_coef + size_t(blockIdx.z) * 8;
-    double acc = 0.0;
-    acc += co[0] * r0[c - 1];
-    acc += co[1] * rp[c - 1];
-    acc += co[2] * rm[c];
-    acc += co[3] * r0[c];
-    acc += co[4] * rp[c];
-    acc += co[5] * rm[c + 1];
-    acc += co[6] * r0[c + 1];
-    r0[c] = r0[c] + div_by(b[base + ro[r] + c] - acc, co[7], 1.0 / co[7]);
+    const double* br = bf + ro[r];
+    int cs = ((colour - 2 * r) % 3 + 3) % 3; // first column of this colour
+    if (cs == 0) cs = 3;                      // c = 0 is the border
+    const int cmax = n - 1 - r;
+    for (int c = cs + 3 * lane; c <= cmax; c += 192) {
+        const int c2 = c + 96;
+        double v[8], w[8];
+        cgs_point_loads(rm, r0, rp, br, c, v);
+        if (c2 <= cmax) cgs_point_loads(rm, r0, rp, br, c2, w);
+        const double u = cgs_point_update(v, co, rd);
+        if (c2 <= cmax) {
+            const double u2 = cgs_point_update(w, co, rd);
+            r0[c2] = u2;
+        }
+        r0[c] = u;
+    }
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int CGS_K>
+__global__ void __launch_bounds__(CGS_WARPS * 32) k_cgs_faces(LevelTables t, const double* __restrict__ b,
+                                                              double* x) {
+    const int n = t.n;
+    const int last = n - 2; // interior rows 1..n-2
+    const int64_t base = int64_t(blockIdx.x) * t.face_stride;
+    double* xf = x + base;
+    const double* bf = b + base;
+    double co[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) co[i] = t.face_coef[size_t(blockIdx.x) * 8 + i];
+    const double rd = 1.0 / co[7];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t* __restrict__ ro = t.rowoff;
+    for (int j = 1; j - 2 <= last; j += CGS_K) {
+        if (threadIdx.x == 0) { // next block's rows into L2 while this one computes
+            const int xlo = j + CGS_K + 1, xhi = min(n - 1, j + 2 * CGS_K); // x rows read by the next C0
+            if (xlo <= xhi) prefetch_l2(xf + ro[xlo], uint32_t((ro[xhi + 1] - ro[xlo]) * 8) & ~15u);
+            const int blo = j + CGS_K, bhi = min(last, j + 2 * CGS_K - 1);
+            if (blo <= bhi) prefetch_l2(bf + ro[blo], uint32_t((ro[bhi + 1] - ro[blo]) * 8) & ~15u);
+        }
+#pragma unroll 1
+        for (int colour = 0; colour < 3; ++colour) {
+            const int lo = max(1, j - colour), hi = min(last, j - colour + CGS_K - 1);
+            for (int r = lo + warp; r <= hi; r += CGS_WARPS) cgs_row(xf, bf, t.rowoff, n, r, colour, co, rd, lane);
+            __syncthreads();
+        }
+    }
 }
 
 // edges: colour 1 = odd k, colour 0 = even k, one thread per line DoF

@@ -525,12 +525,9 @@ void launch_gs_faces(const LevelTables& t, const double* b, double* x, const int
 }
 
 void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
-    if (t.nfaces <= 0 || t.n < 3) return;
-    for (int color = 0; color < 3; ++color) {
-        const dim3 grid(unsigned(((t.n - 1) / 3 + 1 + 127) / 128), unsigned(t.n - 2), unsigned(t.nfaces));
-        k_cgs_faces<<<grid, 128, 0, st>>>(t, b, x, color);
-        check_launch("coloured gauss-seidel faces");
-    }
+    if (t.nfaces <= 0 || t.n < 4) return; // n = 3: no interior face DoF
+    k_cgs_faces<8><<<unsigned(t.nfaces), CGS_WARPS * 32, 0, st>>>(t, b, x);
+    check_launch("coloured gauss-seidel faces");
 }
 
 void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st) {
