@@ -767,6 +767,119 @@ __global__ void __launch_bounds__(CG_THREADS) k_coarse_cg(int64_t n, const int32
     }
 }
 
+// Large min-level systems (e.g. configuration 4: 66k DoFs at level 2 of a
+// 8192-face mesh): the same CG on the whole GPU. One CTA per SM, launched
+// cooperatively (all co-resident); three grid barriers per iteration (after
+// each dot, after the p update). Dots are deterministic and identical in every
+// CTA: per-CTA partials, then every CTA sums the same partials in the same
+// fixed order. Partial buffers alternate, and a barrier always separates a
+// buffer's last read from its next write.
+constexpr int CGG_THREADS = 512;
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ double block_sum(double s, double* red) {
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = s;
+    __syncthreads();
+    if (w == 0) {
+        double t = l < CGG_THREADS / 32 ? red[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+        if (l == 0) red[32] = t;
+    }
+    __syncthreads();
+    const double out = red[32];
+    __syncthreads();
+    return out;
+}
+
+__device__ double grid_dot(const double* u, const double* v, int64_t n, double* red, double* part, unsigned* bar) {
+    const int64_t stride = int64_t(gridDim.x) * CGG_THREADS;
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * int64_t(CGG_THREADS) + threadIdx.x; i < n; i += stride) s += u[i] * v[i];
+    const double b = block_sum(s, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = b;
+    grid_barrier(bar);
+    double t = 0.0;
+    for (int i = threadIdx.x; i < int(gridDim.x); i += CGG_THREADS) t += __ldcg(part + i);
+    return block_sum(t, red);
+}
+
+__global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_grid(int64_t n, const int32_t* __restrict__ rowptr,
+                                                                const int32_t* __restrict__ col,
+                                                                const double* __restrict__ val,
+                                                                const double* __restrict__ b, double* x, double* r,
+                                                                double* p, double* ap, double tol, int max_iter,
+                                                                CoarseStatus* st, double* part, unsigned* bar) {
+    __shared__ double red[33];
+    const int64_t stride = int64_t(gridDim.x) * CGG_THREADS;
+    const int64_t i0 = blockIdx.x * int64_t(CGG_THREADS) + threadIdx.x;
+    double* part0 = part;
+    double* part1 = part + gridDim.x;
+    for (int64_t i = i0; i < n; i += stride) {
+        x[i] = 0.0;
+        r[i] = b[i];
+        p[i] = b[i];
+    }
+    const double target = tol * sqrt(grid_dot(b, b, n, red, part0, bar));
+    double rs = grid_dot(r, r, n, red, part1, bar); // also publishes p
+    int it = 0, breakdown = 0;
+    while (it < max_iter && sqrt(rs) > target) {
+        for (int64_t i = i0; i < n; i += stride) {
+            double acc = 0.0;
+            for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) acc += val[k] * __ldcg(p + col[k]);
+            ap[i] = acc;
+        }
+        const double pap = grid_dot(p, ap, n, red, part0, bar);
+        if (pap <= 0.0) {
+            breakdown = 1;
+            break;
+        }
+        const double alpha = rs / pap;
+        for (int64_t i = i0; i < n; i += stride) {
+            x[i] += alpha * p[i];
+            r[i] -= alpha * ap[i];
+        }
+        const double rs_new = grid_dot(r, r, n, red, part1, bar);
+        const double beta = rs_new / rs;
+        for (int64_t i = i0; i < n; i += stride) p[i] = r[i] + beta * p[i];
+        grid_barrier(bar);
+        rs = rs_new;
+        ++it;
+    }
+    grid_barrier(bar); // x complete (the breakdown exit skips the loop's barriers)
+    for (int64_t i = i0; i < n; i += stride) {
+        double acc = 0.0;
+        for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) acc += val[k] * __ldcg(x + col[k]);
+        ap[i] = b[i] - acc;
+    }
+    const double res = sqrt(grid_dot(ap, ap, n, red, part0, bar));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->iterations = it;
+        st->breakdown = breakdown;
+        st->converged = res <= target ? 1 : 0;
+        st->target = target;
+        st->residual = res;
+    }
+}
+
 } // namespace
 
 void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos, const double* arena, double* glob,
@@ -776,9 +889,38 @@ void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos,
     check_launch("coarse gather");
 }
 
+int coarse_grid_blocks() {
+    static const int g = [] {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coarse_cg_grid, CGG_THREADS, 0);
+        return sms * (per > 0 ? 1 : 0);
+    }();
+    return g;
+}
+
 void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* b,
                       double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
-                      cudaStream_t stream) {
+                      double* grid_part, unsigned* grid_bar, cudaStream_t stream) {
+    if (n >= kCoarseGridMinRows && grid_part && grid_bar && coarse_grid_blocks() > 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(coarse_grid_blocks()));
+        cfg.blockDim = dim3(CGG_THREADS);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr{};
+        attr.id = cudaLaunchAttributeCooperative;
+        attr.val.cooperative = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k_coarse_cg_grid, n, rowptr, col, val, b, x, r, p, ap, tol,
+                                                 max_iter, st, grid_part, grid_bar);
+        if (e != cudaSuccess)
+            throw std::runtime_error(std::string("CUDA launch failed (coarse cg grid): ") + cudaGetErrorString(e));
+        check_launch("coarse cg grid");
+        return;
+    }
     const size_t smem = size_t(5 * n) * sizeof(double);
     const bool in_smem = smem <= 200 * 1024;
     if (in_smem) {

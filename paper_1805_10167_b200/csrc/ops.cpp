@@ -365,6 +365,10 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
     coarse_.vec = DevMem(size_t(5 * std::max<int64_t>(csr.n, 1)) * 8);
     coarse_.status = DevMem(sizeof(CoarseStatus));
     HYB_CUDA(cudaMemsetAsync(coarse_.status.as<void>(), 0, sizeof(CoarseStatus), d.stream()));
+    if (csr.n >= kCoarseGridMinRows) { // whole-GPU CG: per-CTA partials + barrier words
+        coarse_.grid = DevMem(size_t(2 * std::max(coarse_grid_blocks(), 1)) * 8 + 64);
+        HYB_CUDA(cudaMemsetAsync(coarse_.grid.as<void>(), 0, coarse_.grid.bytes(), d.stream()));
+    }
 }
 
 void Hierarchy::smooth(Function& rhs, Function& x, int level) {
@@ -486,7 +490,7 @@ void Hierarchy::coarse_correct(Function& rhs, Function& x) {
     d.timer_begin("coarse_cg");
     launch_coarse_cg(n, coarse_.rowptr.as<int32_t>(), coarse_.col.as<int32_t>(), coarse_.val.as<double>(), b, cx,
                      b + 2 * n, b + 3 * n, b + 4 * n, coarse_tol_, coarse_max_iter_,
-                     coarse_.status.as<CoarseStatus>(), d.stream());
+                     coarse_.status.as<CoarseStatus>(), coarse_.grid_part(), coarse_.grid_bar(), d.stream());
     d.timer_end();
     launch_coarse_scatter_add(coarse_.nloc, coarse_.gidx.as<int64_t>(), coarse_.pos.as<int64_t>(),
                               coarse_.flag.as<uint8_t>(), kSmoothMask, cx, x.data(L), d.stream());

@@ -112,6 +112,35 @@ def test_cfg4_fmg_vs_restatement(ranks):
     np.testing.assert_allclose(x.download(L), o.get(1, L), rtol=0, atol=1e-9 * np.abs(o.get(1, L)).max())
 
 
+@pytest.mark.parametrize("ranks", [1, 2])
+def test_fmg_whole_gpu_coarse_cg_vs_restatement(ranks):
+    """min level 2 of channel(32, 32) has 16,641 DoFs: the coarse CG runs as
+    the cooperative one-CTA-per-SM kernel (>= 16384 rows); FMG history vs
+    og_fmg, and graph replay of the cooperative launch."""
+    mesh = H.meshgen.channel(32, 32)
+    lmin, L = 2, 5
+    dom = H.DistributedDomain(mesh, ranks)
+    assert dom.owned_count(lmin)[0] == 16641
+    ctl = H.Controller(dom)
+    rhs = H.ScalarFunction("rhs", dom, lmin, L)
+    x = H.ScalarFunction("x", dom, lmin, L)
+    b = cfg4_rhs(dom, mesh, L, rhs.flags(L))
+    rhs.upload(L, b)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, lmin, L, smoother="jacobi", coarse_tol=1e-10)
+    rep = mg.fmg(rhs, x, L, 1e-9, 30)
+    o = O.Session(mesh, lmin, L, 7)
+    o.set(0, L, b)
+    ref = o.fmg(0, 1, L, 0, 2, 2, 2.0 / 3.0, 1e-10, 1, 1e-9, 30)
+    mine = np.array(rep.residuals)
+    assert rep.converged and len(mine) == len(ref), (mine, ref)
+    assert np.all(np.abs(mine - ref) <= 1e-8 * ref + 1e-13 * ref[0]), (mine, ref)
+    # again: the cycles now replay from CUDA graphs holding the cooperative launch
+    rhs.upload(L, b)
+    rep2 = mg.fmg(rhs, x, L, 1e-9, 30)
+    assert mg.use_graphs() > 0
+    assert rep2.residuals == rep.residuals
+
+
 @pytest.mark.parametrize("ranks", [1, 3])
 def test_cfg5_pcg_vs_restatement(ranks):
     """Config 5 shape at reduced size: channel 4 x 8 (64 faces), level 6,
