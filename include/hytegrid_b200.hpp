@@ -8,13 +8,14 @@
 //   Controller(domain), register_function       Controller(domain), register_function (no-ops)
 //   ScalarFunction(name, dom, P1, min, max, bc) ScalarFunction(name, dom, min, max, bc)
 //   StencilOperator(dom, form, P1, min, max, bc) StencilOperator(dom, form, min, max, bc)
-//   apply / smooth_jacobi / diagonal            same (operators.hpp:108-125)
+//   apply / smooth_jacobi / smooth_gs / diagonal same (operators.hpp:108-125)
 //   prolongate / restrict_to_coarse             same (solvers.hpp:26-33)
 //   assign / add_scaled / dot / norm2 / max_abs same (function.hpp:60-74)
 //   interpolate(f, expr, level, mask)           same; expr evaluated on the host at the
 //                                               reference's DoF coordinates, then uploaded
 //   sync_all(ctl, f, level)                     same
-//   GridHierarchy(dom, ctl, form, min, max, bc) same + smoother weight / coarse tolerance
+//   GridHierarchy(dom, ctl, form, min, max, bc) same (+ smoother choice, Jacobi weight, coarse tolerance;
+//                                               default: the reference's Gauss-Seidel)
 //   f.values(id, level)                         f.download(level) / f.upload(level, v)
 //                                               (GlobalDoFMap order, numbering.hpp:41-43)
 #pragma once
@@ -35,6 +36,9 @@ enum class DoFFlag : std::uint8_t { INNER = 1, DIRICHLET = 2, NEUMANN = 4 };
 constexpr std::uint8_t ALL_DOF_FLAGS = 7;
 inline std::uint8_t flag_bit(DoFFlag f) { return static_cast<std::uint8_t>(f); }
 enum class Form : int { LAPLACE = HYB_LAPLACE, MASS = HYB_MASS };
+/// GridHierarchy smoother: the reference always uses its hybrid Gauss-Seidel
+/// (solvers.cpp:417, 427); weighted Jacobi and coloured GS are additions.
+enum class Smoother : int { GAUSS_SEIDEL = HYB_SMOOTH_GS, JACOBI = HYB_SMOOTH_JACOBI, COLORED_GS = HYB_SMOOTH_COLORED_GS };
 
 struct BoundaryConditions {
     std::map<int, DoFFlag> marker_flag;
@@ -195,6 +199,15 @@ inline void smooth_jacobi(const StencilOperator& A, Controller&, const ScalarFun
                           double omega, int level) {
     check(hyb_smooth_jacobi(A.handle(), rhs.handle(), x.handle(), omega, level));
 }
+/// the reference's hybrid Gauss-Seidel sweep (operators.hpp:120-121), bitwise
+inline void smooth_gs(const StencilOperator& A, Controller&, const ScalarFunction& rhs, ScalarFunction& x, int level) {
+    check(hyb_smooth_gs(A.handle(), rhs.handle(), x.handle(), level));
+}
+/// coloured variant (faces by (c + 2r) mod 3, edges odd/even); no reference counterpart
+inline void smooth_colored_gs(const StencilOperator& A, Controller&, const ScalarFunction& rhs, ScalarFunction& x,
+                              int level) {
+    check(hyb_smooth_cgs(A.handle(), rhs.handle(), x.handle(), level));
+}
 inline void diagonal(const StencilOperator& A, ScalarFunction& d, int level) {
     check(hyb_diagonal(A.handle(), d.handle(), level));
 }
@@ -235,13 +248,14 @@ struct SolveReport {
 class GridHierarchy {
   public:
     GridHierarchy(DistributedDomain& d, Controller&, Form form, int min_level, int max_level,
-                  BoundaryConditions bc = {}, double omega = 2.0 / 3.0, double coarse_tol = 1e-12)
+                  BoundaryConditions bc = {}, Smoother smoother = Smoother::GAUSS_SEIDEL, double omega = 2.0 / 3.0,
+                  double coarse_tol = 1e-12)
         : max_(max_level) {
         std::vector<int32_t> m;
         std::vector<uint8_t> f;
         detail::bc_arrays(bc, m, f);
         check(hyb_hierarchy_create(d.handle(), int(form), min_level, max_level, m.data(), f.data(), int(m.size()),
-                                   HYB_SMOOTH_JACOBI, omega, coarse_tol, -1, &h_));
+                                   int(smoother), omega, coarse_tol, -1, &h_));
     }
     ~GridHierarchy() { hyb_hierarchy_destroy(h_); }
     GridHierarchy(const GridHierarchy&) = delete;

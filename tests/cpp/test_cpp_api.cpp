@@ -60,6 +60,22 @@ int main() {
     for (size_t i = 0; i < xs.size(); ++i)
         err = std::fmax(err, std::fabs(xs[i] - (1.5 + 2.0 * xy[2 * i] - 0.75 * xy[2 * i + 1])));
     EXPECT(err <= 1e-10);
-    std::printf("cpp api ok: %d cycles, residual %.3e, error %.3e\n", rep.iterations, rep.residuals.back(), err);
+    // the exact solution is a fixed point of the reference's GS sweep (tests/test_operators.cpp:287-310)
+    StencilOperator As(sq, Form::LAPLACE, level, level);
+    smooth_gs(As, c2, rhs, x, level);
+    const auto xg = x.download(level);
+    double moved = 0;
+    for (size_t i = 0; i < xs.size(); ++i) moved = std::fmax(moved, std::fabs(xg[i] - xs[i]));
+    EXPECT(moved <= 1e-12);
+    // the additions: weighted-Jacobi FMG and V(1,1)-preconditioned CG
+    GridHierarchy mj(sq, c2, Form::LAPLACE, 1, level, {}, Smoother::JACOBI);
+    ScalarFunction f("f", sq, 1, level), u("u", sq, 1, level);
+    interpolate(f, [](double a, double b) { return a * (1 - a) + b; }, level, flag_bit(DoFFlag::INNER));
+    const SolveReport fr = mj.fmg(f, u, level, 1e-8, 40);
+    EXPECT(fr.converged && fr.residuals.back() <= 1e-8 * fr.residuals.front());
+    const SolveReport pr = mj.pcg(f, u, level, 20);
+    EXPECT(pr.residuals.size() == 21 && pr.residuals.back() <= 1e-9 * pr.residuals.front());
+    std::printf("cpp api ok: %d cycles, residual %.3e, error %.3e; fmg %d cycles, pcg %.1e\n", rep.iterations,
+                rep.residuals.back(), err, fr.iterations, pr.residuals.back() / pr.residuals.front());
     return 0;
 }
