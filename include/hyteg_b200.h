@@ -183,6 +183,13 @@ int hyb_prolongate(hyb_function* coarse, hyb_function* fine, int coarse_level, u
 int hyb_prolongate_add(hyb_function* coarse, hyb_function* fine, int coarse_level, uint8_t mask);
 /* restrict_to_coarse(ctl, fine, coarse, coarse_level, mask) solvers.hpp:32-33 */
 int hyb_restrict(hyb_function* fine, hyb_function* coarse, int coarse_level, uint8_t mask);
+/* residual (apply + assign, solvers.cpp:418-419) followed by
+ * restrict_to_coarse(r, coarse, coarse_level, ALL) (:420), fused on face
+ * interiors; bitwise the composed result on every owned coarse DoF. r is
+ * scratch: afterwards it holds b - A x on edges, vertices and the face rows /
+ * columns next to the borders only. */
+int hyb_residual_restrict(hyb_operator* A, hyb_function* rhs, hyb_function* x, hyb_function* r,
+                          hyb_function* coarse, int coarse_level);
 /* assign / add_scaled / dot / norm2 / max_abs     function.hpp:60-74 */
 int hyb_assign(double alpha, hyb_function* x1, double beta, hyb_function* x2, hyb_function* dst, int level,
                uint8_t mask);

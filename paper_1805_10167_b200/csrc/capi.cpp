@@ -603,6 +603,18 @@ int hyb_restrict(hyb_function* fine, hyb_function* coarse, int coarse_level, uin
     });
 }
 
+int hyb_residual_restrict(hyb_operator* A, hyb_function* rhs, hyb_function* x, hyb_function* r,
+                          hyb_function* coarse, int coarse_level) {
+    return guarded([&] {
+        need(A, "hyb_residual_restrict");
+        need(rhs, "hyb_residual_restrict");
+        need(x, "hyb_residual_restrict");
+        need(r, "hyb_residual_restrict");
+        need(coarse, "hyb_residual_restrict");
+        hyb::residual_restrict(*A->a, *rhs->f, *x->f, *r->f, *coarse->f, coarse_level);
+    });
+}
+
 int hyb_assign(double alpha, hyb_function* x1, double beta, hyb_function* x2, hyb_function* dst, int level,
                uint8_t mask) {
     return guarded([&] {

@@ -234,6 +234,11 @@ void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level);
 void diagonal(const Operator& A, Function& d, int level);
 void prolongate(Function& coarse, Function& fine, int coarse_level, uint8_t mask, bool add);
 void restrict_to_coarse(Function& fine, Function& coarse, int coarse_level, uint8_t mask);
+/// coarse := P^T (rhs - A x) at coarse_level on every owned DoF, fused (the
+/// cycle's residual + restrict_to_coarse); r is scratch: it ends up holding the
+/// residual on edges, vertices and the face border layer only
+void residual_restrict(const Operator& A, Function& rhs, Function& x, Function& r, Function& coarse,
+                       int coarse_level);
 void assign(double alpha, Function& x1, double beta, Function& x2, Function& dst, int level, uint8_t mask);
 void add_scaled(Function& dst, double gamma, Function& y, int level, uint8_t mask);
 void fill_const(Function& f, double value, int level, uint8_t mask);

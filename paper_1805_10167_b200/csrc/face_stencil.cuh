@@ -19,6 +19,13 @@ constexpr int FS_CWARPS = 4;                 // consumer warps
 constexpr int FS_THREADS = (FS_CWARPS + 1) * 32;
 constexpr int FS_COLS = FS_CWARPS * 64;      // 256 columns per CTA
 constexpr int FS_XW = FS_COLS + 4;           // staged x columns [c0-2, c0+FS_COLS+2)
+// fused residual+restriction (ST_RESTRICT_RESIDUAL): lane 0 of every warp
+// recomputes the previous warp's last pair, so each lane gets the residual at
+// c-1 by shuffle and no lane runs an extra chain: 31 new pairs per warp,
+// 248 columns per CTA, x staged from c0-4 and b from c0-2
+constexpr int FS_COLS_RR = FS_CWARPS * 62;   // 248
+constexpr int FS_XW_RR = FS_COLS_RR + 8;     // [c0-4, c0+252)
+constexpr int FS_BW_RR = FS_COLS_RR + 4;     // [c0-2, c0+250)
 // rows per band: long bands amortise the 2 halo rows at fine levels, short
 // ones give coarse levels enough CTAs (the row march is latency-bound there)
 __host__ __device__ __forceinline__ int fs_band(int n) { return n >= 1024 ? 64 : (n >= 512 ? 32 : (n >= 128 ? 16 : 8)); }
@@ -64,28 +71,53 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <int MODE> struct FaceSmem {
-    double x[FS_S][FS_XW];
-    double b[MODE == ST_APPLY ? 1 : FS_S][FS_COLS];
+    double x[FS_S][MODE == ST_RESTRICT_RESIDUAL ? FS_XW_RR : FS_XW];
+    double b[MODE == ST_APPLY ? 1 : FS_S][MODE == ST_RESTRICT_RESIDUAL ? FS_BW_RR : FS_COLS];
     uint64_t full[FS_S];
     uint64_t empty[FS_S];
 };
 
+// ST_RESTRICT_RESIDUAL: y is the coarse arena (level L-1, row offsets cro,
+// face stride cstride); the band is fs_band/2 coarse rows R, whose fine rows
+// 2R-1 .. 2R+1 are computed as residuals and restricted on the fly (see
+// k_residual_restrict_faces in transfer.cuh for why only face-interior fine
+// points are involved); nothing fine is stored.
 template <int MODE>
 __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, const double* __restrict__ x,
                                                                  const double* __restrict__ b,
-                                                                 double* __restrict__ y, double omega) {
+                                                                 double* __restrict__ y, double omega,
+                                                                 const int64_t* __restrict__ cro, int64_t cstride) {
+    constexpr bool RR = MODE == ST_RESTRICT_RESIDUAL;
+    constexpr int XOFF = RR ? 4 : 2;           // smem x index of column c0
+    constexpr int XW = RR ? FS_XW_RR : FS_XW;  // staged x width
+    constexpr int BOFF = RR ? 2 : 0;           // smem b index of column c0
+    constexpr int BW = RR ? FS_BW_RR : FS_COLS;
     __shared__ __align__(128) FaceSmem<MODE> sm;
     const int n = t.n, W = t.W;
     const int face = blockIdx.z;
-    const int c0 = blockIdx.x * FS_COLS;
+    const int c0 = blockIdx.x * (RR ? FS_COLS_RR : FS_COLS);
     const int rb = fs_band(t.n);
-    int r_lo = blockIdx.y * rb;
-    if (r_lo < 1) r_lo = 1;
-    int r_hi = (blockIdx.y + 1) * rb; // exclusive
-    if (r_hi > n - 1) r_hi = n - 1;     // interior rows r <= n-2
-    const int cmin = c0 < 1 ? 1 : c0;
-    if (r_hi > n - cmin) r_hi = n - cmin; // first column of the block stays interior
-    if (r_lo >= r_hi) return;           // CTA-uniform, before any barrier use
+    int r_lo, r_hi;
+    if (RR) {
+        const int nc = n / 2, cb = rb / 2;
+        int R_lo = blockIdx.y * cb;
+        if (R_lo < 1) R_lo = 1;
+        int R_hi = (blockIdx.y + 1) * cb;
+        if (R_hi > nc - 1) R_hi = nc - 1; // coarse interior rows 1..nc-2
+        const int Cmin = c0 / 2 < 1 ? 1 : c0 / 2;
+        if (R_hi > nc - Cmin) R_hi = nc - Cmin;
+        if (R_lo >= R_hi) return;
+        r_lo = 2 * R_lo - 1; // fine rows 2R_lo-1 .. 2R_hi-1
+        r_hi = 2 * R_hi;
+    } else {
+        r_lo = blockIdx.y * rb;
+        if (r_lo < 1) r_lo = 1;
+        r_hi = (blockIdx.y + 1) * rb;       // exclusive
+        if (r_hi > n - 1) r_hi = n - 1;     // interior rows r <= n-2
+        const int cmin = c0 < 1 ? 1 : c0;
+        if (r_hi > n - cmin) r_hi = n - cmin; // first column of the block stays interior
+        if (r_lo >= r_hi) return;           // CTA-uniform, before any barrier use
+    }
     const int nrows = r_hi - r_lo;      // computed rows
     const int nstage = nrows + 2;       // x rows r_lo-1 .. r_hi
 
@@ -112,19 +144,21 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                 mbar_wait(&sm.empty[s], ((i / FS_S) & 1) ^ 1);
                 const int q = r_lo - 1 + i; // x row of this stage
                 const int plen = (W - q + 3) & ~3; // padded row length
-                const int xs = c0 - 2 < 0 ? 0 : c0 - 2;
-                const int xe = c0 - 2 + FS_XW < plen ? c0 - 2 + FS_XW : plen;
+                const int xs = c0 - XOFF < 0 ? 0 : c0 - XOFF;
+                const int xe = c0 - XOFF + XW < plen ? c0 - XOFF + XW : plen;
                 const uint32_t bx = xe > xs ? uint32_t(xe - xs) * 8u : 0u;
                 uint32_t bb = 0;
-                int be = 0;
+                int bs0 = 0;
                 if (MODE != ST_APPLY && i >= 2) { // b row q-1 pairs with x row q
                     const int pb = (W - (q - 1) + 3) & ~3;
-                    be = c0 + FS_COLS < pb ? c0 + FS_COLS : pb;
-                    bb = be > c0 ? uint32_t(be - c0) * 8u : 0u;
+                    bs0 = c0 - BOFF < 0 ? 0 : c0 - BOFF;
+                    const int be = c0 - BOFF + BW < pb ? c0 - BOFF + BW : pb;
+                    bb = be > bs0 ? uint32_t(be - bs0) * 8u : 0u;
                 }
                 mbar_arrive_expect_tx(&sm.full[s], bx + bb);
-                if (bx) bulk_g2s(&sm.x[s][xs - (c0 - 2)], xf + ro[q] + xs, bx, &sm.full[s]);
-                if (MODE != ST_APPLY && bb) bulk_g2s(&sm.b[s][0], bf + ro[q - 1] + c0, bb, &sm.full[s]);
+                if (bx) bulk_g2s(&sm.x[s][xs - (c0 - XOFF)], xf + ro[q] + xs, bx, &sm.full[s]);
+                if (MODE != ST_APPLY && bb)
+                    bulk_g2s(&sm.b[s][bs0 - (c0 - BOFF)], bf + ro[q - 1] + bs0, bb, &sm.full[s]);
             }
         }
         return;
@@ -132,15 +166,20 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
 
     // ---------------- consumers: lane owns columns c, c+1
     const int tid = threadIdx.x; // 0 .. 127
-    const int c = c0 + 2 * tid;
-    const int k = 2 + 2 * tid; // smem index of column c
+    const int c = RR ? c0 + 2 * (31 * warp + lane - 1) : c0 + 2 * tid;
+    const int k = XOFF + (c - c0); // smem index of column c
+    const int kb = BOFF + (c - c0); // smem index of b at column c
     const double* co = t.face_coef + size_t(face) * 8;
     const double cW = co[0], cNW = co[1], cS = co[2], cC = co[3], cN = co[4], cSE = co[5], cE = co[6], dg = co[7];
     const double rdg = 1.0 / dg;
     double* __restrict__ yf = y + base;
 
-    // window: rows r-1 (m*) and r (z*) at columns c-1, c, c+1, c+2
+    // window: rows r-1 (m*) and r (z*) at columns c-1, c, c+1, c+2 (and c-2: *ll)
     double ml = 0, m0 = 0, m1 = 0, mr = 0, zl = 0, z0 = 0, z1 = 0, zr = 0;
+    // ST_RESTRICT_RESIDUAL: residual rows q-2 (s*) and q-1 (h*) at c-1, c, c+1
+    double sl = 0, s0 = 0, s1 = 0, hl = 0, h0 = 0, h1 = 0;
+    const int nc = n / 2;
+    const int C = c / 2; // coarse column of this lane (RR)
     for (int i = 0; i < nstage; ++i) {
         const int s = i % FS_S;
         mbar_wait(&sm.full[s], (i / FS_S) & 1);
@@ -149,11 +188,42 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         const double2 pc2 = *reinterpret_cast<const double2*>(sx + k);
         const double2 pr2 = *reinterpret_cast<const double2*>(sx + k + 2);
         double2 bb = make_double2(0.0, 0.0);
-        if (MODE != ST_APPLY && i >= 2) bb = *reinterpret_cast<const double2*>(&sm.b[s][2 * tid]);
+        if (MODE != ST_APPLY && i >= 2) bb = *reinterpret_cast<const double2*>(&sm.b[s][kb]);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
         const double pl = pl2.y, p0 = pc2.x, p1 = pc2.y, pr = pr2.x;
-        if (i >= 2) {
+        if (RR && i >= 2) {
+            // residual of fine row q at c, c+1, same operations as
+            // ST_RESIDUAL; every lane computes (the shuffle follows)
+            const int q = r_lo + i - 2;
+            double a0 = 0.0;
+            a0 += cW * zl;
+            a0 += cNW * pl;
+            a0 += cS * m0;
+            a0 += cC * z0;
+            a0 += cN * p0;
+            a0 += cSE * m1;
+            a0 += cE * z1;
+            double a1 = 0.0;
+            a1 += cW * z0;
+            a1 += cNW * p0;
+            a1 += cS * m1;
+            a1 += cC * z1;
+            a1 += cN * p1;
+            a1 += cSE * mr;
+            a1 += cE * zr;
+            const double o0 = bb.x - a0, o1 = bb.y - a1;
+            const double ol = __shfl_up_sync(0xffffffffu, o1, 1); // residual at c-1 (lane 0: unused)
+            if ((q & 1) && q >= r_lo + 2) { // q = 2R+1: restrict rows 2R-1 (s), 2R (h), 2R+1 (o)
+                const int R = (q - 1) / 2;
+                if (lane >= 1 && C >= 1 && C <= nc - 1 - R)
+                    // f(2c,2r) + 0.5*(W + E + S + N + SE + NW), left to right (k_restrict_faces)
+                    y[int64_t(face) * cstride + cro[R] + C] = h0 + 0.5 * (hl + h1 + s0 + o0 + s1 + ol);
+            }
+            sl = hl; s0 = h0; s1 = h1;
+            hl = ol; h0 = o0; h1 = o1;
+        }
+        if (!RR && i >= 2) {
             const int r = r_lo + i - 2;
             const int last = n - 1 - r; // last interior column of row r
             const bool v0 = c >= 1 && c <= last;
@@ -196,9 +266,16 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         zl = pl; z0 = p0; z1 = p1; zr = pr;
     }
     (void)ml;
+    (void)sl;
 }
 
 inline dim3 face_stencil_grid(const LevelTables& t) {
     return dim3(unsigned((t.n - 1 + FS_COLS - 1) / FS_COLS), unsigned((t.n - 1 + fs_band(t.n) - 1) / fs_band(t.n)),
+                unsigned(t.nfaces));
+}
+// ST_RESTRICT_RESIDUAL: bands of fs_band(n)/2 coarse rows
+inline dim3 face_rr_grid(const LevelTables& t) {
+    const int nc = t.n / 2, cb = fs_band(t.n) / 2;
+    return dim3(unsigned((t.n - 1 + FS_COLS_RR - 1) / FS_COLS_RR), unsigned((nc - 1 + cb - 1) / cb + 1),
                 unsigned(t.nfaces));
 }

@@ -463,9 +463,11 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
     if ((parts & 1) && (mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
         const dim3 grid = face_stencil_grid(t);
         switch (mode) {
-        case ST_APPLY: k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega); break;
-        case ST_RESIDUAL: k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega); break;
-        default: k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega); break;
+        case ST_APPLY: k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0); break;
+        case ST_RESIDUAL:
+            k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0);
+            break;
+        default: k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0); break;
         }
         check_launch("face stencil");
     }
@@ -558,6 +560,24 @@ void launch_restrict(const LevelTables& tc, const LevelTables& tf, const FlagTab
         k_restrict_faces<<<transfer_grid(tc.n, tc.nfaces), TR_WARPS * 32, 0, st>>>(tc, tf, xf, xc);
         check_launch("restrict faces");
     }
+    launch_restrict_ev(tc, tf, cf, xf, xc, mask, st);
+}
+
+void launch_residual_restrict_faces(const LevelTables& tc, const LevelTables& tf, const double* x, const double* b,
+                                    double* r, double* xc, cudaStream_t st) {
+    if (tf.nfaces <= 0 || tf.n < 3) return;
+    if (tc.n >= 3) {
+        k_face_stencil<ST_RESTRICT_RESIDUAL><<<face_rr_grid(tf), FS_THREADS, 0, st>>>(tf, x, b, xc, 0.0, tc.rowoff,
+                                                                                      tc.face_stride);
+        check_launch("residual+restrict faces");
+    }
+    const dim3 grid(unsigned((tf.n - 2 + 127) / 128), 3u, unsigned(tf.nfaces));
+    k_residual_layer<<<grid, 128, 0, st>>>(tf, x, b, r);
+    check_launch("residual border layer");
+}
+
+void launch_restrict_ev(const LevelTables& tc, const LevelTables& tf, const FlagTables& cf, const double* xf,
+                        double* xc, uint8_t mask, cudaStream_t st) {
     const int kb = kblocks_for(tc.n);
     const int blocks = tc.nedges * kb + (tc.nverts + 127) / 128;
     if (blocks > 0) {

@@ -47,7 +47,7 @@ struct FlagTables {
     const uint8_t* vtx_flag = nullptr;
 };
 
-enum StencilMode : int { ST_APPLY = 0, ST_RESIDUAL = 1, ST_JACOBI = 2 };
+enum StencilMode : int { ST_APPLY = 0, ST_RESIDUAL = 1, ST_JACOBI = 2, ST_RESTRICT_RESIDUAL = 3 };
 
 // ---- launchers (all asynchronous on `st`) ----
 // parts: 1 = face interiors (K1), 2 = edge lines + vertices (K2/K3), 3 = both
@@ -66,6 +66,14 @@ void launch_prolongate(const LevelTables& coarse, const LevelTables& fine, const
                        const double* xc, double* xf, uint8_t mask, bool add, cudaStream_t st);
 void launch_restrict(const LevelTables& coarse, const LevelTables& fine, const FlagTables& coarse_flags,
                      const double* xf, double* xc, uint8_t mask, cudaStream_t st);
+// edge/vertex part of launch_restrict only
+void launch_restrict_ev(const LevelTables& coarse, const LevelTables& fine, const FlagTables& coarse_flags,
+                        const double* xf, double* xc, uint8_t mask, cudaStream_t st);
+// fused residual + restriction on face interiors: xc (coarse face interiors)
+// := P^T (b - A x); r := b - A x on the fine faces' border layer only (row 1,
+// column 1, diagonal). fine tables carry the operator's coefficients.
+void launch_residual_restrict_faces(const LevelTables& coarse, const LevelTables& fine, const double* x,
+                                    const double* b, double* r, double* xc, cudaStream_t st);
 // hybrid Gauss-Seidel: face tiles (face, I, J, dependency bits) over skewed
 // coordinates (t = c + 2r in GS_TILE_COLS-wide slabs, rows in GS_TILE_ROWS),
 // queue ordered by I + J; per-tile done flags and the queue counter zeroed by

@@ -205,6 +205,32 @@ void restrict_to_coarse(Function& fine, Function& coarse, int lc, uint8_t mask) 
     d.timer_end();
 }
 
+// residual (reference solvers.cpp:418-419) + restrict_to_coarse (:420),
+// fused on face interiors: the fine residual there is never stored
+// (k_residual_restrict_faces); edges/vertices and the face layer next to the
+// borders are computed as in residual(), synced, and restricted as usual.
+void residual_restrict(const Operator& A, Function& rhs, Function& x, Function& r, Function& coarse, int lc) {
+    const int level = lc + 1;
+    check_op_function(A, rhs, level, "residual_restrict", false);
+    check_op_function(A, x, level, "residual_restrict", false);
+    check_op_function(A, r, level, "residual_restrict", true);
+    check_transfer(coarse, r, lc, "residual_restrict");
+    // coarse is written at coarse_level only, so it may be rhs or x (other levels)
+    if (&x == &r || &rhs == &r || &coarse == &r)
+        throw InvalidArgument("residual_restrict: r must be distinct from x, rhs and coarse");
+    Domain& d = A.domain();
+    d.sync(x, level);
+    const LevelTables t = A.tables(level);
+    const LevelTables& tc = d.level(lc).t;
+    d.timer_begin("residual_restrict");
+    launch_residual_restrict_faces(tc, t, x.data(level), rhs.data(level), r.data(level), coarse.data(lc), d.stream());
+    d.timer_end();
+    launch_stencil(ST_RESIDUAL, t, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
+                   d.stream(), 2);
+    d.sync(r, level);
+    launch_restrict_ev(tc, t, coarse.flags(), r.data(level), coarse.data(lc), ALL_FLAGS, d.stream());
+}
+
 void assign(double alpha, Function& x1, double beta, Function& x2, Function& dst, int level, uint8_t mask) {
     check_pair("assign", x1, x2, level);
     check_pair("assign", x1, dst, level);
@@ -462,8 +488,7 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
         return;
     }
     for (int i = 0; i < nu_pre; ++i) smooth(rhs, x, level);
-    residual(a_, rhs, x, r_, level);
-    restrict_to_coarse(r_, b_, level - 1, ALL_FLAGS);
+    residual_restrict(a_, rhs, x, r_, b_, level - 1); // residual + restrict_to_coarse, fused
     fill_const(b_, 0.0, level - 1, kDirichletMask);
     fill_const(e_, 0.0, level - 1, ALL_FLAGS);
     cycle(b_, e_, level - 1, nu_pre, nu_post);

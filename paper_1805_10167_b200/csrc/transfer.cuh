@@ -143,3 +143,44 @@ __global__ void __launch_bounds__(TR_WARPS * 32) k_restrict_faces(LevelTables tc
         s = cp;
     }
 }
+
+// ---------------------------------------------------------------------------
+// K6: fused residual + restriction, coarse := P^T (b - A x) on coarse face
+// interiors (the cycle's residual followed by restrict_to_coarse,
+// src/solvers.cpp:418-421). A coarse interior point (c, r) -- c, r >= 1,
+// c + r <= nc-1 -- restricts the seven fine points (2c, 2r), (2c+-1, 2r),
+// (2c, 2r+-1), (2c+1, 2r-1), (2c-1, 2r+1), all face-interior (c', r' >= 1,
+// c' + r' <= n-1), so the fine residual is computed on the fly from x (synced)
+// and b and never stored: 8 + 8 B per fine DoF read, 2 B written, instead of
+// 24 (residual) + 10 (restriction). The face part is k_face_stencil
+// <ST_RESTRICT_RESIDUAL> (face_stencil.cuh: TMA-staged rows, lanes own the
+// fine pairs (2c, 2c+1)); this file adds the border layer below.
+// ---------------------------------------------------------------------------
+// The fine residual on the face points next to the borders (row 1, column 1,
+// diagonal c + r = n-1): the sources of the edges' halo rows, which the
+// edge/vertex part of the restriction reads after a sync. Same formula as
+// k_face_stencil<RESIDUAL>.
+__global__ void __launch_bounds__(128) k_residual_layer(LevelTables t, const double* __restrict__ x,
+                                                        const double* __restrict__ b, double* __restrict__ r) {
+    const int n = t.n;
+    const int k = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > n - 2) return;
+    const int seg = blockIdx.y;
+    const int q = seg == 0 ? 1 : k;
+    const int c = seg == 0 ? k : (seg == 1 ? 1 : n - 1 - k);
+    const int64_t base = int64_t(blockIdx.z) * t.face_stride;
+    const int64_t* __restrict__ ro = t.rowoff;
+    const double* xm = x + base + ro[q - 1];
+    const double* x0 = x + base + ro[q];
+    const double* xp = x + base + ro[q + 1];
+    const double* co = t.face_coef + size_t(blockIdx.z) * 8;
+    double a = 0.0;
+    a += co[0] * x0[c - 1];
+    a += co[1] * xp[c - 1];
+    a += co[2] * xm[c];
+    a += co[3] * x0[c];
+    a += co[4] * xp[c];
+    a += co[5] * xm[c + 1];
+    a += co[6] * x0[c + 1];
+    r[base + ro[q] + c] = b[base + ro[q] + c] - a;
+}

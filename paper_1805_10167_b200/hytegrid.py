@@ -386,6 +386,13 @@ def restrict_to_coarse(ctl: Controller, fine: ScalarFunction, coarse: ScalarFunc
     check(lib.hyb_restrict(fine._h, coarse._h, coarse_level, flag_mask))
 
 
+def residual_restrict(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: ScalarFunction,  # noqa: ARG001
+                      r: ScalarFunction, coarse: ScalarFunction, coarse_level: int) -> None:
+    """coarse := P^T (rhs - A x) at coarse_level, fused on face interiors (the
+    V-cycle's residual + restrict_to_coarse); r is scratch."""
+    check(lib.hyb_residual_restrict(A._h, rhs._h, x._h, r._h, coarse._h, coarse_level))
+
+
 def assign(alpha: float, x1: ScalarFunction, beta: float, x2: ScalarFunction, dst: ScalarFunction, level: int,
            flag_mask: int = ALL_DOF_FLAGS) -> None:
     check(lib.hyb_assign(alpha, x1._h, beta, x2._h, dst._h, level, flag_mask))
