@@ -15,8 +15,13 @@
 // shared-memory copy of the tile plus halo (row r stored from c = 32 I - 2r - 2).
 // Warps take tiles from a global queue ordered by I + J and wait on the done
 // flags of the two predecessors, dequeued earlier, hence running or done: no
-// deadlock. Tile loads bypass L1 (__ldcg): neighbour tiles are written on other
-// SMs.
+// deadlock. Tile loads bypass L1 (cp.async.cg): neighbour tiles are written on
+// other SMs. Everything the predecessors do not write (own rows, E/N halo, b)
+// is staged before their flags are awaited; the step chain keeps W (own
+// previous result), SE (row below, by shuffle) and S (the previous SE) in
+// registers. Measured at L10 (512 faces): 3.6 ms per sweep; without the
+// 32-step compute it still takes 2.9 ms, so per-tile staging / write-back /
+// release latency at ~10 resident warps per SM bounds it, not FP64.
 #pragma once
 
 constexpr int GS_T = 32;           // t-width of a tile (steps)
@@ -49,6 +54,14 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
     double(*sx)[GS_XS] = s_x[warp];
     double(*sb)[GS_BS] = s_b[warp];
     const int64_t* __restrict__ ro = t.rowoff;
+    // staged chunk (q, o): row r0-1+q, columns c = t0 - 2r + o - 2 and +1
+    // (c even: 16-byte aligned), zero-filled outside the closed triangle
+    auto stage = [&](const double* xf, int t0, int r0, int q, int o) {
+        const int r = r0 - 1 + q, c = t0 - 2 * r + o - 2;
+        const int len = r <= n ? n - r : -1; // last column of row r
+        const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
+        cp_async16(&sx[q][o], bytes ? xf + ro[r] + c : xf, bytes);
+    };
     for (;;) {
         int idx = 0;
         if (lane == 0) idx = atomicAdd(counter, 1);
@@ -59,6 +72,24 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
         // a point's dependencies (t-1, t-2 in rows r, r-1) lie in exactly those
         const int face = tl.x, ti = tl.y, tj = tl.z, has = tl.w;
         int* fflags = flags + int64_t(face) * ni * nj;
+        const int t0 = ti * GS_T, r0 = 1 + tj * GS_R;
+        const double* xf = x + int64_t(face) * t.face_stride;
+        const double* bf = b + int64_t(face) * t.face_stride;
+        // (1) before the predecessors are done: everything they do not write --
+        // the tile's own rows and the north row from t0 on (own points, E and N
+        // halo: old values), and the tile's b
+        for (int e = lane; e < (GS_R + 1) * (GS_K / 2 - 1); e += 32)
+            stage(xf, t0, r0, 1 + e / (GS_K / 2 - 1), 2 + 2 * (e % (GS_K / 2 - 1)));
+        for (int e = lane; e < GS_R * (GS_T / 2); e += 32) {
+            const int qb = e / (GS_T / 2), o = 2 * (e % (GS_T / 2));
+            const int rb = r0 + qb, c = t0 - 2 * rb + o;
+            const int len = rb <= n ? n - rb : -1;
+            const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
+            cp_async16(&sb[qb][o], bytes ? bf + ro[rb] + c : bf, bytes);
+        }
+        const int r = r0 + lane; // this lane's row
+        // (2) wait for W / S / SW, then stage what they wrote: the W halo
+        // (chunk o = 0 of the own rows) and the south row
         if (lane == 0) {
             if (has & 1) wait_flag(fflags + tj * ni + (ti - 1));
             if (has & 2) wait_flag(fflags + (tj - 1) * ni + ti);
@@ -66,48 +97,45 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
             __threadfence();
         }
         __syncwarp();
-        const int t0 = ti * GS_T, r0 = 1 + tj * GS_R;
-        const double* xf = x + int64_t(face) * t.face_stride;
-        const double* bf = b + int64_t(face) * t.face_stride;
-        // stage rows r0-1 .. r0+32 (row r holds c = t0 - 2r + kk, kk in
-        // [-2, 34)) and the tile's b with 16-byte cp.async.cg copies (L2 only,
-        // all in flight at once, zero-fill outside the closed triangle)
-        for (int e = lane; e < (GS_R + 2) * (GS_K / 2); e += 32) {
-            const int q = e / (GS_K / 2), o = 2 * (e % (GS_K / 2));
-            const int r = r0 - 1 + q, c = t0 - 2 * r + o - 2; // c is even: 16-byte aligned
-            const int len = r <= n ? n - r : -1;              // last column of row r
-            const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
-            cp_async16(&sx[q][o], bytes ? xf + ro[r] + c : xf, bytes);
-        }
-        for (int e = lane; e < GS_R * (GS_T / 2); e += 32) {
-            const int q = e / (GS_T / 2), o = 2 * (e % (GS_T / 2));
-            const int r = r0 + q, c = t0 - 2 * r + o;
-            const int len = r <= n ? n - r : -1;
-            const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
-            cp_async16(&sb[q][o], bytes ? bf + ro[r] + c : bf, bytes);
+        for (int e = lane; e < GS_R + GS_K / 2; e += 32) {
+            if (e < GS_R) stage(xf, t0, r0, 1 + e, 0);
+            else stage(xf, t0, r0, 0, 2 * (e - GS_R));
         }
         cp_async_wait_all();
         __syncwarp();
         const double* co = t.face_coef + size_t(face) * 8;
         const double cW = co[0], cNW = co[1], cS = co[2], cC = co[3], cN = co[4], cSE = co[5], cE = co[6], dg = co[7];
         const double rdg = 1.0 / dg;
-        const int q = lane + 1, r = r0 + lane; // this lane's row
+        const int q = lane + 1;
+        // dependencies in registers: W = this lane's previous result, SE =
+        // the row below's previous result (shuffle), S = the SE of one step
+        // earlier; lane 0's row below is the staged south row
+        double w = sx[q][1];           // (t0-1, r)
+        double s_prev = sx[q - 1][1];  // (t0-1, r-1): S of step 1
+        double res = 0.0;
+#pragma unroll
         for (int kk = 0; kk < GS_T; ++kk) {
+            const int k = kk + 2; // staged column of (c, r)
+            const double up = __shfl_up_sync(0xffffffffu, res, 1);
+            const double S = kk == 0 ? sx[q - 1][k - 2] : (lane == 0 ? sx[0][k - 2] : s_prev);
+            const double SE = (kk == 0 || lane == 0) ? sx[q - 1][k - 1] : up;
+            const double Cv = sx[q][k];
             const int c = t0 + kk - 2 * r;
-            if (r <= n - 2 && c >= 1 && c + r <= n - 1) {
-                const int k = kk + 2; // staged column of (c, r)
-                double acc = 0.0;     // reference term order, in-place operands
-                acc += cW * sx[q][k - 1];
-                acc += cNW * sx[q + 1][k + 1];
-                acc += cS * sx[q - 1][k - 2];
-                acc += cC * sx[q][k];
-                acc += cN * sx[q + 1][k + 2];
-                acc += cSE * sx[q - 1][k - 1];
-                acc += cE * sx[q][k + 1];
-                sx[q][k] = sx[q][k] + div_by(sb[lane][kk] - acc, dg, rdg);
-            }
-            __syncwarp();
+            double acc = 0.0; // reference term order
+            acc += cW * w;
+            acc += cNW * sx[q + 1][k + 1];
+            acc += cS * S;
+            acc += cC * Cv;
+            acc += cN * sx[q + 1][k + 2];
+            acc += cSE * SE;
+            acc += cE * sx[q][k + 1];
+            const bool valid = r <= n - 2 && c >= 1 && c + r <= n - 1;
+            res = valid ? Cv + div_by(sb[lane][kk] - acc, dg, rdg) : Cv;
+            sx[q][k] = res;
+            w = res;
+            s_prev = SE;
         }
+        __syncwarp();
         double* xw = x + int64_t(face) * t.face_stride;
         for (int qq = 0; qq < GS_R; ++qq) { // write back row by row (coalesced)
             const int rr = r0 + qq, c = t0 - 2 * rr + lane;

@@ -521,7 +521,7 @@ void launch_gs_faces(const LevelTables& t, const double* b, double* x, const int
                      int* flags, int* counter, cudaStream_t st) {
     if (ntiles <= 0) return;
     int blocks = (ntiles + GS_WARPS - 1) / GS_WARPS;
-    if (blocks > 148 * 8) blocks = 148 * 8; // warps pull tiles from the queue
+    if (blocks > 148 * 8) blocks = 148 * 8; // persistent warps pull tiles from the queue
     k_gs_faces<<<blocks, GS_WARPS * 32, 0, st>>>(t, b, x, tiles, ntiles, ni, nj, flags, counter);
     check_launch("gauss-seidel faces");
 }
