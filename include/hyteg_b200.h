@@ -142,6 +142,17 @@ int hyb_function_create(hyb_domain* d, const char* name, int min_level, int max_
 int hyb_function_destroy(hyb_function* f);
 int hyb_function_upload(hyb_function* f, int level, const double* host, int64_t n, int global_order, uint8_t mask);
 int hyb_function_download(hyb_function* f, int level, double* host, int64_t n, int global_order);
+/* Stream-ordered variants for pipelines (no reference counterpart): this
+ * process's owned DoFs in local order (= GlobalDoFMap order when the process
+ * owns every primitive). The copy runs on the domain's H2D / D2H stream after
+ * the work already queued; later operations see an upload's values; a
+ * download's host buffer is complete after hyb_domain_synchronize (or any call
+ * that returns host data), and later operations on the domain wait for it
+ * before touching device data. Page-locked host memory (hyb_host_alloc) makes
+ * the copies asynchronous, so one step's uploads overlap the previous step's
+ * downloads. The host buffer must stay valid until the copy completes. */
+int hyb_function_upload_async(hyb_function* f, int level, const double* host, int64_t n, uint8_t mask);
+int hyb_function_download_async(hyb_function* f, int level, double* host, int64_t n);
 int hyb_function_flags(hyb_function* f, int level, uint8_t* flags, int64_t n, int global_order);
 /* interpolate(f, const, level, mask) (function.hpp:55-56) */
 int hyb_interpolate_const(hyb_function* f, double value, int level, uint8_t mask);

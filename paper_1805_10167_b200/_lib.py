@@ -95,6 +95,8 @@ _SIGS = {
     "hyb_function_destroy": (_i, [_p]),
     "hyb_function_upload": (_i, [_p, _i, _pd, _i64, _i, _u8]),
     "hyb_function_download": (_i, [_p, _i, _pd, _i64, _i]),
+    "hyb_function_upload_async": (_i, [_p, _i, _pd, _i64, _u8]),
+    "hyb_function_download_async": (_i, [_p, _i, _pd, _i64]),
     "hyb_function_flags": (_i, [_p, _i, _pu8, _i64, _i]),
     "hyb_interpolate_const": (_i, [_p, _d, _i, _u8]),
     "hyb_interpolate_random": (_i, [_p, _i, _u64, _u64, _d, _d, _u8]),

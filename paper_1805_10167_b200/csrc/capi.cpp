@@ -423,6 +423,22 @@ int hyb_function_download(hyb_function* f, int level, double* host, int64_t n, i
     });
 }
 
+int hyb_function_upload_async(hyb_function* f, int level, const double* host, int64_t n, uint8_t mask) {
+    return guarded([&] {
+        need(f, "hyb_function_upload_async");
+        need(host, "hyb_function_upload_async");
+        hyb::upload_async(*f->f, level, host, n, mask);
+    });
+}
+
+int hyb_function_download_async(hyb_function* f, int level, double* host, int64_t n) {
+    return guarded([&] {
+        need(f, "hyb_function_download_async");
+        need(host, "hyb_function_download_async");
+        hyb::download_async(*f->f, level, host, n);
+    });
+}
+
 int hyb_function_flags(hyb_function* fh, int level, uint8_t* flags, int64_t n, int global_order) {
     return guarded([&] {
         need(fh, "hyb_function_flags");

@@ -113,6 +113,10 @@ Domain::Domain(const std::string& mesh_text, int world_ranks, const std::vector<
     HYB_CUDA(cudaSetDevice(device_));
     HYB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     HYB_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+    HYB_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+    HYB_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+    HYB_CUDA(cudaEventCreateWithFlags(&ev_xfer_, cudaEventDisableTiming));
+    HYB_CUDA(cudaEventCreateWithFlags(&ev_down_, cudaEventDisableTiming));
     HYB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     HYB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     place_ = place(g_, rank_of_, local_ranks_);
@@ -129,8 +133,49 @@ Domain::~Domain() {
     if (nccl_comm_) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (ev_xfer_) cudaEventDestroy(ev_xfer_);
+    if (ev_down_) cudaEventDestroy(ev_down_);
+    if (h2d_) cudaStreamDestroy(h2d_);
+    if (d2h_) cudaStreamDestroy(d2h_);
     if (aux_) cudaStreamDestroy(aux_);
     if (stream_) cudaStreamDestroy(stream_);
+}
+
+double* Domain::stage_h2d(int64_t doubles) {
+    if (int64_t(stage_h2d_.bytes() / 8) < doubles) {
+        HYB_CUDA(cudaStreamSynchronize(h2d_));
+        stage_h2d_ = DevMem(size_t(std::max<int64_t>(doubles, 1)) * 8);
+    }
+    return stage_h2d_.as<double>();
+}
+
+double* Domain::stage_d2h(int64_t doubles) {
+    if (int64_t(stage_d2h_.bytes() / 8) < doubles) {
+        HYB_CUDA(cudaStreamSynchronize(d2h_));
+        stage_d2h_ = DevMem(size_t(std::max<int64_t>(doubles, 1)) * 8);
+    }
+    return stage_d2h_.as<double>();
+}
+
+void Domain::after_main(cudaStream_t s) {
+    HYB_CUDA(cudaEventRecord(ev_xfer_, stream_));
+    HYB_CUDA(cudaStreamWaitEvent(s, ev_xfer_, 0));
+}
+
+void Domain::main_waits(cudaStream_t s) {
+    HYB_CUDA(cudaEventRecord(ev_xfer_, s));
+    HYB_CUDA(cudaStreamWaitEvent(stream_, ev_xfer_, 0));
+}
+
+void Domain::download_issued() {
+    HYB_CUDA(cudaEventRecord(ev_down_, d2h_)); // covers every earlier download (one stream)
+    down_pending_ = true;
+}
+
+void Domain::settle_transfers() {
+    if (!down_pending_) return;
+    HYB_CUDA(cudaStreamWaitEvent(stream_, ev_down_, 0));
+    down_pending_ = false;
 }
 
 bool Domain::is_local_rank(int r) const {
@@ -284,7 +329,12 @@ void Domain::timer_reset() {
     timers_.clear();
 }
 
-void Domain::synchronize() { HYB_CUDA(cudaStreamSynchronize(stream_)); }
+void Domain::synchronize() {
+    HYB_CUDA(cudaStreamSynchronize(stream_));
+    HYB_CUDA(cudaStreamSynchronize(h2d_));
+    HYB_CUDA(cudaStreamSynchronize(d2h_));
+    down_pending_ = false;
+}
 
 void Domain::fork() {
     HYB_CUDA(cudaEventRecord(ev_fork_, stream_));
@@ -383,8 +433,15 @@ void Function::check_level(int level, const char* op) const {
                          ", " + std::to_string(max_) + "] of '" + name_ + "'");
 }
 
-double* Function::data(int level) const { return arenas_.at(size_t(level - min_)).as<double>(); }
-DevMem& Function::arena(int level) { return arenas_.at(size_t(level - min_)); }
+double* Function::data(int level) const {
+    dom_->settle_transfers();
+    return arenas_.at(size_t(level - min_)).as<double>();
+}
+DevMem& Function::arena(int level) {
+    dom_->settle_transfers();
+    return arenas_.at(size_t(level - min_));
+}
+double* Function::raw(int level) const { return arenas_.at(size_t(level - min_)).as<double>(); }
 
 // ---------------------------------------------------------------- Operator
 Operator::Operator(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc)

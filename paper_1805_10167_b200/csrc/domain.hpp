@@ -85,8 +85,12 @@ class Function {
     int min_level() const { return min_; }
     int max_level() const { return max_; }
     const BoundaryMap& bc() const { return bc_; }
+    /// arena of `level` for an operation: first makes the domain stream wait
+    /// for any asynchronous download still reading device data
     double* data(int level) const;
     DevMem& arena(int level);
+    /// arena without that wait (the asynchronous transfers themselves)
+    double* raw(int level) const;
     FlagTables flags() const { return {edge_flag_.as<uint8_t>(), vtx_flag_.as<uint8_t>()}; }
     void check_level(int level, const char* op) const;
 
@@ -202,7 +206,26 @@ class Domain {
     void fork(); // aux stream waits for the main stream
     void join(); // main stream waits for the aux stream
 
+    /// Asynchronous host transfers (upload_async / download_async): copies run
+    /// on their own H2D / D2H streams, after the work already queued on the
+    /// main stream; an upload is waited for by the main stream at once, a
+    /// download only when the main stream next touches function data
+    /// (settle_transfers), so the next step's uploads overlap this step's
+    /// downloads over the full-duplex link.
+    cudaStream_t h2d_stream() const { return h2d_; }
+    cudaStream_t d2h_stream() const { return d2h_; }
+    double* stage_h2d(int64_t doubles);
+    double* stage_d2h(int64_t doubles);
+    void after_main(cudaStream_t s);       // s waits for the main stream's queued work
+    void main_waits(cudaStream_t s);       // the main stream waits for s's queued work
+    void download_issued();                // a download is in flight on the D2H stream
+    void settle_transfers();               // main stream waits for in-flight downloads
+
   private:
+    cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+    cudaEvent_t ev_xfer_ = nullptr, ev_down_ = nullptr;
+    bool down_pending_ = false;
+    DevMem stage_h2d_, stage_d2h_;
     std::map<int, GsPlan> gs_;
     cudaStream_t aux_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
@@ -247,6 +270,9 @@ double dot(Function& a, Function& b, int level);
 double max_abs(Function& a, int level);
 void upload(Function& f, int level, const double* host, int64_t n, bool global_order, uint8_t mask);
 void download(Function& f, int level, double* host, int64_t n, bool global_order);
+/// stream-ordered host transfers in local order (Domain::h2d_stream)
+void upload_async(Function& f, int level, const double* host, int64_t n, uint8_t mask);
+void download_async(Function& f, int level, double* host, int64_t n);
 
 enum Smoother : int { SMOOTH_JACOBI = 0, SMOOTH_GS = 1, SMOOTH_CGS = 2 };
 

@@ -341,6 +341,37 @@ void upload(Function& f, int level, const double* host, int64_t n, bool global_o
     launch_scatter_owned(t, f.flags(), stage, f.data(level), mask, d.stream());
 }
 
+// Stream-ordered transfers for pipelines (see Domain::h2d_stream): `host`
+// holds this process's owned DoFs in local order (GlobalDoFMap order when the
+// process owns every primitive); pinned memory makes the copies asynchronous.
+void upload_async(Function& f, int level, const double* host, int64_t n, uint8_t mask) {
+    f.check_level(level, "upload_async");
+    Domain& d = f.domain();
+    const LevelTables& t = d.level(level).t;
+    if (n != t.owned_local)
+        throw InvalidArgument("upload_async: vector has " + std::to_string(n) + " entries, expected " +
+                              std::to_string(t.owned_local));
+    double* stage = d.stage_h2d(n);
+    d.after_main(d.h2d_stream()); // earlier work may still read f
+    HYB_CUDA(cudaMemcpyAsync(stage, host, size_t(n) * 8, cudaMemcpyHostToDevice, d.h2d_stream()));
+    launch_scatter_owned(t, f.flags(), stage, f.raw(level), mask, d.h2d_stream());
+    d.main_waits(d.h2d_stream()); // later work reads the new values
+}
+
+void download_async(Function& f, int level, double* host, int64_t n) {
+    f.check_level(level, "download_async");
+    Domain& d = f.domain();
+    const LevelTables& t = d.level(level).t;
+    if (n != t.owned_local)
+        throw InvalidArgument("download_async: vector has " + std::to_string(n) + " entries, expected " +
+                              std::to_string(t.owned_local));
+    double* stage = d.stage_d2h(n);
+    d.after_main(d.d2h_stream()); // the values f holds once the queued work is done
+    launch_gather_owned(t, f.raw(level), stage, d.d2h_stream());
+    HYB_CUDA(cudaMemcpyAsync(host, stage, size_t(n) * 8, cudaMemcpyDeviceToHost, d.d2h_stream()));
+    d.download_issued();
+}
+
 void download(Function& f, int level, double* host, int64_t n, bool global_order) {
     f.check_level(level, "download");
     Domain& d = f.domain();
@@ -457,6 +488,7 @@ void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int
         return;
     }
     cudaGraph_t graph = nullptr;
+    d.settle_transfers(); // no wait on an outside event inside the capture
     HYB_CUDA(cudaStreamBeginCapture(d.stream(), cudaStreamCaptureModeThreadLocal));
     try {
         cycle(rhs, x, level, nu_pre, nu_post);

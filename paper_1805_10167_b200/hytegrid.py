@@ -283,6 +283,21 @@ class ScalarFunction:
         check(lib.hyb_function_download(self._h, level, _pd(out), n, int(global_order)))
         return out
 
+    def upload_async(self, level: int, values: np.ndarray, mask: int = ALL_DOF_FLAGS) -> None:
+        """Stream-ordered upload of this process's owned DoFs (local order);
+        `values` (float64, contiguous; page-locked for overlap, see
+        PinnedBuffer) must stay alive until the domain synchronises."""
+        if values.dtype != np.float64 or not values.flags["C_CONTIGUOUS"]:
+            raise ValueError("upload_async needs a contiguous float64 array (no temporary copy)")
+        check(lib.hyb_function_upload_async(self._h, level, _pd(values), values.size, mask))
+
+    def download_async(self, level: int, out: np.ndarray) -> None:
+        """Stream-ordered download into `out` (local order), complete after
+        domain.synchronize()."""
+        if out.dtype != np.float64 or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError("download_async needs a contiguous float64 array")
+        check(lib.hyb_function_download_async(self._h, level, _pd(out), out.size))
+
     def flags(self, level: int, global_order: bool = True) -> np.ndarray:
         n = self._n(level, global_order)
         out = np.zeros(n, dtype=np.uint8)
