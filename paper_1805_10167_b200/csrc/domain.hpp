@@ -252,6 +252,8 @@ class Domain {
 void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t mask);
 void residual(const Operator& A, Function& rhs, Function& x, Function& r, int level);
 void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level);
+/// first sweep from x = 0: does not read x (Hierarchy::cycle)
+void smooth_jacobi_zero(const Operator& A, Function& rhs, Function& x, double omega, int level);
 void smooth_gs(const Operator& A, Function& rhs, Function& x, int level);
 void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level);
 void diagonal(const Operator& A, Function& d, int level);
@@ -295,12 +297,12 @@ class Hierarchy {
     int last_coarse_iterations = 0;
 
   private:
-    void cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post);
+    void cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero = false);
     void coarse_correct(Function& rhs, Function& x);
     void smooth(Function& rhs, Function& x, int level);
     void check_coarse(); // throws if the last coarse solve did not converge
-    void run_cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post);
-    std::vector<const void*> graph_key(Function& rhs, Function& x, int level, int nu_pre, int nu_post);
+    void run_cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero = false);
+    std::vector<const void*> graph_key(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero);
 
     // CUDA-graph replay of whole V-cycles: a cycle with an even number of
     // Jacobi sweeps per level leaves every arena where it found it, so the

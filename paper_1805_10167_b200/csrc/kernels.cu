@@ -55,6 +55,10 @@ __global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl
         if (!(f & mask)) return;
         const int64_t off = t.edge_off[e];
         const double* L = x + off;
+        if (MODE == ST_JACOBI_ZERO) {
+            y[off + k] = (f & F_DIRICHLET) ? b[off + k] : 0.0 + omega * (b[off + k] - 0.0) / t.edge_coef[size_t(e) * 8 + 7];
+            return;
+        }
         if (f & F_DIRICHLET) {
             y[off + k] = MODE == ST_RESIDUAL ? b[off + k] - L[k] : L[k];
             return;
@@ -83,6 +87,11 @@ __global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl
     const uint8_t f = fl.vtx_flag[v];
     if (!(f & mask)) return;
     const int64_t off = t.vtx_off[v];
+    if (MODE == ST_JACOBI_ZERO) {
+        const int ne0 = t.vtx_ne[v];
+        y[off] = (f & F_DIRICHLET) ? b[off] : 0.0 + omega * (b[off] - 0.0) / t.vtx_coef[t.vtx_coef_off[v] + ne0 + 1];
+        return;
+    }
     if (f & F_DIRICHLET) {
         y[off] = MODE == ST_RESIDUAL ? b[off] - x[off] : x[off];
         return;
@@ -457,8 +466,39 @@ inline int kblocks_for(int n) { return n - 1 > 0 ? (n - 1 + 127) / 128 : 0; }
 // ===========================================================================
 int64_t kernel_launch_count() { return g_launches.load(); }
 
+// face part of ST_JACOBI_ZERO: every slot of every face (border and padding
+// slots get values nobody reads before the next ghost refresh), double2-wide
+__global__ void __launch_bounds__(256) k_jacobi_zero_faces(LevelTables t, const double* __restrict__ b,
+                                                           double* __restrict__ y, double omega) {
+    const int face = blockIdx.y;
+    const double dg = t.face_coef[size_t(face) * 8 + 7];
+    const double rdg = 1.0 / dg;
+    const int64_t base = int64_t(face) * t.face_stride;
+    const double2* bb = reinterpret_cast<const double2*>(b + base);
+    double2* yy = reinterpret_cast<double2*>(y + base);
+    const int64_t n2 = t.face_stride / 2;
+    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n2; i += int64_t(gridDim.x) * 256) {
+        const double2 v = __ldcs(bb + i);
+        __stcs(yy + i, make_double2(0.0 + div_by(omega * (v.x - 0.0), dg, rdg), 0.0 + div_by(omega * (v.y - 0.0), dg, rdg)));
+    }
+}
+
 void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const double* x, const double* b, double* y,
                     double omega, uint8_t mask, cudaStream_t st, int parts) {
+    if (mode == ST_JACOBI_ZERO) {
+        if ((parts & 1) && t.nfaces > 0 && t.n >= 3) {
+            const int64_t per = (t.face_stride / 2 + 255) / 256;
+            k_jacobi_zero_faces<<<dim3(unsigned(per < 64 ? per : 64), unsigned(t.nfaces)), 256, 0, st>>>(t, b, y, omega);
+            check_launch("jacobi zero-guess faces");
+        }
+        const int kb = kblocks_for(t.n);
+        const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+        if ((parts & 2) && blocks > 0) {
+            k_ev_stencil<ST_JACOBI_ZERO><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb);
+            check_launch("edge/vertex stencil");
+        }
+        return;
+    }
     // faces: interior DoFs are INNER; only present for n >= 3
     if ((parts & 1) && (mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
         const dim3 grid = face_stencil_grid(t);

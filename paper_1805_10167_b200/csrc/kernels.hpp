@@ -47,7 +47,11 @@ struct FlagTables {
     const uint8_t* vtx_flag = nullptr;
 };
 
-enum StencilMode : int { ST_APPLY = 0, ST_RESIDUAL = 1, ST_JACOBI = 2, ST_RESTRICT_RESIDUAL = 3 };
+// ST_JACOBI_ZERO: a weighted-Jacobi sweep from x = 0 (the V-cycle's coarse
+// corrections, PCG's z): y = 0 + omega * (b - 0) / diag on non-Dirichlet rows,
+// y = b on Dirichlet rows (x there would be the cycle's assign of rhs);
+// bitwise the ST_JACOBI sweep of a zero-filled x, without reading x
+enum StencilMode : int { ST_APPLY = 0, ST_RESIDUAL = 1, ST_JACOBI = 2, ST_RESTRICT_RESIDUAL = 3, ST_JACOBI_ZERO = 4 };
 
 // ---- launchers (all asynchronous on `st`) ----
 // parts: 1 = face interiors (K1), 2 = edge lines + vertices (K2/K3), 3 = both

@@ -115,6 +115,24 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
     x.arena(level).swap(next);
 }
 
+// the first weighted-Jacobi sweep of a cycle whose x starts at zero (see
+// ST_JACOBI_ZERO): x is neither synced nor read; Dirichlet rows take rhs,
+// exactly what the cycle's assign would have put there
+void smooth_jacobi_zero(const Operator& A, Function& rhs, Function& x, double omega, int level) {
+    check_op_function(A, rhs, level, "smooth_jacobi", true);
+    check_op_function(A, x, level, "smooth_jacobi", true);
+    if (&rhs == &x) throw InvalidArgument("smooth_jacobi: rhs and x must be distinct functions");
+    check_diagonals(A, x, level, "smooth_jacobi");
+    Domain& d = A.domain();
+    DevMem& next = d.jacobi_scratch(level);
+    const LevelTables t = A.tables(level);
+    d.timer_begin("jacobi_zero");
+    launch_stencil(ST_JACOBI_ZERO, t, x.flags(), nullptr, rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
+                   d.stream(), 3);
+    d.timer_end();
+    x.arena(level).swap(next);
+}
+
 // hybrid Gauss-Seidel (reference smooth_gs, src/operators.cpp:423-482): one
 // sync, then every primitive in place in lattice order with frozen halos;
 // faces (wavefront tiles) and edges/vertices are independent, so the latter
@@ -447,10 +465,12 @@ Hierarchy::~Hierarchy() {
         if (g.exec) cudaGraphExecDestroy(g.exec);
 }
 
-std::vector<const void*> Hierarchy::graph_key(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
+std::vector<const void*> Hierarchy::graph_key(Function& rhs, Function& x, int level, int nu_pre, int nu_post,
+                                              bool x_zero) {
     std::vector<const void*> k{&rhs, &x, rhs.data(level), x.data(level), reinterpret_cast<const void*>(intptr_t(level)),
                                reinterpret_cast<const void*>(intptr_t(nu_pre)),
-                               reinterpret_cast<const void*>(intptr_t(nu_post))};
+                               reinterpret_cast<const void*>(intptr_t(nu_post)),
+                               reinterpret_cast<const void*>(intptr_t(x_zero))};
     for (int l = a_.min_level(); l <= level; ++l) {
         k.push_back(r_.data(l));
         if (l < level) {
@@ -465,15 +485,15 @@ std::vector<const void*> Hierarchy::graph_key(Function& rhs, Function& x, int le
 // One cycle, replayed from a CUDA graph when possible: the first call with a
 // given argument/arena state runs eagerly (allocations, plans), the second
 // captures the whole cycle (kernels, copies, NCCL) and later calls replay it.
-void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
+void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero) {
     Domain& d = *dom_;
     const bool swaps_restore = smoother_ != SMOOTH_JACOBI || (nu_pre + nu_post) % 2 == 0; // GS works in place
     if (!use_graphs || !swaps_restore || d.profiling) {
-        cycle(rhs, x, level, nu_pre, nu_post);
+        cycle(rhs, x, level, nu_pre, nu_post, x_zero);
         check_coarse();
         return;
     }
-    const std::vector<const void*> key = graph_key(rhs, x, level, nu_pre, nu_post);
+    const std::vector<const void*> key = graph_key(rhs, x, level, nu_pre, nu_post, x_zero);
     for (const auto& g : graphs_)
         if (g.key == key) {
             HYB_CUDA(cudaGraphLaunch(g.exec, d.stream()));
@@ -482,7 +502,7 @@ void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int
             return;
         }
     if (std::find(warm_.begin(), warm_.end(), key) == warm_.end()) {
-        cycle(rhs, x, level, nu_pre, nu_post);
+        cycle(rhs, x, level, nu_pre, nu_post, x_zero);
         check_coarse();
         warm_.push_back(key);
         return;
@@ -491,7 +511,7 @@ void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int
     d.settle_transfers(); // no wait on an outside event inside the capture
     HYB_CUDA(cudaStreamBeginCapture(d.stream(), cudaStreamCaptureModeThreadLocal));
     try {
-        cycle(rhs, x, level, nu_pre, nu_post);
+        cycle(rhs, x, level, nu_pre, nu_post, x_zero);
     } catch (...) {
         cudaStreamEndCapture(d.stream(), &graph);
         if (graph) cudaGraphDestroy(graph);
@@ -502,7 +522,7 @@ void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int
     const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     HYB_CUDA(ie);
-    if (graph_key(rhs, x, level, nu_pre, nu_post) != key) { // capture ran no kernels, only host bookkeeping
+    if (graph_key(rhs, x, level, nu_pre, nu_post, x_zero) != key) { // capture ran no kernels, only host bookkeeping
         cudaGraphExecDestroy(exec);
         throw LogicError("vcycle: arena state not restored by the captured cycle");
     }
@@ -512,18 +532,25 @@ void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int
     check_coarse();
 }
 
-// reference src/solvers.cpp:406-428 with the smoother of the configuration
-void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
-    assign(1.0, rhs, 0.0, rhs, x, level, kDirichletMask);
+// reference src/solvers.cpp:406-428 with the smoother of the configuration.
+// x_zero: x is known to be zero (a coarse correction, PCG's z); with Jacobi
+// pre-smoothing the zero-fill, the Dirichlet assign and the first sweep's read
+// of x are replaced by one zero-guess sweep (bitwise the same values).
+void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero) {
+    const bool zero_sweep = x_zero && level > a_.min_level() && nu_pre > 0 && smoother_ == SMOOTH_JACOBI;
+    if (x_zero && !zero_sweep) fill_const(x, 0.0, level, ALL_FLAGS);
+    if (!zero_sweep) assign(1.0, rhs, 0.0, rhs, x, level, kDirichletMask);
     if (level == a_.min_level()) {
         coarse_correct(rhs, x);
         return;
     }
-    for (int i = 0; i < nu_pre; ++i) smooth(rhs, x, level);
+    for (int i = 0; i < nu_pre; ++i) {
+        if (i == 0 && zero_sweep) smooth_jacobi_zero(a_, rhs, x, omega_, level);
+        else smooth(rhs, x, level);
+    }
     residual_restrict(a_, rhs, x, r_, b_, level - 1); // residual + restrict_to_coarse, fused
     fill_const(b_, 0.0, level - 1, kDirichletMask);
-    fill_const(e_, 0.0, level - 1, ALL_FLAGS);
-    cycle(b_, e_, level - 1, nu_pre, nu_post);
+    cycle(b_, e_, level - 1, nu_pre, nu_post, true); // e = 0 on entry
     // prolongate(e -> r) + add_scaled(x, 1, r) on the smooth mask, fused
     prolongate(e_, x, level - 1, kSmoothMask, true);
     for (int i = 0; i < nu_post; ++i) smooth(rhs, x, level);
@@ -649,8 +676,7 @@ std::vector<double> Hierarchy::pcg(Function& rhs, Function& x, int level, int ma
     residual(a_, rhs, x, r, level);
     std::vector<double> res{std::sqrt(dot(r, r, level))};
     const double target = tol * res.front();
-    fill_const(z, 0.0, level, ALL_FLAGS);
-    run_cycle(r, z, level, nu_pre, nu_post);
+    run_cycle(r, z, level, nu_pre, nu_post, true); // z = M r from z = 0
     assign(1.0, z, 0.0, z, p, level, ALL_FLAGS);
     double rz = dot(r, z, level);
     for (int k = 0; k < max_iter && res.back() > target; ++k) {
@@ -660,8 +686,7 @@ std::vector<double> Hierarchy::pcg(Function& rhs, Function& x, int level, int ma
         const double alpha = rz / pap;
         add_scaled(x, alpha, p, level, ALL_FLAGS);
         add_scaled(r, -alpha, ap, level, ALL_FLAGS);
-        fill_const(z, 0.0, level, ALL_FLAGS);
-        run_cycle(r, z, level, nu_pre, nu_post);
+        run_cycle(r, z, level, nu_pre, nu_post, true);
         const double rz_new = dot(r, z, level);
         assign(1.0, z, rz_new / rz, p, p, level, ALL_FLAGS);
         rz = rz_new;
