@@ -268,6 +268,8 @@ void assign(double alpha, Function& x1, double beta, Function& x2, Function& dst
 void add_scaled(Function& dst, double gamma, Function& y, int level, uint8_t mask);
 void fill_const(Function& f, double value, int level, uint8_t mask);
 void fill_random(Function& f, int level, uint64_t seed, uint64_t stream, double lo, double hi, uint8_t mask);
+/// PCG update: x += alpha p, r -= alpha ap, returns r.r (bitwise the unfused ops)
+double pcg_update(Function& x, Function& p, Function& r, Function& ap, double alpha, int level);
 double dot(Function& a, Function& b, int level);
 double max_abs(Function& a, int level);
 void upload(Function& f, int level, const double* host, int64_t n, bool global_order, uint8_t mask);

@@ -20,7 +20,7 @@ namespace hyb {
 
 namespace {
 
-constexpr uint8_t F_INNER = 1, F_DIRICHLET = 2;
+constexpr uint8_t F_INNER = 1, F_DIRICHLET = 2, F_ALL = 7;
 
 std::atomic<int64_t> g_launches{0};
 
@@ -399,6 +399,52 @@ __global__ void __launch_bounds__(256) k_partials_faces(LevelTables t, const dou
     if (threadIdx.x == 0) scratch[int64_t(blockIdx.y) * bands + blockIdx.x] = tot;
 }
 
+// PCG's x += alpha p; r += (-alpha) ap (add_scaled, bitwise) with the partials
+// of r.r in k_partials_faces' exact shape, so the fused dot is bitwise the
+// separate dot(r, r). Face interiors only (owned DoFs).
+__global__ void __launch_bounds__(256) k_pcg_update_faces(LevelTables t, double* __restrict__ x,
+                                                          const double* __restrict__ p, double* __restrict__ r,
+                                                          const double* __restrict__ ap, double alpha, double nalpha,
+                                                          double* scratch, int bands) {
+    __shared__ double sh[256];
+    const int n = t.n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t base = int64_t(blockIdx.y) * t.face_stride;
+    double s0 = 0.0, s1 = 0.0;
+    const int r0 = 1 + blockIdx.x * PB;
+    for (int row = r0 + warp; row < r0 + PB && row <= n - 2; row += 8) {
+        const int64_t o = base + t.rowoff[row];
+        const int last = n - 1 - row;
+        for (int col = 2 * lane; col <= last; col += 64) {
+            double2* xx = reinterpret_cast<double2*>(x + o + col);
+            double2* rr = reinterpret_cast<double2*>(r + o + col);
+            const double2 vx = *xx, vr = *rr;
+            const double2 vp = __ldg(reinterpret_cast<const double2*>(p + o + col));
+            const double2 va = __ldg(reinterpret_cast<const double2*>(ap + o + col));
+            const double nx0 = vx.x + alpha * vp.x, nx1 = vx.y + alpha * vp.y;
+            const double nr0 = vr.x + nalpha * va.x, nr1 = vr.y + nalpha * va.y;
+            const bool v0 = col >= 1, v1 = col + 1 <= last;
+            if (v0 && v1) {
+                *xx = make_double2(nx0, nx1);
+                *rr = make_double2(nr0, nr1);
+            } else {
+                if (v0) {
+                    x[o + col] = nx0;
+                    r[o + col] = nr0;
+                }
+                if (v1) {
+                    x[o + col + 1] = nx1;
+                    r[o + col + 1] = nr1;
+                }
+            }
+            if (v0) s0 = s0 + nr0 * nr0;
+            if (v1) s1 = s1 + nr1 * nr1;
+        }
+    }
+    const double tot = block_reduce_256<0>(s0 + s1, sh);
+    if (threadIdx.x == 0) scratch[int64_t(blockIdx.y) * bands + blockIdx.x] = tot;
+}
+
 // faces: fold the bands in order (one thread per face); edges: one warp per
 // edge over k = 1..n-1 with a fixed shuffle tree; vertices: one thread each
 template <int OP>
@@ -700,6 +746,28 @@ void launch_partials(int op, const LevelTables& t, const double* x1, const doubl
         const int blocks = (warps + 3) / 4;
         if (op == 0) k_partials_finish<0><<<blocks, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
         else k_partials_finish<1><<<blocks, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
+        check_launch("partials finish");
+    }
+}
+
+void launch_pcg_update(const LevelTables& t, const FlagTables& fl, double* x, const double* p, double* r,
+                       const double* ap, double alpha, double* part, double* scratch, cudaStream_t st) {
+    const int bands = t.n >= 3 ? (t.n - 2 + PB - 1) / PB : 0;
+    if (t.nfaces > 0 && bands > 0) {
+        k_pcg_update_faces<<<dim3(unsigned(bands), unsigned(t.nfaces)), 256, 0, st>>>(t, x, p, r, ap, alpha, -alpha,
+                                                                                    scratch, bands);
+        check_launch("pcg update faces");
+    }
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    if (blocks > 0) { // edges / vertices: add_scaled as usual
+        k_blas1_ev<<<blocks, 128, 0, st>>>(1, t, fl, alpha, p, 0.0, p, x, F_ALL, kb);
+        k_blas1_ev<<<blocks, 128, 0, st>>>(1, t, fl, -alpha, ap, 0.0, ap, r, F_ALL, kb);
+        check_launch("pcg update edges/vertices");
+    }
+    const int warps = (t.nfaces + 31) / 32 + t.nedges + (t.nverts + 31) / 32;
+    if (warps > 0) {
+        k_partials_finish<0><<<(warps + 3) / 4, 128, 0, st>>>(t, r, r, scratch, bands, part);
         check_launch("partials finish");
     }
 }

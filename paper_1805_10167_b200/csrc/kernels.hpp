@@ -105,6 +105,10 @@ void launch_gather_owned(const LevelTables& t, const double* arena, double* pack
 void launch_partials(int op, const LevelTables& t, const double* x1, const double* x2, double* part,
                      double* scratch, cudaStream_t st);
 // fixed pairwise fold (op 0 sum, op 1 max) of v[0..len) -> out[0]; v is clobbered
+// PCG: x += alpha p, r += (-alpha) ap on every owned DoF, and the
+// per-primitive partials of r.r (bitwise those of launch_partials(0, r, r))
+void launch_pcg_update(const LevelTables& t, const FlagTables& fl, double* x, const double* p, double* r,
+                       const double* ap, double alpha, double* part, double* scratch, cudaStream_t st);
 void launch_combine_tree(int op, double* v, int64_t len, double* out, cudaStream_t st);
 
 // ---- coarse-grid solve (device-resident, replicated per rank) ----

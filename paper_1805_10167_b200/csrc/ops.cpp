@@ -297,6 +297,30 @@ double reduce(int op, Function& a, Function& b, int level) {
 }
 } // namespace
 
+// x += alpha p; r -= alpha ap (add_scaled twice, bitwise) and return r.r
+// (bitwise dot(r, r)) from one pass over the faces
+double pcg_update(Function& x, Function& p, Function& r, Function& ap, double alpha, int level) {
+    check_pair("pcg_update", x, p, level);
+    check_pair("pcg_update", r, ap, level);
+    check_pair("pcg_update", x, r, level);
+    Domain& d = x.domain();
+    const LevelTables& t = d.level(level).t;
+    const int64_t np = int64_t(d.graph().size());
+    const int bands = t.n >= 3 ? (t.n - 2 + 31) / 32 : 0;
+    double* buf = d.partials(2 * np + int64_t(t.nfaces) * bands + 1);
+    double* part = buf;
+    double* scratch = buf + 2 * np;
+    HYB_CUDA(cudaMemsetAsync(part, 0, size_t(np) * 8, d.stream()));
+    launch_pcg_update(t, r.flags(), x.data(level), p.data(level), r.data(level), ap.data(level), alpha, part, scratch,
+                      d.stream());
+    d.allreduce_sum(part, np);
+    launch_combine_tree(0, part, np, d.scalar_out(), d.stream());
+    double out = 0.0;
+    HYB_CUDA(cudaMemcpyAsync(&out, d.scalar_out(), 8, cudaMemcpyDeviceToHost, d.stream()));
+    HYB_CUDA(cudaStreamSynchronize(d.stream()));
+    return out;
+}
+
 double dot(Function& a, Function& b, int level) {
     check_pair("dot", a, b, level);
     return reduce(0, a, b, level);
@@ -684,13 +708,12 @@ std::vector<double> Hierarchy::pcg(Function& rhs, Function& x, int level, int ma
         const double pap = dot(p, ap, level);
         if (!(pap > 0.0)) throw RuntimeError("pcg: non-positive curvature p.Ap = " + std::to_string(pap));
         const double alpha = rz / pap;
-        add_scaled(x, alpha, p, level, ALL_FLAGS);
-        add_scaled(r, -alpha, ap, level, ALL_FLAGS);
+        const double rr = pcg_update(x, p, r, ap, alpha, level); // x += alpha p, r -= alpha Ap, r.r
         run_cycle(r, z, level, nu_pre, nu_post, true);
         const double rz_new = dot(r, z, level);
         assign(1.0, z, rz_new / rz, p, p, level, ALL_FLAGS);
         rz = rz_new;
-        res.push_back(std::sqrt(dot(r, r, level)));
+        res.push_back(std::sqrt(rr));
     }
     if (converged) *converged = res.back() <= target;
     return res;
