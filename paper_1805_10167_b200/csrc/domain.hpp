@@ -251,7 +251,10 @@ class Domain {
 //      solvers.hpp:26-33, function.hpp:55-81) ----
 void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t mask);
 void residual(const Operator& A, Function& rhs, Function& x, Function& r, int level);
-void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level);
+/// dotp: optional per-CTA partials of rhs.x_new over the faces (face_dot_slots)
+void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level, double* dotp = nullptr);
+/// dst = A src (all flags) and returns src.dst, one pass over the faces
+double apply_dot(const Operator& A, Function& src, Function& dst, int level);
 /// first sweep from x = 0: does not read x (Hierarchy::cycle)
 void smooth_jacobi_zero(const Operator& A, Function& rhs, Function& x, double omega, int level);
 void smooth_gs(const Operator& A, Function& rhs, Function& x, int level);
@@ -301,7 +304,7 @@ class Hierarchy {
   private:
     void cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero = false);
     void coarse_correct(Function& rhs, Function& x);
-    void smooth(Function& rhs, Function& x, int level);
+    void smooth(Function& rhs, Function& x, int level, double* dotp = nullptr);
     void check_coarse(); // throws if the last coarse solve did not converge
     void run_cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero = false);
     std::vector<const void*> graph_key(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero);
@@ -329,6 +332,10 @@ class Hierarchy {
     Operator a_;
     Function r_, b_, e_; // b_, e_ (coarse rhs/correction) stop one level below max
     std::unique_ptr<Function> pcg_r_, pcg_z_, pcg_p_; // PCG vectors at one level (Ap lives in r_)
+    // PCG's r.z from the cycle's last post-smoothing sweep at cycle_dot_level_
+    DevMem dot_scratch_;
+    double* cycle_dot_ = nullptr;
+    int cycle_dot_level_ = -1;
     int smoother_;
     double omega_;
     double coarse_tol_;

@@ -86,7 +86,8 @@ template <int MODE>
 __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, const double* __restrict__ x,
                                                                  const double* __restrict__ b,
                                                                  double* __restrict__ y, double omega,
-                                                                 const int64_t* __restrict__ cro, int64_t cstride) {
+                                                                 const int64_t* __restrict__ cro, int64_t cstride,
+                                                                 double* __restrict__ dotp) {
     constexpr bool RR = MODE == ST_RESTRICT_RESIDUAL;
     constexpr int XOFF = RR ? 4 : 2;           // smem x index of column c0
     constexpr int XW = RR ? FS_XW_RR : FS_XW;  // staged x width
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         if (R_hi > nc - 1) R_hi = nc - 1; // coarse interior rows 1..nc-2
         const int Cmin = c0 / 2 < 1 ? 1 : c0 / 2;
         if (R_hi > nc - Cmin) R_hi = nc - Cmin;
-        if (R_lo >= R_hi) return;
+        if (R_lo >= R_hi) return; // (no dot in this mode)
         r_lo = 2 * R_lo - 1; // fine rows 2R_lo-1 .. 2R_hi-1
         r_hi = 2 * R_hi;
     } else {
@@ -116,7 +117,11 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         if (r_hi > n - 1) r_hi = n - 1;     // interior rows r <= n-2
         const int cmin = c0 < 1 ? 1 : c0;
         if (r_hi > n - cmin) r_hi = n - cmin; // first column of the block stays interior
-        if (r_lo >= r_hi) return;           // CTA-uniform, before any barrier use
+        if (r_lo >= r_hi) {                 // CTA-uniform, before any barrier use
+            if (dotp && threadIdx.x == 0)
+                dotp[(int64_t(face) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = 0.0;
+            return;
+        }
     }
     const int nrows = r_hi - r_lo;      // computed rows
     const int nstage = nrows + 2;       // x rows r_lo-1 .. r_hi
@@ -180,6 +185,9 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     double sl = 0, s0 = 0, s1 = 0, hl = 0, h0 = 0, h1 = 0;
     const int nc = n / 2;
     const int C = c / 2; // coarse column of this lane (RR)
+    // optional dot partials (dotp): APPLY x.(Ax), JACOBI b.x_new, per lane for
+    // its two columns over the band's rows, then a fixed tree over the CTA
+    double d0 = 0.0, d1 = 0.0;
     for (int i = 0; i < nstage; ++i) {
         const int s = i % FS_S;
         mbar_wait(&sm.full[s], (i / FS_S) & 1);
@@ -253,6 +261,15 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                     o0 = z0 + div_by(omega * (bb.x - a0), dg, rdg); // x + omega*(b - Ax)/diag
                     o1 = z1 + div_by(omega * (bb.y - a1), dg, rdg);
                 }
+                if (dotp) {
+                    if (MODE == ST_APPLY) {
+                        if (v0) d0 = d0 + z0 * o0;
+                        if (v1) d1 = d1 + z1 * o1;
+                    } else if (MODE == ST_JACOBI) {
+                        if (v0) d0 = d0 + bb.x * o0;
+                        if (v1) d1 = d1 + bb.y * o1;
+                    }
+                }
                 double* yrow = yf + ro[r];
                 if (v0 && v1) {
                     __stcs(reinterpret_cast<double2*>(yrow + c), make_double2(o0, o1));
@@ -264,6 +281,18 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         }
         ml = zl; m0 = z0; m1 = z1; mr = zr;
         zl = pl; z0 = p0; z1 = p1; zr = pr;
+    }
+    if (!RR && dotp) { // consumer warps only (the producer has returned)
+        double v = d0 + d1;
+        for (int o = 16; o > 0; o >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, o);
+        __shared__ double red[FS_CWARPS];
+        if (lane == 0) red[warp] = v;
+        asm volatile("bar.sync 1, %0;" ::"n"(FS_CWARPS * 32) : "memory");
+        if (tid == 0) {
+            double tsum = red[0];
+            for (int w = 1; w < FS_CWARPS; ++w) tsum = tsum + red[w];
+            dotp[(int64_t(face) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = tsum;
+        }
     }
     (void)ml;
     (void)sl;

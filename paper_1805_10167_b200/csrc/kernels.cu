@@ -529,8 +529,23 @@ __global__ void __launch_bounds__(256) k_jacobi_zero_faces(LevelTables t, const 
     }
 }
 
+int face_dot_slots(const LevelTables& t) {
+    if (t.nfaces <= 0 || t.n < 3) return 0;
+    const dim3 g = face_stencil_grid(t);
+    return int(g.x * g.y);
+}
+
+void launch_partials_finish(const LevelTables& t, const double* u, const double* v, const double* scratch, int bands,
+                            double* part, cudaStream_t st) {
+    const int warps = (t.nfaces + 31) / 32 + t.nedges + (t.nverts + 31) / 32;
+    if (warps > 0) {
+        k_partials_finish<0><<<(warps + 3) / 4, 128, 0, st>>>(t, u, v, scratch, bands, part);
+        check_launch("partials finish");
+    }
+}
+
 void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const double* x, const double* b, double* y,
-                    double omega, uint8_t mask, cudaStream_t st, int parts) {
+                    double omega, uint8_t mask, cudaStream_t st, int parts, double* dotp) {
     if (mode == ST_JACOBI_ZERO) {
         if ((parts & 1) && t.nfaces > 0 && t.n >= 3) {
             const int64_t per = (t.face_stride / 2 + 255) / 256;
@@ -549,11 +564,11 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
     if ((parts & 1) && (mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
         const dim3 grid = face_stencil_grid(t);
         switch (mode) {
-        case ST_APPLY: k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0); break;
+        case ST_APPLY: k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp); break;
         case ST_RESIDUAL:
-            k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0);
+            k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr);
             break;
-        default: k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0); break;
+        default: k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp); break;
         }
         check_launch("face stencil");
     }
@@ -654,7 +669,7 @@ void launch_residual_restrict_faces(const LevelTables& tc, const LevelTables& tf
     if (tf.nfaces <= 0 || tf.n < 3) return;
     if (tc.n >= 3) {
         k_face_stencil<ST_RESTRICT_RESIDUAL><<<face_rr_grid(tf), FS_THREADS, 0, st>>>(tf, x, b, xc, 0.0, tc.rowoff,
-                                                                                      tc.face_stride);
+                                                                                      tc.face_stride, nullptr);
         check_launch("residual+restrict faces");
     }
     const dim3 grid(unsigned((tf.n - 2 + 127) / 128), 3u, unsigned(tf.nfaces));

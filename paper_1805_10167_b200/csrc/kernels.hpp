@@ -56,7 +56,13 @@ enum StencilMode : int { ST_APPLY = 0, ST_RESIDUAL = 1, ST_JACOBI = 2, ST_RESTRI
 // ---- launchers (all asynchronous on `st`) ----
 // parts: 1 = face interiors (K1), 2 = edge lines + vertices (K2/K3), 3 = both
 void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const double* x, const double* b,
-                    double* y, double omega, uint8_t mask, cudaStream_t st, int parts = 3);
+                    double* y, double omega, uint8_t mask, cudaStream_t st, int parts = 3,
+                    double* dotp = nullptr);
+// dotp (APPLY: x.(Ax); JACOBI: b.x_new): one partial per face-kernel CTA,
+// face_dot_slots(t) per face, folded per face by launch_partials_finish
+int face_dot_slots(const LevelTables& t);
+void launch_partials_finish(const LevelTables& t, const double* u, const double* v, const double* scratch, int bands,
+                            double* part, cudaStream_t st);
 /// number of kernels launched by this library so far (process-wide)
 int64_t kernel_launch_count();
 /// Ghost refresh, one pass: arena[dst[i]] = arena[src[i]] for i < nlocal

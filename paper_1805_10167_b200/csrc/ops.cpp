@@ -95,7 +95,7 @@ void residual(const Operator& A, Function& rhs, Function& x, Function& r, int le
     d.timer_end();
 }
 
-void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level) {
+void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level, double* dotp) {
     check_op_function(A, rhs, level, "smooth_jacobi", true);
     check_op_function(A, x, level, "smooth_jacobi", true);
     if (&rhs == &x) throw InvalidArgument("smooth_jacobi: rhs and x must be distinct functions");
@@ -110,9 +110,50 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
                    d.stream(), 2);
     d.timer_begin("jacobi");
     launch_stencil(ST_JACOBI, t, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
-                   d.stream(), 1);
+                   d.stream(), 1, dotp);
     d.timer_end();
     x.arena(level).swap(next);
+}
+
+namespace {
+// per-primitive partials already in `part` (faces: `slots` CTA partials each
+// in scratch) -> the reference's fold over the global vector -> host
+double finish_dot(Domain& d, const LevelTables& t, const double* u, const double* v, const double* scratch, int slots,
+                  double* part) {
+    launch_partials_finish(t, u, v, scratch, slots, part, d.stream());
+    const int64_t np = int64_t(d.graph().size());
+    d.allreduce_sum(part, np);
+    launch_combine_tree(0, part, np, d.scalar_out(), d.stream());
+    double out = 0.0;
+    HYB_CUDA(cudaMemcpyAsync(&out, d.scalar_out(), 8, cudaMemcpyDeviceToHost, d.stream()));
+    HYB_CUDA(cudaStreamSynchronize(d.stream()));
+    return out;
+}
+} // namespace
+
+// dst = A src and src.dst in one pass over the faces (PCG's p.Ap): the face
+// partials come from the stencil kernel's CTAs (fixed shapes, so the result is
+// deterministic and partition invariant, though not bitwise dot()'s order)
+double apply_dot(const Operator& A, Function& src, Function& dst, int level) {
+    check_op_function(A, src, level, "apply", false);
+    check_op_function(A, dst, level, "apply", true);
+    if (&src == &dst) throw InvalidArgument("apply: src and dst must be distinct functions");
+    Domain& d = A.domain();
+    d.sync(src, level);
+    const LevelTables t = A.tables(level);
+    const int slots = face_dot_slots(t);
+    const int64_t np = int64_t(d.graph().size());
+    double* buf = d.partials(np + int64_t(t.nfaces) * slots + 1);
+    double* part = buf;
+    double* scratch = buf + np;
+    HYB_CUDA(cudaMemsetAsync(part, 0, size_t(np) * 8, d.stream()));
+    launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, ALL_FLAGS,
+                   d.stream(), 2);
+    d.timer_begin("apply");
+    launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, ALL_FLAGS,
+                   d.stream(), 1, scratch);
+    d.timer_end();
+    return finish_dot(d, t, src.data(level), dst.data(level), scratch, slots, part);
 }
 
 // the first weighted-Jacobi sweep of a cycle whose x starts at zero (see
@@ -470,10 +511,10 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
     }
 }
 
-void Hierarchy::smooth(Function& rhs, Function& x, int level) {
+void Hierarchy::smooth(Function& rhs, Function& x, int level, double* dotp) {
     if (smoother_ == SMOOTH_GS) smooth_gs(a_, rhs, x, level); // the reference's own choice (solvers.cpp:417, 427)
     else if (smoother_ == SMOOTH_CGS) smooth_cgs(a_, rhs, x, level);
-    else smooth_jacobi(a_, rhs, x, omega_, level);
+    else smooth_jacobi(a_, rhs, x, omega_, level, dotp);
 }
 
 void Hierarchy::vcycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post) {
@@ -494,7 +535,8 @@ std::vector<const void*> Hierarchy::graph_key(Function& rhs, Function& x, int le
     std::vector<const void*> k{&rhs, &x, rhs.data(level), x.data(level), reinterpret_cast<const void*>(intptr_t(level)),
                                reinterpret_cast<const void*>(intptr_t(nu_pre)),
                                reinterpret_cast<const void*>(intptr_t(nu_post)),
-                               reinterpret_cast<const void*>(intptr_t(x_zero))};
+                               reinterpret_cast<const void*>(intptr_t(x_zero)), cycle_dot_,
+                               reinterpret_cast<const void*>(intptr_t(cycle_dot_level_))};
     for (int l = a_.min_level(); l <= level; ++l) {
         k.push_back(r_.data(l));
         if (l < level) {
@@ -577,7 +619,8 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
     cycle(b_, e_, level - 1, nu_pre, nu_post, true); // e = 0 on entry
     // prolongate(e -> r) + add_scaled(x, 1, r) on the smooth mask, fused
     prolongate(e_, x, level - 1, kSmoothMask, true);
-    for (int i = 0; i < nu_post; ++i) smooth(rhs, x, level);
+    for (int i = 0; i < nu_post; ++i)
+        smooth(rhs, x, level, (level == cycle_dot_level_ && i == nu_post - 1) ? cycle_dot_ : nullptr);
 }
 
 // reference src/solvers.cpp:430-442: residual, gather into the global coarse
@@ -703,14 +746,39 @@ std::vector<double> Hierarchy::pcg(Function& rhs, Function& x, int level, int ma
     run_cycle(r, z, level, nu_pre, nu_post, true); // z = M r from z = 0
     assign(1.0, z, 0.0, z, p, level, ALL_FLAGS);
     double rz = dot(r, z, level);
+    // r.z from the cycle's last post-smoothing sweep when it is a Jacobi sweep
+    // at this level (its partials land in dot_scratch_), else a separate dot
+    const bool fused_rz = smoother_ == SMOOTH_JACOBI && nu_post > 0 && level > a_.min_level();
+    const LevelTables tl = a_.tables(level);
+    const int slots = face_dot_slots(tl);
+    const int64_t np = int64_t(d.graph().size());
+    if (fused_rz && int64_t(dot_scratch_.bytes() / 8) < np + int64_t(tl.nfaces) * slots + 1)
+        dot_scratch_ = DevMem(size_t(np + int64_t(tl.nfaces) * slots + 1) * 8);
     for (int k = 0; k < max_iter && res.back() > target; ++k) {
-        apply(a_, p, ap, level, ALL_FLAGS);
-        const double pap = dot(p, ap, level);
+        const double pap = apply_dot(a_, p, ap, level); // Ap and p.Ap in one pass
         if (!(pap > 0.0)) throw RuntimeError("pcg: non-positive curvature p.Ap = " + std::to_string(pap));
         const double alpha = rz / pap;
         const double rr = pcg_update(x, p, r, ap, alpha, level); // x += alpha p, r -= alpha Ap, r.r
-        run_cycle(r, z, level, nu_pre, nu_post, true);
-        const double rz_new = dot(r, z, level);
+        double rz_new;
+        if (fused_rz) {
+            double* part = dot_scratch_.as<double>();
+            HYB_CUDA(cudaMemsetAsync(part, 0, size_t(np) * 8, d.stream()));
+            cycle_dot_ = part + np;
+            cycle_dot_level_ = level;
+            try {
+                run_cycle(r, z, level, nu_pre, nu_post, true);
+            } catch (...) {
+                cycle_dot_ = nullptr;
+                cycle_dot_level_ = -1;
+                throw;
+            }
+            cycle_dot_ = nullptr;
+            cycle_dot_level_ = -1;
+            rz_new = finish_dot(d, tl, r.data(level), z.data(level), part + np, slots, part);
+        } else {
+            run_cycle(r, z, level, nu_pre, nu_post, true);
+            rz_new = dot(r, z, level);
+        }
         assign(1.0, z, rz_new / rz, p, p, level, ALL_FLAGS);
         rz = rz_new;
         res.push_back(std::sqrt(rr));
