@@ -82,7 +82,7 @@ template <int MODE> struct FaceSmem {
 // 2R-1 .. 2R+1 are computed as residuals and restricted on the fly (see
 // k_residual_restrict_faces in transfer.cuh for why only face-interior fine
 // points are involved); nothing fine is stored.
-template <int MODE>
+template <int MODE, bool DOT = false>
 __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, const double* __restrict__ x,
                                                                  const double* __restrict__ b,
                                                                  double* __restrict__ y, double omega,
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         const int cmin = c0 < 1 ? 1 : c0;
         if (r_hi > n - cmin) r_hi = n - cmin; // first column of the block stays interior
         if (r_lo >= r_hi) {                 // CTA-uniform, before any barrier use
-            if (dotp && threadIdx.x == 0)
+            if (DOT && threadIdx.x == 0)
                 dotp[(int64_t(face) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = 0.0;
             return;
         }
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                     o0 = z0 + div_by(omega * (bb.x - a0), dg, rdg); // x + omega*(b - Ax)/diag
                     o1 = z1 + div_by(omega * (bb.y - a1), dg, rdg);
                 }
-                if (dotp) {
+                if (DOT) {
                     if (MODE == ST_APPLY) {
                         if (v0) d0 = d0 + z0 * o0;
                         if (v1) d1 = d1 + z1 * o1;
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         ml = zl; m0 = z0; m1 = z1; mr = zr;
         zl = pl; z0 = p0; z1 = p1; zr = pr;
     }
-    if (!RR && dotp) { // consumer warps only (the producer has returned)
+    if (DOT) { // consumer warps only (the producer has returned)
         double v = d0 + d1;
         for (int o = 16; o > 0; o >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, o);
         __shared__ double red[FS_CWARPS];

@@ -564,11 +564,17 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
     if ((parts & 1) && (mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
         const dim3 grid = face_stencil_grid(t);
         switch (mode) {
-        case ST_APPLY: k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp); break;
+        case ST_APPLY:
+            if (dotp) k_face_stencil<ST_APPLY, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp);
+            else k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr);
+            break;
         case ST_RESIDUAL:
             k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr);
             break;
-        default: k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp); break;
+        default:
+            if (dotp) k_face_stencil<ST_JACOBI, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp);
+            else k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr);
+            break;
         }
         check_launch("face stencil");
     }
