@@ -343,6 +343,7 @@ class Hierarchy {
     // min-level system, replicated on every rank (see coarse.hpp)
     struct Coarse {
         int64_t n = 0, nloc = 0;
+        int max_row_nnz = 0;
         DevMem rowptr, col, val;  // constrained CSR
         DevMem gidx, pos, flag;   // this process's owned min-level DoFs
         DevMem vec;               // b, x, r, p, ap (n each)

@@ -959,6 +959,16 @@ __device__ double block_sum(double s, double* red) {
     return out;
 }
 
+// grid-wide sum of one value per thread, identical in every CTA
+__device__ double grid_sum(double s, double* red, double* part, unsigned* bar) {
+    const double b = block_sum(s, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = b;
+    grid_barrier(bar);
+    double t = 0.0;
+    for (int i = threadIdx.x; i < int(gridDim.x); i += CGG_THREADS) t += __ldcg(part + i);
+    return block_sum(t, red);
+}
+
 __device__ double grid_dot(const double* u, const double* v, int64_t n, double* red, double* part, unsigned* bar) {
     const int64_t stride = int64_t(gridDim.x) * CGG_THREADS;
     double s = 0.0;
@@ -1038,21 +1048,135 @@ void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos,
     check_launch("coarse gather");
 }
 
+// Register-resident variant (at most one row per thread, at most NZ entries
+// per row): the row's matrix entries and its x, r, p, Ap stay in registers for
+// the whole solve; per iteration only p is exchanged through L2 (one gather
+// round for the SpMV) plus the three grid reductions. Same row-to-thread
+// mapping and entry order as k_coarse_cg_grid: the same arithmetic.
+template <int NZ>
+__global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const int32_t* __restrict__ rowptr,
+                                                               const int32_t* __restrict__ col,
+                                                               const double* __restrict__ val,
+                                                               const double* __restrict__ b, double* x, double* P,
+                                                               double tol, int max_iter, CoarseStatus* st,
+                                                               double* part, unsigned* bar) {
+    __shared__ double red[33];
+    const int64_t i = blockIdx.x * int64_t(CGG_THREADS) + threadIdx.x;
+    const bool own = i < n;
+    double* part0 = part;
+    double* part1 = part + gridDim.x;
+    int cj[NZ];
+    double vj[NZ];
+    int nz = 0;
+    if (own) {
+        const int32_t k0 = rowptr[i];
+        nz = rowptr[i + 1] - k0;
+#pragma unroll
+        for (int q = 0; q < NZ; ++q) {
+            cj[q] = q < nz ? col[k0 + q] : 0;
+            vj[q] = q < nz ? val[k0 + q] : 0.0;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < NZ; ++q) {
+            cj[q] = 0;
+            vj[q] = 0.0;
+        }
+    }
+    const double bi = own ? b[i] : 0.0;
+    double xi = 0.0, ri = bi, pi = bi;
+    if (own) P[i] = pi;
+    double s = 0.0;
+    if (own) s += bi * bi;
+    const double target = tol * sqrt(grid_sum(s, red, part0, bar));
+    s = 0.0;
+    if (own) s += ri * ri;
+    double rs = grid_sum(s, red, part1, bar); // also publishes P
+    int it = 0, breakdown = 0;
+    while (it < max_iter && sqrt(rs) > target) {
+        double api = 0.0;
+#pragma unroll
+        for (int q = 0; q < NZ; ++q)
+            if (q < nz) api += vj[q] * __ldcg(P + cj[q]);
+        s = 0.0;
+        if (own) s += pi * api;
+        const double pap = grid_sum(s, red, part0, bar);
+        if (pap <= 0.0) {
+            breakdown = 1;
+            break;
+        }
+        const double alpha = rs / pap;
+        xi += alpha * pi;
+        ri -= alpha * api;
+        s = 0.0;
+        if (own) s += ri * ri;
+        const double rs_new = grid_sum(s, red, part1, bar);
+        const double beta = rs_new / rs;
+        pi = ri + beta * pi;
+        if (own) P[i] = pi;
+        grid_barrier(bar);
+        rs = rs_new;
+        ++it;
+    }
+    if (own) x[i] = xi;
+    grid_barrier(bar); // x complete
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < NZ; ++q)
+        if (q < nz) acc += vj[q] * __ldcg(x + cj[q]);
+    const double ti = bi - acc;
+    s = 0.0;
+    if (own) s += ti * ti;
+    const double res = sqrt(grid_sum(s, red, part0, bar));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->iterations = it;
+        st->breakdown = breakdown;
+        st->converged = res <= target ? 1 : 0;
+        st->target = target;
+        st->residual = res;
+    }
+}
+
 int coarse_grid_blocks() {
     static const int g = [] {
         int dev = 0, sms = 0, per = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coarse_cg_grid, CGG_THREADS, 0);
-        return sms * (per > 0 ? 1 : 0);
+        int per16 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per16, k_coarse_cg_reg<16>, CGG_THREADS, 0);
+        return sms * (per > 0 && per16 > 0 ? 1 : 0);
     }();
     return g;
 }
 
 void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* b,
                       double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
-                      double* grid_part, unsigned* grid_bar, cudaStream_t stream) {
+                      double* grid_part, unsigned* grid_bar, int max_row_nnz, cudaStream_t stream) {
     if (n >= kCoarseGridMinRows && grid_part && grid_bar && coarse_grid_blocks() > 0) {
+        const int64_t threads = int64_t(coarse_grid_blocks()) * CGG_THREADS;
+        if (n <= threads && max_row_nnz <= 16) { // register-resident rows
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(unsigned(coarse_grid_blocks()));
+            cfg.blockDim = dim3(CGG_THREADS);
+            cfg.stream = stream;
+            cudaLaunchAttribute attr{};
+            attr.id = cudaLaunchAttributeCooperative;
+            attr.val.cooperative = 1;
+            cfg.attrs = &attr;
+            cfg.numAttrs = 1;
+            const cudaError_t e =
+                max_row_nnz <= 8
+                    ? cudaLaunchKernelEx(&cfg, k_coarse_cg_reg<8>, n, rowptr, col, val, b, x, p, tol, max_iter, st,
+                                         grid_part, grid_bar)
+                    : cudaLaunchKernelEx(&cfg, k_coarse_cg_reg<16>, n, rowptr, col, val, b, x, p, tol, max_iter, st,
+                                         grid_part, grid_bar);
+            if (e != cudaSuccess)
+                throw std::runtime_error(std::string("CUDA launch failed (coarse cg registers): ") +
+                                         cudaGetErrorString(e));
+            check_launch("coarse cg registers");
+            return;
+        }
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(unsigned(coarse_grid_blocks()));
         cfg.blockDim = dim3(CGG_THREADS);

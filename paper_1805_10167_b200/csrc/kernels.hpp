@@ -138,7 +138,7 @@ constexpr int64_t kCoarseGridMinRows = 16384;
 int coarse_grid_blocks();
 void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* b,
                       double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
-                      double* grid_part, unsigned* grid_bar, cudaStream_t stream);
+                      double* grid_part, unsigned* grid_bar, int max_row_nnz, cudaStream_t stream);
 // arena[pos[i]] += glob[gidx[i]] where flag[i] & mask
 void launch_coarse_scatter_add(int64_t nloc, const int64_t* gidx, const int64_t* pos, const uint8_t* flag,
                                uint8_t mask, const double* glob, double* arena, cudaStream_t st);

@@ -495,6 +495,8 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
     std::vector<uint8_t> fl(gidx.size());
     for (size_t i = 0; i < gidx.size(); ++i) fl[i] = csr.flag[size_t(gidx[i])];
     coarse_.n = csr.n;
+    for (int64_t i = 0; i < csr.n; ++i)
+        coarse_.max_row_nnz = std::max(coarse_.max_row_nnz, csr.rowptr[size_t(i) + 1] - csr.rowptr[size_t(i)]);
     coarse_.nloc = int64_t(gidx.size());
     coarse_.rowptr = upload_vec(csr.rowptr, d.stream());
     coarse_.col = upload_vec(csr.col, d.stream());
@@ -641,7 +643,8 @@ void Hierarchy::coarse_correct(Function& rhs, Function& x) {
     d.timer_begin("coarse_cg");
     launch_coarse_cg(n, coarse_.rowptr.as<int32_t>(), coarse_.col.as<int32_t>(), coarse_.val.as<double>(), b, cx,
                      b + 2 * n, b + 3 * n, b + 4 * n, coarse_tol_, coarse_max_iter_,
-                     coarse_.status.as<CoarseStatus>(), coarse_.grid_part(), coarse_.grid_bar(), d.stream());
+                     coarse_.status.as<CoarseStatus>(), coarse_.grid_part(), coarse_.grid_bar(), coarse_.max_row_nnz,
+                     d.stream());
     d.timer_end();
     launch_coarse_scatter_add(coarse_.nloc, coarse_.gidx.as<int64_t>(), coarse_.pos.as<int64_t>(),
                               coarse_.flag.as<uint8_t>(), kSmoothMask, cx, x.data(L), d.stream());
