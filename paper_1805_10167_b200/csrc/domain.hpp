@@ -170,6 +170,10 @@ class Domain {
 
     // scratch
     DevMem& jacobi_scratch(int level);
+    /// exchange staging (reallocated when a level with more traffic is built:
+    /// part of the V-cycle graph key)
+    const void* send_buffer() const { return sendbuf_.as<void>(); }
+    const void* recv_buffer() const { return recvbuf_.as<void>(); }
     double* staging(int64_t doubles);
     double* partials(int64_t doubles);
     double* scalar_out() { return scalars_.as<double>(); }

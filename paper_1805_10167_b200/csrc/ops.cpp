@@ -538,7 +538,8 @@ std::vector<const void*> Hierarchy::graph_key(Function& rhs, Function& x, int le
                                reinterpret_cast<const void*>(intptr_t(nu_pre)),
                                reinterpret_cast<const void*>(intptr_t(nu_post)),
                                reinterpret_cast<const void*>(intptr_t(x_zero)), cycle_dot_,
-                               reinterpret_cast<const void*>(intptr_t(cycle_dot_level_))};
+                               reinterpret_cast<const void*>(intptr_t(cycle_dot_level_)), dom_->send_buffer(),
+                               dom_->recv_buffer()};
     for (int l = a_.min_level(); l <= level; ++l) {
         k.push_back(r_.data(l));
         if (l < level) {
