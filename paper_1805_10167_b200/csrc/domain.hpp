@@ -24,9 +24,6 @@
 
 namespace hyb {
 
-struct CudaError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
 struct NcclError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };

@@ -27,7 +27,7 @@ std::atomic<int64_t> g_launches{0};
 inline void check_launch(const char* what) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA launch failed (") + what + "): " + cudaGetErrorString(e));
+    if (e != cudaSuccess) throw CudaError(std::string("CUDA launch failed (") + what + "): " + cudaGetErrorString(e));
 }
 
 __device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -1172,7 +1172,7 @@ void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, cons
                     : cudaLaunchKernelEx(&cfg, k_coarse_cg_reg<16>, n, rowptr, col, val, b, x, p, tol, max_iter, st,
                                          grid_part, grid_bar);
             if (e != cudaSuccess)
-                throw std::runtime_error(std::string("CUDA launch failed (coarse cg registers): ") +
+                throw CudaError(std::string("CUDA launch failed (coarse cg registers): ") +
                                          cudaGetErrorString(e));
             check_launch("coarse cg registers");
             return;
@@ -1190,7 +1190,7 @@ void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, cons
         const cudaError_t e = cudaLaunchKernelEx(&cfg, k_coarse_cg_grid, n, rowptr, col, val, b, x, r, p, ap, tol,
                                                  max_iter, st, grid_part, grid_bar);
         if (e != cudaSuccess)
-            throw std::runtime_error(std::string("CUDA launch failed (coarse cg grid): ") + cudaGetErrorString(e));
+            throw CudaError(std::string("CUDA launch failed (coarse cg grid): ") + cudaGetErrorString(e));
         check_launch("coarse cg grid");
         return;
     }

@@ -14,8 +14,14 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <stdexcept>
 
 namespace hyb {
+
+/// CUDA runtime / launch failure (C ABI status HYB_CUDA_ERROR)
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 /// Per-level stencil/transfer tables for all local primitives (device ptrs).
 struct LevelTables {
