@@ -349,7 +349,7 @@ class Hierarchy {
         DevMem gidx, pos, flag;   // this process's owned min-level DoFs
         DevMem vec;               // b, x, r, p, ap (n each)
         DevMem status;            // CoarseStatus
-        DevMem grid;              // whole-GPU CG: 2 x #SMs partials, then 2 barrier words
+        DevMem grid;              // whole-GPU CG: 4 x #SMs partials, then 2 barrier words
         double* grid_part() const { return grid.bytes() ? grid.as<double>() : nullptr; }
         unsigned* grid_bar() const {
             return grid.bytes() ? reinterpret_cast<unsigned*>(grid.as<char>() + grid.bytes() - 64) : nullptr;

@@ -969,6 +969,50 @@ __device__ double grid_sum(double s, double* red, double* part, unsigned* bar) {
     return block_sum(t, red);
 }
 
+// two sums at once (one barrier): red needs 66 doubles, part 2 x gridDim.x
+__device__ double2 block_sum2(double2 s, double* red) {
+    for (int o = 16; o > 0; o >>= 1) {
+        s.x += __shfl_down_sync(0xffffffffu, s.x, o);
+        s.y += __shfl_down_sync(0xffffffffu, s.y, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        red[w] = s.x;
+        red[33 + w] = s.y;
+    }
+    __syncthreads();
+    if (w == 0) {
+        double a = l < CGG_THREADS / 32 ? red[l] : 0.0, b = l < CGG_THREADS / 32 ? red[33 + l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_down_sync(0xffffffffu, a, o);
+            b += __shfl_down_sync(0xffffffffu, b, o);
+        }
+        if (l == 0) {
+            red[32] = a;
+            red[65] = b;
+        }
+    }
+    __syncthreads();
+    const double2 out = make_double2(red[32], red[65]);
+    __syncthreads();
+    return out;
+}
+
+__device__ double2 grid_sum2(double2 s, double* red, double* part, unsigned* bar) {
+    const double2 bsum = block_sum2(s, red);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = bsum.x;
+        part[2 * blockIdx.x + 1] = bsum.y;
+    }
+    grid_barrier(bar);
+    double2 t = make_double2(0.0, 0.0);
+    for (int i = threadIdx.x; i < int(gridDim.x); i += CGG_THREADS) {
+        t.x += __ldcg(part + 2 * i);
+        t.y += __ldcg(part + 2 * i + 1);
+    }
+    return block_sum2(t, red);
+}
+
 __device__ double grid_dot(const double* u, const double* v, int64_t n, double* red, double* part, unsigned* bar) {
     const int64_t stride = int64_t(gridDim.x) * CGG_THREADS;
     double s = 0.0;
@@ -1049,22 +1093,24 @@ void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos,
 }
 
 // Register-resident variant (at most one row per thread, at most NZ entries
-// per row): the row's matrix entries and its x, r, p, Ap stay in registers for
-// the whole solve; per iteration only p is exchanged through L2 (one gather
-// round for the SpMV) plus the three grid reductions. Same row-to-thread
-// mapping and entry order as k_coarse_cg_grid: the same arithmetic.
+// per row): the row's matrix entries and its x, r, p, s = Ap, w = Ar stay in
+// registers for the whole solve; per iteration r is exchanged through L2 for
+// the SpMV, and gamma = (r, r), delta = (w, r) come from ONE two-value grid
+// reduction (Chronopoulos-Gear CG: the same iterates as cg_solve's recurrence
+// in exact arithmetic, two grid barriers per iteration instead of three).
+// Convergence is tested on gamma = ||r||^2 and confirmed by the true residual.
 template <int NZ>
 __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const int32_t* __restrict__ rowptr,
                                                                const int32_t* __restrict__ col,
                                                                const double* __restrict__ val,
-                                                               const double* __restrict__ b, double* x, double* P,
+                                                               const double* __restrict__ b, double* x, double* R,
                                                                double tol, int max_iter, CoarseStatus* st,
                                                                double* part, unsigned* bar) {
-    __shared__ double red[33];
+    __shared__ double red[66];
     const int64_t i = blockIdx.x * int64_t(CGG_THREADS) + threadIdx.x;
     const bool own = i < n;
-    double* part0 = part;
-    double* part1 = part + gridDim.x;
+    double* part0 = part;                  // 2 x gridDim.x
+    double* part1 = part + 2 * gridDim.x;  // 2 x gridDim.x
     int cj[NZ];
     double vj[NZ];
     int nz = 0;
@@ -1083,51 +1129,65 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const 
             vj[q] = 0.0;
         }
     }
-    const double bi = own ? b[i] : 0.0;
-    double xi = 0.0, ri = bi, pi = bi;
-    if (own) P[i] = pi;
-    double s = 0.0;
-    if (own) s += bi * bi;
-    const double target = tol * sqrt(grid_sum(s, red, part0, bar));
-    s = 0.0;
-    if (own) s += ri * ri;
-    double rs = grid_sum(s, red, part1, bar); // also publishes P
-    int it = 0, breakdown = 0;
-    while (it < max_iter && sqrt(rs) > target) {
-        double api = 0.0;
+    auto spmv = [&](const double* u) {
+        double acc = 0.0;
 #pragma unroll
         for (int q = 0; q < NZ; ++q)
-            if (q < nz) api += vj[q] * __ldcg(P + cj[q]);
-        s = 0.0;
-        if (own) s += pi * api;
-        const double pap = grid_sum(s, red, part0, bar);
-        if (pap <= 0.0) {
-            breakdown = 1;
+            if (q < nz) acc += vj[q] * __ldcg(u + cj[q]);
+        return acc;
+    };
+    const double bi = own ? b[i] : 0.0;
+    double xi = 0.0, ri = bi;
+    if (own) R[i] = ri;
+    double2 sb = make_double2(0.0, 0.0);
+    if (own) sb.x += bi * bi;
+    const double target = tol * sqrt(grid_sum2(sb, red, part0, bar).x); // also publishes R
+    double wi = spmv(R);
+    double2 gd = make_double2(0.0, 0.0);
+    if (own) {
+        gd.x += ri * ri;
+        gd.y += wi * ri;
+    }
+    double2 g = grid_sum2(gd, red, part1, bar);
+    double gamma = g.x;
+    double alpha = g.y > 0.0 ? gamma / g.y : 0.0;
+    double pi = ri, si = wi;
+    int it = 0, breakdown = (g.y > 0.0 || gamma == 0.0) ? 0 : 1;
+    int flip = 0;
+    while (!breakdown && it < max_iter && sqrt(gamma) > target) {
+        xi += alpha * pi;
+        ri -= alpha * si;
+        if (own) R[i] = ri;
+        grid_barrier(bar); // r published
+        wi = spmv(R);
+        gd = make_double2(0.0, 0.0);
+        if (own) {
+            gd.x += ri * ri;
+            gd.y += wi * ri;
+        }
+        g = grid_sum2(gd, red, flip ? part1 : part0, bar);
+        flip ^= 1;
+        const double gamma_new = g.x;
+        const double beta = gamma_new / gamma;
+        const double denom = g.y - beta * gamma_new / alpha;
+        if (!(denom > 0.0)) {
+            if (gamma_new > 0.0) breakdown = 1;
+            gamma = gamma_new;
+            ++it;
             break;
         }
-        const double alpha = rs / pap;
-        xi += alpha * pi;
-        ri -= alpha * api;
-        s = 0.0;
-        if (own) s += ri * ri;
-        const double rs_new = grid_sum(s, red, part1, bar);
-        const double beta = rs_new / rs;
+        alpha = gamma_new / denom;
         pi = ri + beta * pi;
-        if (own) P[i] = pi;
-        grid_barrier(bar);
-        rs = rs_new;
+        si = wi + beta * si;
+        gamma = gamma_new;
         ++it;
     }
     if (own) x[i] = xi;
     grid_barrier(bar); // x complete
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < NZ; ++q)
-        if (q < nz) acc += vj[q] * __ldcg(x + cj[q]);
-    const double ti = bi - acc;
-    s = 0.0;
-    if (own) s += ti * ti;
-    const double res = sqrt(grid_sum(s, red, part0, bar));
+    const double ti = bi - spmv(x);
+    double2 tr = make_double2(0.0, 0.0);
+    if (own) tr.x += ti * ti;
+    const double res = sqrt(grid_sum2(tr, red, flip ? part1 : part0, bar).x);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->iterations = it;
         st->breakdown = breakdown;

@@ -508,7 +508,7 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
     coarse_.status = DevMem(sizeof(CoarseStatus));
     HYB_CUDA(cudaMemsetAsync(coarse_.status.as<void>(), 0, sizeof(CoarseStatus), d.stream()));
     if (csr.n >= kCoarseGridMinRows) { // whole-GPU CG: per-CTA partials + barrier words
-        coarse_.grid = DevMem(size_t(2 * std::max(coarse_grid_blocks(), 1)) * 8 + 64);
+        coarse_.grid = DevMem(size_t(4 * std::max(coarse_grid_blocks(), 1)) * 8 + 64);
         HYB_CUDA(cudaMemsetAsync(coarse_.grid.as<void>(), 0, coarse_.grid.bytes(), d.stream()));
     }
 }
