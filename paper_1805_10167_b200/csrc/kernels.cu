@@ -1215,9 +1215,10 @@ void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, cons
                       double* grid_part, unsigned* grid_bar, int max_row_nnz, cudaStream_t stream) {
     if (n >= kCoarseGridMinRows && grid_part && grid_bar && coarse_grid_blocks() > 0) {
         const int64_t threads = int64_t(coarse_grid_blocks()) * CGG_THREADS;
-        if (n <= threads && max_row_nnz <= 16) { // register-resident rows
+        if (n <= threads && max_row_nnz <= 16) { // register-resident rows, just enough CTAs
+            const int blocks = int((n + CGG_THREADS - 1) / CGG_THREADS);
             cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3(unsigned(coarse_grid_blocks()));
+            cfg.gridDim = dim3(unsigned(blocks));
             cfg.blockDim = dim3(CGG_THREADS);
             cfg.stream = stream;
             cudaLaunchAttribute attr{};

@@ -138,9 +138,10 @@ void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos,
 // CG on the assembled constrained CSR system, one CTA (reference cg_solve,
 // src/solvers.cpp:226-259): x := A^-1 b to tol * ||b||, status written to st
 // min-level CG: one CTA (vectors in shared memory when they fit) below
-// kCoarseGridMinRows rows, else a cooperative one-CTA-per-SM launch that needs
+// kCoarseGridMinRows rows, else a cooperative launch of ceil(n / 512) CTAs
+// (register-resident rows, at most one CTA per SM) or one CTA per SM; both need
 // grid_part (>= 4 x #SMs doubles) and grid_bar (2 unsigned, zero-initialised)
-constexpr int64_t kCoarseGridMinRows = 16384;
+constexpr int64_t kCoarseGridMinRows = 2048;
 int coarse_grid_blocks();
 void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* b,
                       double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
