@@ -1,5 +1,5 @@
 """Config-2 hot kernels once each (after one warm-up round): apply, residual,
-Jacobi, restrict, prolongate-add at level 10 on channel(16,16) -- the command
+Jacobi, restrict, prolongate-add, fused residual+restrict at level 10 on channel(16,16) -- the command
 profiled with `ncu --set full` (one launch per kernel after -s skips)."""
 import os
 import sys
@@ -14,6 +14,7 @@ dom = H.DistributedDomain(mesh, 1)
 ctl = H.Controller(dom)
 A = H.StencilOperator(dom, H.LAPLACE, L - 1, L)
 x, b, y = (H.ScalarFunction(nm, dom, L - 1, L) for nm in ("x", "b", "y"))
+c = H.ScalarFunction("c", dom, L - 1, L - 1)
 H.interpolate_random(x, L, seed=1, stream=0)
 H.interpolate_random(b, L, seed=1, stream=1)
 for _ in range(2):  # round 0 warms up, round 1 is profiled
@@ -22,5 +23,6 @@ for _ in range(2):  # round 0 warms up, round 1 is profiled
     H.smooth_jacobi(A, ctl, b, x, 2.0 / 3.0, L)
     H.restrict_to_coarse(ctl, y, b, L - 1)
     H.prolongate_add(ctl, b, x, L - 1, H.SMOOTH_MASK)
+    H.residual_restrict(A, ctl, b, x, y, c, L - 1)
 dom.synchronize()
 print("done")
