@@ -12,12 +12,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--level", type=int, default=10)
 ap.add_argument("--min-level", type=int, default=0)
 ap.add_argument("--cycles", type=int, default=1)
+ap.add_argument("--smoother", default="jacobi")
 args = ap.parse_args()
 mesh = H.meshgen.channel(16, 16)
 dom = H.DistributedDomain(mesh, 1)
 ctl = H.Controller(dom)
 L = args.level
-mg = H.GridHierarchy(dom, ctl, H.LAPLACE, args.min_level, L, smoother="jacobi", omega=2.0 / 3.0, coarse_tol=1e-12)
+mg = H.GridHierarchy(dom, ctl, H.LAPLACE, args.min_level, L, smoother=args.smoother, omega=2.0 / 3.0, coarse_tol=1e-12)
 rhs = H.ScalarFunction("rhs", dom, args.min_level, L)
 x = H.ScalarFunction("x", dom, args.min_level, L)
 H.interpolate_random(rhs, L, seed=4, flag_mask=H.INNER)
