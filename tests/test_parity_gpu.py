@@ -354,3 +354,38 @@ def test_graph_replayed_vcycles_bitwise_equal_eager():
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]
     assert out[0][2] == 0 and out[1][2] >= 4
+
+
+MIXED = {1: H.DIRICHLET, 2: H.NEUMANN}  # channel: Dirichlet inflow side; ring8: Dirichlet outside, Neumann hole
+
+
+@pytest.mark.parametrize("mesh_name", ["channel21", "ring8"])
+@pytest.mark.parametrize("ranks", [1, 3])
+def test_vcycle_history_mixed_bc(mesh_name, ranks):
+    """Jacobi V(2,2) with Neumann rows (smoothed, transferred on the smooth
+    mask) vs the reference's composed cycle under the same boundary map."""
+    mesh = FIXTURES[mesh_name]()
+    L = 5
+    rig = Rig(mesh, ranks, 1, L, 2, MIXED)
+    rig.rand(0, L, seed=33)
+    mg = H.GridHierarchy(rig.dom, rig.ctl, H.LAPLACE, 1, L, MIXED, smoother="jacobi", omega=2.0 / 3.0,
+                         coarse_tol=1e-12)
+    rep = mg.solve(rig.f[0], rig.f[1], L, 0.0, 6)
+    ref_hist = rig.ref.vcycle_jacobi(0, 1, L, 2, 2, 2.0 / 3.0, 1e-12, 6)
+    rel = np.abs(np.array(rep.residuals) - ref_hist) / ref_hist
+    assert rel.max() <= 1e-8, (rep.residuals, ref_hist)
+    assert rep.residuals[-1] < 0.1 * rep.residuals[0]
+
+
+@pytest.mark.parametrize("mesh_name", ["channel21", "ring8"])
+def test_gridhierarchy_gs_mixed_bc_matches_reference(mesh_name):
+    """The reference's own GridHierarchy (hybrid GS) with a Neumann boundary."""
+    mesh = FIXTURES[mesh_name]()
+    L = 5
+    rig = Rig(mesh, 2, 1, L, 2, MIXED)
+    rig.rand(0, L, seed=34)
+    mg = H.GridHierarchy(rig.dom, rig.ctl, H.LAPLACE, 1, L, MIXED, smoother="gs", coarse_tol=1e-12)
+    rep = mg.solve(rig.f[0], rig.f[1], L, 0.0, 6)
+    ref_hist = rig.ref.gridhierarchy_solve(0, 1, L, 0.0, 6)
+    mine = np.array(rep.residuals)
+    assert np.max(np.abs(mine - ref_hist) / ref_hist) <= 1e-8, (mine, ref_hist)
