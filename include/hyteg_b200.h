@@ -201,6 +201,12 @@ int hyb_restrict(hyb_function* fine, hyb_function* coarse, int coarse_level, uin
  * columns next to the borders only. */
 int hyb_residual_restrict(hyb_operator* A, hyb_function* rhs, hyb_function* x, hyb_function* r,
                           hyb_function* coarse, int coarse_level);
+/* prolongate_add(e, x, coarse_level, INNER|NEUMANN) (solvers.cpp:421-422)
+ * followed by smooth_jacobi(A, rhs, x, omega, coarse_level + 1), fused on the
+ * faces: the corrected face interiors are formed on the fly, never stored.
+ * Bitwise the two calls in sequence. */
+int hyb_prolongate_add_jacobi(hyb_operator* A, hyb_function* e, hyb_function* rhs, hyb_function* x, double omega,
+                              int coarse_level);
 /* assign / add_scaled / dot / norm2 / max_abs     function.hpp:60-74 */
 int hyb_assign(double alpha, hyb_function* x1, double beta, hyb_function* x2, hyb_function* dst, int level,
                uint8_t mask);

@@ -631,6 +631,17 @@ int hyb_residual_restrict(hyb_operator* A, hyb_function* rhs, hyb_function* x, h
     });
 }
 
+int hyb_prolongate_add_jacobi(hyb_operator* A, hyb_function* e, hyb_function* rhs, hyb_function* x, double omega,
+                              int coarse_level) {
+    return guarded([&] {
+        need(A, "hyb_prolongate_add_jacobi");
+        need(e, "hyb_prolongate_add_jacobi");
+        need(rhs, "hyb_prolongate_add_jacobi");
+        need(x, "hyb_prolongate_add_jacobi");
+        hyb::prolongate_add_jacobi(*A->a, *e->f, *rhs->f, *x->f, omega, coarse_level);
+    });
+}
+
 int hyb_assign(double alpha, hyb_function* x1, double beta, hyb_function* x2, hyb_function* dst, int level,
                uint8_t mask) {
     return guarded([&] {

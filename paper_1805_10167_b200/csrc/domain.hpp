@@ -256,6 +256,9 @@ void residual(const Operator& A, Function& rhs, Function& x, Function& r, int le
 void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level, double* dotp = nullptr);
 /// dst = A src (all flags) and returns src.dst, one pass over the faces
 double apply_dot(const Operator& A, Function& src, Function& dst, int level);
+/// prolongate_add(e -> x) then one weighted-Jacobi sweep, fused on the faces
+void prolongate_add_jacobi(const Operator& A, Function& e, Function& rhs, Function& x, double omega, int coarse_level,
+                           double* dotp = nullptr);
 /// first sweep from x = 0: does not read x (Hierarchy::cycle)
 void smooth_jacobi_zero(const Operator& A, Function& rhs, Function& x, double omega, int level);
 void smooth_gs(const Operator& A, Function& rhs, Function& x, int level);
@@ -315,6 +318,7 @@ class Hierarchy {
     // captured kernel/NCCL sequence can be replayed while the pointers match.
   public:
     bool use_graphs = true;
+    bool fuse_post_ = true; // prolongate_add fused with the first Jacobi post-sweep
     int64_t graph_replays = 0;
 
   private:

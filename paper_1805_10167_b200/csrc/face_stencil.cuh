@@ -70,11 +70,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
+// ST_JACOBI_PROLONG also stages coarse rows R, R+1 of each fine row q (R = q/2),
+// coarse columns [c0/2 - 2, c0/2 + FS_CW - 2)
+constexpr int FS_CW = FS_COLS / 2 + 4;
+
+// ring depth: the fused prolongation mode stages coarse rows too, so it keeps
+// 6 stages to stay within the 48 KB of static shared memory
+template <int MODE> constexpr int fs_stages() { return MODE == ST_JACOBI_PROLONG ? 6 : FS_S; }
+
 template <int MODE> struct FaceSmem {
-    double x[FS_S][MODE == ST_RESTRICT_RESIDUAL ? FS_XW_RR : FS_XW];
-    double b[MODE == ST_APPLY ? 1 : FS_S][MODE == ST_RESTRICT_RESIDUAL ? FS_BW_RR : FS_COLS];
-    uint64_t full[FS_S];
-    uint64_t empty[FS_S];
+    static constexpr int NS = fs_stages<MODE>();
+    double x[NS][MODE == ST_RESTRICT_RESIDUAL ? FS_XW_RR : FS_XW];
+    double b[MODE == ST_APPLY ? 1 : NS][MODE == ST_RESTRICT_RESIDUAL ? FS_BW_RR : FS_COLS];
+    double cr[MODE == ST_JACOBI_PROLONG ? NS : 1][2][MODE == ST_JACOBI_PROLONG ? FS_CW : 2];
+    uint64_t full[NS];
+    uint64_t empty[NS];
 };
 
 // ST_RESTRICT_RESIDUAL: y is the coarse arena (level L-1, row offsets cro,
@@ -87,13 +97,16 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                                                                  const double* __restrict__ b,
                                                                  double* __restrict__ y, double omega,
                                                                  const int64_t* __restrict__ cro, int64_t cstride,
-                                                                 double* __restrict__ dotp) {
+                                                                 double* __restrict__ dotp,
+                                                                 const double* __restrict__ xc) {
     constexpr bool RR = MODE == ST_RESTRICT_RESIDUAL;
+    constexpr bool JP = MODE == ST_JACOBI_PROLONG; // xc: coarse correction (level L-1, cro, cstride)
     constexpr int XOFF = RR ? 4 : 2;           // smem x index of column c0
     constexpr int XW = RR ? FS_XW_RR : FS_XW;  // staged x width
     constexpr int BOFF = RR ? 2 : 0;           // smem b index of column c0
     constexpr int BW = RR ? FS_BW_RR : FS_COLS;
     __shared__ __align__(128) FaceSmem<MODE> sm;
+    constexpr int NS = FaceSmem<MODE>::NS;
     const int n = t.n, W = t.W;
     const int face = blockIdx.z;
     const int c0 = blockIdx.x * (RR ? FS_COLS_RR : FS_COLS);
@@ -131,7 +144,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < FS_S; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], FS_CWARPS);
         }
@@ -145,8 +158,8 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
             const double* xf = x + base;
             const double* bf = b + base;
             for (int i = 0; i < nstage; ++i) {
-                const int s = i % FS_S;
-                mbar_wait(&sm.empty[s], ((i / FS_S) & 1) ^ 1);
+                const int s = i % NS;
+                mbar_wait(&sm.empty[s], ((i / NS) & 1) ^ 1);
                 const int q = r_lo - 1 + i; // x row of this stage
                 const int plen = (W - q + 3) & ~3; // padded row length
                 const int xs = c0 - XOFF < 0 ? 0 : c0 - XOFF;
@@ -160,10 +173,30 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                     const int be = c0 - BOFF + BW < pb ? c0 - BOFF + BW : pb;
                     bb = be > bs0 ? uint32_t(be - bs0) * 8u : 0u;
                 }
-                mbar_arrive_expect_tx(&sm.full[s], bx + bb);
+                uint32_t bc[2] = {0u, 0u};
+                int cs0[2] = {0, 0};
+                if (JP) { // coarse rows R, R+1 (closed rows nc+1-R long, padded to 4)
+                    const int nc = n / 2, C0 = c0 / 2;
+                    for (int h = 0; h < 2; ++h) {
+                        const int R = (q >> 1) + h;
+                        if (R > nc) continue;
+                        const int plc = (nc + 1 - R + 3) & ~3;
+                        cs0[h] = C0 - 2 < 0 ? 0 : C0 - 2;
+                        const int ce = C0 - 2 + FS_CW < plc ? C0 - 2 + FS_CW : plc;
+                        bc[h] = ce > cs0[h] ? uint32_t(ce - cs0[h]) * 8u : 0u;
+                    }
+                }
+                mbar_arrive_expect_tx(&sm.full[s], bx + bb + bc[0] + bc[1]);
                 if (bx) bulk_g2s(&sm.x[s][xs - (c0 - XOFF)], xf + ro[q] + xs, bx, &sm.full[s]);
                 if (MODE != ST_APPLY && bb)
                     bulk_g2s(&sm.b[s][bs0 - (c0 - BOFF)], bf + ro[q - 1] + bs0, bb, &sm.full[s]);
+                if (JP) {
+                    const double* cf = xc + int64_t(face) * cstride;
+                    for (int h = 0; h < 2; ++h)
+                        if (bc[h])
+                            bulk_g2s(&sm.cr[s][h][cs0[h] - (c0 / 2 - 2)], cf + cro[(q >> 1) + h] + cs0[h], bc[h],
+                                     &sm.full[s]);
+                }
             }
         }
         return;
@@ -184,13 +217,14 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     // ST_RESTRICT_RESIDUAL: residual rows q-2 (s*) and q-1 (h*) at c-1, c, c+1
     double sl = 0, s0 = 0, s1 = 0, hl = 0, h0 = 0, h1 = 0;
     const int nc = n / 2;
-    const int C = c / 2; // coarse column of this lane (RR)
+    const int C = c / 2; // coarse column of this lane (RR, JP)
+
     // optional dot partials (dotp): APPLY x.(Ax), JACOBI b.x_new, per lane for
     // its two columns over the band's rows, then a fixed tree over the CTA
     double d0 = 0.0, d1 = 0.0;
     for (int i = 0; i < nstage; ++i) {
-        const int s = i % FS_S;
-        mbar_wait(&sm.full[s], (i / FS_S) & 1);
+        const int s = i % NS;
+        mbar_wait(&sm.full[s], (i / NS) & 1);
         const double* sx = sm.x[s];
         const double2 pl2 = *reinterpret_cast<const double2*>(sx + k - 2);
         const double2 pc2 = *reinterpret_cast<const double2*>(sx + k);
@@ -199,7 +233,32 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         if (MODE != ST_APPLY && i >= 2) bb = *reinterpret_cast<const double2*>(&sm.b[s][kb]);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
-        const double pl = pl2.y, p0 = pc2.x, p1 = pc2.y, pr = pr2.x;
+        double pl = pl2.y, p0 = pc2.x, p1 = pc2.y, pr = pr2.x;
+        if (JP) { // x row q = r_lo-1+i at columns c-1 .. c+2: add P e at points >= 2 away from the border
+            const int q = r_lo - 1 + i;
+            // staged coarse columns C-1, C, C+1 (C = c/2) of rows R (index 0) and R+1 (1)
+            const double* c0r = sm.cr[s][0] + tid + 1;
+            const double* c1r = sm.cr[s][1] + tid + 1;
+            const double l0 = c0r[0], a0 = c0r[1], r0 = c0r[2];
+            const double l1 = c1r[0], a1 = c1r[1], r1 = c1r[2];
+            double vl, v0, v1, vr; // prolongation at columns c-1, c, c+1, c+2 (k_prolongate_faces' formulas)
+            if ((q & 1) == 0) {
+                vl = 0.5 * (l0 + a0);
+                v0 = a0;
+                v1 = 0.5 * (a0 + r0);
+                vr = r0;
+            } else {
+                vl = 0.5 * (a0 + l1);
+                v0 = 0.5 * (a0 + a1);
+                v1 = 0.5 * (r0 + a1);
+                vr = 0.5 * (r0 + r1);
+            }
+            auto deep = [&](int col) { return q >= 2 && col >= 2 && col + q <= n - 2; };
+            if (deep(c - 1)) pl = pl + vl;
+            if (deep(c)) p0 = p0 + v0;
+            if (deep(c + 1)) p1 = p1 + v1;
+            if (deep(c + 2)) pr = pr + vr;
+        }
         if (RR && i >= 2) {
             // residual of fine row q at c, c+1, same operations as
             // ST_RESIDUAL; every lane computes (the shuffle follows)
@@ -257,7 +316,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                 if (MODE == ST_RESIDUAL) {
                     o0 = bb.x - a0;
                     o1 = bb.y - a1;
-                } else if (MODE == ST_JACOBI) {
+                } else if (MODE == ST_JACOBI || JP) {
                     o0 = z0 + div_by(omega * (bb.x - a0), dg, rdg); // x + omega*(b - Ax)/diag
                     o1 = z1 + div_by(omega * (bb.y - a1), dg, rdg);
                 }
@@ -265,7 +324,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                     if (MODE == ST_APPLY) {
                         if (v0) d0 = d0 + z0 * o0;
                         if (v1) d1 = d1 + z1 * o1;
-                    } else if (MODE == ST_JACOBI) {
+                    } else if (MODE == ST_JACOBI || JP) {
                         if (v0) d0 = d0 + bb.x * o0;
                         if (v1) d1 = d1 + bb.y * o1;
                     }

@@ -30,8 +30,6 @@ inline void check_launch(const char* what) {
     if (e != cudaSuccess) throw CudaError(std::string("CUDA launch failed (") + what + "): " + cudaGetErrorString(e));
 }
 
-__device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-__device__ __forceinline__ double shfl_down1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
 // ---------------------------------------------------------------------------
 #include "face_stencil.cuh"
@@ -565,15 +563,15 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
         const dim3 grid = face_stencil_grid(t);
         switch (mode) {
         case ST_APPLY:
-            if (dotp) k_face_stencil<ST_APPLY, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp);
-            else k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr);
+            if (dotp) k_face_stencil<ST_APPLY, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp, nullptr);
+            else k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr);
             break;
         case ST_RESIDUAL:
-            k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr);
+            k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr);
             break;
         default:
-            if (dotp) k_face_stencil<ST_JACOBI, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp);
-            else k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr);
+            if (dotp) k_face_stencil<ST_JACOBI, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp, nullptr);
+            else k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr);
             break;
         }
         check_launch("face stencil");
@@ -611,8 +609,8 @@ void launch_ghost_pack(const int64_t* src, int64_t n, const double* arena, doubl
 }
 
 void launch_prolongate(const LevelTables& tc, const LevelTables& tf, const FlagTables& ff, const double* xc,
-                       double* xf, uint8_t mask, bool add, cudaStream_t st) {
-    if ((mask & F_INNER) && tf.nfaces > 0 && tf.n >= 3) {
+                       double* xf, uint8_t mask, bool add, cudaStream_t st, bool faces) {
+    if (faces && (mask & F_INNER) && tf.nfaces > 0 && tf.n >= 3) {
         k_prolongate_faces<<<transfer_grid(tc.n, tf.nfaces), TR_WARPS * 32, 0, st>>>(tc, tf, xc, xf, add);
         check_launch("prolongate faces");
     }
@@ -670,12 +668,65 @@ void launch_restrict(const LevelTables& tc, const LevelTables& tf, const FlagTab
     launch_restrict_ev(tc, tf, cf, xf, xc, mask, st);
 }
 
+// fine += P coarse on the face points next to the border (row 1, column 1,
+// diagonal c + r = n-1), each once; k_prolongate_faces' formulas
+__global__ void __launch_bounds__(128) k_prolongate_layer(LevelTables tc, LevelTables tf, const double* __restrict__ xc,
+                                                          double* xf) {
+    const int n = tf.n, nc = tc.n;
+    const int k = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int seg = blockIdx.y;
+    int col, row;
+    if (seg == 0) { // row 1, columns 1 .. n-2
+        row = 1;
+        col = k;
+        if (col > n - 2) return;
+    } else if (seg == 1) { // column 1, rows 2 .. n-3
+        col = 1;
+        row = k + 1;
+        if (row > n - 3) return;
+    } else { // diagonal, rows 2 .. n-2
+        row = k + 1;
+        col = n - 1 - row;
+        if (row > n - 2) return;
+    }
+    const double* cv = xc + int64_t(blockIdx.z) * tc.face_stride;
+    const int64_t* __restrict__ cro = tc.rowoff;
+    auto C = [&](int cc, int R) { return (cc >= 0 && R >= 0 && cc + R <= nc) ? __ldg(cv + cro[R] + cc) : 0.0; };
+    const int R = row >> 1, cc = col >> 1;
+    double v;
+    if ((row & 1) == 0) v = (col & 1) == 0 ? C(cc, R) : 0.5 * (C(cc, R) + C(cc + 1, R));
+    else v = (col & 1) == 0 ? 0.5 * (C(cc, R) + C(cc, R + 1)) : 0.5 * (C(cc + 1, R) + C(cc, R + 1));
+    double* p = xf + int64_t(blockIdx.z) * tf.face_stride + tf.rowoff[row] + col;
+    *p = *p + v;
+}
+
+void launch_prolongate_layer(const LevelTables& tc, const LevelTables& tf, const double* xc, double* xf,
+                             cudaStream_t st) {
+    if (tf.nfaces <= 0 || tf.n < 3) return;
+    const dim3 grid(unsigned((tf.n - 2 + 127) / 128), 3u, unsigned(tf.nfaces));
+    k_prolongate_layer<<<grid, 128, 0, st>>>(tc, tf, xc, xf);
+    check_launch("prolongate border layer");
+}
+
+void launch_jacobi_prolong_faces(const LevelTables& tc, const LevelTables& tf, const double* x, const double* xc,
+                                 const double* b, double* y, double omega, double* dotp, cudaStream_t st) {
+    if (tf.nfaces <= 0 || tf.n < 3) return;
+    const dim3 grid = face_stencil_grid(tf);
+    if (dotp)
+        k_face_stencil<ST_JACOBI_PROLONG, true><<<grid, FS_THREADS, 0, st>>>(tf, x, b, y, omega, tc.rowoff,
+                                                                             tc.face_stride, dotp, xc);
+    else
+        k_face_stencil<ST_JACOBI_PROLONG><<<grid, FS_THREADS, 0, st>>>(tf, x, b, y, omega, tc.rowoff, tc.face_stride,
+                                                                       nullptr, xc);
+    check_launch("jacobi after prolongation faces");
+}
+
 void launch_residual_restrict_faces(const LevelTables& tc, const LevelTables& tf, const double* x, const double* b,
                                     double* r, double* xc, cudaStream_t st) {
     if (tf.nfaces <= 0 || tf.n < 3) return;
     if (tc.n >= 3) {
         k_face_stencil<ST_RESTRICT_RESIDUAL><<<face_rr_grid(tf), FS_THREADS, 0, st>>>(tf, x, b, xc, 0.0, tc.rowoff,
-                                                                                      tc.face_stride, nullptr);
+                                                                                      tc.face_stride, nullptr, nullptr);
         check_launch("residual+restrict faces");
     }
     const dim3 grid(unsigned((tf.n - 2 + 127) / 128), 3u, unsigned(tf.nfaces));
@@ -957,16 +1008,6 @@ __device__ double block_sum(double s, double* red) {
     const double out = red[32];
     __syncthreads();
     return out;
-}
-
-// grid-wide sum of one value per thread, identical in every CTA
-__device__ double grid_sum(double s, double* red, double* part, unsigned* bar) {
-    const double b = block_sum(s, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = b;
-    grid_barrier(bar);
-    double t = 0.0;
-    for (int i = threadIdx.x; i < int(gridDim.x); i += CGG_THREADS) t += __ldcg(part + i);
-    return block_sum(t, red);
 }
 
 // two sums at once (one barrier): red needs 66 doubles, part 2 x gridDim.x

@@ -57,7 +57,18 @@ struct FlagTables {
 // corrections, PCG's z): y = 0 + omega * (b - 0) / diag on non-Dirichlet rows,
 // y = b on Dirichlet rows (x there would be the cycle's assign of rhs);
 // bitwise the ST_JACOBI sweep of a zero-filled x, without reading x
-enum StencilMode : int { ST_APPLY = 0, ST_RESIDUAL = 1, ST_JACOBI = 2, ST_RESTRICT_RESIDUAL = 3, ST_JACOBI_ZERO = 4 };
+// ST_JACOBI_PROLONG: a weighted-Jacobi sweep of x + P e (the cycle's
+// coarse-grid correction followed by the first post-smoothing sweep): the
+// corrected x is formed on the fly at face points two or more away from the
+// border; border rows and the layer next to them already hold x + P e.
+enum StencilMode : int {
+    ST_APPLY = 0,
+    ST_RESIDUAL = 1,
+    ST_JACOBI = 2,
+    ST_RESTRICT_RESIDUAL = 3,
+    ST_JACOBI_ZERO = 4,
+    ST_JACOBI_PROLONG = 5
+};
 
 // ---- launchers (all asynchronous on `st`) ----
 // parts: 1 = face interiors (K1), 2 = edge lines + vertices (K2/K3), 3 = both
@@ -79,7 +90,7 @@ void launch_ghost_gather(const void* dst, const void* src, bool idx32, int64_t n
 /// send[i] = arena[src[i]] (owned values other processes hold ghosts of)
 void launch_ghost_pack(const int64_t* src, int64_t n, const double* arena, double* send, cudaStream_t st);
 void launch_prolongate(const LevelTables& coarse, const LevelTables& fine, const FlagTables& fine_flags,
-                       const double* xc, double* xf, uint8_t mask, bool add, cudaStream_t st);
+                       const double* xc, double* xf, uint8_t mask, bool add, cudaStream_t st, bool faces = true);
 void launch_restrict(const LevelTables& coarse, const LevelTables& fine, const FlagTables& coarse_flags,
                      const double* xf, double* xc, uint8_t mask, cudaStream_t st);
 // edge/vertex part of launch_restrict only
@@ -88,6 +99,14 @@ void launch_restrict_ev(const LevelTables& coarse, const LevelTables& fine, cons
 // fused residual + restriction on face interiors: xc (coarse face interiors)
 // := P^T (b - A x); r := b - A x on the fine faces' border layer only (row 1,
 // column 1, diagonal). fine tables carry the operator's coefficients.
+// fine += P coarse on the face border layer (row 1, column 1, diagonal)
+void launch_prolongate_layer(const LevelTables& coarse, const LevelTables& fine, const double* xc, double* xf,
+                             cudaStream_t st);
+// y's face interiors := one weighted-Jacobi sweep of x + P xc, where x already
+// holds the correction on the border rows and the layer next to them
+// (ST_JACOBI_PROLONG); dotp as launch_stencil
+void launch_jacobi_prolong_faces(const LevelTables& coarse, const LevelTables& fine, const double* x, const double* xc,
+                                 const double* b, double* y, double omega, double* dotp, cudaStream_t st);
 void launch_residual_restrict_faces(const LevelTables& coarse, const LevelTables& fine, const double* x,
                                     const double* b, double* r, double* xc, cudaStream_t st);
 // hybrid Gauss-Seidel: face tiles (face, I, J, dependency bits) over skewed

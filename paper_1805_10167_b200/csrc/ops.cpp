@@ -254,6 +254,37 @@ void prolongate(Function& coarse, Function& fine, int lc, uint8_t mask, bool add
     d.timer_end();
 }
 
+// prolongate(e -> x, smooth mask, add) followed by smooth_jacobi(A, rhs, x,
+// omega, lc+1), fused on the faces (ST_JACOBI_PROLONG): edges, vertices and
+// the face layer next to the borders take the correction in place, a sync
+// refreshes the ghosts, and the face kernel forms x + P e on the fly for the
+// remaining points, so the corrected face interiors are never stored.
+// Bitwise the two operations in sequence.
+void prolongate_add_jacobi(const Operator& A, Function& e, Function& rhs, Function& x, double omega, int lc,
+                           double* dotp) {
+    const int level = lc + 1;
+    check_transfer(e, x, lc, "prolongate");
+    check_op_function(A, rhs, level, "smooth_jacobi", true);
+    check_op_function(A, x, level, "smooth_jacobi", true);
+    if (&rhs == &x) throw InvalidArgument("smooth_jacobi: rhs and x must be distinct functions");
+    check_diagonals(A, x, level, "smooth_jacobi");
+    Domain& d = A.domain();
+    d.sync(e, lc);
+    const LevelTables& tc = d.level(lc).t;
+    const LevelTables t = A.tables(level);
+    launch_prolongate(tc, t, x.flags(), e.data(lc), x.data(level), kSmoothMask, true, d.stream(), false);
+    launch_prolongate_layer(tc, t, e.data(lc), x.data(level), d.stream());
+    d.sync(x, level);
+    DevMem& next = d.jacobi_scratch(level);
+    launch_stencil(ST_JACOBI, t, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
+                   d.stream(), 2);
+    d.timer_begin("prolongate_jacobi");
+    launch_jacobi_prolong_faces(tc, t, x.data(level), e.data(lc), rhs.data(level), next.as<double>(), omega, dotp,
+                                d.stream());
+    d.timer_end();
+    x.arena(level).swap(next);
+}
+
 void restrict_to_coarse(Function& fine, Function& coarse, int lc, uint8_t mask) {
     check_transfer(coarse, fine, lc, "restrict_to_coarse");
     Domain& d = fine.domain();
@@ -620,10 +651,17 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
     residual_restrict(a_, rhs, x, r_, b_, level - 1); // residual + restrict_to_coarse, fused
     fill_const(b_, 0.0, level - 1, kDirichletMask);
     cycle(b_, e_, level - 1, nu_pre, nu_post, true); // e = 0 on entry
-    // prolongate(e -> r) + add_scaled(x, 1, r) on the smooth mask, fused
-    prolongate(e_, x, level - 1, kSmoothMask, true);
-    for (int i = 0; i < nu_post; ++i)
-        smooth(rhs, x, level, (level == cycle_dot_level_ && i == nu_post - 1) ? cycle_dot_ : nullptr);
+    // prolongate(e -> r) + add_scaled(x, 1, r) on the smooth mask, fused; with
+    // Jacobi post-smoothing also fused with the first sweep
+    auto dot_for = [&](int i) { return (level == cycle_dot_level_ && i == nu_post - 1) ? cycle_dot_ : nullptr; };
+    int i0 = 0;
+    if (nu_post > 0 && smoother_ == SMOOTH_JACOBI && fuse_post_) {
+        prolongate_add_jacobi(a_, e_, rhs, x, omega_, level - 1, dot_for(0));
+        i0 = 1;
+    } else {
+        prolongate(e_, x, level - 1, kSmoothMask, true);
+    }
+    for (int i = i0; i < nu_post; ++i) smooth(rhs, x, level, dot_for(i));
 }
 
 // reference src/solvers.cpp:430-442: residual, gather into the global coarse

@@ -408,6 +408,13 @@ def residual_restrict(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, 
     check(lib.hyb_residual_restrict(A._h, rhs._h, x._h, r._h, coarse._h, coarse_level))
 
 
+def prolongate_add_jacobi(A: StencilOperator, ctl: Controller, e: ScalarFunction, rhs: ScalarFunction,  # noqa: ARG001
+                          x: ScalarFunction, omega: float, coarse_level: int) -> None:
+    """prolongate_add(e -> x, smooth mask) then smooth_jacobi(rhs, x, omega),
+    fused (the V-cycle's correction and first post-smoothing sweep)."""
+    check(lib.hyb_prolongate_add_jacobi(A._h, e._h, rhs._h, x._h, omega, coarse_level))
+
+
 def assign(alpha: float, x1: ScalarFunction, beta: float, x2: ScalarFunction, dst: ScalarFunction, level: int,
            flag_mask: int = ALL_DOF_FLAGS) -> None:
     check(lib.hyb_assign(alpha, x1._h, beta, x2._h, dst._h, level, flag_mask))
