@@ -74,8 +74,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // coarse columns [c0/2 - 2, c0/2 + FS_CW - 2)
 constexpr int FS_CW = FS_COLS / 2 + 4;
 
-// ring depth: the fused prolongation mode stages coarse rows too, so it keeps
-// 6 stages to stay within the 48 KB of static shared memory
+// ring depth (the fused prolongation mode, with coarse rows staged too, needs
+// ~50 KB: it uses dynamic shared memory)
 template <int MODE> constexpr int fs_stages() { return MODE == ST_JACOBI_PROLONG ? 6 : FS_S; }
 
 template <int MODE> struct FaceSmem {
@@ -105,8 +105,10 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     constexpr int XW = RR ? FS_XW_RR : FS_XW;  // staged x width
     constexpr int BOFF = RR ? 2 : 0;           // smem b index of column c0
     constexpr int BW = RR ? FS_BW_RR : FS_COLS;
-    __shared__ __align__(128) FaceSmem<MODE> sm;
     constexpr int NS = FaceSmem<MODE>::NS;
+    extern __shared__ __align__(128) unsigned char fs_dyn[];
+    __shared__ __align__(128) unsigned char fs_static[MODE == ST_JACOBI_PROLONG ? 16 : sizeof(FaceSmem<MODE>)];
+    FaceSmem<MODE>& sm = *reinterpret_cast<FaceSmem<MODE>*>(MODE == ST_JACOBI_PROLONG ? fs_dyn : fs_static);
     const int n = t.n, W = t.W;
     const int face = blockIdx.z;
     const int c0 = blockIdx.x * (RR ? FS_COLS_RR : FS_COLS);
@@ -253,11 +255,12 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                 v1 = 0.5 * (r0 + a1);
                 vr = 0.5 * (r0 + r1);
             }
-            auto deep = [&](int col) { return q >= 2 && col >= 2 && col + q <= n - 2; };
-            if (deep(c - 1)) pl = pl + vl;
-            if (deep(c)) p0 = p0 + v0;
-            if (deep(c + 1)) p1 = p1 + v1;
-            if (deep(c + 2)) pr = pr + vr;
+            // points two or more away from every border take the correction here
+            const int lim = q >= 2 ? n - 2 - q : -1; // deep columns 2 .. lim
+            pl = (c - 1 >= 2 && c - 1 <= lim) ? pl + vl : pl;
+            p0 = (c >= 2 && c <= lim) ? p0 + v0 : p0;
+            p1 = (c + 1 >= 2 && c + 1 <= lim) ? p1 + v1 : p1;
+            pr = (c + 2 >= 2 && c + 2 <= lim) ? pr + vr : pr;
         }
         if (RR && i >= 2) {
             // residual of fine row q at c, c+1, same operations as

@@ -712,12 +712,20 @@ void launch_jacobi_prolong_faces(const LevelTables& tc, const LevelTables& tf, c
                                  const double* b, double* y, double omega, double* dotp, cudaStream_t st) {
     if (tf.nfaces <= 0 || tf.n < 3) return;
     const dim3 grid = face_stencil_grid(tf);
+    constexpr size_t smem = sizeof(FaceSmem<ST_JACOBI_PROLONG>);
+    static const bool attr = cudaFuncSetAttribute(k_face_stencil<ST_JACOBI_PROLONG, true>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) ==
+                                 cudaSuccess &&
+                             cudaFuncSetAttribute(k_face_stencil<ST_JACOBI_PROLONG, false>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) ==
+                                 cudaSuccess;
+    if (!attr) throw CudaError("jacobi after prolongation: cannot reserve shared memory");
     if (dotp)
-        k_face_stencil<ST_JACOBI_PROLONG, true><<<grid, FS_THREADS, 0, st>>>(tf, x, b, y, omega, tc.rowoff,
-                                                                             tc.face_stride, dotp, xc);
+        k_face_stencil<ST_JACOBI_PROLONG, true><<<grid, FS_THREADS, smem, st>>>(tf, x, b, y, omega, tc.rowoff,
+                                                                                tc.face_stride, dotp, xc);
     else
-        k_face_stencil<ST_JACOBI_PROLONG><<<grid, FS_THREADS, 0, st>>>(tf, x, b, y, omega, tc.rowoff, tc.face_stride,
-                                                                       nullptr, xc);
+        k_face_stencil<ST_JACOBI_PROLONG><<<grid, FS_THREADS, smem, st>>>(tf, x, b, y, omega, tc.rowoff,
+                                                                          tc.face_stride, nullptr, xc);
     check_launch("jacobi after prolongation faces");
 }
 
