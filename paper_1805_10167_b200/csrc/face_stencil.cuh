@@ -76,7 +76,7 @@ constexpr int FS_CW = FS_COLS / 2 + 4;
 
 // ring depth (the fused prolongation mode, with coarse rows staged too, needs
 // ~50 KB: it uses dynamic shared memory)
-template <int MODE> constexpr int fs_stages() { return MODE == ST_JACOBI_PROLONG ? 6 : FS_S; }
+template <int MODE> constexpr int fs_stages() { return MODE == ST_JACOBI_PROLONG ? 4 : FS_S; }
 
 template <int MODE> struct FaceSmem {
     static constexpr int NS = fs_stages<MODE>();
