@@ -154,6 +154,21 @@ int hyb_function_download(hyb_function* f, int level, double* host, int64_t n, i
 int hyb_function_upload_async(hyb_function* f, int level, const double* host, int64_t n, uint8_t mask);
 int hyb_function_download_async(hyb_function* f, int level, double* host, int64_t n);
 int hyb_function_flags(hyb_function* f, int level, uint8_t* flags, int64_t n, int global_order);
+/* One primitive's data in the reference's checkpoint / migration format:
+ * DataCallbacks::serialize / ::deserialize of a ScalarFunction
+ * (src/field.cpp:157-175; the bytes MessageBuffer holds, buffer.hpp) - every
+ * level of the function: i64 level, the primitive's per-slot values (faces:
+ * the closed triangle; edges: line + per face halo rows 0 and 1; vertices:
+ * own value + one ghost per edge) and their flags. Serialisation first
+ * refreshes the ghosts of every level (the reference's state after sync_all),
+ * so the record equals the reference's for the same owned values.
+ * serialize: *len = record size; out == NULL is a size query; cap < *len is
+ * HYB_INVALID_ARGUMENT. deserialize: levels, sizes and flags must match this
+ * function (HYB_INVALID_ARGUMENT otherwise); owned and ghost slots are set,
+ * an edge's halo row 0 (not stored on the device) is ignored. The primitive
+ * must be owned by this process. */
+int hyb_function_serialize(hyb_function* f, uint64_t prim, uint8_t* out, int64_t cap, int64_t* len);
+int hyb_function_deserialize(hyb_function* f, uint64_t prim, const uint8_t* in, int64_t len);
 /* interpolate(f, const, level, mask) (function.hpp:55-56) */
 int hyb_interpolate_const(hyb_function* f, double value, int level, uint8_t mask);
 /* device counter-based U[lo,hi] keyed on (seed, stream, DoF identity) */

@@ -158,6 +158,18 @@ class ScalarFunction {
     void upload(int level, const std::vector<double>& v, std::uint8_t mask = ALL_DOF_FLAGS) {
         check(hyb_function_upload(h_, level, v.data(), int64_t(v.size()), 1, mask));
     }
+    /// the primitive's record as DataCallbacks::serialize writes it (field.cpp:157-175)
+    std::vector<std::uint8_t> serialize(std::uint64_t prim) const {
+        int64_t n = 0;
+        check(hyb_function_serialize(h_, prim, nullptr, 0, &n));
+        std::vector<std::uint8_t> out(static_cast<size_t>(n));
+        check(hyb_function_serialize(h_, prim, out.data(), n, &n));
+        return out;
+    }
+    /// DataCallbacks::deserialize into this function's slots of `prim`
+    void deserialize(std::uint64_t prim, const std::vector<std::uint8_t>& record) {
+        check(hyb_function_deserialize(h_, prim, record.data(), int64_t(record.size())));
+    }
 
   private:
     DistributedDomain* dom_;

@@ -44,6 +44,7 @@ def lib():
             "ref_flags": (i, [p, i, i, C.POINTER(C.c_uint8)]),
             "ref_coords": (i, [p, i, pd]),
             "ref_sync": (i, [p, i, i]),
+            "ref_serialize": (i, [p, i, C.c_uint64, C.POINTER(C.c_uint8), C.c_int64, C.POINTER(C.c_int64)]),
             "ref_apply": (i, [p, i, i, i, u8]),
             "ref_residual": (i, [p, i, i, i, i]),
             "ref_jacobi": (i, [p, i, i, d, i]),
@@ -146,6 +147,14 @@ class RefSession:
 
     def sync(self, fi, level):
         _ck(lib().ref_sync(self.h, fi, level))
+
+    def serialize(self, fi, prim) -> bytes:
+        """The reference's DataCallbacks::serialize of primitive `prim`'s data of function fi."""
+        n = C.c_int64()
+        _ck(lib().ref_serialize(self.h, fi, prim, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * max(n.value, 1))()
+        _ck(lib().ref_serialize(self.h, fi, prim, buf, n.value, C.byref(n)))
+        return bytes(buf[: n.value])
 
     def apply(self, src, dst, level, mask=7):
         _ck(lib().ref_apply(self.h, src, dst, level, mask))

@@ -201,6 +201,20 @@ int ref_sync(void* sp, int fi, int level) {
     });
 }
 
+// The reference's own DataCallbacks::serialize of one primitive's field data
+// (src/field.cpp:157-166): the checkpoint / migration byte format.
+int ref_serialize(void* sp, int fi, uint64_t prim, uint8_t* out, int64_t cap, int64_t* len) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        ScalarFunction& fn = *s.f.at(size_t(fi));
+        const Primitive& p = s.dom->primitive(PrimitiveID{prim});
+        MessageBuffer buf;
+        s.dom->callbacks(fn.handle()).serialize(primitive_data(p, fn.handle()), buf);
+        *len = int64_t(buf.size());
+        if (out && cap >= int64_t(buf.size())) std::memcpy(out, buf.bytes().data(), buf.size());
+    });
+}
+
 int ref_apply(void* sp, int src, int dst, int level, uint8_t mask) {
     return guard([&] {
         Session& s = *static_cast<Session*>(sp);

@@ -98,6 +98,8 @@ _SIGS = {
     "hyb_function_upload_async": (_i, [_p, _i, _pd, _i64, _u8]),
     "hyb_function_download_async": (_i, [_p, _i, _pd, _i64]),
     "hyb_function_flags": (_i, [_p, _i, _pu8, _i64, _i]),
+    "hyb_function_serialize": (_i, [_p, _u64, _pu8, _i64, C.POINTER(_i64)]),
+    "hyb_function_deserialize": (_i, [_p, _u64, _pu8, _i64]),
     "hyb_interpolate_const": (_i, [_p, _d, _i, _u8]),
     "hyb_interpolate_random": (_i, [_p, _i, _u64, _u64, _d, _d, _u8]),
     "hyb_sync": (_i, [_p, _i]),

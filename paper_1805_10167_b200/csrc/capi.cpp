@@ -439,6 +439,27 @@ int hyb_function_download_async(hyb_function* f, int level, double* host, int64_
     });
 }
 
+int hyb_function_serialize(hyb_function* f, uint64_t prim, uint8_t* out, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        need(f, "hyb_function_serialize");
+        need(len, "hyb_function_serialize");
+        const std::vector<uint8_t> rec = hyb::serialize_field(*f->f, prim);
+        *len = int64_t(rec.size());
+        if (!out) return; // size query
+        if (cap < *len) throw hyb::InvalidArgument("hyb_function_serialize: buffer too small");
+        std::memcpy(out, rec.data(), rec.size());
+    });
+}
+
+int hyb_function_deserialize(hyb_function* f, uint64_t prim, const uint8_t* in, int64_t len) {
+    return guarded([&] {
+        need(f, "hyb_function_deserialize");
+        need(in, "hyb_function_deserialize");
+        if (len < 0) throw hyb::InvalidArgument("hyb_function_deserialize: negative length");
+        hyb::deserialize_field(*f->f, prim, in, size_t(len));
+    });
+}
+
 int hyb_function_flags(hyb_function* fh, int level, uint8_t* flags, int64_t n, int global_order) {
     return guarded([&] {
         need(fh, "hyb_function_flags");

@@ -284,6 +284,12 @@ void download(Function& f, int level, double* host, int64_t n, bool global_order
 /// stream-ordered host transfers in local order (Domain::h2d_stream)
 void upload_async(Function& f, int level, const double* host, int64_t n, uint8_t mask);
 void download_async(Function& f, int level, double* host, int64_t n);
+/// one primitive's record in the reference's DataCallbacks::serialize format
+/// (src/field.cpp:157-175), taken after a ghost refresh of every level
+std::vector<uint8_t> serialize_field(Function& f, uint64_t id);
+/// inverse: values of the primitive's slots from such a record (levels, sizes
+/// and flags must match this function)
+void deserialize_field(Function& f, uint64_t id, const uint8_t* data, size_t len);
 
 enum Smoother : int { SMOOTH_JACOBI = 0, SMOOTH_GS = 1, SMOOTH_CGS = 2 };
 

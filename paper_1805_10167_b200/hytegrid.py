@@ -298,6 +298,22 @@ class ScalarFunction:
             raise ValueError("download_async needs a contiguous float64 array")
         check(lib.hyb_function_download_async(self._h, level, _pd(out), out.size))
 
+    def serialize(self, prim: int) -> bytes:
+        """The primitive's record in the reference's DataCallbacks::serialize
+        format (src/field.cpp:157-175), after a ghost refresh of every level."""
+        n = C.c_int64(0)
+        check(lib.hyb_function_serialize(self._h, prim, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.uint8)
+        check(lib.hyb_function_serialize(self._h, prim, out.ctypes.data_as(C.POINTER(C.c_uint8)), out.size,
+                                         C.byref(n)))
+        return out.tobytes()
+
+    def deserialize(self, prim: int, record: bytes) -> None:
+        """Inverse of serialize (DataCallbacks::deserialize); the record's
+        levels, sizes and flags must match this function."""
+        buf = np.frombuffer(bytes(record), dtype=np.uint8).copy()
+        check(lib.hyb_function_deserialize(self._h, prim, buf.ctypes.data_as(C.POINTER(C.c_uint8)), buf.size))
+
     def flags(self, level: int, global_order: bool = True) -> np.ndarray:
         n = self._n(level, global_order)
         out = np.zeros(n, dtype=np.uint8)

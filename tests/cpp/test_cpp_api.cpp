@@ -75,6 +75,11 @@ int main() {
     EXPECT(fr.converged && fr.residuals.back() <= 1e-8 * fr.residuals.front());
     const SolveReport pr = mj.pcg(f, u, level, 20);
     EXPECT(pr.residuals.size() == 21 && pr.residuals.back() <= 1e-9 * pr.residuals.front());
+    // checkpoint record of a face (DataCallbacks::serialize) round-trips into a fresh function
+    ScalarFunction w("w", sq, 1, level);
+    const std::uint64_t face = 9 + 2 - 1; // unit square: 4 vertices, 5 edges, 2 faces
+    w.deserialize(face, u.serialize(face));
+    EXPECT(w.serialize(face) == u.serialize(face));
     std::printf("cpp api ok: %d cycles, residual %.3e, error %.3e; fmg %d cycles, pcg %.1e\n", rep.iterations,
                 rep.residuals.back(), err, fr.iterations, pr.residuals.back() / pr.residuals.front());
     return 0;
