@@ -75,11 +75,13 @@ int main() {
     EXPECT(fr.converged && fr.residuals.back() <= 1e-8 * fr.residuals.front());
     const SolveReport pr = mj.pcg(f, u, level, 20);
     EXPECT(pr.residuals.size() == 21 && pr.residuals.back() <= 1e-9 * pr.residuals.front());
-    // checkpoint record of a face (DataCallbacks::serialize) round-trips into a fresh function
+    // checkpoint records (DataCallbacks::serialize) of every primitive round-trip into a fresh
+    // function. Records hold the state after a ghost refresh, so the comparison is made once every
+    // owner has been restored (unit square: 4 vertices, 5 edges, 2 faces)
     ScalarFunction w("w", sq, 1, level);
-    const std::uint64_t face = 9 + 2 - 1; // unit square: 4 vertices, 5 edges, 2 faces
-    w.deserialize(face, u.serialize(face));
-    EXPECT(w.serialize(face) == u.serialize(face));
+    for (std::uint64_t p = 0; p < 11; ++p) w.deserialize(p, u.serialize(p));
+    for (std::uint64_t p = 0; p < 11; ++p) EXPECT(w.serialize(p) == u.serialize(p));
+    EXPECT(w.download(level) == u.download(level));
     std::printf("cpp api ok: %d cycles, residual %.3e, error %.3e; fmg %d cycles, pcg %.1e\n", rep.iterations,
                 rep.residuals.back(), err, fr.iterations, pr.residuals.back() / pr.residuals.front());
     return 0;
