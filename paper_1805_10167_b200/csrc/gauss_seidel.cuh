@@ -53,14 +53,14 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double(*sx)[GS_XS] = s_x[warp];
     double(*sb)[GS_BS] = s_b[warp];
-    const int64_t* __restrict__ ro = t.rowoff;
+    const int W = t.W; // row offsets in closed form: off the staging address chain
     // staged chunk (q, o): row r0-1+q, columns c = t0 - 2r + o - 2 and +1
     // (c even: 16-byte aligned), zero-filled outside the closed triangle
     auto stage = [&](const double* xf, int t0, int r0, int q, int o) {
         const int r = r0 - 1 + q, c = t0 - 2 * r + o - 2;
         const int len = r <= n ? n - r : -1; // last column of row r
         const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
-        cp_async16(&sx[q][o], bytes ? xf + ro[r] + c : xf, bytes);
+        cp_async16(&sx[q][o], bytes ? xf + face_rowoff(W, r) + c : xf, bytes);
     };
     for (;;) {
         int idx = 0;
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
             const int rb = r0 + qb, c = t0 - 2 * rb + o;
             const int len = rb <= n ? n - rb : -1;
             const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
-            cp_async16(&sb[qb][o], bytes ? bf + ro[rb] + c : bf, bytes);
+            cp_async16(&sb[qb][o], bytes ? bf + face_rowoff(W, rb) + c : bf, bytes);
         }
         const int r = r0 + lane; // this lane's row
         // (2) wait for W / S / SW, then stage what they wrote: the W halo
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
         double* xw = x + int64_t(face) * t.face_stride;
         for (int qq = 0; qq < GS_R; ++qq) { // write back row by row (coalesced)
             const int rr = r0 + qq, c = t0 - 2 * rr + lane;
-            if (rr <= n - 2 && c >= 1 && c + rr <= n - 1) __stcg(xw + ro[rr] + c, sx[qq + 1][lane + 2]);
+            if (rr <= n - 2 && c >= 1 && c + rr <= n - 1) __stcg(xw + face_rowoff(W, rr) + c, sx[qq + 1][lane + 2]);
         }
         __syncwarp();
         if (lane == 0) {
@@ -203,12 +203,13 @@ __device__ __forceinline__ double cgs_point_update(const double (&v)[8], const d
 // one warp, one row, one colour: two points per lane per iteration with all
 // loads issued before the stores (points of one colour are independent)
 __device__ __forceinline__ void cgs_row(double* __restrict__ xf, const double* __restrict__ bf,
-                                        const int64_t* __restrict__ ro, int n, int r, int colour, const double (&co)[8],
+                                        int W, int n, int r, int colour, const double (&co)[8],
                                         double rd, int lane) {
-    const double* rm = xf + ro[r - 1];
-    double* r0 = xf + ro[r];
-    const double* rp = xf + ro[r + 1];
-    const double* br = bf + ro[r];
+    const int64_t o = face_rowoff(W, r);
+    const double* rm = xf + face_rowoff(W, r - 1);
+    double* r0 = xf + o;
+    const double* rp = xf + face_rowoff(W, r + 1);
+    const double* br = bf + o;
     int cs = ((colour - 2 * r) % 3 + 3) % 3; // first column of this colour
     if (cs == 0) cs = 3;                      // c = 0 is the border
     const int cmax = n - 1 - r;
@@ -243,20 +244,180 @@ __global__ void __launch_bounds__(CGS_WARPS * 32) k_cgs_faces(LevelTables t, con
     for (int i = 0; i < 8; ++i) co[i] = t.face_coef[size_t(blockIdx.x) * 8 + i];
     const double rd = 1.0 / co[7];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t* __restrict__ ro = t.rowoff;
+    const int W = t.W;
+    auto ro = [W](int r) { return face_rowoff(W, r); };
     for (int j = 1; j - 2 <= last; j += CGS_K) {
         if (threadIdx.x == 0) { // next block's rows into L2 while this one computes
             const int xlo = j + CGS_K + 1, xhi = min(n - 1, j + 2 * CGS_K); // x rows read by the next C0
-            if (xlo <= xhi) prefetch_l2(xf + ro[xlo], uint32_t((ro[xhi + 1] - ro[xlo]) * 8) & ~15u);
+            if (xlo <= xhi) prefetch_l2(xf + ro(xlo), uint32_t((ro(xhi + 1) - ro(xlo)) * 8) & ~15u);
             const int blo = j + CGS_K, bhi = min(last, j + 2 * CGS_K - 1);
-            if (blo <= bhi) prefetch_l2(bf + ro[blo], uint32_t((ro[bhi + 1] - ro[blo]) * 8) & ~15u);
+            if (blo <= bhi) prefetch_l2(bf + ro(blo), uint32_t((ro(bhi + 1) - ro(blo)) * 8) & ~15u);
         }
 #pragma unroll 1
         for (int colour = 0; colour < 3; ++colour) {
             const int lo = max(1, j - colour), hi = min(last, j - colour + CGS_K - 1);
-            for (int r = lo + warp; r <= hi; r += CGS_WARPS) cgs_row(xf, bf, t.rowoff, n, r, colour, co, rd, lane);
+            for (int r = lo + warp; r <= hi; r += CGS_WARPS) cgs_row(xf, bf, W, n, r, colour, co, rd, lane);
             __syncthreads();
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Coloured face sweep on shared-memory row rings fed by TMA (faces with
+// n <= 512: configuration 3's level 9 and below; larger faces use
+// k_cgs_faces). One CTA per face: 6K consumer warps (two per row of a step)
+// and one producer warp. Step i (j = 1 + iK) updates
+//     C0 on rows [j, j+K),  C1 on rows [j-s, j-s+K),  C2 on rows [j-2s, j-2s+K),  s = K+1.
+// With the skew s = K+1 the three blocks neither read what another writes in
+// the same step (C1's rows j-s-1..j-s+K stay below C0's rows, C2's below
+// C1's), so a step needs ONE consumer barrier, and every update still sees
+// exactly the operands of the three full-face passes (C0 reads old C1/C2, C1
+// new C0 / old C2, C2 new C0/C1): bitwise og_cgs. x rows live in an RX-row
+// ring and b rows in an RB-row ring (slot = row mod R). Producer lanes issue
+// one cp.async.bulk each for the rows first read at step i+D (one mbarrier
+// per step) once the consumers have signalled step i done (a second
+// mbarrier), and write every row that became final (its C2 block is done)
+// back with a bulk shared->global copy: x and b cross HBM exactly once (ncu:
+// 17.35 GB read, 8.62 GB written at config 3 L9). Ring safety: an x slot is
+// reloaded with row q at step i only when its old row q - RX is below both the
+// rows step i+1 reads (>= j + K - 2s - 1) and the rows stored at step i
+// (>= j - 2s), whose bulk reads may still be in flight: RX > DK + 3K + 2;
+// b: RB > DK + 2K + 1. Measured at config 3 L9: 6.9 ms per sweep (k_cgs_faces:
+// 7.7); deeper rings (one CTA per SM) and K = 1 were slower: the per-step
+// chain (wait, smem loads, fp64 chain, barrier) is exposed without a second
+// CTA per SM, and two CTAs cap the ring at ~110 KB.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int K, int D> struct CgtCfg {
+    static constexpr int RX = D * K + 3 * K + 3; // x ring rows
+    static constexpr int RB = D * K + 2 * K + 2; // b ring rows
+    static constexpr int NB = D + 1;             // per-step barrier sets
+    static constexpr int CW = 6 * K;             // consumer warps: two per row of a step
+    static constexpr int THREADS = (CW + 1) * 32; // + one producer warp
+    static size_t smem(int W) { return size_t(RX + RB) * size_t((W + 1) & ~1) * 8 + 16 * NB; }
+};
+
+template <int NT> __device__ __forceinline__ void consumer_sync() { // named barrier 1 over the consumers
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+template <int K, int D, int MINB>
+__global__ void __launch_bounds__(CgtCfg<K, D>::THREADS, MINB) k_cgs_tma(LevelTables t, const double* __restrict__ b,
+                                                                         double* x) {
+    using C = CgtCfg<K, D>;
+    extern __shared__ __align__(16) double cg_ring[];
+    constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = K + 1;
+    const int n = t.n, W = t.W, last = n - 2;
+    const int RS = (W + 1) & ~1; // ring row stride (doubles), a 16-byte multiple
+    double* xring = cg_ring;
+    double* bring = cg_ring + size_t(RX) * RS;
+    uint64_t* full = reinterpret_cast<uint64_t*>(cg_ring + size_t(RX + RB) * RS); // rows of step s landed
+    uint64_t* done = full + NB;                                                    // consumers finished step s
+    const int64_t base = int64_t(blockIdx.x) * t.face_stride;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nsteps = (last + 2 * S - 1) / K + 1; // steps while j - 2S <= last
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NB; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&done[i], C::CW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == C::CW) { // producer warp: lanes issue one bulk copy each
+        double* xf = x + base;
+        const double* bf = b + base;
+        // every row first read at step s: x rows (1 + sK, 1 + (s+1)K] (from row 0 at step 0),
+        // b rows [1 + sK, (s+1)K]; lane l takes the l-th of them
+        auto load_step = [&](int s_) {
+            uint64_t* br_ = &full[s_ % NB];
+            const int xlo = s_ == 0 ? 0 : 2 + s_ * K, xhi = min(n - 1, 1 + (s_ + 1) * K);
+            const int blo = 1 + s_ * K, bhi = min(last, (s_ + 1) * K);
+            const int nx = max(0, xhi - xlo + 1), nb = max(0, bhi - blo + 1);
+            uint32_t bytes = 0;
+            int q = -1;
+            bool isx = false;
+            if (lane < nx) q = xlo + lane, isx = true;
+            else if (lane < nx + nb) q = blo + lane - nx;
+            if (q >= 0) bytes = uint32_t((W - q + 1) & ~1) * 8;
+            const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
+            if (lane == 0) mbar_arrive_expect_tx(br_, total); // zero past the last row: completes on arrival
+            if (q >= 0) {
+                if (isx) bulk_g2s(xring + size_t(q % RX) * RS, xf + face_rowoff(W, q), bytes, br_);
+                else bulk_g2s(bring + size_t(q % RB) * RS, bf + face_rowoff(W, q), bytes, br_);
+            }
+        };
+        for (int s_ = 0; s_ < D && s_ < nsteps; ++s_) load_step(s_);
+        for (int i = 0; i < nsteps; ++i) {
+            mbar_wait(&done[i % NB], uint32_t((i / NB) & 1));
+            if (lane == 0) { // rows final after step i (its C2 block) go back to HBM
+                const int j = 1 + i * K;
+                for (int q = max(1, j - 2 * S); q <= min(last, j - 2 * S + K - 1); ++q)
+                    bulk_s2g(xf + face_rowoff(W, q), xring + size_t(q % RX) * RS, uint32_t((W - q + 1) & ~1) * 8);
+                bulk_commit();
+                bulk_wait_read1(); // earlier steps' stores have left their slots
+            }
+            __syncwarp();
+            if (i + D < nsteps) load_step(i + D);
+        }
+        if (lane == 0) bulk_wait_all();
+        return;
+    }
+    double co[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) co[i] = __ldg(t.face_coef + size_t(blockIdx.x) * 8 + i);
+    const double rd = 1.0 / co[7];
+    const int h = warp >> 1; // row of the step: block h / K, row h % K in it
+    const int colour = h / K, roff = h % K;
+    const int u0 = ((warp & 1) << 5) + lane; // colour points u0, u0 + 64, u0 + 128, ...
+    // this warp's row r = j - S colour + roff moves up K rows per step; ring slots and
+    // the colour's first-column residue follow incrementally
+    int r = 1 - S * colour + roff;
+    auto wrap = [](int v, int m) { return ((v % m) + m) % m; };
+    int sxm = wrap(r - 1, RX), sx0 = wrap(r, RX), sxp = wrap(r + 1, RX), sb = wrap(r, RB);
+    int t3 = wrap(colour - 2 * r, 3);
+    constexpr int DT3 = (3 - (2 * K) % 3) % 3; // (colour - 2(r + K)) - (colour - 2r) mod 3
+#pragma unroll 1
+    for (int i = 0; i < nsteps; ++i) {
+        mbar_wait(&full[i % NB], uint32_t((i / NB) & 1));
+        if (r >= 1 && r <= last) {
+            const double* rm = xring + sxm * RS;
+            double* r0 = xring + sx0 * RS;
+            const double* rp = xring + sxp * RS;
+            const double* br = bring + sb * RS;
+            const int cmax = n - 1 - r;
+#pragma unroll 1
+            for (int c = (t3 == 0 ? 3 : t3) + 3 * u0; c <= cmax; c += 384) {
+                const int c2 = c + 192;
+                double v[8], w[8];
+                v[0] = r0[c - 1], v[1] = rp[c - 1], v[2] = rm[c], v[3] = r0[c];
+                v[4] = rp[c], v[5] = rm[c + 1], v[6] = r0[c + 1], v[7] = br[c];
+                const bool two = c2 <= cmax;
+                if (two) {
+                    w[0] = r0[c2 - 1], w[1] = rp[c2 - 1], w[2] = rm[c2], w[3] = r0[c2];
+                    w[4] = rp[c2], w[5] = rm[c2 + 1], w[6] = r0[c2 + 1], w[7] = br[c2];
+                }
+                r0[c] = cgs_point_update(v, co, rd);
+                if (two) r0[c2] = cgs_point_update(w, co, rd);
+            }
+            fence_proxy_async_smem(); // generic-proxy writes -> the producer's bulk store
+        }
+        consumer_sync<C::CW * 32>(); // step i+1 reads what step i wrote
+        if (lane == 0) mbar_arrive(&done[i % NB]);
+        r += K;
+        sxm = sxm + K >= RX ? sxm + K - RX : sxm + K;
+        sx0 = sx0 + K >= RX ? sx0 + K - RX : sx0 + K;
+        sxp = sxp + K >= RX ? sxp + K - RX : sxp + K;
+        sb = sb + K >= RB ? sb + K - RB : sb + K;
+        t3 = t3 + DT3 >= 3 ? t3 + DT3 - 3 : t3 + DT3;
     }
 }
 

@@ -631,9 +631,19 @@ void launch_gs_faces(const LevelTables& t, const double* b, double* x, const int
     check_launch("gauss-seidel faces");
 }
 
+template <int K, int D, int MINB>
+void launch_cgs_tma(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
+    using C = CgtCfg<K, D>;
+    static const bool attr = cudaFuncSetAttribute(k_cgs_tma<K, D, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  int(C::smem(513))) == cudaSuccess;
+    if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
+    k_cgs_tma<K, D, MINB><<<unsigned(t.nfaces), C::THREADS, C::smem(t.W), st>>>(t, b, x);
+}
+
 void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
     if (t.nfaces <= 0 || t.n < 4) return; // n = 3: no interior face DoF
-    k_cgs_faces<8><<<unsigned(t.nfaces), CGS_WARPS * 32, 0, st>>>(t, b, x);
+    if (t.n <= 512) launch_cgs_tma<2, 3, 2>(t, b, x, st); // the shared-memory row ring (config 3: L9)
+    else k_cgs_faces<8><<<unsigned(t.nfaces), CGS_WARPS * 32, 0, st>>>(t, b, x);
     check_launch("coloured gauss-seidel faces");
 }
 

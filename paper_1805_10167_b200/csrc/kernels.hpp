@@ -46,6 +46,22 @@ struct LevelTables {
     int64_t owned_local = 0;
 };
 
+/// rowoff[r] in closed form (plan_layout, csrc/plan.cpp): sum over i < r of
+/// round_up(W - i, 4) = F(W) - F(W - r) with F(x) = sum_{m=1..x} round_up(m, 4)
+/// = x(x+1)/2 + 6 floor(x/4) + {0, 3, 5, 6}[x mod 4]. Kernels whose row
+/// addresses sit on a dependency chain use it instead of a table load.
+__host__ __device__ __forceinline__ int64_t padded_prefix(int64_t x) {
+    return x * (x + 1) / 2 + 6 * (x >> 2) + ((0x6530 >> (4 * (x & 3))) & 0xf);
+}
+__host__ __device__ __forceinline__ int64_t face_rowoff(int W, int r) {
+    return padded_prefix(W) - padded_prefix(int64_t(W) - r);
+}
+/// rowoff as an indexable value: `ro[r]` without a memory load
+struct RowOff {
+    int W;
+    __host__ __device__ __forceinline__ int64_t operator[](int r) const { return face_rowoff(W, r); }
+};
+
 /// Per-function flags of the owned line / vertex DoFs (face interiors are
 /// always INNER, reference src/field.cpp:20-33).
 struct FlagTables {
