@@ -1,5 +1,5 @@
 """Config-2 hot kernels once each (after one warm-up round): apply, residual,
-Jacobi, restrict, prolongate-add, fused residual+restrict at level 10 on channel(16,16) -- the command
+Jacobi, restrict, prolongate-add, fused residual+restrict, fused prolongate-add+Jacobi at level 10 on channel(16,16) -- the command
 profiled with `ncu --set full` (one launch per kernel after -s skips)."""
 import os
 import sys
@@ -24,5 +24,6 @@ for _ in range(2):  # round 0 warms up, round 1 is profiled
     H.restrict_to_coarse(ctl, y, b, L - 1)
     H.prolongate_add(ctl, b, x, L - 1, H.SMOOTH_MASK)
     H.residual_restrict(A, ctl, b, x, y, c, L - 1)
+    H.prolongate_add_jacobi(A, ctl, c, b, x, 2.0 / 3.0, L - 1)
 dom.synchronize()
 print("done")

@@ -1,0 +1,27 @@
+#!/bin/bash
+# One GPU-box pass that produces a round's profile set under gpurun_out/$1:
+# the bench line (and the reference arm), the bench's ncu launch list, one
+# `ncu --set full` capture of the config-2 hot kernels and of the config-3
+# coloured sweep, the other configurations' timings and the GPU test log.
+# Each ncu command runs after the same program has exited 0 without ncu.
+set -u
+out=gpurun_out/${1:-prof}
+mkdir -p "$out"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$out/smi.txt" 2>&1
+timeout 1200 python -m pytest tests -m gpu -q > "$out/pytest_gpu.log" 2>&1; echo "pytest_exit=$?" >> "$out/pytest_gpu.log"
+timeout 900 python bench.py > "$out/bench.json" 2> "$out/bench.err"; echo "bench_exit=$?" >> "$out/bench.err"
+timeout 900 python bench.py --impl reference > "$out/bench_ref.json" 2> "$out/bench_ref.err"
+timeout 900 python tools/configs_time.py > "$out/configs_time.jsonl" 2> "$out/configs_time.err"
+if timeout 600 python bench.py --steps 2 --warmup 1 > "$out/bench_short.json" 2>&1; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+    --log-file "$out/bench_launches.csv" python bench.py --steps 2 --warmup 1 > "$out/ncu_launches.log" 2>&1
+fi
+if timeout 300 python tools/kernels_once.py 10 > "$out/kernels_once.log" 2>&1; then
+  timeout 1200 ncu --set full --import-source on --clock-control none -o "$out/kernels_L10" \
+    python tools/kernels_once.py 10 > "$out/ncu_kernels.log" 2>&1
+fi
+if timeout 300 python tools/smoother_time.py cgs 9 1 > "$out/cgs_once.log" 2>&1; then
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_cgs -s 1 -c 1 -o "$out/cgs_L9" \
+    python tools/smoother_time.py cgs 9 1 > "$out/ncu_cgs.log" 2>&1
+fi
+echo done > "$out/DONE"
