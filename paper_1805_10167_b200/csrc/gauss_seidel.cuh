@@ -264,8 +264,8 @@ __global__ void __launch_bounds__(CGS_WARPS * 32) k_cgs_faces(LevelTables t, con
 
 // ---------------------------------------------------------------------------
 // Coloured face sweep on shared-memory row rings fed by TMA (faces with
-// n <= 512: configuration 3's level 9 and below; larger faces use
-// k_cgs_faces). One CTA per face: 6K consumer warps (two per row of a step)
+// n = 512: configuration 3's level 9; other sizes use k_cgs_faces, see
+// launch_cgs_faces). One CTA per face: 6K consumer warps (two per row of a step)
 // and one producer warp. Step i (j = 1 + iK) updates
 //     C0 on rows [j, j+K),  C1 on rows [j-s, j-s+K),  C2 on rows [j-2s, j-2s+K),  s = K+1.
 // With the skew s = K+1 the three blocks neither read what another writes in

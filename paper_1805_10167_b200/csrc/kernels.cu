@@ -642,7 +642,10 @@ void launch_cgs_tma(const LevelTables& t, const double* b, double* x, cudaStream
 
 void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
     if (t.nfaces <= 0 || t.n < 4) return; // n = 3: no interior face DoF
-    if (t.n <= 512) launch_cgs_tma<2, 3, 2>(t, b, x, st); // the shared-memory row ring (config 3: L9)
+    // the shared-memory row ring runs one step per ~0.95 us per CTA (two per SM): it wins only
+    // where a face has enough rows per step to keep HBM busy -- n = 512 (config 3's L9: 6.9 vs
+    // 7.8 ms); at n = 256 it loses (3.3 vs 2.3 ms), and above 512 its ring does not fit
+    if (t.n == 512) launch_cgs_tma<2, 3, 2>(t, b, x, st);
     else k_cgs_faces<8><<<unsigned(t.nfaces), CGS_WARPS * 32, 0, st>>>(t, b, x);
     check_launch("coloured gauss-seidel faces");
 }

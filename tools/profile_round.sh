@@ -21,7 +21,19 @@ if timeout 300 python tools/kernels_once.py 10 > "$out/kernels_once.log" 2>&1; t
     python tools/kernels_once.py 10 > "$out/ncu_kernels.log" 2>&1
 fi
 if timeout 300 python tools/smoother_time.py cgs 9 1 > "$out/cgs_once.log" 2>&1; then
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_cgs -s 1 -c 1 -o "$out/cgs_L9" \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_cgs_tma -s 1 -c 1 -o "$out/cgs_L9" \
     python tools/smoother_time.py cgs 9 1 > "$out/ncu_cgs.log" 2>&1
 fi
+# the reports stay on the box; their tables come back (gpurun copies <= 64 MiB)
+for rep in "$out"/*.ncu-rep; do
+  [ -f "$rep" ] || continue
+  base="${rep%.ncu-rep}"
+  python tools/ncu_table.py "$rep" "$base.csv" --note "$(basename "$rep")" > /dev/null 2>&1
+  ncu -i "$rep" --page raw --csv > "$base.raw.csv" 2> /dev/null
+  ncu -i "$rep" --page source --csv --print-source sass > "$base.sass.csv" 2> /dev/null
+  python tools/sass_hot.py "$base.sass.csv" 40 > "$base.sass_hot.txt" 2> /dev/null
+  rm -f "$base.sass.csv"
+  [ "$(stat -c %s "$rep")" -lt 20000000 ] || rm -f "$rep"
+done
+du -sh "$out" > "$out/du.txt"
 echo done > "$out/DONE"
