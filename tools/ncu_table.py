@@ -59,15 +59,16 @@ def main():
     tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit.get("gpu__time_duration.sum"), 1.0)
     bscale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     rs, ws = bscale.get(unit.get("dram__bytes_read.sum"), 1.0), bscale.get(unit.get("dram__bytes_write.sum"), 1.0)
-    with open(a.out, "w") as fh:
+    with open(a.out, "w", newline="") as fh:
         if a.note:
             fh.write(f"# {a.note}\n")
-        fh.write("kernel,grid,us,dram_read_GB,dram_write_GB,dram_GB_per_s,registers\n")
+        w = csv.writer(fh)
+        w.writerow(["kernel", "grid", "us", "dram_read_GB", "dram_write_GB", "dram_GB_per_s", "registers"])
         for t in sorted(table, key=lambda t: -t["us"] * tscale):
             us = t["us"] * tscale
             rd, wr = t["dram_read"] * rs, t["dram_write"] * ws
-            fh.write(f"{t['kernel']},({t['grid']}),{us:.1f},{rd / 1e9:.4f},{wr / 1e9:.4f},"
-                     f"{(rd + wr) / (us * 1e3) if us else 0:.0f},{t['registers']}\n")
+            w.writerow([t["kernel"], f"({t['grid']})", f"{us:.1f}", f"{rd / 1e9:.4f}", f"{wr / 1e9:.4f}",
+                        f"{(rd + wr) / (us * 1e3) if us else 0:.0f}", t["registers"]])
     if a.traffic is not None:
         L = a.traffic
         path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
