@@ -203,13 +203,12 @@ __device__ __forceinline__ double cgs_point_update(const double (&v)[8], const d
 // one warp, one row, one colour: two points per lane per iteration with all
 // loads issued before the stores (points of one colour are independent)
 __device__ __forceinline__ void cgs_row(double* __restrict__ xf, const double* __restrict__ bf,
-                                        int W, int n, int r, int colour, const double (&co)[8],
-                                        double rd, int lane) {
-    const int64_t o = face_rowoff(W, r);
-    const double* rm = xf + face_rowoff(W, r - 1);
-    double* r0 = xf + o;
-    const double* rp = xf + face_rowoff(W, r + 1);
-    const double* br = bf + o;
+                                        const int64_t* __restrict__ ro, int n, int r, int colour,
+                                        const double (&co)[8], double rd, int lane) {
+    const double* rm = xf + ro[r - 1];
+    double* r0 = xf + ro[r];
+    const double* rp = xf + ro[r + 1];
+    const double* br = bf + ro[r];
     int cs = ((colour - 2 * r) % 3 + 3) % 3; // first column of this colour
     if (cs == 0) cs = 3;                      // c = 0 is the border
     const int cmax = n - 1 - r;
@@ -244,19 +243,18 @@ __global__ void __launch_bounds__(CGS_WARPS * 32) k_cgs_faces(LevelTables t, con
     for (int i = 0; i < 8; ++i) co[i] = t.face_coef[size_t(blockIdx.x) * 8 + i];
     const double rd = 1.0 / co[7];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int W = t.W;
-    auto ro = [W](int r) { return face_rowoff(W, r); };
+    const int64_t* __restrict__ ro = t.rowoff;
     for (int j = 1; j - 2 <= last; j += CGS_K) {
         if (threadIdx.x == 0) { // next block's rows into L2 while this one computes
             const int xlo = j + CGS_K + 1, xhi = min(n - 1, j + 2 * CGS_K); // x rows read by the next C0
-            if (xlo <= xhi) prefetch_l2(xf + ro(xlo), uint32_t((ro(xhi + 1) - ro(xlo)) * 8) & ~15u);
+            if (xlo <= xhi) prefetch_l2(xf + ro[xlo], uint32_t((ro[xhi + 1] - ro[xlo]) * 8) & ~15u);
             const int blo = j + CGS_K, bhi = min(last, j + 2 * CGS_K - 1);
-            if (blo <= bhi) prefetch_l2(bf + ro(blo), uint32_t((ro(bhi + 1) - ro(blo)) * 8) & ~15u);
+            if (blo <= bhi) prefetch_l2(bf + ro[blo], uint32_t((ro[bhi + 1] - ro[blo]) * 8) & ~15u);
         }
 #pragma unroll 1
         for (int colour = 0; colour < 3; ++colour) {
             const int lo = max(1, j - colour), hi = min(last, j - colour + CGS_K - 1);
-            for (int r = lo + warp; r <= hi; r += CGS_WARPS) cgs_row(xf, bf, W, n, r, colour, co, rd, lane);
+            for (int r = lo + warp; r <= hi; r += CGS_WARPS) cgs_row(xf, bf, t.rowoff, n, r, colour, co, rd, lane);
             __syncthreads();
         }
     }

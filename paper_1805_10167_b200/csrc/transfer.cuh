@@ -36,8 +36,8 @@ __global__ void __launch_bounds__(TR_WARPS * 32) k_prolongate_faces(LevelTables 
     if (cw > nc - 1 - r_lo || r_lo >= r_hi) return; // warp-uniform: no fine output here
     const double* cv = xc + int64_t(blockIdx.z) * tc.face_stride;
     double* fv = xf + int64_t(blockIdx.z) * tf.face_stride;
-    const RowOff cro{tc.W};
-    const RowOff fro{tf.W};
+    const int64_t* __restrict__ cro = tc.rowoff;
+    const int64_t* __restrict__ fro = tf.rowoff;
     const int fc = 2 * c;
     // coarse value at (col, row) if it exists in the closed triangle, else 0
     auto cload = [&](int col, int row) { return col + row <= nc ? __ldg(cv + cro[row] + col) : 0.0; };
@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(TR_WARPS * 32) k_restrict_faces(LevelTables tc
     if (r_lo >= r_hi) return; // warp-uniform
     const double* fv = xf + int64_t(blockIdx.z) * tf.face_stride;
     double* cv = xc + int64_t(blockIdx.z) * tc.face_stride;
-    const RowOff cro{tc.W};
-    const RowOff fro{tf.W};
+    const int64_t* __restrict__ cro = tc.rowoff;
+    const int64_t* __restrict__ fro = tf.rowoff;
     const int fc = 2 * c;
     // raw loads of fine row q: pair (2c, 2c+1); lane 0 also the value at 2c-1
     auto fpair = [&](int q) {
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(128) k_residual_layer(LevelTables t, const dou
     const int q = seg == 0 ? 1 : k;
     const int c = seg == 0 ? k : (seg == 1 ? 1 : n - 1 - k);
     const int64_t base = int64_t(blockIdx.z) * t.face_stride;
-    const RowOff ro{t.W};
+    const int64_t* __restrict__ ro = t.rowoff;
     const double* xm = x + base + ro[q - 1];
     const double* x0 = x + base + ro[q];
     const double* xp = x + base + ro[q + 1];
