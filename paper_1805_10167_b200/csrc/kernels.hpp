@@ -59,12 +59,6 @@ __host__ __device__ __forceinline__ int64_t padded_prefix(int64_t x) {
 __host__ __device__ __forceinline__ int64_t face_rowoff(int W, int r) {
     return padded_prefix(W) - padded_prefix(int64_t(W) - r);
 }
-/// rowoff as an indexable value: `ro[r]` without a memory load
-struct RowOff {
-    int W;
-    __host__ __device__ __forceinline__ int64_t operator[](int r) const { return face_rowoff(W, r); }
-};
-
 /// Per-function flags of the owned line / vertex DoFs (face interiors are
 /// always INNER, reference src/field.cpp:20-33).
 struct FlagTables {
