@@ -62,22 +62,13 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
         const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
         cp_async16(&sx[q][o], bytes ? xf + face_rowoff(W, r) + c : xf, bytes);
     };
-    for (;;) {
-        int idx = 0;
-        if (lane == 0) idx = atomicAdd(counter, 1);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= ntiles) break;
-        const int4 tl = tiles[idx];
-        // has: bits 0/1/2 = the W (I-1, J), S (I, J-1), SW (I-1, J-1) tiles hold points;
-        // a point's dependencies (t-1, t-2 in rows r, r-1) lie in exactly those
-        const int face = tl.x, ti = tl.y, tj = tl.z, has = tl.w;
-        int* fflags = flags + int64_t(face) * ni * nj;
-        const int t0 = ti * GS_T, r0 = 1 + tj * GS_R;
-        const double* xf = x + int64_t(face) * t.face_stride;
-        const double* bf = b + int64_t(face) * t.face_stride;
-        // (1) before the predecessors are done: everything they do not write --
-        // the tile's own rows and the north row from t0 on (own points, E and N
-        // halo: old values), and the tile's b
+    // (1) before the predecessors are done: everything they do not write -- the
+    // tile's own rows and the north row from t0 on (own points, E and N halo:
+    // old values), and the tile's b
+    auto phase1 = [&](const int4 tl) {
+        const int t0 = tl.y * GS_T, r0 = 1 + tl.z * GS_R;
+        const double* xf = x + int64_t(tl.x) * t.face_stride;
+        const double* bf = b + int64_t(tl.x) * t.face_stride;
         for (int e = lane; e < (GS_R + 1) * (GS_K / 2 - 1); e += 32)
             stage(xf, t0, r0, 1 + e / (GS_K / 2 - 1), 2 + 2 * (e % (GS_K / 2 - 1)));
         for (int e = lane; e < GS_R * (GS_T / 2); e += 32) {
@@ -87,6 +78,29 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
             const int bytes = (c < 0 || c > len) ? 0 : (c + 1 <= len ? 16 : 8);
             cp_async16(&sb[qb][o], bytes ? bf + face_rowoff(W, rb) + c : bf, bytes);
         }
+    };
+    // software pipeline over the warp's tiles: the next tile is dequeued while
+    // this one waits for its predecessors, and its phase (1) copies are issued
+    // between this tile's write-back and the fence that releases it, so their
+    // latency overlaps the fence's. The shared-memory buffer is free by then:
+    // the write-back has read it into registers. Deadlock-free: a dequeued
+    // tile's predecessors were dequeued earlier and are running or done, and
+    // the release of a finished tile never waits on a later one.
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= ntiles) return;
+    int4 tl = tiles[idx];
+    phase1(tl);
+    for (;;) {
+        // has: bits 0/1/2 = the W (I-1, J), S (I, J-1), SW (I-1, J-1) tiles hold points;
+        // a point's dependencies (t-1, t-2 in rows r, r-1) lie in exactly those
+        const int face = tl.x, ti = tl.y, tj = tl.z, has = tl.w;
+        int* fflags = flags + int64_t(face) * ni * nj;
+        const int t0 = ti * GS_T, r0 = 1 + tj * GS_R;
+        const double* xf = x + int64_t(face) * t.face_stride;
+        int nidx = 0;
+        if (lane == 0) nidx = atomicAdd(counter, 1); // the next tile, consumed after this one
         const int r = r0 + lane; // this lane's row
         // (2) wait for W / S / SW, then stage what they wrote: the W halo
         // (chunk o = 0 of the own rows) and the south row
@@ -101,6 +115,8 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
             if (e < GS_R) stage(xf, t0, r0, 1 + e, 0);
             else stage(xf, t0, r0, 0, 2 * (e - GS_R));
         }
+        nidx = __shfl_sync(0xffffffffu, nidx, 0);
+        const int4 tl_next = nidx < ntiles ? tiles[nidx] : make_int4(0, 0, 0, 0);
         cp_async_wait_all();
         __syncwarp();
         const double* co = t.face_coef + size_t(face) * 8;
@@ -141,11 +157,14 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
             const int rr = r0 + qq, c = t0 - 2 * rr + lane;
             if (rr <= n - 2 && c >= 1 && c + rr <= n - 1) __stcg(xw + face_rowoff(W, rr) + c, sx[qq + 1][lane + 2]);
         }
-        __syncwarp();
+        __syncwarp(); // every lane's write-back has read the buffer
+        if (nidx < ntiles) phase1(tl_next);
         if (lane == 0) {
             __threadfence();
             atomicExch(fflags + tj * ni + ti, 1);
         }
+        if (nidx >= ntiles) break;
+        tl = tl_next;
     }
 }
 
