@@ -152,10 +152,17 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const
             s_prev = SE;
         }
         __syncwarp();
-        double* xw = x + int64_t(face) * t.face_stride;
-        for (int qq = 0; qq < GS_R; ++qq) { // write back row by row (coalesced)
-            const int rr = r0 + qq, c = t0 - 2 * rr + lane;
-            if (rr <= n - 2 && c >= 1 && c + rr <= n - 1) __stcg(xw + face_rowoff(W, rr) + c, sx[qq + 1][lane + 2]);
+        if (r <= n - 2) { // write back this lane's row: 16-byte pairs (the first column t0 - 2r is even)
+            double* xw = x + int64_t(face) * t.face_stride + face_rowoff(W, r);
+            const int cb = t0 - 2 * r, cmax = n - 1 - r;
+#pragma unroll
+            for (int kk = 0; kk < GS_T; kk += 2) {
+                const int c = cb + kk;
+                const bool v0 = c >= 1 && c <= cmax, v1 = c + 1 >= 1 && c + 1 <= cmax;
+                if (v0 && v1) __stcg(reinterpret_cast<double2*>(xw + c), make_double2(sx[q][kk + 2], sx[q][kk + 3]));
+                else if (v0) __stcg(xw + c, sx[q][kk + 2]);
+                else if (v1) __stcg(xw + c + 1, sx[q][kk + 3]);
+            }
         }
         __syncwarp(); // every lane's write-back has read the buffer
         if (nidx < ntiles) phase1(tl_next);
