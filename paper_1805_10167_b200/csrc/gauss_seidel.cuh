@@ -288,9 +288,10 @@ __global__ void __launch_bounds__(CGS_WARPS * 32) k_cgs_faces(LevelTables t, con
 
 // ---------------------------------------------------------------------------
 // Coloured face sweep on shared-memory row rings fed by TMA (faces with
-// n = 512: configuration 3's level 9; other sizes use k_cgs_faces, see
-// launch_cgs_faces). One CTA per face: 6K consumer warps (two per row of a step)
-// and one producer warp. Step i (j = 1 + iK) updates
+// n = 256 and 512: configuration 3's levels 8 and 9; other sizes use
+// k_cgs_faces, see launch_cgs_faces). One CTA per face: 3K * WPR consumer
+// warps (WPR per row of a step; one measured fastest) and one producer warp.
+// Step i (j = 1 + iK) updates
 //     C0 on rows [j, j+K),  C1 on rows [j-s, j-s+K),  C2 on rows [j-2s, j-2s+K),  s = K+1.
 // With the skew s = K+1 the three blocks neither read what another writes in
 // the same step (C1's rows j-s-1..j-s+K stay below C0's rows, C2's below
@@ -306,10 +307,11 @@ __global__ void __launch_bounds__(CGS_WARPS * 32) k_cgs_faces(LevelTables t, con
 // reloaded with row q at step i only when its old row q - RX is below both the
 // rows step i+1 reads (>= j + K - 2s - 1) and the rows stored at step i
 // (>= j - 2s), whose bulk reads may still be in flight: RX > DK + 3K + 2;
-// b: RB > DK + 2K + 1. Measured at config 3 L9: 6.9 ms per sweep (k_cgs_faces:
-// 7.7); deeper rings (one CTA per SM) and K = 1 were slower: the per-step
-// chain (wait, smem loads, fp64 chain, barrier) is exposed without a second
-// CTA per SM, and two CTAs cap the ring at ~110 KB.
+// b: RB > DK + 2K + 1. Measured at config 3: 6.35 ms per sweep at L9
+// (k_cgs_faces: 7.8), 1.90 at L8 (2.31); deeper rings (one CTA per SM) and
+// K = 1 were slower: the per-step chain (wait, smem loads, fp64 chain,
+// barrier) is exposed without a second CTA per SM, and two CTAs cap the ring
+// at ~110 KB at L9.
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
                  "r"(bytes)
@@ -320,11 +322,11 @@ __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-template <int K, int D> struct CgtCfg {
+template <int K, int D, int WPR = 2> struct CgtCfg {
     static constexpr int RX = D * K + 3 * K + 3; // x ring rows
     static constexpr int RB = D * K + 2 * K + 2; // b ring rows
     static constexpr int NB = D + 1;             // per-step barrier sets
-    static constexpr int CW = 6 * K;             // consumer warps: two per row of a step
+    static constexpr int CW = 3 * K * WPR;       // consumer warps: WPR per row of a step
     static constexpr int THREADS = (CW + 1) * 32; // + one producer warp
     static size_t smem(int W) { return size_t(RX + RB) * size_t((W + 1) & ~1) * 8 + 16 * NB; }
 };
@@ -333,10 +335,10 @@ template <int NT> __device__ __forceinline__ void consumer_sync() { // named bar
     asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
-template <int K, int D, int MINB>
-__global__ void __launch_bounds__(CgtCfg<K, D>::THREADS, MINB) k_cgs_tma(LevelTables t, const double* __restrict__ b,
+template <int K, int D, int MINB, int WPR>
+__global__ void __launch_bounds__(CgtCfg<K, D, WPR>::THREADS, MINB) k_cgs_tma(LevelTables t, const double* __restrict__ b,
                                                                          double* x) {
-    using C = CgtCfg<K, D>;
+    using C = CgtCfg<K, D, WPR>;
     extern __shared__ __align__(16) double cg_ring[];
     constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = K + 1;
     const int n = t.n, W = t.W, last = n - 2;
@@ -399,9 +401,9 @@ __global__ void __launch_bounds__(CgtCfg<K, D>::THREADS, MINB) k_cgs_tma(LevelTa
 #pragma unroll
     for (int i = 0; i < 8; ++i) co[i] = __ldg(t.face_coef + size_t(blockIdx.x) * 8 + i);
     const double rd = 1.0 / co[7];
-    const int h = warp >> 1; // row of the step: block h / K, row h % K in it
+    const int h = warp / WPR; // row of the step: block h / K, row h % K in it
     const int colour = h / K, roff = h % K;
-    const int u0 = ((warp & 1) << 5) + lane; // colour points u0, u0 + 64, u0 + 128, ...
+    const int u0 = ((warp % WPR) << 5) + lane; // colour points u0, u0 + 32 WPR, ...
     // this warp's row r = j - S colour + roff moves up K rows per step; ring slots and
     // the colour's first-column residue follow incrementally
     int r = 1 - S * colour + roff;
@@ -419,8 +421,8 @@ __global__ void __launch_bounds__(CgtCfg<K, D>::THREADS, MINB) k_cgs_tma(LevelTa
             const double* br = bring + sb * RS;
             const int cmax = n - 1 - r;
 #pragma unroll 1
-            for (int c = (t3 == 0 ? 3 : t3) + 3 * u0; c <= cmax; c += 384) {
-                const int c2 = c + 192;
+            for (int c = (t3 == 0 ? 3 : t3) + 3 * u0; c <= cmax; c += 192 * WPR) {
+                const int c2 = c + 96 * WPR;
                 double v[8], w[8];
                 v[0] = r0[c - 1], v[1] = rp[c - 1], v[2] = rm[c], v[3] = r0[c];
                 v[4] = rp[c], v[5] = rm[c + 1], v[6] = r0[c + 1], v[7] = br[c];

@@ -631,21 +631,24 @@ void launch_gs_faces(const LevelTables& t, const double* b, double* x, const int
     check_launch("gauss-seidel faces");
 }
 
-template <int K, int D, int MINB>
+template <int K, int D, int MINB, int WPR>
 void launch_cgs_tma(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
-    using C = CgtCfg<K, D>;
-    static const bool attr = cudaFuncSetAttribute(k_cgs_tma<K, D, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    using C = CgtCfg<K, D, WPR>;
+    static const bool attr = cudaFuncSetAttribute(k_cgs_tma<K, D, MINB, WPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(C::smem(513))) == cudaSuccess;
     if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
-    k_cgs_tma<K, D, MINB><<<unsigned(t.nfaces), C::THREADS, C::smem(t.W), st>>>(t, b, x);
+    k_cgs_tma<K, D, MINB, WPR><<<unsigned(t.nfaces), C::THREADS, C::smem(t.W), st>>>(t, b, x);
 }
 
 void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
     if (t.nfaces <= 0 || t.n < 4) return; // n = 3: no interior face DoF
-    // the shared-memory row ring runs one step per ~0.95 us per CTA (two per SM): it wins only
-    // where a face has enough rows per step to keep HBM busy -- n = 512 (config 3's L9: 6.9 vs
-    // 7.8 ms); at n = 256 it loses (3.3 vs 2.3 ms), and above 512 its ring does not fit
-    if (t.n == 512) launch_cgs_tma<2, 3, 2>(t, b, x, st);
+    // the shared-memory row rings (one consumer warp per row of a step) win where a face has
+    // enough rows per step to keep HBM busy. Measured per sweep on config 3's 8192 faces:
+    // n = 512: 6.35 ms (2 CTAs per SM; two warps per row 6.89, k_cgs_faces 7.83);
+    // n = 256: 1.90 ms (4 CTAs per SM; k_cgs_faces 2.31); n = 128: no gain (0.89 vs 0.88);
+    // larger faces do not fit the ring
+    if (t.n == 512) launch_cgs_tma<2, 3, 2, 1>(t, b, x, st);
+    else if (t.n == 256) launch_cgs_tma<2, 3, 4, 1>(t, b, x, st);
     else k_cgs_faces<8><<<unsigned(t.nfaces), CGS_WARPS * 32, 0, st>>>(t, b, x);
     check_launch("coloured gauss-seidel faces");
 }

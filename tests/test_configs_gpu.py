@@ -47,6 +47,28 @@ def test_colored_gs_bitwise_vs_restatement(mesh_name, ranks):
             assert np.array_equal(x.download(level), o.get(1, level)), (mesh_name, ranks, level, sweep)
 
 
+@pytest.mark.parametrize("mesh_name", ["square", "annulus"])
+@pytest.mark.parametrize("ranks", [1, 3])
+def test_colored_gs_bitwise_large_faces(mesh_name, ranks):
+    """Faces of n = 128, 256, 512 (the shared-memory ring kernels of the coloured sweep, see
+    launch_cgs_faces) against the restatement, bitwise, three sweeps each."""
+    mesh = cfg3_mesh(4, 2) if mesh_name == "annulus" else FIXTURES[mesh_name]()
+    for level in (7, 8, 9):
+        dom = H.DistributedDomain(mesh, ranks)
+        ctl = H.Controller(dom)
+        A = H.StencilOperator(dom, H.LAPLACE, level, level)
+        rhs, x = H.ScalarFunction("rhs", dom, level, level), H.ScalarFunction("x", dom, level, level)
+        o = O.Session(mesh, level, level, 2)
+        for f, i, seed in ((rhs, 0, 61), (x, 1, 62)):
+            v = keyed_uniform(mesh, level, seed)
+            f.upload(level, v)
+            o.set(i, level, v)
+        for sweep in range(3):
+            H.smooth_colored_gs(A, ctl, rhs, x, level)
+            o.cgs(0, 1, level)
+            assert np.array_equal(x.download(level), o.get(1, level)), (mesh_name, ranks, level, sweep)
+
+
 def test_cfg3_reduced_vcycle_history():
     """Config 3 shape at reduced size: perturbed annulus(32, 8) levels 5 -> 0,
     V(3,3) coloured GS, rhs U[-1,1] (seed 2) on INNER, x0 = 0, 5 cycles."""
