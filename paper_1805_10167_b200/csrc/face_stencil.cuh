@@ -26,9 +26,12 @@ constexpr int FS_XW = FS_COLS + 4;           // staged x columns [c0-2, c0+FS_CO
 constexpr int FS_COLS_RR = FS_CWARPS * 62;   // 248
 constexpr int FS_XW_RR = FS_COLS_RR + 8;     // [c0-4, c0+252)
 constexpr int FS_BW_RR = FS_COLS_RR + 4;     // [c0-2, c0+250)
-// rows per band: long bands amortise the 2 halo rows at fine levels, short
-// ones give coarse levels enough CTAs (the row march is latency-bound there)
-__host__ __device__ __forceinline__ int fs_band(int n) { return n >= 1024 ? 64 : (n >= 512 ? 32 : (n >= 128 ? 16 : 8)); }
+// rows per band: long bands amortise the 2 halo rows and the ring's fill at
+// fine levels, short ones give coarse levels enough CTAs (the row march is
+// latency-bound there). Measured Jacobi sweeps on config 3's 8192 faces with
+// 32 -> 64 rows: L9 4.67 -> 4.58 ms, L8 (16 -> 64) 1.73 -> 1.51 ms; 128 rows
+// at L9 was slower on config 2's 512 faces (0.293 -> 0.309 ms)
+__host__ __device__ __forceinline__ int fs_band(int n) { return n >= 256 ? 64 : (n >= 128 ? 32 : (n >= 64 ? 16 : 8)); }
 
 // Correctly rounded a / d from y = RN(1/d) (Markstein: q = RN(a y),
 // r = a - d q exactly by FMA, RN(q + r y) = RN(a / d) barring
