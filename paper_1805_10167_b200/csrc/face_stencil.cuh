@@ -73,9 +73,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
-// ST_JACOBI_PROLONG also stages coarse rows R, R+1 of each fine row q (R = q/2),
-// coarse columns [c0/2 - 2, c0/2 + FS_CW - 2)
+// ST_JACOBI_PROLONG also stages coarse rows (columns [c0/2 - 2, c0/2 + FS_CW - 2))
+// into a ring of FS_NCR rows, each once: fine row q reads coarse rows q/2 and
+// q/2 + 1, so the stage of an even q brings q/2 + 1 and the first stage both.
+// A coarse row R is last read at fine row 2R + 1; its slot is refilled (with
+// R + FS_NCR, at fine row 2R + 2 FS_NCR - 2) once the consumers have freed the
+// stage NS back. They free a stage before reading its coarse rows, so only
+// the stages before that one are certainly done: 2 FS_NCR >= NS + 4.
 constexpr int FS_CW = FS_COLS / 2 + 4;
+constexpr int FS_NCR = 4;
+static_assert(2 * FS_NCR >= 4 + 4, "coarse ring too short for the 4-stage fused mode");
 
 // ring depth (the fused prolongation mode, with coarse rows staged too, needs
 // ~50 KB: it uses dynamic shared memory)
@@ -85,7 +92,7 @@ template <int MODE> struct FaceSmem {
     static constexpr int NS = fs_stages<MODE>();
     double x[NS][MODE == ST_RESTRICT_RESIDUAL ? FS_XW_RR : FS_XW];
     double b[MODE == ST_APPLY ? 1 : NS][MODE == ST_RESTRICT_RESIDUAL ? FS_BW_RR : FS_COLS];
-    double cr[MODE == ST_JACOBI_PROLONG ? NS : 1][2][MODE == ST_JACOBI_PROLONG ? FS_CW : 2];
+    double cr[MODE == ST_JACOBI_PROLONG ? FS_NCR : 1][MODE == ST_JACOBI_PROLONG ? FS_CW : 2];
     uint64_t full[NS];
     uint64_t empty[NS];
 };
@@ -180,11 +187,11 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                 }
                 uint32_t bc[2] = {0u, 0u};
                 int cs0[2] = {0, 0};
-                if (JP) { // coarse rows R, R+1 (closed rows nc+1-R long, padded to 4)
+                if (JP) { // new coarse rows of this stage (closed rows nc+1-R long, padded to 4)
                     const int nc = n / 2, C0 = c0 / 2;
                     for (int h = 0; h < 2; ++h) {
                         const int R = (q >> 1) + h;
-                        if (R > nc) continue;
+                        if (R > nc || (i > 0 && (h == 0 || (q & 1)))) continue;
                         const int plc = (nc + 1 - R + 3) & ~3;
                         cs0[h] = C0 - 2 < 0 ? 0 : C0 - 2;
                         const int ce = C0 - 2 + FS_CW < plc ? C0 - 2 + FS_CW : plc;
@@ -199,8 +206,8 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                     const double* cf = xc + int64_t(face) * cstride;
                     for (int h = 0; h < 2; ++h)
                         if (bc[h])
-                            bulk_g2s(&sm.cr[s][h][cs0[h] - (c0 / 2 - 2)], cf + cro[(q >> 1) + h] + cs0[h], bc[h],
-                                     &sm.full[s]);
+                            bulk_g2s(&sm.cr[((q >> 1) + h) % FS_NCR][cs0[h] - (c0 / 2 - 2)],
+                                     cf + cro[(q >> 1) + h] + cs0[h], bc[h], &sm.full[s]);
                 }
             }
         }
@@ -242,8 +249,8 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         if (JP) { // x row q = r_lo-1+i at columns c-1 .. c+2: add P e at points >= 2 away from the border
             const int q = r_lo - 1 + i;
             // staged coarse columns C-1, C, C+1 (C = c/2) of rows R (index 0) and R+1 (1)
-            const double* c0r = sm.cr[s][0] + tid + 1;
-            const double* c1r = sm.cr[s][1] + tid + 1;
+            const double* c0r = sm.cr[(q >> 1) % FS_NCR] + tid + 1;
+            const double* c1r = sm.cr[((q >> 1) + 1) % FS_NCR] + tid + 1;
             const double l0 = c0r[0], a0 = c0r[1], r0 = c0r[2];
             const double l1 = c1r[0], a1 = c1r[1], r1 = c1r[2];
             double vl, v0, v1, vr; // prolongation at columns c-1, c, c+1, c+2 (k_prolongate_faces' formulas)
