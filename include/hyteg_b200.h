@@ -174,6 +174,14 @@ int hyb_interpolate_const(hyb_function* f, double value, int level, uint8_t mask
 /* device counter-based U[lo,hi] keyed on (seed, stream, DoF identity) */
 int hyb_interpolate_random(hyb_function* f, int level, uint64_t seed, uint64_t stream, double lo, double hi,
                            uint8_t mask);
+/* interpolate(f, expr, level, mask) (function.hpp:55-56) for analytic expressions, evaluated on the
+ * device at the reference's DoF coordinates (src/layout.cpp:239-282):
+ *   HYB_EXPR_POLY2   p0 + p1 x + p2 y + p3 x^2 + p4 x y + p5 y^2 (left to right)
+ *   HYB_EXPR_SINSIN  p0 sin(p1 x + p2) sin(p3 y + p4) + p5
+ * nparams 0..8 (missing parameters are 0); an unknown kind is HYB_INVALID_ARGUMENT */
+#define HYB_EXPR_POLY2 0
+#define HYB_EXPR_SINSIN 1
+int hyb_interpolate_expr(hyb_function* f, int level, int kind, const double* params, int nparams, uint8_t mask);
 /* sync / sync_all (function.hpp:79-81): full schedule V->E, E->F, F->E, E->V */
 int hyb_sync(hyb_function* f, int level);
 

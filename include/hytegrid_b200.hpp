@@ -202,6 +202,21 @@ inline void interpolate(ScalarFunction& f, const std::function<double(double, do
     for (size_t i = 0; i < v.size(); ++i) v[i] = expr(xy[2 * i], xy[2 * i + 1]);
     f.upload(level, v, mask);
 }
+/// an analytic expression evaluated on the device at the reference's DoF coordinates (no host round trip)
+struct Expr {
+    int kind = HYB_EXPR_POLY2;
+    std::vector<double> params;
+    static Expr poly2(double p0, double px, double py, double pxx = 0, double pxy = 0, double pyy = 0) {
+        return {HYB_EXPR_POLY2, {p0, px, py, pxx, pxy, pyy}};
+    }
+    /// a sin(kx x + phx) sin(ky y + phy) + c
+    static Expr sinsin(double a, double kx, double phx, double ky, double phy, double c = 0) {
+        return {HYB_EXPR_SINSIN, {a, kx, phx, ky, phy, c}};
+    }
+};
+inline void interpolate(ScalarFunction& f, const Expr& e, int level, std::uint8_t mask = ALL_DOF_FLAGS) {
+    check(hyb_interpolate_expr(f.handle(), level, e.kind, e.params.data(), int(e.params.size()), mask));
+}
 inline void sync_all(Controller&, const ScalarFunction& f, int level) { check(hyb_sync(f.handle(), level)); }
 inline void apply(const StencilOperator& A, Controller&, const ScalarFunction& src, ScalarFunction& dst, int level,
                   std::uint8_t mask = ALL_DOF_FLAGS) {

@@ -102,6 +102,7 @@ _SIGS = {
     "hyb_function_deserialize": (_i, [_p, _u64, _pu8, _i64]),
     "hyb_interpolate_const": (_i, [_p, _d, _i, _u8]),
     "hyb_interpolate_random": (_i, [_p, _i, _u64, _u64, _d, _d, _u8]),
+    "hyb_interpolate_expr": (_i, [_p, _i, _i, _p, _i, _u8]),
     "hyb_sync": (_i, [_p, _i]),
     "hyb_operator_create": (_i, [_p, _i, _i, _i, _pi32, _pu8, _i, C.POINTER(_p)]),
     "hyb_operator_destroy": (_i, [_p]),

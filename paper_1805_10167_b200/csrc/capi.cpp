@@ -499,6 +499,18 @@ int hyb_interpolate_random(hyb_function* f, int level, uint64_t seed, uint64_t s
     });
 }
 
+int hyb_interpolate_expr(hyb_function* f, int level, int kind, const double* params, int nparams, uint8_t mask) {
+    return guarded([&] {
+        need(f, "hyb_interpolate_expr");
+        if (nparams < 0 || nparams > 8 || (nparams > 0 && !params))
+            throw hyb::InvalidArgument("hyb_interpolate_expr: 0..8 parameters");
+        hyb::Expr e;
+        e.kind = kind;
+        for (int i = 0; i < nparams; ++i) e.p[i] = params[i];
+        hyb::fill_expr(*f->f, level, e, mask);
+    });
+}
+
 int hyb_sync(hyb_function* f, int level) {
     return guarded([&] {
         need(f, "hyb_sync");

@@ -286,6 +286,26 @@ double* Domain::staging(int64_t doubles) {
     return staging_.as<double>();
 }
 
+const double* Domain::geometry() {
+    if (!geo_.bytes()) {
+        const MacroGraph& g = g_;
+        std::vector<double> h;
+        for (uint64_t id : place_.faces) { // reference src/layout.cpp:271 (o, u, v)
+            const MacroFace& f = g.faces[g.face_index(id)];
+            const Vec2 o = f.coord[0], u = f.coord[1] - f.coord[0], v = f.coord[2] - f.coord[0];
+            h.insert(h.end(), {o.x, o.y, u.x, u.y, v.x, v.y});
+        }
+        for (uint64_t id : place_.edges) {
+            const MacroEdge& e = g.edges[g.edge_index(id)];
+            h.insert(h.end(), {e.coord[0].x, e.coord[0].y, e.coord[1].x, e.coord[1].y});
+        }
+        for (uint64_t id : place_.verts) h.insert(h.end(), {g.vertices[id].coord.x, g.vertices[id].coord.y});
+        if (h.empty()) h.push_back(0.0);
+        geo_ = upload_vec(h, stream_);
+    }
+    return geo_.as<double>();
+}
+
 double* Domain::partials(int64_t doubles) {
     if (int64_t(partials_.bytes() / 8) < doubles) {
         HYB_CUDA(cudaStreamSynchronize(stream_));

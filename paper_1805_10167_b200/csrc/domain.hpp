@@ -173,6 +173,8 @@ class Domain {
     const void* recv_buffer() const { return recvbuf_.as<void>(); }
     double* staging(int64_t doubles);
     double* partials(int64_t doubles);
+    /// local primitive geometry for device interpolation (launch_expr layout), built on first use
+    const double* geometry();
     double* scalar_out() { return scalars_.as<double>(); }
 
     // in-process all-reduce of a per-primitive vector (sum) across processes
@@ -240,6 +242,7 @@ class Domain {
     int device_;
     cudaStream_t stream_ = nullptr;
     Placement place_;
+    DevMem geo_;
     std::map<int, std::unique_ptr<LevelGeom>> levels_;
     std::map<int, DevMem> jacobi_;
     DevMem staging_, partials_, scalars_, sendbuf_, recvbuf_;
@@ -275,6 +278,7 @@ void assign(double alpha, Function& x1, double beta, Function& x2, Function& dst
 void add_scaled(Function& dst, double gamma, Function& y, int level, uint8_t mask);
 void fill_const(Function& f, double value, int level, uint8_t mask);
 void fill_random(Function& f, int level, uint64_t seed, uint64_t stream, double lo, double hi, uint8_t mask);
+void fill_expr(Function& f, int level, const Expr& e, uint8_t mask);
 /// PCG update: x += alpha p, r -= alpha ap, returns r.r (bitwise the unfused ops)
 double pcg_update(Function& x, Function& p, Function& r, Function& ap, double alpha, int level);
 double dot(Function& a, Function& b, int level);

@@ -801,6 +801,67 @@ void launch_random(const LevelTables& t, const FlagTables& fl, uint64_t seed, ui
     }
 }
 
+// ---------------------------------------------------------------------------
+// Device interpolation of an analytic expression at the reference's DoF
+// coordinates: faces p = (o + (c/n) u) + (r/n) v, edges a + (k/n)(b - a),
+// vertices their coordinate -- the same operations as the reference's
+// for_each_owned_coord (src/layout.cpp:239-282), so the coordinates are
+// bitwise the reference's (and hyb_owned_coords').
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double expr_eval(const Expr& e, double x, double y) {
+    if (e.kind == EXPR_SINSIN) return e.p[0] * sin(e.p[1] * x + e.p[2]) * sin(e.p[3] * y + e.p[4]) + e.p[5];
+    return ((((e.p[0] + e.p[1] * x) + e.p[2] * y) + e.p[3] * (x * x)) + e.p[4] * (x * y)) + e.p[5] * (y * y);
+}
+
+__global__ void __launch_bounds__(128) k_expr_faces(LevelTables t, const double* __restrict__ geo, Expr e,
+                                                    double* dst) {
+    const int n = t.n;
+    const int col = 1 + blockIdx.x * 128 + threadIdx.x;
+    const double* g = geo + size_t(blockIdx.z) * 6;
+    const double ox = g[0], oy = g[1], ux = g[2], uy = g[3], vx = g[4], vy = g[5];
+    double* fv = dst + int64_t(blockIdx.z) * t.face_stride;
+    const int r0 = 1 + blockIdx.y * FR_RB;
+    for (int row = r0; row < r0 + FR_RB && row <= n - 2; ++row) {
+        if (col > n - 1 - row) break;
+        const double s = double(col) / n, q = double(row) / n;
+        fv[t.rowoff[row] + col] = expr_eval(e, (ox + s * ux) + q * vx, (oy + s * uy) + q * vy);
+    }
+}
+
+__global__ void __launch_bounds__(128) k_expr_ev(LevelTables t, FlagTables fl, const double* __restrict__ geo, Expr e,
+                                                 double* dst, uint8_t mask, int kblocks) {
+    const int n = t.n;
+    const int eblocks = t.nedges * kblocks;
+    const double* ge = geo + size_t(t.nfaces) * 6;
+    if (int(blockIdx.x) < eblocks) {
+        const int ei = blockIdx.x / kblocks;
+        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+        if (k > n - 1 || !(fl.edge_flag[ei] & mask)) return;
+        const double* g = ge + size_t(ei) * 4;
+        const double s = double(k) / n;
+        dst[t.edge_off[ei] + k] = expr_eval(e, g[0] + s * (g[2] - g[0]), g[1] + s * (g[3] - g[1]));
+        return;
+    }
+    const int v = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+    if (v >= t.nverts || !(fl.vtx_flag[v] & mask)) return;
+    const double* g = ge + size_t(t.nedges) * 4 + size_t(v) * 2;
+    dst[t.vtx_off[v]] = expr_eval(e, g[0], g[1]);
+}
+
+void launch_expr(const LevelTables& t, const FlagTables& fl, const double* geo, const Expr& e, double* dst,
+                 uint8_t mask, cudaStream_t st) {
+    if ((mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
+        k_expr_faces<<<face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st>>>(t, geo, e, dst);
+        check_launch("expression faces");
+    }
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    if (blocks > 0) {
+        k_expr_ev<<<blocks, 128, 0, st>>>(t, fl, geo, e, dst, mask, kb);
+        check_launch("expression edges/vertices");
+    }
+}
+
 void launch_scatter_owned(const LevelTables& t, const FlagTables& fl, const double* packed, double* arena,
                           uint8_t mask, cudaStream_t st) {
     if (t.nfaces > 0 && t.n >= 3) {

@@ -138,6 +138,19 @@ void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, 
 void launch_blas1(int op, const LevelTables& t, const FlagTables& fl, double alpha, const double* x1, double beta,
                   const double* x2, double* dst, uint8_t mask, cudaStream_t st);
 // counter-based U[lo,hi] keyed on (seed, stream, canonical DoF key)
+/// analytic expression evaluated at the reference's DoF coordinates
+/// (reference interpolate, src/function.cpp:170-190, over for_each_owned_coord,
+/// src/layout.cpp:239-282), kind EXPR_POLY2: p0 + p1 x + p2 y + p3 x^2 + p4 x y +
+/// p5 y^2 (left to right); EXPR_SINSIN: p0 sin(p1 x + p2) sin(p3 y + p4) + p5
+enum ExprKind : int { EXPR_POLY2 = 0, EXPR_SINSIN = 1 };
+struct Expr {
+    int kind = EXPR_POLY2;
+    double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+/// geo: local faces (o, u = c1 - c0, v = c2 - c0: 6 doubles), then local edges
+/// (a, b: 4), then local vertices (2)
+void launch_expr(const LevelTables& t, const FlagTables& fl, const double* geo, const Expr& e, double* dst,
+                 uint8_t mask, cudaStream_t st);
 void launch_random(const LevelTables& t, const FlagTables& fl, uint64_t seed, uint64_t stream, double lo, double hi,
                    double* dst, uint8_t mask, cudaStream_t st);
 // packed owned order <-> arena (local primitives); mask only for scatter

@@ -349,6 +349,14 @@ void fill_random(Function& f, int level, uint64_t seed, uint64_t stream, double 
     launch_random(d.level(level).t, f.flags(), seed, stream, lo, hi, f.data(level), mask, d.stream());
 }
 
+void fill_expr(Function& f, int level, const Expr& e, uint8_t mask) {
+    f.check_level(level, "interpolate");
+    if (e.kind != EXPR_POLY2 && e.kind != EXPR_SINSIN)
+        throw InvalidArgument("interpolate: unknown expression kind " + std::to_string(e.kind));
+    Domain& d = f.domain();
+    launch_expr(d.level(level).t, f.flags(), d.geometry(), e, f.data(level), mask, d.stream());
+}
+
 namespace {
 double reduce(int op, Function& a, Function& b, int level) {
     Domain& d = a.domain();

@@ -37,6 +37,10 @@ MASS = 1
 
 SMOOTHERS = {"jacobi": 0, "gs": 1, "colored_gs": 2}
 
+# analytic expressions for interpolate_expr (evaluated on the device)
+EXPR_POLY2 = 0   # p0 + p1 x + p2 y + p3 x^2 + p4 x y + p5 y^2
+EXPR_SINSIN = 1  # p0 sin(p1 x + p2) sin(p3 y + p4) + p5
+
 
 def _pd(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
@@ -360,6 +364,15 @@ def interpolate(f: ScalarFunction, expr, level: int, flag_mask: int = ALL_DOF_FL
         f.upload(level, vals, global_order=False, mask=flag_mask)
     else:
         check(lib.hyb_interpolate_const(f._h, float(expr), level, flag_mask))
+
+
+def interpolate_expr(f: ScalarFunction, level: int, kind: int, params, flag_mask: int = ALL_DOF_FLAGS) -> None:
+    """Owned DoFs with flag in mask := an analytic expression (EXPR_POLY2 / EXPR_SINSIN) of the
+    reference's DoF coordinates, evaluated on the device: no host coordinates, no upload, so it
+    works at sizes the host cannot hold (configuration 4's rhs at level 11 is 137 GB)."""
+    p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).ravel())
+    check(lib.hyb_interpolate_expr(f._h, level, int(kind), p.ctypes.data if p.size else None, int(p.size),
+                                   flag_mask))
 
 
 def interpolate_random(f: ScalarFunction, level: int, seed: int, stream: int = 0, lo: float = -1.0, hi: float = 1.0,

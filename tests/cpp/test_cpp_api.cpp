@@ -52,6 +52,10 @@ int main() {
     ScalarFunction rhs("rhs", sq, 1, level), x("x", sq, 1, level);
     interpolate(rhs, [](double a, double b) { return 1.5 + 2.0 * a - 0.75 * b; }, level,
                 flag_bit(DoFFlag::DIRICHLET));
+    // the same boundary data from a device-evaluated expression: bitwise the host callable's
+    ScalarFunction rhs2("rhs2", sq, 1, level);
+    interpolate(rhs2, Expr::poly2(1.5, 2.0, -0.75), level, flag_bit(DoFFlag::DIRICHLET));
+    EXPECT(rhs2.download(level) == rhs.download(level));
     const SolveReport rep = mg.solve(rhs, x, level, 1e-12, 60);
     EXPECT(rep.converged);
     const auto xs = x.download(level);
