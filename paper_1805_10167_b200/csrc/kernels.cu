@@ -591,12 +591,16 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
 void launch_ghost_gather(const void* dst, const void* src, bool idx32, int64_t nlocal, int64_t ntotal, double* arena,
                          const double* recv, cudaStream_t st) {
     if (ntotal <= 0) return;
+    // one thread per ghost: every index and owner load is in flight at once (with a capped
+    // grid-stride loop, config 3's 25 M ghosts at level 9 left each thread a chain of ~40
+    // dependent round trips)
+    const int blocks = grid_for(ntotal, 256, 1 << 30);
     if (idx32)
-        k_ghost_gather<int32_t><<<grid_for(ntotal), 256, 0, st>>>(static_cast<const int32_t*>(dst),
+        k_ghost_gather<int32_t><<<blocks, 256, 0, st>>>(static_cast<const int32_t*>(dst),
                                                                    static_cast<const int32_t*>(src), nlocal, ntotal,
                                                                    arena, recv);
     else
-        k_ghost_gather<int64_t><<<grid_for(ntotal), 256, 0, st>>>(static_cast<const int64_t*>(dst),
+        k_ghost_gather<int64_t><<<blocks, 256, 0, st>>>(static_cast<const int64_t*>(dst),
                                                                    static_cast<const int64_t*>(src), nlocal, ntotal,
                                                                    arena, recv);
     check_launch("ghost gather");
