@@ -393,7 +393,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--level", type=int, default=LEVEL)
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--vcycles", type=int, default=3)
     ap.add_argument("--vcycle-min-level", type=int, default=0)
