@@ -102,13 +102,31 @@ template <int MODE> struct FaceSmem {
 // 2R-1 .. 2R+1 are computed as residuals and restricted on the fly (see
 // k_residual_restrict_faces in transfer.cuh for why only face-interior fine
 // points are involved); nothing fine is stored.
+// Trailing CTAs (blockIdx.z >= nfaces) run the operator's edge/vertex rows
+// (ev_stencil_block), so APPLY / RESIDUAL / JACOBI are one launch: the small
+// edge/vertex work fills the face kernel's tail instead of a launch of its own.
+struct EvTail {
+    FlagTables fl;
+    uint8_t mask = 0;
+    int kblocks = 0, blocks = 0;
+};
+
 template <int MODE, bool DOT = false>
 __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, const double* __restrict__ x,
                                                                  const double* __restrict__ b,
                                                                  double* __restrict__ y, double omega,
                                                                  const int64_t* __restrict__ cro, int64_t cstride,
                                                                  double* __restrict__ dotp,
-                                                                 const double* __restrict__ xc) {
+                                                                 const double* __restrict__ xc, EvTail ev = EvTail{}) {
+    if constexpr (MODE == ST_APPLY || MODE == ST_RESIDUAL || MODE == ST_JACOBI) {
+        if (int(blockIdx.z) >= t.nfaces) { // CTA-uniform: before any barrier
+            const int blk = (int(blockIdx.z - t.nfaces) * int(gridDim.y) + int(blockIdx.y)) * int(gridDim.x) +
+                            int(blockIdx.x);
+            if (blk < ev.blocks && threadIdx.x < 128)
+                ev_stencil_block<MODE>(t, ev.fl, x, b, y, omega, ev.mask, ev.kblocks, blk);
+            return;
+        }
+    }
     constexpr bool RR = MODE == ST_RESTRICT_RESIDUAL;
     constexpr bool JP = MODE == ST_JACOBI_PROLONG; // xc: coarse correction (level L-1, cro, cstride)
     constexpr int XOFF = RR ? 4 : 2;           // smem x index of column c0

@@ -32,22 +32,23 @@ inline void check_launch(const char* what) {
 
 
 // ---------------------------------------------------------------------------
-#include "face_stencil.cuh"
-
 // ---------------------------------------------------------------------------
 // K2/K3: edge line rows and vertex rows, one launch. Flags are per primitive
 // (SURVEY F6): a masked-out primitive is skipped, a DIRICHLET row is the
 // identity (apply), b - x (residual) or kept (Jacobi).
 // ---------------------------------------------------------------------------
+// The body is also run by the face-stencil kernel's trailing CTAs (ev_block:
+// the logical block, 128 threads), so one launch covers a whole operator.
 template <int MODE>
-__global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl, const double* __restrict__ x,
-                                                    const double* __restrict__ b, double* __restrict__ y,
-                                                    double omega, uint8_t mask, int kblocks) {
+__device__ __forceinline__ void ev_stencil_block(const LevelTables& t, const FlagTables& fl,
+                                                 const double* __restrict__ x, const double* __restrict__ b,
+                                                 double* __restrict__ y, double omega, uint8_t mask, int kblocks,
+                                                 int ev_block) {
     const int n = t.n;
     const int eblocks = t.nedges * kblocks;
-    if (int(blockIdx.x) < eblocks) {
-        const int e = blockIdx.x / kblocks;
-        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+    if (ev_block < eblocks) {
+        const int e = ev_block / kblocks;
+        const int k = 1 + (ev_block % kblocks) * 128 + int(threadIdx.x);
         if (k > n - 1) return;
         const uint8_t f = fl.edge_flag[e];
         if (!(f & mask)) return;
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl
         y[off + k] = o;
         return;
     }
-    const int v = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+    const int v = (ev_block - eblocks) * 128 + int(threadIdx.x);
     if (v >= t.nverts) return;
     const uint8_t f = fl.vtx_flag[v];
     if (!(f & mask)) return;
@@ -103,6 +104,15 @@ __global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl
     else if (MODE == ST_JACOBI) o = x[off] + omega * (b[off] - acc) / co[ne + 1];
     y[off] = o;
 }
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl, const double* __restrict__ x,
+                                                    const double* __restrict__ b, double* __restrict__ y,
+                                                    double omega, uint8_t mask, int kblocks) {
+    ev_stencil_block<MODE>(t, fl, x, b, y, omega, mask, kblocks, int(blockIdx.x));
+}
+
+#include "face_stencil.cuh"
 
 // ---------------------------------------------------------------------------
 // K11: ghost refresh. Every ghost slot (face border rows, edge line ends and
@@ -559,26 +569,37 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
         return;
     }
     // faces: interior DoFs are INNER; only present for n >= 3
-    if ((parts & 1) && (mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
-        const dim3 grid = face_stencil_grid(t);
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    const bool faces = (parts & 1) && (mask & F_INNER) && t.nfaces > 0 && t.n >= 3;
+    bool ev_done = false;
+    if (faces) {
+        dim3 grid = face_stencil_grid(t);
+        EvTail ev;
+        if ((parts & 2) && blocks > 0) { // edge/vertex rows as trailing CTAs of the same launch
+            ev.fl = fl;
+            ev.mask = mask;
+            ev.kblocks = kb;
+            ev.blocks = blocks;
+            grid.z += unsigned((blocks + int(grid.x * grid.y) - 1) / int(grid.x * grid.y));
+            ev_done = true;
+        }
         switch (mode) {
         case ST_APPLY:
-            if (dotp) k_face_stencil<ST_APPLY, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp, nullptr);
-            else k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr);
+            if (dotp) k_face_stencil<ST_APPLY, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp, nullptr, ev);
+            else k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
             break;
         case ST_RESIDUAL:
-            k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr);
+            k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
             break;
         default:
-            if (dotp) k_face_stencil<ST_JACOBI, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp, nullptr);
-            else k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr);
+            if (dotp) k_face_stencil<ST_JACOBI, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp, nullptr, ev);
+            else k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
             break;
         }
         check_launch("face stencil");
     }
-    const int kb = kblocks_for(t.n);
-    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
-    if ((parts & 2) && blocks > 0) {
+    if ((parts & 2) && blocks > 0 && !ev_done) {
         switch (mode) {
         case ST_APPLY: k_ev_stencil<ST_APPLY><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb); break;
         case ST_RESIDUAL: k_ev_stencil<ST_RESIDUAL><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb); break;

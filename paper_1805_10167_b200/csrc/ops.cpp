@@ -73,9 +73,8 @@ void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t m
     Domain& d = A.domain();
     d.sync(src, level); // full schedule first (reference src/operators.cpp:390)
     const LevelTables t = A.tables(level);
-    launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, mask, d.stream(), 2);
-    d.timer_begin("apply");
-    launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, mask, d.stream(), 1);
+    d.timer_begin("apply"); // face interiors, then edge/vertex rows as the same launch's trailing CTAs
+    launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, mask, d.stream(), 3);
     d.timer_end();
 }
 
@@ -87,11 +86,9 @@ void residual(const Operator& A, Function& rhs, Function& x, Function& r, int le
     Domain& d = A.domain();
     d.sync(x, level);
     const LevelTables t = A.tables(level);
-    launch_stencil(ST_RESIDUAL, t, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
-                   d.stream(), 2);
     d.timer_begin("residual");
     launch_stencil(ST_RESIDUAL, t, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
-                   d.stream(), 1);
+                   d.stream(), 3);
     d.timer_end();
 }
 
@@ -106,11 +103,9 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
     // pending write-back of the reference (src/operators.cpp:435-468) is a
     // second buffer here: read x, write x', swap.
     const LevelTables t = A.tables(level);
-    launch_stencil(ST_JACOBI, t, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
-                   d.stream(), 2);
     d.timer_begin("jacobi");
     launch_stencil(ST_JACOBI, t, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
-                   d.stream(), 1, dotp);
+                   d.stream(), 3, dotp);
     d.timer_end();
     x.arena(level).swap(next);
 }
@@ -147,11 +142,9 @@ double apply_dot(const Operator& A, Function& src, Function& dst, int level) {
     double* part = buf;
     double* scratch = buf + np;
     HYB_CUDA(cudaMemsetAsync(part, 0, size_t(np) * 8, d.stream()));
-    launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, ALL_FLAGS,
-                   d.stream(), 2);
     d.timer_begin("apply");
     launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, ALL_FLAGS,
-                   d.stream(), 1, scratch);
+                   d.stream(), 3, scratch);
     d.timer_end();
     return finish_dot(d, t, src.data(level), dst.data(level), scratch, slots, part);
 }
