@@ -118,12 +118,14 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                                                                  const int64_t* __restrict__ cro, int64_t cstride,
                                                                  double* __restrict__ dotp,
                                                                  const double* __restrict__ xc, EvTail ev = EvTail{}) {
-    if constexpr (MODE == ST_APPLY || MODE == ST_RESIDUAL || MODE == ST_JACOBI) {
+    if constexpr (MODE == ST_APPLY || MODE == ST_RESIDUAL || MODE == ST_JACOBI || MODE == ST_JACOBI_PROLONG) {
         if (int(blockIdx.z) >= t.nfaces) { // CTA-uniform: before any barrier
             const int blk = (int(blockIdx.z - t.nfaces) * int(gridDim.y) + int(blockIdx.y)) * int(gridDim.x) +
                             int(blockIdx.x);
+            // (the fused correction's edges and vertices were corrected in place: a plain Jacobi row)
+            constexpr int EVM = MODE == ST_JACOBI_PROLONG ? int(ST_JACOBI) : MODE;
             if (blk < ev.blocks && threadIdx.x < 128)
-                ev_stencil_block<MODE>(t, ev.fl, x, b, y, omega, ev.mask, ev.kblocks, blk);
+                ev_stencil_block<EVM>(t, ev.fl, x, b, y, omega, ev.mask, ev.kblocks, blk);
             return;
         }
     }

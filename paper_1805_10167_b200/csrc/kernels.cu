@@ -750,9 +750,25 @@ void launch_prolongate_layer(const LevelTables& tc, const LevelTables& tf, const
 }
 
 void launch_jacobi_prolong_faces(const LevelTables& tc, const LevelTables& tf, const double* x, const double* xc,
-                                 const double* b, double* y, double omega, double* dotp, cudaStream_t st) {
-    if (tf.nfaces <= 0 || tf.n < 3) return;
-    const dim3 grid = face_stencil_grid(tf);
+                                 const double* b, double* y, double omega, double* dotp, cudaStream_t st,
+                                 const FlagTables* ev_flags) {
+    if (tf.nfaces <= 0 || tf.n < 3) {
+        if (ev_flags) launch_stencil(ST_JACOBI, tf, *ev_flags, x, b, y, omega, F_ALL, st, 2);
+        return;
+    }
+    dim3 grid = face_stencil_grid(tf);
+    EvTail ev;
+    if (ev_flags) { // the edge/vertex Jacobi rows as trailing CTAs
+        const int kb = kblocks_for(tf.n);
+        const int blocks = tf.nedges * kb + (tf.nverts + 127) / 128;
+        if (blocks > 0) {
+            ev.fl = *ev_flags;
+            ev.mask = F_ALL;
+            ev.kblocks = kb;
+            ev.blocks = blocks;
+            grid.z += unsigned((blocks + int(grid.x * grid.y) - 1) / int(grid.x * grid.y));
+        }
+    }
     constexpr size_t smem = sizeof(FaceSmem<ST_JACOBI_PROLONG>);
     static const bool attr = cudaFuncSetAttribute(k_face_stencil<ST_JACOBI_PROLONG, true>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) ==
@@ -763,10 +779,10 @@ void launch_jacobi_prolong_faces(const LevelTables& tc, const LevelTables& tf, c
     if (!attr) throw CudaError("jacobi after prolongation: cannot reserve shared memory");
     if (dotp)
         k_face_stencil<ST_JACOBI_PROLONG, true><<<grid, FS_THREADS, smem, st>>>(tf, x, b, y, omega, tc.rowoff,
-                                                                                tc.face_stride, dotp, xc);
+                                                                                tc.face_stride, dotp, xc, ev);
     else
         k_face_stencil<ST_JACOBI_PROLONG><<<grid, FS_THREADS, smem, st>>>(tf, x, b, y, omega, tc.rowoff,
-                                                                          tc.face_stride, nullptr, xc);
+                                                                          tc.face_stride, nullptr, xc, ev);
     check_launch("jacobi after prolongation faces");
 }
 

@@ -119,7 +119,8 @@ void launch_prolongate_layer(const LevelTables& coarse, const LevelTables& fine,
 // holds the correction on the border rows and the layer next to them
 // (ST_JACOBI_PROLONG); dotp as launch_stencil
 void launch_jacobi_prolong_faces(const LevelTables& coarse, const LevelTables& fine, const double* x, const double* xc,
-                                 const double* b, double* y, double omega, double* dotp, cudaStream_t st);
+                                 const double* b, double* y, double omega, double* dotp, cudaStream_t st,
+                                 const FlagTables* ev_flags = nullptr);
 void launch_residual_restrict_faces(const LevelTables& coarse, const LevelTables& fine, const double* x,
                                     const double* b, double* r, double* xc, cudaStream_t st);
 // hybrid Gauss-Seidel: face tiles (face, I, J, dependency bits) over skewed

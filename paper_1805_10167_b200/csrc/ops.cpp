@@ -269,11 +269,10 @@ void prolongate_add_jacobi(const Operator& A, Function& e, Function& rhs, Functi
     launch_prolongate_layer(tc, t, e.data(lc), x.data(level), d.stream());
     d.sync(x, level);
     DevMem& next = d.jacobi_scratch(level);
-    launch_stencil(ST_JACOBI, t, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
-                   d.stream(), 2);
-    d.timer_begin("prolongate_jacobi");
+    d.timer_begin("prolongate_jacobi"); // edge/vertex Jacobi rows as the launch's trailing CTAs
+    const FlagTables fl = x.flags();
     launch_jacobi_prolong_faces(tc, t, x.data(level), e.data(lc), rhs.data(level), next.as<double>(), omega, dotp,
-                                d.stream());
+                                d.stream(), &fl);
     d.timer_end();
     x.arena(level).swap(next);
 }
