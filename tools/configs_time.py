@@ -77,7 +77,7 @@ def cfg4(args):
     H.interpolate_random(noise, L, seed=3, lo=-1e-3, hi=1e-3, flag_mask=H.INNER)
     H.add_scaled(rhs, 1.0, noise, L)
     del noise
-    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, lmin, L, coarse_tol=1e-9)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, lmin, L, coarse_tol=args.cfg4_coarse_tol)
     fine = H.ScalarFunction("b", dom, L, L)
     H.assign(1.0, rhs, 0.0, rhs, fine, L)
     mg.fmg(rhs, x, L, args.cfg4_tol, 3)  # warm: plans, graphs
@@ -111,6 +111,7 @@ ap.add_argument("--configs", default="cfg1,cfg3,cfg4,cfg5")
 ap.add_argument("--cfg3-level", type=int, default=9)
 ap.add_argument("--cfg4-level", type=int, default=9)
 ap.add_argument("--cfg4-tol", type=float, default=1e-7)
+ap.add_argument("--cfg4-coarse-tol", type=float, default=1e-9)
 ap.add_argument("--cfg5-level", type=int, default=11)
 args = ap.parse_args()
 for name in args.configs.split(","):
