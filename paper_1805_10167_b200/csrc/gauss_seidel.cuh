@@ -256,9 +256,8 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <int CGS_K>
-__global__ void __launch_bounds__(CGS_WARPS * 32) k_cgs_faces(LevelTables t, const double* __restrict__ b,
-                                                              double* x) {
+template <int CGS_K, int NW = CGS_WARPS>
+__global__ void __launch_bounds__(NW * 32) k_cgs_faces(LevelTables t, const double* __restrict__ b, double* x) {
     const int n = t.n;
     const int last = n - 2; // interior rows 1..n-2
     const int64_t base = int64_t(blockIdx.x) * t.face_stride;
@@ -280,7 +279,7 @@ __global__ void __launch_bounds__(CGS_WARPS * 32) k_cgs_faces(LevelTables t, con
 #pragma unroll 1
         for (int colour = 0; colour < 3; ++colour) {
             const int lo = max(1, j - colour), hi = min(last, j - colour + CGS_K - 1);
-            for (int r = lo + warp; r <= hi; r += CGS_WARPS) cgs_row(xf, bf, t.rowoff, n, r, colour, co, rd, lane);
+            for (int r = lo + warp; r <= hi; r += NW) cgs_row(xf, bf, t.rowoff, n, r, colour, co, rd, lane);
             __syncthreads();
         }
     }

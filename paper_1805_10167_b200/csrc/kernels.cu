@@ -674,6 +674,9 @@ void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStre
     // larger faces do not fit the ring
     if (t.n == 512) launch_cgs_tma<2, 3, 2, 1>(t, b, x, st);
     else if (t.n == 256) launch_cgs_tma<2, 3, 4, 1>(t, b, x, st);
+    // small faces: two warps per face, 8-row blocks (config 3, 8192 faces: L7 0.88 -> 0.67 ms,
+    // L6 0.42 -> 0.29, L5 0.22 -> 0.15 against 8 warps); faces above 512 keep 8 warps
+    else if (t.n <= 128) k_cgs_faces<8, 2><<<unsigned(t.nfaces), 64, 0, st>>>(t, b, x);
     else k_cgs_faces<8><<<unsigned(t.nfaces), CGS_WARPS * 32, 0, st>>>(t, b, x);
     check_launch("coloured gauss-seidel faces");
 }
