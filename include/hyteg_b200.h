@@ -78,6 +78,14 @@ int hyb_partition(const char* mesh_text, int ranks, int partitioner, int weight_
 int hyb_stencil_host(const char* mesh_text, int form, int level, uint64_t primitive_id, double* out, int cap,
                      int* len);
 
+/* host-only min-level system of GridHierarchy (constrained_matrix,
+ * src/solvers.cpp:358-364: assemble_global_sparse + constrain_dirichlet) as the
+ * device coarse CG holds it: COO rows / columns ascending, GlobalDoFMap order;
+ * *nnz = entries (cap 0: size query) */
+int hyb_coarse_matrix_host(const char* mesh_text, int form, int level, const int32_t* bc_markers,
+                           const uint8_t* bc_flags, int n_bc, int64_t* rows, int64_t* cols, double* vals, int64_t cap,
+                           int64_t* nnz);
+
 /* ---- host-only plans (no device) ------------------------------------------
  * The arena layout and one-round ghost-exchange plan one process derives for
  * `level` (the device runtime uses exactly these), for multi-process checks on

@@ -21,6 +21,7 @@
 #pragma once
 
 #include <cmath>
+#include <cstdio>
 #include <cstdint>
 #include <functional>
 #include <map>
@@ -268,8 +269,27 @@ inline double max_abs(const ScalarFunction& a, int level) {
 
 struct SolveReport {
     bool converged = false;
+    bool breakdown = false;
     int iterations = 0;
     std::vector<double> residuals;
+
+    /// One "cycle <k> residual <norm> factor <reduction>" line per entry, the
+    /// format of the reference's SolveReport::history (src/solvers.cpp:208-224).
+    std::string history() const {
+        std::string out;
+        char line[96];
+        for (std::size_t k = 0; k < residuals.size(); ++k) {
+            if (k == 0) {
+                std::snprintf(line, sizeof line, "cycle %zu residual %.6e\n", k, residuals[k]);
+            } else {
+                const double f = residuals[k - 1] > 0.0 ? residuals[k] / residuals[k - 1] : 0.0;
+                std::snprintf(line, sizeof line, "cycle %zu residual %.6e factor %.4f\n", k, residuals[k], f);
+            }
+            out += line;
+        }
+        if (breakdown) out += "breakdown\n";
+        return out;
+    }
 };
 
 class GridHierarchy {

@@ -72,6 +72,13 @@ struct og_session {
     double** ediag;  /* [lvl][ei] */
     double** vst;    /* [lvl] flat: per vertex 1+ne terms + diag */
     int64_t* vcoff;  /* per vertex offset in vst */
+    /* coarse solve of the cycles: 0 matrix-free CG with sequential dots,
+     * 1 the device's (assembled constrained CSR, its fixed reduction shapes) */
+    int cmode, nsm;
+    int64_t cn;      /* CSR of the min level (cmode 1), built on first use */
+    int32_t *crp, *cci;
+    double* ccv;
+    int cnz_max;
 };
 
 /* ------------------------------------------------------------------ mesh
@@ -443,7 +450,8 @@ void og_destroy(og_session* s) {
         free(s->off[li]); free(s->fst[li]); free(s->est[li]); free(s->ent[li]); free(s->ediag[li]); free(s->vst[li]);
     }
     free(s->val); free(s->off); free(s->asize); free(s->fst); free(s->est); free(s->ent); free(s->ediag);
-    free(s->vst); free(s->vcoff); free(s->V); free(s->E); free(s->F); free(s);
+    free(s->vst); free(s->vcoff); free(s->V); free(s->E); free(s->F);
+    free(s->crp); free(s->cci); free(s->ccv); free(s);
 }
 
 static int check(og_session* s, int f, int level) {
@@ -892,8 +900,279 @@ static int matvec(Cyc* c, const double* v, double* out) {
     return og_get(c->s, c->AP, c->lmin, out);
 }
 
+/* ---------------------------------------------------------- device coarse CG
+ * cmode 1 restates the product's coarse solve so that cycle histories can be
+ * compared bitwise, not to a rounding floor. Matrix: the reference's
+ * constrained min-level matrix (assemble_global_sparse + constrain_dirichlet,
+ * src/operators.cpp:507-546, src/solvers.cpp:322-364): DIRICHLET rows are
+ * identity, DIRICHLET columns dropped, rows in GlobalDoFMap order, columns
+ * ascending (the reference's row maps), duplicate columns summed in term
+ * order from 0. Recurrence: cg_solve's (src/solvers.cpp:226-259) incl. the
+ * true-residual check of finish_report. Only the dot products deviate from the
+ * reference's sequential vec_dot (src/solvers.cpp:36-41): they use the fixed
+ * reduction shapes of the device kernels (paper_1805_10167_b200/csrc/kernels.cu
+ * k_coarse_cg / k_coarse_cg_grid / k_coarse_cg_reg), restated here; none
+ * depends on timing, and only k_coarse_cg_grid's depends on the SM count. */
+void og_coarse_solver(og_session* s, int mode, int nsm) {
+    s->cmode = mode;
+    s->nsm = nsm > 0 ? nsm : 148;
+}
+
+typedef struct { int64_t col; double v; } CEnt;
+static int cent_cmp(const void* a, const void* b) {
+    const int64_t x = ((const CEnt*)a)->col, y = ((const CEnt*)b)->col;
+    return x < y ? -1 : x > y;
+}
+static void cent_add(CEnt* row, int* len, int64_t col, double v) {
+    for (int i = 0; i < *len; ++i)
+        if (row[i].col == col) { row[i].v += v; return; }
+    row[*len].col = col;
+    row[*len].v = 0.0 + v;
+    ++*len;
+}
+
+/* owner index of every slot: the global indices 0..N-1 set on the owned DoFs
+ * of scratch function f and synced (every ghost then holds its owner's) */
+static int build_csr(og_session* s, int f, int L) {
+    const int64_t N = og_owned(s, L);
+    double* gid = malloc(sizeof(double) * (size_t)(N + 1));
+    unsigned char* fl = malloc((size_t)N + 1);
+    for (int64_t i = 0; i < N; ++i) gid[i] = (double)i;
+    og_set(s, f, L, gid);
+    og_sync(s, f, L);
+    og_flags(s, L, fl);
+    s->crp = malloc(sizeof(int32_t) * (size_t)(N + 1));
+    s->cci = malloc(sizeof(int32_t) * (size_t)(16 * N + 1));
+    s->ccv = malloc(sizeof(double) * (size_t)(16 * N + 1));
+    const int li = L - s->lmin, n = 1 << L, W = n + 1;
+    static const int o[7][2] = {{-1, 0}, {-1, 1}, {0, -1}, {0, 0}, {0, 1}, {1, -1}, {1, 0}};
+    int64_t row = 0, nnz = 0;
+    s->crp[0] = 0;
+    s->cnz_max = 0;
+    for (int id = 0; id < s->np; ++id) {
+        const double* xv = prim(s, f, L, id);
+        FOR_ROWS(s, id, L, slot, c, r, {
+            CEnt ent[32];
+            int len = 0;
+            if (fl[row] & F_DIRICHLET) {
+                ent[len].col = row; ent[len].v = 1.0; ++len;
+            } else {
+                CEnt raw[32];
+                int nr = 0;
+                switch (kind_of(s, id)) {
+                case 0: {
+                    const double* st = s->vst[li] + s->vcoff[id];
+                    for (int j = 0; j <= s->V[id].ne; ++j) cent_add(raw, &nr, (int64_t)xv[j], st[j]);
+                    break;
+                }
+                case 1: {
+                    const int ei = id - s->nv;
+                    for (int t = 0; t < s->ent[li][ei]; ++t) {
+                        const ETerm* e = &s->est[li][7 * ei + t];
+                        cent_add(raw, &nr, (int64_t)xv[e->base + slot + e->dk], e->coeff);
+                    }
+                    break;
+                }
+                default: {
+                    const double* st = s->fst[li] + 8 * (id - s->nv - s->ne);
+                    for (int t = 0; t < 7; ++t)
+                        cent_add(raw, &nr, (int64_t)xv[fidx(W, c + o[t][0], r + o[t][1])], st[t]);
+                }
+                }
+                for (int q = 0; q < nr; ++q)
+                    if (!(fl[raw[q].col] & F_DIRICHLET)) ent[len++] = raw[q];
+            }
+            qsort(ent, (size_t)len, sizeof(CEnt), cent_cmp);
+            for (int q = 0; q < len; ++q) { s->cci[nnz] = (int32_t)ent[q].col; s->ccv[nnz] = ent[q].v; ++nnz; }
+            if (len > s->cnz_max) s->cnz_max = len;
+            ++row;
+            s->crp[row] = (int32_t)nnz;
+        });
+    }
+    s->cn = N;
+    free(gid);
+    free(fl);
+    return row == N ? 0 : fail("coarse CSR: row count mismatch");
+}
+
+static void csr_mul(const og_session* s, const double* u, double* out) {
+    for (int64_t i = 0; i < s->cn; ++i) {
+        double acc = 0.0;
+        for (int32_t k = s->crp[i]; k < s->crp[i + 1]; ++k) acc += s->ccv[k] * u[s->cci[k]];
+        out[i] = acc;
+    }
+}
+
+/* __shfl_down_sync tree of one warp (lane 0's value): v[l] += v[l + o], o = 16..1 */
+static double warp_tree(double* v) {
+    for (int o = 16; o > 0; o >>= 1)
+        for (int l = 0; l < o; ++l) v[l] = v[l] + v[l + o];
+    return v[0];
+}
+/* block reduction of `threads` per-thread values (k_coarse_cg's cg_dot with
+ * 1024 threads, block_sum with 512): warp trees, then warp 0's tree over the
+ * warp sums (zero-padded to 32) */
+static double block_tree(const double* per_thread, int threads) {
+    double red[32], w[32];
+    for (int q = 0; q < 32; ++q) red[q] = 0.0;
+    for (int q = 0; q < threads / 32; ++q) {
+        memcpy(w, per_thread + 32 * q, sizeof w);
+        red[q] = warp_tree(w);
+    }
+    return warp_tree(red);
+}
+/* dot of k_coarse_cg: thread t sums i = t, t + 1024, ... */
+static double dot_cta(const double* u, const double* v, int64_t n, double* tmp) {
+    for (int t = 0; t < 1024; ++t) {
+        double a = 0.0;
+        for (int64_t i = t; i < n; i += 1024) a += u[i] * v[i];
+        tmp[t] = a;
+    }
+    return block_tree(tmp, 1024);
+}
+/* grid_dot of k_coarse_cg_grid (nb CTAs of 512): strided per-thread sums,
+ * per-CTA block_sum, then block_sum of the CTA partials (thread t holds part[t]) */
+static double dot_grid(const double* u, const double* v, int64_t n, int nb, double* tmp) {
+    const int64_t stride = (int64_t)nb * 512;
+    double* part = tmp + 512;
+    for (int b = 0; b < nb; ++b) {
+        for (int t = 0; t < 512; ++t) {
+            double a = 0.0;
+            for (int64_t i = (int64_t)b * 512 + t; i < n; i += stride) a += u[i] * v[i];
+            tmp[t] = a;
+        }
+        part[b] = block_tree(tmp, 512);
+    }
+    for (int t = 0; t < 512; ++t) {
+        double a = 0.0;
+        for (int i = t; i < nb; i += 512) a += part[i];
+        tmp[t] = a;
+    }
+    return block_tree(tmp, 512);
+}
+/* grid_sum2's .x of k_coarse_cg_reg for per-row values w (rows >= n are 0):
+ * per-CTA block_sum of its 512 rows, then block_sum of the CTA partials */
+static double sum_reg(const double* w, int64_t n, double* tmp) {
+    const int nb = (int)((n + 511) / 512);
+    double* part = tmp + 512;
+    for (int b = 0; b < nb; ++b) {
+        for (int t = 0; t < 512; ++t) {
+            const int64_t i = (int64_t)b * 512 + t;
+            tmp[t] = i < n ? 0.0 + w[i] : 0.0;
+        }
+        part[b] = block_tree(tmp, 512);
+    }
+    for (int t = 0; t < 512; ++t) tmp[t] = t < nb ? 0.0 + part[t] : 0.0;
+    return block_tree(tmp, 512);
+}
+
+/* cg_solve from x = 0 on the CSR with the device's dots; returns 1 if converged */
+static int cg_device(og_session* s, const double* b, double* x, double tol, int max_iter) {
+    const int64_t n = s->cn;
+    double* w = malloc(sizeof(double) * (size_t)(4 * n + 2048 + (int64_t)s->nsm + 8));
+    double *r = w, *p = r + n, *ap = p + n, *tmp = ap + n;
+    int conv;
+    const int grid = n >= 2048, reg = grid && n <= (int64_t)s->nsm * 512 && s->cnz_max <= 16;
+    if (reg) {
+        /* k_coarse_cg_reg: Chronopoulos-Gear recurrence, two sums per reduction */
+        double* pv = malloc(sizeof(double) * (size_t)(3 * n + 1));
+        double *sv = pv + n, *wv = sv + n;
+        for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; }
+        for (int64_t i = 0; i < n; ++i) ap[i] = b[i] * b[i];
+        const double target = tol * sqrt(sum_reg(ap, n, tmp));
+        csr_mul(s, r, wv);
+        for (int64_t i = 0; i < n; ++i) ap[i] = r[i] * r[i];
+        double gamma = sum_reg(ap, n, tmp);
+        for (int64_t i = 0; i < n; ++i) ap[i] = wv[i] * r[i];
+        double dl = sum_reg(ap, n, tmp);
+        double alpha = dl > 0.0 ? gamma / dl : 0.0;
+        for (int64_t i = 0; i < n; ++i) { pv[i] = r[i]; sv[i] = wv[i]; }
+        int it = 0, breakdown = (dl > 0.0 || gamma == 0.0) ? 0 : 1;
+        while (!breakdown && it < max_iter && sqrt(gamma) > target) {
+            for (int64_t i = 0; i < n; ++i) { x[i] += alpha * pv[i]; r[i] -= alpha * sv[i]; }
+            csr_mul(s, r, wv);
+            for (int64_t i = 0; i < n; ++i) ap[i] = r[i] * r[i];
+            const double gamma_new = sum_reg(ap, n, tmp);
+            for (int64_t i = 0; i < n; ++i) ap[i] = wv[i] * r[i];
+            const double delta = sum_reg(ap, n, tmp);
+            const double beta = gamma_new / gamma;
+            const double denom = delta - beta * gamma_new / alpha;
+            if (!(denom > 0.0)) {
+                if (gamma_new > 0.0) breakdown = 1;
+                gamma = gamma_new;
+                ++it;
+                break;
+            }
+            alpha = gamma_new / denom;
+            for (int64_t i = 0; i < n; ++i) { pv[i] = r[i] + beta * pv[i]; sv[i] = wv[i] + beta * sv[i]; }
+            gamma = gamma_new;
+            ++it;
+        }
+        csr_mul(s, x, ap);
+        for (int64_t i = 0; i < n; ++i) { const double t = b[i] - ap[i]; ap[i] = t * t; }
+        const double res = sqrt(sum_reg(ap, n, tmp));
+        conv = res <= target;
+        free(pv);
+    } else {
+        /* k_coarse_cg (one CTA) / k_coarse_cg_grid: cg_solve's recurrence */
+#define DOTD(u, v) (grid ? dot_grid(u, v, n, s->nsm, tmp) : dot_cta(u, v, n, tmp))
+        for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; p[i] = b[i]; }
+        const double target = tol * sqrt(DOTD(b, b));
+        double rs = DOTD(r, r);
+        int it = 0;
+        while (it < max_iter && sqrt(rs) > target) {
+            csr_mul(s, p, ap);
+            const double pap = DOTD(p, ap);
+            if (pap <= 0.0) break;
+            const double alpha = rs / pap;
+            for (int64_t i = 0; i < n; ++i) { x[i] += alpha * p[i]; r[i] -= alpha * ap[i]; }
+            const double rs_new = DOTD(r, r);
+            const double beta = rs_new / rs;
+            for (int64_t i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
+            rs = rs_new;
+            ++it;
+        }
+        csr_mul(s, x, ap);
+        for (int64_t i = 0; i < n; ++i) ap[i] = b[i] - ap[i];
+        conv = sqrt(DOTD(ap, ap)) <= target;
+#undef DOTD
+    }
+    free(w);
+    return conv;
+}
+
+/* the min-level CSR as COO (size query: cap 0); f is a scratch function */
+int og_coarse_matrix(og_session* s, int f, int64_t* rows, int64_t* cols, double* vals, int64_t cap, int64_t* nnz) {
+    if (check(s, f, s->lmin)) return 1;
+    if (!s->crp && build_csr(s, f, s->lmin)) return 1;
+    int64_t k = 0;
+    for (int64_t i = 0; i < s->cn; ++i)
+        for (int32_t q = s->crp[i]; q < s->crp[i + 1]; ++q, ++k)
+            if (k < cap) { rows[k] = i; cols[k] = s->cci[q]; vals[k] = s->ccv[q]; }
+    *nnz = k;
+    return 0;
+}
+
+static int coarse_device(Cyc* c, int rhs, int x) {
+    og_session* s = c->s;
+    const int L = c->lmin;
+    if (!s->crp && build_csr(s, c->P, L)) return 1;
+    if (og_residual(s, rhs, x, c->R, L)) return 1;
+    const int64_t n = s->cn;
+    double* b = malloc(sizeof(double) * (size_t)(2 * n + 2));
+    double* e = b + n;
+    og_get(s, c->R, L, b);
+    const int ok = cg_device(s, b, e, c->tol, (int)n + 100);
+    if (!ok) { free(b); return fail("vcycle: coarse CG did not converge"); }
+    og_set(s, c->R, L, e);
+    free(b);
+    /* scatter-add on the smooth mask: x += 1.0 * e (k_coarse_scatter_add) */
+    return og_add_scaled(s, x, 1.0, c->R, L, F_INNER | F_NEUMANN);
+}
+
 static int coarse(Cyc* c, int rhs, int x) {
     og_session* s = c->s;
+    if (s->cmode == 1) return coarse_device(c, rhs, x);
     const int L = c->lmin;
     if (og_residual(s, rhs, x, c->R, L)) return 1;
     const int64_t n = og_owned(s, L);

@@ -43,6 +43,12 @@ int og_prolongate(og_session* s, int coarse, int fine, int lc, int mask);
 int og_assign(og_session* s, double alpha, int x1, double beta, int x2, int dst, int level, int mask);
 int og_add_scaled(og_session* s, int dst, double gamma, int y, int level, int mask);
 int og_dot(og_session* s, int a, int b, int level, double* out);
+/* coarse solve of og_vcycle / og_fmg / og_pcg: mode 0 (default) matrix-free
+ * CG with sequential dots; mode 1 the product's: assembled constrained CSR and
+ * the device kernels' fixed reduction shapes (nsm = SM count, 148 on B200) */
+void og_coarse_solver(og_session* s, int mode, int nsm);
+/* that CSR (min level) as COO in row / column order; f = a scratch function */
+int og_coarse_matrix(og_session* s, int f, int64_t* rows, int64_t* cols, double* vals, int64_t cap, int64_t* nnz);
 /* smoother 0 weighted Jacobi (omega), 1 hybrid GS, 2 coloured GS */
 int og_vcycle(og_session* s, int rhs, int x, int level, int smoother, int nu1, int nu2, double omega,
               double coarse_tol, int ncycles, double* residuals);

@@ -56,6 +56,9 @@ def lib():
             "ref_dot": (i, [p, i, i, i, pd]),
             "ref_stencil": (i, [p, u64, i, pd, C.POINTER(C.c_int)]),
             "ref_vcycle_jacobi": (i, [p, i, i, i, i, i, d, d, i, pd]),
+            "ref_diagonal": (i, [p, i, i, i]),
+            "ref_fill_keyed": (i, [p, i, i, u64, u64, d, d]),
+            "ref_coarse_matrix": (i, [p, i, C.POINTER(i64), C.POINTER(i64), pd, i64, C.POINTER(i64)]),
             "ref_gridhierarchy_solve": (i, [p, i, i, i, d, i, i, i, pd, C.POINTER(C.c_int)]),
         }
         for name, (res, args) in sig.items():
@@ -196,6 +199,25 @@ class RefSession:
         _ck(lib().ref_vcycle_jacobi(self.h, rhs, x, level, nu1, nu2, omega, coarse_tol, ncycles,
                                     res.ctypes.data_as(C.POINTER(C.c_double))))
         return res
+
+    def fill_keyed(self, fi, level, seed, stream=0, lo=-1.0, hi=1.0):
+        """keyed U[lo, hi] of the device generator, written in place"""
+        _ck(lib().ref_fill_keyed(self.h, fi, level, seed, stream, lo, hi))
+
+    def diagonal(self, form, d, level):
+        _ck(lib().ref_diagonal(self.h, form, d, level))
+
+    def coarse_matrix(self, level):
+        """GridHierarchy's constrained min-level matrix as COO (rows, cols, vals)."""
+        n = C.c_int64()
+        _ck(lib().ref_coarse_matrix(self.h, level, None, None, None, 0, C.byref(n)))
+        r = np.empty(n.value, dtype=np.int64)
+        c = np.empty(n.value, dtype=np.int64)
+        v = np.empty(n.value)
+        _ck(lib().ref_coarse_matrix(self.h, level, r.ctypes.data_as(C.POINTER(C.c_int64)),
+                                    c.ctypes.data_as(C.POINTER(C.c_int64)), v.ctypes.data_as(C.POINTER(C.c_double)), n.value,
+                                    C.byref(n)))
+        return r, c, v
 
     def gridhierarchy_solve(self, rhs, x, level, tol, max_cycles, nu1=2, nu2=2) -> np.ndarray:
         res = np.zeros(max_cycles + 1)

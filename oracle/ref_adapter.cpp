@@ -395,4 +395,81 @@ int ref_gridhierarchy_solve(void* sp, int rhs, int x, int level, double tol, int
     });
 }
 
+// keyed U[lo, hi] of the device generator (the restatement's og_keyed_uniform)
+// written straight into function fi at `level` (no host vector in GlobalDoFMap
+// order: config 2 at level 10 is 268 M DoFs)
+namespace {
+uint64_t kmix(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+} // namespace
+int ref_fill_keyed(void* sp, int fi, int level, uint64_t seed, uint64_t stream, double lo, double hi) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        ScalarFunction& fn = *s.f.at(size_t(fi));
+        const uint64_t sk = kmix(kmix(seed) ^ (stream * 0xD1B54A32D192ED03ull));
+        const int n = 1 << level;
+        auto u = [&](uint64_t key) { return lo + (hi - lo) * (double(kmix(sk ^ kmix(key)) >> 11) * 0x1p-53); };
+        for (const PrimitiveID id : ids_sorted(*s.dom)) {
+            const Primitive& p = s.dom->primitive(id);
+            auto& vals = fn.values(id, level);
+            const uint64_t base = uint64_t(id.value) << 40;
+            int q = 1, r = 1, c = 1; // for_each_owned order: edges k = 1..n-1; faces r = 1..n-2, c = 1..n-1-r
+            for_each_owned(FunctionKind::P1, p.kind, p.info, level, fn.layout(), [&](std::size_t slot) {
+                if (p.kind == PrimitiveKind::VERTEX) {
+                    vals[slot] = u(base);
+                } else if (p.kind == PrimitiveKind::EDGE) {
+                    vals[slot] = u(base ^ (uint64_t(q) << 20));
+                    ++q;
+                } else {
+                    vals[slot] = u(base ^ (uint64_t(c) << 20) ^ uint64_t(r));
+                    if (++c + r > n - 1) {
+                        c = 1;
+                        ++r;
+                    }
+                }
+            });
+        }
+    });
+}
+
+// diagonal(A, d, level) (include/hytegrid/operators.hpp:125, src/operators.cpp:484-505)
+// of a fresh StencilOperator of `form` (0 LAPLACE, 1 MASS) into function d
+int ref_diagonal(void* sp, int form, int d, int level) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        StencilOperator A(*s.dom, form == 1 ? Form::MASS : Form::LAPLACE, FunctionKind::P1, s.min_level,
+                          s.max_level, s.bc);
+        diagonal(A, *s.f.at(size_t(d)), level);
+    });
+}
+
+// The GridHierarchy coarse matrix (constrained_matrix, src/solvers.cpp:358-364):
+// assemble_global_sparse + constrain_dirichlet at `level`, as COO in row then
+// column order (SparseMatrix row maps); *nnz = entries (size query: cap 0).
+int ref_coarse_matrix(void* sp, int level, int64_t* rows, int64_t* cols, double* vals, int64_t cap, int64_t* nnz) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        GlobalDoFMap map(*s.dom, FunctionKind::P1, level);
+        const std::vector<uint8_t> flags = map.gather_flags(*s.f.at(0));
+        SparseMatrix M = assemble_global_sparse(*s.A, level, map);
+        std::vector<double> zero(M.rows(), 0.0);
+        constrain_dirichlet(M, zero, flags);
+        int64_t k = 0;
+        for (size_t r = 0; r < M.rows(); ++r)
+            for (const auto& [c, v] : M.row(r)) {
+                if (k < cap) {
+                    rows[k] = int64_t(r);
+                    cols[k] = int64_t(c);
+                    vals[k] = v;
+                }
+                ++k;
+            }
+        *nnz = k;
+    });
+}
+
 } // extern "C"

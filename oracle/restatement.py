@@ -48,6 +48,8 @@ def lib():
             "og_add_scaled": (i, [p, i, d, i, i, i]),
             "og_dot": (i, [p, i, i, i, pd]),
             "og_vcycle_jacobi": (i, [p, i, i, i, i, i, d, d, i, pd]),
+            "og_coarse_solver": (None, [p, i, i]),
+            "og_coarse_matrix": (i, [p, i, C.POINTER(i64), C.POINTER(i64), pd, i64, C.POINTER(i64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -144,6 +146,23 @@ class Session:
         res = np.zeros(iters + 1)
         _ck(lib().og_pcg(self.h, rhs, x, level, nu1, nu2, omega, coarse_tol, iters, _pd(res)))
         return res
+
+    def coarse_solver(self, mode, nsm=148):
+        """0: matrix-free CG with sequential dots (default); 1: the product's
+        coarse solve (assembled constrained CSR, the device kernels' reduction
+        shapes; nsm = SM count, which only the largest systems depend on)."""
+        lib().og_coarse_solver(self.h, mode, nsm)
+
+    def coarse_matrix(self, scratch):
+        """the min-level CSR of coarse_solver(1) as COO (rows, cols, vals)"""
+        n = C.c_int64()
+        _ck(lib().og_coarse_matrix(self.h, scratch, None, None, None, 0, C.byref(n)))
+        r = np.empty(n.value, dtype=np.int64)
+        c = np.empty(n.value, dtype=np.int64)
+        v = np.empty(n.value)
+        _ck(lib().og_coarse_matrix(self.h, scratch, r.ctypes.data_as(C.POINTER(C.c_int64)),
+                                   c.ctypes.data_as(C.POINTER(C.c_int64)), _pd(v), n.value, C.byref(n)))
+        return r, c, v
 
     def restrict(self, fine, coarse, lc, mask=7):
         _ck(lib().og_restrict(self.h, fine, coarse, lc, mask))

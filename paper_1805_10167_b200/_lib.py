@@ -73,6 +73,7 @@ _SIGS = {
     "hyb_mesh_counts": (_i, [_cs, _pi64, _pi64, _pi64]),
     "hyb_partition": (_i, [_cs, _i, _i, _i, _pi32]),
     "hyb_stencil_host": (_i, [_cs, _i, _i, _u64, _pd, _i, C.POINTER(_i)]),
+    "hyb_coarse_matrix_host": (_i, [_cs, _i, _i, _pi32, C.POINTER(C.c_uint8), _i, _pi64, _pi64, _pd, _i64, _pi64]),
     "hyb_plan_create": (_i, [_cs, _i, _pi32, _pi32, _i, _i, C.POINTER(_p)]),
     "hyb_plan_destroy": (_i, [_p]),
     "hyb_plan_sizes": (_i, [_p, _pi64]),

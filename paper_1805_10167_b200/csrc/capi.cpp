@@ -5,6 +5,7 @@
 #include <string>
 
 #include "../../include/hyteg_b200.h"
+#include "coarse.hpp"
 #include "domain.hpp"
 
 // Objects built on a domain share ownership of it: destroying the domain
@@ -187,6 +188,27 @@ int hyb_stencil_host(const char* mesh_text, int form, int level, uint64_t id, do
         if (len) *len = int(v.size());
         if (cap < int(v.size())) throw hyb::InvalidArgument("hyb_stencil_host: buffer too small");
         for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+    });
+}
+
+int hyb_coarse_matrix_host(const char* mesh_text, int form, int level, const int32_t* bc_markers,
+                           const uint8_t* bc_flags, int n_bc, int64_t* rows, int64_t* cols, double* vals, int64_t cap,
+                           int64_t* nnz) {
+    return guarded([&] {
+        need(mesh_text, "hyb_coarse_matrix_host");
+        need(nnz, "hyb_coarse_matrix_host");
+        if (level < 0 || level > 12) throw hyb::OutOfRange("hyb_coarse_matrix_host: level");
+        const auto g = hyb::build_macro_graph(hyb::parse_mesh_text(mesh_text));
+        const hyb::HostCsr m = hyb::assemble_constrained(g, hyb::Form(form), level, make_bc(bc_markers, bc_flags, n_bc));
+        int64_t k = 0;
+        for (int64_t r = 0; r < m.n; ++r)
+            for (int32_t q = m.rowptr[size_t(r)]; q < m.rowptr[size_t(r) + 1]; ++q, ++k)
+                if (k < cap) {
+                    rows[k] = r;
+                    cols[k] = m.col[size_t(q)];
+                    vals[k] = m.val[size_t(q)];
+                }
+        *nnz = k;
     });
 }
 

@@ -110,6 +110,17 @@ Domain::Domain(const std::string& mesh_text, int world_ranks, const std::vector<
     for (int r : local_ranks_)
         if (r < 0 || r >= world_) throw InvalidArgument("Domain: local rank out of range");
     rank_of_ = assignment;
+    {
+        // face kernels put the process's faces on grid.z (at most 65535)
+        int64_t nf_here = 0;
+        for (size_t i = 0; i < g_.nf(); ++i)
+            if (std::find(local_ranks_.begin(), local_ranks_.end(), rank_of_[size_t(g_.face_id(i))]) !=
+                local_ranks_.end())
+                ++nf_here;
+        if (nf_here > 65535)
+            throw InvalidArgument("Domain: " + std::to_string(nf_here) +
+                                  " macro-faces in one process; at most 65535 (partition over more processes)");
+    }
     HYB_CUDA(cudaSetDevice(device_));
     HYB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     HYB_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));

@@ -576,12 +576,15 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
     if (faces) {
         dim3 grid = face_stencil_grid(t);
         EvTail ev;
-        if ((parts & 2) && blocks > 0) { // edge/vertex rows as trailing CTAs of the same launch
+        const unsigned ev_z = unsigned((blocks + int(grid.x * grid.y) - 1) / int(grid.x * grid.y));
+        // edge/vertex rows as trailing CTAs of the same launch, while grid.z stays
+        // within its 65535 limit (else a separate k_ev_stencil launch below)
+        if ((parts & 2) && blocks > 0 && grid.z + ev_z <= 65535u) {
             ev.fl = fl;
             ev.mask = mask;
             ev.kblocks = kb;
             ev.blocks = blocks;
-            grid.z += unsigned((blocks + int(grid.x * grid.y) - 1) / int(grid.x * grid.y));
+            grid.z += ev_z;
             ev_done = true;
         }
         switch (mode) {
@@ -761,15 +764,19 @@ void launch_jacobi_prolong_faces(const LevelTables& tc, const LevelTables& tf, c
     }
     dim3 grid = face_stencil_grid(tf);
     EvTail ev;
-    if (ev_flags) { // the edge/vertex Jacobi rows as trailing CTAs
+    bool ev_separate = false;
+    if (ev_flags) { // the edge/vertex Jacobi rows as trailing CTAs (grid.z <= 65535, else separately)
         const int kb = kblocks_for(tf.n);
         const int blocks = tf.nedges * kb + (tf.nverts + 127) / 128;
-        if (blocks > 0) {
+        const unsigned ev_z = unsigned((blocks + int(grid.x * grid.y) - 1) / int(grid.x * grid.y));
+        if (blocks > 0 && grid.z + ev_z <= 65535u) {
             ev.fl = *ev_flags;
             ev.mask = F_ALL;
             ev.kblocks = kb;
             ev.blocks = blocks;
-            grid.z += unsigned((blocks + int(grid.x * grid.y) - 1) / int(grid.x * grid.y));
+            grid.z += ev_z;
+        } else if (blocks > 0) {
+            ev_separate = true;
         }
     }
     constexpr size_t smem = sizeof(FaceSmem<ST_JACOBI_PROLONG>);
@@ -787,6 +794,7 @@ void launch_jacobi_prolong_faces(const LevelTables& tc, const LevelTables& tf, c
         k_face_stencil<ST_JACOBI_PROLONG><<<grid, FS_THREADS, smem, st>>>(tf, x, b, y, omega, tc.rowoff,
                                                                           tc.face_stride, nullptr, xc, ev);
     check_launch("jacobi after prolongation faces");
+    if (ev_separate) launch_stencil(ST_JACOBI, tf, *ev_flags, x, b, y, omega, F_ALL, st, 2);
 }
 
 void launch_residual_restrict_faces(const LevelTables& tc, const LevelTables& tf, const double* x, const double* b,

@@ -119,6 +119,21 @@ def stencil_host(mesh_text: str, level: int, primitive_id: int, form: int = 0) -
     return out[: n.value].copy()
 
 
+def coarse_matrix_host(mesh_text: str, level: int, form: int = 0, bc: dict | None = None):
+    """GridHierarchy's constrained min-level matrix exactly as the device coarse
+    CG holds it, as COO (rows, cols, vals); host only."""
+    m, f, nb = _bc_arrays(bc)
+    n = C.c_int64()
+    check(lib.hyb_coarse_matrix_host(mesh_text.encode(), form, level, m, f, nb, None, None, None, 0, C.byref(n)))
+    r = np.empty(n.value, dtype=np.int64)
+    c = np.empty(n.value, dtype=np.int64)
+    v = np.empty(n.value)
+    i64p = C.POINTER(C.c_int64)
+    check(lib.hyb_coarse_matrix_host(mesh_text.encode(), form, level, m, f, nb, r.ctypes.data_as(i64p),
+                                     c.ctypes.data_as(i64p), _pd(v), n.value, C.byref(n)))
+    return r, c, v
+
+
 class ExchangePlan:
     """Host-only view of the layout and one-round ghost-exchange plan that a
     process driving ``local_ranks`` builds for ``level`` (no device needed)."""
@@ -494,12 +509,14 @@ class SolveReport:
 class GridHierarchy:
     """V-cycle multigrid (reference GridHierarchy, solvers.hpp:81-102).
 
-    smoother 'jacobi' with weight omega; coarse level solved on the device by
-    CG to coarse_tol (reference default 1e-12, max_iter #DoFs + 100).
+    smoother 'gs' (default: the reference's hybrid Gauss-Seidel, hardcoded at
+    src/solvers.cpp:417, 427), 'jacobi' with weight omega, or 'colored_gs';
+    coarse level solved on the device by CG to coarse_tol (reference default
+    1e-12, max_iter #DoFs + 100).
     """
 
     def __init__(self, domain: DistributedDomain, ctl: Controller, form: int, min_level: int, max_level: int,  # noqa
-                 bc: dict | None = None, smoother: str = "jacobi", omega: float = 2.0 / 3.0,
+                 bc: dict | None = None, smoother: str = "gs", omega: float = 2.0 / 3.0,
                  coarse_tol: float = 1e-12, coarse_max_iter: int = -1):
         self.domain = domain
         self.min_level = min_level

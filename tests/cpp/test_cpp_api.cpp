@@ -86,6 +86,17 @@ int main() {
     for (std::uint64_t p = 0; p < 11; ++p) w.deserialize(p, u.serialize(p));
     for (std::uint64_t p = 0; p < 11; ++p) EXPECT(w.serialize(p) == u.serialize(p));
     EXPECT(w.download(level) == u.download(level));
+    // SolveReport::history() of the reference GridHierarchy's own cycle (smooth_gs, min level 1) on a
+    // keyed U[-1,1] rhs (seed 5): tests/test_cpp_api.py prints the reference's text for the same solve
+    {
+        DistributedDomain hd(meshgen::unit_square(), 1);
+        Controller hc(hd);
+        GridHierarchy hg(hd, hc, Form::LAPLACE, 1, level);
+        ScalarFunction hr("hr", hd, 1, level), hx("hx", hd, 1, level);
+        EXPECT(hyb_interpolate_random(hr.handle(), level, 5, 0, -1.0, 1.0, HYB_ALL_FLAGS) == HYB_OK);
+        const SolveReport hrep = hg.solve(hr, hx, level, 0.0, 6);
+        std::printf("HISTORY_BEGIN\n%sHISTORY_END\n", hrep.history().c_str());
+    }
     std::printf("cpp api ok: %d cycles, residual %.3e, error %.3e; fmg %d cycles, pcg %.1e\n", rep.iterations,
                 rep.residuals.back(), err, fr.iterations, pr.residuals.back() / pr.residuals.front());
     return 0;

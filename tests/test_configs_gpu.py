@@ -10,8 +10,12 @@ properties.
 config 4 -- full multigrid (og_fmg) and config 5 -- V(1,1)-preconditioned CG
 (og_pcg): neither exists in the reference; both are compositions of the pinned
 primitives (restrict, prolongate, cycle, apply, dot) restated in the C oracle.
-Residual histories within 1e-8 relative at reduced sizes; full-size shares
-through convergence properties."""
+Residual histories within 1e-8 relative per entry at reduced sizes, with no
+absolute floor: the restatement runs the product's coarse solve
+(og_coarse_solver mode 1: the reference's constrained CSR and cg_solve
+recurrence, with the device kernels' fixed dot shapes), so x stays bitwise
+the restatement's through every cycle. Full-size shares through convergence
+properties."""
 import numpy as np
 import pytest
 
@@ -20,6 +24,11 @@ from paper_1805_10167_b200 import hytegrid as H
 from tests.helpers import FIXTURES, keyed_uniform
 
 pytestmark = pytest.mark.gpu
+
+
+def torch_sm_count():
+    import torch
+    return torch.cuda.get_device_properties(0).multi_processor_count
 
 
 def cfg3_mesh(segments=128, layers=32):
@@ -84,6 +93,7 @@ def test_cfg3_reduced_vcycle_history():
     mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="colored_gs", coarse_tol=1e-12)
     rep = mg.solve(rhs, x, L, 0.0, 5, 3, 3)
     o = O.Session(mesh, 0, L, 7)
+    o.coarse_solver(1)
     o.set(0, L, b)
     ref = o.vcycle(0, 1, L, 2, 3, 3, 1.0, 1e-12, 5)
     mine = np.array(rep.residuals)
@@ -114,15 +124,14 @@ def test_cfg4_fmg_vs_restatement(ranks):
     mg = H.GridHierarchy(dom, ctl, H.LAPLACE, lmin, L, smoother="jacobi", coarse_tol=1e-12)
     rep = mg.fmg(rhs, x, L, 1e-10, 40)
     o = O.Session(mesh, lmin, L, 7)
+    o.coarse_solver(1)
     o.set(0, L, b)
     ref = o.fmg(0, 1, L, 0, 2, 2, 2.0 / 3.0, 1e-12, 1, 1e-10, 40)
     mine = np.array(rep.residuals)
     assert rep.converged and len(mine) == len(ref), (mine, ref)
-    # 1e-8 relative per cycle above the rounding floor of ||b - A x||: the
-    # coarse CG solutions differ at 1e-12 (assembled CSR here, matrix-free in
-    # the restatement), leaving ulp-level differences in x whose residuals
-    # differ by ~eps * ||r0|| absolute once ||r|| < 1e-9 ||r0||
-    assert np.all(np.abs(mine - ref) <= 1e-8 * ref + 1e-13 * ref[0]), (mine, ref)
+    assert np.all(np.abs(mine - ref) <= 1e-8 * ref), (np.abs(mine - ref) / ref, mine, ref)
+    # the iterate itself is bitwise the restatement's
+    assert np.array_equal(x.download(L), o.get(1, L))
     # the FMG sweep alone reaches discretisation-level accuracy
     assert mine[1] / mine[0] < 0.1
     # restricted rhs on a coarse level agrees too (DIRICHLET rows zeroed)
@@ -131,7 +140,6 @@ def test_cfg4_fmg_vs_restatement(ranks):
         o.restrict(0, 0, lc)
         o.assign(0.0, 0, 0.0, 0, 0, lc, H.DIRICHLET)
     assert np.array_equal(rhs.download(lmin), o.get(0, lmin))
-    np.testing.assert_allclose(x.download(L), o.get(1, L), rtol=0, atol=1e-9 * np.abs(o.get(1, L)).max())
 
 
 @pytest.mark.parametrize("ranks", [1, 2])
@@ -151,11 +159,13 @@ def test_fmg_whole_gpu_coarse_cg_vs_restatement(ranks):
     mg = H.GridHierarchy(dom, ctl, H.LAPLACE, lmin, L, smoother="jacobi", coarse_tol=1e-10)
     rep = mg.fmg(rhs, x, L, 1e-9, 30)
     o = O.Session(mesh, lmin, L, 7)
+    o.coarse_solver(1, torch_sm_count())
     o.set(0, L, b)
     ref = o.fmg(0, 1, L, 0, 2, 2, 2.0 / 3.0, 1e-10, 1, 1e-9, 30)
     mine = np.array(rep.residuals)
     assert rep.converged and len(mine) == len(ref), (mine, ref)
-    assert np.all(np.abs(mine - ref) <= 1e-8 * ref + 1e-13 * ref[0]), (mine, ref)
+    assert np.all(np.abs(mine - ref) <= 1e-8 * ref), (np.abs(mine - ref) / ref, mine, ref)
+    assert np.array_equal(x.download(L), o.get(1, L))
     # again: the cycles now replay from CUDA graphs holding the cooperative launch
     rhs.upload(L, b)
     rep2 = mg.fmg(rhs, x, L, 1e-9, 30)
@@ -179,11 +189,15 @@ def test_cfg5_pcg_vs_restatement(ranks):
     mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="jacobi", coarse_tol=1e-12)
     rep = mg.pcg(rhs, x, L, 12)
     o = O.Session(mesh, 0, L, 11)
+    o.coarse_solver(1)
     o.set(0, L, b)
     ref = o.pcg(0, 1, L, 1, 1, 2.0 / 3.0, 1e-12, 12)
     mine = np.array(rep.residuals)
     assert len(mine) == 13
-    assert np.all(np.abs(mine - ref) <= 1e-8 * ref + 1e-13 * ref[0]), (mine, ref)
+    # alpha and beta come from dots whose summation shapes differ (per-primitive
+    # sequential here, fixed device trees there: ~1 ulp), so x is not bitwise;
+    # the recurrence residuals still agree to 1e-8 relative per iteration
+    assert np.all(np.abs(mine - ref) <= 1e-8 * ref), (np.abs(mine - ref) / ref, mine, ref)
     assert mine[-1] / mine[0] < 1e-5, mine
     # x solves A x = b to the final residual
     r = H.ScalarFunction("r", dom, L, L)
@@ -202,7 +216,7 @@ def test_pcg_graph_replay_matches_eager():
     rhs = H.ScalarFunction("rhs", dom, L, L)
     x = H.ScalarFunction("x", dom, L, L)
     H.interpolate_random(rhs, L, seed=4, flag_mask=H.INNER)
-    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="jacobi")
     mg.use_graphs(False)
     eager = mg.pcg(rhs, x, L, 10).residuals
     mg.use_graphs(True)

@@ -30,3 +30,18 @@ def test_cpp_api_runs_on_gpu():
     out = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "cpp api ok" in out.stdout
+    # SolveReport::history(): the same text as the reference's for the same solve
+    # (GridHierarchy on unit_square, levels 1..5, keyed U[-1,1] rhs seed 5, 6 cycles)
+    from oracle import ref as R
+    from tests.helpers import keyed_uniform
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    mine = out.stdout.split("HISTORY_BEGIN\n")[1].split("HISTORY_END")[0]
+    mesh = R.meshgen("unit_square")
+    r = R.RefSession(mesh, 1, 1, 5, 2)
+    r.set(0, 5, keyed_uniform(mesh, 5, seed=5))
+    res = r.gridhierarchy_solve(0, 1, 5, 0.0, 6)
+    want = "".join(f"cycle {k} residual {v:.6e}\n" if k == 0 else
+                   f"cycle {k} residual {v:.6e} factor {v / res[k - 1] if res[k - 1] > 0 else 0.0:.4f}\n"
+                   for k, v in enumerate(res))
+    assert mine == want, (mine, want)

@@ -146,3 +146,56 @@ def test_restatement_fmg_and_pcg_converge():
     assert res[-1] / res[0] < 1e-6
     o.residual(0, 1, 2, 6)
     assert abs(np.sqrt(o.dot(2, 2, 6)) - res[-1]) <= 1e-6 * res[-1]
+
+
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("mesh_kind,lmin,L", [(("channel", 3, 2, 2.0, 1.5), 1, 5), (("annulus", 16, 3, 1.0, 2.0), 1, 5),
+                                              (("channel", 16, 8, 1.0, 1.0), 2, 5)])
+def test_device_coarse_solver_matches_reference_gridhierarchy(mesh_kind, lmin, L):
+    """og_coarse_solver(1) -- the product's coarse solve restated: the
+    constrained CSR of the min level and cg_solve's recurrence with the device
+    kernels' dot shapes -- inside the reference GridHierarchy's own cycle
+    (smooth_gs, min level >= 1) against GridHierarchy::solve itself. The matrix
+    is the reference's, so only the dot order differs: <= 1e-10 per cycle.
+    channel(16, 8) at level 2 has 2,145 DoFs: the register-resident
+    (Chronopoulos-Gear) coarse kernel's path."""
+    mesh = R.meshgen(*mesh_kind)
+    b = keyed_uniform(mesh, L, seed=9)
+    r = R.RefSession(mesh, 1, lmin, L, 2)
+    fl = r.flags(0, L)
+    b[fl != 1] = 0.0
+    r.set(0, L, b)
+    ref = r.gridhierarchy_solve(0, 1, L, 0.0, 4)
+    for nsm in (148, 2):  # nsm 2: n > nsm * 512 forces the grid-kernel dot shape
+        o = O.Session(mesh, lmin, L, 7)
+        o.coarse_solver(1, nsm)
+        o.set(0, L, b)
+        mine = o.vcycle(0, 1, L, 1, 2, 2, 1.0, 1e-12, 4)
+        assert np.max(np.abs(mine - ref) / ref) <= 1e-10, (nsm, mine, ref)
+
+
+def _nz(coo):
+    r, c, v = coo
+    keep = v != 0.0
+    return r[keep], c[keep], v[keep]
+
+
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("mesh_kind", [("unit_square",), ("square_ring8",), ("channel", 3, 2, 2.0, 1.5),
+                                       ("annulus", 16, 3, 1.0, 2.0)])
+@pytest.mark.parametrize("bc", ["dirichlet", "mixed"])
+def test_coarse_matrix_bitwise_reference(mesh_kind, bc):
+    """The min-level system the device coarse CG solves (hyb_coarse_matrix_host,
+    csrc/coarse.cpp) and the one og_coarse_solver(1) restates are bitwise the
+    reference GridHierarchy's constrained_matrix (assemble_global_sparse +
+    constrain_dirichlet, src/solvers.cpp:358-364), stored zeros aside."""
+    from paper_1805_10167_b200 import hytegrid as H
+    mesh = R.meshgen(*mesh_kind)
+    bcd = BCS[bc]
+    for level in range(0, 4):
+        ref = _nz(R.RefSession(mesh, 2, level, level, 1, bcd).coarse_matrix(level))
+        dev = _nz(H.coarse_matrix_host(mesh, level, 0, bcd))
+        og = _nz(O.Session(mesh, level, level, 1, bcd).coarse_matrix(0))
+        for a, b in ((ref, dev), (ref, og)):
+            for u, w in zip(a, b):
+                assert np.array_equal(u, w), (mesh_kind, bc, level)

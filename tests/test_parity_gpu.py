@@ -166,7 +166,7 @@ def test_partition_invariance_of_jacobi_and_vcycle(ranks):
     out = []
     for rk in (1, ranks):
         dom = H.DistributedDomain(mesh, rk)
-        mg = H.GridHierarchy(dom, H.Controller(dom), H.LAPLACE, 1, 4)
+        mg = H.GridHierarchy(dom, H.Controller(dom), H.LAPLACE, 1, 4, smoother="jacobi")
         rhs = H.ScalarFunction("rhs", dom, 1, 4)
         x = H.ScalarFunction("x", dom, 1, 4)
         H.interpolate(rhs, probe, 4)
@@ -233,7 +233,7 @@ def test_harmonic_extension_of_linear_data():
     L = 5
     dom = H.DistributedDomain(mesh, 3)
     ctl = H.Controller(dom)
-    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 1, L)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 1, L, smoother="jacobi")
     rhs = H.ScalarFunction("rhs", dom, 1, L)
     x = H.ScalarFunction("x", dom, 1, L)
     lin = lambda a, b: 1.5 + 2.0 * a - 0.75 * b  # noqa: E731
@@ -278,16 +278,34 @@ def test_smoothers_keep_exact_solution_fixed():
     assert np.array_equal(rig.f[2].download(2), want)
 
 
-def test_diagonal_matches_reference_stencils():
-    mesh = H.meshgen.square_ring8()
-    dom = H.DistributedDomain(mesh, 2)
-    A = H.StencilOperator(dom, H.LAPLACE, 3, 3)
-    d = H.ScalarFunction("d", dom, 3, 3)
-    H.diagonal(A, d, 3)
-    vals = d.download(3)
-    flags = d.flags(3)
-    assert np.all(vals[flags == H.DIRICHLET] == 1.0)
-    assert np.all(vals[flags == H.INNER] > 0)
+@pytest.mark.parametrize("mesh_name,ranks", [("ring8", 2), ("square_rev", 3), ("channel21", 1), ("tri", 2)])
+@pytest.mark.parametrize("form", [H.LAPLACE, H.MASS], ids=["laplace", "mass"])
+@pytest.mark.parametrize("bc", [None, MIXED_BC], ids=["dirichlet", "mixed"])
+def test_diagonal_bitwise_reference(mesh_name, ranks, form, bc):
+    """diagonal(A, d, level) (src/operators.cpp:484-505) against the reference's,
+    bitwise, on every owned DoF (DIRICHLET rows included), levels 0-4."""
+    mesh = FIXTURES[mesh_name]()
+    for level in range(0, 5):
+        dom = H.DistributedDomain(mesh, ranks)
+        A = H.StencilOperator(dom, form, level, level, bc)
+        d = H.ScalarFunction("d", dom, level, level, bc)
+        H.diagonal(A, d, level)
+        ref = R.RefSession(mesh, ranks, level, level, 1, bc)
+        ref.diagonal(int(form), 0, level)
+        mine, want = d.download(level), ref.get(0, level)
+        assert np.array_equal(mine, want), (level, np.flatnonzero(mine != want)[:5])
+
+
+def test_diagonal_annulus_perturbed_bitwise():
+    """per-face affine stencils (config 3 family): non-trivial diagonals per face"""
+    mesh = H.meshgen.perturb(H.meshgen.annulus(16, 4, 1.0, 2.0), 0.1, 2)
+    dom = H.DistributedDomain(mesh, 3)
+    A = H.StencilOperator(dom, H.LAPLACE, 4, 4)
+    d = H.ScalarFunction("d", dom, 4, 4)
+    H.diagonal(A, d, 4)
+    ref = R.RefSession(mesh, 3, 4, 4, 1)
+    ref.diagonal(0, 0, 4)
+    assert np.array_equal(d.download(4), ref.get(0, 4))
 
 
 @pytest.mark.slow
@@ -344,7 +362,7 @@ def test_graph_replayed_vcycles_bitwise_equal_eager():
     for graphs in (False, True):
         dom = H.DistributedDomain(mesh, 2)
         ctl = H.Controller(dom)
-        mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L)
+        mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="jacobi")
         mg.use_graphs(graphs)
         rhs = H.ScalarFunction("rhs", dom, 0, L)
         x = H.ScalarFunction("x", dom, 0, L)

@@ -12,7 +12,7 @@ dom = H.DistributedDomain(mesh, 1)
 ctl = H.Controller(dom)
 rhs, x = H.ScalarFunction("rhs", dom, L, L), H.ScalarFunction("x", dom, L, L)
 H.interpolate_random(rhs, L, seed=3, flag_mask=H.INNER)
-mg = H.GridHierarchy(dom, ctl, H.LAPLACE, L, L, coarse_tol=float(sys.argv[1]) if len(sys.argv) > 1 else 1e-9)
+mg = H.GridHierarchy(dom, ctl, H.LAPLACE, L, L, smoother="jacobi", coarse_tol=float(sys.argv[1]) if len(sys.argv) > 1 else 1e-9)
 mg.vcycle(rhs, x, L)
 dom.synchronize()
 dom.event_record(0)

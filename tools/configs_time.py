@@ -39,7 +39,7 @@ def cfg1(args):
     ctl = H.Controller(dom)
     rhs, x = H.ScalarFunction("rhs", dom, 0, L), H.ScalarFunction("x", dom, 0, L)
     H.interpolate_random(rhs, L, seed=0, flag_mask=H.INNER)
-    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, coarse_tol=1e-14)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="jacobi", coarse_tol=1e-14)
     mg.solve(rhs, x, L, 0.0, 2)  # warm (graph capture)
     H.interpolate(x, 0.0, L)
     rep, ms, wall = timed(dom, lambda: mg.solve(rhs, x, L, 0.0, 10))
@@ -77,7 +77,7 @@ def cfg4(args):
     H.interpolate_random(noise, L, seed=3, lo=-1e-3, hi=1e-3, flag_mask=H.INNER)
     H.add_scaled(rhs, 1.0, noise, L)
     del noise
-    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, lmin, L, coarse_tol=args.cfg4_coarse_tol)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, lmin, L, smoother="jacobi", coarse_tol=args.cfg4_coarse_tol)
     fine = H.ScalarFunction("b", dom, L, L)
     H.assign(1.0, rhs, 0.0, rhs, fine, L)
     mg.fmg(rhs, x, L, args.cfg4_tol, 3)  # warm: plans, graphs
@@ -97,7 +97,7 @@ def cfg5(args):
     ctl = H.Controller(dom)
     rhs, x = H.ScalarFunction("rhs", dom, L, L), H.ScalarFunction("x", dom, L, L)
     H.interpolate_random(rhs, L, seed=4, flag_mask=H.INNER)
-    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L)
+    mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="jacobi")
     mg.pcg(rhs, x, L, 3)  # warm: plans, graph capture
     rep, ms, wall = timed(dom, lambda: mg.pcg(rhs, x, L, 50))
     dofs = dom.owned_count(L)[0]
