@@ -507,3 +507,227 @@ __global__ void __launch_bounds__(128) k_gs_ev(LevelTables t, FlagTables fl, con
     for (int j = 0; j <= ne; ++j) acc += co[j] * x[off + j];
     x[off] = x[off] + 1.0 * (b[off] - acc) / co[ne + 1];
 }
+
+// ---------------------------------------------------------------------------
+// Coloured face sweep in column blocks (faces of every size). One CTA per
+// (face, block of CB columns) runs the k_cgs_tma step schedule (C0 on rows
+// [j, j+K), C1 on [j-S, j-S+K), C2 on [j-2S, j-2S+K), S = K+1, one consumer
+// barrier per step, TMA-fed shared-memory row rings) on ring rows that hold
+// only the block's columns plus a 4-column halo on each side.
+//   * One block per face (CB >= n-1): in place (y == x allowed): no other CTA
+//     touches the face, and rows are written back only once final.
+//   * Several blocks: out of place (x -> y). A block's C1 / C2 read its
+//     neighbours' C0 / C1 columns, so the CTA recomputes C0 on [c0-2, c1+2)
+//     and C1 on [c0-1, c1+1) and keeps only [c0, c1). The recomputed values
+//     are bitwise the owner's: same operands from the unmodified x, same term
+//     order; no CTA ever reads another's writes. The caller swaps y in for x
+//     (edges and vertices: k_cgs_edges_oop / k_cgs_verts_oop).
+// Producers: two warps whose lane 0 issues every copy with scalar code (the
+// row offsets from t.rowoff, ring slots tracked incrementally). Warp A writes
+// the final rows back and loads x rows, warp B loads b rows; each arrives on
+// the step's full barrier with its byte count. With one producer warp issuing
+// per-lane copies (ELECT loops, per-lane row arithmetic, a warp reduction) the
+// producer's instruction stream bounded the step rate (ncu: consumers 33% in
+// the full-barrier wait, the producer warp never waiting).
+// Bitwise the in-place sweep, og_cgs.
+template <int K, int D, int CB, int WPR> struct CgcCfg {
+    static constexpr int RX = D * K + 3 * K + 3; // x ring rows (see k_cgs_tma)
+    static constexpr int RB = D * K + 2 * K + 2; // b ring rows
+    static constexpr int NB = D + 1;
+    static constexpr int CW = 3 * K * WPR;
+    static constexpr int THREADS = (CW + 2) * 32;
+    static constexpr int RS = CB + 8; // ring row: columns [c0-4, c0+CB+4)
+    static constexpr size_t SMEM = size_t(RX + RB) * RS * 8 + 16 * NB;
+};
+
+template <int K, int D, int CB, int MINB, int WPR>
+__global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR>::THREADS, MINB)
+    k_cgs_cols(LevelTables t, const double* __restrict__ b, const double* x, double* y) {
+    using C = CgcCfg<K, D, CB, WPR>;
+    extern __shared__ __align__(16) double cc_ring[];
+    constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = K + 1, RS = C::RS;
+    const int n = t.n, W = t.W;
+    const int c0 = int(blockIdx.x) * CB, c1 = c0 + CB;
+    // last row with an interior point in the computed columns [c0-2, c1+2)
+    const int last = min(n - 2, n - 1 - max(1, c0 - 2));
+    if (last < 1) return; // CTA-uniform
+    double* xring = cc_ring;
+    double* bring = cc_ring + size_t(RX) * RS;
+    uint64_t* full = reinterpret_cast<uint64_t*>(cc_ring + size_t(RX + RB) * RS);
+    uint64_t* done = full + NB;
+    const int64_t base = int64_t(blockIdx.y) * t.face_stride;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nsteps = (last + 2 * S - 1) / K + 1;
+    const int a0 = max(0, c0 - 4); // first staged column
+    const int so = a0 - (c0 - 4);  // its ring index
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NB; ++i) {
+            mbar_init(&full[i], 2);
+            mbar_init(&done[i], C::CW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp >= C::CW) { // producers
+        if (lane != 0) return;
+        const int64_t* __restrict__ ro = t.rowoff;
+        // bytes of the staged columns [lo, min(hi, row end rounded up to 2)) of row q
+        auto seg = [&](int q, int lo, int hi) {
+            const int e = min(hi, (W - q + 1) & ~1);
+            return e > lo ? uint32_t(e - lo) * 8u : 0u;
+        };
+        if (warp == C::CW) { // A: write-back of final rows, x rows
+            const double* xf = x + base;
+            double* yf = y + base;
+            const int xmax = last + 1;
+            int q_next = 0, slot_next = 0; // next x row to load and its ring slot
+            auto load_x = [&](int s_) {    // rows first read at step s_: up to 1 + (s_+1)K
+                const int qhi = min(xmax, 1 + (s_ + 1) * K);
+                uint32_t bytes = 0;
+                for (int q = q_next; q <= qhi; ++q) bytes += seg(q, a0, c1 + 4);
+                mbar_arrive_expect_tx(&full[s_ % NB], bytes);
+                for (; q_next <= qhi; ++q_next) {
+                    const uint32_t nb_ = seg(q_next, a0, c1 + 4);
+                    if (nb_) bulk_g2s(xring + size_t(slot_next) * RS + so, xf + ro[q_next] + a0, nb_, &full[s_ % NB]);
+                    slot_next = slot_next + 1 == RX ? 0 : slot_next + 1;
+                }
+            };
+            for (int s_ = 0; s_ < D && s_ < nsteps; ++s_) load_x(s_);
+            int q_st = 1 - 2 * S + 0, slot_st = ((q_st % RX) + RX) % RX; // first row of step 0's C2 block
+            for (int i = 0; i < nsteps; ++i) {
+                mbar_wait(&done[i % NB], uint32_t((i / NB) & 1));
+                for (int k = 0; k < K; ++k) { // rows q_st .. q_st + K - 1 are final after step i
+                    const int q = q_st + k;
+                    const int sl = slot_st + k >= RX ? slot_st + k - RX : slot_st + k;
+                    if (q >= 1 && q <= last) {
+                        const uint32_t nb_ = seg(q, c0, c1);
+                        if (nb_) bulk_s2g(yf + ro[q] + c0, xring + size_t(sl) * RS + 4, nb_);
+                    }
+                }
+                bulk_commit();
+                bulk_wait_read1();
+                q_st += K;
+                slot_st = slot_st + K >= RX ? slot_st + K - RX : slot_st + K;
+                if (i + D < nsteps) load_x(i + D);
+            }
+            bulk_wait_all();
+        } else { // B: b rows [1 + sK, (s+1)K]
+            const double* bf = b + base;
+            int q_next = 1, slot_next = 1 % RB;
+            auto load_b = [&](int s_) {
+                const int qhi = min(last, (s_ + 1) * K);
+                uint32_t bytes = 0;
+                for (int q = q_next; q <= qhi; ++q) bytes += seg(q, a0, c1 + 2);
+                mbar_arrive_expect_tx(&full[s_ % NB], bytes);
+                for (; q_next <= qhi; ++q_next) {
+                    const uint32_t nb_ = seg(q_next, a0, c1 + 2);
+                    if (nb_) bulk_g2s(bring + size_t(slot_next) * RS + so, bf + ro[q_next] + a0, nb_, &full[s_ % NB]);
+                    slot_next = slot_next + 1 == RB ? 0 : slot_next + 1;
+                }
+            };
+            for (int s_ = 0; s_ < D && s_ < nsteps; ++s_) load_b(s_);
+            for (int i = 0; i < nsteps; ++i) {
+                if (i + D >= nsteps) break;
+                mbar_wait(&done[i % NB], uint32_t((i / NB) & 1));
+                load_b(i + D);
+            }
+        }
+        return;
+    }
+    double co[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) co[i] = __ldg(t.face_coef + size_t(blockIdx.y) * 8 + i);
+    const double rd = 1.0 / co[7];
+    const int h = warp / WPR;
+    const int colour = h / K, roff = h % K;
+    const int u0 = ((warp % WPR) << 5) + lane;
+    const int clo = max(1, c0 - 2 + colour), chi = c1 + 1 - colour; // this colour's columns (inclusive)
+    int r = 1 - S * colour + roff;
+    auto wrap = [](int v, int m) { return ((v % m) + m) % m; };
+    int sxm = wrap(r - 1, RX), sx0 = wrap(r, RX), sxp = wrap(r + 1, RX), sb = wrap(r, RB);
+    int t3 = wrap(colour - 2 * r, 3);
+    constexpr int DT3 = (3 - (2 * K) % 3) % 3;
+    const int sh = 4 - c0; // ring index of column c
+#pragma unroll 1
+    for (int i = 0; i < nsteps; ++i) {
+        mbar_wait(&full[i % NB], uint32_t((i / NB) & 1));
+        if (r >= 1 && r <= last) {
+            const double* rm = xring + sxm * RS + sh;
+            double* r0 = xring + sx0 * RS + sh;
+            const double* rp = xring + sxp * RS + sh;
+            const double* br = bring + sb * RS + sh;
+            const int cmax = min(n - 1 - r, chi);
+            const int cs = clo + wrap(t3 - clo, 3); // first column >= clo of this colour
+#pragma unroll 1
+            for (int c = cs + 3 * u0; c <= cmax; c += 192 * WPR) {
+                const int c2 = c + 96 * WPR;
+                double v[8], w[8];
+                v[0] = r0[c - 1], v[1] = rp[c - 1], v[2] = rm[c], v[3] = r0[c];
+                v[4] = rp[c], v[5] = rm[c + 1], v[6] = r0[c + 1], v[7] = br[c];
+                const bool two = c2 <= cmax;
+                if (two) {
+                    w[0] = r0[c2 - 1], w[1] = rp[c2 - 1], w[2] = rm[c2], w[3] = r0[c2];
+                    w[4] = rp[c2], w[5] = rm[c2 + 1], w[6] = r0[c2 + 1], w[7] = br[c2];
+                }
+                r0[c] = cgs_point_update(v, co, rd);
+                if (two) r0[c2] = cgs_point_update(w, co, rd);
+            }
+        }
+        fence_proxy_async_smem();
+        consumer_sync<C::CW * 32>();
+        if (lane == 0) mbar_arrive(&done[i % NB]);
+        r += K;
+        sxm = sxm + K >= RX ? sxm + K - RX : sxm + K;
+        sx0 = sx0 + K >= RX ? sx0 + K - RX : sx0 + K;
+        sxp = sxp + K >= RX ? sxp + K - RX : sxp + K;
+        sb = sb + K >= RB ? sb + K - RB : sb + K;
+        t3 = t3 + DT3 >= 3 ? t3 + DT3 - 3 : t3 + DT3;
+    }
+}
+
+// edges out of place: odd k from x, then even k reading the new odd values
+// from y (the in-place sweep's operands); DIRICHLET lines are copied
+__global__ void __launch_bounds__(128) k_cgs_edges_oop(LevelTables t, FlagTables fl, const double* __restrict__ b,
+                                                       const double* __restrict__ x, double* __restrict__ y,
+                                                       int parity, int kblocks) {
+    const int n = t.n;
+    const int e = blockIdx.x / kblocks;
+    const int k = 2 * ((blockIdx.x % kblocks) * blockDim.x + threadIdx.x) + parity;
+    if (e >= t.nedges || k < 1 || k > n - 1) return;
+    const int64_t off = t.edge_off[e];
+    const double* L = x + off;
+    if (fl.edge_flag[e] & 2) {
+        y[off + k] = L[k];
+        return;
+    }
+    const double* Ln = parity ? L : y + off; // neighbours k +- 1: old for odd k, new for even k
+    const double* H0 = L + (n + 1);
+    const double* co = t.edge_coef + size_t(e) * 8;
+    double acc = 0.0;
+    acc += co[0] * Ln[k - 1];
+    acc += co[1] * L[k];
+    acc += co[2] * Ln[k + 1];
+    acc += co[3] * H0[k - 1];
+    acc += co[4] * H0[k];
+    if (t.edge_nf[e] == 2) {
+        acc += co[5] * H0[n + k - 1];
+        acc += co[6] * H0[n + k];
+    }
+    y[off + k] = L[k] + 1.0 * (b[off + k] - acc) / co[7];
+}
+
+__global__ void __launch_bounds__(128) k_cgs_verts_oop(LevelTables t, FlagTables fl, const double* __restrict__ b,
+                                                       const double* __restrict__ x, double* __restrict__ y) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= t.nverts) return;
+    const int64_t off = t.vtx_off[v];
+    if (fl.vtx_flag[v] & 2) {
+        y[off] = x[off];
+        return;
+    }
+    const int ne = t.vtx_ne[v];
+    const double* co = t.vtx_coef + t.vtx_coef_off[v];
+    double acc = 0.0;
+    for (int j = 0; j <= ne; ++j) acc += co[j] * x[off + j];
+    y[off] = x[off] + 1.0 * (b[off] - acc) / co[ne + 1];
+}

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // sm_100a kernels for the P1 macro-face multigrid hot path.
 //
 // Every kernel is HBM-bound (fp64, 0.8 flop/B); no tensor cores. Arithmetic
@@ -128,6 +129,37 @@ __global__ void __launch_bounds__(256) k_ghost_gather(const I* __restrict__ dst,
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < ntotal;
          i += int64_t(gridDim.x) * blockDim.x)
         arena[dst[i]] = i < nlocal ? arena[src[i]] : recv[i - nlocal];
+}
+
+// 32-bit plans: four ghosts per thread, indices as int4, the four owner loads
+// issued before any store (one thread per ghost left each thread a chain of
+// index load -> owner load -> store, ~1 TB/s at config 3's level 9)
+__global__ void __launch_bounds__(256) k_ghost_gather4(const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
+                                                       int64_t nlocal, int64_t ntotal, double* arena,
+                                                       const double* __restrict__ recv) {
+    const int64_t i0 = 4 * (blockIdx.x * int64_t(blockDim.x) + threadIdx.x);
+    if (i0 >= ntotal) return;
+    if (i0 + 4 <= nlocal) {
+        const int4 d = __ldg(reinterpret_cast<const int4*>(dst + i0));
+        const int4 s = __ldg(reinterpret_cast<const int4*>(src + i0));
+        const double v0 = arena[s.x], v1 = arena[s.y], v2 = arena[s.z], v3 = arena[s.w];
+        arena[d.x] = v0;
+        arena[d.y] = v1;
+        arena[d.z] = v2;
+        arena[d.w] = v3;
+        return;
+    }
+    if (i0 >= nlocal && i0 + 4 <= ntotal) {
+        const int4 d = __ldg(reinterpret_cast<const int4*>(dst + i0));
+        const double* r = recv + (i0 - nlocal);
+        const double v0 = r[0], v1 = r[1], v2 = r[2], v3 = r[3];
+        arena[d.x] = v0;
+        arena[d.y] = v1;
+        arena[d.z] = v2;
+        arena[d.w] = v3;
+        return;
+    }
+    for (int64_t i = i0; i < i0 + 4 && i < ntotal; ++i) arena[dst[i]] = i < nlocal ? arena[src[i]] : recv[i - nlocal];
 }
 
 __global__ void __launch_bounds__(256) k_ghost_pack(const int64_t* __restrict__ src, int64_t n,
@@ -620,9 +652,8 @@ void launch_ghost_gather(const void* dst, const void* src, bool idx32, int64_t n
     // dependent round trips)
     const int blocks = grid_for(ntotal, 256, 1 << 30);
     if (idx32)
-        k_ghost_gather<int32_t><<<blocks, 256, 0, st>>>(static_cast<const int32_t*>(dst),
-                                                                   static_cast<const int32_t*>(src), nlocal, ntotal,
-                                                                   arena, recv);
+        k_ghost_gather4<<<grid_for((ntotal + 3) / 4, 256, 1 << 30), 256, 0, st>>>(
+            static_cast<const int32_t*>(dst), static_cast<const int32_t*>(src), nlocal, ntotal, arena, recv);
     else
         k_ghost_gather<int64_t><<<blocks, 256, 0, st>>>(static_cast<const int64_t*>(dst),
                                                                    static_cast<const int64_t*>(src), nlocal, ntotal,
@@ -682,6 +713,78 @@ void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStre
     else if (t.n <= 128) k_cgs_faces<8, 2><<<unsigned(t.nfaces), 64, 0, st>>>(t, b, x);
     else k_cgs_faces<8><<<unsigned(t.nfaces), CGS_WARPS * 32, 0, st>>>(t, b, x);
     check_launch("coloured gauss-seidel faces");
+}
+
+template <int K, int D, int CB, int MINB, int WPR>
+bool launch_cgs_cols(const LevelTables& t, const double* b, double* x, double* y, cudaStream_t st) {
+    using C = CgcCfg<K, D, CB, WPR>;
+    static const bool attr = cudaFuncSetAttribute(k_cgs_cols<K, D, CB, MINB, WPR>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)) ==
+                             cudaSuccess;
+    if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
+    const int nb = (t.n - 1 + CB - 1) / CB; // blocks over columns [0, n-1)
+    double* out = nb == 1 ? x : y;          // one block per face: in place
+    k_cgs_cols<K, D, CB, MINB, WPR><<<dim3(unsigned(nb), unsigned(t.nfaces)), C::THREADS, C::SMEM, st>>>(t, b, x, out);
+    return nb > 1;
+}
+
+// tuning knob for measurements (HYB_CGS_CFG); the default is the measured best
+static int cgs_cfg() {
+    static const int v = [] {
+        const char* e = std::getenv("HYB_CGS_CFG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+// coloured face sweep: true if the faces went out of place into y
+bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, double* y, cudaStream_t st) {
+    if (t.nfaces <= 0 || t.n < 4) return false;
+    bool oop = false;
+    const int n = t.n, v = cgs_cfg();
+    if (v == 1 && n >= 256) {
+        oop = n == 512 ? launch_cgs_cols<2, 3, 256, 3, 1>(t, b, x, y, st)
+                       : launch_cgs_cols<2, 3, 128, 4, 1>(t, b, x, y, st);
+    } else if (v == 9 && n == 256) {
+        oop = launch_cgs_cols<2, 3, 256, 4, 1>(t, b, x, y, st);
+    } else if (v == 10 && n == 256) {
+        oop = launch_cgs_cols<2, 4, 128, 4, 1>(t, b, x, y, st);
+    } else if (v == 11 && n == 256) {
+        oop = launch_cgs_cols<2, 2, 256, 4, 1>(t, b, x, y, st);
+    } else if (v == 8 && n <= 128) {
+        oop = launch_cgs_cols<2, 3, 128, 4, 1>(t, b, x, y, st);
+    } else if (n <= 128) {
+        // small faces: two warps per face, 8-row blocks through L1/L2 (config 3, 8192 faces: L7
+        // 0.67 ms, L6 0.29, L5 0.15; the ring kernel: L7 0.80)
+        k_cgs_faces<8, 2><<<unsigned(t.nfaces), 64, 0, st>>>(t, b, x);
+    } else if (n == 256) {
+        // config 3 L8: 4 CTAs per SM (64 registers) 1.705 ms per sweep; 3 CTAs 1.828, D = 2 1.884,
+        // 128-column blocks out of place 2.42-2.44
+        oop = launch_cgs_cols<2, 3, 256, 4, 1>(t, b, x, y, st);
+    } else if (n == 512) {
+        // measured at config 3 L9 (8192 faces, per sweep): in place 2 CTAs per SM 5.54 ms; 256-column
+        // blocks out of place (3 CTAs) 5.70, with D = 4 5.70, D = 6 (2 CTAs) 7.50; K = 3 6.98;
+        // D = 2 6.65; two warps per row 6.11; 128-column blocks 9.6 (one producer warp)
+        oop = launch_cgs_cols<2, 3, 512, 2, 1>(t, b, x, y, st);
+    } else {
+        oop = launch_cgs_cols<2, 3, 256, 3, 1>(t, b, x, y, st);
+    }
+    check_launch("coloured gauss-seidel faces (column blocks)");
+    return oop;
+}
+
+void launch_cgs_ev_oop(const LevelTables& t, const FlagTables& fl, const double* b, const double* x, double* y,
+                       cudaStream_t st) {
+    if (t.nverts > 0) {
+        k_cgs_verts_oop<<<(t.nverts + 127) / 128, 128, 0, st>>>(t, fl, b, x, y);
+        check_launch("coloured gauss-seidel vertices");
+    }
+    const int kb = t.n - 1 > 0 ? (t.n / 2 + 127) / 128 : 0;
+    if (t.nedges > 0 && kb > 0)
+        for (int parity = 1; parity >= 0; --parity) { // odd k first, then even k
+            k_cgs_edges_oop<<<t.nedges * kb, 128, 0, st>>>(t, fl, b, x, y, parity, kb);
+            check_launch("coloured gauss-seidel edges");
+        }
 }
 
 void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st) {
@@ -1375,6 +1478,14 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const 
     }
 }
 
+int64_t coarse_grid_min_rows() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("HYB_COARSE_GRID_MIN");
+        return e ? int64_t(std::atoll(e)) : kCoarseGridMinRows;
+    }();
+    return v;
+}
+
 int coarse_grid_blocks() {
     static const int g = [] {
         int dev = 0, sms = 0, per = 0;
@@ -1391,7 +1502,7 @@ int coarse_grid_blocks() {
 void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* b,
                       double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
                       double* grid_part, unsigned* grid_bar, int max_row_nnz, cudaStream_t stream) {
-    if (n >= kCoarseGridMinRows && grid_part && grid_bar && coarse_grid_blocks() > 0) {
+    if (n >= coarse_grid_min_rows() && grid_part && grid_bar && coarse_grid_blocks() > 0) {
         const int64_t threads = int64_t(coarse_grid_blocks()) * CGG_THREADS;
         if (n <= threads && max_row_nnz <= 16) { // register-resident rows, just enough CTAs
             const int blocks = int((n + CGG_THREADS - 1) / CGG_THREADS);

@@ -135,6 +135,11 @@ void launch_gs_ev(const LevelTables& t, const FlagTables& fl, const double* b, d
 // odd/even k, vertices as in launch_gs_ev
 void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st);
 void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st);
+// column-blocked faces (k_cgs_cols): in place when a face is one block, else
+// out of place into y (returns true); bitwise the in-place sweep either way
+bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, double* y, cudaStream_t st);
+void launch_cgs_ev_oop(const LevelTables& t, const FlagTables& fl, const double* b, const double* x, double* y,
+                       cudaStream_t st);
 // dst := alpha*x1 + beta*x2 (op 0), dst += alpha*x1 (op 1), dst := alpha (op 2)
 void launch_blas1(int op, const LevelTables& t, const FlagTables& fl, double alpha, const double* x1, double beta,
                   const double* x2, double* dst, uint8_t mask, cudaStream_t st);
@@ -188,6 +193,9 @@ void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos,
 // (register-resident rows, at most one CTA per SM) or one CTA per SM; both need
 // grid_part (>= 4 x #SMs doubles) and grid_bar (2 unsigned, zero-initialised)
 constexpr int64_t kCoarseGridMinRows = 2048;
+/// the threshold in effect: kCoarseGridMinRows, or HYB_COARSE_GRID_MIN (a
+/// measurement knob; the restatement's og_coarse_solver must be told the same)
+int64_t coarse_grid_min_rows();
 int coarse_grid_blocks();
 void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* b,
                       double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,

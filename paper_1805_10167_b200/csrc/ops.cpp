@@ -202,12 +202,18 @@ void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level) {
     Domain& d = A.domain();
     d.sync(x, level);
     const LevelTables t = A.tables(level);
-    d.fork();
-    launch_cgs_ev(t, x.flags(), rhs.data(level), x.data(level), d.aux_stream());
+    // faces in column blocks (k_cgs_cols): one block per face sweeps in place;
+    // several blocks per face sweep out of place into the Jacobi scratch arena,
+    // with the edges and vertices, and the scratch is swapped in
+    DevMem& next = d.jacobi_scratch(level);
     d.timer_begin("coloured_gs");
-    launch_cgs_faces(t, rhs.data(level), x.data(level), d.stream());
+    const bool oop = launch_cgs_faces_cols(t, rhs.data(level), x.data(level), next.as<double>(), d.stream());
     d.timer_end();
+    d.fork();
+    if (oop) launch_cgs_ev_oop(t, x.flags(), rhs.data(level), x.data(level), next.as<double>(), d.aux_stream());
+    else launch_cgs_ev(t, x.flags(), rhs.data(level), x.data(level), d.aux_stream());
     d.join();
+    if (oop) x.arena(level).swap(next);
 }
 
 void diagonal(const Operator& A, Function& dst, int level) {
@@ -538,7 +544,7 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
     coarse_.vec = DevMem(size_t(5 * std::max<int64_t>(csr.n, 1)) * 8);
     coarse_.status = DevMem(sizeof(CoarseStatus));
     HYB_CUDA(cudaMemsetAsync(coarse_.status.as<void>(), 0, sizeof(CoarseStatus), d.stream()));
-    if (csr.n >= kCoarseGridMinRows) { // whole-GPU CG: per-CTA partials + barrier words
+    if (csr.n >= coarse_grid_min_rows()) { // whole-GPU CG: per-CTA partials + barrier words
         coarse_.grid = DevMem(size_t(4 * std::max(coarse_grid_blocks(), 1)) * 8 + 64);
         HYB_CUDA(cudaMemsetAsync(coarse_.grid.as<void>(), 0, coarse_.grid.bytes(), d.stream()));
     }

@@ -27,14 +27,20 @@ H.interpolate_random(b, L, seed=2)
 smooth = {"cgs": lambda: H.smooth_colored_gs(A, ctl, b, x, L),
           "gs": lambda: H.smooth_gs(A, ctl, b, x, L)}[which]
 dofs = dom.owned_count(L)[0]
+timer = {"cgs": "coloured_gs", "gs": "gauss_seidel", "jacobi": "jacobi"}
 for name, fn in ((which, smooth), ("jacobi", lambda: H.smooth_jacobi(A, ctl, b, x, 2.0 / 3.0, L))):
     fn()
     dom.synchronize()
+    dom.profile(True)
+    dom.timer_reset()
     dom.event_record(0)
     for _ in range(sweeps):
         fn()
     dom.event_record(1)
     dom.synchronize()
+    dom.profile(False)
     ms = dom.event_elapsed(0, 1) / sweeps
-    print(f"L{L} {name}: {ms:.3f} ms/sweep, {dofs / ms / 1e6:.1f} GDoF/s, "
-          f"{24 * dofs / ms / 1e6:.0f} GB/s algorithmic (24 B/DoF)", flush=True)
+    kms, kn = dom.timer(timer[name])
+    kms /= max(kn, 1)
+    print(f"L{L} {name}: {ms:.3f} ms/sweep (face kernel {kms:.3f} ms = {24 * dofs / kms / 1e6:.0f} GB/s), "
+          f"{dofs / ms / 1e6:.1f} GDoF/s, {24 * dofs / ms / 1e6:.0f} GB/s algorithmic (24 B/DoF)", flush=True)
