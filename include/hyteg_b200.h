@@ -42,8 +42,11 @@ enum hyb_status {
 
 /* DoF flags (include/hytegrid/field.hpp:14-21) */
 enum hyb_flag { HYB_INNER = 1, HYB_DIRICHLET = 2, HYB_NEUMANN = 4, HYB_ALL_FLAGS = 7 };
-/* forms (include/hytegrid/elements.hpp:17-25; P1 LAPLACE and MASS) */
-enum hyb_form { HYB_LAPLACE = 0, HYB_MASS = 1 };
+/* forms (include/hytegrid/elements.hpp:17-25, P1): the Laplacian, the mass
+ * matrix, the Stokes blocks DIV_* = -(q, d* u), GRAD_* = DIV_*^T and the PSPG
+ * stabilisation -h_T^2/12 (grad q, grad p) (src/elements.cpp:31-76) */
+enum hyb_form { HYB_LAPLACE = 0, HYB_MASS = 1, HYB_DIV_X = 2, HYB_DIV_Y = 3, HYB_GRAD_X = 4, HYB_GRAD_Y = 5,
+                HYB_PSPG = 6 };
 enum hyb_smoother { HYB_SMOOTH_JACOBI = 0, HYB_SMOOTH_GS = 1, HYB_SMOOTH_COLORED_GS = 2 };
 enum hyb_partitioner { HYB_PARTITION_ROUND_ROBIN = 0, HYB_PARTITION_GREEDY_EDGECUT = 1 };
 

@@ -36,7 +36,15 @@ namespace hytegrid_b200 {
 enum class DoFFlag : std::uint8_t { INNER = 1, DIRICHLET = 2, NEUMANN = 4 };
 constexpr std::uint8_t ALL_DOF_FLAGS = 7;
 inline std::uint8_t flag_bit(DoFFlag f) { return static_cast<std::uint8_t>(f); }
-enum class Form : int { LAPLACE = HYB_LAPLACE, MASS = HYB_MASS };
+enum class Form : int {
+    LAPLACE = HYB_LAPLACE,
+    MASS = HYB_MASS,
+    DIV_X = HYB_DIV_X,
+    DIV_Y = HYB_DIV_Y,
+    GRAD_X = HYB_GRAD_X,
+    GRAD_Y = HYB_GRAD_Y,
+    PSPG = HYB_PSPG
+};
 /// GridHierarchy smoother: the reference always uses its hybrid Gauss-Seidel
 /// (solvers.cpp:417, 427); weighted Jacobi and coloured GS are additions.
 enum class Smoother : int { GAUSS_SEIDEL = HYB_SMOOTH_GS, JACOBI = HYB_SMOOTH_JACOBI, COLORED_GS = HYB_SMOOTH_COLORED_GS };

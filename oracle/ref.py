@@ -57,6 +57,7 @@ def lib():
             "ref_stencil": (i, [p, u64, i, pd, C.POINTER(C.c_int)]),
             "ref_vcycle_jacobi": (i, [p, i, i, i, i, i, d, d, i, pd]),
             "ref_diagonal": (i, [p, i, i, i]),
+            "ref_set_form": (i, [p, i]),
             "ref_fill_keyed": (i, [p, i, i, u64, u64, d, d]),
             "ref_coarse_matrix": (i, [p, i, C.POINTER(i64), C.POINTER(i64), pd, i64, C.POINTER(i64)]),
             "ref_gridhierarchy_solve": (i, [p, i, i, i, d, i, i, i, pd, C.POINTER(C.c_int)]),
@@ -199,6 +200,10 @@ class RefSession:
         _ck(lib().ref_vcycle_jacobi(self.h, rhs, x, level, nu1, nu2, omega, coarse_tol, ncycles,
                                     res.ctypes.data_as(C.POINTER(C.c_double))))
         return res
+
+    def set_form(self, form):
+        """operator of `form` (0 LAPLACE .. 6 PSPG) for apply / residual / stencil"""
+        _ck(lib().ref_set_form(self.h, form))
 
     def fill_keyed(self, fi, level, seed, stream=0, lo=-1.0, hi=1.0):
         """keyed U[lo, hi] of the device generator, written in place"""

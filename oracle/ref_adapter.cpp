@@ -215,6 +215,16 @@ int ref_serialize(void* sp, int fi, uint64_t prim, uint8_t* out, int64_t cap, in
     });
 }
 
+// replace the session's operator by one of `form` (include/hytegrid/elements.hpp:17-25)
+int ref_set_form(void* sp, int form) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        if (form < 0 || form > 6) throw std::invalid_argument("ref_set_form: bad form");
+        s.A = std::make_unique<StencilOperator>(*s.dom, Form(form), FunctionKind::P1, s.min_level, s.max_level,
+                                                s.bc);
+    });
+}
+
 int ref_apply(void* sp, int src, int dst, int level, uint8_t mask) {
     return guard([&] {
         Session& s = *static_cast<Session*>(sp);

@@ -184,6 +184,7 @@ int hyb_stencil_host(const char* mesh_text, int form, int level, uint64_t id, do
         need(mesh_text, "hyb_stencil_host");
         const auto g = hyb::build_macro_graph(hyb::parse_mesh_text(mesh_text));
         if (id >= g.size()) throw hyb::OutOfRange("no primitive " + std::to_string(id));
+        if (form < HYB_LAPLACE || form > HYB_PSPG) throw hyb::InvalidArgument("hyb_stencil_host: unsupported form");
         const auto v = stencil_values(g, hyb::Form(form), level, id);
         if (len) *len = int(v.size());
         if (cap < int(v.size())) throw hyb::InvalidArgument("hyb_stencil_host: buffer too small");
@@ -199,6 +200,7 @@ int hyb_coarse_matrix_host(const char* mesh_text, int form, int level, const int
         need(nnz, "hyb_coarse_matrix_host");
         if (level < 0 || level > 12) throw hyb::OutOfRange("hyb_coarse_matrix_host: level");
         const auto g = hyb::build_macro_graph(hyb::parse_mesh_text(mesh_text));
+        if (form < HYB_LAPLACE || form > HYB_PSPG) throw hyb::InvalidArgument("hyb_coarse_matrix_host: unsupported form");
         const hyb::HostCsr m = hyb::assemble_constrained(g, hyb::Form(form), level, make_bc(bc_markers, bc_flags, n_bc));
         int64_t k = 0;
         for (int64_t r = 0; r < m.n; ++r)
@@ -544,7 +546,7 @@ int hyb_operator_create(hyb_domain* d, int form, int min_level, int max_level, c
                         const uint8_t* bc_flags, int n_bc, hyb_operator** out) {
     return guarded([&] {
         need(d, "hyb_operator_create");
-        if (form != HYB_LAPLACE && form != HYB_MASS) throw hyb::InvalidArgument("StencilOperator: unsupported form");
+        if (form < HYB_LAPLACE || form > HYB_PSPG) throw hyb::InvalidArgument("StencilOperator: unsupported form");
         auto h = std::make_unique<hyb_operator>();
         h->keep = d->d;
         h->a = std::make_unique<hyb::Operator>(*d->d, hyb::Form(form), min_level, max_level,

@@ -451,13 +451,37 @@ Elem3 p1_element(Form form, const std::array<Vec2, 3>& tri) {
     gr[2] = {-u1.y / det, u1.x / det};
     gr[0] = {-gr[1].x - gr[2].x, -gr[1].y - gr[2].y};
     Elem3 m{};
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j <= i; ++j) {
-            const double v = form == LAPLACE ? area * dot2(gr[i], gr[j]) : (i == j ? area / 6.0 : area / 12.0);
-            m.m[i][j] = v;
-            m.m[j][i] = v;
-        }
-    return m;
+    switch (form) {
+    case LAPLACE:
+    case PSPG: {
+        // PSPG: -delta h_T^2 (grad q, grad p), delta = 1/12, h_T^2 = 2|T| (elements.cpp:33-47)
+        const double s = form == LAPLACE ? area : -(1.0 / 12.0) * 2.0 * area * area;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j <= i; ++j) {
+                const double v = s * dot2(gr[i], gr[j]);
+                m.m[i][j] = v;
+                m.m[j][i] = v;
+            }
+        return m;
+    }
+    case MASS:
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) m.m[i][j] = i == j ? area / 6.0 : area / 12.0;
+        return m;
+    case DIV_X:
+    case DIV_Y: // -(q, d* u): hat integral area/3 times the constant trial derivative (:54-63)
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) m.m[i][j] = -(area / 3.0) * (form == DIV_X ? gr[j].x : gr[j].y);
+        return m;
+    case GRAD_X:
+    case GRAD_Y: { // the transpose of DIV (:64-71)
+        const Elem3 d = p1_element(form == GRAD_X ? DIV_X : DIV_Y, tri);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) m.m[i][j] = d.m[j][i];
+        return m;
+    }
+    }
+    throw InvalidArgument("local_stiffness: bad form");
 }
 
 // =====================================================================

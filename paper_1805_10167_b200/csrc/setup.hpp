@@ -163,7 +163,8 @@ struct BoundaryMap {
 };
 
 // ---------------------------------------------------------------- stencils
-enum Form : uint8_t { LAPLACE = 0, MASS = 1 };
+/// include/hytegrid/elements.hpp:17-25 (same values)
+enum Form : uint8_t { LAPLACE = 0, MASS = 1, DIV_X = 2, DIV_Y = 3, GRAD_X = 4, GRAD_Y = 5, PSPG = 6 };
 
 struct Elem3 {
     double m[3][3];

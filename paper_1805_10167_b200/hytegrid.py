@@ -34,6 +34,13 @@ SMOOTH_MASK = INNER | NEUMANN
 
 LAPLACE = 0
 MASS = 1
+DIV_X = 2
+DIV_Y = 3
+GRAD_X = 4
+GRAD_Y = 5
+PSPG = 6
+FORMS = {"LAPLACE": LAPLACE, "MASS": MASS, "DIV_X": DIV_X, "DIV_Y": DIV_Y, "GRAD_X": GRAD_X, "GRAD_Y": GRAD_Y,
+         "PSPG": PSPG}
 
 SMOOTHERS = {"jacobi": 0, "gs": 1, "colored_gs": 2}
 

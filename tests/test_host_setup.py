@@ -97,6 +97,26 @@ def test_stencils_bitwise(name):
             assert mine.shape == ref.shape and np.array_equal(mine, ref), (name, level, pid, mine, ref)
 
 
+@needs_ref
+@pytest.mark.parametrize("form", ["MASS", "DIV_X", "DIV_Y", "GRAD_X", "GRAD_Y", "PSPG"])
+@pytest.mark.parametrize("name", ["square", "annulus_perturbed", "channel32", "ring8"])
+def test_other_form_stencils_bitwise(name, form):
+    """P1 MASS, DIV_X/Y, GRAD_X/Y and PSPG stencils (src/elements.cpp:31-76,
+    src/operators.cpp:95-263) bitwise the reference's, every primitive, L0-4."""
+    mesh = STENCIL_MESHES[name]
+    nv, ne, nf = H.mesh_counts(mesh)
+    f = H.FORMS[form]
+    for level in range(0, 5):
+        s = R.RefSession(mesh, 1, level, level, 1)
+        s.set_form(f)
+        for pid in range(nv + ne + nf):
+            if nv <= pid < nv + ne and level == 0:
+                continue
+            mine = H.stencil_host(mesh, level, pid, form=f)
+            ref = s.stencil(pid, level)
+            assert mine.shape == ref.shape and np.array_equal(mine, ref), (name, form, level, pid, mine, ref)
+
+
 def test_interior_stencil_of_structured_triangle():
     # reference tests/test_operators.cpp:58-82: {4,-1,-1,-1,-1,0,0}, level independent
     mesh = H.meshgen.unit_triangle()

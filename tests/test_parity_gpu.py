@@ -430,3 +430,43 @@ def test_nccl_single_rank_communicator_path():
     assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
     assert np.array_equal(out[0][2], out[1][2])
     assert out[1][3] > 0  # graphs were replayed with the NCCL allreduce inside
+
+
+@pytest.mark.parametrize("form", ["MASS", "DIV_X", "DIV_Y", "GRAD_X", "GRAD_Y", "PSPG"])
+@pytest.mark.parametrize("mesh_name,ranks", [("square", 1), ("ring8", 2), ("channel21", 3), ("square_rev", 2)])
+@pytest.mark.parametrize("bc", [None, MIXED_BC], ids=["dirichlet", "mixed"])
+def test_apply_other_forms_bitwise(form, mesh_name, ranks, bc):
+    """apply(A, ...) of the P1 MASS, DIV_X/Y, GRAD_X/Y and PSPG operators
+    (src/elements.cpp:31-76) bitwise the reference's, every mask, L0-5; and
+    r = b - A x for the same operator."""
+    mesh = FIXTURES[mesh_name]()
+    f = H.FORMS[form]
+    for level in range(0, 6):
+        rig = Rig(mesh, ranks, level, level, 3, bc)
+        rig.A = H.StencilOperator(rig.dom, f, level, level, bc)
+        rig.ref.set_form(f)
+        rig.rand(0, level, seed=1)
+        rig.rand(1, level, seed=5)
+        for mask in (H.ALL_DOF_FLAGS, H.DIRICHLET, H.SMOOTH_MASK):
+            H.apply(rig.A, rig.ctl, rig.f[0], rig.f[1], level, mask)
+            rig.ref.apply(0, 1, level, mask)
+            assert_same(rig, 1, level, f"{form} apply L{level} mask {mask}")
+        rig.rand(2, level, seed=6)
+        H.residual(rig.A, rig.ctl, rig.f[2], rig.f[0], rig.f[1], level)
+        rig.ref.residual(2, 0, 1, level)
+        assert_same(rig, 1, level, f"{form} residual L{level}")
+
+
+@pytest.mark.parametrize("form", ["DIV_X", "GRAD_Y", "PSPG"])
+def test_apply_other_forms_perturbed_annulus_level7(form):
+    """non-right-angled faces (config 3 family) at level 7: the face kernel's
+    full column blocks with all seven couplings of the non-symmetric stencils"""
+    mesh = H.meshgen.perturb(H.meshgen.annulus(16, 4, 1.0, 2.0), 0.1, 2)
+    f = H.FORMS[form]
+    rig = Rig(mesh, 2, 7, 7, 2)
+    rig.A = H.StencilOperator(rig.dom, f, 7, 7)
+    rig.ref.set_form(f)
+    rig.rand(0, 7, seed=3)
+    H.apply(rig.A, rig.ctl, rig.f[0], rig.f[1], 7)
+    rig.ref.apply(0, 1, 7)
+    assert_same(rig, 1, 7, f"{form} apply annulus L7")
