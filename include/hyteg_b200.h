@@ -195,6 +195,21 @@ int hyb_interpolate_random(hyb_function* f, int level, uint64_t seed, uint64_t s
 int hyb_interpolate_expr(hyb_function* f, int level, int kind, const double* params, int nparams, uint8_t mask);
 /* sync / sync_all (function.hpp:79-81): full schedule V->E, E->F, F->E, E->V */
 int hyb_sync(hyb_function* f, int level);
+/* sync(c, f, level, span<Direction>) (function.hpp:79-80, communication.hpp:48-49):
+ * the listed relay directions in order, with the reference's Direction values
+ * (transport.hpp:19-26) HYB_V2E 0, HYB_E2F 1, HYB_F2E 2, HYB_E2V 3; each copies
+ * the sender's current slots exactly as FieldPackInfo::pack/unpack does
+ * (src/communication.cpp:272-403). Other values: HYB_INVALID_ARGUMENT. */
+enum hyb_direction { HYB_V2E = 0, HYB_E2F = 1, HYB_F2E = 2, HYB_E2V = 3 };
+int hyb_sync_directions(hyb_function* f, int level, const int* dirs, int n);
+/* values(id, level) (function.hpp:37-39): the primitive's slots in the
+ * reference's layout (face closed triangle row-major; edge line (n+1), then
+ * per face halo rows 0 (n+1) and 1 (n); vertex own + one ghost per edge) as
+ * they are now, no refresh. An edge's halo row 0 is not stored on the device
+ * (no P1 operation reads it): it is reported as the edge's line. out == NULL:
+ * size query. set_values writes every slot (halo row 0 ignored). */
+int hyb_function_values(hyb_function* f, uint64_t prim, int level, double* out, int64_t cap, int64_t* len);
+int hyb_function_set_values(hyb_function* f, uint64_t prim, int level, const double* in, int64_t n);
 
 /* ---- operators ------------------------------------------------------------
  * StencilOperator(domain, form, P1, min, max, bc) (operators.hpp:76-88).

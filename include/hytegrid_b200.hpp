@@ -227,6 +227,15 @@ inline void interpolate(ScalarFunction& f, const Expr& e, int level, std::uint8_
     check(hyb_interpolate_expr(f.handle(), level, e.kind, e.params.data(), int(e.params.size()), mask));
 }
 inline void sync_all(Controller&, const ScalarFunction& f, int level) { check(hyb_sync(f.handle(), level)); }
+/// the reference's Direction (transport.hpp:19-26)
+enum class Direction : int { VERTEX_TO_EDGE = HYB_V2E, EDGE_TO_FACE = HYB_E2F, FACE_TO_EDGE = HYB_F2E,
+                             EDGE_TO_VERTEX = HYB_E2V };
+/// sync(c, f, level, span<Direction>) (function.hpp:79-80): the directions in order
+inline void sync(Controller&, const ScalarFunction& f, int level, const std::vector<Direction>& dirs) {
+    std::vector<int> d;
+    for (Direction x : dirs) d.push_back(int(x));
+    check(hyb_sync_directions(f.handle(), level, d.data(), int(d.size())));
+}
 inline void apply(const StencilOperator& A, Controller&, const ScalarFunction& src, ScalarFunction& dst, int level,
                   std::uint8_t mask = ALL_DOF_FLAGS) {
     check(hyb_apply(A.handle(), src.handle(), dst.handle(), level, mask));

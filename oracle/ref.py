@@ -58,6 +58,9 @@ def lib():
             "ref_vcycle_jacobi": (i, [p, i, i, i, i, i, d, d, i, pd]),
             "ref_diagonal": (i, [p, i, i, i]),
             "ref_set_form": (i, [p, i]),
+            "ref_sync_dirs": (i, [p, i, i, C.POINTER(C.c_int), i]),
+            "ref_values": (i, [p, i, u64, i, pd, i64, C.POINTER(i64)]),
+            "ref_set_values": (i, [p, i, u64, i, pd, i64]),
             "ref_fill_keyed": (i, [p, i, i, u64, u64, d, d]),
             "ref_coarse_matrix": (i, [p, i, C.POINTER(i64), C.POINTER(i64), pd, i64, C.POINTER(i64)]),
             "ref_gridhierarchy_solve": (i, [p, i, i, i, d, i, i, i, pd, C.POINTER(C.c_int)]),
@@ -200,6 +203,22 @@ class RefSession:
         _ck(lib().ref_vcycle_jacobi(self.h, rhs, x, level, nu1, nu2, omega, coarse_tol, ncycles,
                                     res.ctypes.data_as(C.POINTER(C.c_double))))
         return res
+
+    def sync_dirs(self, fi, level, dirs):
+        d = (C.c_int * max(len(dirs), 1))(*dirs)
+        _ck(lib().ref_sync_dirs(self.h, fi, level, d, len(dirs)))
+
+    def values(self, fi, prim, level):
+        n = C.c_int64()
+        _ck(lib().ref_values(self.h, fi, prim, level, None, 0, C.byref(n)))
+        out = np.zeros(n.value)
+        _ck(lib().ref_values(self.h, fi, prim, level, out.ctypes.data_as(C.POINTER(C.c_double)), n.value,
+                             C.byref(n)))
+        return out
+
+    def set_values(self, fi, prim, level, v):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        _ck(lib().ref_set_values(self.h, fi, prim, level, v.ctypes.data_as(C.POINTER(C.c_double)), v.size))
 
     def set_form(self, form):
         """operator of `form` (0 LAPLACE .. 6 PSPG) for apply / residual / stencil"""

@@ -201,6 +201,34 @@ int ref_sync(void* sp, int fi, int level) {
     });
 }
 
+// sync(c, f, level, directions) (src/function.cpp:234-237)
+int ref_sync_dirs(void* sp, int fi, int level, const int* dirs, int n) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        std::vector<Direction> d;
+        for (int i = 0; i < n; ++i) d.push_back(Direction(dirs[i]));
+        sync(*s.ctl, *s.f.at(size_t(fi)), level, std::span<const Direction>(d));
+    });
+}
+
+// values(id, level): the primitive's raw slots; set writes them
+int ref_values(void* sp, int fi, uint64_t prim, int level, double* out, int64_t cap, int64_t* len) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        auto& v = s.f.at(size_t(fi))->values(PrimitiveID{prim}, level);
+        *len = int64_t(v.size());
+        if (out && cap >= int64_t(v.size())) std::memcpy(out, v.data(), v.size() * 8);
+    });
+}
+int ref_set_values(void* sp, int fi, uint64_t prim, int level, const double* in, int64_t n) {
+    return guard([&] {
+        Session& s = *static_cast<Session*>(sp);
+        auto& v = s.f.at(size_t(fi))->values(PrimitiveID{prim}, level);
+        if (int64_t(v.size()) != n) throw std::invalid_argument("ref_set_values: size");
+        std::memcpy(v.data(), in, size_t(n) * 8);
+    });
+}
+
 // The reference's own DataCallbacks::serialize of one primitive's field data
 // (src/field.cpp:157-166): the checkpoint / migration byte format.
 int ref_serialize(void* sp, int fi, uint64_t prim, uint8_t* out, int64_t cap, int64_t* len) {

@@ -105,6 +105,9 @@ _SIGS = {
     "hyb_interpolate_random": (_i, [_p, _i, _u64, _u64, _d, _d, _u8]),
     "hyb_interpolate_expr": (_i, [_p, _i, _i, _p, _i, _u8]),
     "hyb_sync": (_i, [_p, _i]),
+    "hyb_sync_directions": (_i, [_p, _i, C.POINTER(_i), _i]),
+    "hyb_function_values": (_i, [_p, _u64, _i, _pd, _i64, _pi64]),
+    "hyb_function_set_values": (_i, [_p, _u64, _i, _pd, _i64]),
     "hyb_operator_create": (_i, [_p, _i, _i, _i, _pi32, _pu8, _i, C.POINTER(_p)]),
     "hyb_operator_destroy": (_i, [_p]),
     "hyb_operator_stencil": (_i, [_p, _i, _u64, _pd, _i, C.POINTER(_i)]),

@@ -542,6 +542,34 @@ int hyb_sync(hyb_function* f, int level) {
     });
 }
 
+int hyb_sync_directions(hyb_function* f, int level, const int* dirs, int n) {
+    return guarded([&] {
+        need(f, "hyb_sync_directions");
+        if (n < 0 || (n > 0 && !dirs)) throw hyb::InvalidArgument("hyb_sync_directions: bad direction list");
+        f->f->domain().sync_directions(*f->f, level, dirs, n);
+    });
+}
+
+int hyb_function_values(hyb_function* f, uint64_t prim, int level, double* out, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        need(f, "hyb_function_values");
+        const std::vector<double> v = hyb::primitive_values(*f->f, prim, level);
+        if (len) *len = int64_t(v.size());
+        if (!out) return;
+        if (cap < int64_t(v.size())) throw hyb::InvalidArgument("hyb_function_values: buffer too small");
+        std::memcpy(out, v.data(), v.size() * 8);
+    });
+}
+
+int hyb_function_set_values(hyb_function* f, uint64_t prim, int level, const double* in, int64_t n) {
+    return guarded([&] {
+        need(f, "hyb_function_set_values");
+        need(in, "hyb_function_set_values");
+        if (n < 0) throw hyb::InvalidArgument("hyb_function_set_values: negative length");
+        hyb::set_primitive_values(*f->f, prim, level, in, size_t(n));
+    });
+}
+
 int hyb_operator_create(hyb_domain* d, int form, int min_level, int max_level, const int32_t* bc_markers,
                         const uint8_t* bc_flags, int n_bc, hyb_operator** out) {
     return guarded([&] {

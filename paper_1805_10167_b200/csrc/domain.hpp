@@ -68,6 +68,8 @@ struct LevelGeom {
     DevMem rowoff, edge_off, edge_nf, vtx_off, vtx_ne, vtx_coef_off, face_gid, edge_gid, vtx_gid;
     std::vector<int64_t> h_rowoff, h_edge_off, h_vtx_off;
     Exchange xch;
+    Exchange xdir[4];            // one relay direction each (sync_directions), built on first use
+    bool xdir_built[4] = {false, false, false, false};
     int64_t send_size = 0, recv_size = 0;
 };
 
@@ -164,6 +166,9 @@ class Domain {
 
     // ghost exchange of one function, full schedule V->E, E->F, F->E, E->V
     void sync(Function& f, int level);
+    // the reference's sync(c, f, level, span<Direction>) (src/function.cpp:234-237):
+    // the given relay directions (0 V->E, 1 E->F, 2 F->E, 3 E->V) in order
+    void sync_directions(Function& f, int level, const int* dirs, int n);
 
     // scratch
     DevMem& jacobi_scratch(int level);
@@ -234,6 +239,7 @@ class Domain {
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     cudaEvent_t events_[16] = {};
     void build_exchange(LevelGeom& lg, const HostLayout& lay);
+    void run_exchange(Exchange& X, double* arena);
 
     MacroGraph g_;
     int world_;
@@ -291,6 +297,9 @@ void download_async(Function& f, int level, double* host, int64_t n);
 /// one primitive's record in the reference's DataCallbacks::serialize format
 /// (src/field.cpp:157-175), taken after a ghost refresh of every level
 std::vector<uint8_t> serialize_field(Function& f, uint64_t id);
+/// values(id, level) without a refresh, and its inverse (reference layout of the primitive)
+std::vector<double> primitive_values(Function& f, uint64_t id, int level);
+void set_primitive_values(Function& f, uint64_t id, int level, const double* v, size_t n);
 /// inverse: values of the primitive's slots from such a record (levels, sizes
 /// and flags must match this function)
 void deserialize_field(Function& f, uint64_t id, const uint8_t* data, size_t len);

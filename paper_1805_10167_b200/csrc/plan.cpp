@@ -148,8 +148,70 @@ bool relevant(const MacroGraph& g, const Placement& p, uint64_t id) {
 
 } // namespace
 
+// The ghosts ONE relay direction writes, each from the sender's own storage
+// (FieldPackInfo::pack / unpack, src/communication.cpp:272-403):
+//   0 V->E  edge line ends <- the vertex values
+//   1 E->F  face border <- the edge line (its ends included), walk-oriented;
+//           a corner lies on two borders and keeps the later slot's value
+//           (unpack in slot order 0, 1, 2): (0,0) from slot 1, (n,0) and
+//           (0,n) from slot 2
+//   2 F->E  edge halo row 1 <- the face lattice (halo row 0 is not stored)
+//   3 E->V  vertex ghost <- the edge's line DoF next to the vertex (its far
+//           end at level 0)
+template <class Emit>
+void emit_direction(const MacroGraph& g, const HostLayout& lay, const Placement& p, uint64_t id, bool rl, int li,
+                    int dir, Emit& emit) {
+    (void)p;
+    const int n = lay.n, W = lay.W;
+    switch (g.kind_of(id)) {
+    case FACE: {
+        if (dir != 1) return;
+        const MacroFace& f = g.faces[g.face_index(id)];
+        const int64_t fb = rl ? int64_t(li) * lay.face_stride : 0;
+        for (int s = 0; s < 3; ++s) {
+            const int w0 = s == 0 ? 1 : 0, w1 = s == 1 ? n - 1 : (s == 0 ? n - 1 : n);
+            for (int w = w0; w <= w1; ++w) {
+                const int c = s == 0 ? w : (s == 1 ? 0 : W - 1 - w), r = s == 0 ? 0 : w;
+                const int k = f.aligned[size_t(s)] ? w : n - w;
+                emit(id, rl ? fb + lay.rowoff[size_t(r)] + c : -1, OwnerSlot{f.e[size_t(s)], k, 0});
+            }
+        }
+        return;
+    }
+    case EDGE: {
+        const MacroEdge& e = g.edges[g.edge_index(id)];
+        const int64_t eb = rl ? lay.edge_off[size_t(li)] : 0;
+        if (dir == 0) {
+            emit(id, rl ? eb : -1, OwnerSlot{e.v[0], 0, 0});
+            emit(id, rl ? eb + n : -1, OwnerSlot{e.v[1], 0, 0});
+        } else if (dir == 2) {
+            for (size_t j = 0; j < e.faces.size(); ++j) {
+                const FaceSide& fs = e.faces[j];
+                for (int q = 0; q < n; ++q) {
+                    const int w = fs.aligned ? q : n - 1 - q;
+                    const int c = fs.slot == 0 ? w : (fs.slot == 1 ? 1 : W - 2 - w);
+                    const int r = fs.slot == 0 ? 1 : w;
+                    emit(id, rl ? eb + (n + 1) + int64_t(j) * n + q : -1, OwnerSlot{fs.face, c, r});
+                }
+            }
+        }
+        return;
+    }
+    case VERTEX: {
+        if (dir != 3) return;
+        const MacroVertex& v = g.vertices[id];
+        const int64_t vb = rl ? lay.vtx_off[size_t(li)] : 0;
+        for (size_t j = 0; j < v.edges.size(); ++j) {
+            const MacroEdge& e = g.edges[g.edge_index(v.edges[j])];
+            emit(id, rl ? vb + 1 + int64_t(j) : -1, OwnerSlot{v.edges[j], e.v[0] == id ? 1 : n - 1, 0});
+        }
+        return;
+    }
+    }
+}
+
 HostExchange plan_exchange(const MacroGraph& g, const std::vector<int>& rank_of, const std::vector<int>& local_ranks,
-                           const Placement& p, const HostLayout& lay) {
+                           const Placement& p, const HostLayout& lay, int direction) {
     const int n = lay.n, W = lay.W;
     auto is_local = [&](int r) { return std::find(local_ranks.begin(), local_ranks.end(), r) != local_ranks.end(); };
     auto pos_of = [&](const OwnerSlot& o) -> int64_t {
@@ -169,6 +231,15 @@ HostExchange plan_exchange(const MacroGraph& g, const std::vector<int>& rank_of,
     };
     std::map<std::pair<int, int>, Lists> blocks;
 
+    // o: the source slot -- the owner (full refresh) or the relaying sender's
+    // storage (one direction); its owner's global index for the tests
+    auto gidx_of = [&](const OwnerSlot& o) {
+        switch (g.kind_of(o.prim)) {
+        case EDGE: return global_owned_index(g, resolve_edge(g, o.prim, o.c, n), n);
+        case FACE: return global_owned_index(g, resolve_face(g, o.prim, o.c, o.r, n), n);
+        default: return global_owned_index(g, o, n);
+        }
+    };
     auto emit = [&](uint64_t rcv, int64_t dst, const OwnerSlot& o) {
         const int rq = rank_of[size_t(rcv)], rs = rank_of[size_t(o.prim)];
         const bool rl = is_local(rq), sl = is_local(rs);
@@ -176,7 +247,7 @@ HostExchange plan_exchange(const MacroGraph& g, const std::vector<int>& rank_of,
             if (rl) {
                 X.dst.push_back(dst);
                 X.src.push_back(pos_of(o));
-                lgid.push_back(global_owned_index(g, o, n));
+                lgid.push_back(gidx_of(o));
             }
             return;
         }
@@ -186,7 +257,7 @@ HostExchange plan_exchange(const MacroGraph& g, const std::vector<int>& rank_of,
         if (sl) b.send_src.push_back(pos_of(o));
         if (rl) {
             b.recv_dst.push_back(dst);
-            b.recv_gidx.push_back(global_owned_index(g, o, n));
+            b.recv_gidx.push_back(gidx_of(o));
         }
     };
 
@@ -194,6 +265,10 @@ HostExchange plan_exchange(const MacroGraph& g, const std::vector<int>& rank_of,
         if (!relevant(g, p, id)) continue;
         const int li = p.lidx[size_t(id)];
         const bool rl = li >= 0;
+        if (direction >= 0) { // one relay direction (reference Controller::sync, src/communication.cpp:126-173)
+            emit_direction(g, lay, p, id, rl, li, direction, emit);
+            continue;
+        }
         switch (g.kind_of(id)) {
         case FACE: {
             const int64_t fb = rl ? int64_t(li) * lay.face_stride : 0;

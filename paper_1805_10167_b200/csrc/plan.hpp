@@ -57,8 +57,11 @@ struct HostExchange {
     std::vector<ExBlock> inproc, sends, recvs;
     int64_t send_size = 0, recv_size = 0;
 };
+/// direction -1: the one-round refresh (every ghost from its owner); 0..3:
+/// one relay direction of the reference (V->E, E->F, F->E, E->V), every ghost
+/// it writes from the sender's own storage (see emit_direction in plan.cpp)
 HostExchange plan_exchange(const MacroGraph& g, const std::vector<int>& rank_of, const std::vector<int>& local_ranks,
-                           const Placement& p, const HostLayout& lay);
+                           const Placement& p, const HostLayout& lay, int direction = -1);
 
 /// Arena slot / global index of each local owned DoF, in local packed order.
 std::vector<int64_t> owned_positions(const MacroGraph& g, const Placement& p, const HostLayout& lay);

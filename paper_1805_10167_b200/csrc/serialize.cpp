@@ -253,4 +253,66 @@ void deserialize_field(Function& f, uint64_t id, const uint8_t* data, size_t len
     if (rd.at != len) throw InvalidArgument("deserialize: trailing bytes after the record");
 }
 
+// values(id, level) (include/hytegrid/function.hpp:37-39): the primitive's
+// reference-layout slots as they are now -- no refresh. An edge's halo row 0
+// is not stored on the device (no P1 kernel reads it) and is reported as the
+// edge's own line, its value after every full sync.
+std::vector<double> primitive_values(Function& f, uint64_t id, int level) {
+    Domain& d = f.domain();
+    f.check_level(level, "values");
+    const int li = local_of(d, id, "values");
+    const Block bl = block_of(d, d.graph().kind_of(id), li, level);
+    std::vector<double> blk(size_t(bl.len)), vals;
+    std::vector<uint8_t> flags;
+    HYB_CUDA(cudaMemcpyAsync(blk.data(), f.data(level) + bl.off, size_t(bl.len) * 8, cudaMemcpyDeviceToHost,
+                             d.stream()));
+    HYB_CUDA(cudaStreamSynchronize(d.stream()));
+    reference_record(d, f.bc(), id, level, d.level(level), blk, vals, flags);
+    return vals;
+}
+
+// writes every slot of the primitive's reference layout (an edge's halo row 0
+// is ignored: not stored)
+void set_primitive_values(Function& f, uint64_t id, int level, const double* v, size_t n_in) {
+    Domain& d = f.domain();
+    f.check_level(level, "values");
+    const int li = local_of(d, id, "values");
+    const Kind kind = d.graph().kind_of(id);
+    const Block bl = block_of(d, kind, li, level);
+    std::vector<double> blk(size_t(bl.len)), want;
+    std::vector<uint8_t> flags;
+    HYB_CUDA(cudaMemcpyAsync(blk.data(), f.data(level) + bl.off, size_t(bl.len) * 8, cudaMemcpyDeviceToHost,
+                             d.stream()));
+    HYB_CUDA(cudaStreamSynchronize(d.stream()));
+    reference_record(d, f.bc(), id, level, d.level(level), blk, want, flags);
+    if (n_in != want.size())
+        throw InvalidArgument("values: primitive " + std::to_string(id) + " holds " + std::to_string(want.size()) +
+                              " slots at level " + std::to_string(level) + ", got " + std::to_string(n_in));
+    const int n = 1 << level;
+    const MacroGraph& g = d.graph();
+    const LevelGeom& lg = d.level(level);
+    size_t pos = 0;
+    switch (kind) {
+    case FACE:
+        for (int r = 0; r <= n; ++r)
+            for (int c = 0; c + r <= n; ++c) blk[size_t(lg.h_rowoff[size_t(r)] + c)] = v[pos++];
+        break;
+    case EDGE: {
+        const size_t nf = g.edges[g.edge_index(id)].faces.size();
+        for (int k = 0; k <= n; ++k) blk[size_t(k)] = v[pos++];
+        for (size_t j = 0; j < nf; ++j) {
+            pos += size_t(n + 1);
+            for (int q = 0; q < n; ++q) blk[size_t(n + 1) + j * size_t(n) + size_t(q)] = v[pos++];
+        }
+        break;
+    }
+    case VERTEX:
+        for (size_t k = 0; k < blk.size(); ++k) blk[k] = v[k];
+        break;
+    }
+    HYB_CUDA(cudaMemcpyAsync(f.data(level) + bl.off, blk.data(), size_t(bl.len) * 8, cudaMemcpyHostToDevice,
+                             d.stream()));
+    HYB_CUDA(cudaStreamSynchronize(d.stream()));
+}
+
 } // namespace hyb

@@ -340,6 +340,20 @@ class ScalarFunction:
         buf = np.frombuffer(bytes(record), dtype=np.uint8).copy()
         check(lib.hyb_function_deserialize(self._h, prim, buf.ctypes.data_as(C.POINTER(C.c_uint8)), buf.size))
 
+    def values(self, prim: int, level: int) -> np.ndarray:
+        """values(id, level) (function.hpp:37-39) without a refresh: the
+        primitive's slots in the reference layout (an edge's halo row 0, not
+        stored on the device, reads as the edge's line)."""
+        n = C.c_int64(0)
+        check(lib.hyb_function_values(self._h, prim, level, None, 0, C.byref(n)))
+        out = np.zeros(n.value)
+        check(lib.hyb_function_values(self._h, prim, level, _pd(out), out.size, C.byref(n)))
+        return out
+
+    def set_values(self, prim: int, level: int, v) -> None:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        check(lib.hyb_function_set_values(self._h, prim, level, _pd(v), v.size))
+
     def flags(self, level: int, global_order: bool = True) -> np.ndarray:
         n = self._n(level, global_order)
         out = np.zeros(n, dtype=np.uint8)
@@ -404,6 +418,18 @@ def interpolate_random(f: ScalarFunction, level: int, seed: int, stream: int = 0
 
 def sync_all(ctl: Controller, f: ScalarFunction, level: int) -> None:  # noqa: ARG001
     check(lib.hyb_sync(f._h, level))
+
+
+# reference Direction (transport.hpp:19-26)
+VERTEX_TO_EDGE, EDGE_TO_FACE, FACE_TO_EDGE, EDGE_TO_VERTEX = 0, 1, 2, 3
+FULL_SYNC_SCHEDULE = (VERTEX_TO_EDGE, EDGE_TO_FACE, FACE_TO_EDGE, EDGE_TO_VERTEX)
+
+
+def sync(ctl: Controller, f: ScalarFunction, level: int, directions) -> None:  # noqa: ARG001
+    """sync(c, f, level, span<Direction>) (src/function.cpp:234-237): the given
+    relay directions in order, each exactly as the reference's pack/unpack."""
+    d = (C.c_int * max(len(directions), 1))(*[int(x) for x in directions])
+    check(lib.hyb_sync_directions(f._h, level, d, len(directions)))
 
 
 def apply(A: StencilOperator, ctl: Controller, src: ScalarFunction, dst: ScalarFunction, level: int,  # noqa: ARG001

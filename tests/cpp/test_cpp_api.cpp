@@ -64,6 +64,9 @@ int main() {
     for (size_t i = 0; i < xs.size(); ++i)
         err = std::fmax(err, std::fabs(xs[i] - (1.5 + 2.0 * xy[2 * i] - 0.75 * xy[2 * i + 1])));
     EXPECT(err <= 1e-10);
+    // partial-direction sync in the reference's full order == sync_all (function.hpp:79-81)
+    sync(c2, x, level, {Direction::VERTEX_TO_EDGE, Direction::EDGE_TO_FACE, Direction::FACE_TO_EDGE,
+                        Direction::EDGE_TO_VERTEX});
     // the exact solution is a fixed point of the reference's GS sweep (tests/test_operators.cpp:287-310)
     StencilOperator As(sq, Form::LAPLACE, level, level);
     smooth_gs(As, c2, rhs, x, level);
