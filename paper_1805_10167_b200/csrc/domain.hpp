@@ -265,6 +265,8 @@ void residual(const Operator& A, Function& rhs, Function& x, Function& r, int le
 void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level, double* dotp = nullptr);
 /// dst = A src (all flags) and returns src.dst, one pass over the faces
 double apply_dot(const Operator& A, Function& src, Function& dst, int level);
+/// the same with src.dst left on the device at *out (no host round trip)
+void apply_dot_dev(const Operator& A, Function& src, Function& dst, int level, double* out);
 /// prolongate_add(e -> x) then one weighted-Jacobi sweep, fused on the faces
 void prolongate_add_jacobi(const Operator& A, Function& e, Function& rhs, Function& x, double omega, int coarse_level,
                            double* dotp = nullptr);
@@ -287,7 +289,11 @@ void fill_random(Function& f, int level, uint64_t seed, uint64_t stream, double 
 void fill_expr(Function& f, int level, const Expr& e, uint8_t mask);
 /// PCG update: x += alpha p, r -= alpha ap, returns r.r (bitwise the unfused ops)
 double pcg_update(Function& x, Function& p, Function& r, Function& ap, double alpha, int level);
+/// device-scalar forms: alpha read from alpha_dev when set, r.r / a.b written to device memory
+void pcg_update_dev(Function& x, Function& p, Function& r, Function& ap, double alpha, const double* alpha_dev,
+                    int level, double* rr_out);
 double dot(Function& a, Function& b, int level);
+void dot_dev(Function& a, Function& b, int level, double* out);
 double max_abs(Function& a, int level);
 void upload(Function& f, int level, const double* host, int64_t n, bool global_order, uint8_t mask);
 void download(Function& f, int level, double* host, int64_t n, bool global_order);
@@ -356,6 +362,7 @@ class Hierarchy {
     Operator a_;
     Function r_, b_, e_; // b_, e_ (coarse rhs/correction) stop one level below max
     std::unique_ptr<Function> pcg_r_, pcg_z_, pcg_p_; // PCG vectors at one level (Ap lives in r_)
+    DevMem pcg_s_, pcg_res_;                          // PCG's device scalars and residual history
     // PCG's r.z from the cycle's last post-smoothing sweep at cycle_dot_level_
     DevMem dot_scratch_;
     double* cycle_dot_ = nullptr;

@@ -253,8 +253,13 @@ __device__ __forceinline__ double blas_op(int op, double alpha, double a, double
     return alpha;
 }
 
+// DevScalars: alpha = sa * *pa / beta = *pb when the pointers are set (scalars
+// computed on the device, e.g. PCG's alpha and beta: no host round trip)
 __global__ void __launch_bounds__(256) k_blas1_faces(int op, int64_t n2, double alpha, const double2* __restrict__ x1,
-                                                     double beta, const double2* __restrict__ x2, double2* dst) {
+                                                     double beta, const double2* __restrict__ x2, double2* dst,
+                                                     DevScalars ds) {
+    if (ds.pa) alpha = ds.sa * *ds.pa;
+    if (ds.pb) beta = *ds.pb;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
         const double2 a = op != 2 ? x1[i] : make_double2(0, 0);
         const double2 b = op == 0 ? x2[i] : make_double2(0, 0);
@@ -266,7 +271,9 @@ __global__ void __launch_bounds__(256) k_blas1_faces(int op, int64_t n2, double 
 __global__ void __launch_bounds__(128) k_blas1_ev(int op, LevelTables t, FlagTables fl, double alpha,
                                                   const double* __restrict__ x1, double beta,
                                                   const double* __restrict__ x2, double* dst, uint8_t mask,
-                                                  int kblocks) {
+                                                  int kblocks, DevScalars ds = DevScalars{}) {
+    if (ds.pa) alpha = ds.sa * *ds.pa;
+    if (ds.pb) beta = *ds.pb;
     const int n = t.n;
     const int eblocks = t.nedges * kblocks;
     int64_t i;
@@ -445,7 +452,11 @@ __global__ void __launch_bounds__(256) k_partials_faces(LevelTables t, const dou
 __global__ void __launch_bounds__(256) k_pcg_update_faces(LevelTables t, double* __restrict__ x,
                                                           const double* __restrict__ p, double* __restrict__ r,
                                                           const double* __restrict__ ap, double alpha, double nalpha,
-                                                          double* scratch, int bands) {
+                                                          double* scratch, int bands, const double* alpha_p) {
+    if (alpha_p) {
+        alpha = *alpha_p;
+        nalpha = -alpha;
+    }
     __shared__ double sh[256];
     const int n = t.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -924,19 +935,19 @@ void launch_restrict_ev(const LevelTables& tc, const LevelTables& tf, const Flag
 }
 
 void launch_blas1(int op, const LevelTables& t, const FlagTables& fl, double alpha, const double* x1, double beta,
-                  const double* x2, double* dst, uint8_t mask, cudaStream_t st) {
+                  const double* x2, double* dst, uint8_t mask, cudaStream_t st, DevScalars ds) {
     if ((mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
         const int64_t n2 = t.faces_size / 2;
         const int64_t want = (n2 + 255) / 256;
         const int grid = int(want < 148 * 16 ? want : 148 * 16);
         k_blas1_faces<<<grid, 256, 0, st>>>(op, n2, alpha, reinterpret_cast<const double2*>(x1), beta,
-                                            reinterpret_cast<const double2*>(x2), reinterpret_cast<double2*>(dst));
+                                            reinterpret_cast<const double2*>(x2), reinterpret_cast<double2*>(dst), ds);
         check_launch("blas1 faces");
     }
     const int kb = kblocks_for(t.n);
     const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
     if (blocks > 0) {
-        k_blas1_ev<<<blocks, 128, 0, st>>>(op, t, fl, alpha, x1, beta, x2, dst, mask, kb);
+        k_blas1_ev<<<blocks, 128, 0, st>>>(op, t, fl, alpha, x1, beta, x2, dst, mask, kb, ds);
         check_launch("blas1 edges/vertices");
     }
 }
@@ -1063,18 +1074,22 @@ void launch_partials(int op, const LevelTables& t, const double* x1, const doubl
 }
 
 void launch_pcg_update(const LevelTables& t, const FlagTables& fl, double* x, const double* p, double* r,
-                       const double* ap, double alpha, double* part, double* scratch, cudaStream_t st) {
+                       const double* ap, double alpha, double* part, double* scratch, cudaStream_t st,
+                       const double* alpha_p) {
     const int bands = t.n >= 3 ? (t.n - 2 + PB - 1) / PB : 0;
     if (t.nfaces > 0 && bands > 0) {
         k_pcg_update_faces<<<dim3(unsigned(bands), unsigned(t.nfaces)), 256, 0, st>>>(t, x, p, r, ap, alpha, -alpha,
-                                                                                    scratch, bands);
+                                                                                    scratch, bands, alpha_p);
         check_launch("pcg update faces");
     }
     const int kb = kblocks_for(t.n);
     const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
     if (blocks > 0) { // edges / vertices: add_scaled as usual
-        k_blas1_ev<<<blocks, 128, 0, st>>>(1, t, fl, alpha, p, 0.0, p, x, F_ALL, kb);
-        k_blas1_ev<<<blocks, 128, 0, st>>>(1, t, fl, -alpha, ap, 0.0, ap, r, F_ALL, kb);
+        DevScalars up, dn;
+        up.pa = dn.pa = alpha_p;
+        dn.sa = -1.0;
+        k_blas1_ev<<<blocks, 128, 0, st>>>(1, t, fl, alpha, p, 0.0, p, x, F_ALL, kb, up);
+        k_blas1_ev<<<blocks, 128, 0, st>>>(1, t, fl, -alpha, ap, 0.0, ap, r, F_ALL, kb, dn);
         check_launch("pcg update edges/vertices");
     }
     const int warps = (t.nfaces + 31) / 32 + t.nedges + (t.nverts + 31) / 32;
@@ -1082,6 +1097,26 @@ void launch_pcg_update(const LevelTables& t, const FlagTables& fl, double* x, co
         k_partials_finish<0><<<(warps + 3) / 4, 128, 0, st>>>(t, r, r, scratch, bands, part);
         check_launch("partials finish");
     }
+}
+
+// PCG's scalar recurrence on the device (cg_solve, src/solvers.cpp:238-255):
+// stage 0: alpha = rz / pAp (pAp <= 0 sets the breakdown flag);
+// stage 1: beta = rz_new / rz, rz = rz_new, res[k] = sqrt(r.r)
+__global__ void k_pcg_scalars(int stage, PcgScalars* s, double* res, int k) {
+    if (threadIdx.x != 0) return;
+    if (stage == 0) {
+        if (!(s->pap > 0.0) && s->bad == 0.0) s->bad = double(k) + 1.0;
+        s->alpha = s->rz / s->pap;
+    } else {
+        s->beta = s->rz_new / s->rz;
+        s->rz = s->rz_new;
+        res[k] = sqrt(s->rr);
+    }
+}
+
+void launch_pcg_scalars(int stage, PcgScalars* s, double* res, int k, cudaStream_t st) {
+    k_pcg_scalars<<<1, 32, 0, st>>>(stage, s, res, k);
+    check_launch("pcg scalars");
 }
 
 void launch_combine_tree(int op, double* v, int64_t len, double* out, cudaStream_t st) {

@@ -141,8 +141,19 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
 void launch_cgs_ev_oop(const LevelTables& t, const FlagTables& fl, const double* b, const double* x, double* y,
                        cudaStream_t st);
 // dst := alpha*x1 + beta*x2 (op 0), dst += alpha*x1 (op 1), dst := alpha (op 2)
+/// scalars read on the device at launch time: alpha = sa * *pa, beta = *pb (unset: the host values)
+struct DevScalars {
+    const double* pa = nullptr;
+    double sa = 1.0;
+    const double* pb = nullptr;
+};
+/// PCG's device-resident scalars (Hierarchy::pcg)
+struct PcgScalars {
+    double rz, pap, alpha, rz_new, rr, beta, bad;
+};
+void launch_pcg_scalars(int stage, PcgScalars* s, double* res, int k, cudaStream_t st);
 void launch_blas1(int op, const LevelTables& t, const FlagTables& fl, double alpha, const double* x1, double beta,
-                  const double* x2, double* dst, uint8_t mask, cudaStream_t st);
+                  const double* x2, double* dst, uint8_t mask, cudaStream_t st, DevScalars ds = DevScalars{});
 // counter-based U[lo,hi] keyed on (seed, stream, canonical DoF key)
 /// analytic expression evaluated at the reference's DoF coordinates
 /// (reference interpolate, src/function.cpp:170-190, over for_each_owned_coord,
@@ -171,7 +182,8 @@ void launch_partials(int op, const LevelTables& t, const double* x1, const doubl
 // PCG: x += alpha p, r += (-alpha) ap on every owned DoF, and the
 // per-primitive partials of r.r (bitwise those of launch_partials(0, r, r))
 void launch_pcg_update(const LevelTables& t, const FlagTables& fl, double* x, const double* p, double* r,
-                       const double* ap, double alpha, double* part, double* scratch, cudaStream_t st);
+                       const double* ap, double alpha, double* part, double* scratch, cudaStream_t st,
+                       const double* alpha_p = nullptr);
 void launch_combine_tree(int op, double* v, int64_t len, double* out, cudaStream_t st);
 
 // ---- coarse-grid solve (device-resident, replicated per rank) ----

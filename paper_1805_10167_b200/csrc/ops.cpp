@@ -113,16 +113,23 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
 namespace {
 // per-primitive partials already in `part` (faces: `slots` CTA partials each
 // in scratch) -> the reference's fold over the global vector -> host
-double finish_dot(Domain& d, const LevelTables& t, const double* u, const double* v, const double* scratch, int slots,
-                  double* part) {
+void finish_dot_dev(Domain& d, const LevelTables& t, const double* u, const double* v, const double* scratch,
+                    int slots, double* part, double* out) {
     launch_partials_finish(t, u, v, scratch, slots, part, d.stream());
     const int64_t np = int64_t(d.graph().size());
     d.allreduce_sum(part, np);
-    launch_combine_tree(0, part, np, d.scalar_out(), d.stream());
+    launch_combine_tree(0, part, np, out, d.stream());
+}
+double to_host(Domain& d, const double* dev) {
     double out = 0.0;
-    HYB_CUDA(cudaMemcpyAsync(&out, d.scalar_out(), 8, cudaMemcpyDeviceToHost, d.stream()));
+    HYB_CUDA(cudaMemcpyAsync(&out, dev, 8, cudaMemcpyDeviceToHost, d.stream()));
     HYB_CUDA(cudaStreamSynchronize(d.stream()));
     return out;
+}
+double finish_dot(Domain& d, const LevelTables& t, const double* u, const double* v, const double* scratch, int slots,
+                  double* part) {
+    finish_dot_dev(d, t, u, v, scratch, slots, part, d.scalar_out());
+    return to_host(d, d.scalar_out());
 }
 } // namespace
 
@@ -130,6 +137,11 @@ double finish_dot(Domain& d, const LevelTables& t, const double* u, const double
 // partials come from the stencil kernel's CTAs (fixed shapes, so the result is
 // deterministic and partition invariant, though not bitwise dot()'s order)
 double apply_dot(const Operator& A, Function& src, Function& dst, int level) {
+    apply_dot_dev(A, src, dst, level, A.domain().scalar_out());
+    return to_host(A.domain(), A.domain().scalar_out());
+}
+
+void apply_dot_dev(const Operator& A, Function& src, Function& dst, int level, double* out) {
     check_op_function(A, src, level, "apply", false);
     check_op_function(A, dst, level, "apply", true);
     if (&src == &dst) throw InvalidArgument("apply: src and dst must be distinct functions");
@@ -146,7 +158,7 @@ double apply_dot(const Operator& A, Function& src, Function& dst, int level) {
     launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, ALL_FLAGS,
                    d.stream(), 3, scratch);
     d.timer_end();
-    return finish_dot(d, t, src.data(level), dst.data(level), scratch, slots, part);
+    finish_dot_dev(d, t, src.data(level), dst.data(level), scratch, slots, part, out);
 }
 
 // the first weighted-Jacobi sweep of a cycle whose x starts at zero (see
@@ -356,7 +368,7 @@ void fill_expr(Function& f, int level, const Expr& e, uint8_t mask) {
 }
 
 namespace {
-double reduce(int op, Function& a, Function& b, int level) {
+void reduce_dev(int op, Function& a, Function& b, int level, double* out) {
     Domain& d = a.domain();
     const LevelTables& t = d.level(level).t;
     const int64_t np = int64_t(d.graph().size());
@@ -367,17 +379,23 @@ double reduce(int op, Function& a, Function& b, int level) {
     HYB_CUDA(cudaMemsetAsync(part, 0, size_t(np) * 8, d.stream()));
     launch_partials(op, t, a.data(level), b.data(level), part, scratch, d.stream());
     d.allreduce_sum(part, np); // one non-zero entry per primitive: exact
-    launch_combine_tree(op, part, np, d.scalar_out(), d.stream());
-    double out = 0.0;
-    HYB_CUDA(cudaMemcpyAsync(&out, d.scalar_out(), 8, cudaMemcpyDeviceToHost, d.stream()));
-    HYB_CUDA(cudaStreamSynchronize(d.stream()));
-    return out;
+    launch_combine_tree(op, part, np, out, d.stream());
+}
+double reduce(int op, Function& a, Function& b, int level) {
+    reduce_dev(op, a, b, level, a.domain().scalar_out());
+    return to_host(a.domain(), a.domain().scalar_out());
 }
 } // namespace
 
 // x += alpha p; r -= alpha ap (add_scaled twice, bitwise) and return r.r
 // (bitwise dot(r, r)) from one pass over the faces
 double pcg_update(Function& x, Function& p, Function& r, Function& ap, double alpha, int level) {
+    pcg_update_dev(x, p, r, ap, alpha, nullptr, level, x.domain().scalar_out());
+    return to_host(x.domain(), x.domain().scalar_out());
+}
+
+void pcg_update_dev(Function& x, Function& p, Function& r, Function& ap, double alpha, const double* alpha_dev,
+                    int level, double* rr_out) {
     check_pair("pcg_update", x, p, level);
     check_pair("pcg_update", r, ap, level);
     check_pair("pcg_update", x, r, level);
@@ -390,13 +408,14 @@ double pcg_update(Function& x, Function& p, Function& r, Function& ap, double al
     double* scratch = buf + 2 * np;
     HYB_CUDA(cudaMemsetAsync(part, 0, size_t(np) * 8, d.stream()));
     launch_pcg_update(t, r.flags(), x.data(level), p.data(level), r.data(level), ap.data(level), alpha, part, scratch,
-                      d.stream());
+                      d.stream(), alpha_dev);
     d.allreduce_sum(part, np);
-    launch_combine_tree(0, part, np, d.scalar_out(), d.stream());
-    double out = 0.0;
-    HYB_CUDA(cudaMemcpyAsync(&out, d.scalar_out(), 8, cudaMemcpyDeviceToHost, d.stream()));
-    HYB_CUDA(cudaStreamSynchronize(d.stream()));
-    return out;
+    launch_combine_tree(0, part, np, rr_out, d.stream());
+}
+
+void dot_dev(Function& a, Function& b, int level, double* out) {
+    check_pair("dot", a, b, level);
+    reduce_dev(0, a, b, level, out);
 }
 
 double dot(Function& a, Function& b, int level) {
@@ -787,13 +806,21 @@ std::vector<double> Hierarchy::pcg(Function& rhs, Function& x, int level, int ma
         pcg_p_ = std::make_unique<Function>(d, "pcg.p", level, level, a_.bc());
     }
     Function &r = *pcg_r_, &z = *pcg_z_, &p = *pcg_p_, &ap = r_;
+    // the scalar recurrence stays on the device (k_pcg_scalars): an iteration
+    // queues its kernels without waiting for the host; only a positive tol
+    // reads each residual back for the stopping test
+    if (pcg_s_.bytes() < sizeof(PcgScalars)) pcg_s_ = DevMem(sizeof(PcgScalars));
+    if (int64_t(pcg_res_.bytes() / 8) < int64_t(max_iter) + 1) pcg_res_ = DevMem(size_t(max_iter + 1) * 8);
+    PcgScalars* S = pcg_s_.as<PcgScalars>();
+    double* R = pcg_res_.as<double>();
+    HYB_CUDA(cudaMemsetAsync(S, 0, sizeof(PcgScalars), d.stream()));
     fill_const(x, 0.0, level, ALL_FLAGS);
     residual(a_, rhs, x, r, level);
     std::vector<double> res{std::sqrt(dot(r, r, level))};
     const double target = tol * res.front();
     run_cycle(r, z, level, nu_pre, nu_post, true); // z = M r from z = 0
     assign(1.0, z, 0.0, z, p, level, ALL_FLAGS);
-    double rz = dot(r, z, level);
+    dot_dev(r, z, level, &S->rz);
     // r.z from the cycle's last post-smoothing sweep when it is a Jacobi sweep
     // at this level (its partials land in dot_scratch_), else a separate dot
     const bool fused_rz = smoother_ == SMOOTH_JACOBI && nu_post > 0 && level > a_.min_level();
@@ -802,12 +829,13 @@ std::vector<double> Hierarchy::pcg(Function& rhs, Function& x, int level, int ma
     const int64_t np = int64_t(d.graph().size());
     if (fused_rz && int64_t(dot_scratch_.bytes() / 8) < np + int64_t(tl.nfaces) * slots + 1)
         dot_scratch_ = DevMem(size_t(np + int64_t(tl.nfaces) * slots + 1) * 8);
-    for (int k = 0; k < max_iter && res.back() > target; ++k) {
-        const double pap = apply_dot(a_, p, ap, level); // Ap and p.Ap in one pass
-        if (!(pap > 0.0)) throw RuntimeError("pcg: non-positive curvature p.Ap = " + std::to_string(pap));
-        const double alpha = rz / pap;
-        const double rr = pcg_update(x, p, r, ap, alpha, level); // x += alpha p, r -= alpha Ap, r.r
-        double rz_new;
+    DevScalars beta_dev;
+    beta_dev.pb = &S->beta;
+    int done = 0;
+    for (int k = 0; k < max_iter && res.front() > target; ++k) {
+        apply_dot_dev(a_, p, ap, level, &S->pap); // Ap and p.Ap in one pass
+        launch_pcg_scalars(0, S, R, k, d.stream()); // alpha = r.z / p.Ap
+        pcg_update_dev(x, p, r, ap, 0.0, &S->alpha, level, &S->rr); // x += alpha p, r -= alpha Ap, r.r
         if (fused_rz) {
             double* part = dot_scratch_.as<double>();
             HYB_CUDA(cudaMemsetAsync(part, 0, size_t(np) * 8, d.stream()));
@@ -822,15 +850,26 @@ std::vector<double> Hierarchy::pcg(Function& rhs, Function& x, int level, int ma
             }
             cycle_dot_ = nullptr;
             cycle_dot_level_ = -1;
-            rz_new = finish_dot(d, tl, r.data(level), z.data(level), part + np, slots, part);
+            finish_dot_dev(d, tl, r.data(level), z.data(level), part + np, slots, part, &S->rz_new);
         } else {
             run_cycle(r, z, level, nu_pre, nu_post, true);
-            rz_new = dot(r, z, level);
+            dot_dev(r, z, level, &S->rz_new);
         }
-        assign(1.0, z, rz_new / rz, p, p, level, ALL_FLAGS);
-        rz = rz_new;
-        res.push_back(std::sqrt(rr));
+        launch_pcg_scalars(1, S, R, k + 1, d.stream()); // beta, rz, ||r_k+1||
+        launch_blas1(0, tl, p.flags(), 1.0, z.data(level), 0.0, p.data(level), p.data(level), ALL_FLAGS, d.stream(),
+                     beta_dev); // p = z + beta p
+        done = k + 1;
+        if (target > 0.0 && to_host(d, R + k + 1) <= target) break;
     }
+    if (done > 0) {
+        res.resize(size_t(done) + 1);
+        HYB_CUDA(cudaMemcpyAsync(res.data() + 1, R + 1, size_t(done) * 8, cudaMemcpyDeviceToHost, d.stream()));
+    }
+    PcgScalars host{};
+    HYB_CUDA(cudaMemcpyAsync(&host, S, sizeof host, cudaMemcpyDeviceToHost, d.stream()));
+    HYB_CUDA(cudaStreamSynchronize(d.stream()));
+    if (host.bad != 0.0)
+        throw RuntimeError("pcg: non-positive curvature p.Ap at iteration " + std::to_string(int(host.bad) - 1));
     if (converged) *converged = res.back() <= target;
     return res;
 }
