@@ -64,6 +64,18 @@ def lib():
             "ref_fill_keyed": (i, [p, i, i, u64, u64, d, d]),
             "ref_coarse_matrix": (i, [p, i, C.POINTER(i64), C.POINTER(i64), pd, i64, C.POINTER(i64)]),
             "ref_gridhierarchy_solve": (i, [p, i, i, i, d, i, i, i, pd, C.POINTER(C.c_int)]),
+            "ref_stokes_create": (i, [C.c_char_p, i, i, i, i, i, C.POINTER(C.c_int), C.POINTER(C.c_uint8), i,
+                                      C.POINTER(C.c_int), C.POINTER(C.c_uint8), i, i, d, C.POINTER(p)]),
+            "ref_stokes_destroy": (None, [p]),
+            "ref_stokes_set": (i, [p, i, i, i, pd]),
+            "ref_stokes_get": (i, [p, i, i, i, pd]),
+            "ref_stokes_uzawa": (i, [p, i, d]),
+            "ref_stokes_residual": (i, [p, i]),
+            "ref_stokes_vcycle": (i, [p, i, i, i]),
+            "ref_stokes_solve": (i, [p, i, d, i, i, i, pd, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+            "ref_stokes_residual_norm": (i, [p, i, pd]),
+            "ref_stokes_pressure_mean": (i, [p, i, pd]),
+            "ref_stokes_matrix": (i, [p, i, C.POINTER(i64), C.POINTER(i64), pd, i64, C.POINTER(i64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -249,3 +261,82 @@ class RefSession:
         _ck(lib().ref_gridhierarchy_solve(self.h, rhs, x, level, tol, max_cycles, nu1, nu2,
                                           res.ctypes.data_as(C.POINTER(C.c_double)), C.byref(n)))
         return res[: n.value]
+
+
+def _bc_arrays(bc: dict):
+    m = (C.c_int * max(len(bc), 1))(*bc.keys())
+    f = (C.c_uint8 * max(len(bc), 1))(*bc.values())
+    return m, f, len(bc)
+
+
+class RefStokes:
+    """The reference's StokesMultigrid (src/solvers.cpp:640-753) with states
+    rhs (0), x (1), r (2); components 0 u1, 1 u2, 2 p."""
+
+    def __init__(self, mesh: str, ranks: int, min_level: int, max_level: int, bc_velocity: dict,
+                 bc_pressure: dict, project: bool = False, omega: float = 0.3, partitioner: int = 0,
+                 weight_level: int = 1):
+        mu, fu, nu = _bc_arrays(bc_velocity)
+        mp, fp, npr = _bc_arrays(bc_pressure)
+        h = C.c_void_p()
+        _ck(lib().ref_stokes_create(mesh.encode(), ranks, partitioner, weight_level, min_level, max_level, mu, fu, nu,
+                                    mp, fp, npr, int(project), omega, C.byref(h)))
+        self.h = h
+        self.mesh, self.ranks = mesh, ranks
+        self._owned = RefSession(mesh, 1, min_level, max_level, nfuncs=1)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_stokes_destroy(self.h)
+            self.h = None
+
+    def owned(self, level):
+        return self._owned.owned(level)
+
+    def set(self, state, comp, level, values):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        assert v.size == self.owned(level)
+        _ck(lib().ref_stokes_set(self.h, state, comp, level, v.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def get(self, state, comp, level) -> np.ndarray:
+        out = np.empty(self.owned(level))
+        _ck(lib().ref_stokes_get(self.h, state, comp, level, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def uzawa(self, level, omega=0.3):
+        _ck(lib().ref_stokes_uzawa(self.h, level, omega))
+
+    def residual(self, level):
+        _ck(lib().ref_stokes_residual(self.h, level))
+
+    def vcycle(self, level, nu1=2, nu2=2):
+        _ck(lib().ref_stokes_vcycle(self.h, level, nu1, nu2))
+
+    def solve(self, level, tol, max_cycles, nu1=2, nu2=2):
+        """(residual history, converged); raises RefError(3) when a coarse MINRES fails"""
+        res = np.zeros(max_cycles + 1)
+        n, conv = C.c_int(), C.c_int()
+        _ck(lib().ref_stokes_solve(self.h, level, tol, max_cycles, nu1, nu2,
+                                   res.ctypes.data_as(C.POINTER(C.c_double)), C.byref(n), C.byref(conv)))
+        return res[: n.value], bool(conv.value)
+
+    def residual_norm(self, level) -> float:
+        out = C.c_double()
+        _ck(lib().ref_stokes_residual_norm(self.h, level, C.byref(out)))
+        return out.value
+
+    def pressure_mean(self, level) -> float:
+        out = C.c_double()
+        _ck(lib().ref_stokes_pressure_mean(self.h, level, C.byref(out)))
+        return out.value
+
+    def matrix(self, level):
+        n = C.c_int64()
+        _ck(lib().ref_stokes_matrix(self.h, level, None, None, None, 0, C.byref(n)))
+        r = np.empty(n.value, dtype=np.int64)
+        c = np.empty(n.value, dtype=np.int64)
+        v = np.empty(n.value)
+        _ck(lib().ref_stokes_matrix(self.h, level, r.ctypes.data_as(C.POINTER(C.c_int64)),
+                                    c.ctypes.data_as(C.POINTER(C.c_int64)), v.ctypes.data_as(C.POINTER(C.c_double)),
+                                    n.value, C.byref(n)))
+        return r, c, v

@@ -510,4 +510,141 @@ int ref_coarse_matrix(void* sp, int level, int64_t* rows, int64_t* cols, double*
     });
 }
 
+
+// ---- P1-P1-PSPG Stokes (src/solvers.cpp:466-753): the reference's own
+// StokesMultigrid, uzawa_smooth and stokes_residual on states rhs (0), x (1)
+// and r (2); component 0 u1, 1 u2, 2 p. Velocity and pressure have separate
+// boundary conditions (marker -> flag). A solve whose coarse MINRES fails
+// returns 3 (runtime_error) with the reference's message and history.
+namespace {
+struct StokesSession {
+    SetupGraph setup;
+    std::unique_ptr<DistributedDomain> dom;
+    std::unique_ptr<Controller> ctl;
+    BoundaryConditions bcu, bcp;
+    int min_level = 1, max_level = 1;
+    std::unique_ptr<StokesMultigrid> mg;
+    std::vector<std::unique_ptr<StokesState>> st; // rhs, x, r
+};
+ScalarFunction& stokes_comp(StokesState& s, int comp) { return comp == 0 ? s.u1 : comp == 1 ? s.u2 : s.p; }
+void stokes_move(StokesSession& s, int state, int comp, int level, double* data, bool to_field) {
+    ScalarFunction& fn = stokes_comp(*s.st.at(size_t(state)), comp);
+    size_t pos = 0;
+    for (const PrimitiveID id : ids_sorted(*s.dom)) {
+        const Primitive& p = s.dom->primitive(id);
+        auto& vals = fn.values(id, level);
+        for_each_owned(FunctionKind::P1, p.kind, p.info, level, fn.layout(), [&](std::size_t slot) {
+            if (to_field) vals[slot] = data[pos];
+            else data[pos] = vals[slot];
+            ++pos;
+        });
+    }
+}
+} // namespace
+
+int ref_stokes_create(const char* mesh, int ranks, int partitioner, int weight_level, int min_level, int max_level,
+                      const int* bcu_markers, const uint8_t* bcu_flags, int nbcu, const int* bcp_markers,
+                      const uint8_t* bcp_flags, int nbcp, int project, double omega, void** out) {
+    return guard([&] {
+        auto s = std::make_unique<StokesSession>();
+        s->setup = build_setup_graph(parse_mesh_string(mesh));
+        const Assignment a = partitioner == 1
+                                 ? partition_greedy_edgecut(s->setup,
+                                                            weighted_graph(s->setup, FunctionKind::P1, weight_level),
+                                                            ranks)
+                                 : partition_round_robin(s->setup, ranks);
+        s->dom = std::make_unique<DistributedDomain>(s->setup, a, ranks);
+        s->ctl = std::make_unique<Controller>(*s->dom);
+        for (int i = 0; i < nbcu; ++i) s->bcu.marker_flag[bcu_markers[i]] = DoFFlag(bcu_flags[i]);
+        for (int i = 0; i < nbcp; ++i) s->bcp.marker_flag[bcp_markers[i]] = DoFFlag(bcp_flags[i]);
+        s->min_level = min_level;
+        s->max_level = max_level;
+        s->mg = std::make_unique<StokesMultigrid>(*s->dom, *s->ctl, min_level, max_level, s->bcu, s->bcp,
+                                                  project != 0, omega);
+        for (const char* nm : {"rhs", "x", "r"}) {
+            s->st.push_back(std::make_unique<StokesState>(nm, *s->dom, min_level, max_level, s->bcu, s->bcp));
+            register_state(*s->ctl, *s->st.back());
+        }
+        *out = s.release();
+    });
+}
+void ref_stokes_destroy(void* s) { delete static_cast<StokesSession*>(s); }
+int ref_stokes_set(void* s, int state, int comp, int level, const double* data) {
+    return guard([&] {
+        stokes_move(*static_cast<StokesSession*>(s), state, comp, level, const_cast<double*>(data), true);
+    });
+}
+int ref_stokes_get(void* s, int state, int comp, int level, double* data) {
+    return guard([&] { stokes_move(*static_cast<StokesSession*>(s), state, comp, level, data, false); });
+}
+int ref_stokes_uzawa(void* sp, int level, double omega) {
+    return guard([&] {
+        StokesSession& s = *static_cast<StokesSession*>(sp);
+        uzawa_smooth(s.mg->system(), *s.ctl, *s.st[0], *s.st[1], level, omega);
+    });
+}
+int ref_stokes_residual(void* sp, int level) {
+    return guard([&] {
+        StokesSession& s = *static_cast<StokesSession*>(sp);
+        stokes_residual(s.mg->system(), *s.ctl, *s.st[0], *s.st[1], *s.st[2], level);
+    });
+}
+int ref_stokes_vcycle(void* sp, int level, int nu1, int nu2) {
+    return guard([&] {
+        StokesSession& s = *static_cast<StokesSession*>(sp);
+        s.mg->vcycle(*s.st[0], *s.st[1], level, nu1, nu2);
+    });
+}
+// residuals: capacity max_cycles + 1; *n_out entries written (also on failure:
+// the residuals recorded before the failing cycle)
+int ref_stokes_solve(void* sp, int level, double tol, int max_cycles, int nu1, int nu2, double* residuals,
+                     int* n_out, int* converged) {
+    StokesSession& s = *static_cast<StokesSession*>(sp);
+    *n_out = 0;
+    return guard([&] {
+        const SolveReport rep = s.mg->solve(*s.st[0], *s.st[1], level, tol, max_cycles, nu1, nu2);
+        for (size_t i = 0; i < rep.residuals.size(); ++i) residuals[i] = rep.residuals[i];
+        *n_out = int(rep.residuals.size());
+        *converged = rep.converged ? 1 : 0;
+    });
+}
+int ref_stokes_residual_norm(void* sp, int level, double* out) {
+    return guard([&] {
+        StokesSession& s = *static_cast<StokesSession*>(sp);
+        *out = s.mg->residual_norm(*s.st[0], *s.st[1], level);
+    });
+}
+int ref_stokes_pressure_mean(void* sp, int level, double* out) {
+    return guard([&] {
+        StokesSession& s = *static_cast<StokesSession*>(sp);
+        *out = s.mg->pressure_mean(s.st[1]->p, level);
+    });
+}
+// the assembled, constrained monolithic min-level matrix (constrained_stokes_matrix,
+// src/solvers.cpp:578-592) as COO (size query: cap 0)
+int ref_stokes_matrix(void* sp, int level, int64_t* rows, int64_t* cols, double* vals, int64_t cap, int64_t* nnz) {
+    return guard([&] {
+        StokesSession& s = *static_cast<StokesSession*>(sp);
+        GlobalDoFMap map(*s.dom, FunctionKind::P1, level);
+        const auto fu = map.gather_flags(s.st[0]->u1);
+        const auto fp = map.gather_flags(s.st[0]->p);
+        SparseMatrix M = assemble_stokes_sparse(s.mg->system(), level, map, fu, fp);
+        std::vector<double> zero(M.rows(), 0.0);
+        std::vector<std::uint8_t> f3(fu);
+        f3.insert(f3.end(), fu.begin(), fu.end());
+        f3.insert(f3.end(), fp.begin(), fp.end());
+        constrain_dirichlet(M, zero, f3);
+        int64_t k = 0;
+        for (size_t r = 0; r < M.rows(); ++r)
+            for (const auto& [c, v] : M.row(r)) {
+                if (k < cap) {
+                    rows[k] = int64_t(r);
+                    cols[k] = int64_t(c);
+                    vals[k] = v;
+                }
+                ++k;
+            }
+        *nnz = k;
+    });
+}
 } // extern "C"
