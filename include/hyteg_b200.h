@@ -298,6 +298,51 @@ int hyb_hierarchy_fmg(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int 
 int hyb_hierarchy_pcg(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, int max_iter, int nu_pre,
                       int nu_post, double tol, double* residuals, int* n_out, int* converged);
 
+/* ---- P1-P1-PSPG Stokes (include/hytegrid/solvers.hpp:117-236,
+ *      src/solvers.cpp:466-753) -------------------------------------------
+ * A state is three functions {u1, u2, p}: u1, u2 carry the velocity BCs, p
+ * the pressure BCs (StokesState). hyb_stokes_create with multigrid 0 is
+ * StokesSystem(domain, min, max, bc_velocity, bc_pressure) (any levels); with
+ * multigrid 1 it is StokesMultigrid(domain, ctl, min, max, bc_velocity,
+ * bc_pressure, project_pressure_mean, omega) (1 <= min <= max; the min-level
+ * monolithic system is assembled and constrained as the reference does and
+ * solved by MINRES on the device to 1e-12, max 3 x 3N + 200 iterations; a
+ * MINRES that does not converge is HYB_RUNTIME_ERROR with the reference's
+ * message "stokes vcycle: coarse MINRES did not converge" + its history).
+ * Every operation is the reference's call sequence on the bitwise kernels:
+ * uzawa_smooth, stokes_residual and the solve history equal the reference's
+ * bit for bit (tests/test_stokes_gpu.py). */
+typedef struct hyb_stokes hyb_stokes;
+int hyb_stokes_create(hyb_domain* d, int min_level, int max_level, const int32_t* bcu_markers,
+                      const uint8_t* bcu_flags, int n_bcu, const int32_t* bcp_markers, const uint8_t* bcp_flags,
+                      int n_bcp, int multigrid, int project_pressure_mean, double omega, hyb_stokes** out);
+int hyb_stokes_destroy(hyb_stokes* S);
+/* uzawa_smooth(S, ctl, rhs, x, level, omega)      solvers.hpp:186-187 */
+int hyb_uzawa_smooth(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3], int level, double omega);
+/* stokes_residual(S, ctl, rhs, x, r, level)       solvers.hpp:191-192 */
+int hyb_stokes_residual(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3],
+                        hyb_function* const r[3], int level);
+/* stokes_dot(a, b, level)                          solvers.hpp:136 */
+int hyb_stokes_dot(hyb_function* const a[3], hyb_function* const b[3], int level, double* out);
+/* StokesMultigrid::vcycle / solve / residual_norm / pressure_mean (solvers.hpp:214-223);
+ * residuals capacity max_cycles + 1 */
+int hyb_stokes_vcycle(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3], int level, int nu_pre,
+                      int nu_post);
+int hyb_stokes_solve(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3], int level, double tol,
+                     int max_cycles, int nu_pre, int nu_post, double* residuals, int* n_out, int* converged);
+int hyb_stokes_residual_norm(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3], int level,
+                             double* out);
+int hyb_stokes_pressure_mean(hyb_stokes* S, hyb_function* p, int level, double* out);
+/* MINRES iterations of the last coarse solve */
+int hyb_stokes_coarse_iterations(hyb_stokes* S, int* out);
+/* host-only: the constrained monolithic min-level matrix (constrained_stokes_matrix,
+ * src/solvers.cpp:578-592) as COO, rows/columns ascending (cap 0: size query) */
+int hyb_stokes_matrix_host(const char* mesh_text, int level, const int32_t* bcu_markers, const uint8_t* bcu_flags,
+                           int n_bcu, const int32_t* bcp_markers, const uint8_t* bcp_flags, int n_bcp, int64_t* rows,
+                           int64_t* cols, double* vals, int64_t cap, int64_t* nnz);
+/* the coarse MINRES's hypot (glibc's algorithm, as the reference links it), host copy for pinning */
+double hyb_coarse_hypot(double x, double y);
+
 /* ---- pinned host memory (end-to-end transfers) ---- */
 int hyb_host_alloc(int64_t bytes, void** out);
 int hyb_host_free(void* p);

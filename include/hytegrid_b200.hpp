@@ -16,6 +16,8 @@
 //   sync_all(ctl, f, level)                     same
 //   GridHierarchy(dom, ctl, form, min, max, bc) same (+ smoother choice, Jacobi weight, coarse tolerance;
 //                                               default: the reference's Gauss-Seidel)
+//   StokesState / StokesSystem / uzawa_smooth / same (solvers.hpp:117-236)
+//   stokes_residual / stokes_dot / StokesMultigrid
 //   f.values(id, level)                         f.download(level) / f.upload(level, v)
 //                                               (GlobalDoFMap order, numbering.hpp:41-43)
 #pragma once
@@ -374,6 +376,122 @@ class GridHierarchy {
   private:
     hyb_hierarchy* h_ = nullptr;
     int max_;
+};
+
+// ---- P1-P1-PSPG Stokes (reference include/hytegrid/solvers.hpp:117-236) ----
+
+/// u1, u2 carry the velocity boundary conditions, p the pressure ones
+struct StokesState {
+    StokesState(const std::string& name, DistributedDomain& d, int min_level, int max_level,
+                const BoundaryConditions& bc_velocity, const BoundaryConditions& bc_pressure)
+        : u1(name + ".u1", d, min_level, max_level, bc_velocity), u2(name + ".u2", d, min_level, max_level, bc_velocity),
+          p(name + ".p", d, min_level, max_level, bc_pressure) {}
+    ScalarFunction u1, u2, p;
+};
+
+inline void register_state(Controller&, const StokesState&) {}
+
+namespace detail {
+struct State3 {
+    hyb_function* f[3];
+    explicit State3(const StokesState& s) : f{s.u1.handle(), s.u2.handle(), s.p.handle()} {}
+};
+} // namespace detail
+
+inline double stokes_dot(const StokesState& a, const StokesState& b, int level) {
+    double out = 0;
+    check(hyb_stokes_dot(detail::State3(a).f, detail::State3(b).f, level, &out));
+    return out;
+}
+
+class StokesSystem {
+  public:
+    StokesSystem(DistributedDomain& d, int min_level, int max_level, BoundaryConditions bc_velocity,
+                 BoundaryConditions bc_pressure) {
+        std::vector<int32_t> mu, mp;
+        std::vector<uint8_t> fu, fp;
+        detail::bc_arrays(bc_velocity, mu, fu);
+        detail::bc_arrays(bc_pressure, mp, fp);
+        check(hyb_stokes_create(d.handle(), min_level, max_level, mu.data(), fu.data(), int(mu.size()), mp.data(),
+                                fp.data(), int(mp.size()), 0, 0, 0.3, &h_));
+    }
+    ~StokesSystem() {
+        if (owner_) hyb_stokes_destroy(h_);
+    }
+    StokesSystem(const StokesSystem&) = delete;
+    StokesSystem& operator=(const StokesSystem&) = delete;
+    hyb_stokes* handle() const { return h_; }
+
+  private:
+    friend class StokesMultigrid;
+    explicit StokesSystem(hyb_stokes* h) : h_(h), owner_(false) {}
+    hyb_stokes* h_ = nullptr;
+    bool owner_ = true;
+};
+
+inline void uzawa_smooth(StokesSystem& S, Controller&, const StokesState& rhs, StokesState& x, int level,
+                         double omega = 0.3) {
+    check(hyb_uzawa_smooth(S.handle(), detail::State3(rhs).f, detail::State3(x).f, level, omega));
+}
+
+inline void stokes_residual(StokesSystem& S, Controller&, const StokesState& rhs, const StokesState& x,
+                            StokesState& r, int level) {
+    check(hyb_stokes_residual(S.handle(), detail::State3(rhs).f, detail::State3(x).f, detail::State3(r).f, level));
+}
+
+class StokesMultigrid {
+  public:
+    StokesMultigrid(DistributedDomain& d, Controller&, int min_level, int max_level, BoundaryConditions bc_velocity,
+                    BoundaryConditions bc_pressure, bool project_pressure_mean = false, double omega = 0.3)
+        : h_(create(d, min_level, max_level, bc_velocity, bc_pressure, project_pressure_mean, omega)), sys_(h_),
+          min_(min_level), max_(max_level) {}
+    ~StokesMultigrid() { hyb_stokes_destroy(h_); }
+    StokesMultigrid(const StokesMultigrid&) = delete;
+    StokesMultigrid& operator=(const StokesMultigrid&) = delete;
+    StokesSystem& system() { return sys_; }
+    int min_level() const { return min_; }
+    int max_level() const { return max_; }
+    void vcycle(const StokesState& rhs, StokesState& x, int level, int nu_pre = 2, int nu_post = 2) {
+        check(hyb_stokes_vcycle(h_, detail::State3(rhs).f, detail::State3(x).f, level, nu_pre, nu_post));
+    }
+    SolveReport solve(const StokesState& rhs, StokesState& x, int level, double tol, int max_cycles, int nu_pre = 2,
+                      int nu_post = 2) {
+        SolveReport rep;
+        rep.residuals.resize(size_t(max_cycles) + 1);
+        int n = 0, conv = 0;
+        check(hyb_stokes_solve(h_, detail::State3(rhs).f, detail::State3(x).f, level, tol, max_cycles, nu_pre, nu_post,
+                               rep.residuals.data(), &n, &conv));
+        rep.residuals.resize(size_t(n));
+        rep.iterations = n - 1;
+        rep.converged = conv != 0;
+        return rep;
+    }
+    double residual_norm(const StokesState& rhs, const StokesState& x, int level) {
+        double out = 0;
+        check(hyb_stokes_residual_norm(h_, detail::State3(rhs).f, detail::State3(x).f, level, &out));
+        return out;
+    }
+    double pressure_mean(const ScalarFunction& p, int level) {
+        double out = 0;
+        check(hyb_stokes_pressure_mean(h_, p.handle(), level, &out));
+        return out;
+    }
+
+  private:
+    static hyb_stokes* create(DistributedDomain& d, int lo, int hi, const BoundaryConditions& bu,
+                              const BoundaryConditions& bp, bool project, double omega) {
+        std::vector<int32_t> mu, mp;
+        std::vector<uint8_t> fu, fp;
+        detail::bc_arrays(bu, mu, fu);
+        detail::bc_arrays(bp, mp, fp);
+        hyb_stokes* h = nullptr;
+        check(hyb_stokes_create(d.handle(), lo, hi, mu.data(), fu.data(), int(mu.size()), mp.data(), fp.data(),
+                                int(mp.size()), 1, project ? 1 : 0, omega, &h));
+        return h;
+    }
+    hyb_stokes* h_;
+    StokesSystem sys_;
+    int min_, max_;
 };
 
 } // namespace hytegrid_b200

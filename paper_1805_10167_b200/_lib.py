@@ -135,6 +135,19 @@ _SIGS = {
     "hyb_hierarchy_solve": (_i, [_p, _p, _p, _i, _d, _i, _i, _i, _pd, C.POINTER(_i), C.POINTER(_i)]),
     "hyb_hierarchy_fmg": (_i, [_p, _p, _p, _i, _i, _i, _i, _d, _i, _pd, C.POINTER(_i), C.POINTER(_i)]),
     "hyb_hierarchy_pcg": (_i, [_p, _p, _p, _i, _i, _i, _i, _d, _pd, C.POINTER(_i), C.POINTER(_i)]),
+    "hyb_stokes_create": (_i, [_p, _i, _i, _pi32, _pu8, _i, _pi32, _pu8, _i, _i, _i, _d, C.POINTER(_p)]),
+    "hyb_stokes_destroy": (_i, [_p]),
+    "hyb_uzawa_smooth": (_i, [_p, C.POINTER(_p), C.POINTER(_p), _i, _d]),
+    "hyb_stokes_residual": (_i, [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(_p), _i]),
+    "hyb_stokes_dot": (_i, [C.POINTER(_p), C.POINTER(_p), _i, _pd]),
+    "hyb_stokes_vcycle": (_i, [_p, C.POINTER(_p), C.POINTER(_p), _i, _i, _i]),
+    "hyb_stokes_solve": (_i, [_p, C.POINTER(_p), C.POINTER(_p), _i, _d, _i, _i, _i, _pd, C.POINTER(_i),
+                              C.POINTER(_i)]),
+    "hyb_stokes_residual_norm": (_i, [_p, C.POINTER(_p), C.POINTER(_p), _i, _pd]),
+    "hyb_stokes_pressure_mean": (_i, [_p, _p, _i, _pd]),
+    "hyb_stokes_coarse_iterations": (_i, [_p, C.POINTER(_i)]),
+    "hyb_stokes_matrix_host": (_i, [_cs, _i, _pi32, _pu8, _i, _pi32, _pu8, _i, _pi64, _pi64, _pd, _i64, _pi64]),
+    "hyb_coarse_hypot": (_d, [_d, _d]),
     "hyb_host_alloc": (_i, [_i64, C.POINTER(_p)]),
     "hyb_host_free": (_i, [_p]),
 }

@@ -7,6 +7,7 @@
 #include "../../include/hyteg_b200.h"
 #include "coarse.hpp"
 #include "domain.hpp"
+#include "stokes.hpp"
 
 // Objects built on a domain share ownership of it: destroying the domain
 // handle first (any order is legal, e.g. a garbage collector finalising a
@@ -26,6 +27,12 @@ struct hyb_operator {
 struct hyb_hierarchy {
     std::shared_ptr<hyb::Domain> keep;
     std::unique_ptr<hyb::Hierarchy> h;
+};
+struct hyb_stokes {
+    std::shared_ptr<hyb::Domain> keep;
+    std::unique_ptr<hyb::StokesSystem> sys;     // system-only handle
+    std::unique_ptr<hyb::StokesMultigrid> mg;  // multigrid handle (owns its system)
+    hyb::StokesSystem& system() { return mg ? mg->system() : *sys; }
 };
 struct hyb_plan {
     hyb::MacroGraph g;
@@ -860,5 +867,132 @@ int hyb_host_free(void* p) {
         if (p) HYB_CUDA(cudaFreeHost(p));
     });
 }
+
+} // extern "C"
+
+// ---- P1-P1-PSPG Stokes (src/solvers.cpp:466-753) ----
+namespace {
+hyb::StokesState state_of(hyb_function* const f[3], const char* what) {
+    if (!f) throw hyb::InvalidArgument(std::string(what) + ": null state");
+    for (int k = 0; k < 3; ++k) need(f[k], what);
+    return hyb::StokesState(*f[0]->f, *f[1]->f, *f[2]->f);
+}
+hyb::StokesMultigrid& need_mg(hyb_stokes* S, const char* what) {
+    need(S, what);
+    if (!S->mg) throw hyb::InvalidArgument(std::string(what) + ": handle holds a StokesSystem only");
+    return *S->mg;
+}
+} // namespace
+
+extern "C" {
+
+int hyb_stokes_create(hyb_domain* d, int min_level, int max_level, const int32_t* bcu_markers,
+                      const uint8_t* bcu_flags, int n_bcu, const int32_t* bcp_markers, const uint8_t* bcp_flags,
+                      int n_bcp, int multigrid, int project_pressure_mean, double omega, hyb_stokes** out) {
+    return guarded([&] {
+        need(d, "hyb_stokes_create");
+        auto h = std::make_unique<hyb_stokes>();
+        h->keep = d->d;
+        const hyb::BoundaryMap bcu = make_bc(bcu_markers, bcu_flags, n_bcu);
+        const hyb::BoundaryMap bcp = make_bc(bcp_markers, bcp_flags, n_bcp);
+        if (multigrid)
+            h->mg = std::make_unique<hyb::StokesMultigrid>(*d->d, min_level, max_level, bcu, bcp,
+                                                           project_pressure_mean != 0, omega);
+        else
+            h->sys = std::make_unique<hyb::StokesSystem>(*d->d, min_level, max_level, bcu, bcp);
+        *out = h.release();
+    });
+}
+int hyb_stokes_destroy(hyb_stokes* S) {
+    return guarded([&] { delete S; });
+}
+int hyb_uzawa_smooth(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3], int level, double omega) {
+    return guarded([&] {
+        need(S, "hyb_uzawa_smooth");
+        auto r = state_of(rhs, "hyb_uzawa_smooth");
+        auto xs = state_of(x, "hyb_uzawa_smooth");
+        hyb::uzawa_smooth(S->system(), r, xs, level, omega);
+    });
+}
+int hyb_stokes_residual(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3], hyb_function* const r[3],
+                        int level) {
+    return guarded([&] {
+        need(S, "hyb_stokes_residual");
+        auto b = state_of(rhs, "hyb_stokes_residual");
+        auto xs = state_of(x, "hyb_stokes_residual");
+        auto rs = state_of(r, "hyb_stokes_residual");
+        hyb::stokes_residual(S->system(), b, xs, rs, level);
+    });
+}
+int hyb_stokes_dot(hyb_function* const a[3], hyb_function* const b[3], int level, double* out) {
+    return guarded([&] {
+        auto as = state_of(a, "hyb_stokes_dot");
+        auto bs = state_of(b, "hyb_stokes_dot");
+        *out = hyb::stokes_dot(as, bs, level);
+    });
+}
+int hyb_stokes_vcycle(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3], int level, int nu_pre,
+                      int nu_post) {
+    return guarded([&] {
+        auto& mg = need_mg(S, "hyb_stokes_vcycle");
+        auto b = state_of(rhs, "hyb_stokes_vcycle");
+        auto xs = state_of(x, "hyb_stokes_vcycle");
+        mg.vcycle(b, xs, level, nu_pre, nu_post);
+    });
+}
+int hyb_stokes_solve(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3], int level, double tol,
+                     int max_cycles, int nu_pre, int nu_post, double* residuals, int* n_out, int* converged) {
+    return guarded([&] {
+        auto& mg = need_mg(S, "hyb_stokes_solve");
+        auto b = state_of(rhs, "hyb_stokes_solve");
+        auto xs = state_of(x, "hyb_stokes_solve");
+        bool conv = false;
+        const auto res = mg.solve(b, xs, level, tol, max_cycles, nu_pre, nu_post, &conv);
+        for (size_t i = 0; i < res.size(); ++i) residuals[i] = res[i];
+        if (n_out) *n_out = int(res.size());
+        if (converged) *converged = conv ? 1 : 0;
+    });
+}
+int hyb_stokes_residual_norm(hyb_stokes* S, hyb_function* const rhs[3], hyb_function* const x[3], int level,
+                             double* out) {
+    return guarded([&] {
+        auto& mg = need_mg(S, "hyb_stokes_residual_norm");
+        auto b = state_of(rhs, "hyb_stokes_residual_norm");
+        auto xs = state_of(x, "hyb_stokes_residual_norm");
+        *out = mg.residual_norm(b, xs, level);
+    });
+}
+int hyb_stokes_pressure_mean(hyb_stokes* S, hyb_function* p, int level, double* out) {
+    return guarded([&] {
+        auto& mg = need_mg(S, "hyb_stokes_pressure_mean");
+        need(p, "hyb_stokes_pressure_mean");
+        *out = mg.pressure_mean(*p->f, level);
+    });
+}
+int hyb_stokes_coarse_iterations(hyb_stokes* S, int* out) {
+    return guarded([&] { *out = need_mg(S, "hyb_stokes_coarse_iterations").last_coarse_iterations; });
+}
+int hyb_stokes_matrix_host(const char* mesh_text, int level, const int32_t* bcu_markers, const uint8_t* bcu_flags,
+                           int n_bcu, const int32_t* bcp_markers, const uint8_t* bcp_flags, int n_bcp, int64_t* rows,
+                           int64_t* cols, double* vals, int64_t cap, int64_t* nnz) {
+    return guarded([&] {
+        need(mesh_text, "hyb_stokes_matrix_host");
+        need(nnz, "hyb_stokes_matrix_host");
+        if (level < 0 || level > 12) throw hyb::OutOfRange("hyb_stokes_matrix_host: level");
+        const auto g = hyb::build_macro_graph(hyb::parse_mesh_text(mesh_text));
+        const hyb::HostCsr m = hyb::assemble_stokes_constrained(g, level, make_bc(bcu_markers, bcu_flags, n_bcu),
+                                                                make_bc(bcp_markers, bcp_flags, n_bcp));
+        int64_t k = 0;
+        for (int64_t r = 0; r < m.n; ++r)
+            for (int32_t q = m.rowptr[size_t(r)]; q < m.rowptr[size_t(r) + 1]; ++q, ++k)
+                if (k < cap) {
+                    rows[k] = r;
+                    cols[k] = m.col[size_t(q)];
+                    vals[k] = m.val[size_t(q)];
+                }
+        *nnz = k;
+    });
+}
+double hyb_coarse_hypot(double x, double y) { return hyb::glibc_hypot_host(x, y); }
 
 } // extern "C"

@@ -5,13 +5,14 @@
 
 namespace hyb {
 
-HostCsr assemble_constrained(const MacroGraph& g, Form form, int L, const BoundaryMap& bc) {
+HostRows assemble_rows(const MacroGraph& g, Form form, int L, const BoundaryMap& bc) {
     const int n = 1 << L, W = n + 1;
-    HostCsr m;
+    HostRows m;
     m.n = int64_t(g.nv()) + int64_t(g.ne()) * (n - 1) + int64_t(g.nf()) * ((int64_t(n) - 1) * (n - 2) / 2);
     if (m.n > (int64_t(1) << 30)) throw InvalidArgument("coarse system too large for the device coarse solver");
     m.flag.assign(size_t(m.n), INNER);
-    std::vector<std::map<int64_t, double>> rows(size_t(m.n));
+    m.rows.resize(size_t(m.n));
+    auto& rows = m.rows;
     auto gi = [&](const OwnerSlot& o) { return global_owned_index(g, o, n); };
 
     // vertex rows: own + one ghost per incident edge (src/operators.cpp:275-281)
@@ -64,7 +65,16 @@ HostCsr assemble_constrained(const MacroGraph& g, Form form, int L, const Bounda
                 for (int t = 0; t < 7; ++t) acc[gi(resolve_face(g, fid, c + off[t][0], r + off[t][1], n))] += s.c[t];
             }
     }
-    // DIRICHLET rows -> identity, DIRICHLET columns dropped elsewhere
+    return m;
+}
+
+namespace {
+// constrain_dirichlet (src/solvers.cpp:322-352) on rows whose DIRICHLET rows
+// are already identities: DIRICHLET columns dropped from every other row
+HostCsr constrained_csr(const std::vector<std::map<int64_t, double>>& rows, const std::vector<uint8_t>& flag) {
+    HostCsr m;
+    m.n = int64_t(rows.size());
+    m.flag = flag;
     m.rowptr.push_back(0);
     for (int64_t row = 0; row < m.n; ++row) {
         if (m.flag[size_t(row)] & DIRICHLET) {
@@ -80,6 +90,52 @@ HostCsr assemble_constrained(const MacroGraph& g, Form form, int L, const Bounda
         m.rowptr.push_back(int32_t(m.col.size()));
     }
     return m;
+}
+} // namespace
+
+HostCsr assemble_constrained(const MacroGraph& g, Form form, int L, const BoundaryMap& bc) {
+    const HostRows r = assemble_rows(g, form, L, bc);
+    return constrained_csr(r.rows, r.flag);
+}
+
+// assemble_stokes_sparse (src/solvers.cpp:548-576) + constrain_dirichlet with
+// the flags (u, u, p) (:578-592): blocks at offsets 0, N, 2N
+HostCsr assemble_stokes_constrained(const MacroGraph& g, int L, const BoundaryMap& bc_u, const BoundaryMap& bc_p) {
+    const HostRows A = assemble_rows(g, LAPLACE, L, bc_u);
+    const HostRows Gx = assemble_rows(g, GRAD_X, L, bc_u);
+    const HostRows Gy = assemble_rows(g, GRAD_Y, L, bc_u);
+    const HostRows Bx = assemble_rows(g, DIV_X, L, bc_p);
+    const HostRows By = assemble_rows(g, DIV_Y, L, bc_p);
+    const HostRows C = assemble_rows(g, PSPG, L, bc_p);
+    const int64_t n = A.n;
+    if (3 * n > (int64_t(1) << 30)) throw InvalidArgument("coarse Stokes system too large for the device solver");
+    std::vector<std::map<int64_t, double>> M(size_t(3 * n));
+    std::vector<uint8_t> f3(size_t(3 * n));
+    for (int64_t r = 0; r < n; ++r) {
+        const uint8_t fu = A.flag[size_t(r)], fp = C.flag[size_t(r)];
+        f3[size_t(r)] = fu;
+        f3[size_t(n + r)] = fu;
+        f3[size_t(2 * n + r)] = fp;
+        if (fu & DIRICHLET) {
+            M[size_t(r)][r] = 1.0;
+            M[size_t(n + r)][n + r] = 1.0;
+        } else {
+            for (const auto& [c, v] : A.rows[size_t(r)]) {
+                M[size_t(r)][c] += v;
+                M[size_t(n + r)][n + c] += v;
+            }
+            for (const auto& [c, v] : Gx.rows[size_t(r)]) M[size_t(r)][2 * n + c] += v;
+            for (const auto& [c, v] : Gy.rows[size_t(r)]) M[size_t(n + r)][2 * n + c] += v;
+        }
+        if (fp & DIRICHLET) {
+            M[size_t(2 * n + r)][2 * n + r] = 1.0;
+        } else {
+            for (const auto& [c, v] : Bx.rows[size_t(r)]) M[size_t(2 * n + r)][c] += v;
+            for (const auto& [c, v] : By.rows[size_t(r)]) M[size_t(2 * n + r)][n + c] += v;
+            for (const auto& [c, v] : C.rows[size_t(r)]) M[size_t(2 * n + r)][2 * n + c] += v;
+        }
+    }
+    return constrained_csr(M, f3);
 }
 
 } // namespace hyb

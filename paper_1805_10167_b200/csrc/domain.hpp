@@ -275,6 +275,8 @@ void smooth_jacobi_zero(const Operator& A, Function& rhs, Function& x, double om
 void smooth_gs(const Operator& A, Function& rhs, Function& x, int level);
 void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level);
 void diagonal(const Operator& A, Function& d, int level);
+/// some row x's flags leave to a smoother has a zero diagonal in A
+bool zero_diagonal_row(const Operator& A, const Function& x, int level);
 void prolongate(Function& coarse, Function& fine, int coarse_level, uint8_t mask, bool add);
 void restrict_to_coarse(Function& fine, Function& coarse, int coarse_level, uint8_t mask);
 /// coarse := P^T (rhs - A x) at coarse_level on every owned DoF, fused (the

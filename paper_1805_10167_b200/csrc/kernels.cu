@@ -250,6 +250,9 @@ __global__ void __launch_bounds__(128) k_restrict_ev(LevelTables tc, LevelTables
 __device__ __forceinline__ double blas_op(int op, double alpha, double a, double beta, double b, double d) {
     if (op == 0) return alpha * a + beta * b;
     if (op == 1) return d + alpha * a;
+    // uzawa_smooth's pressure update p += omega * r / diag (src/solvers.cpp:536-544);
+    // slots without a diagonal (padding, stale ghosts) are left alone
+    if (op == 3) return b != 0.0 ? d + alpha * a / b : d;
     return alpha;
 }
 
@@ -262,8 +265,8 @@ __global__ void __launch_bounds__(256) k_blas1_faces(int op, int64_t n2, double 
     if (ds.pb) beta = *ds.pb;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
         const double2 a = op != 2 ? x1[i] : make_double2(0, 0);
-        const double2 b = op == 0 ? x2[i] : make_double2(0, 0);
-        const double2 d = op == 1 ? dst[i] : make_double2(0, 0);
+        const double2 b = (op == 0 || op == 3) ? x2[i] : make_double2(0, 0);
+        const double2 d = (op == 1 || op == 3) ? dst[i] : make_double2(0, 0);
         dst[i] = make_double2(blas_op(op, alpha, a.x, beta, b.x, d.x), blas_op(op, alpha, a.y, beta, b.y, d.y));
     }
 }
@@ -287,7 +290,8 @@ __global__ void __launch_bounds__(128) k_blas1_ev(int op, LevelTables t, FlagTab
         if (v >= t.nverts || !(fl.vtx_flag[v] & mask)) return;
         i = t.vtx_off[v];
     }
-    dst[i] = blas_op(op, alpha, op != 2 ? x1[i] : 0.0, beta, op == 0 ? x2[i] : 0.0, op == 1 ? dst[i] : 0.0);
+    dst[i] = blas_op(op, alpha, op != 2 ? x1[i] : 0.0, beta, (op == 0 || op == 3) ? x2[i] : 0.0,
+                     (op == 1 || op == 3) ? dst[i] : 0.0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1598,6 +1602,198 @@ void launch_coarse_scatter_add(int64_t nloc, const int64_t* gidx, const int64_t*
     if (nloc <= 0) return;
     k_coarse_scatter_add<<<grid_for(nloc), 256, 0, st>>>(nloc, gidx, pos, flag, mask, glob, arena);
     check_launch("coarse scatter");
+}
+
+// ---------------------------------------------------------------------------
+// Min-level MINRES of StokesMultigrid (reference minres_solve,
+// src/solvers.cpp:261-320, with the pressure-mean projections of
+// coarse_correct :702-726), one CTA. Bitwise the reference: the SpMV sums each
+// row in column order, every dot is the reference's sequential vec_dot
+// (src/solvers.cpp:36-41, one lane), hypot is glibc's (below), and every
+// product / sum rounds separately (-fmad=false).
+// ---------------------------------------------------------------------------
+constexpr int MR_THREADS = 512;
+
+// glibc 2.39 __hypot (sysdeps/ieee754/dbl-64/e_hypot.c, the non-FMA kernel
+// after Borges' correction) for the finite normal range the solver sees:
+// pinned against the host libm on 2e5 random pairs (tests/test_stokes_cpu.py)
+__host__ __device__ inline double glibc_hypot(double x, double y) {
+    x = fabs(x);
+    y = fabs(y);
+    const double ax = x < y ? y : x;
+    const double ay = x < y ? x : y;
+    if (ay <= ax * 0x1p-54) return ax + ay;
+    double h = sqrt(ax * ax + ay * ay);
+    double t1, t2;
+    if (h <= 2.0 * ay) {
+        const double delta = h - ay;
+        t1 = ax * (2.0 * delta - ax);
+        t2 = (delta - 2.0 * (ax - ay)) * delta;
+    } else {
+        const double delta = h - ax;
+        t1 = 2.0 * delta * (ax - 2.0 * ay);
+        t2 = (4.0 * delta - ay) * ay + delta * delta;
+    }
+    h -= (t1 + t2) / (2.0 * h);
+    return h;
+}
+
+__device__ double mr_seq_dot(const double* u, const double* v, int64_t n, double* bcast) {
+    if (threadIdx.x == 0) {
+        double s = 0;
+        for (int64_t i = 0; i < n; ++i) s += u[i] * v[i];
+        *bcast = s;
+    }
+    __syncthreads();
+    const double out = *bcast;
+    __syncthreads();
+    return out;
+}
+
+// subtract_mean (src/solvers.cpp:594-600) of v[b, e)
+__device__ void mr_subtract_mean(double* v, int64_t b, int64_t e, double* bcast) {
+    if (threadIdx.x == 0) {
+        double s = 0;
+        for (int64_t i = b; i < e; ++i) s += v[i];
+        *bcast = s / double(e - b);
+    }
+    __syncthreads();
+    const double m = *bcast;
+    for (int64_t i = b + threadIdx.x; i < e; i += MR_THREADS) v[i] -= m;
+    __syncthreads();
+}
+
+__device__ void mr_spmv(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                        const double* __restrict__ val, const double* u, double* out, int64_t n) {
+    for (int64_t i = threadIdx.x; i < n; i += MR_THREADS) {
+        double acc = 0.0;
+        for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) acc += val[k] * u[col[k]];
+        out[i] = acc;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(MR_THREADS) k_coarse_minres(int64_t n, const int32_t* __restrict__ rowptr,
+                                                             const int32_t* __restrict__ col,
+                                                             const double* __restrict__ val, double* bg, double* xg,
+                                                             double* work, double tol, int max_iter, int64_t pb,
+                                                             int64_t pe, CoarseStatus* st, double* hist, int in_smem) {
+    __shared__ double bc[2];
+    extern __shared__ double dsm[];
+    double* base = in_smem ? dsm : work;
+    double* b = base;
+    double* x = base + n;
+    double* v = base + 2 * n;
+    double* v_old = base + 3 * n;
+    double* w = base + 4 * n;
+    double* w_old = base + 5 * n;
+    double* av = base + 6 * n;
+    for (int64_t i = threadIdx.x; i < n; i += MR_THREADS) {
+        b[i] = bg[i];
+        x[i] = 0.0;
+        v_old[i] = 0.0;
+        w[i] = 0.0;
+        w_old[i] = 0.0;
+    }
+    __syncthreads();
+    if (pe > pb) mr_subtract_mean(b, pb, pe, bc);
+    const double target = tol * sqrt(mr_seq_dot(b, b, n, bc));
+    // v = rhs - A x with x = 0: A x is +0 in every row, so v = rhs bitwise
+    for (int64_t i = threadIdx.x; i < n; i += MR_THREADS) v[i] = b[i] - 0.0;
+    __syncthreads();
+    double beta = sqrt(mr_seq_dot(v, v, n, bc));
+    double last = beta;
+    if (threadIdx.x == 0) hist[0] = beta;
+    double eta = beta;
+    double c_old = 1.0, c = 1.0, s_old = 0.0, s = 0.0;
+    if (beta > 0.0)
+        for (int64_t i = threadIdx.x; i < n; i += MR_THREADS) v[i] /= beta;
+    __syncthreads();
+    int it = 0, breakdown = 0;
+    while (it < max_iter && last > target) {
+        mr_spmv(rowptr, col, val, v, av, n);
+        const double alpha = mr_seq_dot(v, av, n, bc);
+        for (int64_t i = threadIdx.x; i < n; i += MR_THREADS) av[i] -= alpha * v[i] + beta * v_old[i];
+        __syncthreads();
+        const double beta_new = sqrt(mr_seq_dot(av, av, n, bc));
+        const double rho1 = c * alpha - c_old * s * beta;
+        const double rho2 = s * alpha + c_old * c * beta;
+        const double rho3 = s_old * beta;
+        const double delta = glibc_hypot(rho1, beta_new);
+        if (delta == 0.0) {
+            breakdown = 1;
+            break;
+        }
+        const double c_new = rho1 / delta;
+        const double s_new = beta_new / delta;
+        for (int64_t i = threadIdx.x; i < n; i += MR_THREADS) {
+            const double wn = (v[i] - rho2 * w[i] - rho3 * w_old[i]) / delta;
+            w_old[i] = w[i];
+            w[i] = wn;
+            x[i] += c_new * eta * wn;
+        }
+        __syncthreads();
+        eta = -s_new * eta;
+        ++it;
+        last = fabs(eta);
+        if (threadIdx.x == 0) hist[it] = last;
+        if (beta_new == 0.0) break;
+        for (int64_t i = threadIdx.x; i < n; i += MR_THREADS) {
+            const double t = v[i];
+            v[i] = av[i] / beta_new;
+            v_old[i] = t;
+        }
+        __syncthreads();
+        c_old = c;
+        c = c_new;
+        s_old = s;
+        s = s_new;
+        beta = beta_new;
+    }
+    // finish_report: the true residual of the returned iterate (sequential sum)
+    mr_spmv(rowptr, col, val, x, av, n);
+    if (threadIdx.x == 0) {
+        double q = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            const double d = b[i] - av[i];
+            q += d * d;
+        }
+        bc[0] = sqrt(q);
+    }
+    __syncthreads();
+    const double res = bc[0];
+    __syncthreads();
+    if (pe > pb) mr_subtract_mean(x, pb, pe, bc);
+    for (int64_t i = threadIdx.x; i < n; i += MR_THREADS) xg[i] = x[i];
+    if (threadIdx.x == 0) {
+        hist[it] = res;
+        st->iterations = it;
+        st->breakdown = breakdown;
+        st->converged = res <= target ? 1 : 0;
+        st->target = target;
+        st->residual = res;
+    }
+}
+
+double glibc_hypot_host(double x, double y) { return glibc_hypot(x, y); }
+
+size_t coarse_minres_work_doubles(int64_t n) { return size_t(7 * n) * sizeof(double) <= 200 * 1024 ? 0 : size_t(7 * n); }
+
+void launch_coarse_minres(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, double* b,
+                          double* x, double* work, double tol, int max_iter, int64_t proj_begin, int64_t proj_end,
+                          CoarseStatus* st, double* hist, cudaStream_t stream) {
+    const size_t smem = size_t(7 * n) * sizeof(double);
+    const bool in_smem = smem <= 200 * 1024;
+    if (in_smem) {
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(k_coarse_minres, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr_set = true;
+        }
+    }
+    k_coarse_minres<<<1, MR_THREADS, in_smem ? smem : 0, stream>>>(n, rowptr, col, val, b, x, work, tol, max_iter,
+                                                                   proj_begin, proj_end, st, hist, in_smem ? 1 : 0);
+    check_launch("coarse minres");
 }
 
 } // namespace hyb

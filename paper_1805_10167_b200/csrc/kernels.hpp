@@ -213,6 +213,18 @@ void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, cons
                       double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
                       double* grid_part, unsigned* grid_bar, int max_row_nnz, cudaStream_t stream);
 // arena[pos[i]] += glob[gidx[i]] where flag[i] & mask
+/// StokesMultigrid's min-level MINRES (minres_solve, src/solvers.cpp:261-320)
+/// on the constrained monolithic CSR, one CTA, bitwise the reference. b is
+/// the gathered rhs (its pressure mean over [proj_begin, proj_end) removed
+/// first when proj_end > proj_begin, and again from the solution); x the
+/// solution; hist[0..iterations] the residual history (capacity max_iter + 1);
+/// work: coarse_minres_work_doubles(n) doubles (0: vectors in shared memory)
+size_t coarse_minres_work_doubles(int64_t n);
+void launch_coarse_minres(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, double* b,
+                          double* x, double* work, double tol, int max_iter, int64_t proj_begin, int64_t proj_end,
+                          CoarseStatus* st, double* hist, cudaStream_t stream);
+/// host copy of the device hypot (glibc's), for the CPU pin
+double glibc_hypot_host(double x, double y);
 void launch_coarse_scatter_add(int64_t nloc, const int64_t* gidx, const int64_t* pos, const uint8_t* flag,
                                uint8_t mask, const double* glob, double* arena, cudaStream_t st);
 

@@ -40,31 +40,38 @@ void check_transfer(const Function& coarse, const Function& fine, int lc, const 
 
 // zero diagonal on a row that a smoother would update -> runtime_error
 // (reference src/operators.cpp:457-458)
-void check_diagonals(const Operator& A, const Function& x, int level, const char* what) {
+bool zero_diagonal_row_impl(const Operator& A, const Function& x, int level) {
     Domain& d = A.domain();
     const MacroGraph& g = d.graph();
     const int n = 1 << level;
     const auto& hf = A.host_face_coef(level);
     if (n >= 3)
         for (size_t i = 0; i < d.local_faces().size(); ++i)
-            if (hf[i * 8 + 7] == 0.0) throw RuntimeError(std::string(what) + ": zero diagonal entry");
+            if (hf[i * 8 + 7] == 0.0) return true;
     const auto& he = A.host_edge_coef(level);
     if (n >= 2)
         for (size_t i = 0; i < d.local_edges().size(); ++i)
             if (!(x.bc().flag_for(g.edges[g.edge_index(d.local_edges()[i])].marker) & DIRICHLET) && he[i * 8 + 7] == 0.0)
-                throw RuntimeError(std::string(what) + ": zero diagonal entry");
+                return true;
     const auto& hv = A.host_vtx_coef(level);
     size_t pos = 0;
     for (uint64_t id : d.local_verts()) {
         const MacroVertex& v = g.vertices[id];
         pos += 1 + v.edges.size();
         if (!(x.bc().flag_for(v.marker) & DIRICHLET) && hv[pos] == 0.0)
-            throw RuntimeError(std::string(what) + ": zero diagonal entry");
+            return true;
         pos += 1;
     }
+    return false;
+}
+
+void check_diagonals(const Operator& A, const Function& x, int level, const char* what) {
+    if (zero_diagonal_row_impl(A, x, level)) throw RuntimeError(std::string(what) + ": zero diagonal entry");
 }
 
 } // namespace
+
+bool zero_diagonal_row(const Operator& A, const Function& x, int level) { return zero_diagonal_row_impl(A, x, level); }
 
 void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t mask) {
     check_op_function(A, src, level, "apply", false);

@@ -614,6 +614,128 @@ class GridHierarchy:
         return SolveReport(bool(conv.value), n.value - 1, list(res[: n.value]))
 
 
+
+# ---- P1-P1-PSPG Stokes (include/hytegrid/solvers.hpp:117-236) ----
+
+class StokesState:
+    """u1, u2 (velocity BCs) and p (pressure BCs) (reference StokesState)."""
+
+    def __init__(self, name: str, domain: DistributedDomain, min_level: int, max_level: int,
+                 bc_velocity: dict | None = None, bc_pressure: dict | None = None):
+        self.u1 = ScalarFunction(name + ".u1", domain, min_level, max_level, bc_velocity)
+        self.u2 = ScalarFunction(name + ".u2", domain, min_level, max_level, bc_velocity)
+        self.p = ScalarFunction(name + ".p", domain, min_level, max_level, bc_pressure)
+
+    def _arr(self):
+        return (C.c_void_p * 3)(self.u1._h, self.u2._h, self.p._h)
+
+    def components(self):
+        return (self.u1, self.u2, self.p)
+
+
+def register_state(ctl: Controller, s: StokesState) -> None:  # noqa: ARG001 - API parity
+    """register_state: every function of the domain shares the exchange plan."""
+
+
+def stokes_dot(a: StokesState, b: StokesState, level: int) -> float:
+    out = C.c_double()
+    check(lib.hyb_stokes_dot(a._arr(), b._arr(), level, C.byref(out)))
+    return out.value
+
+
+class _StokesHandle:
+    def __init__(self, domain, min_level, max_level, bc_velocity, bc_pressure, multigrid, project, omega):
+        mu, fu, nu = _bc_arrays(bc_velocity)
+        mp, fp, npr = _bc_arrays(bc_pressure)
+        h = C.c_void_p()
+        check(lib.hyb_stokes_create(domain._h, min_level, max_level, mu, fu, nu, mp, fp, npr, int(multigrid),
+                                    int(project), omega, C.byref(h)))
+        self._h = h
+        self.domain = domain
+        self.min_level, self.max_level = min_level, max_level
+
+    def __del__(self):
+        if getattr(self, "_h", None) and alive():
+            lib.hyb_stokes_destroy(self._h)
+            self._h = None
+
+
+class StokesSystem(_StokesHandle):
+    """Operator blocks A (per velocity component), G = (GRAD_X, GRAD_Y),
+    B = (DIV_X, DIV_Y) and the PSPG block C (reference StokesSystem)."""
+
+    def __init__(self, domain: DistributedDomain, min_level: int, max_level: int, bc_velocity: dict | None = None,
+                 bc_pressure: dict | None = None):
+        super().__init__(domain, min_level, max_level, bc_velocity, bc_pressure, False, False, 0.3)
+
+
+def uzawa_smooth(S, ctl: Controller, rhs: StokesState, x: StokesState, level: int,  # noqa: ARG001
+                 omega: float = 0.3) -> None:
+    """One inexact-Uzawa sweep (src/solvers.cpp:506-546); S is a StokesSystem
+    or a StokesMultigrid's system()."""
+    check(lib.hyb_uzawa_smooth(S._h, rhs._arr(), x._arr(), level, omega))
+
+
+def stokes_residual(S, ctl: Controller, rhs: StokesState, x: StokesState, r: StokesState,  # noqa: ARG001
+                    level: int) -> None:
+    check(lib.hyb_stokes_residual(S._h, rhs._arr(), x._arr(), r._arr(), level))
+
+
+class StokesMultigrid(_StokesHandle):
+    """Monolithic Uzawa-smoothed multigrid with a device MINRES on the
+    assembled min-level system (reference StokesMultigrid)."""
+
+    def __init__(self, domain: DistributedDomain, ctl: Controller, min_level: int, max_level: int,  # noqa: ARG002
+                 bc_velocity: dict | None = None, bc_pressure: dict | None = None,
+                 project_pressure_mean: bool = False, omega: float = 0.3):
+        super().__init__(domain, min_level, max_level, bc_velocity, bc_pressure, True, project_pressure_mean, omega)
+
+    def system(self) -> "StokesMultigrid":
+        return self
+
+    def vcycle(self, rhs: StokesState, x: StokesState, level: int, nu_pre: int = 2, nu_post: int = 2) -> None:
+        check(lib.hyb_stokes_vcycle(self._h, rhs._arr(), x._arr(), level, nu_pre, nu_post))
+
+    def solve(self, rhs: StokesState, x: StokesState, level: int, tol: float, max_cycles: int, nu_pre: int = 2,
+              nu_post: int = 2) -> SolveReport:
+        res = np.zeros(max_cycles + 1)
+        n = C.c_int()
+        conv = C.c_int()
+        check(lib.hyb_stokes_solve(self._h, rhs._arr(), x._arr(), level, tol, max_cycles, nu_pre, nu_post, _pd(res),
+                                   C.byref(n), C.byref(conv)))
+        return SolveReport(bool(conv.value), n.value - 1, list(res[: n.value]))
+
+    def residual_norm(self, rhs: StokesState, x: StokesState, level: int) -> float:
+        out = C.c_double()
+        check(lib.hyb_stokes_residual_norm(self._h, rhs._arr(), x._arr(), level, C.byref(out)))
+        return out.value
+
+    def pressure_mean(self, p: ScalarFunction, level: int) -> float:
+        out = C.c_double()
+        check(lib.hyb_stokes_pressure_mean(self._h, p._h, level, C.byref(out)))
+        return out.value
+
+    def coarse_iterations(self) -> int:
+        out = C.c_int()
+        check(lib.hyb_stokes_coarse_iterations(self._h, C.byref(out)))
+        return out.value
+
+
+def stokes_matrix_host(mesh_text: str, level: int, bc_velocity: dict | None = None, bc_pressure: dict | None = None):
+    """StokesMultigrid's constrained monolithic min-level matrix (COO), host only."""
+    mu, fu, nu = _bc_arrays(bc_velocity)
+    mp, fp, npr = _bc_arrays(bc_pressure)
+    n = C.c_int64()
+    check(lib.hyb_stokes_matrix_host(mesh_text.encode(), level, mu, fu, nu, mp, fp, npr, None, None, None, 0,
+                                     C.byref(n)))
+    r = np.empty(n.value, dtype=np.int64)
+    c = np.empty(n.value, dtype=np.int64)
+    v = np.empty(n.value)
+    check(lib.hyb_stokes_matrix_host(mesh_text.encode(), level, mu, fu, nu, mp, fp, npr,
+                                     r.ctypes.data_as(C.POINTER(C.c_int64)), c.ctypes.data_as(C.POINTER(C.c_int64)),
+                                     _pd(v), n.value, C.byref(n)))
+    return r, c, v
+
 class PinnedBuffer:
     """Page-locked host memory (for end-to-end H2D/D2H timing)."""
 

@@ -100,6 +100,26 @@ int main() {
         const SolveReport hrep = hg.solve(hr, hx, level, 0.0, 6);
         std::printf("HISTORY_BEGIN\n%sHISTORY_END\n", hrep.history().c_str());
     }
+    // P1-P1-PSPG Stokes: the reference's enclosed-cavity test (tests/test_solvers.cpp:689-719) through
+    // the drop-in types: all-Dirichlet velocity, free pressure with its mean projected out
+    {
+        DistributedDomain sd(meshgen::unit_square(), 2);
+        Controller scx(sd);
+        BoundaryConditions free_p;
+        for (int m = 1; m <= 3; ++m) free_p.marker_flag[m] = DoFFlag::NEUMANN;
+        StokesMultigrid smg(sd, scx, 1, 3, {}, free_p, true);
+        StokesState srhs("rhs", sd, 1, 3, {}, free_p), sx("x", sd, 1, 3, {}, free_p);
+        register_state(scx, srhs);
+        interpolate(srhs.u1, [](double a, double b) { return std::exp(0.3 * a - 0.2 * b) + 0.1 * a * b; }, 3,
+                    flag_bit(DoFFlag::INNER) | flag_bit(DoFFlag::NEUMANN));
+        const SolveReport srep = smg.solve(srhs, sx, 3, 1e-8, 20);
+        EXPECT(srep.converged);
+        EXPECT(std::fabs(smg.pressure_mean(sx.p, 3)) <= 1e-9);
+        StokesState sr("r", sd, 1, 3, {}, free_p);
+        stokes_residual(smg.system(), scx, srhs, sx, sr, 3);
+        EXPECT(std::sqrt(stokes_dot(sr, sr, 3)) <= 1e-8 * srep.residuals.front());
+        uzawa_smooth(smg.system(), scx, srhs, sx, 3);
+    }
     std::printf("cpp api ok: %d cycles, residual %.3e, error %.3e; fmg %d cycles, pcg %.1e\n", rep.iterations,
                 rep.residuals.back(), err, fr.iterations, pr.residuals.back() / pr.residuals.front());
     return 0;
