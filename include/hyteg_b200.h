@@ -47,6 +47,10 @@ enum hyb_flag { HYB_INNER = 1, HYB_DIRICHLET = 2, HYB_NEUMANN = 4, HYB_ALL_FLAGS
  * stabilisation -h_T^2/12 (grad q, grad p) (src/elements.cpp:31-76) */
 enum hyb_form { HYB_LAPLACE = 0, HYB_MASS = 1, HYB_DIV_X = 2, HYB_DIV_Y = 3, HYB_GRAD_X = 4, HYB_GRAD_Y = 5,
                 HYB_PSPG = 6 };
+/* function kinds (include/hytegrid/indexing.hpp:28): P2 is the reference's
+ * four-group quadratic element (vertex + three edge groups), stored on the
+ * once-refined lattice of the P1 arena (csrc/p2.hpp); DG0 is not provided */
+enum hyb_kind { HYB_P1 = 0, HYB_P2 = 1 };
 enum hyb_smoother { HYB_SMOOTH_JACOBI = 0, HYB_SMOOTH_GS = 1, HYB_SMOOTH_COLORED_GS = 2 };
 enum hyb_partitioner { HYB_PARTITION_ROUND_ROBIN = 0, HYB_PARTITION_GREEDY_EDGECUT = 1 };
 
@@ -138,6 +142,8 @@ int hyb_kernel_launches(int64_t* count);
 /* coordinates (x, y interleaved) of owned DoFs: for_each_owned_coord
  * (src/layout.cpp:239-282); global_order 1: whole domain in ID order */
 int hyb_owned_coords(hyb_domain* d, int level, int global_order, double* xy, int64_t n);
+/* the same for a function kind (HYB_P2: the reference's P2 DoF coordinates in its P2 order) */
+int hyb_owned_coords_kind(hyb_domain* d, int kind, int level, int global_order, double* xy, int64_t n);
 
 /* ---- functions ------------------------------------------------------------
  * ScalarFunction(name, domain, P1, min, max, bc) (include/hytegrid/function.hpp:19-20);
@@ -150,6 +156,18 @@ int hyb_owned_coords(hyb_domain* d, int level, int global_order, double* xy, int
  */
 int hyb_function_create(hyb_domain* d, const char* name, int min_level, int max_level, const int32_t* bc_markers,
                         const uint8_t* bc_flags, int n_bc, hyb_function** out);
+/* ScalarFunction(name, domain, kind, min, max, bc): P1 or P2. A P2 function
+ * supports sync, upload / download (the reference's P2 GlobalDoFMap order:
+ * per primitive vertex; edge line k = 1..n-1 then midline m = 0..n-1; face
+ * groups EH, ED, EV, then interior vertices, src/layout.cpp:176-237; at level
+ * L it holds the DoF count of P1 at level L+1), assign / add_scaled / dot /
+ * norm2 / max_abs / interpolate, and the P2 operators' apply, smooth_jacobi,
+ * smooth_gs and diagonal. Level transfers (P1 only in the reference too),
+ * the fused residual, coloured GS, hierarchies, serialisation and single
+ * relay directions are P1-only here: HYB_INVALID_ARGUMENT. */
+int hyb_function_create_kind(hyb_domain* d, const char* name, int kind, int min_level, int max_level,
+                             const int32_t* bc_markers, const uint8_t* bc_flags, int n_bc, hyb_function** out);
+int hyb_function_kind(hyb_function* f, int* kind);
 int hyb_function_destroy(hyb_function* f);
 int hyb_function_upload(hyb_function* f, int level, const double* host, int64_t n, int global_order, uint8_t mask);
 int hyb_function_download(hyb_function* f, int level, double* host, int64_t n, int global_order);
@@ -218,6 +236,11 @@ int hyb_function_set_values(hyb_function* f, uint64_t prim, int level, const dou
  */
 int hyb_operator_create(hyb_domain* d, int form, int min_level, int max_level, const int32_t* bc_markers,
                         const uint8_t* bc_flags, int n_bc, hyb_operator** out);
+/* StencilOperator(domain, form, kind, min, max, bc): kind HYB_P2 assembles the
+ * reference's P2 stencils (19 / 9 / 9 / 9 terms per face group,
+ * src/operators.cpp:95-263) for every form */
+int hyb_operator_create_kind(hyb_domain* d, int form, int kind, int min_level, int max_level,
+                             const int32_t* bc_markers, const uint8_t* bc_flags, int n_bc, hyb_operator** out);
 int hyb_operator_destroy(hyb_operator* A);
 int hyb_operator_stencil(hyb_operator* A, int level, uint64_t primitive_id, double* out, int cap, int* len);
 

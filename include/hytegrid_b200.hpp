@@ -6,8 +6,8 @@
 //   reference                                   here
 //   DistributedDomain(setup, assignment, P)     DistributedDomain(mesh_text, P[, assignment])
 //   Controller(domain), register_function       Controller(domain), register_function (no-ops)
-//   ScalarFunction(name, dom, P1, min, max, bc) ScalarFunction(name, dom, min, max, bc)
-//   StencilOperator(dom, form, P1, min, max, bc) StencilOperator(dom, form, min, max, bc)
+//   ScalarFunction(name, dom, kind, min, max, bc) same (kind P1 or P2; P1 when omitted)
+//   StencilOperator(dom, form, kind, min, max, bc) same (kind P1 or P2; P1 when omitted)
 //   apply / smooth_jacobi / smooth_gs / diagonal same (operators.hpp:108-125)
 //   prolongate / restrict_to_coarse             same (solvers.hpp:26-33)
 //   assign / add_scaled / dot / norm2 / max_abs same (function.hpp:60-74)
@@ -29,6 +29,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "hyteg_b200.h"
@@ -36,6 +37,8 @@
 namespace hytegrid_b200 {
 
 enum class DoFFlag : std::uint8_t { INNER = 1, DIRICHLET = 2, NEUMANN = 4 };
+/// include/hytegrid/indexing.hpp:28 (DG0 is not provided)
+enum class FunctionKind : int { P1 = HYB_P1, P2 = HYB_P2 };
 constexpr std::uint8_t ALL_DOF_FLAGS = 7;
 inline std::uint8_t flag_bit(DoFFlag f) { return static_cast<std::uint8_t>(f); }
 enum class Form : int {
@@ -115,9 +118,10 @@ class DistributedDomain {
         check(hyb_domain_owned_count(h_, level, &t, nullptr));
         return t;
     }
-    std::vector<double> coords(int level) const {
-        std::vector<double> xy(size_t(2 * owned(level)));
-        check(hyb_owned_coords(h_, level, 1, xy.data(), owned(level)));
+    std::vector<double> coords(int level, int kind = HYB_P1) const {
+        const int64_t n = owned(kind == HYB_P2 ? level + 1 : level);
+        std::vector<double> xy(size_t(2 * n));
+        check(hyb_owned_coords_kind(h_, kind, level, 1, xy.data(), n));
         return xy;
     }
 
@@ -149,20 +153,26 @@ class ScalarFunction {
   public:
     ScalarFunction(const std::string& name, DistributedDomain& d, int min_level, int max_level,
                    BoundaryConditions bc = {})
-        : dom_(&d) {
+        : ScalarFunction(name, d, FunctionKind::P1, min_level, max_level, std::move(bc)) {}
+    /// the reference's signature (function.hpp:19-20)
+    ScalarFunction(const std::string& name, DistributedDomain& d, FunctionKind kind, int min_level, int max_level,
+                   BoundaryConditions bc = {})
+        : dom_(&d), kind_(kind) {
         std::vector<int32_t> m;
         std::vector<uint8_t> f;
         detail::bc_arrays(bc, m, f);
-        check(hyb_function_create(d.handle(), name.c_str(), min_level, max_level, m.data(), f.data(), int(m.size()),
-                                  &h_));
+        check(hyb_function_create_kind(d.handle(), name.c_str(), int(kind), min_level, max_level, m.data(), f.data(),
+                                       int(m.size()), &h_));
     }
+    FunctionKind kind() const { return kind_; }
     ~ScalarFunction() { hyb_function_destroy(h_); }
     ScalarFunction(const ScalarFunction&) = delete;
     ScalarFunction& operator=(const ScalarFunction&) = delete;
     hyb_function* handle() const { return h_; }
     DistributedDomain& domain() const { return *dom_; }
     std::vector<double> download(int level) const {
-        std::vector<double> v(size_t(dom_->owned(level)));
+        // a P2 function at level L holds the DoF count of P1 at level L + 1
+        std::vector<double> v(size_t(dom_->owned(kind_ == FunctionKind::P2 ? level + 1 : level)));
         check(hyb_function_download(h_, level, v.data(), int64_t(v.size()), 1));
         return v;
     }
@@ -184,6 +194,7 @@ class ScalarFunction {
 
   private:
     DistributedDomain* dom_;
+    FunctionKind kind_ = FunctionKind::P1;
     hyb_function* h_ = nullptr;
 };
 
@@ -191,11 +202,16 @@ inline void register_function(Controller&, const ScalarFunction&) {}
 
 class StencilOperator {
   public:
-    StencilOperator(DistributedDomain& d, Form form, int min_level, int max_level, BoundaryConditions bc = {}) {
+    StencilOperator(DistributedDomain& d, Form form, int min_level, int max_level, BoundaryConditions bc = {})
+        : StencilOperator(d, form, FunctionKind::P1, min_level, max_level, std::move(bc)) {}
+    /// the reference's signature (operators.hpp:76-88)
+    StencilOperator(DistributedDomain& d, Form form, FunctionKind kind, int min_level, int max_level,
+                    BoundaryConditions bc = {}) {
         std::vector<int32_t> m;
         std::vector<uint8_t> f;
         detail::bc_arrays(bc, m, f);
-        check(hyb_operator_create(d.handle(), int(form), min_level, max_level, m.data(), f.data(), int(m.size()), &h_));
+        check(hyb_operator_create_kind(d.handle(), int(form), int(kind), min_level, max_level, m.data(), f.data(),
+                                       int(m.size()), &h_));
     }
     ~StencilOperator() { hyb_operator_destroy(h_); }
     StencilOperator(const StencilOperator&) = delete;
@@ -208,7 +224,7 @@ class StencilOperator {
 
 inline void interpolate(ScalarFunction& f, const std::function<double(double, double)>& expr, int level,
                         std::uint8_t mask = ALL_DOF_FLAGS) {
-    const std::vector<double> xy = f.domain().coords(level);
+    const std::vector<double> xy = f.domain().coords(level, int(f.kind()));
     std::vector<double> v(xy.size() / 2);
     for (size_t i = 0; i < v.size(); ++i) v[i] = expr(xy[2 * i], xy[2 * i + 1]);
     f.upload(level, v, mask);

@@ -38,6 +38,8 @@ def lib():
             "ref_create": (i, [C.c_char_p, i, i, i, i, i, C.POINTER(C.c_int), C.POINTER(C.c_uint8), i, i,
                                C.POINTER(p)]),
             "ref_destroy": (None, [p]),
+            "ref_create_kind": (i, [C.c_char_p, i, i, i, i, i, C.POINTER(C.c_int), C.POINTER(C.c_uint8), i, i, i,
+                                    C.POINTER(p)]),
             "ref_owned": (i64, [p, i]),
             "ref_set": (i, [p, i, i, pd]),
             "ref_get": (i, [p, i, i, pd]),
@@ -126,13 +128,13 @@ class RefSession:
     """Reference domain + controller + nfuncs functions + LAPLACE operator."""
 
     def __init__(self, mesh: str, ranks: int, min_level: int, max_level: int, nfuncs: int = 4,
-                 bc: dict | None = None, partitioner: int = 0, weight_level: int = 1):
+                 bc: dict | None = None, partitioner: int = 0, weight_level: int = 1, kind: int = 0):
         bc = bc or {}
         m = (C.c_int * max(len(bc), 1))(*bc.keys())
         f = (C.c_uint8 * max(len(bc), 1))(*bc.values())
         h = C.c_void_p()
-        _ck(lib().ref_create(mesh.encode(), ranks, partitioner, weight_level, min_level, max_level, m, f, len(bc),
-                             nfuncs, C.byref(h)))
+        _ck(lib().ref_create_kind(mesh.encode(), ranks, partitioner, weight_level, min_level, max_level, m, f,
+                                  len(bc), nfuncs, kind, C.byref(h)))
         self.h = h
         self.min_level, self.max_level = min_level, max_level
 

@@ -56,6 +56,7 @@ struct Session {
     std::unique_ptr<Controller> ctl;
     BoundaryConditions bc;
     int min_level = 0, max_level = 0;
+    FunctionKind kind = FunctionKind::P1;
     std::vector<std::unique_ptr<ScalarFunction>> f;
     std::unique_ptr<StencilOperator> A;
     // composed V-cycle scratch (GridHierarchy's r_, b_, e_)
@@ -76,7 +77,7 @@ void move_owned(Session& s, int fi, int level, double* data, bool to_field) {
     for (const PrimitiveID id : ids_sorted(*s.dom)) {
         const Primitive& p = s.dom->primitive(id);
         auto& vals = fn.values(id, level);
-        for_each_owned(FunctionKind::P1, p.kind, p.info, level, fn.layout(), [&](std::size_t slot) {
+        for_each_owned(fn.kind(), p.kind, p.info, level, fn.layout(), [&](std::size_t slot) {
             if (to_field) vals[slot] = data[pos];
             else data[pos] = vals[slot];
             ++pos;
@@ -122,10 +123,11 @@ int ref_partition(const char* mesh, int ranks, int partitioner, int weight_level
 }
 
 // partitioner: 0 round robin, 1 greedy edge cut (weights at weight_level)
-int ref_create(const char* mesh, int ranks, int partitioner, int weight_level, int min_level, int max_level,
-               const int* bc_markers, const uint8_t* bc_flags, int nbc, int nfuncs, void** out) {
+int ref_create_kind(const char* mesh, int ranks, int partitioner, int weight_level, int min_level, int max_level,
+                    const int* bc_markers, const uint8_t* bc_flags, int nbc, int nfuncs, int kind, void** out) {
     return guard([&] {
         auto s = std::make_unique<Session>();
+        s->kind = FunctionKind(kind);
         s->setup = build_setup_graph(parse_mesh_string(mesh));
         const Assignment a = partitioner == 1
                                  ? partition_greedy_edgecut(s->setup,
@@ -138,13 +140,19 @@ int ref_create(const char* mesh, int ranks, int partitioner, int weight_level, i
         s->min_level = min_level;
         s->max_level = max_level;
         for (int i = 0; i < nfuncs; ++i) {
-            s->f.push_back(std::make_unique<ScalarFunction>("f" + std::to_string(i), *s->dom, FunctionKind::P1,
+            s->f.push_back(std::make_unique<ScalarFunction>("f" + std::to_string(i), *s->dom, s->kind,
                                                             min_level, max_level, s->bc));
             register_function(*s->ctl, *s->f.back());
         }
-        s->A = std::make_unique<StencilOperator>(*s->dom, Form::LAPLACE, FunctionKind::P1, min_level, max_level, s->bc);
+        s->A = std::make_unique<StencilOperator>(*s->dom, Form::LAPLACE, s->kind, min_level, max_level, s->bc);
         *out = s.release();
     });
+}
+
+int ref_create(const char* mesh, int ranks, int partitioner, int weight_level, int min_level, int max_level,
+               const int* bc_markers, const uint8_t* bc_flags, int nbc, int nfuncs, void** out) {
+    return ref_create_kind(mesh, ranks, partitioner, weight_level, min_level, max_level, bc_markers, bc_flags, nbc,
+                           nfuncs, 0, out);
 }
 
 void ref_destroy(void* s) { delete static_cast<Session*>(s); }
@@ -154,7 +162,7 @@ int64_t ref_owned(void* sp, int level) {
     int64_t n = 0;
     for (const PrimitiveID id : ids_sorted(*s.dom)) {
         const Primitive& p = s.dom->primitive(id);
-        for_each_owned(FunctionKind::P1, p.kind, p.info, level, row_major_layout(), [&](std::size_t) { ++n; });
+        for_each_owned(s.kind, p.kind, p.info, level, row_major_layout(), [&](std::size_t) { ++n; });
     }
     return n;
 }
@@ -172,7 +180,7 @@ int ref_flags(void* sp, int fi, int level, uint8_t* out) {
         for (const PrimitiveID id : ids_sorted(*s.dom)) {
             const Primitive& p = s.dom->primitive(id);
             const auto& fl = s.f.at(size_t(fi))->flags(id, level);
-            for_each_owned(FunctionKind::P1, p.kind, p.info, level, row_major_layout(),
+            for_each_owned(s.kind, p.kind, p.info, level, row_major_layout(),
                            [&](std::size_t slot) { out[pos++] = fl[slot]; });
         }
     });
@@ -184,7 +192,7 @@ int ref_coords(void* sp, int level, double* xy) {
         size_t pos = 0;
         for (const PrimitiveID id : ids_sorted(*s.dom)) {
             const Primitive& p = s.dom->primitive(id);
-            for_each_owned_coord(FunctionKind::P1, p.kind, p.info, level, row_major_layout(),
+            for_each_owned_coord(s.kind, p.kind, p.info, level, row_major_layout(),
                                  [&](std::size_t, double x, double y) {
                                      xy[2 * pos] = x;
                                      xy[2 * pos + 1] = y;
@@ -248,7 +256,7 @@ int ref_set_form(void* sp, int form) {
     return guard([&] {
         Session& s = *static_cast<Session*>(sp);
         if (form < 0 || form > 6) throw std::invalid_argument("ref_set_form: bad form");
-        s.A = std::make_unique<StencilOperator>(*s.dom, Form(form), FunctionKind::P1, s.min_level, s.max_level,
+        s.A = std::make_unique<StencilOperator>(*s.dom, Form(form), s.kind, s.min_level, s.max_level,
                                                 s.bc);
     });
 }
@@ -479,7 +487,7 @@ int ref_fill_keyed(void* sp, int fi, int level, uint64_t seed, uint64_t stream, 
 int ref_diagonal(void* sp, int form, int d, int level) {
     return guard([&] {
         Session& s = *static_cast<Session*>(sp);
-        StencilOperator A(*s.dom, form == 1 ? Form::MASS : Form::LAPLACE, FunctionKind::P1, s.min_level,
+        StencilOperator A(*s.dom, form == 1 ? Form::MASS : Form::LAPLACE, s.kind, s.min_level,
                           s.max_level, s.bc);
         diagonal(A, *s.f.at(size_t(d)), level);
     });

@@ -135,6 +135,10 @@ _SIGS = {
     "hyb_hierarchy_solve": (_i, [_p, _p, _p, _i, _d, _i, _i, _i, _pd, C.POINTER(_i), C.POINTER(_i)]),
     "hyb_hierarchy_fmg": (_i, [_p, _p, _p, _i, _i, _i, _i, _d, _i, _pd, C.POINTER(_i), C.POINTER(_i)]),
     "hyb_hierarchy_pcg": (_i, [_p, _p, _p, _i, _i, _i, _i, _d, _pd, C.POINTER(_i), C.POINTER(_i)]),
+    "hyb_function_create_kind": (_i, [_p, _cs, _i, _i, _i, _pi32, _pu8, _i, C.POINTER(_p)]),
+    "hyb_function_kind": (_i, [_p, C.POINTER(_i)]),
+    "hyb_owned_coords_kind": (_i, [_p, _i, _i, _i, _pd, _i64]),
+    "hyb_operator_create_kind": (_i, [_p, _i, _i, _i, _i, _pi32, _pu8, _i, C.POINTER(_p)]),
     "hyb_stokes_create": (_i, [_p, _i, _i, _pi32, _pu8, _i, _pi32, _pu8, _i, _i, _i, _d, C.POINTER(_p)]),
     "hyb_stokes_destroy": (_i, [_p]),
     "hyb_uzawa_smooth": (_i, [_p, C.POINTER(_p), C.POINTER(_p), _i, _d]),

@@ -380,12 +380,19 @@ int hyb_kernel_launches(int64_t* count) {
 }
 
 int hyb_owned_coords(hyb_domain* dh, int level, int global_order, double* xy, int64_t n) {
+    return hyb_owned_coords_kind(dh, HYB_P1, level, global_order, xy, n);
+}
+
+int hyb_owned_coords_kind(hyb_domain* dh, int kind, int level, int global_order, double* xy, int64_t n) {
     return guarded([&] {
         need(dh, "hyb_owned_coords");
         hyb::Domain& d = *dh->d;
         const hyb::MacroGraph& g = d.graph();
         const int N = 1 << level;
-        const int64_t want = global_order ? d.owned_total(level) : d.owned_local(level);
+        if (kind != HYB_P1 && kind != HYB_P2) throw hyb::InvalidArgument("hyb_owned_coords: unsupported kind");
+        const bool p2 = kind == HYB_P2;
+        const int ol = p2 ? level + 1 : level; // a P2 level holds P1's level + 1 DoF count
+        const int64_t want = global_order ? d.owned_total(ol) : d.owned_local(ol);
         if (n != want) throw hyb::InvalidArgument("hyb_owned_coords: wrong length");
         int64_t pos = 0;
         auto put = [&](double x, double y) {
@@ -406,11 +413,29 @@ int hyb_owned_coords(hyb_domain* dh, int level, int global_order, double* xy, in
                 const hyb::Vec2 p = a + t * (b - a);
                 put(p.x, p.y);
             }
+            if (p2)
+                for (int i = 0; i < N; ++i) {
+                    const double t = (i + 0.5) / N;
+                    const hyb::Vec2 p = a + t * (b - a);
+                    put(p.x, p.y);
+                }
         }
         for (size_t fi = 0; fi < g.nf(); ++fi) {
             if (!take(g.face_id(fi))) continue;
             const auto& f = g.faces[fi];
             const hyb::Vec2 o = f.coord[0], u = f.coord[1] - f.coord[0], v = f.coord[2] - f.coord[0];
+            auto at = [&](double lx, double ly) {
+                const hyb::Vec2 p = o + (lx / N) * u + (ly / N) * v;
+                put(p.x, p.y);
+            };
+            if (p2) { // groups EH, ED, EV at group_lattice_coord (src/indexing.cpp:85-95)
+                for (int r = 1; r <= N - 1; ++r)
+                    for (int c = 0; c + r <= N - 1; ++c) at(c + 0.5, r);
+                for (int r = 0; r <= N - 2; ++r)
+                    for (int c = 0; c + r <= N - 2; ++c) at(c + 0.5, r + 0.5);
+                for (int r = 0; r <= N - 2; ++r)
+                    for (int c = 1; c + r <= N - 1; ++c) at(c, r + 0.5);
+            }
             for (int r = 1; r <= N - 2; ++r)
                 for (int c = 1; c + r <= N - 1; ++c) {
                     const double lx = c, ly = r;
@@ -423,13 +448,26 @@ int hyb_owned_coords(hyb_domain* dh, int level, int global_order, double* xy, in
 
 int hyb_function_create(hyb_domain* d, const char* name, int min_level, int max_level, const int32_t* bc_markers,
                         const uint8_t* bc_flags, int n_bc, hyb_function** out) {
+    return hyb_function_create_kind(d, name, HYB_P1, min_level, max_level, bc_markers, bc_flags, n_bc, out);
+}
+
+int hyb_function_create_kind(hyb_domain* d, const char* name, int kind, int min_level, int max_level,
+                             const int32_t* bc_markers, const uint8_t* bc_flags, int n_bc, hyb_function** out) {
     return guarded([&] {
         need(d, "hyb_function_create");
+        if (kind != HYB_P1 && kind != HYB_P2) throw hyb::InvalidArgument("ScalarFunction: unsupported function kind");
         auto h = std::make_unique<hyb_function>();
         h->keep = d->d;
         h->f = std::make_unique<hyb::Function>(*d->d, name ? name : "f", min_level, max_level,
-                                               make_bc(bc_markers, bc_flags, n_bc));
+                                               make_bc(bc_markers, bc_flags, n_bc), kind);
         *out = h.release();
+    });
+}
+
+int hyb_function_kind(hyb_function* f, int* kind) {
+    return guarded([&] {
+        need(f, "hyb_function_kind");
+        *kind = f->f->kind();
     });
 }
 
@@ -579,13 +617,19 @@ int hyb_function_set_values(hyb_function* f, uint64_t prim, int level, const dou
 
 int hyb_operator_create(hyb_domain* d, int form, int min_level, int max_level, const int32_t* bc_markers,
                         const uint8_t* bc_flags, int n_bc, hyb_operator** out) {
+    return hyb_operator_create_kind(d, form, HYB_P1, min_level, max_level, bc_markers, bc_flags, n_bc, out);
+}
+
+int hyb_operator_create_kind(hyb_domain* d, int form, int kind, int min_level, int max_level,
+                             const int32_t* bc_markers, const uint8_t* bc_flags, int n_bc, hyb_operator** out) {
     return guarded([&] {
         need(d, "hyb_operator_create");
         if (form < HYB_LAPLACE || form > HYB_PSPG) throw hyb::InvalidArgument("StencilOperator: unsupported form");
+        if (kind != HYB_P1 && kind != HYB_P2) throw hyb::InvalidArgument("StencilOperator: unsupported function kind");
         auto h = std::make_unique<hyb_operator>();
         h->keep = d->d;
         h->a = std::make_unique<hyb::Operator>(*d->d, hyb::Form(form), min_level, max_level,
-                                               make_bc(bc_markers, bc_flags, n_bc));
+                                               make_bc(bc_markers, bc_flags, n_bc), kind);
         *out = h.release();
     });
 }

@@ -1,5 +1,6 @@
 // Device-resident runtime: see domain.hpp.
 #include "domain.hpp"
+#include "p2.hpp"
 
 #include <dlfcn.h>
 
@@ -269,6 +270,53 @@ LevelGeom& Domain::level(int L) {
     return ref;
 }
 
+LevelGeom& Domain::level_p2(int L) {
+    auto it = levels_.find(L + 64);
+    if (it != levels_.end()) return *it->second;
+    if (L < 0 || L > 19) throw OutOfRange("level " + std::to_string(L) + " unsupported");
+    auto lg = std::make_unique<LevelGeom>();
+    const HostLayout lay = plan_layout_p2(g_, place_, L);
+    lg->p2 = true;
+    LevelTables& t = lg->t;
+    t.level = L;
+    t.n = lay.n;
+    t.W = lay.W;
+    t.nfaces = int(place_.faces.size());
+    t.nedges = int(place_.edges.size());
+    t.nverts = int(place_.verts.size());
+    t.face_stride = lay.face_stride;
+    t.faces_size = lay.faces_size;
+    t.arena_size = lay.arena_size;
+    t.owned_local = lay.owned_local;
+    lg->h_rowoff = lay.rowoff;
+    lg->h_edge_off = lay.edge_off;
+    lg->h_vtx_off = lay.vtx_off;
+    lg->rowoff = upload_vec(lay.rowoff, stream_);
+    lg->edge_off = upload_vec(lay.edge_off, stream_);
+    lg->edge_nf = upload_vec(lay.edge_nf, stream_);
+    lg->vtx_off = upload_vec(lay.vtx_off, stream_);
+    lg->vtx_coef_off = upload_vec(lay.vtx_coef_off, stream_);
+    lg->vtx_ne = upload_vec(lay.vtx_ne, stream_);
+    lg->face_gid = upload_vec(place_.faces, stream_);
+    lg->edge_gid = upload_vec(place_.edges, stream_);
+    lg->vtx_gid = upload_vec(place_.verts, stream_);
+    t.rowoff = lg->rowoff.as<int64_t>();
+    t.edge_off = lg->edge_off.as<int64_t>();
+    t.edge_nf = lg->edge_nf.as<int8_t>();
+    t.vtx_off = lg->vtx_off.as<int64_t>();
+    t.vtx_ne = lg->vtx_ne.as<int32_t>();
+    t.vtx_coef_off = lg->vtx_coef_off.as<int64_t>();
+    t.face_gid = lg->face_gid.as<uint64_t>();
+    t.edge_gid = lg->edge_gid.as<uint64_t>();
+    t.vtx_gid = lg->vtx_gid.as<uint64_t>();
+    build_exchange(*lg, lay);
+    lg->h_owned_pos = owned_positions_p2(place_, lay);
+    lg->owned_pos = upload_vec(lg->h_owned_pos, stream_);
+    auto& ref = *lg;
+    levels_[L + 64] = std::move(lg);
+    return ref;
+}
+
 void nccl_group_exchange(void* comm_, cudaStream_t st, double* sb, double* rb, const std::vector<ExBlock>& sends,
                          const std::vector<ExBlock>& recvs) {
     auto& api = nccl();
@@ -281,12 +329,13 @@ void nccl_group_exchange(void* comm_, cudaStream_t st, double* sb, double* rb, c
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
 }
 
-DevMem& Domain::jacobi_scratch(int L) {
-    auto it = jacobi_.find(L);
+DevMem& Domain::jacobi_scratch(int L, int kind) {
+    const int key = L + 64 * kind;
+    auto it = jacobi_.find(key);
     if (it != jacobi_.end()) return it->second;
-    DevMem m(size_t(level(L).t.arena_size) * 8);
+    DevMem m(size_t(geom(kind, L).t.arena_size) * 8);
     HYB_CUDA(cudaMemsetAsync(m.as<void>(), 0, m.bytes(), stream_));
-    return jacobi_[L] = std::move(m);
+    return jacobi_[key] = std::move(m);
 }
 
 double* Domain::staging(int64_t doubles) {
@@ -437,13 +486,15 @@ float Domain::event_elapsed(int a, int b) {
 }
 
 // ---------------------------------------------------------------- Function
-Function::Function(Domain& d, std::string name, int min_level, int max_level, BoundaryMap bc)
-    : dom_(&d), name_(std::move(name)), min_(min_level), max_(max_level), bc_(std::move(bc)) {
+Function::Function(Domain& d, std::string name, int min_level, int max_level, BoundaryMap bc, int kind)
+    : dom_(&d), name_(std::move(name)), min_(min_level), max_(max_level), bc_(std::move(bc)), kind_(kind) {
     if (min_ < 0 || max_ < min_)
         throw InvalidArgument("ScalarFunction '" + name_ + "': bad level range [" + std::to_string(min_) + ", " +
                               std::to_string(max_) + "]");
+    if (kind_ != KIND_P1 && kind_ != KIND_P2)
+        throw InvalidArgument("ScalarFunction '" + name_ + "': unsupported function kind");
     for (int L = min_; L <= max_; ++L) {
-        DevMem m(size_t(d.level(L).t.arena_size) * 8);
+        DevMem m(size_t(d.geom(kind_, L).t.arena_size) * 8);
         HYB_CUDA(cudaMemsetAsync(m.as<void>(), 0, m.bytes(), d.stream())); // zero-initialised like the reference
         arenas_.push_back(std::move(m));
     }
@@ -456,6 +507,16 @@ Function::Function(Domain& d, std::string name, int min_level, int max_level, Bo
     vtx_flag_ = DevMem(std::max<size_t>(vf.size(), 1));
     if (!ef.empty()) HYB_CUDA(cudaMemcpy(edge_flag_.as<void>(), ef.data(), ef.size(), cudaMemcpyHostToDevice));
     if (!vf.empty()) HYB_CUDA(cudaMemcpy(vtx_flag_.as<void>(), vf.data(), vf.size(), cudaMemcpyHostToDevice));
+    if (kind_ == KIND_P2) // per owned DoF, owned_pos order: vertex, edge (line + midline), face (INNER)
+        for (int L = min_; L <= max_; ++L) {
+            const int n = 1 << L;
+            std::vector<uint8_t> of;
+            of.reserve(size_t(d.geom(kind_, L).t.owned_local));
+            for (uint8_t f : vf) of.push_back(f);
+            for (uint8_t f : ef) of.insert(of.end(), size_t(2 * n - 1), f);
+            of.resize(size_t(d.geom(kind_, L).t.owned_local), INNER);
+            owned_flag_.push_back(upload_vec(of, d.stream()));
+        }
 }
 
 void Function::check_level(int level, const char* op) const {
@@ -475,12 +536,87 @@ DevMem& Function::arena(int level) {
 double* Function::raw(int level) const { return arenas_.at(size_t(level - min_)).as<double>(); }
 
 // ---------------------------------------------------------------- Operator
-Operator::Operator(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc)
-    : dom_(&d), form_(form), min_(min_level), max_(max_level), bc_(std::move(bc)) {
+Operator::Operator(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc, int kind)
+    : dom_(&d), form_(form), min_(min_level), max_(max_level), bc_(std::move(bc)), kind_(kind) {
     if (min_ < 0 || max_ < min_)
         throw InvalidArgument("StencilOperator: bad level range [" + std::to_string(min_) + ", " +
                               std::to_string(max_) + "]");
+    if (kind_ != KIND_P1 && kind_ != KIND_P2) throw InvalidArgument("StencilOperator: unsupported function kind");
     const MacroGraph& g = d.graph();
+    if (kind_ == KIND_P2) {
+        // assemble_stencils with FunctionKind::P2 (reference src/operators.cpp:342-352)
+        for (int L = min_; L <= max_; ++L) {
+            P2Lv lv;
+            std::vector<P2FaceCoef> fc;
+            for (uint64_t id : d.local_faces()) {
+                const P2FaceStencil s = assemble_p2_face(form, g.faces[g.face_index(id)], L);
+                P2FaceCoef c{};
+                for (int k = 0; k < 4; ++k) {
+                    if (s.cls[k].size() > size_t(P2_MAX_FACE_TERMS)) throw LogicError("P2 face stencil too wide");
+                    c.nt[k] = int(s.cls[k].size());
+                    for (size_t q = 0; q < s.cls[k].size(); ++q) {
+                        c.c[k][q] = s.cls[k][q].coeff;
+                        c.dc[k][q] = int8_t(s.cls[k][q].dc);
+                        c.dr[k][q] = int8_t(s.cls[k][q].dr);
+                    }
+                    c.diag[k] = s.diag[k];
+                    lv.hdiag.push_back(s.diag[k]);
+                }
+                fc.push_back(c);
+            }
+            std::vector<P2EdgeCoef> ec;
+            for (uint64_t id : d.local_edges()) {
+                const P2EdgeStencil s = assemble_p2_edge(form, g.edges[g.edge_index(id)], L);
+                if (s.line.size() > size_t(P2_MAX_EDGE_TERMS) || s.mid.size() > size_t(P2_MAX_EDGE_TERMS))
+                    throw LogicError("P2 edge stencil too wide");
+                P2EdgeCoef c{};
+                c.nl = int(s.line.size());
+                c.nm = int(s.mid.size());
+                for (size_t q = 0; q < s.line.size(); ++q) {
+                    c.lc[q] = s.line[q].coeff;
+                    c.lb[q] = s.line[q].base;
+                    c.ld[q] = s.line[q].dk;
+                }
+                for (size_t q = 0; q < s.mid.size(); ++q) {
+                    c.mc[q] = s.mid[q].coeff;
+                    c.mb[q] = s.mid[q].base;
+                    c.md[q] = s.mid[q].dk;
+                }
+                c.ldiag = s.line_diag;
+                c.mdiag = s.mid_diag;
+                lv.hdiag.push_back(s.line_diag);
+                lv.hdiag.push_back(s.mid_diag);
+                ec.push_back(c);
+            }
+            std::vector<int> toff{0}, slot;
+            std::vector<double> coef, vdiag;
+            for (uint64_t id : d.local_verts()) {
+                const P2VertexStencil s = assemble_p2_vertex(form, g.vertices[id], L);
+                for (const auto& [sl, cf] : s.terms) {
+                    slot.push_back(sl);
+                    coef.push_back(cf);
+                }
+                toff.push_back(int(slot.size()));
+                vdiag.push_back(s.diag);
+                lv.hdiag.push_back(s.diag);
+            }
+            if (fc.empty()) fc.resize(1);
+            if (ec.empty()) ec.resize(1);
+            if (slot.empty()) {
+                slot.push_back(0);
+                coef.push_back(0.0);
+            }
+            if (vdiag.empty()) vdiag.push_back(0.0);
+            lv.face = upload_vec(fc, d.stream());
+            lv.edge = upload_vec(ec, d.stream());
+            lv.vtoff = upload_vec(toff, d.stream());
+            lv.vslot = upload_vec(slot, d.stream());
+            lv.vcoef = upload_vec(coef, d.stream());
+            lv.vdiag = upload_vec(vdiag, d.stream());
+            p2_.push_back(std::move(lv));
+        }
+        return;
+    }
     for (int L = min_; L <= max_; ++L) {
         Lv lv;
         for (uint64_t id : d.local_faces()) {
@@ -505,9 +641,26 @@ Operator::Operator(Domain& d, Form form, int min_level, int max_level, BoundaryM
     }
 }
 
+P2Tables Operator::tables_p2(int level) const {
+    if (level < min_ || level > max_)
+        throw OutOfRange("StencilOperator: no stencil at level " + std::to_string(level));
+    if (kind_ != KIND_P2) throw InvalidArgument("StencilOperator: not a P2 operator");
+    P2Tables T;
+    T.t = dom_->level_p2(level).t;
+    const P2Lv& lv = p2_[size_t(level - min_)];
+    T.face = lv.face.as<P2FaceCoef>();
+    T.edge = lv.edge.as<P2EdgeCoef>();
+    T.vtx_term_off = lv.vtoff.as<int>();
+    T.vtx_slot = lv.vslot.as<int>();
+    T.vtx_coef = lv.vcoef.as<double>();
+    T.vtx_diag = lv.vdiag.as<double>();
+    return T;
+}
+
 LevelTables Operator::tables(int level) const {
     if (level < min_ || level > max_)
         throw OutOfRange("StencilOperator: no stencil at level " + std::to_string(level));
+    if (kind_ != KIND_P1) throw InvalidArgument("StencilOperator: P1 tables of a P2 operator");
     LevelGeom& lg = dom_->level(level);
     LevelTables t = lg.t;
     const Lv& lv = lv_[size_t(level - min_)];

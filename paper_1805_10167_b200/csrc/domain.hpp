@@ -67,6 +67,9 @@ struct LevelGeom {
     LevelTables t; // geometry part (coefficient pointers left null)
     DevMem rowoff, edge_off, edge_nf, vtx_off, vtx_ne, vtx_coef_off, face_gid, edge_gid, vtx_gid;
     std::vector<int64_t> h_rowoff, h_edge_off, h_vtx_off;
+    DevMem owned_pos;                  // P2 levels: arena slot of each owned DoF, P2 GlobalDoFMap order
+    std::vector<int64_t> h_owned_pos;
+    bool p2 = false;
     Exchange xch;
     Exchange xdir[4];            // one relay direction each (sync_directions), built on first use
     bool xdir_built[4] = {false, false, false, false};
@@ -76,9 +79,15 @@ struct LevelGeom {
 
 class Domain;
 
+/// FunctionKind (reference include/hytegrid/indexing.hpp:28)
+enum FunctionKind : int { KIND_P1 = 0, KIND_P2 = 1 };
+
 class Function {
   public:
-    Function(Domain& d, std::string name, int min_level, int max_level, BoundaryMap bc);
+    Function(Domain& d, std::string name, int min_level, int max_level, BoundaryMap bc, int kind = KIND_P1);
+    int kind() const { return kind_; }
+    /// P2: flag of each owned DoF (owned_pos order) at `level`
+    const uint8_t* owned_flags(int level) const { return owned_flag_.at(size_t(level - min_)).as<uint8_t>(); }
     Domain& domain() const { return *dom_; }
     const std::string& name() const { return name_; }
     int min_level() const { return min_; }
@@ -100,11 +109,19 @@ class Function {
     BoundaryMap bc_;
     std::vector<DevMem> arenas_;
     DevMem edge_flag_, vtx_flag_;
+    int kind_ = KIND_P1;
+    std::vector<DevMem> owned_flag_; // P2 only
 };
 
 class Operator {
   public:
-    Operator(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc);
+    Operator(Domain& d, Form form, int min_level, int max_level, BoundaryMap bc, int kind = KIND_P1);
+    int kind() const { return kind_; }
+    /// P2 tables of `level` (geometry + coefficients)
+    P2Tables tables_p2(int level) const;
+    /// host copies of the P2 diagonals: faces [nfaces][4 classes], edges
+    /// [nedges][2] (vertex rows, midline rows), vertices [nverts]
+    const std::vector<double>& host_p2_diag(int level) const { return p2_.at(size_t(level - min_)).hdiag; }
     Domain& domain() const { return *dom_; }
     int min_level() const { return min_; }
     int max_level() const { return max_; }
@@ -127,6 +144,12 @@ class Operator {
     int min_, max_;
     BoundaryMap bc_;
     std::vector<Lv> lv_;
+    int kind_ = KIND_P1;
+    struct P2Lv {
+        DevMem face, edge, vtoff, vslot, vcoef, vdiag;
+        std::vector<double> hdiag;
+    };
+    std::vector<P2Lv> p2_;
 };
 
 struct KernelTimer {
@@ -156,6 +179,9 @@ class Domain {
     int local_index(uint64_t gid) const { return place_.lidx[size_t(gid)]; }
 
     LevelGeom& level(int L);
+    /// geometry of a P2 level (plan_layout_p2)
+    LevelGeom& level_p2(int L);
+    LevelGeom& geom(int kind, int L) { return kind == KIND_P2 ? level_p2(L) : level(L); }
     int64_t owned_total(int L) const;  // all primitives of the graph
     int64_t owned_local(int L);        // this process's primitives
 
@@ -171,7 +197,7 @@ class Domain {
     void sync_directions(Function& f, int level, const int* dirs, int n);
 
     // scratch
-    DevMem& jacobi_scratch(int level);
+    DevMem& jacobi_scratch(int level, int kind = KIND_P1);
     /// exchange staging (reallocated when a level with more traffic is built:
     /// part of the V-cycle graph key)
     const void* send_buffer() const { return sendbuf_.as<void>(); }
@@ -250,7 +276,7 @@ class Domain {
     Placement place_;
     DevMem geo_;
     std::map<int, std::unique_ptr<LevelGeom>> levels_;
-    std::map<int, DevMem> jacobi_;
+    std::map<int, DevMem> jacobi_; // key level + 64 * kind
     DevMem staging_, partials_, scalars_, sendbuf_, recvbuf_;
     void* nccl_comm_ = nullptr;
     std::vector<KernelTimer> pending_;

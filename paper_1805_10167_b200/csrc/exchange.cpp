@@ -27,7 +27,8 @@ void fill_exchange(Exchange& X, HostExchange&& h, int64_t arena_size, cudaStream
 } // namespace
 
 void Domain::build_exchange(LevelGeom& lg, const HostLayout& lay) {
-    HostExchange h = plan_exchange(g_, rank_of_, local_ranks_, place_, lay);
+    HostExchange h = lay.p2 ? plan_exchange_p2(g_, rank_of_, local_ranks_, place_, lay)
+                            : plan_exchange(g_, rank_of_, local_ranks_, place_, lay);
     lg.send_size = h.send_size;
     lg.recv_size = h.recv_size;
     if (int64_t(sendbuf_.bytes() / 8) < h.send_size) sendbuf_ = DevMem(size_t(h.send_size) * 8);
@@ -40,7 +41,7 @@ void Domain::build_exchange(LevelGeom& lg, const HostLayout& lay) {
 // processes), then one gather fills every ghost slot from its owner.
 void Domain::sync(Function& f, int L) {
     f.check_level(L, "sync");
-    run_exchange(level(L).xch, f.data(L));
+    run_exchange(geom(f.kind(), L).xch, f.data(L));
 }
 
 void Domain::run_exchange(Exchange& X, double* arena) {
@@ -65,6 +66,7 @@ void Domain::run_exchange(Exchange& X, double* arena) {
 // round is exactly the reference's pack/unpack of that direction
 void Domain::sync_directions(Function& f, int L, const int* dirs, int n) {
     f.check_level(L, "sync");
+    if (f.kind() != KIND_P1) throw InvalidArgument("sync: single relay directions are provided for P1 functions");
     for (int i = 0; i < n; ++i)
         if (dirs[i] < 0 || dirs[i] > 3) throw InvalidArgument("sync: not a sync direction");
     LevelGeom& lg = level(L);

@@ -1796,4 +1796,6 @@ void launch_coarse_minres(int64_t n, const int32_t* rowptr, const int32_t* col, 
     check_launch("coarse minres");
 }
 
+#include "p2_kernels.cuh"
+
 } // namespace hyb

@@ -213,6 +213,41 @@ void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, cons
                       double* x, double* r, double* p, double* ap, double tol, int max_iter, CoarseStatus* st,
                       double* grid_part, unsigned* grid_bar, int max_row_nnz, cudaStream_t stream);
 // arena[pos[i]] += glob[gidx[i]] where flag[i] & mask
+// ---- P2 (four-group quadratic stencils on the level-(L+1) lattice, p2.hpp) ----
+constexpr int P2_MAX_FACE_TERMS = 20, P2_MAX_EDGE_TERMS = 40;
+struct P2FaceCoef { // per face; classes (c' & 1) + 2 (r' & 1): 0 V, 1 EH, 2 EV, 3 ED
+    double c[4][P2_MAX_FACE_TERMS];
+    int8_t dc[4][P2_MAX_FACE_TERMS], dr[4][P2_MAX_FACE_TERMS];
+    int nt[4];
+    double diag[4];
+};
+struct P2EdgeCoef { // per edge: vertex rows (even k'), midline rows (odd k')
+    double lc[P2_MAX_EDGE_TERMS], mc[P2_MAX_EDGE_TERMS];
+    int lb[P2_MAX_EDGE_TERMS], ld[P2_MAX_EDGE_TERMS], mb[P2_MAX_EDGE_TERMS], md[P2_MAX_EDGE_TERMS];
+    int nl, nm;
+    double ldiag, mdiag;
+};
+struct P2Tables {
+    LevelTables t; // geometry of the P2 level: n = 2^(L+1), rowoff, edge_off, vtx_off
+    const P2FaceCoef* face = nullptr;
+    const P2EdgeCoef* edge = nullptr;
+    const int* vtx_term_off = nullptr; // [nverts + 1]
+    const int* vtx_slot = nullptr;
+    const double* vtx_coef = nullptr;
+    const double* vtx_diag = nullptr;
+};
+constexpr int P2_APPLY = 0, P2_JACOBI = 1;
+/// P2_APPLY: y = A x on rows whose flag is in mask (DIRICHLET rows y = x);
+/// P2_JACOBI: y = x + omega (b - A x) / diag on every owned row (DIRICHLET rows copied)
+void launch_p2(int mode, const P2Tables& T, const FlagTables& fl, const double* x, const double* b, double* y,
+               double omega, uint8_t mask, cudaStream_t st);
+/// smooth_gs on a P2 level, in place
+void launch_p2_gs(const P2Tables& T, const FlagTables& fl, const double* b, double* x, cudaStream_t st);
+/// owned DoFs through explicit arena positions (flag per owned DoF)
+void launch_scatter_pos(int64_t n, const int64_t* pos, const uint8_t* flag, uint8_t mask, const double* packed,
+                        double* arena, cudaStream_t st);
+void launch_gather_pos(int64_t n, const int64_t* pos, const double* arena, double* packed, cudaStream_t st);
+
 /// StokesMultigrid's min-level MINRES (minres_solve, src/solvers.cpp:261-320)
 /// on the constrained monolithic CSR, one CTA, bitwise the reference. b is
 /// the gathered rhs (its pressure mean over [proj_begin, proj_end) removed

@@ -17,6 +17,7 @@ constexpr uint8_t kDirichletMask = DIRICHLET;
 
 void check_op_function(const Operator& A, const Function& f, int level, const char* what, bool check_bc) {
     if (&f.domain() != &A.domain()) throw InvalidArgument(std::string(what) + ": function lives on a different domain");
+    if (f.kind() != A.kind()) throw InvalidArgument(std::string(what) + ": function kind differs from the operator");
     if (level < f.min_level() || level > f.max_level() || level < A.min_level() || level > A.max_level())
         throw OutOfRange(std::string(what) + ": level " + std::to_string(level) + " outside the allocated range");
     if (check_bc && !(f.bc() == A.bc()))
@@ -28,9 +29,40 @@ void check_pair(const char* op, const Function& a, const Function& b, int level)
     b.check_level(level, op);
     if (&a.domain() != &b.domain())
         throw InvalidArgument(std::string(op) + ": '" + a.name() + "' and '" + b.name() + "' live on different domains");
+    if (a.kind() != b.kind())
+        throw InvalidArgument(std::string(op) + ": '" + a.name() + "' and '" + b.name() +
+                              "' have different function kinds");
+}
+
+// operations this engine provides for P1 only (the reference's level
+// transfers are P1-only too, src/solvers.cpp:24-25)
+void require_p1(const Function& f, const char* what) {
+    if (f.kind() != KIND_P1) throw InvalidArgument(std::string(what) + ": provided for P1 functions");
+}
+
+// zero diagonal on a P2 row a smoother would update (src/operators.cpp:457-458)
+void check_diagonals_p2(const Operator& A, const Function& x, int level, const char* what) {
+    Domain& d = A.domain();
+    const MacroGraph& g = d.graph();
+    const auto& h = A.host_p2_diag(level);
+    size_t pos = 0;
+    const int n = 1 << level;
+    for (size_t i = 0; i < d.local_faces().size(); ++i, pos += 4)
+        for (int k = 0; k < 4; ++k)
+            if (n >= 2 && h[pos + size_t(k)] == 0.0) throw RuntimeError(std::string(what) + ": zero diagonal entry");
+    for (size_t i = 0; i < d.local_edges().size(); ++i, pos += 2) {
+        if (x.bc().flag_for(g.edges[g.edge_index(d.local_edges()[i])].marker) & DIRICHLET) continue;
+        if ((n >= 2 && h[pos] == 0.0) || h[pos + 1] == 0.0)
+            throw RuntimeError(std::string(what) + ": zero diagonal entry");
+    }
+    for (size_t i = 0; i < d.local_verts().size(); ++i, ++pos)
+        if (!(x.bc().flag_for(g.vertices[d.local_verts()[i]].marker) & DIRICHLET) && h[pos] == 0.0)
+            throw RuntimeError(std::string(what) + ": zero diagonal entry");
 }
 
 void check_transfer(const Function& coarse, const Function& fine, int lc, const char* what) {
+    if (coarse.kind() != KIND_P1 || fine.kind() != KIND_P1) // reference src/solvers.cpp:24-25
+        throw InvalidArgument(std::string(what) + ": level transfers are defined for P1");
     if (&coarse.domain() != &fine.domain())
         throw InvalidArgument(std::string(what) + ": functions live on different domains");
     if (lc < coarse.min_level() || lc > coarse.max_level() || lc + 1 < fine.min_level() || lc + 1 > fine.max_level())
@@ -79,6 +111,11 @@ void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t m
     if (&src == &dst) throw InvalidArgument("apply: src and dst must be distinct functions");
     Domain& d = A.domain();
     d.sync(src, level); // full schedule first (reference src/operators.cpp:390)
+    if (A.kind() == KIND_P2) {
+        launch_p2(P2_APPLY, A.tables_p2(level), dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0,
+                  mask, d.stream());
+        return;
+    }
     const LevelTables t = A.tables(level);
     d.timer_begin("apply"); // face interiors, then edge/vertex rows as the same launch's trailing CTAs
     launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, mask, d.stream(), 3);
@@ -90,6 +127,7 @@ void residual(const Operator& A, Function& rhs, Function& x, Function& r, int le
     check_op_function(A, x, level, "residual", false);
     check_op_function(A, r, level, "residual", true);
     if (&x == &r || &rhs == &r) throw InvalidArgument("residual: r must be distinct from x and rhs");
+    require_p1(x, "residual (fused)");
     Domain& d = A.domain();
     d.sync(x, level);
     const LevelTables t = A.tables(level);
@@ -103,6 +141,17 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
     check_op_function(A, rhs, level, "smooth_jacobi", true);
     check_op_function(A, x, level, "smooth_jacobi", true);
     if (&rhs == &x) throw InvalidArgument("smooth_jacobi: rhs and x must be distinct functions");
+    if (A.kind() == KIND_P2) {
+        if (dotp) throw InvalidArgument("smooth_jacobi: fused dot provided for P1");
+        check_diagonals_p2(A, x, level, "smooth_jacobi");
+        Domain& d = A.domain();
+        d.sync(x, level);
+        DevMem& next = d.jacobi_scratch(level, KIND_P2);
+        launch_p2(P2_JACOBI, A.tables_p2(level), x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega,
+                  ALL_FLAGS, d.stream());
+        x.arena(level).swap(next);
+        return;
+    }
     check_diagonals(A, x, level, "smooth_jacobi");
     Domain& d = A.domain();
     d.sync(x, level);
@@ -175,6 +224,7 @@ void smooth_jacobi_zero(const Operator& A, Function& rhs, Function& x, double om
     check_op_function(A, rhs, level, "smooth_jacobi", true);
     check_op_function(A, x, level, "smooth_jacobi", true);
     if (&rhs == &x) throw InvalidArgument("smooth_jacobi: rhs and x must be distinct functions");
+    require_p1(x, "smooth_jacobi (from zero)");
     check_diagonals(A, x, level, "smooth_jacobi");
     Domain& d = A.domain();
     DevMem& next = d.jacobi_scratch(level);
@@ -194,6 +244,13 @@ void smooth_gs(const Operator& A, Function& rhs, Function& x, int level) {
     check_op_function(A, rhs, level, "smooth_gs", true);
     check_op_function(A, x, level, "smooth_gs", true);
     if (&rhs == &x) throw InvalidArgument("smooth_gs: rhs and x must be distinct functions");
+    if (A.kind() == KIND_P2) {
+        check_diagonals_p2(A, x, level, "smooth_gs");
+        Domain& d = A.domain();
+        d.sync(x, level);
+        launch_p2_gs(A.tables_p2(level), x.flags(), rhs.data(level), x.data(level), d.stream());
+        return;
+    }
     check_diagonals(A, x, level, "smooth_gs");
     Domain& d = A.domain();
     d.sync(x, level);
@@ -217,6 +274,7 @@ void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level) {
     check_op_function(A, rhs, level, "smooth_cgs", true);
     check_op_function(A, x, level, "smooth_cgs", true);
     if (&rhs == &x) throw InvalidArgument("smooth_cgs: rhs and x must be distinct functions");
+    require_p1(x, "smooth_cgs");
     check_diagonals(A, x, level, "smooth_cgs");
     Domain& d = A.domain();
     d.sync(x, level);
@@ -240,6 +298,34 @@ void diagonal(const Operator& A, Function& dst, int level) {
     Domain& d = A.domain();
     const MacroGraph& g = d.graph();
     const int n = 1 << level;
+    if (A.kind() == KIND_P2) { // packed in the P2 owned order (owned_positions_p2)
+        const auto& h = A.host_p2_diag(level);
+        std::vector<double> packed;
+        packed.reserve(size_t(d.geom(KIND_P2, level).t.owned_local));
+        const size_t nf = d.local_faces().size(), ne = d.local_edges().size();
+        for (size_t i = 0; i < d.local_verts().size(); ++i)
+            packed.push_back((dst.bc().flag_for(g.vertices[d.local_verts()[i]].marker) & DIRICHLET) ? 1.0
+                                                                                                : h[4 * nf + 2 * ne + i]);
+        for (size_t i = 0; i < ne; ++i) {
+            const bool dir = dst.bc().flag_for(g.edges[g.edge_index(d.local_edges()[i])].marker) & DIRICHLET;
+            for (int k = 1; k <= n - 1; ++k) packed.push_back(dir ? 1.0 : h[4 * nf + 2 * i]);
+            for (int m = 0; m < n; ++m) packed.push_back(dir ? 1.0 : h[4 * nf + 2 * i + 1]);
+        }
+        // face groups EH, ED, EV, V (classes 1, 3, 2, 0)
+        for (size_t i = 0; i < nf; ++i) {
+            const double* fd = &h[4 * i];
+            for (int r = 1; r <= n - 1; ++r)
+                for (int c = 0; c + r <= n - 1; ++c) packed.push_back(fd[1]);
+            for (int r = 0; r <= n - 2; ++r)
+                for (int c = 0; c + r <= n - 2; ++c) packed.push_back(fd[3]);
+            for (int r = 0; r <= n - 2; ++r)
+                for (int c = 1; c + r <= n - 1; ++c) packed.push_back(fd[2]);
+            for (int r = 1; r <= n - 2; ++r)
+                for (int c = 1; c + r <= n - 1; ++c) packed.push_back(fd[0]);
+        }
+        upload(dst, level, packed.data(), int64_t(packed.size()), false, ALL_FLAGS);
+        return;
+    }
     std::vector<double> packed(size_t(d.owned_local(level)));
     size_t pos = 0;
     const auto& hv = A.host_vtx_coef(level);
@@ -285,6 +371,17 @@ void prolongate_add_jacobi(const Operator& A, Function& e, Function& rhs, Functi
     check_op_function(A, rhs, level, "smooth_jacobi", true);
     check_op_function(A, x, level, "smooth_jacobi", true);
     if (&rhs == &x) throw InvalidArgument("smooth_jacobi: rhs and x must be distinct functions");
+    if (A.kind() == KIND_P2) {
+        if (dotp) throw InvalidArgument("smooth_jacobi: fused dot provided for P1");
+        check_diagonals_p2(A, x, level, "smooth_jacobi");
+        Domain& d = A.domain();
+        d.sync(x, level);
+        DevMem& next = d.jacobi_scratch(level, KIND_P2);
+        launch_p2(P2_JACOBI, A.tables_p2(level), x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega,
+                  ALL_FLAGS, d.stream());
+        x.arena(level).swap(next);
+        return;
+    }
     check_diagonals(A, x, level, "smooth_jacobi");
     Domain& d = A.domain();
     d.sync(e, lc);
@@ -342,28 +439,28 @@ void assign(double alpha, Function& x1, double beta, Function& x2, Function& dst
     check_pair("assign", x1, x2, level);
     check_pair("assign", x1, dst, level);
     Domain& d = dst.domain();
-    launch_blas1(0, d.level(level).t, dst.flags(), alpha, x1.data(level), beta, x2.data(level), dst.data(level), mask,
+    launch_blas1(0, d.geom(dst.kind(), level).t, dst.flags(), alpha, x1.data(level), beta, x2.data(level), dst.data(level), mask,
                  d.stream());
 }
 
 void add_scaled(Function& dst, double gamma, Function& y, int level, uint8_t mask) {
     check_pair("add_scaled", dst, y, level);
     Domain& d = dst.domain();
-    launch_blas1(1, d.level(level).t, dst.flags(), gamma, y.data(level), 0.0, y.data(level), dst.data(level), mask,
+    launch_blas1(1, d.geom(dst.kind(), level).t, dst.flags(), gamma, y.data(level), 0.0, y.data(level), dst.data(level), mask,
                  d.stream());
 }
 
 void fill_const(Function& f, double value, int level, uint8_t mask) {
     f.check_level(level, "interpolate");
     Domain& d = f.domain();
-    launch_blas1(2, d.level(level).t, f.flags(), value, f.data(level), 0.0, f.data(level), f.data(level), mask,
+    launch_blas1(2, d.geom(f.kind(), level).t, f.flags(), value, f.data(level), 0.0, f.data(level), f.data(level), mask,
                  d.stream());
 }
 
 void fill_random(Function& f, int level, uint64_t seed, uint64_t stream, double lo, double hi, uint8_t mask) {
     f.check_level(level, "interpolate");
     Domain& d = f.domain();
-    launch_random(d.level(level).t, f.flags(), seed, stream, lo, hi, f.data(level), mask, d.stream());
+    launch_random(d.geom(f.kind(), level).t, f.flags(), seed, stream, lo, hi, f.data(level), mask, d.stream());
 }
 
 void fill_expr(Function& f, int level, const Expr& e, uint8_t mask) {
@@ -371,13 +468,13 @@ void fill_expr(Function& f, int level, const Expr& e, uint8_t mask) {
     if (e.kind != EXPR_POLY2 && e.kind != EXPR_SINSIN)
         throw InvalidArgument("interpolate: unknown expression kind " + std::to_string(e.kind));
     Domain& d = f.domain();
-    launch_expr(d.level(level).t, f.flags(), d.geometry(), e, f.data(level), mask, d.stream());
+    launch_expr(d.geom(f.kind(), level).t, f.flags(), d.geometry(), e, f.data(level), mask, d.stream());
 }
 
 namespace {
 void reduce_dev(int op, Function& a, Function& b, int level, double* out) {
     Domain& d = a.domain();
-    const LevelTables& t = d.level(level).t;
+    const LevelTables& t = d.geom(a.kind(), level).t;
     const int64_t np = int64_t(d.graph().size());
     const int bands = t.n >= 3 ? (t.n - 2 + 31) / 32 : 0;
     double* buf = d.partials(2 * np + int64_t(t.nfaces) * bands + 1);
@@ -471,8 +568,11 @@ void global_local(Domain& d, int level, const double* src, double* dst, bool to_
 void upload(Function& f, int level, const double* host, int64_t n, bool global_order, uint8_t mask) {
     f.check_level(level, "upload");
     Domain& d = f.domain();
-    const LevelTables& t = d.level(level).t;
-    const int64_t want = global_order ? d.owned_total(level) : t.owned_local;
+    const LevelGeom& lg = d.geom(f.kind(), level);
+    const LevelTables& t = lg.t;
+    // a P2 level holds the owned set of P1 level + 1 (per primitive counts equal)
+    const int olevel = f.kind() == KIND_P2 ? level + 1 : level;
+    const int64_t want = global_order ? d.owned_total(olevel) : t.owned_local;
     if (n != want)
         throw InvalidArgument("upload: vector has " + std::to_string(n) + " entries, expected " + std::to_string(want));
     double* stage = d.staging(t.owned_local);
@@ -480,11 +580,15 @@ void upload(Function& f, int level, const double* host, int64_t n, bool global_o
         HYB_CUDA(cudaMemcpyAsync(stage, host, size_t(t.owned_local) * 8, cudaMemcpyHostToDevice, d.stream()));
     } else {
         std::vector<double> tmp(size_t(t.owned_local));
-        global_local(d, level, host, tmp.data(), true);
+        global_local(d, olevel, host, tmp.data(), true);
         HYB_CUDA(cudaMemcpyAsync(stage, tmp.data(), tmp.size() * 8, cudaMemcpyHostToDevice, d.stream()));
         HYB_CUDA(cudaStreamSynchronize(d.stream()));
     }
-    launch_scatter_owned(t, f.flags(), stage, f.data(level), mask, d.stream());
+    if (f.kind() == KIND_P2)
+        launch_scatter_pos(t.owned_local, lg.owned_pos.as<int64_t>(), f.owned_flags(level), mask, stage, f.data(level),
+                           d.stream());
+    else
+        launch_scatter_owned(t, f.flags(), stage, f.data(level), mask, d.stream());
 }
 
 // Stream-ordered transfers for pipelines (see Domain::h2d_stream): `host`
@@ -492,6 +596,7 @@ void upload(Function& f, int level, const double* host, int64_t n, bool global_o
 // process owns every primitive); pinned memory makes the copies asynchronous.
 void upload_async(Function& f, int level, const double* host, int64_t n, uint8_t mask) {
     f.check_level(level, "upload_async");
+    require_p1(f, "upload_async");
     Domain& d = f.domain();
     const LevelTables& t = d.level(level).t;
     if (n != t.owned_local)
@@ -506,6 +611,7 @@ void upload_async(Function& f, int level, const double* host, int64_t n, uint8_t
 
 void download_async(Function& f, int level, double* host, int64_t n) {
     f.check_level(level, "download_async");
+    require_p1(f, "download_async");
     Domain& d = f.domain();
     const LevelTables& t = d.level(level).t;
     if (n != t.owned_local)
@@ -521,12 +627,15 @@ void download_async(Function& f, int level, double* host, int64_t n) {
 void download(Function& f, int level, double* host, int64_t n, bool global_order) {
     f.check_level(level, "download");
     Domain& d = f.domain();
-    const LevelTables& t = d.level(level).t;
-    const int64_t want = global_order ? d.owned_total(level) : t.owned_local;
+    const LevelGeom& lg = d.geom(f.kind(), level);
+    const LevelTables& t = lg.t;
+    const int olevel = f.kind() == KIND_P2 ? level + 1 : level;
+    const int64_t want = global_order ? d.owned_total(olevel) : t.owned_local;
     if (n != want)
         throw InvalidArgument("download: vector has " + std::to_string(n) + " entries, expected " + std::to_string(want));
     double* stage = d.staging(t.owned_local);
-    launch_gather_owned(t, f.data(level), stage, d.stream());
+    if (f.kind() == KIND_P2) launch_gather_pos(t.owned_local, lg.owned_pos.as<int64_t>(), f.data(level), stage, d.stream());
+    else launch_gather_owned(t, f.data(level), stage, d.stream());
     if (!global_order || all_local(d)) {
         HYB_CUDA(cudaMemcpyAsync(host, stage, size_t(t.owned_local) * 8, cudaMemcpyDeviceToHost, d.stream()));
         HYB_CUDA(cudaStreamSynchronize(d.stream()));
@@ -534,7 +643,7 @@ void download(Function& f, int level, double* host, int64_t n, bool global_order
         std::vector<double> tmp(size_t(t.owned_local));
         HYB_CUDA(cudaMemcpyAsync(tmp.data(), stage, tmp.size() * 8, cudaMemcpyDeviceToHost, d.stream()));
         HYB_CUDA(cudaStreamSynchronize(d.stream()));
-        global_local(d, level, tmp.data(), host, false);
+        global_local(d, olevel, tmp.data(), host, false);
     }
 }
 

@@ -16,6 +16,8 @@
 //   vertex one ghost per incident edge (its first line DoF next to the vertex)
 #include "plan.hpp"
 
+#include "p2.hpp"
+
 #include <algorithm>
 #include <map>
 
@@ -74,6 +76,30 @@ HostLayout plan_layout(const MacroGraph& g, const Placement& p, int L) {
     h.arena_size = round_up(std::max<int64_t>(pos, 32), 32);
     h.owned_local = int64_t(p.verts.size()) + int64_t(p.edges.size()) * (n - 1) +
                     int64_t(p.faces.size()) * ((int64_t(n) - 1) * (n - 2) / 2);
+    return h;
+}
+
+HostLayout plan_layout_p2(const MacroGraph& g, const Placement& p, int L) {
+    HostLayout h = plan_layout(g, p, L + 1); // faces: the level-(L+1) closed triangles
+    h.p2 = true;
+    h.L = L;
+    const int64_t n2 = h.n;
+    h.edge_off.clear();
+    h.vtx_off.clear();
+    h.vtx_coef_off.clear();
+    int64_t pos = h.faces_size;
+    for (uint64_t id : p.edges) {
+        const MacroEdge& e = g.edges[g.edge_index(id)];
+        h.edge_off.push_back(pos);
+        pos += round_up((n2 + 1) + int64_t(e.faces.size()) * (2 * n2 - 1), 4);
+    }
+    pos = round_up(pos, 32);
+    for (uint64_t id : p.verts) {
+        const MacroVertex& v = g.vertices[id];
+        h.vtx_off.push_back(pos);
+        pos += 1 + 2 * int64_t(v.edges.size()) + int64_t(v.faces.size());
+    }
+    h.arena_size = round_up(std::max<int64_t>(pos, 32), 32);
     return h;
 }
 
@@ -332,6 +358,150 @@ HostExchange plan_exchange(const MacroGraph& g, const std::vector<int>& rank_of,
     X.send_size = so;
     X.recv_size = ro;
     return X;
+}
+
+// Ghost slots per receiver (every process enumerates the same sequence):
+//   face   border rows of slots 0, 1, 2 of the fine triangle (each corner once)
+//   edge   line ends, then per adjacent face fine halo rows 1 and 2 in edge order
+//   vertex per incident edge the next line vertex (fine index 2 from the
+//          vertex) and the midpoint (index 1), then per incident face the
+//          corner cell's interior midpoint (corner_opposite_midpoint,
+//          src/field.cpp:90-100: fine (1,1), (n2-2,1), (1,n2-2))
+// No relevance filter: a vertex's face ghost can be owned by the face's
+// opposite edge (level 0), outside the vertex's closure.
+HostExchange plan_exchange_p2(const MacroGraph& g, const std::vector<int>& rank_of, const std::vector<int>& local_ranks,
+                              const Placement& p, const HostLayout& lay) {
+    const int n2 = lay.n, W = lay.W;
+    auto is_local = [&](int r) { return std::find(local_ranks.begin(), local_ranks.end(), r) != local_ranks.end(); };
+    auto pos_of = [&](const OwnerSlot& o) -> int64_t {
+        const int li = p.lidx[size_t(o.prim)];
+        switch (g.kind_of(o.prim)) {
+        case VERTEX: return lay.vtx_off[size_t(li)];
+        case EDGE: return lay.edge_off[size_t(li)] + o.c;
+        case FACE: return int64_t(li) * lay.face_stride + lay.rowoff[size_t(o.r)] + o.c;
+        }
+        return -1;
+    };
+    HostExchange X;
+    struct Lists {
+        std::vector<int64_t> send_src, recv_dst;
+        int64_t count = 0;
+    };
+    std::map<std::pair<int, int>, Lists> blocks;
+    auto emit = [&](uint64_t rcv, int64_t dst, const OwnerSlot& o) {
+        const int rq = rank_of[size_t(rcv)], rs = rank_of[size_t(o.prim)];
+        const bool rl = is_local(rq), sl = is_local(rs);
+        if (rs == rq) {
+            if (rl) {
+                X.dst.push_back(dst);
+                X.src.push_back(pos_of(o));
+            }
+            return;
+        }
+        if (!(rl || sl)) return;
+        Lists& b = blocks[{rs, rq}];
+        ++b.count;
+        if (sl) b.send_src.push_back(pos_of(o));
+        if (rl) b.recv_dst.push_back(dst);
+    };
+    for (uint64_t id = 0; id < g.size(); ++id) {
+        const int li = p.lidx[size_t(id)];
+        const bool rl = li >= 0;
+        switch (g.kind_of(id)) {
+        case FACE: {
+            const int64_t fb = rl ? int64_t(li) * lay.face_stride : 0;
+            for (int s = 0; s < 3; ++s) {
+                const int w0 = s == 0 ? 0 : 1, w1 = s == 2 ? n2 - 1 : n2;
+                for (int w = w0; w <= w1; ++w) {
+                    const int c = s == 0 ? w : (s == 1 ? 0 : W - 1 - w), r = s == 0 ? 0 : w;
+                    emit(id, rl ? fb + lay.rowoff[size_t(r)] + c : -1, resolve_face(g, id, c, r, n2));
+                }
+            }
+            break;
+        }
+        case EDGE: {
+            const MacroEdge& e = g.edges[g.edge_index(id)];
+            const int64_t eb = rl ? lay.edge_off[size_t(li)] : 0;
+            emit(id, rl ? eb : -1, resolve_edge(g, id, 0, n2));
+            emit(id, rl ? eb + n2 : -1, resolve_edge(g, id, n2, n2));
+            for (size_t j = 0; j < e.faces.size(); ++j) {
+                const FaceSide& fs = e.faces[j];
+                for (int d = 1; d <= 2; ++d) {
+                    const int len = n2 + 1 - d;
+                    const int64_t rb = d == 1 ? p2_edge_halo1(n2, int(j)) : p2_edge_halo1(n2, int(j)) + n2;
+                    for (int q = 0; q < len; ++q) {
+                        const int w = fs.aligned ? q : len - 1 - q;
+                        const int c = fs.slot == 0 ? w : (fs.slot == 1 ? d : n2 - d - w);
+                        const int r = fs.slot == 0 ? d : w;
+                        emit(id, rl ? eb + rb + q : -1, resolve_face(g, fs.face, c, r, n2));
+                    }
+                }
+            }
+            break;
+        }
+        case VERTEX: {
+            const MacroVertex& v = g.vertices[id];
+            const int64_t vb = rl ? lay.vtx_off[size_t(li)] : 0;
+            const int64_t ne = int64_t(v.edges.size());
+            for (size_t j = 0; j < v.edges.size(); ++j) {
+                const MacroEdge& e = g.edges[g.edge_index(v.edges[j])];
+                const bool first = e.v[0] == id;
+                emit(id, rl ? vb + 1 + 2 * int64_t(j) : -1, resolve_edge(g, v.edges[j], first ? 2 : n2 - 2, n2));
+                emit(id, rl ? vb + 2 + 2 * int64_t(j) : -1, resolve_edge(g, v.edges[j], first ? 1 : n2 - 1, n2));
+            }
+            for (size_t f = 0; f < v.faces.size(); ++f) {
+                const int ci = v.faces[f].corner;
+                const int c = ci == 1 ? n2 - 2 : 1, r = ci == 2 ? n2 - 2 : 1;
+                emit(id, rl ? vb + 1 + 2 * ne + int64_t(f) : -1, resolve_face(g, v.faces[f].face, c, r, n2));
+            }
+            break;
+        }
+        }
+    }
+    X.nlocal = int64_t(X.dst.size());
+    int64_t so = 0, ro = 0;
+    for (auto& [key, b] : blocks) {
+        const bool sl = is_local(key.first), rl = is_local(key.second);
+        ExBlock blk{key.first, key.second, sl ? so : -1, rl ? ro : -1, b.count};
+        if (sl) {
+            X.pack.insert(X.pack.end(), b.send_src.begin(), b.send_src.end());
+            so += b.count;
+        }
+        if (rl) {
+            X.dst.insert(X.dst.end(), b.recv_dst.begin(), b.recv_dst.end());
+            ro += b.count;
+        }
+        if (sl && rl) X.inproc.push_back(blk);
+        else if (sl) X.sends.push_back(blk);
+        else X.recvs.push_back(blk);
+    }
+    X.send_size = so;
+    X.recv_size = ro;
+    return X;
+}
+
+std::vector<int64_t> owned_positions_p2(const Placement& p, const HostLayout& lay) {
+    const int n2 = lay.n, n = n2 / 2;
+    std::vector<int64_t> out;
+    out.reserve(size_t(lay.owned_local));
+    for (size_t i = 0; i < p.verts.size(); ++i) out.push_back(lay.vtx_off[i]);
+    for (size_t i = 0; i < p.edges.size(); ++i) {
+        for (int k = 1; k <= n - 1; ++k) out.push_back(lay.edge_off[i] + 2 * k);
+        for (int m = 0; m < n; ++m) out.push_back(lay.edge_off[i] + 2 * m + 1);
+    }
+    for (size_t i = 0; i < p.faces.size(); ++i) {
+        const int64_t fb = int64_t(i) * lay.face_stride;
+        auto at = [&](int fc, int fr) { out.push_back(fb + lay.rowoff[size_t(fr)] + fc); };
+        for (int r = 1; r <= n - 1; ++r) // EH off the bottom line
+            for (int c = 0; c + r <= n - 1; ++c) at(2 * c + 1, 2 * r);
+        for (int r = 0; r <= n - 2; ++r) // ED off the diagonal
+            for (int c = 0; c + r <= n - 2; ++c) at(2 * c + 1, 2 * r + 1);
+        for (int r = 0; r <= n - 2; ++r) // EV off the left line
+            for (int c = 1; c + r <= n - 1; ++c) at(2 * c, 2 * r + 1);
+        for (int r = 1; r <= n - 2; ++r) // interior vertices
+            for (int c = 1; c + r <= n - 1; ++c) at(2 * c, 2 * r);
+    }
+    return out;
 }
 
 std::vector<int64_t> owned_positions(const MacroGraph& g, const Placement& p, const HostLayout& lay) {

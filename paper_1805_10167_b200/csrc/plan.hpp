@@ -28,8 +28,13 @@ struct HostLayout {
     std::vector<int64_t> vtx_coef_off;
     std::vector<int8_t> edge_nf;
     std::vector<int32_t> vtx_ne;
+    bool p2 = false; // a P2 level (see p2.hpp): n = 2^(L+1) fine lattice
 };
 HostLayout plan_layout(const MacroGraph& g, const Placement& p, int L);
+/// P2 functions at level L (p2.hpp): faces and edge lines of the level-(L+1)
+/// lattice, edges with fine halo rows 1 and 2 per face, vertices with the
+/// reference's P2 ghosts (own, 2 per incident edge, 1 per incident face)
+HostLayout plan_layout_p2(const MacroGraph& g, const Placement& p, int L);
 
 /// Owner of a DoF: vertex (c = r = 0), edge line index c, face lattice (c, r).
 struct OwnerSlot {
@@ -62,6 +67,14 @@ struct HostExchange {
 /// it writes from the sender's own storage (see emit_direction in plan.cpp)
 HostExchange plan_exchange(const MacroGraph& g, const std::vector<int>& rank_of, const std::vector<int>& local_ranks,
                            const Placement& p, const HostLayout& lay, int direction = -1);
+
+/// one-round refresh of a P2 level: every ghost slot from its owner
+HostExchange plan_exchange_p2(const MacroGraph& g, const std::vector<int>& rank_of, const std::vector<int>& local_ranks,
+                              const Placement& p, const HostLayout& lay);
+/// arena slot of each local owned P2 DoF in the reference's P2 GlobalDoFMap
+/// order per primitive (vertex; edge line k = 1..n-1 then midline; face
+/// groups EH, ED, EV, V: for_each_owned, src/layout.cpp:176-237)
+std::vector<int64_t> owned_positions_p2(const Placement& p, const HostLayout& lay);
 
 /// Arena slot / global index of each local owned DoF, in local packed order.
 std::vector<int64_t> owned_positions(const MacroGraph& g, const Placement& p, const HostLayout& lay);

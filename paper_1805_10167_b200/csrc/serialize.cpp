@@ -170,6 +170,7 @@ int local_of(Domain& d, uint64_t id, const char* what) {
 } // namespace
 
 std::vector<uint8_t> serialize_field(Function& f, uint64_t id) {
+    if (f.kind() != KIND_P1) throw InvalidArgument("serialize: provided for P1 functions");
     Domain& d = f.domain();
     const int li = local_of(d, id, "serialize");
     const Kind kind = d.graph().kind_of(id);
@@ -195,6 +196,7 @@ std::vector<uint8_t> serialize_field(Function& f, uint64_t id) {
 }
 
 void deserialize_field(Function& f, uint64_t id, const uint8_t* data, size_t len) {
+    if (f.kind() != KIND_P1) throw InvalidArgument("deserialize: provided for P1 functions");
     Domain& d = f.domain();
     const int li = local_of(d, id, "deserialize");
     const Kind kind = d.graph().kind_of(id);
@@ -258,6 +260,7 @@ void deserialize_field(Function& f, uint64_t id, const uint8_t* data, size_t len
 // is not stored on the device (no P1 kernel reads it) and is reported as the
 // edge's own line, its value after every full sync.
 std::vector<double> primitive_values(Function& f, uint64_t id, int level) {
+    if (f.kind() != KIND_P1) throw InvalidArgument("values: provided for P1 functions");
     Domain& d = f.domain();
     f.check_level(level, "values");
     const int li = local_of(d, id, "values");
@@ -274,6 +277,7 @@ std::vector<double> primitive_values(Function& f, uint64_t id, int level) {
 // writes every slot of the primitive's reference layout (an edge's halo row 0
 // is ignored: not stored)
 void set_primitive_values(Function& f, uint64_t id, int level, const double* v, size_t n_in) {
+    if (f.kind() != KIND_P1) throw InvalidArgument("set_values: provided for P1 functions");
     Domain& d = f.domain();
     f.check_level(level, "values");
     const int li = local_of(d, id, "values");

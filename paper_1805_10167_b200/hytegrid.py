@@ -31,6 +31,7 @@ DIRICHLET = 2
 NEUMANN = 4
 ALL_DOF_FLAGS = 7
 SMOOTH_MASK = INNER | NEUMANN
+P1, P2 = 0, 1  # FunctionKind (reference include/hytegrid/indexing.hpp:28)
 
 LAPLACE = 0
 MASS = 1
@@ -230,10 +231,11 @@ class DistributedDomain:
         check(lib.hyb_domain_arena_bytes(self._h, level, C.byref(b)))
         return b.value
 
-    def coords(self, level: int, global_order: bool = True) -> np.ndarray:
-        n = self.owned_count(level)[0 if global_order else 1]
+    def coords(self, level: int, global_order: bool = True, kind: int = 0) -> np.ndarray:
+        """owned DoF coordinates (for_each_owned_coord, src/layout.cpp:239-282) of a P1 or P2 function"""
+        n = self.owned_count(level + (1 if kind == 1 else 0))[0 if global_order else 1]
         xy = np.zeros((n, 2))
-        check(lib.hyb_owned_coords(self._h, level, int(global_order), _pd(xy), n))
+        check(lib.hyb_owned_coords_kind(self._h, kind, level, int(global_order), _pd(xy), n))
         return xy
 
     def synchronize(self) -> None:
@@ -277,17 +279,20 @@ def register_function(ctl: Controller, f: "ScalarFunction") -> None:  # noqa: AR
 
 
 class ScalarFunction:
-    """P1 grid function: one HBM arena per level (zero-initialised)."""
+    """P1 or P2 grid function: one HBM arena per level (zero-initialised).
+    kind: P1 (default) or P2 (reference FunctionKind, indexing.hpp:28)."""
 
-    def __init__(self, name: str, domain: DistributedDomain, min_level: int, max_level: int, bc: dict | None = None):
+    def __init__(self, name: str, domain: DistributedDomain, min_level: int, max_level: int, bc: dict | None = None,
+                 kind: int = 0):
         self.name = name
         self.domain = domain
         self.min_level = min_level
         self.max_level = max_level
+        self.kind = kind
         self.bc = dict(bc or {})
         m, f, n = _bc_arrays(self.bc)
         h = C.c_void_p()
-        check(lib.hyb_function_create(domain._h, name.encode(), min_level, max_level, m, f, n, C.byref(h)))
+        check(lib.hyb_function_create_kind(domain._h, name.encode(), kind, min_level, max_level, m, f, n, C.byref(h)))
         self._h = h
 
     def __del__(self):
@@ -296,7 +301,8 @@ class ScalarFunction:
             self._h = None
 
     def _n(self, level: int, global_order: bool) -> int:
-        return self.domain.owned_count(level)[0 if global_order else 1]
+        # a P2 function at level L holds the DoF count of P1 at level L + 1
+        return self.domain.owned_count(level + (1 if self.kind == P2 else 0))[0 if global_order else 1]
 
     def upload(self, level: int, values, global_order: bool = True, mask: int = ALL_DOF_FLAGS) -> None:
         v = np.ascontiguousarray(values, dtype=np.float64)
@@ -366,15 +372,16 @@ class StencilOperator:
     """Constant-coefficient P1 operator (LAPLACE or MASS), stencils per level."""
 
     def __init__(self, domain: DistributedDomain, form: int = LAPLACE, min_level: int = 0, max_level: int = 0,
-                 bc: dict | None = None):
+                 bc: dict | None = None, kind: int = 0):
         self.domain = domain
         self.form = form
+        self.kind = kind
         self.min_level = min_level
         self.max_level = max_level
         self.bc = dict(bc or {})
         m, f, n = _bc_arrays(self.bc)
         h = C.c_void_p()
-        check(lib.hyb_operator_create(domain._h, form, min_level, max_level, m, f, n, C.byref(h)))
+        check(lib.hyb_operator_create_kind(domain._h, form, kind, min_level, max_level, m, f, n, C.byref(h)))
         self._h = h
 
     def __del__(self):
@@ -393,7 +400,7 @@ class StencilOperator:
 def interpolate(f: ScalarFunction, expr, level: int, flag_mask: int = ALL_DOF_FLAGS) -> None:
     """Owned DoFs with flag in mask := expr(x, y) (or a constant)."""
     if callable(expr):
-        xy = f.domain.coords(level, global_order=False)
+        xy = f.domain.coords(level, global_order=False, kind=f.kind)
         vals = np.asarray(expr(xy[:, 0], xy[:, 1]), dtype=np.float64)
         if vals.shape != (xy.shape[0],):
             vals = np.array([expr(x, y) for x, y in xy], dtype=np.float64)

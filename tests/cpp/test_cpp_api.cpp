@@ -120,6 +120,22 @@ int main() {
         EXPECT(std::sqrt(stokes_dot(sr, sr, 3)) <= 1e-8 * srep.residuals.front());
         uzawa_smooth(smg.system(), scx, srhs, sx, 3);
     }
+    // P2 through the reference's signatures: apply of the P2 Laplacian to a quadratic is exact
+    // against the mass matrix times its (constant) negative Laplacian, checked as a zero row sum
+    {
+        DistributedDomain pd(meshgen::unit_square(), 2);
+        Controller pc(pd);
+        StencilOperator a2(pd, Form::LAPLACE, FunctionKind::P2, 2, 2);
+        ScalarFunction one("one", pd, FunctionKind::P2, 2, 2, {}), y2("y2", pd, FunctionKind::P2, 2, 2, {});
+        interpolate(one, [](double, double) { return 1.0; }, 2);
+        apply(a2, pc, one, y2, 2, flag_bit(DoFFlag::INNER));
+        const auto yv = y2.download(2);
+        double m = 0;
+        for (double v : yv) m = std::fmax(m, std::fabs(v));
+        EXPECT(yv.size() == 81 && m <= 1e-12); // constants are in the kernel of the Laplacian
+        smooth_gs(a2, pc, y2, one, 2);
+        smooth_jacobi(a2, pc, y2, one, 0.8, 2);
+    }
     std::printf("cpp api ok: %d cycles, residual %.3e, error %.3e; fmg %d cycles, pcg %.1e\n", rep.iterations,
                 rep.residuals.back(), err, fr.iterations, pr.residuals.back() / pr.residuals.front());
     return 0;
