@@ -137,6 +137,15 @@ int hyb_domain_timer_reset(hyb_domain* d);
 /* CUDA events on the domain stream (16 slots) and elapsed ms between two */
 int hyb_domain_event_record(hyb_domain* d, int slot);
 int hyb_domain_event_elapsed(hyb_domain* d, int a, int b, double* ms);
+/* Communication/computation overlap (the paper's Algorithm 3; the reference
+ * syncs before every operator, src/operators.cpp:390): apply, the residual and
+ * the Jacobi sweep compute the primitives whose ghosts all have same-rank
+ * owners while ghosts from other ranks (NCCL between processes, device copies
+ * between co-resident ranks) are in flight on a communication stream, and the
+ * rest after they land. Results are bitwise those of the unsplit launch.
+ * Default on; enable < 0 leaves the setting; *split_launches counts subset
+ * launches so far. */
+int hyb_domain_overlap(hyb_domain* d, int enable, int64_t* split_launches);
 /* kernels launched by this library so far (process-wide) */
 int hyb_kernel_launches(int64_t* count);
 /* coordinates (x, y interleaved) of owned DoFs: for_each_owned_coord

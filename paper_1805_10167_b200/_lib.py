@@ -137,6 +137,7 @@ _SIGS = {
     "hyb_hierarchy_pcg": (_i, [_p, _p, _p, _i, _i, _i, _i, _d, _pd, C.POINTER(_i), C.POINTER(_i)]),
     "hyb_function_create_kind": (_i, [_p, _cs, _i, _i, _i, _pi32, _pu8, _i, C.POINTER(_p)]),
     "hyb_function_kind": (_i, [_p, C.POINTER(_i)]),
+    "hyb_domain_overlap": (_i, [_p, _i, _pi64]),
     "hyb_owned_coords_kind": (_i, [_p, _i, _i, _i, _pd, _i64]),
     "hyb_operator_create_kind": (_i, [_p, _i, _i, _i, _i, _pi32, _pu8, _i, C.POINTER(_p)]),
     "hyb_stokes_create": (_i, [_p, _i, _i, _pi32, _pu8, _i, _pi32, _pu8, _i, _i, _i, _d, C.POINTER(_p)]),

@@ -379,6 +379,14 @@ int hyb_kernel_launches(int64_t* count) {
     return guarded([&] { *count = hyb::kernel_launch_count(); });
 }
 
+int hyb_domain_overlap(hyb_domain* d, int enable, int64_t* split_launches) {
+    return guarded([&] {
+        need(d, "hyb_domain_overlap");
+        if (enable >= 0) d->d->overlap = enable != 0;
+        if (split_launches) *split_launches = d->d->overlap_launches;
+    });
+}
+
 int hyb_owned_coords(hyb_domain* dh, int level, int global_order, double* xy, int64_t n) {
     return hyb_owned_coords_kind(dh, HYB_P1, level, global_order, xy, n);
 }

@@ -125,6 +125,9 @@ Domain::Domain(const std::string& mesh_text, int world_ranks, const std::vector<
     HYB_CUDA(cudaSetDevice(device_));
     HYB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     HYB_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+    HYB_CUDA(cudaStreamCreateWithFlags(&comm_, cudaStreamNonBlocking));
+    HYB_CUDA(cudaEventCreateWithFlags(&ev_packed_, cudaEventDisableTiming));
+    HYB_CUDA(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming));
     HYB_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
     HYB_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
     HYB_CUDA(cudaEventCreateWithFlags(&ev_xfer_, cudaEventDisableTiming));
@@ -150,6 +153,9 @@ Domain::~Domain() {
     if (h2d_) cudaStreamDestroy(h2d_);
     if (d2h_) cudaStreamDestroy(d2h_);
     if (aux_) cudaStreamDestroy(aux_);
+    if (comm_) cudaStreamDestroy(comm_);
+    if (ev_packed_) cudaEventDestroy(ev_packed_);
+    if (ev_comm_) cudaEventDestroy(ev_comm_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 

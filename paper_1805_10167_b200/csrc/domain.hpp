@@ -72,6 +72,17 @@ struct LevelGeom {
     bool p2 = false;
     Exchange xch;
     Exchange xdir[4];            // one relay direction each (sync_directions), built on first use
+    // communication/computation overlap (the paper's Algorithm 3): primitives
+    // whose every ghost has an owner on the same rank ("interior") are
+    // computed while the remote ghosts are in flight; the rest after
+    struct Overlap {
+        bool active = false;     // the level has ghosts from other ranks
+        DevMem lists;            // interior faces | boundary faces | edges | vertices
+        int nf[2] = {0, 0}, ne[2] = {0, 0}, nv[2] = {0, 0};
+        const int32_t* fl[2] = {nullptr, nullptr};
+        const int32_t* el[2] = {nullptr, nullptr};
+        const int32_t* vl[2] = {nullptr, nullptr};
+    } ov;
     bool xdir_built[4] = {false, false, false, false};
     int64_t send_size = 0, recv_size = 0;
 };
@@ -192,6 +203,18 @@ class Domain {
 
     // ghost exchange of one function, full schedule V->E, E->F, F->E, E->V
     void sync(Function& f, int level);
+    /// overlapped form of sync: sync_begin packs, starts the transfers to and
+    /// from other ranks on the communication stream and refreshes the ghosts
+    /// with same-rank owners; sync_end waits for the transfers and refreshes
+    /// the rest. Between the two, only overlap_tables(.., 0) primitives may
+    /// read ghosts. Falls back to sync() when the level has no remote ghosts.
+    bool overlap = true;
+    bool overlap_active(Function& f, int level);
+    void sync_begin(Function& f, int level);
+    void sync_end(Function& f, int level);
+    /// the level's tables restricted to the interior (part 0) or boundary (1) primitives
+    LevelTables overlap_tables(const LevelTables& t, Function& f, int level, int part);
+    int64_t overlap_launches = 0; // subset launches issued (tests)
     // the reference's sync(c, f, level, span<Direction>) (src/function.cpp:234-237):
     // the given relay directions (0 V->E, 1 E->F, 2 F->E, 3 E->V) in order
     void sync_directions(Function& f, int level, const int* dirs, int n);
@@ -263,6 +286,9 @@ class Domain {
     std::map<int, GsPlan> gs_;
     cudaStream_t aux_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    cudaStream_t comm_ = nullptr;
+    cudaEvent_t ev_packed_ = nullptr, ev_comm_ = nullptr;
+    void build_overlap(LevelGeom& lg, const HostLayout& lay, const HostExchange& h);
     cudaEvent_t events_[16] = {};
     void build_exchange(LevelGeom& lg, const HostLayout& lay);
     void run_exchange(Exchange& X, double* arena);

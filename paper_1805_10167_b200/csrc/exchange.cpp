@@ -1,6 +1,8 @@
 // Device side of the one-round ghost exchange (plan: plan.cpp).
 #include "domain.hpp"
 
+#include <algorithm>
+
 namespace hyb {
 
 void nccl_group_exchange(void* comm, cudaStream_t st, double* sb, double* rb, const std::vector<ExBlock>& sends,
@@ -29,6 +31,7 @@ void fill_exchange(Exchange& X, HostExchange&& h, int64_t arena_size, cudaStream
 void Domain::build_exchange(LevelGeom& lg, const HostLayout& lay) {
     HostExchange h = lay.p2 ? plan_exchange_p2(g_, rank_of_, local_ranks_, place_, lay)
                             : plan_exchange(g_, rank_of_, local_ranks_, place_, lay);
+    build_overlap(lg, lay, h);
     lg.send_size = h.send_size;
     lg.recv_size = h.recv_size;
     if (int64_t(sendbuf_.bytes() / 8) < h.send_size) sendbuf_ = DevMem(size_t(h.send_size) * 8);
@@ -58,6 +61,106 @@ void Domain::run_exchange(Exchange& X, double* arena) {
         nccl_group_exchange(nccl_comm_, stream_, sb, rb, X.sends, X.recvs);
     }
     launch_ghost_gather(X.dst.as<void>(), X.src.as<void>(), X.idx32, X.nlocal, X.ntotal, arena, rb, stream_);
+}
+
+// A primitive is "boundary" when one of its ghost slots is filled from the
+// receive buffer (an owner on another rank: a co-resident logical rank or a
+// remote process); every other primitive reads only ghosts with same-rank
+// owners, which the local part of the gather refreshes.
+void Domain::build_overlap(LevelGeom& lg, const HostLayout& lay, const HostExchange& h) {
+    LevelGeom::Overlap& ov = lg.ov;
+    ov = LevelGeom::Overlap{};
+    if (int64_t(h.dst.size()) <= h.nlocal) return;
+    const size_t nf = place_.faces.size(), ne = place_.edges.size(), nv = place_.verts.size();
+    std::vector<char> bf(nf, 0), be(ne, 0), bv(nv, 0);
+    const int64_t edges_end = nv ? lay.vtx_off[0] : lay.arena_size;
+    for (size_t i = size_t(h.nlocal); i < h.dst.size(); ++i) {
+        const int64_t pos = h.dst[i];
+        if (pos < lay.faces_size) {
+            bf[size_t(pos / lay.face_stride)] = 1;
+        } else if (pos < edges_end) {
+            const auto it = std::upper_bound(lay.edge_off.begin(), lay.edge_off.end(), pos);
+            be[size_t(it - lay.edge_off.begin()) - 1] = 1;
+        } else {
+            const auto it = std::upper_bound(lay.vtx_off.begin(), lay.vtx_off.end(), pos);
+            bv[size_t(it - lay.vtx_off.begin()) - 1] = 1;
+        }
+    }
+    std::vector<int32_t> all;
+    int off[7];
+    auto put = [&](const std::vector<char>& b, size_t n, int part) {
+        int cnt = 0;
+        for (size_t i = 0; i < n; ++i)
+            if (b[i] == part) {
+                all.push_back(int32_t(i));
+                ++cnt;
+            }
+        return cnt;
+    };
+    off[0] = 0;
+    ov.nf[0] = put(bf, nf, 0);
+    off[1] = int(all.size());
+    ov.nf[1] = put(bf, nf, 1);
+    off[2] = int(all.size());
+    ov.ne[0] = put(be, ne, 0);
+    off[3] = int(all.size());
+    ov.ne[1] = put(be, ne, 1);
+    off[4] = int(all.size());
+    ov.nv[0] = put(bv, nv, 0);
+    off[5] = int(all.size());
+    ov.nv[1] = put(bv, nv, 1);
+    ov.lists = upload_vec(all, stream_);
+    const int32_t* base = ov.lists.as<int32_t>();
+    ov.fl[0] = base + off[0];
+    ov.fl[1] = base + off[1];
+    ov.el[0] = base + off[2];
+    ov.el[1] = base + off[3];
+    ov.vl[0] = base + off[4];
+    ov.vl[1] = base + off[5];
+    ov.active = true;
+}
+
+bool Domain::overlap_active(Function& f, int L) { return overlap && geom(f.kind(), L).ov.active; }
+
+void Domain::sync_begin(Function& f, int L) {
+    f.check_level(L, "sync");
+    Exchange& X = geom(f.kind(), L).xch;
+    double* arena = f.data(L);
+    double* sb = sendbuf_.as<double>();
+    double* rb = recvbuf_.as<double>();
+    if (X.npack) launch_ghost_pack(X.pack.as<int64_t>(), X.npack, arena, sb, stream_);
+    // transfers on the communication stream, after the pack
+    HYB_CUDA(cudaEventRecord(ev_packed_, stream_));
+    HYB_CUDA(cudaStreamWaitEvent(comm_, ev_packed_, 0));
+    for (const auto& b : X.inproc)
+        HYB_CUDA(cudaMemcpyAsync(rb + b.recv_off, sb + b.send_off, size_t(b.count) * 8, cudaMemcpyDeviceToDevice,
+                                 comm_));
+    if (!X.sends.empty() || !X.recvs.empty()) {
+        if (!nccl_comm_) throw LogicError("sync: remote ranks present but NCCL is not connected");
+        nccl_group_exchange(nccl_comm_, comm_, sb, rb, X.sends, X.recvs);
+    }
+    HYB_CUDA(cudaEventRecord(ev_comm_, comm_));
+    // same-rank ghosts meanwhile (the first nlocal entries of the gather)
+    launch_ghost_gather(X.dst.as<void>(), X.src.as<void>(), X.idx32, X.nlocal, X.nlocal, arena, rb, stream_);
+}
+
+void Domain::sync_end(Function& f, int L) {
+    Exchange& X = geom(f.kind(), L).xch;
+    HYB_CUDA(cudaStreamWaitEvent(stream_, ev_comm_, 0));
+    launch_ghost_recv(X.dst.as<void>(), X.idx32, X.nlocal, X.ntotal, f.data(L), recvbuf_.as<double>(), stream_);
+}
+
+LevelTables Domain::overlap_tables(const LevelTables& t, Function& f, int L, int part) {
+    const LevelGeom::Overlap& ov = geom(f.kind(), L).ov;
+    LevelTables s = t;
+    s.nfaces = ov.nf[part];
+    s.nedges = ov.ne[part];
+    s.nverts = ov.nv[part];
+    s.face_list = ov.fl[part];
+    s.edge_list = ov.el[part];
+    s.vtx_list = ov.vl[part];
+    ++overlap_launches;
+    return s;
 }
 
 // one gather round per relay direction: within a direction no slot is both

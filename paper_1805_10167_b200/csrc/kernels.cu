@@ -48,7 +48,7 @@ __device__ __forceinline__ void ev_stencil_block(const LevelTables& t, const Fla
     const int n = t.n;
     const int eblocks = t.nedges * kblocks;
     if (ev_block < eblocks) {
-        const int e = ev_block / kblocks;
+        const int e = t.edge_list ? t.edge_list[ev_block / kblocks] : ev_block / kblocks;
         const int k = 1 + (ev_block % kblocks) * 128 + int(threadIdx.x);
         if (k > n - 1) return;
         const uint8_t f = fl.edge_flag[e];
@@ -82,8 +82,9 @@ __device__ __forceinline__ void ev_stencil_block(const LevelTables& t, const Fla
         y[off + k] = o;
         return;
     }
-    const int v = (ev_block - eblocks) * 128 + int(threadIdx.x);
-    if (v >= t.nverts) return;
+    const int vi = (ev_block - eblocks) * 128 + int(threadIdx.x);
+    if (vi >= t.nverts) return;
+    const int v = t.vtx_list ? t.vtx_list[vi] : vi;
     const uint8_t f = fl.vtx_flag[v];
     if (!(f & mask)) return;
     const int64_t off = t.vtx_off[v];
@@ -674,6 +675,19 @@ void launch_ghost_gather(const void* dst, const void* src, bool idx32, int64_t n
                                                                    static_cast<const int64_t*>(src), nlocal, ntotal,
                                                                    arena, recv);
     check_launch("ghost gather");
+}
+
+void launch_ghost_recv(const void* dst, bool idx32, int64_t begin, int64_t end, double* arena, const double* recv,
+                       cudaStream_t st) {
+    if (end <= begin) return;
+    const int blocks = grid_for(end - begin, 256, 1 << 30);
+    if (idx32)
+        k_ghost_gather<int32_t><<<blocks, 256, 0, st>>>(static_cast<const int32_t*>(dst) + begin, nullptr, 0,
+                                                        end - begin, arena, recv);
+    else
+        k_ghost_gather<int64_t><<<blocks, 256, 0, st>>>(static_cast<const int64_t*>(dst) + begin, nullptr, 0,
+                                                        end - begin, arena, recv);
+    check_launch("ghost receive gather");
 }
 
 void launch_ghost_pack(const int64_t* src, int64_t n, const double* arena, double* send, cudaStream_t st) {

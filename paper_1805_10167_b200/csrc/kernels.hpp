@@ -44,6 +44,12 @@ struct LevelTables {
     const uint64_t* vtx_gid = nullptr;
     // packed owned order of local primitives: vertices, edges, faces by ID
     int64_t owned_local = 0;
+    // a subset launch (communication/computation overlap): when set, the
+    // launch covers nfaces / nedges / nverts primitives listed here (local
+    // indices); face, edge and vertex tables stay indexed by local index
+    const int32_t* face_list = nullptr;
+    const int32_t* edge_list = nullptr;
+    const int32_t* vtx_list = nullptr;
 };
 
 /// rowoff[r] in closed form (plan_layout, csrc/plan.cpp): sum over i < r of
@@ -98,6 +104,9 @@ int64_t kernel_launch_count();
 /// Ghost refresh, one pass: arena[dst[i]] = arena[src[i]] for i < nlocal
 /// (owner on this process), arena[dst[i]] = recv[i - nlocal] for the rest.
 /// dst/src are int32 (idx32, arenas below 2^31 slots) or int64 arrays.
+/// ghost slots dst[begin, end) from recv[0, end - begin) (the overlapped exchange's second half)
+void launch_ghost_recv(const void* dst, bool idx32, int64_t begin, int64_t end, double* arena, const double* recv,
+                       cudaStream_t st);
 void launch_ghost_gather(const void* dst, const void* src, bool idx32, int64_t nlocal, int64_t ntotal, double* arena,
                          const double* recv, cudaStream_t st);
 /// send[i] = arena[src[i]] (owned values other processes hold ghosts of)

@@ -105,20 +105,43 @@ void check_diagonals(const Operator& A, const Function& x, int level, const char
 
 bool zero_diagonal_row(const Operator& A, const Function& x, int level) { return zero_diagonal_row_impl(A, x, level); }
 
+namespace {
+// The ghost refresh of x and one stencil launch. With other ranks' ghosts in
+// play (Domain::overlap_active) the launch is split: primitives whose ghosts
+// all have same-rank owners run while the transfers are in flight, the others
+// after the receive half of the refresh (the paper's Algorithm 3; the
+// reference itself syncs first, src/operators.cpp:390). Every row is
+// computed from the same values either way: bitwise the unsplit launch.
+template <class Launch> void synced_launch(Domain& d, Function& x, int level, const LevelTables& t, Launch launch) {
+    if (!d.overlap_active(x, level)) {
+        d.sync(x, level);
+        launch(t);
+        return;
+    }
+    d.sync_begin(x, level);
+    launch(d.overlap_tables(t, x, level, 0));
+    d.sync_end(x, level);
+    launch(d.overlap_tables(t, x, level, 1));
+}
+} // namespace
+
 void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t mask) {
     check_op_function(A, src, level, "apply", false);
     check_op_function(A, dst, level, "apply", true);
     if (&src == &dst) throw InvalidArgument("apply: src and dst must be distinct functions");
     Domain& d = A.domain();
-    d.sync(src, level); // full schedule first (reference src/operators.cpp:390)
     if (A.kind() == KIND_P2) {
+        d.sync(src, level); // full schedule first (reference src/operators.cpp:390)
         launch_p2(P2_APPLY, A.tables_p2(level), dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0,
                   mask, d.stream());
         return;
     }
     const LevelTables t = A.tables(level);
     d.timer_begin("apply"); // face interiors, then edge/vertex rows as the same launch's trailing CTAs
-    launch_stencil(ST_APPLY, t, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, mask, d.stream(), 3);
+    synced_launch(d, src, level, t, [&](const LevelTables& tt) {
+        launch_stencil(ST_APPLY, tt, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, mask,
+                       d.stream(), 3);
+    });
     d.timer_end();
 }
 
@@ -129,11 +152,12 @@ void residual(const Operator& A, Function& rhs, Function& x, Function& r, int le
     if (&x == &r || &rhs == &r) throw InvalidArgument("residual: r must be distinct from x and rhs");
     require_p1(x, "residual (fused)");
     Domain& d = A.domain();
-    d.sync(x, level);
     const LevelTables t = A.tables(level);
     d.timer_begin("residual");
-    launch_stencil(ST_RESIDUAL, t, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
-                   d.stream(), 3);
+    synced_launch(d, x, level, t, [&](const LevelTables& tt) {
+        launch_stencil(ST_RESIDUAL, tt, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
+                       d.stream(), 3);
+    });
     d.timer_end();
 }
 
@@ -154,14 +178,15 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
     }
     check_diagonals(A, x, level, "smooth_jacobi");
     Domain& d = A.domain();
-    d.sync(x, level);
     DevMem& next = d.jacobi_scratch(level);
     // pending write-back of the reference (src/operators.cpp:435-468) is a
     // second buffer here: read x, write x', swap.
     const LevelTables t = A.tables(level);
     d.timer_begin("jacobi");
-    launch_stencil(ST_JACOBI, t, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
-                   d.stream(), 3, dotp);
+    synced_launch(d, x, level, t, [&](const LevelTables& tt) {
+        launch_stencil(ST_JACOBI, tt, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
+                       d.stream(), 3, dotp);
+    });
     d.timer_end();
     x.arena(level).swap(next);
 }

@@ -238,6 +238,13 @@ class DistributedDomain:
         check(lib.hyb_owned_coords_kind(self._h, kind, level, int(global_order), _pd(xy), n))
         return xy
 
+    def overlap(self, enable: bool | None = None) -> int:
+        """Toggle communication/computation overlap (default on); returns the
+        number of split (interior / boundary) launches so far."""
+        n = C.c_int64()
+        check(lib.hyb_domain_overlap(self._h, -1 if enable is None else int(enable), C.byref(n)))
+        return n.value
+
     def synchronize(self) -> None:
         check(lib.hyb_domain_synchronize(self._h))
 
