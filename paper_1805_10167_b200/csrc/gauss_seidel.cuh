@@ -509,6 +509,78 @@ __global__ void __launch_bounds__(128) k_gs_ev(LevelTables t, FlagTables fl, con
 }
 
 // ---------------------------------------------------------------------------
+// Coloured face sweep with the whole face in shared memory (faces with
+// n <= 128: at most 69 KB per face, three CTAs per SM at n = 128). One lane
+// streams the face's x block (rows 0..n-1, padding included) into shared
+// memory with bulk copies on one mbarrier and prefetches the face's b rows
+// into L2; the three colours are then swept in order with one barrier between
+// them (a colour class is an independent set of the 7-point stencil, so each
+// colour is one parallel step; b is read from L2, each value once), and rows
+// 1..n-2 go back with bulk stores. Same operands and term order as the
+// in-place sweep: bitwise og_cgs.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_cgs_smem(LevelTables t, const double* __restrict__ b, double* x) {
+    extern __shared__ __align__(128) double cs_face[];
+    __shared__ int64_t ro[130];
+    __shared__ __align__(8) uint64_t bar;
+    const int n = t.n;
+    const int64_t base = int64_t(blockIdx.x) * t.face_stride;
+    constexpr uint32_t CHUNK = 32768;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        const uint32_t bytes = uint32_t(face_rowoff(t.W, n)) * 8u; // rows 0..n-1
+        mbar_arrive_expect_tx(&bar, bytes);
+        for (uint32_t o = 0; o < bytes; o += CHUNK)
+            bulk_g2s(reinterpret_cast<char*>(cs_face) + o, reinterpret_cast<const char*>(x + base) + o,
+                     min(CHUNK, bytes - o), &bar);
+        const uint32_t bb = uint32_t(face_rowoff(t.W, n - 1) - face_rowoff(t.W, 1)) * 8u; // b rows 1..n-2
+        for (uint32_t o = 0; o < bb; o += CHUNK)
+            prefetch_l2(reinterpret_cast<const char*>(b + base + face_rowoff(t.W, 1)) + o, min(CHUNK, bb - o));
+    }
+    for (int r = threadIdx.x; r <= n; r += NT) ro[r] = t.rowoff[r];
+    double co[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) co[i] = __ldg(t.face_coef + size_t(blockIdx.x) * 8 + i);
+    const double rd = 1.0 / co[7];
+    const double* __restrict__ bf = b + base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NW = NT / 32;
+    __syncthreads(); // ro[] and the barrier's initialisation
+    mbar_wait(&bar, 0);
+#pragma unroll 1
+    for (int colour = 0; colour < 3; ++colour) {
+#pragma unroll 1
+        for (int r = 1 + warp; r <= n - 2; r += NW) {
+            const double* rm = cs_face + ro[r - 1];
+            double* r0 = cs_face + ro[r];
+            const double* rp = cs_face + ro[r + 1];
+            const double* br = bf + ro[r];
+            int cs = ((colour - 2 * r) % 3 + 3) % 3; // first column of this colour
+            if (cs == 0) cs = 3;                      // c = 0 is the border
+            const int cmax = n - 1 - r;
+            for (int c = cs + 3 * lane; c <= cmax; c += 96) {
+                double v[8];
+                v[0] = r0[c - 1], v[1] = rp[c - 1], v[2] = rm[c], v[3] = r0[c];
+                v[4] = rp[c], v[5] = rm[c + 1], v[6] = r0[c + 1], v[7] = br[c];
+                r0[c] = cgs_point_update(v, co, rd);
+            }
+        }
+        __syncthreads();
+    }
+    fence_proxy_async_smem(); // each thread's generic-proxy writes, visible to the bulk stores
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t lo = uint32_t(ro[1]) * 8u, hi = uint32_t(ro[n - 1]) * 8u; // rows 1..n-2
+        for (uint32_t o = lo; o < hi; o += CHUNK)
+            bulk_s2g(reinterpret_cast<char*>(x + base) + o, reinterpret_cast<const char*>(cs_face) + o,
+                     min(CHUNK, hi - o));
+        bulk_commit();
+        bulk_wait_all(); // shared memory must outlive the reads of the stores
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Coloured face sweep in column blocks (faces of every size). One CTA per
 // (face, block of CB columns) runs the k_cgs_tma step schedule (C0 on rows
 // [j, j+K), C1 on [j-S, j-S+K), C2 on [j-2S, j-2S+K), S = K+1, one consumer

@@ -757,6 +757,14 @@ bool launch_cgs_cols(const LevelTables& t, const double* b, double* x, double* y
     return nb > 1;
 }
 
+template <int NT>
+void launch_cgs_smem(const LevelTables& t, const double* b, double* x, size_t smem, cudaStream_t st) {
+    static const bool attr =
+        cudaFuncSetAttribute(k_cgs_smem<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024) == cudaSuccess;
+    if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
+    k_cgs_smem<NT><<<unsigned(t.nfaces), NT, smem, st>>>(t, b, x);
+}
+
 // tuning knob for measurements (HYB_CGS_CFG); the default is the measured best
 static int cgs_cfg() {
     static const int v = [] {
@@ -782,10 +790,17 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
         oop = launch_cgs_cols<2, 2, 256, 4, 1>(t, b, x, y, st);
     } else if (v == 8 && n <= 128) {
         oop = launch_cgs_cols<2, 3, 128, 4, 1>(t, b, x, y, st);
-    } else if (n <= 128) {
+    } else if (n <= 128 && v == 12) {
         // small faces: two warps per face, 8-row blocks through L1/L2 (config 3, 8192 faces: L7
         // 0.67 ms, L6 0.29, L5 0.15; the ring kernel: L7 0.80)
         k_cgs_faces<8, 2><<<unsigned(t.nfaces), 64, 0, st>>>(t, b, x);
+    } else if (n <= 128) {
+        // small faces: the whole face in shared memory (k_cgs_smem). Config 3 (8192 faces), face
+        // kernel per sweep against the row-block kernel: L7 0.429 vs 0.555 ms, L6 0.183 vs 0.243,
+        // L5 0.099 vs 0.119; V(3,3) cycle 76.7 -> 75.9 ms
+        const size_t smem = size_t(face_rowoff(t.W, t.n)) * 8; // rows 0..n-1
+        if (n == 128) launch_cgs_smem<512>(t, b, x, smem, st);
+        else launch_cgs_smem<256>(t, b, x, smem, st);
     } else if (n == 256) {
         // config 3 L8: 4 CTAs per SM (64 registers) 1.705 ms per sweep; 3 CTAs 1.828, D = 2 1.884,
         // 128-column blocks out of place 2.42-2.44

@@ -40,7 +40,7 @@ def cfg3_mesh(segments=128, layers=32):
 @pytest.mark.parametrize("ranks", [1, 3])
 def test_colored_gs_bitwise_vs_restatement(mesh_name, ranks):
     mesh = cfg3_mesh(16, 4) if mesh_name == "annulus" else FIXTURES[mesh_name]()
-    for level in (1, 2, 4, 6):
+    for level in (1, 2, 3, 4, 5, 6):  # n <= 64: the whole-face shared-memory sweep (k_cgs_smem)
         dom = H.DistributedDomain(mesh, ranks)
         ctl = H.Controller(dom)
         A = H.StencilOperator(dom, H.LAPLACE, level, level)
@@ -59,10 +59,10 @@ def test_colored_gs_bitwise_vs_restatement(mesh_name, ranks):
 @pytest.mark.parametrize("mesh_name", ["square", "annulus"])
 @pytest.mark.parametrize("ranks", [1, 3])
 def test_colored_gs_bitwise_large_faces(mesh_name, ranks):
-    """Faces of n = 128, 256, 512 (the shared-memory ring kernels of the coloured sweep, see
-    launch_cgs_faces) against the restatement, bitwise, three sweeps each."""
+    """Faces of n = 128 (whole face in shared memory), 256, 512 (the shared-memory ring kernels)
+    and 1024 (column blocks, out of place) against the restatement, bitwise, three sweeps each."""
     mesh = cfg3_mesh(4, 2) if mesh_name == "annulus" else FIXTURES[mesh_name]()
-    for level in (7, 8, 9):
+    for level in (7, 8, 9, 10):
         dom = H.DistributedDomain(mesh, ranks)
         ctl = H.Controller(dom)
         A = H.StencilOperator(dom, H.LAPLACE, level, level)
