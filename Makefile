@@ -16,7 +16,7 @@ CXXFLAGS := -O2 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -I$(CUDA)/inclu
 LDFLAGS  := -shared -Wl,--no-undefined -static-libstdc++ -static-libgcc -Wl,--exclude-libs,ALL -L$(CUDA)/lib64 -lcudart_static -ldl -lpthread -lrt
 
 HDRS := $(wildcard $(CSRC)/*.hpp) $(wildcard $(CSRC)/*.cuh) include/hyteg_b200.h
-OBJS := $(BUILD)/kernels.o $(BUILD)/setup.o $(BUILD)/domain.o $(BUILD)/exchange.o $(BUILD)/plan.o $(BUILD)/coarse.o $(BUILD)/ops.o $(BUILD)/serialize.o $(BUILD)/stokes.o $(BUILD)/p2.o $(BUILD)/capi.o
+OBJS := $(BUILD)/kernels.o $(BUILD)/setup.o $(BUILD)/domain.o $(BUILD)/exchange.o $(BUILD)/plan.o $(BUILD)/coarse.o $(BUILD)/ops.o $(BUILD)/serialize.o $(BUILD)/stokes.o $(BUILD)/p2.o $(BUILD)/controller.o $(BUILD)/capi.o
 
 .PHONY: all lib oracle clean
 all: lib oracle

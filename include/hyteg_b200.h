@@ -229,6 +229,23 @@ int hyb_sync(hyb_function* f, int level);
  * (src/communication.cpp:272-403). Other values: HYB_INVALID_ARGUMENT. */
 enum hyb_direction { HYB_V2E = 0, HYB_E2F = 1, HYB_F2E = 2, HYB_E2V = 3 };
 int hyb_sync_directions(hyb_function* f, int level, const int* dirs, int n);
+/* The PackInfo extension point (communication.hpp:24-34) and Controller::sync
+ * (communication.hpp:40-56, src/communication.cpp:126-173) for data the caller
+ * keeps on the host, of any kind: pack writes the sender primitive's message
+ * for `receiver` in direction `dir` (out == NULL: size query into *len);
+ * unpack scatters a message into the receiver's ghosts and reports the bytes
+ * it consumed (fewer than len is the reference's logic_error, HYB_LOGIC_ERROR);
+ * a non-zero callback return is HYB_RUNTIME_ERROR. hyb_controller_sync runs the
+ * listed directions with the reference's schedule: remote packs of the local
+ * senders (ID order), then receiver-driven unpacks (rank order, then ID order;
+ * sources in the reference's order), same-rank pairs as local_copy = pack +
+ * unpack. Other processes' messages travel over the domain's NCCL communicator. */
+typedef int (*hyb_pack_fn)(void* user, uint64_t sender, uint64_t receiver, int dir, int level, uint8_t* out,
+                           int64_t cap, int64_t* len);
+typedef int (*hyb_unpack_fn)(void* user, uint64_t receiver, uint64_t sender, int dir, int level, const uint8_t* in,
+                             int64_t len, int64_t* used);
+int hyb_register_pack_info(hyb_domain* d, uint32_t channel, hyb_pack_fn pack, hyb_unpack_fn unpack, void* user);
+int hyb_controller_sync(hyb_domain* d, uint32_t channel, int level, const int* dirs, int n);
 /* values(id, level) (function.hpp:37-39): the primitive's slots in the
  * reference's layout (face closed triangle row-major; edge line (n+1), then
  * per face halo rows 0 (n+1) and 1 (n); vertex own + one ghost per edge) as

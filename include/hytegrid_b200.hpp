@@ -27,6 +27,8 @@
 #include <cstdint>
 #include <functional>
 #include <map>
+#include <memory>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -131,13 +133,64 @@ class DistributedDomain {
 
 class ScalarFunction;
 
+enum class Direction : int { VERTEX_TO_EDGE = HYB_V2E, EDGE_TO_FACE = HYB_E2F, FACE_TO_EDGE = HYB_F2E,
+                             EDGE_TO_VERTEX = HYB_E2V };
+
+/// The reference's extension point (communication.hpp:24-34) for data the
+/// caller keeps on the host: primitives are named by ID (the device owns the
+/// field storage, so no Primitive object is handed out); unpack returns the
+/// bytes it consumed (fewer than the message is the reference's logic_error).
+class PackInfo {
+  public:
+    virtual ~PackInfo() = default;
+    virtual void pack(std::uint64_t sender, std::uint64_t receiver, Direction dir, int level,
+                      std::vector<std::uint8_t>& out) const = 0;
+    virtual std::size_t unpack(std::uint64_t receiver, std::uint64_t sender, Direction dir, int level,
+                               const std::uint8_t* in, std::size_t len) const = 0;
+};
+
 class Controller {
   public:
     explicit Controller(DistributedDomain& d) : domain_(&d) {}
     DistributedDomain& domain() { return *domain_; }
+    /// Controller::register_pack_info / sync (communication.hpp:44-49)
+    void register_pack_info(std::uint32_t channel, std::shared_ptr<const PackInfo> info) {
+        if (!info) throw std::invalid_argument("register_pack_info: null PackInfo");
+        check(hyb_register_pack_info(domain_->handle(), channel, &pack_cb, &unpack_cb,
+                                     const_cast<PackInfo*>(info.get())));
+        infos_[channel] = std::move(info);
+    }
+    void sync(std::uint32_t channel, int level, const std::vector<Direction>& dirs) {
+        std::vector<int> d;
+        for (Direction x : dirs) d.push_back(int(x));
+        check(hyb_controller_sync(domain_->handle(), channel, level, d.data(), int(d.size())));
+    }
 
   private:
+    static int pack_cb(void* user, std::uint64_t s, std::uint64_t r, int dir, int level, std::uint8_t* out,
+                       std::int64_t cap, std::int64_t* len) {
+        try {
+            std::vector<std::uint8_t> buf;
+            static_cast<const PackInfo*>(user)->pack(s, r, Direction(dir), level, buf);
+            *len = std::int64_t(buf.size());
+            if (out && cap >= *len && !buf.empty()) std::memcpy(out, buf.data(), buf.size());
+            return 0;
+        } catch (...) {
+            return 1;
+        }
+    }
+    static int unpack_cb(void* user, std::uint64_t r, std::uint64_t s, int dir, int level, const std::uint8_t* in,
+                         std::int64_t len, std::int64_t* used) {
+        try {
+            *used = std::int64_t(static_cast<const PackInfo*>(user)->unpack(r, s, Direction(dir), level, in,
+                                                                            std::size_t(len)));
+            return 0;
+        } catch (...) {
+            return 1;
+        }
+    }
     DistributedDomain* domain_;
+    std::map<std::uint32_t, std::shared_ptr<const PackInfo>> infos_;
 };
 
 namespace detail {
@@ -246,8 +299,6 @@ inline void interpolate(ScalarFunction& f, const Expr& e, int level, std::uint8_
 }
 inline void sync_all(Controller&, const ScalarFunction& f, int level) { check(hyb_sync(f.handle(), level)); }
 /// the reference's Direction (transport.hpp:19-26)
-enum class Direction : int { VERTEX_TO_EDGE = HYB_V2E, EDGE_TO_FACE = HYB_E2F, FACE_TO_EDGE = HYB_F2E,
-                             EDGE_TO_VERTEX = HYB_E2V };
 /// sync(c, f, level, span<Direction>) (function.hpp:79-80): the directions in order
 inline void sync(Controller&, const ScalarFunction& f, int level, const std::vector<Direction>& dirs) {
     std::vector<int> d;

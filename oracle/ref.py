@@ -69,6 +69,8 @@ def lib():
             "ref_stokes_create": (i, [C.c_char_p, i, i, i, i, i, C.POINTER(C.c_int), C.POINTER(C.c_uint8), i,
                                       C.POINTER(C.c_int), C.POINTER(C.c_uint8), i, i, d, C.POINTER(p)]),
             "ref_stokes_destroy": (None, [p]),
+            "ref_controller_trace": (i, [C.c_char_p, i, i, i, i, C.POINTER(C.c_int), i, C.POINTER(i64), i64,
+                                         C.POINTER(i64)]),
             "ref_stokes_set": (i, [p, i, i, i, pd]),
             "ref_stokes_get": (i, [p, i, i, i, pd]),
             "ref_stokes_uzawa": (i, [p, i, d]),
@@ -342,3 +344,15 @@ class RefStokes:
                                     c.ctypes.data_as(C.POINTER(C.c_int64)), v.ctypes.data_as(C.POINTER(C.c_double)),
                                     n.value, C.byref(n)))
         return r, c, v
+
+
+def controller_trace(mesh: str, ranks: int, level: int, dirs, partitioner: int = 0) -> np.ndarray:
+    """The reference Controller's unpack sequence for a tracing PackInfo: rows
+    (receiver, sender, direction, level, message sender, receiver, direction, level)."""
+    d = (C.c_int * max(len(dirs), 1))(*dirs)
+    n = C.c_int64()
+    _ck(lib().ref_controller_trace(mesh.encode(), ranks, partitioner, 1, level, d, len(dirs), None, 0, C.byref(n)))
+    out = np.zeros(n.value, dtype=np.int64)
+    _ck(lib().ref_controller_trace(mesh.encode(), ranks, partitioner, 1, level, d, len(dirs),
+                                   out.ctypes.data_as(C.POINTER(C.c_int64)), n.value, C.byref(n)))
+    return out.reshape(-1, 8)

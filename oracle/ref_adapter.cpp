@@ -656,3 +656,46 @@ int ref_stokes_matrix(void* sp, int level, int64_t* rows, int64_t* cols, double*
     });
 }
 } // extern "C"
+
+// ---- Controller::sync with a tracing PackInfo (src/communication.cpp:126-173) ----
+// Every message is (sender, receiver, direction, level) as four u64; every
+// unpack is logged as (receiver, sender, direction, level) + the message.
+namespace {
+struct TracePack : PackInfo {
+    std::vector<int64_t>* log = nullptr;
+    void pack(const Primitive& sender, PrimitiveID receiver, Direction dir, int level,
+              MessageBuffer& out) const override {
+        out.put_u64(sender.id.value);
+        out.put_u64(receiver.value);
+        out.put_u64(uint64_t(dir));
+        out.put_u64(uint64_t(level));
+    }
+    void unpack(Primitive& receiver, PrimitiveID sender, Direction dir, int level, MessageBuffer& in) const override {
+        const int64_t a = int64_t(in.get_u64()), b = int64_t(in.get_u64()), c = int64_t(in.get_u64()),
+                      d = int64_t(in.get_u64());
+        log->insert(log->end(), {int64_t(receiver.id.value), int64_t(sender.value), int64_t(dir), int64_t(level), a,
+                                 b, c, d});
+    }
+};
+} // namespace
+extern "C" int ref_controller_trace(const char* mesh, int ranks, int partitioner, int weight_level, int level,
+                                    const int* dirs, int n, int64_t* out, int64_t cap, int64_t* len) {
+    return guard([&] {
+        const SetupGraph setup = build_setup_graph(parse_mesh_string(mesh));
+        const Assignment a = partitioner == 1
+                                 ? partition_greedy_edgecut(setup, weighted_graph(setup, FunctionKind::P1, weight_level),
+                                                            ranks)
+                                 : partition_round_robin(setup, ranks);
+        DistributedDomain dom(setup, a, ranks);
+        Controller ctl(dom);
+        std::vector<int64_t> log;
+        auto info = std::make_shared<TracePack>();
+        info->log = &log;
+        ctl.register_pack_info(7, info);
+        std::vector<Direction> d;
+        for (int i = 0; i < n; ++i) d.push_back(Direction(dirs[i]));
+        ctl.sync(7, level, std::span<const Direction>(d));
+        *len = int64_t(log.size());
+        for (int64_t i = 0; i < *len && i < cap; ++i) out[i] = log[size_t(i)];
+    });
+}

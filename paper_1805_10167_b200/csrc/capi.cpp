@@ -8,6 +8,7 @@
 #include "coarse.hpp"
 #include "domain.hpp"
 #include "stokes.hpp"
+#include "controller.hpp"
 
 // Objects built on a domain share ownership of it: destroying the domain
 // handle first (any order is legal, e.g. a garbage collector finalising a
@@ -15,6 +16,7 @@
 // `keep` is declared first so it is destroyed after the object using it.
 struct hyb_domain {
     std::shared_ptr<hyb::Domain> d;
+    std::unique_ptr<hyb::HostController> ctl; // PackInfo plugins, created on first registration
 };
 struct hyb_function {
     std::shared_ptr<hyb::Domain> keep;
@@ -1047,4 +1049,26 @@ int hyb_stokes_matrix_host(const char* mesh_text, int level, const int32_t* bcu_
 }
 double hyb_coarse_hypot(double x, double y) { return hyb::glibc_hypot_host(x, y); }
 
+} // extern "C"
+
+// ---- PackInfo extension point (include/hytegrid/communication.hpp:24-56) ----
+extern "C" {
+int hyb_register_pack_info(hyb_domain* d, uint32_t channel, hyb_pack_fn pack, hyb_unpack_fn unpack, void* user) {
+    return guarded([&] {
+        need(d, "hyb_register_pack_info");
+        if (!d->ctl) d->ctl = std::make_unique<hyb::HostController>(*d->d);
+        hyb::PackCallbacks cb;
+        cb.pack = pack;
+        cb.unpack = unpack;
+        cb.user = user;
+        d->ctl->register_pack_info(channel, cb);
+    });
+}
+int hyb_controller_sync(hyb_domain* d, uint32_t channel, int level, const int* dirs, int n) {
+    return guarded([&] {
+        need(d, "hyb_controller_sync");
+        if (!d->ctl) throw hyb::InvalidArgument("sync: no PackInfo registered for channel " + std::to_string(channel));
+        d->ctl->sync(channel, level, dirs, n);
+    });
+}
 } // extern "C"

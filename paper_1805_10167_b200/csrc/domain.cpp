@@ -225,6 +225,47 @@ void Domain::connect_nccl(const char id[128], int rank) {
     nccl_comm_ = comm;
 }
 
+// byte messages between processes (the host Controller's remote pairs):
+// host buffers staged through device memory, one grouped send/recv round
+void Domain::nccl_bytes(const std::vector<std::pair<int, const std::vector<uint8_t>*>>& sends,
+                        const std::vector<std::pair<int, std::vector<uint8_t>*>>& recvs) {
+    if (sends.empty() && recvs.empty()) return;
+    if (!nccl_comm_) throw LogicError("sync: remote ranks present but NCCL is not connected");
+    size_t sb = 0, rb = 0;
+    for (const auto& s_ : sends) sb += s_.second->size();
+    for (const auto& r_ : recvs) rb += r_.second->size();
+    DevMem ds(std::max<size_t>(sb, 1)), dr(std::max<size_t>(rb, 1));
+    size_t o = 0;
+    for (const auto& s_ : sends) {
+        if (!s_.second->empty())
+            HYB_CUDA(cudaMemcpyAsync(ds.as<char>() + o, s_.second->data(), s_.second->size(), cudaMemcpyHostToDevice,
+                                     stream_));
+        o += s_.second->size();
+    }
+    auto& api = nccl();
+    auto comm = static_cast<ncclComm_t>(nccl_comm_);
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    o = 0;
+    for (const auto& s_ : sends) {
+        nccl_check(api.Send(ds.as<char>() + o, s_.second->size(), ncclUint8, s_.first, comm, stream_), "ncclSend");
+        o += s_.second->size();
+    }
+    o = 0;
+    for (const auto& r_ : recvs) {
+        nccl_check(api.Recv(dr.as<char>() + o, r_.second->size(), ncclUint8, r_.first, comm, stream_), "ncclRecv");
+        o += r_.second->size();
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    o = 0;
+    for (const auto& r_ : recvs) {
+        if (!r_.second->empty())
+            HYB_CUDA(cudaMemcpyAsync(r_.second->data(), dr.as<char>() + o, r_.second->size(), cudaMemcpyDeviceToHost,
+                                     stream_));
+        o += r_.second->size();
+    }
+    HYB_CUDA(cudaStreamSynchronize(stream_));
+}
+
 void Domain::allreduce_sum(double* dev, int64_t n) {
     if (!nccl_comm_) return;
     nccl_check(nccl().AllReduce(dev, dev, size_t(n), ncclFloat64, ncclSum, static_cast<ncclComm_t>(nccl_comm_),

@@ -233,6 +233,9 @@ class Domain {
 
     // in-process all-reduce of a per-primitive vector (sum) across processes
     void allreduce_sum(double* dev, int64_t n);
+    /// host byte messages to / from other processes over NCCL (receive buffers pre-sized)
+    void nccl_bytes(const std::vector<std::pair<int, const std::vector<uint8_t>*>>& sends,
+                    const std::vector<std::pair<int, std::vector<uint8_t>*>>& recvs);
 
     // profiling of named kernels (CUDA events on the domain stream)
     bool profiling = false;

@@ -140,7 +140,9 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     __shared__ __align__(128) unsigned char fs_static[MODE == ST_JACOBI_PROLONG ? 16 : sizeof(FaceSmem<MODE>)];
     FaceSmem<MODE>& sm = *reinterpret_cast<FaceSmem<MODE>*>(MODE == ST_JACOBI_PROLONG ? fs_dyn : fs_static);
     const int n = t.n, W = t.W;
-    const int face = t.face_list ? t.face_list[blockIdx.z] : int(blockIdx.z);
+    // subset launches (communication/computation overlap) exist for apply, residual and Jacobi only
+    constexpr bool LISTED = MODE == ST_APPLY || MODE == ST_RESIDUAL || MODE == ST_JACOBI;
+    const int face = (LISTED && t.face_list) ? t.face_list[blockIdx.z] : int(blockIdx.z);
     const int c0 = blockIdx.x * (RR ? FS_COLS_RR : FS_COLS);
     const int rb = fs_band(t.n);
     int r_lo, r_hi;

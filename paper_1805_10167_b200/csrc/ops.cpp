@@ -112,16 +112,22 @@ namespace {
 // after the receive half of the refresh (the paper's Algorithm 3; the
 // reference itself syncs first, src/operators.cpp:390). Every row is
 // computed from the same values either way: bitwise the unsplit launch.
-template <class Launch> void synced_launch(Domain& d, Function& x, int level, const LevelTables& t, Launch launch) {
+// `timer` brackets the stencil launch(es) only, not the refresh (as before the split)
+template <class Launch>
+void synced_launch(Domain& d, Function& x, int level, const LevelTables& t, const char* timer, Launch launch) {
     if (!d.overlap_active(x, level)) {
         d.sync(x, level);
+        d.timer_begin(timer);
         launch(t);
+        d.timer_end();
         return;
     }
     d.sync_begin(x, level);
+    d.timer_begin(timer);
     launch(d.overlap_tables(t, x, level, 0));
     d.sync_end(x, level);
     launch(d.overlap_tables(t, x, level, 1));
+    d.timer_end();
 }
 } // namespace
 
@@ -137,12 +143,11 @@ void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t m
         return;
     }
     const LevelTables t = A.tables(level);
-    d.timer_begin("apply"); // face interiors, then edge/vertex rows as the same launch's trailing CTAs
-    synced_launch(d, src, level, t, [&](const LevelTables& tt) {
+    // face interiors, then edge/vertex rows as the same launch's trailing CTAs
+    synced_launch(d, src, level, t, "apply", [&](const LevelTables& tt) {
         launch_stencil(ST_APPLY, tt, dst.flags(), src.data(level), src.data(level), dst.data(level), 0.0, mask,
                        d.stream(), 3);
     });
-    d.timer_end();
 }
 
 void residual(const Operator& A, Function& rhs, Function& x, Function& r, int level) {
@@ -153,12 +158,10 @@ void residual(const Operator& A, Function& rhs, Function& x, Function& r, int le
     require_p1(x, "residual (fused)");
     Domain& d = A.domain();
     const LevelTables t = A.tables(level);
-    d.timer_begin("residual");
-    synced_launch(d, x, level, t, [&](const LevelTables& tt) {
+    synced_launch(d, x, level, t, "residual", [&](const LevelTables& tt) {
         launch_stencil(ST_RESIDUAL, tt, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
                        d.stream(), 3);
     });
-    d.timer_end();
 }
 
 void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level, double* dotp) {
@@ -182,12 +185,10 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
     // pending write-back of the reference (src/operators.cpp:435-468) is a
     // second buffer here: read x, write x', swap.
     const LevelTables t = A.tables(level);
-    d.timer_begin("jacobi");
-    synced_launch(d, x, level, t, [&](const LevelTables& tt) {
+    synced_launch(d, x, level, t, "jacobi", [&](const LevelTables& tt) {
         launch_stencil(ST_JACOBI, tt, x.flags(), x.data(level), rhs.data(level), next.as<double>(), omega, ALL_FLAGS,
                        d.stream(), 3, dotp);
     });
-    d.timer_end();
     x.arena(level).swap(next);
 }
 

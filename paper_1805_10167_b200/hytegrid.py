@@ -274,11 +274,59 @@ def kernel_launches() -> int:
     return n.value
 
 
+_PACK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint8),
+                       C.c_int64, C.POINTER(C.c_int64))
+_UNPACK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint8),
+                         C.c_int64, C.POINTER(C.c_int64))
+
+
+class PackInfo:
+    """The reference's extension point (communication.hpp:24-34) for data kept
+    on the host: pack(sender, receiver, direction, level) -> bytes and
+    unpack(receiver, sender, direction, level, data) -> bytes consumed."""
+
+    def pack(self, sender: int, receiver: int, direction: int, level: int) -> bytes:
+        raise NotImplementedError
+
+    def unpack(self, receiver: int, sender: int, direction: int, level: int, data: bytes) -> int:
+        raise NotImplementedError
+
+
 class Controller:
-    """Stateless stand-in for hytegrid::Controller (exchange plans live in the domain)."""
+    """hytegrid::Controller: the device fields' exchange plans live in the
+    domain; user PackInfo plugins are driven with the reference's schedule."""
 
     def __init__(self, domain: DistributedDomain):
         self.domain = domain
+        self._infos = {}  # channel -> (PackInfo, C callbacks kept alive)
+
+    def register_pack_info(self, channel: int, info: PackInfo) -> None:
+        def pack(_user, sender, receiver, direction, level, out, cap, length):
+            try:
+                data = info.pack(sender, receiver, direction, level)
+                length[0] = len(data)
+                if out and cap >= len(data):
+                    C.memmove(out, data, len(data))
+                return 0
+            except Exception:  # noqa: BLE001 - reported as the reference's runtime_error
+                return 1
+
+        def unpack(_user, receiver, sender, direction, level, data, length, used):
+            try:
+                used[0] = int(info.unpack(receiver, sender, direction, level, C.string_at(data, length)))
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        cbs = (_PACK_FN(pack), _UNPACK_FN(unpack))
+        check(lib.hyb_register_pack_info(self.domain._h, channel, C.cast(cbs[0], C.c_void_p),
+                                         C.cast(cbs[1], C.c_void_p), None))
+        self._infos[channel] = (info, cbs)
+
+    def sync(self, channel: int, level: int, directions) -> None:
+        """Controller::sync(channel, level, directions) (src/communication.cpp:126-173)."""
+        d = (C.c_int * max(len(directions), 1))(*[int(x) for x in directions])
+        check(lib.hyb_controller_sync(self.domain._h, channel, level, d, len(directions)))
 
 
 def register_function(ctl: Controller, f: "ScalarFunction") -> None:  # noqa: ARG001 - API parity

@@ -2,6 +2,9 @@
 // tests/test_operators.cpp, tests/test_solvers.cpp) against hytegrid_b200.hpp.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
 #include <stdexcept>
 
 #include "hytegrid_b200.hpp"
@@ -135,6 +138,30 @@ int main() {
         EXPECT(yv.size() == 81 && m <= 1e-12); // constants are in the kernel of the Laplacian
         smooth_gs(a2, pc, y2, one, 2);
         smooth_jacobi(a2, pc, y2, one, 0.8, 2);
+    }
+    // a user PackInfo plugin on the reference's Controller schedule: every face receives its three
+    // edges' messages (E->F), in slot order
+    {
+        struct Count : PackInfo {
+            mutable std::map<std::uint64_t, std::vector<std::uint64_t>> got;
+            void pack(std::uint64_t s, std::uint64_t, Direction, int, std::vector<std::uint8_t>& out) const override {
+                out.resize(8);
+                std::memcpy(out.data(), &s, 8);
+            }
+            std::size_t unpack(std::uint64_t r, std::uint64_t, Direction, int, const std::uint8_t* in,
+                               std::size_t len) const override {
+                std::uint64_t s = 0;
+                std::memcpy(&s, in, 8);
+                got[r].push_back(s);
+                return len;
+            }
+        };
+        DistributedDomain cd(meshgen::unit_square(), 2);
+        Controller cc(cd);
+        auto info = std::make_shared<Count>();
+        cc.register_pack_info(5, info);
+        cc.sync(5, 2, {Direction::EDGE_TO_FACE});
+        EXPECT(info->got.size() == 2 && info->got.begin()->second.size() == 3);
     }
     std::printf("cpp api ok: %d cycles, residual %.3e, error %.3e; fmg %d cycles, pcg %.1e\n", rep.iterations,
                 rep.residuals.back(), err, fr.iterations, pr.residuals.back() / pr.residuals.front());
