@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                                                                  const int64_t* __restrict__ cro, int64_t cstride,
                                                                  double* __restrict__ dotp,
                                                                  const double* __restrict__ xc, EvTail ev = EvTail{}) {
+    pdl_prologue();
     if constexpr (MODE == ST_APPLY || MODE == ST_RESIDUAL || MODE == ST_JACOBI || MODE == ST_JACOBI_PROLONG) {
         if (int(blockIdx.z) >= t.nfaces) { // CTA-uniform: before any barrier
             const int blk = (int(blockIdx.z - t.nfaces) * int(gridDim.y) + int(blockIdx.y)) * int(gridDim.x) +

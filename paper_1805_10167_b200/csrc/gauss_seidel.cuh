@@ -45,6 +45,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const double* __restrict__ b, double* x,
                                                             const int4* __restrict__ tiles, int ntiles, int ni,
                                                             int nj, int* flags, int* counter) {
+    pdl_prologue();
     // lane = row: padded row strides (16-byte aligned for cp.async) keep the
     // per-step column reads of 32 different rows at 2-way bank conflicts
     __shared__ __align__(16) double s_x[GS_WARPS][GS_R + 2][GS_XS];
@@ -258,6 +259,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 
 template <int CGS_K, int NW = CGS_WARPS>
 __global__ void __launch_bounds__(NW * 32) k_cgs_faces(LevelTables t, const double* __restrict__ b, double* x) {
+    pdl_prologue();
     const int n = t.n;
     const int last = n - 2; // interior rows 1..n-2
     const int64_t base = int64_t(blockIdx.x) * t.face_stride;
@@ -337,6 +339,7 @@ template <int NT> __device__ __forceinline__ void consumer_sync() { // named bar
 template <int K, int D, int MINB, int WPR>
 __global__ void __launch_bounds__(CgtCfg<K, D, WPR>::THREADS, MINB) k_cgs_tma(LevelTables t, const double* __restrict__ b,
                                                                          double* x) {
+    pdl_prologue();
     using C = CgtCfg<K, D, WPR>;
     extern __shared__ __align__(16) double cg_ring[];
     constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = K + 1;
@@ -449,6 +452,7 @@ __global__ void __launch_bounds__(CgtCfg<K, D, WPR>::THREADS, MINB) k_cgs_tma(Le
 // edges: colour 1 = odd k, colour 0 = even k, one thread per line DoF
 __global__ void __launch_bounds__(128) k_cgs_edges(LevelTables t, FlagTables fl, const double* __restrict__ b,
                                                    double* x, int parity, int kblocks) {
+    pdl_prologue();
     const int n = t.n;
     const int e = blockIdx.x / kblocks;
     const int k = 2 * ((blockIdx.x % kblocks) * blockDim.x + threadIdx.x) + parity;
@@ -473,6 +477,7 @@ __global__ void __launch_bounds__(128) k_cgs_edges(LevelTables t, FlagTables fl,
 // edges: one thread walks its line k = 1..n-1 in place; vertices: one thread
 __global__ void __launch_bounds__(128) k_gs_ev(LevelTables t, FlagTables fl, const double* __restrict__ b,
                                                double* x) {
+    pdl_prologue();
     const int n = t.n;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < t.nedges) {
@@ -520,6 +525,7 @@ __global__ void __launch_bounds__(128) k_gs_ev(LevelTables t, FlagTables fl, con
 // in-place sweep: bitwise og_cgs.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_cgs_smem(LevelTables t, const double* __restrict__ b, double* x) {
+    pdl_prologue();
     extern __shared__ __align__(128) double cs_face[];
     __shared__ int64_t ro[130];
     __shared__ __align__(8) uint64_t bar;
@@ -615,6 +621,7 @@ template <int K, int D, int CB, int WPR> struct CgcCfg {
 template <int K, int D, int CB, int MINB, int WPR>
 __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR>::THREADS, MINB)
     k_cgs_cols(LevelTables t, const double* __restrict__ b, const double* x, double* y) {
+    pdl_prologue();
     using C = CgcCfg<K, D, CB, WPR>;
     extern __shared__ __align__(16) double cc_ring[];
     constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = K + 1, RS = C::RS;
@@ -762,6 +769,7 @@ __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR>::THREADS, MINB)
 __global__ void __launch_bounds__(128) k_cgs_edges_oop(LevelTables t, FlagTables fl, const double* __restrict__ b,
                                                        const double* __restrict__ x, double* __restrict__ y,
                                                        int parity, int kblocks) {
+    pdl_prologue();
     const int n = t.n;
     const int e = blockIdx.x / kblocks;
     const int k = 2 * ((blockIdx.x % kblocks) * blockDim.x + threadIdx.x) + parity;
@@ -790,6 +798,7 @@ __global__ void __launch_bounds__(128) k_cgs_edges_oop(LevelTables t, FlagTables
 
 __global__ void __launch_bounds__(128) k_cgs_verts_oop(LevelTables t, FlagTables fl, const double* __restrict__ b,
                                                        const double* __restrict__ x, double* __restrict__ y) {
+    pdl_prologue();
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= t.nverts) return;
     const int64_t off = t.vtx_off[v];

@@ -31,6 +31,56 @@ inline void check_launch(const char* what) {
     if (e != cudaSuccess) throw CudaError(std::string("CUDA launch failed (") + what + "): " + cudaGetErrorString(e));
 }
 
+// Programmatic dependent launch: every kernel is launched with programmatic
+// stream serialisation and starts with pdl_prologue(), which lets the next
+// kernel in the stream be scheduled at once (griddepcontrol.launch_dependents)
+// and then waits until the previous kernel has completed and its writes are
+// visible (griddepcontrol.wait). Inputs are read only after the wait, so
+// results are unchanged; what moves is the launch latency of each kernel,
+// which now overlaps its predecessor's tail (the coarse levels of a V-cycle
+// are a chain of such small kernels). Only grids of at most pdl_max_ctas()
+// CTAs are launched this way: for the large HBM-bound grids the early-resident
+// waiting CTAs cost more than the hidden latency (measured: config-2 V-cycle
+// 8.94 -> 9.00 ms with every launch programmatic). HYB_PDL=0 turns it off,
+// HYB_PDL_MAX sets the grid-size limit.
+__device__ __forceinline__ void pdl_prologue() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+bool pdl_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("HYB_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+int64_t pdl_max_ctas() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("HYB_PDL_MAX");
+        return e ? int64_t(std::atoll(e)) : int64_t(148 * 8);
+    }();
+    return v;
+}
+
+template <typename... KArgs, typename... Args>
+void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    const int64_t ctas = int64_t(grid.x) * grid.y * grid.z;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() && ctas <= pdl_max_ctas() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+    if (e != cudaSuccess) throw CudaError(std::string("CUDA launch failed: ") + cudaGetErrorString(e));
+}
+
 
 // ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
@@ -111,6 +161,7 @@ template <int MODE>
 __global__ void __launch_bounds__(128) k_ev_stencil(LevelTables t, FlagTables fl, const double* __restrict__ x,
                                                     const double* __restrict__ b, double* __restrict__ y,
                                                     double omega, uint8_t mask, int kblocks) {
+    pdl_prologue();
     ev_stencil_block<MODE>(t, fl, x, b, y, omega, mask, kblocks, int(blockIdx.x));
 }
 
@@ -127,6 +178,7 @@ template <class I>
 __global__ void __launch_bounds__(256) k_ghost_gather(const I* __restrict__ dst, const I* __restrict__ src,
                                                       int64_t nlocal, int64_t ntotal, double* arena,
                                                       const double* __restrict__ recv) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < ntotal;
          i += int64_t(gridDim.x) * blockDim.x)
         arena[dst[i]] = i < nlocal ? arena[src[i]] : recv[i - nlocal];
@@ -138,6 +190,7 @@ __global__ void __launch_bounds__(256) k_ghost_gather(const I* __restrict__ dst,
 __global__ void __launch_bounds__(256) k_ghost_gather4(const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
                                                        int64_t nlocal, int64_t ntotal, double* arena,
                                                        const double* __restrict__ recv) {
+    pdl_prologue();
     const int64_t i0 = 4 * (blockIdx.x * int64_t(blockDim.x) + threadIdx.x);
     if (i0 >= ntotal) return;
     if (i0 + 4 <= nlocal) {
@@ -165,6 +218,7 @@ __global__ void __launch_bounds__(256) k_ghost_gather4(const int32_t* __restrict
 
 __global__ void __launch_bounds__(256) k_ghost_pack(const int64_t* __restrict__ src, int64_t n,
                                                     const double* __restrict__ arena, double* __restrict__ send) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         send[i] = arena[src[i]];
 }
@@ -193,6 +247,7 @@ inline dim3 face_row_grid(int n_cols, int n_rows, int nfaces) {
 __global__ void __launch_bounds__(128) k_prolongate_ev(LevelTables tc, LevelTables tf, FlagTables ff,
                                                        const double* __restrict__ xc, double* __restrict__ xf,
                                                        uint8_t mask, int add, int kblocks) {
+    pdl_prologue();
     const int nf = tf.n;
     const int eblocks = tf.nedges * kblocks;
     if (int(blockIdx.x) < eblocks) {
@@ -218,6 +273,7 @@ __global__ void __launch_bounds__(128) k_prolongate_ev(LevelTables tc, LevelTabl
 __global__ void __launch_bounds__(128) k_restrict_ev(LevelTables tc, LevelTables tf, FlagTables cf,
                                                      const double* __restrict__ xf, double* __restrict__ xc,
                                                      uint8_t mask, int kblocks) {
+    pdl_prologue();
     const int nc = tc.n, nfn = tf.n;
     const int eblocks = tc.nedges * kblocks;
     if (int(blockIdx.x) < eblocks) {
@@ -262,6 +318,7 @@ __device__ __forceinline__ double blas_op(int op, double alpha, double a, double
 __global__ void __launch_bounds__(256) k_blas1_faces(int op, int64_t n2, double alpha, const double2* __restrict__ x1,
                                                      double beta, const double2* __restrict__ x2, double2* dst,
                                                      DevScalars ds) {
+    pdl_prologue();
     if (ds.pa) alpha = ds.sa * *ds.pa;
     if (ds.pb) beta = *ds.pb;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
@@ -276,6 +333,7 @@ __global__ void __launch_bounds__(128) k_blas1_ev(int op, LevelTables t, FlagTab
                                                   const double* __restrict__ x1, double beta,
                                                   const double* __restrict__ x2, double* dst, uint8_t mask,
                                                   int kblocks, DevScalars ds = DevScalars{}) {
+    pdl_prologue();
     if (ds.pa) alpha = ds.sa * *ds.pa;
     if (ds.pb) beta = *ds.pb;
     const int n = t.n;
@@ -314,6 +372,7 @@ __device__ __forceinline__ double key_uniform(uint64_t sk, uint64_t id, uint64_t
 }
 
 __global__ void __launch_bounds__(128) k_random_faces(LevelTables t, uint64_t sk, double lo, double hi, double* dst) {
+    pdl_prologue();
     const int n = t.n;
     const int col = 1 + blockIdx.x * 128 + threadIdx.x;
     const uint64_t id = t.face_gid[blockIdx.z];
@@ -327,6 +386,7 @@ __global__ void __launch_bounds__(128) k_random_faces(LevelTables t, uint64_t sk
 
 __global__ void __launch_bounds__(128) k_random_ev(LevelTables t, FlagTables fl, uint64_t sk, double lo, double hi,
                                                    double* dst, uint8_t mask, int kblocks) {
+    pdl_prologue();
     const int n = t.n;
     const int eblocks = t.nedges * kblocks;
     if (int(blockIdx.x) < eblocks) {
@@ -352,6 +412,7 @@ __device__ __forceinline__ int64_t face_packed_row(int n, int r) {
 
 __global__ void __launch_bounds__(128) k_pack_faces(LevelTables t, const double* __restrict__ src,
                                                     double* __restrict__ dst, int to_arena, uint8_t mask) {
+    pdl_prologue();
     const int n = t.n;
     const int col = 1 + blockIdx.x * 128 + threadIdx.x;
     if (!(mask & F_INNER)) return;
@@ -370,6 +431,7 @@ __global__ void __launch_bounds__(128) k_pack_faces(LevelTables t, const double*
 
 __global__ void __launch_bounds__(128) k_pack_ev(LevelTables t, FlagTables fl, const double* __restrict__ src,
                                                  double* __restrict__ dst, int to_arena, uint8_t mask, int kblocks) {
+    pdl_prologue();
     const int n = t.n;
     const int eblocks = t.nedges * kblocks;
     int64_t pi, ai;
@@ -430,6 +492,7 @@ template <int OP> __device__ __forceinline__ double warp_fold(double v) {
 template <int OP>
 __global__ void __launch_bounds__(256) k_partials_faces(LevelTables t, const double* __restrict__ x1,
                                                         const double* __restrict__ x2, double* scratch, int bands) {
+    pdl_prologue();
     __shared__ double sh[256];
     const int n = t.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -458,6 +521,7 @@ __global__ void __launch_bounds__(256) k_pcg_update_faces(LevelTables t, double*
                                                           const double* __restrict__ p, double* __restrict__ r,
                                                           const double* __restrict__ ap, double alpha, double nalpha,
                                                           double* scratch, int bands, const double* alpha_p) {
+    pdl_prologue();
     if (alpha_p) {
         alpha = *alpha_p;
         nalpha = -alpha;
@@ -506,6 +570,7 @@ __global__ void __launch_bounds__(256) k_pcg_update_faces(LevelTables t, double*
 template <int OP>
 __global__ void k_partials_finish(LevelTables t, const double* __restrict__ x1, const double* __restrict__ x2,
                                   const double* scratch, int bands, double* part) {
+    pdl_prologue();
     const int n = t.n;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int nfw = (t.nfaces + 31) / 32; // warps spent on faces
@@ -537,6 +602,7 @@ __global__ void k_partials_finish(LevelTables t, const double* __restrict__ x1, 
 
 template <int OP>
 __global__ void __launch_bounds__(1024) k_combine_tree(double* v, int64_t len, double* out) {
+    pdl_prologue();
     // pairwise fold in list order, odd tail carried (reference
     // src/function.cpp:38-51); ping-pong between v[0..len) and v[len..2len)
     double* src = v;
@@ -572,6 +638,7 @@ int64_t kernel_launch_count() { return g_launches.load(); }
 // slots get values nobody reads before the next ghost refresh), double2-wide
 __global__ void __launch_bounds__(256) k_jacobi_zero_faces(LevelTables t, const double* __restrict__ b,
                                                            double* __restrict__ y, double omega) {
+    pdl_prologue();
     const int face = blockIdx.y;
     const double dg = t.face_coef[size_t(face) * 8 + 7];
     const double rdg = 1.0 / dg;
@@ -595,7 +662,7 @@ void launch_partials_finish(const LevelTables& t, const double* u, const double*
                             double* part, cudaStream_t st) {
     const int warps = (t.nfaces + 31) / 32 + t.nedges + (t.nverts + 31) / 32;
     if (warps > 0) {
-        k_partials_finish<0><<<(warps + 3) / 4, 128, 0, st>>>(t, u, v, scratch, bands, part);
+        pdl_launch(k_partials_finish<0>, (warps + 3) / 4, 128, 0, st, t, u, v, scratch, bands, part);
         check_launch("partials finish");
     }
 }
@@ -605,13 +672,13 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
     if (mode == ST_JACOBI_ZERO) {
         if ((parts & 1) && t.nfaces > 0 && t.n >= 3) {
             const int64_t per = (t.face_stride / 2 + 255) / 256;
-            k_jacobi_zero_faces<<<dim3(unsigned(per < 64 ? per : 64), unsigned(t.nfaces)), 256, 0, st>>>(t, b, y, omega);
+            pdl_launch(k_jacobi_zero_faces, dim3(unsigned(per < 64 ? per : 64), unsigned(t.nfaces)), 256, 0, st, t, b, y, omega);
             check_launch("jacobi zero-guess faces");
         }
         const int kb = kblocks_for(t.n);
         const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
         if ((parts & 2) && blocks > 0) {
-            k_ev_stencil<ST_JACOBI_ZERO><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb);
+            pdl_launch(k_ev_stencil<ST_JACOBI_ZERO>, blocks, 128, 0, st, t, fl, x, b, y, omega, mask, kb);
             check_launch("edge/vertex stencil");
         }
         return;
@@ -637,24 +704,24 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
         }
         switch (mode) {
         case ST_APPLY:
-            if (dotp) k_face_stencil<ST_APPLY, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp, nullptr, ev);
-            else k_face_stencil<ST_APPLY><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
+            if (dotp) pdl_launch(k_face_stencil<ST_APPLY, true>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, dotp, nullptr, ev);
+            else pdl_launch(k_face_stencil<ST_APPLY>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
             break;
         case ST_RESIDUAL:
-            k_face_stencil<ST_RESIDUAL><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
+            pdl_launch(k_face_stencil<ST_RESIDUAL>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
             break;
         default:
-            if (dotp) k_face_stencil<ST_JACOBI, true><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, dotp, nullptr, ev);
-            else k_face_stencil<ST_JACOBI><<<grid, FS_THREADS, 0, st>>>(t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
+            if (dotp) pdl_launch(k_face_stencil<ST_JACOBI, true>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, dotp, nullptr, ev);
+            else pdl_launch(k_face_stencil<ST_JACOBI>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
             break;
         }
         check_launch("face stencil");
     }
     if ((parts & 2) && blocks > 0 && !ev_done) {
         switch (mode) {
-        case ST_APPLY: k_ev_stencil<ST_APPLY><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb); break;
-        case ST_RESIDUAL: k_ev_stencil<ST_RESIDUAL><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb); break;
-        default: k_ev_stencil<ST_JACOBI><<<blocks, 128, 0, st>>>(t, fl, x, b, y, omega, mask, kb); break;
+        case ST_APPLY: pdl_launch(k_ev_stencil<ST_APPLY>, blocks, 128, 0, st, t, fl, x, b, y, omega, mask, kb); break;
+        case ST_RESIDUAL: pdl_launch(k_ev_stencil<ST_RESIDUAL>, blocks, 128, 0, st, t, fl, x, b, y, omega, mask, kb); break;
+        default: pdl_launch(k_ev_stencil<ST_JACOBI>, blocks, 128, 0, st, t, fl, x, b, y, omega, mask, kb); break;
         }
         check_launch("edge/vertex stencil");
     }
@@ -668,10 +735,10 @@ void launch_ghost_gather(const void* dst, const void* src, bool idx32, int64_t n
     // dependent round trips)
     const int blocks = grid_for(ntotal, 256, 1 << 30);
     if (idx32)
-        k_ghost_gather4<<<grid_for((ntotal + 3) / 4, 256, 1 << 30), 256, 0, st>>>(
+        pdl_launch(k_ghost_gather4, grid_for((ntotal + 3) / 4, 256, 1 << 30), 256, 0, st, 
             static_cast<const int32_t*>(dst), static_cast<const int32_t*>(src), nlocal, ntotal, arena, recv);
     else
-        k_ghost_gather<int64_t><<<blocks, 256, 0, st>>>(static_cast<const int64_t*>(dst),
+        pdl_launch(k_ghost_gather<int64_t>, blocks, 256, 0, st, static_cast<const int64_t*>(dst),
                                                                    static_cast<const int64_t*>(src), nlocal, ntotal,
                                                                    arena, recv);
     check_launch("ghost gather");
@@ -682,30 +749,30 @@ void launch_ghost_recv(const void* dst, bool idx32, int64_t begin, int64_t end, 
     if (end <= begin) return;
     const int blocks = grid_for(end - begin, 256, 1 << 30);
     if (idx32)
-        k_ghost_gather<int32_t><<<blocks, 256, 0, st>>>(static_cast<const int32_t*>(dst) + begin, nullptr, 0,
+        pdl_launch(k_ghost_gather<int32_t>, blocks, 256, 0, st, static_cast<const int32_t*>(dst) + begin, nullptr, 0,
                                                         end - begin, arena, recv);
     else
-        k_ghost_gather<int64_t><<<blocks, 256, 0, st>>>(static_cast<const int64_t*>(dst) + begin, nullptr, 0,
+        pdl_launch(k_ghost_gather<int64_t>, blocks, 256, 0, st, static_cast<const int64_t*>(dst) + begin, nullptr, 0,
                                                         end - begin, arena, recv);
     check_launch("ghost receive gather");
 }
 
 void launch_ghost_pack(const int64_t* src, int64_t n, const double* arena, double* send, cudaStream_t st) {
     if (n <= 0) return;
-    k_ghost_pack<<<grid_for(n), 256, 0, st>>>(src, n, arena, send);
+    pdl_launch(k_ghost_pack, grid_for(n), 256, 0, st, src, n, arena, send);
     check_launch("ghost pack");
 }
 
 void launch_prolongate(const LevelTables& tc, const LevelTables& tf, const FlagTables& ff, const double* xc,
                        double* xf, uint8_t mask, bool add, cudaStream_t st, bool faces) {
     if (faces && (mask & F_INNER) && tf.nfaces > 0 && tf.n >= 3) {
-        k_prolongate_faces<<<transfer_grid(tc.n, tf.nfaces), TR_WARPS * 32, 0, st>>>(tc, tf, xc, xf, add);
+        pdl_launch(k_prolongate_faces, transfer_grid(tc.n, tf.nfaces), TR_WARPS * 32, 0, st, tc, tf, xc, xf, add);
         check_launch("prolongate faces");
     }
     const int kb = kblocks_for(tf.n);
     const int blocks = tf.nedges * kb + (tf.nverts + 127) / 128;
     if (blocks > 0) {
-        k_prolongate_ev<<<blocks, 128, 0, st>>>(tc, tf, ff, xc, xf, mask, add ? 1 : 0, kb);
+        pdl_launch(k_prolongate_ev, blocks, 128, 0, st, tc, tf, ff, xc, xf, mask, add ? 1 : 0, kb);
         check_launch("prolongate edges/vertices");
     }
 }
@@ -715,7 +782,7 @@ void launch_gs_faces(const LevelTables& t, const double* b, double* x, const int
     if (ntiles <= 0) return;
     int blocks = (ntiles + GS_WARPS - 1) / GS_WARPS;
     if (blocks > 148 * 8) blocks = 148 * 8; // persistent warps pull tiles from the queue
-    k_gs_faces<<<blocks, GS_WARPS * 32, 0, st>>>(t, b, x, tiles, ntiles, ni, nj, flags, counter);
+    pdl_launch(k_gs_faces, blocks, GS_WARPS * 32, 0, st, t, b, x, tiles, ntiles, ni, nj, flags, counter);
     check_launch("gauss-seidel faces");
 }
 
@@ -725,7 +792,7 @@ void launch_cgs_tma(const LevelTables& t, const double* b, double* x, cudaStream
     static const bool attr = cudaFuncSetAttribute(k_cgs_tma<K, D, MINB, WPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(C::smem(513))) == cudaSuccess;
     if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
-    k_cgs_tma<K, D, MINB, WPR><<<unsigned(t.nfaces), C::THREADS, C::smem(t.W), st>>>(t, b, x);
+    pdl_launch(k_cgs_tma<K, D, MINB, WPR>, unsigned(t.nfaces), C::THREADS, C::smem(t.W), st, t, b, x);
 }
 
 void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
@@ -739,8 +806,8 @@ void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStre
     else if (t.n == 256) launch_cgs_tma<2, 3, 4, 1>(t, b, x, st);
     // small faces: two warps per face, 8-row blocks (config 3, 8192 faces: L7 0.88 -> 0.67 ms,
     // L6 0.42 -> 0.29, L5 0.22 -> 0.15 against 8 warps); faces above 512 keep 8 warps
-    else if (t.n <= 128) k_cgs_faces<8, 2><<<unsigned(t.nfaces), 64, 0, st>>>(t, b, x);
-    else k_cgs_faces<8><<<unsigned(t.nfaces), CGS_WARPS * 32, 0, st>>>(t, b, x);
+    else if (t.n <= 128) pdl_launch(k_cgs_faces<8, 2>, unsigned(t.nfaces), 64, 0, st, t, b, x);
+    else pdl_launch(k_cgs_faces<8>, unsigned(t.nfaces), CGS_WARPS * 32, 0, st, t, b, x);
     check_launch("coloured gauss-seidel faces");
 }
 
@@ -753,7 +820,7 @@ bool launch_cgs_cols(const LevelTables& t, const double* b, double* x, double* y
     if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
     const int nb = (t.n - 1 + CB - 1) / CB; // blocks over columns [0, n-1)
     double* out = nb == 1 ? x : y;          // one block per face: in place
-    k_cgs_cols<K, D, CB, MINB, WPR><<<dim3(unsigned(nb), unsigned(t.nfaces)), C::THREADS, C::SMEM, st>>>(t, b, x, out);
+    pdl_launch(k_cgs_cols<K, D, CB, MINB, WPR>, dim3(unsigned(nb), unsigned(t.nfaces)), C::THREADS, C::SMEM, st, t, b, x, out);
     return nb > 1;
 }
 
@@ -762,7 +829,7 @@ void launch_cgs_smem(const LevelTables& t, const double* b, double* x, size_t sm
     static const bool attr =
         cudaFuncSetAttribute(k_cgs_smem<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024) == cudaSuccess;
     if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
-    k_cgs_smem<NT><<<unsigned(t.nfaces), NT, smem, st>>>(t, b, x);
+    pdl_launch(k_cgs_smem<NT>, unsigned(t.nfaces), NT, smem, st, t, b, x);
 }
 
 // tuning knob for measurements (HYB_CGS_CFG); the default is the measured best
@@ -793,7 +860,7 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
     } else if (n <= 128 && v == 12) {
         // small faces: two warps per face, 8-row blocks through L1/L2 (config 3, 8192 faces: L7
         // 0.67 ms, L6 0.29, L5 0.15; the ring kernel: L7 0.80)
-        k_cgs_faces<8, 2><<<unsigned(t.nfaces), 64, 0, st>>>(t, b, x);
+        pdl_launch(k_cgs_faces<8, 2>, unsigned(t.nfaces), 64, 0, st, t, b, x);
     } else if (n <= 128) {
         // small faces: the whole face in shared memory (k_cgs_smem). Config 3 (8192 faces), face
         // kernel per sweep against the row-block kernel: L7 0.429 vs 0.555 ms, L6 0.183 vs 0.243,
@@ -820,13 +887,13 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
 void launch_cgs_ev_oop(const LevelTables& t, const FlagTables& fl, const double* b, const double* x, double* y,
                        cudaStream_t st) {
     if (t.nverts > 0) {
-        k_cgs_verts_oop<<<(t.nverts + 127) / 128, 128, 0, st>>>(t, fl, b, x, y);
+        pdl_launch(k_cgs_verts_oop, (t.nverts + 127) / 128, 128, 0, st, t, fl, b, x, y);
         check_launch("coloured gauss-seidel vertices");
     }
     const int kb = t.n - 1 > 0 ? (t.n / 2 + 127) / 128 : 0;
     if (t.nedges > 0 && kb > 0)
         for (int parity = 1; parity >= 0; --parity) { // odd k first, then even k
-            k_cgs_edges_oop<<<t.nedges * kb, 128, 0, st>>>(t, fl, b, x, y, parity, kb);
+            pdl_launch(k_cgs_edges_oop, t.nedges * kb, 128, 0, st, t, fl, b, x, y, parity, kb);
             check_launch("coloured gauss-seidel edges");
         }
 }
@@ -835,13 +902,13 @@ void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, 
     LevelTables tv = t; // vertices: the sequential GS kernel with no edges
     tv.nedges = 0;
     if (t.nverts > 0) {
-        k_gs_ev<<<(t.nverts + 127) / 128, 128, 0, st>>>(tv, fl, b, x);
+        pdl_launch(k_gs_ev, (t.nverts + 127) / 128, 128, 0, st, tv, fl, b, x);
         check_launch("coloured gauss-seidel vertices");
     }
     const int kb = t.n - 1 > 0 ? (t.n / 2 + 127) / 128 : 0;
     if (t.nedges > 0 && kb > 0)
         for (int parity = 1; parity >= 0; --parity) { // odd k first, then even k
-            k_cgs_edges<<<t.nedges * kb, 128, 0, st>>>(t, fl, b, x, parity, kb);
+            pdl_launch(k_cgs_edges, t.nedges * kb, 128, 0, st, t, fl, b, x, parity, kb);
             check_launch("coloured gauss-seidel edges");
         }
 }
@@ -849,14 +916,14 @@ void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, 
 void launch_gs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st) {
     const int total = t.nedges + t.nverts;
     if (total <= 0) return;
-    k_gs_ev<<<(total + 127) / 128, 128, 0, st>>>(t, fl, b, x);
+    pdl_launch(k_gs_ev, (total + 127) / 128, 128, 0, st, t, fl, b, x);
     check_launch("gauss-seidel edges/vertices");
 }
 
 void launch_restrict(const LevelTables& tc, const LevelTables& tf, const FlagTables& cf, const double* xf, double* xc,
                      uint8_t mask, cudaStream_t st) {
     if ((mask & F_INNER) && tc.nfaces > 0 && tc.n >= 3) {
-        k_restrict_faces<<<transfer_grid(tc.n, tc.nfaces), TR_WARPS * 32, 0, st>>>(tc, tf, xf, xc);
+        pdl_launch(k_restrict_faces, transfer_grid(tc.n, tc.nfaces), TR_WARPS * 32, 0, st, tc, tf, xf, xc);
         check_launch("restrict faces");
     }
     launch_restrict_ev(tc, tf, cf, xf, xc, mask, st);
@@ -866,6 +933,7 @@ void launch_restrict(const LevelTables& tc, const LevelTables& tf, const FlagTab
 // diagonal c + r = n-1), each once; k_prolongate_faces' formulas
 __global__ void __launch_bounds__(128) k_prolongate_layer(LevelTables tc, LevelTables tf, const double* __restrict__ xc,
                                                           double* xf) {
+    pdl_prologue();
     const int n = tf.n, nc = tc.n;
     const int k = 1 + blockIdx.x * blockDim.x + threadIdx.x;
     const int seg = blockIdx.y;
@@ -898,7 +966,7 @@ void launch_prolongate_layer(const LevelTables& tc, const LevelTables& tf, const
                              cudaStream_t st) {
     if (tf.nfaces <= 0 || tf.n < 3) return;
     const dim3 grid(unsigned((tf.n - 2 + 127) / 128), 3u, unsigned(tf.nfaces));
-    k_prolongate_layer<<<grid, 128, 0, st>>>(tc, tf, xc, xf);
+    pdl_launch(k_prolongate_layer, grid, 128, 0, st, tc, tf, xc, xf);
     check_launch("prolongate border layer");
 }
 
@@ -935,10 +1003,10 @@ void launch_jacobi_prolong_faces(const LevelTables& tc, const LevelTables& tf, c
                                  cudaSuccess;
     if (!attr) throw CudaError("jacobi after prolongation: cannot reserve shared memory");
     if (dotp)
-        k_face_stencil<ST_JACOBI_PROLONG, true><<<grid, FS_THREADS, smem, st>>>(tf, x, b, y, omega, tc.rowoff,
+        pdl_launch(k_face_stencil<ST_JACOBI_PROLONG, true>, grid, FS_THREADS, smem, st, tf, x, b, y, omega, tc.rowoff,
                                                                                 tc.face_stride, dotp, xc, ev);
     else
-        k_face_stencil<ST_JACOBI_PROLONG><<<grid, FS_THREADS, smem, st>>>(tf, x, b, y, omega, tc.rowoff,
+        pdl_launch(k_face_stencil<ST_JACOBI_PROLONG>, grid, FS_THREADS, smem, st, tf, x, b, y, omega, tc.rowoff,
                                                                           tc.face_stride, nullptr, xc, ev);
     check_launch("jacobi after prolongation faces");
     if (ev_separate) launch_stencil(ST_JACOBI, tf, *ev_flags, x, b, y, omega, F_ALL, st, 2);
@@ -948,12 +1016,12 @@ void launch_residual_restrict_faces(const LevelTables& tc, const LevelTables& tf
                                     double* r, double* xc, cudaStream_t st) {
     if (tf.nfaces <= 0 || tf.n < 3) return;
     if (tc.n >= 3) {
-        k_face_stencil<ST_RESTRICT_RESIDUAL><<<face_rr_grid(tf), FS_THREADS, 0, st>>>(tf, x, b, xc, 0.0, tc.rowoff,
-                                                                                      tc.face_stride, nullptr, nullptr);
+        pdl_launch(k_face_stencil<ST_RESTRICT_RESIDUAL>, face_rr_grid(tf), FS_THREADS, 0, st, tf, x, b, xc, 0.0, tc.rowoff,
+                                                                                      tc.face_stride, nullptr, nullptr, EvTail{});
         check_launch("residual+restrict faces");
     }
     const dim3 grid(unsigned((tf.n - 2 + 127) / 128), 3u, unsigned(tf.nfaces));
-    k_residual_layer<<<grid, 128, 0, st>>>(tf, x, b, r);
+    pdl_launch(k_residual_layer, grid, 128, 0, st, tf, x, b, r);
     check_launch("residual border layer");
 }
 
@@ -962,7 +1030,7 @@ void launch_restrict_ev(const LevelTables& tc, const LevelTables& tf, const Flag
     const int kb = kblocks_for(tc.n);
     const int blocks = tc.nedges * kb + (tc.nverts + 127) / 128;
     if (blocks > 0) {
-        k_restrict_ev<<<blocks, 128, 0, st>>>(tc, tf, cf, xf, xc, mask, kb);
+        pdl_launch(k_restrict_ev, blocks, 128, 0, st, tc, tf, cf, xf, xc, mask, kb);
         check_launch("restrict edges/vertices");
     }
 }
@@ -973,14 +1041,14 @@ void launch_blas1(int op, const LevelTables& t, const FlagTables& fl, double alp
         const int64_t n2 = t.faces_size / 2;
         const int64_t want = (n2 + 255) / 256;
         const int grid = int(want < 148 * 16 ? want : 148 * 16);
-        k_blas1_faces<<<grid, 256, 0, st>>>(op, n2, alpha, reinterpret_cast<const double2*>(x1), beta,
+        pdl_launch(k_blas1_faces, grid, 256, 0, st, op, n2, alpha, reinterpret_cast<const double2*>(x1), beta,
                                             reinterpret_cast<const double2*>(x2), reinterpret_cast<double2*>(dst), ds);
         check_launch("blas1 faces");
     }
     const int kb = kblocks_for(t.n);
     const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
     if (blocks > 0) {
-        k_blas1_ev<<<blocks, 128, 0, st>>>(op, t, fl, alpha, x1, beta, x2, dst, mask, kb, ds);
+        pdl_launch(k_blas1_ev, blocks, 128, 0, st, op, t, fl, alpha, x1, beta, x2, dst, mask, kb, ds);
         check_launch("blas1 edges/vertices");
     }
 }
@@ -989,13 +1057,13 @@ void launch_random(const LevelTables& t, const FlagTables& fl, uint64_t seed, ui
                    double* dst, uint8_t mask, cudaStream_t st) {
     const uint64_t sk = mix64(mix64(seed) ^ (stream * 0xD1B54A32D192ED03ull));
     if ((mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
-        k_random_faces<<<face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st>>>(t, sk, lo, hi, dst);
+        pdl_launch(k_random_faces, face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st, t, sk, lo, hi, dst);
         check_launch("random faces");
     }
     const int kb = kblocks_for(t.n);
     const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
     if (blocks > 0) {
-        k_random_ev<<<blocks, 128, 0, st>>>(t, fl, sk, lo, hi, dst, mask, kb);
+        pdl_launch(k_random_ev, blocks, 128, 0, st, t, fl, sk, lo, hi, dst, mask, kb);
         check_launch("random edges/vertices");
     }
 }
@@ -1014,6 +1082,7 @@ __device__ __forceinline__ double expr_eval(const Expr& e, double x, double y) {
 
 __global__ void __launch_bounds__(128) k_expr_faces(LevelTables t, const double* __restrict__ geo, Expr e,
                                                     double* dst) {
+    pdl_prologue();
     const int n = t.n;
     const int col = 1 + blockIdx.x * 128 + threadIdx.x;
     const double* g = geo + size_t(blockIdx.z) * 6;
@@ -1029,6 +1098,7 @@ __global__ void __launch_bounds__(128) k_expr_faces(LevelTables t, const double*
 
 __global__ void __launch_bounds__(128) k_expr_ev(LevelTables t, FlagTables fl, const double* __restrict__ geo, Expr e,
                                                  double* dst, uint8_t mask, int kblocks) {
+    pdl_prologue();
     const int n = t.n;
     const int eblocks = t.nedges * kblocks;
     const double* ge = geo + size_t(t.nfaces) * 6;
@@ -1050,13 +1120,13 @@ __global__ void __launch_bounds__(128) k_expr_ev(LevelTables t, FlagTables fl, c
 void launch_expr(const LevelTables& t, const FlagTables& fl, const double* geo, const Expr& e, double* dst,
                  uint8_t mask, cudaStream_t st) {
     if ((mask & F_INNER) && t.nfaces > 0 && t.n >= 3) {
-        k_expr_faces<<<face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st>>>(t, geo, e, dst);
+        pdl_launch(k_expr_faces, face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st, t, geo, e, dst);
         check_launch("expression faces");
     }
     const int kb = kblocks_for(t.n);
     const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
     if (blocks > 0) {
-        k_expr_ev<<<blocks, 128, 0, st>>>(t, fl, geo, e, dst, mask, kb);
+        pdl_launch(k_expr_ev, blocks, 128, 0, st, t, fl, geo, e, dst, mask, kb);
         check_launch("expression edges/vertices");
     }
 }
@@ -1064,26 +1134,26 @@ void launch_expr(const LevelTables& t, const FlagTables& fl, const double* geo, 
 void launch_scatter_owned(const LevelTables& t, const FlagTables& fl, const double* packed, double* arena,
                           uint8_t mask, cudaStream_t st) {
     if (t.nfaces > 0 && t.n >= 3) {
-        k_pack_faces<<<face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st>>>(t, packed, arena, 1, mask);
+        pdl_launch(k_pack_faces, face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st, t, packed, arena, 1, mask);
         check_launch("scatter faces");
     }
     const int kb = kblocks_for(t.n);
     const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
     if (blocks > 0) {
-        k_pack_ev<<<blocks, 128, 0, st>>>(t, fl, packed, arena, 1, mask, kb);
+        pdl_launch(k_pack_ev, blocks, 128, 0, st, t, fl, packed, arena, 1, mask, kb);
         check_launch("scatter edges/vertices");
     }
 }
 
 void launch_gather_owned(const LevelTables& t, const double* arena, double* packed, cudaStream_t st) {
     if (t.nfaces > 0 && t.n >= 3) {
-        k_pack_faces<<<face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st>>>(t, arena, packed, 0, 0xff);
+        pdl_launch(k_pack_faces, face_row_grid(t.n - 2, t.n - 2, t.nfaces), 128, 0, st, t, arena, packed, 0, 0xff);
         check_launch("gather faces");
     }
     const int kb = kblocks_for(t.n);
     const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
     if (blocks > 0) {
-        k_pack_ev<<<blocks, 128, 0, st>>>(t, FlagTables{}, arena, packed, 0, 0xff, kb);
+        pdl_launch(k_pack_ev, blocks, 128, 0, st, t, FlagTables{}, arena, packed, 0, 0xff, kb);
         check_launch("gather edges/vertices");
     }
 }
@@ -1093,15 +1163,15 @@ void launch_partials(int op, const LevelTables& t, const double* x1, const doubl
     const int bands = t.n >= 3 ? (t.n - 2 + PB - 1) / PB : 0;
     if (t.nfaces > 0 && bands > 0) {
         const dim3 grid(unsigned(bands), unsigned(t.nfaces));
-        if (op == 0) k_partials_faces<0><<<grid, 256, 0, st>>>(t, x1, x2, scratch, bands);
-        else k_partials_faces<1><<<grid, 256, 0, st>>>(t, x1, x2, scratch, bands);
+        if (op == 0) pdl_launch(k_partials_faces<0>, grid, 256, 0, st, t, x1, x2, scratch, bands);
+        else pdl_launch(k_partials_faces<1>, grid, 256, 0, st, t, x1, x2, scratch, bands);
         check_launch("partials faces");
     }
     const int warps = (t.nfaces + 31) / 32 + t.nedges + (t.nverts + 31) / 32;
     if (warps > 0) {
         const int blocks = (warps + 3) / 4;
-        if (op == 0) k_partials_finish<0><<<blocks, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
-        else k_partials_finish<1><<<blocks, 128, 0, st>>>(t, x1, x2, scratch, bands, part);
+        if (op == 0) pdl_launch(k_partials_finish<0>, blocks, 128, 0, st, t, x1, x2, scratch, bands, part);
+        else pdl_launch(k_partials_finish<1>, blocks, 128, 0, st, t, x1, x2, scratch, bands, part);
         check_launch("partials finish");
     }
 }
@@ -1111,7 +1181,7 @@ void launch_pcg_update(const LevelTables& t, const FlagTables& fl, double* x, co
                        const double* alpha_p) {
     const int bands = t.n >= 3 ? (t.n - 2 + PB - 1) / PB : 0;
     if (t.nfaces > 0 && bands > 0) {
-        k_pcg_update_faces<<<dim3(unsigned(bands), unsigned(t.nfaces)), 256, 0, st>>>(t, x, p, r, ap, alpha, -alpha,
+        pdl_launch(k_pcg_update_faces, dim3(unsigned(bands), unsigned(t.nfaces)), 256, 0, st, t, x, p, r, ap, alpha, -alpha,
                                                                                     scratch, bands, alpha_p);
         check_launch("pcg update faces");
     }
@@ -1121,13 +1191,13 @@ void launch_pcg_update(const LevelTables& t, const FlagTables& fl, double* x, co
         DevScalars up, dn;
         up.pa = dn.pa = alpha_p;
         dn.sa = -1.0;
-        k_blas1_ev<<<blocks, 128, 0, st>>>(1, t, fl, alpha, p, 0.0, p, x, F_ALL, kb, up);
-        k_blas1_ev<<<blocks, 128, 0, st>>>(1, t, fl, -alpha, ap, 0.0, ap, r, F_ALL, kb, dn);
+        pdl_launch(k_blas1_ev, blocks, 128, 0, st, 1, t, fl, alpha, p, 0.0, p, x, F_ALL, kb, up);
+        pdl_launch(k_blas1_ev, blocks, 128, 0, st, 1, t, fl, -alpha, ap, 0.0, ap, r, F_ALL, kb, dn);
         check_launch("pcg update edges/vertices");
     }
     const int warps = (t.nfaces + 31) / 32 + t.nedges + (t.nverts + 31) / 32;
     if (warps > 0) {
-        k_partials_finish<0><<<(warps + 3) / 4, 128, 0, st>>>(t, r, r, scratch, bands, part);
+        pdl_launch(k_partials_finish<0>, (warps + 3) / 4, 128, 0, st, t, r, r, scratch, bands, part);
         check_launch("partials finish");
     }
 }
@@ -1136,6 +1206,7 @@ void launch_pcg_update(const LevelTables& t, const FlagTables& fl, double* x, co
 // stage 0: alpha = rz / pAp (pAp <= 0 sets the breakdown flag);
 // stage 1: beta = rz_new / rz, rz = rz_new, res[k] = sqrt(r.r)
 __global__ void k_pcg_scalars(int stage, PcgScalars* s, double* res, int k) {
+    pdl_prologue();
     if (threadIdx.x != 0) return;
     if (stage == 0) {
         if (!(s->pap > 0.0) && s->bad == 0.0) s->bad = double(k) + 1.0;
@@ -1148,13 +1219,13 @@ __global__ void k_pcg_scalars(int stage, PcgScalars* s, double* res, int k) {
 }
 
 void launch_pcg_scalars(int stage, PcgScalars* s, double* res, int k, cudaStream_t st) {
-    k_pcg_scalars<<<1, 32, 0, st>>>(stage, s, res, k);
+    pdl_launch(k_pcg_scalars, 1, 32, 0, st, stage, s, res, k);
     check_launch("pcg scalars");
 }
 
 void launch_combine_tree(int op, double* v, int64_t len, double* out, cudaStream_t st) {
-    if (op == 0) k_combine_tree<0><<<1, 1024, 0, st>>>(v, len, out);
-    else k_combine_tree<1><<<1, 1024, 0, st>>>(v, len, out);
+    if (op == 0) pdl_launch(k_combine_tree<0>, 1, 1024, 0, st, v, len, out);
+    else pdl_launch(k_combine_tree<1>, 1, 1024, 0, st, v, len, out);
     check_launch("combine tree");
 }
 
@@ -1168,6 +1239,7 @@ namespace {
 
 __global__ void k_coarse_gather(int64_t nloc, const int64_t* __restrict__ gidx, const int64_t* __restrict__ pos,
                                 const double* __restrict__ arena, double* __restrict__ glob) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nloc; i += int64_t(gridDim.x) * blockDim.x)
         glob[gidx[i]] = arena[pos[i]];
 }
@@ -1175,6 +1247,7 @@ __global__ void k_coarse_gather(int64_t nloc, const int64_t* __restrict__ gidx, 
 __global__ void k_coarse_scatter_add(int64_t nloc, const int64_t* __restrict__ gidx, const int64_t* __restrict__ pos,
                                      const uint8_t* __restrict__ flag, uint8_t mask,
                                      const double* __restrict__ glob, double* __restrict__ arena) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nloc; i += int64_t(gridDim.x) * blockDim.x)
         if (flag[i] & mask) arena[pos[i]] += 1.0 * glob[gidx[i]];
 }
@@ -1217,6 +1290,7 @@ __global__ void __launch_bounds__(CG_THREADS) k_coarse_cg(int64_t n, const int32
                                                           const double* __restrict__ bg, double* xg, double* r,
                                                           double* p, double* ap, double tol, int max_iter,
                                                           CoarseStatus* st, int in_smem) {
+    pdl_prologue();
     __shared__ double red[33];
     extern __shared__ double dsm[]; // small systems: all five vectors on chip
     const double* b = bg;
@@ -1380,6 +1454,7 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_grid(int64_t n, const
                                                                 const double* __restrict__ b, double* x, double* r,
                                                                 double* p, double* ap, double tol, int max_iter,
                                                                 CoarseStatus* st, double* part, unsigned* bar) {
+    pdl_prologue();
     __shared__ double red[33];
     const int64_t stride = int64_t(gridDim.x) * CGG_THREADS;
     const int64_t i0 = blockIdx.x * int64_t(CGG_THREADS) + threadIdx.x;
@@ -1437,7 +1512,7 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_grid(int64_t n, const
 void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos, const double* arena, double* glob,
                           cudaStream_t st) {
     if (nloc <= 0) return;
-    k_coarse_gather<<<grid_for(nloc), 256, 0, st>>>(nloc, gidx, pos, arena, glob);
+    pdl_launch(k_coarse_gather, grid_for(nloc), 256, 0, st, nloc, gidx, pos, arena, glob);
     check_launch("coarse gather");
 }
 
@@ -1455,6 +1530,7 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const 
                                                                const double* __restrict__ b, double* x, double* R,
                                                                double tol, int max_iter, CoarseStatus* st,
                                                                double* part, unsigned* bar) {
+    pdl_prologue();
     __shared__ double red[66];
     const int64_t i = blockIdx.x * int64_t(CGG_THREADS) + threadIdx.x;
     const bool own = i < n;
@@ -1629,7 +1705,7 @@ void launch_coarse_cg(int64_t n, const int32_t* rowptr, const int32_t* col, cons
 void launch_coarse_scatter_add(int64_t nloc, const int64_t* gidx, const int64_t* pos, const uint8_t* flag,
                                uint8_t mask, const double* glob, double* arena, cudaStream_t st) {
     if (nloc <= 0) return;
-    k_coarse_scatter_add<<<grid_for(nloc), 256, 0, st>>>(nloc, gidx, pos, flag, mask, glob, arena);
+    pdl_launch(k_coarse_scatter_add, grid_for(nloc), 256, 0, st, nloc, gidx, pos, flag, mask, glob, arena);
     check_launch("coarse scatter");
 }
 
@@ -1707,6 +1783,7 @@ __global__ void __launch_bounds__(MR_THREADS) k_coarse_minres(int64_t n, const i
                                                              const double* __restrict__ val, double* bg, double* xg,
                                                              double* work, double tol, int max_iter, int64_t pb,
                                                              int64_t pe, CoarseStatus* st, double* hist, int in_smem) {
+    pdl_prologue();
     __shared__ double bc[2];
     extern __shared__ double dsm[];
     double* base = in_smem ? dsm : work;

@@ -15,6 +15,7 @@ template <int MODE>
 __global__ void __launch_bounds__(128) k_p2_face(P2Tables T, const double* __restrict__ x,
                                                  const double* __restrict__ b, double* __restrict__ y, double omega,
                                                  uint8_t mask) {
+    pdl_prologue();
     const int n2 = T.t.n;
     const int r = 1 + int(blockIdx.x);
     const int face = blockIdx.y;
@@ -47,6 +48,7 @@ template <int MODE>
 __global__ void __launch_bounds__(128) k_p2_edge(P2Tables T, FlagTables fl, const double* __restrict__ x,
                                                  const double* __restrict__ b, double* __restrict__ y, double omega,
                                                  uint8_t mask, int kblocks) {
+    pdl_prologue();
     const int n2 = T.t.n;
     const int e = blockIdx.x / kblocks;
     const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
@@ -82,6 +84,7 @@ template <int MODE>
 __global__ void __launch_bounds__(128) k_p2_vertex(P2Tables T, FlagTables fl, const double* __restrict__ x,
                                                    const double* __restrict__ b, double* __restrict__ y, double omega,
                                                    uint8_t mask) {
+    pdl_prologue();
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= T.t.nverts) return;
     const uint8_t f = fl.vtx_flag[v];
@@ -120,6 +123,7 @@ __device__ __forceinline__ void p2_gs_point(const P2Tables& T, const P2FaceCoef&
 }
 
 __global__ void __launch_bounds__(256) k_p2_gs_face(P2Tables T, const double* __restrict__ b, double* x) {
+    pdl_prologue();
     const int n2 = T.t.n, n = n2 / 2;
     const int face = blockIdx.x;
     const P2FaceCoef& F = T.face[face];
@@ -155,6 +159,7 @@ __global__ void __launch_bounds__(256) k_p2_gs_face(P2Tables T, const double* __
 // edges: line vertex rows k = 1..n-1, then midline rows, sequentially in place
 // (one thread per edge); vertices: one row each
 __global__ void __launch_bounds__(128) k_p2_gs_ev(P2Tables T, FlagTables fl, const double* __restrict__ b, double* x) {
+    pdl_prologue();
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     const int n2 = T.t.n;
     if (id < T.t.nedges) {
@@ -184,11 +189,13 @@ __global__ void __launch_bounds__(128) k_p2_gs_ev(P2Tables T, FlagTables fl, con
 // ---- owned DoFs through a position list (P2 GlobalDoFMap order) -----------------
 __global__ void k_scatter_pos(int64_t n, const int64_t* __restrict__ pos, const uint8_t* __restrict__ flag,
                               uint8_t mask, const double* __restrict__ packed, double* __restrict__ arena) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         if (flag[i] & mask) arena[pos[i]] = packed[i];
 }
 __global__ void k_gather_pos(int64_t n, const int64_t* __restrict__ pos, const double* __restrict__ arena,
                              double* __restrict__ packed) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         packed[i] = arena[pos[i]];
 }
@@ -200,33 +207,33 @@ void launch_p2(int mode, const P2Tables& T, const FlagTables& fl, const double* 
     const int n2 = T.t.n;
     if (T.t.nfaces > 0 && n2 >= 3) {
         const dim3 grid(unsigned(n2 - 2), unsigned(T.t.nfaces));
-        if (mode == P2_APPLY) p2dev::k_p2_face<P2_APPLY><<<grid, 128, 0, st>>>(T, x, b, y, omega, mask);
-        else p2dev::k_p2_face<P2_JACOBI><<<grid, 128, 0, st>>>(T, x, b, y, omega, mask);
+        if (mode == P2_APPLY) pdl_launch(p2dev::k_p2_face<P2_APPLY>, grid, 128, 0, st, T, x, b, y, omega, mask);
+        else pdl_launch(p2dev::k_p2_face<P2_JACOBI>, grid, 128, 0, st, T, x, b, y, omega, mask);
         check_launch("p2 faces");
     }
     if (T.t.nedges > 0) {
         const int kb = (n2 - 1 + 127) / 128;
         if (mode == P2_APPLY)
-            p2dev::k_p2_edge<P2_APPLY><<<T.t.nedges * kb, 128, 0, st>>>(T, fl, x, b, y, omega, mask, kb);
-        else p2dev::k_p2_edge<P2_JACOBI><<<T.t.nedges * kb, 128, 0, st>>>(T, fl, x, b, y, omega, mask, kb);
+            pdl_launch(p2dev::k_p2_edge<P2_APPLY>, T.t.nedges * kb, 128, 0, st, T, fl, x, b, y, omega, mask, kb);
+        else pdl_launch(p2dev::k_p2_edge<P2_JACOBI>, T.t.nedges * kb, 128, 0, st, T, fl, x, b, y, omega, mask, kb);
         check_launch("p2 edges");
     }
     if (T.t.nverts > 0) {
         const int blocks = (T.t.nverts + 127) / 128;
-        if (mode == P2_APPLY) p2dev::k_p2_vertex<P2_APPLY><<<blocks, 128, 0, st>>>(T, fl, x, b, y, omega, mask);
-        else p2dev::k_p2_vertex<P2_JACOBI><<<blocks, 128, 0, st>>>(T, fl, x, b, y, omega, mask);
+        if (mode == P2_APPLY) pdl_launch(p2dev::k_p2_vertex<P2_APPLY>, blocks, 128, 0, st, T, fl, x, b, y, omega, mask);
+        else pdl_launch(p2dev::k_p2_vertex<P2_JACOBI>, blocks, 128, 0, st, T, fl, x, b, y, omega, mask);
         check_launch("p2 vertices");
     }
 }
 
 void launch_p2_gs(const P2Tables& T, const FlagTables& fl, const double* b, double* x, cudaStream_t st) {
     if (T.t.nfaces > 0 && T.t.n >= 4) {
-        p2dev::k_p2_gs_face<<<T.t.nfaces, 256, 0, st>>>(T, b, x);
+        pdl_launch(p2dev::k_p2_gs_face, T.t.nfaces, 256, 0, st, T, b, x);
         check_launch("p2 gs faces");
     }
     const int m = T.t.nedges + T.t.nverts;
     if (m > 0) {
-        p2dev::k_p2_gs_ev<<<(m + 127) / 128, 128, 0, st>>>(T, fl, b, x);
+        pdl_launch(p2dev::k_p2_gs_ev, (m + 127) / 128, 128, 0, st, T, fl, b, x);
         check_launch("p2 gs edges/vertices");
     }
 }
@@ -234,11 +241,11 @@ void launch_p2_gs(const P2Tables& T, const FlagTables& fl, const double* b, doub
 void launch_scatter_pos(int64_t n, const int64_t* pos, const uint8_t* flag, uint8_t mask, const double* packed,
                         double* arena, cudaStream_t st) {
     if (n <= 0) return;
-    p2dev::k_scatter_pos<<<grid_for(n), 256, 0, st>>>(n, pos, flag, mask, packed, arena);
+    pdl_launch(p2dev::k_scatter_pos, grid_for(n), 256, 0, st, n, pos, flag, mask, packed, arena);
     check_launch("scatter positions");
 }
 void launch_gather_pos(int64_t n, const int64_t* pos, const double* arena, double* packed, cudaStream_t st) {
     if (n <= 0) return;
-    p2dev::k_gather_pos<<<grid_for(n), 256, 0, st>>>(n, pos, arena, packed);
+    pdl_launch(p2dev::k_gather_pos, grid_for(n), 256, 0, st, n, pos, arena, packed);
     check_launch("gather positions");
 }

@@ -25,6 +25,7 @@ inline dim3 transfer_grid(int nc, int nfaces) {
 __global__ void __launch_bounds__(TR_WARPS * 32) k_prolongate_faces(LevelTables tc, LevelTables tf,
                                                                     const double* __restrict__ xc, double* xf,
                                                                     int add) {
+    pdl_prologue();
     const int nc = tc.n, nf = tf.n;
     const int lane = threadIdx.x & 31;
     const int cw = (blockIdx.x * TR_WARPS + (threadIdx.x >> 5)) * 32; // first coarse column of the warp
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(TR_WARPS * 32) k_prolongate_faces(LevelTables 
 __global__ void __launch_bounds__(TR_WARPS * 32) k_restrict_faces(LevelTables tc, LevelTables tf,
                                                                   const double* __restrict__ xf,
                                                                   double* __restrict__ xc) {
+    pdl_prologue();
     const int nc = tc.n, nf = tf.n;
     const int lane = threadIdx.x & 31;
     const int cw = (blockIdx.x * TR_WARPS + (threadIdx.x >> 5)) * 32;
@@ -162,6 +164,7 @@ __global__ void __launch_bounds__(TR_WARPS * 32) k_restrict_faces(LevelTables tc
 // k_face_stencil<RESIDUAL>.
 __global__ void __launch_bounds__(128) k_residual_layer(LevelTables t, const double* __restrict__ x,
                                                         const double* __restrict__ b, double* __restrict__ r) {
+    pdl_prologue();
     const int n = t.n;
     const int k = 1 + blockIdx.x * blockDim.x + threadIdx.x;
     if (k > n - 2) return;
