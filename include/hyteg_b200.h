@@ -276,6 +276,14 @@ int hyb_apply(hyb_operator* A, hyb_function* src, hyb_function* dst, int level, 
 int hyb_residual(hyb_operator* A, hyb_function* rhs, hyb_function* x, hyb_function* r, int level);
 /* smooth_jacobi(A, ctl, rhs, x, omega, level)     operators.hpp:113-114 */
 int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level);
+/* two smooth_jacobi sweeps in a row, bitwise the two calls. With the tuning knob
+ * "jacobi2_min_n" at or below the level's face size (2^level) they run as one
+ * temporal-blocking pass over the faces (x1 formed in registers, x2 written: 24
+ * instead of 48 bytes per DoF at the face interiors); measured issue-bound and
+ * slower than two sweeps on B200, so the knob defaults to off. */
+int hyb_smooth_jacobi2(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level);
+/* measurement knobs: "jacobi2_min_n" (value < 0: query only; *previous = old value) */
+int hyb_tuning(const char* name, int64_t value, int64_t* previous);
 /* smooth_gs(A, ctl, rhs, x, level): hybrid Gauss-Seidel, lexicographic inside
  * each primitive, halos frozen after the initial sync (operators.hpp:120-121);
  * bitwise the reference's (wavefront over t = c + 2r on faces) */
@@ -327,6 +335,10 @@ int hyb_hierarchy_vcycle(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, i
  * enable < 0 leaves the setting unchanged; *replays = graph launches so far */
 int hyb_hierarchy_graphs(hyb_hierarchy* h, int enable, int64_t* replays);
 int hyb_hierarchy_residual_norm(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, double* out);
+/* Jacobi V(2, nu2 >= 2) cycles smooth the finest pre-smoothing pair with one
+ * two-sweep pass (hyb_smooth_jacobi2; bitwise the two sweeps); default on,
+ * enable < 0 leaves the setting; *state = current setting */
+int hyb_hierarchy_temporal(hyb_hierarchy* h, int enable, int* state);
 /* residuals[0..*n_out): ||rhs - A x|| before each cycle and after the last */
 int hyb_hierarchy_solve(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, double tol, int max_cycles,
                         int nu_pre, int nu_post, double* residuals, int* n_out, int* converged);

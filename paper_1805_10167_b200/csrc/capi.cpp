@@ -733,6 +733,15 @@ int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, doubl
     });
 }
 
+int hyb_smooth_jacobi2(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level) {
+    return guarded([&] {
+        need(A, "hyb_smooth_jacobi2");
+        need(rhs, "hyb_smooth_jacobi2");
+        need(x, "hyb_smooth_jacobi2");
+        hyb::smooth_jacobi2(*A->a, *rhs->f, *x->f, omega, level);
+    });
+}
+
 int hyb_diagonal(hyb_operator* A, hyb_function* d, int level) {
     return guarded([&] {
         need(A, "hyb_diagonal");
@@ -860,6 +869,27 @@ int hyb_hierarchy_graphs(hyb_hierarchy* h, int enable, int64_t* replays) {
         need(h, "hyb_hierarchy_graphs");
         if (enable >= 0) h->h->use_graphs = enable != 0;
         if (replays) *replays = h->h->graph_replays;
+    });
+}
+
+int hyb_tuning(const char* name, int64_t value, int64_t* previous) {
+    return guarded([&] {
+        need(name, "hyb_tuning");
+        const std::string k(name);
+        if (k == "jacobi2_min_n") {
+            if (previous) *previous = hyb::jacobi2_min_n();
+            if (value >= 0) hyb::set_jacobi2_min_n(int(std::min<int64_t>(value, int64_t(1) << 30)));
+        } else {
+            throw hyb::InvalidArgument("hyb_tuning: unknown knob '" + k + "'");
+        }
+    });
+}
+
+int hyb_hierarchy_temporal(hyb_hierarchy* h, int enable, int* state) {
+    return guarded([&] {
+        need(h, "hyb_hierarchy_temporal");
+        if (enable >= 0) h->h->temporal_ = enable != 0;
+        if (state) *state = h->h->temporal_ ? 1 : 0;
     });
 }
 

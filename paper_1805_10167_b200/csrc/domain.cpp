@@ -385,6 +385,21 @@ DevMem& Domain::jacobi_scratch(int L, int kind) {
     return jacobi_[key] = std::move(m);
 }
 
+DevMem& Domain::jacobi_scratch2(int L) {
+    auto it = jacobi2_.find(L);
+    if (it != jacobi2_.end()) return it->second;
+    DevMem m(size_t(level(L).t.arena_size) * 8);
+    HYB_CUDA(cudaMemsetAsync(m.as<void>(), 0, m.bytes(), stream_));
+    return jacobi2_[L] = std::move(m);
+}
+
+const void* Domain::jacobi_scratch2_ptr(int L) const {
+    auto it = jacobi2_.find(L);
+    return it == jacobi2_.end() ? nullptr : it->second.as<void>();
+}
+
+void Domain::swap_scratch(int L) { jacobi_scratch(L).swap(jacobi_scratch2(L)); }
+
 double* Domain::staging(int64_t doubles) {
     if (int64_t(staging_.bytes() / 8) < doubles) {
         HYB_CUDA(cudaStreamSynchronize(stream_));

@@ -221,6 +221,13 @@ class Domain {
 
     // scratch
     DevMem& jacobi_scratch(int level, int kind = KIND_P1);
+    /// a second scratch arena (P1): the two-sweep Jacobi pass writes x2 there
+    DevMem& jacobi_scratch2(int level);
+    const void* jacobi_scratch2_ptr(int level) const; // nullptr until allocated
+    /// exchange the two scratch arenas of a level (their contents are dead between operations)
+    void swap_scratch(int level);
+    /// ghost refresh of an arena of `kind` at `level` that no Function owns (a scratch arena)
+    void sync_arena(int kind, int level, double* arena);
     /// exchange staging (reallocated when a level with more traffic is built:
     /// part of the V-cycle graph key)
     const void* send_buffer() const { return sendbuf_.as<void>(); }
@@ -306,6 +313,7 @@ class Domain {
     DevMem geo_;
     std::map<int, std::unique_ptr<LevelGeom>> levels_;
     std::map<int, DevMem> jacobi_; // key level + 64 * kind
+    std::map<int, DevMem> jacobi2_;
     DevMem staging_, partials_, scalars_, sendbuf_, recvbuf_;
     void* nccl_comm_ = nullptr;
     std::vector<KernelTimer> pending_;
@@ -317,7 +325,17 @@ class Domain {
 void apply(const Operator& A, Function& src, Function& dst, int level, uint8_t mask);
 void residual(const Operator& A, Function& rhs, Function& x, Function& r, int level);
 /// dotp: optional per-CTA partials of rhs.x_new over the faces (face_dot_slots)
-void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level, double* dotp = nullptr);
+/// target 2: the new iterate goes to the level's second scratch arena (Hierarchy's
+/// arena bookkeeping after a two-sweep pass)
+void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level, double* dotp = nullptr,
+                   int target = 1);
+/// two weighted-Jacobi sweeps, bitwise two smooth_jacobi calls, in one pass over the
+/// faces where the level is large enough (temporal blocking, ST_JACOBI2); x's arena
+/// ends up exchanged with the second scratch arena
+void smooth_jacobi2(const Operator& A, Function& rhs, Function& x, double omega, int level);
+/// the smallest face size (n = 2^L) the two-sweep pass is used for (default: never)
+int jacobi2_min_n();
+void set_jacobi2_min_n(int n);
 /// dst = A src (all flags) and returns src.dst, one pass over the faces
 double apply_dot(const Operator& A, Function& src, Function& dst, int level);
 /// the same with src.dst left on the device at *out (no host round trip)
@@ -401,6 +419,7 @@ class Hierarchy {
   public:
     bool use_graphs = true;
     bool fuse_post_ = true; // prolongate_add fused with the first Jacobi post-sweep
+    bool temporal_ = true;  // V(2, nu2 >= 2) Jacobi: the finest pre-smoothing pair as one two-sweep pass
     int64_t graph_replays = 0;
 
   private:

@@ -47,6 +47,8 @@ void Domain::sync(Function& f, int L) {
     run_exchange(geom(f.kind(), L).xch, f.data(L));
 }
 
+void Domain::sync_arena(int kind, int L, double* arena) { run_exchange(geom(kind, L).xch, arena); }
+
 void Domain::run_exchange(Exchange& X, double* arena) {
     double* sb = sendbuf_.as<double>();
     double* rb = recvbuf_.as<double>();

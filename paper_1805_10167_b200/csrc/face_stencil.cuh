@@ -91,7 +91,7 @@ template <int MODE> constexpr int fs_stages() { return MODE == ST_JACOBI_PROLONG
 template <int MODE> struct FaceSmem {
     static constexpr int NS = fs_stages<MODE>();
     double x[NS][MODE == ST_RESTRICT_RESIDUAL ? FS_XW_RR : FS_XW];
-    double b[MODE == ST_APPLY ? 1 : NS][MODE == ST_RESTRICT_RESIDUAL ? FS_BW_RR : FS_COLS];
+    double b[MODE == ST_APPLY ? 1 : NS][MODE == ST_RESTRICT_RESIDUAL ? FS_BW_RR : (MODE == ST_JACOBI2 ? FS_XW : FS_COLS)];
     double cr[MODE == ST_JACOBI_PROLONG ? FS_NCR : 1][MODE == ST_JACOBI_PROLONG ? FS_CW : 2];
     uint64_t full[NS];
     uint64_t empty[NS];
@@ -119,12 +119,13 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                                                                  double* __restrict__ dotp,
                                                                  const double* __restrict__ xc, EvTail ev = EvTail{}) {
     pdl_prologue();
-    if constexpr (MODE == ST_APPLY || MODE == ST_RESIDUAL || MODE == ST_JACOBI || MODE == ST_JACOBI_PROLONG) {
+    if constexpr (MODE == ST_APPLY || MODE == ST_RESIDUAL || MODE == ST_JACOBI || MODE == ST_JACOBI_PROLONG ||
+                  MODE == ST_JACOBI2) {
         if (int(blockIdx.z) >= t.nfaces) { // CTA-uniform: before any barrier
             const int blk = (int(blockIdx.z - t.nfaces) * int(gridDim.y) + int(blockIdx.y)) * int(gridDim.x) +
                             int(blockIdx.x);
             // (the fused correction's edges and vertices were corrected in place: a plain Jacobi row)
-            constexpr int EVM = MODE == ST_JACOBI_PROLONG ? int(ST_JACOBI) : MODE;
+            constexpr int EVM = (MODE == ST_JACOBI_PROLONG || MODE == ST_JACOBI2) ? int(ST_JACOBI) : MODE;
             if (blk < ev.blocks && threadIdx.x < 128)
                 ev_stencil_block<EVM>(t, ev.fl, x, b, y, omega, ev.mask, ev.kblocks, blk);
             return;
@@ -132,10 +133,14 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     }
     constexpr bool RR = MODE == ST_RESTRICT_RESIDUAL;
     constexpr bool JP = MODE == ST_JACOBI_PROLONG; // xc: coarse correction (level L-1, cro, cstride)
+    // ST_JACOBI2: x staged from two rows below the band (x1 of the row below the band needs
+    // it); b staged like x (x1 at the block's outer columns c0-1 and c0+256); dotp is y2
+    constexpr bool J2 = MODE == ST_JACOBI2;
+    constexpr int XR = J2 ? 2 : 1;             // x rows staged below the band
     constexpr int XOFF = RR ? 4 : 2;           // smem x index of column c0
     constexpr int XW = RR ? FS_XW_RR : FS_XW;  // staged x width
-    constexpr int BOFF = RR ? 2 : 0;           // smem b index of column c0
-    constexpr int BW = RR ? FS_BW_RR : FS_COLS;
+    constexpr int BOFF = RR ? 2 : (J2 ? 2 : 0); // smem b index of column c0
+    constexpr int BW = RR ? FS_BW_RR : (J2 ? FS_XW : FS_COLS);
     constexpr int NS = FaceSmem<MODE>::NS;
     extern __shared__ __align__(128) unsigned char fs_dyn[];
     __shared__ __align__(128) unsigned char fs_static[MODE == ST_JACOBI_PROLONG ? 16 : sizeof(FaceSmem<MODE>)];
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         }
     }
     const int nrows = r_hi - r_lo;      // computed rows
-    const int nstage = nrows + 2;       // x rows r_lo-1 .. r_hi
+    const int nstage = nrows + 2 * XR;  // x rows r_lo-XR .. r_hi+XR-1
 
     const int64_t base = int64_t(face) * t.face_stride;
     const int64_t* __restrict__ ro = t.rowoff;
@@ -195,11 +200,11 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
             for (int i = 0; i < nstage; ++i) {
                 const int s = i % NS;
                 mbar_wait(&sm.empty[s], ((i / NS) & 1) ^ 1);
-                const int q = r_lo - 1 + i; // x row of this stage
+                const int q = r_lo - XR + i; // x row of this stage (J2: -1 below row 1 -> nothing staged)
                 const int plen = (W - q + 3) & ~3; // padded row length
                 const int xs = c0 - XOFF < 0 ? 0 : c0 - XOFF;
                 const int xe = c0 - XOFF + XW < plen ? c0 - XOFF + XW : plen;
-                const uint32_t bx = xe > xs ? uint32_t(xe - xs) * 8u : 0u;
+                const uint32_t bx = (q >= 0 && xe > xs) ? uint32_t(xe - xs) * 8u : 0u;
                 uint32_t bb = 0;
                 int bs0 = 0;
                 if (MODE != ST_APPLY && i >= 2) { // b row q-1 pairs with x row q
@@ -249,6 +254,11 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
 
     // window: rows r-1 (m*) and r (z*) at columns c-1, c, c+1, c+2 (and c-2: *ll)
     double ml = 0, m0 = 0, m1 = 0, mr = 0, zl = 0, z0 = 0, z1 = 0, zr = 0;
+    // ST_JACOBI2: x0 at columns c-2 (zll) and c+3 (mrr, zrr); x1 rows s-1 (A*) and s (B*) at
+    // columns c-1 .. c+2; b of the previous x1 row (the x2 row's)
+    double mrr = 0, zll = 0, zrr = 0;
+    double A0 = 0, A1 = 0, A2 = 0, A3 = 0, B0 = 0, B1 = 0, B2 = 0, B3 = 0;
+    double2 bprev = make_double2(0.0, 0.0);
     // ST_RESTRICT_RESIDUAL: residual rows q-2 (s*) and q-1 (h*) at c-1, c, c+1
     double sl = 0, s0 = 0, s1 = 0, hl = 0, h0 = 0, h1 = 0;
     const int nc = n / 2;
@@ -266,9 +276,15 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         const double2 pr2 = *reinterpret_cast<const double2*>(sx + k + 2);
         double2 bb = make_double2(0.0, 0.0);
         if (MODE != ST_APPLY && i >= 2) bb = *reinterpret_cast<const double2*>(&sm.b[s][kb]);
+        double bL = 0.0, bR = 0.0; // J2: b at c-1 (lane 0's extra x1) and c+2 (lane 31's)
+        if (J2 && i >= 2) {
+            bL = sm.b[s][kb - 1];
+            bR = sm.b[s][kb + 2];
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
         double pl = pl2.y, p0 = pc2.x, p1 = pc2.y, pr = pr2.x;
+        const double pll = pl2.x, prr = pr2.y; // J2: columns c-2 and c+3
         if (JP) { // x row q = r_lo-1+i at columns c-1 .. c+2: add P e at points >= 2 away from the border
             const int q = r_lo - 1 + i;
             // staged coarse columns C-1, C, C+1 (C = c/2) of rows R (index 0) and R+1 (1)
@@ -326,7 +342,89 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
             sl = hl; s0 = h0; s1 = h1;
             hl = ol; h0 = o0; h1 = o1;
         }
-        if (!RR && i >= 2) {
+        if (J2 && i >= 2) {
+            // x1 = J(x0) at row r from the window (rows r-1, r, r+1): columns c, c+1 as ST_JACOBI,
+            // plus one outer column per lane, used by lane 0 (c-1) and lane 31 (c+2) only
+            const int r = r_lo - 3 + i;
+            double a0 = 0.0;
+            a0 += cW * zl;
+            a0 += cNW * pl;
+            a0 += cS * m0;
+            a0 += cC * z0;
+            a0 += cN * p0;
+            a0 += cSE * m1;
+            a0 += cE * z1;
+            double a1 = 0.0;
+            a1 += cW * z0;
+            a1 += cNW * p0;
+            a1 += cS * m1;
+            a1 += cC * z1;
+            a1 += cN * p1;
+            a1 += cSE * mr;
+            a1 += cE * zr;
+            const double u0 = z0 + div_by(omega * (bb.x - a0), dg, rdg);
+            const double u1 = z1 + div_by(omega * (bb.y - a1), dg, rdg);
+            const bool left = lane == 0;
+            const double eW = left ? zll : z1, eNW = left ? pll : p1, eS = left ? ml : mr, eC = left ? zl : zr;
+            const double eN = left ? pl : pr, eSE = left ? m0 : mrr, eE = left ? z0 : zrr;
+            double ae = 0.0;
+            ae += cW * eW;
+            ae += cNW * eNW;
+            ae += cS * eS;
+            ae += cC * eC;
+            ae += cN * eN;
+            ae += cSE * eSE;
+            ae += cE * eE;
+            const double ue = eC + div_by(omega * ((left ? bL : bR) - ae), dg, rdg);
+            double vl = __shfl_up_sync(0xffffffffu, u1, 1);   // lane-1's c+1 = c-1
+            double vr = __shfl_down_sync(0xffffffffu, u0, 1); // lane+1's c = c+2
+            if (lane == 0) vl = ue;
+            if (lane == 31) vr = ue;
+            if (r >= r_lo && r < r_hi) { // x1 on the layers one and two away from the borders
+                const int last = n - 1 - r;
+                const bool w0 = c >= 1 && c <= last && (r <= 2 || c <= 2 || n - (c + r) <= 2);
+                const bool w1 = c + 1 <= last && (r <= 2 || c + 1 <= 2 || n - (c + 1 + r) <= 2);
+                double* yrow = yf + ro[r];
+                if (w0) yrow[c] = u0;
+                if (w1) yrow[c + 1] = u1;
+            }
+            if (i >= 4) { // x2 = J(x1) at row r-1 from x1 rows r-2 (A), r-1 (B), r (this step)
+                const int s2 = r - 1;
+                if (s2 >= r_lo && s2 < r_hi && s2 >= 2) {
+                    double c0_ = 0.0;
+                    c0_ += cW * B0;
+                    c0_ += cNW * vl;
+                    c0_ += cS * A1;
+                    c0_ += cC * B1;
+                    c0_ += cN * u0;
+                    c0_ += cSE * A2;
+                    c0_ += cE * B2;
+                    double c1_ = 0.0;
+                    c1_ += cW * B1;
+                    c1_ += cNW * u0;
+                    c1_ += cS * A2;
+                    c1_ += cC * B2;
+                    c1_ += cN * u1;
+                    c1_ += cSE * A3;
+                    c1_ += cE * B3;
+                    const double x20 = B1 + div_by(omega * (bprev.x - c0_), dg, rdg);
+                    const double x21 = B2 + div_by(omega * (bprev.y - c1_), dg, rdg);
+                    const bool d0ok = c >= 2 && c + s2 <= n - 2;   // two or more away from every border
+                    const bool d1ok = c + 1 >= 2 && c + 1 + s2 <= n - 2;
+                    double* zrow = dotp + base + ro[s2];
+                    if (d0ok && d1ok) {
+                        __stcs(reinterpret_cast<double2*>(zrow + c), make_double2(x20, x21));
+                    } else {
+                        if (d0ok) zrow[c] = x20;
+                        if (d1ok) zrow[c + 1] = x21;
+                    }
+                }
+            }
+            A0 = B0; A1 = B1; A2 = B2; A3 = B3;
+            B0 = vl; B1 = u0; B2 = u1; B3 = vr;
+            bprev = bb;
+        }
+        if (!RR && !J2 && i >= 2) {
             const int r = r_lo + i - 2;
             const int last = n - 1 - r; // last interior column of row r
             const bool v0 = c >= 1 && c <= last;
@@ -376,6 +474,11 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
         }
         ml = zl; m0 = z0; m1 = z1; mr = zr;
         zl = pl; z0 = p0; z1 = p1; zr = pr;
+        if (J2) {
+            mrr = zrr;
+            zll = pll;
+            zrr = prr;
+        }
     }
     if (DOT) { // consumer warps only (the producer has returned)
         double v = d0 + d1;

@@ -727,6 +727,94 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
     }
 }
 
+// ST_JACOBI2's second half on the face points one away from a border: x2 =
+// J(x1) from x1 (the layers the pass wrote, the border ghosts refreshed from
+// the edges' x1), same term order and division as ST_JACOBI. Thread j covers
+// row 1 (slot 0), column 1 (slot 1) and the diagonal's neighbour line (slot
+// 2), each corner point once.
+__global__ void __launch_bounds__(128) k_jacobi2_layer(LevelTables t, const double* __restrict__ x1,
+                                                       const double* __restrict__ b, double* __restrict__ x2,
+                                                       double omega) {
+    pdl_prologue();
+    const int n = t.n, m = n - 2;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= 3 * m) return;
+    const int slot = j / m, w = 1 + j % m;
+    int c, r;
+    if (slot == 0) {
+        c = w;
+        r = 1;
+    } else if (slot == 1) {
+        c = 1;
+        r = w;
+        if (r == 1) return;
+    } else {
+        r = w;
+        c = n - 1 - w;
+        if (r == 1 || c == 1) return;
+    }
+    if (c < 1 || c + r > n - 1) return;
+    const int face = blockIdx.y;
+    const double* co = t.face_coef + size_t(face) * 8;
+    const double dg = co[7], rdg = 1.0 / dg;
+    const int64_t base = int64_t(face) * t.face_stride;
+    const int64_t* ro = t.rowoff;
+    const double* xm = x1 + base + ro[r - 1];
+    const double* x0 = x1 + base + ro[r];
+    const double* xp = x1 + base + ro[r + 1];
+    double acc = 0.0;
+    acc += co[0] * x0[c - 1];
+    acc += co[1] * xp[c - 1];
+    acc += co[2] * xm[c];
+    acc += co[3] * x0[c];
+    acc += co[4] * xp[c];
+    acc += co[5] * xm[c + 1];
+    acc += co[6] * x0[c + 1];
+    x2[base + ro[r] + c] = x0[c] + div_by(omega * (b[base + ro[r] + c] - acc), dg, rdg);
+}
+
+void launch_jacobi2(const LevelTables& t, const FlagTables& fl, const double* x, const double* b, double* y1,
+                    double* y2, double omega, cudaStream_t st) {
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    dim3 grid = face_stencil_grid(t);
+    EvTail ev;
+    const unsigned ev_z = unsigned((blocks + int(grid.x * grid.y) - 1) / int(grid.x * grid.y));
+    bool ev_done = false;
+    if (blocks > 0 && grid.z + ev_z <= 65535u) { // edges/vertices' first sweep as trailing CTAs
+        ev.fl = fl;
+        ev.mask = F_ALL;
+        ev.kblocks = kb;
+        ev.blocks = blocks;
+        grid.z += ev_z;
+        ev_done = true;
+    }
+    if (t.nfaces > 0 || ev_done) {
+        pdl_launch(k_face_stencil<ST_JACOBI2>, grid, FS_THREADS, 0, st, t, x, b, y1, omega, nullptr, int64_t(0), y2,
+                   nullptr, ev);
+        check_launch("two-sweep jacobi faces");
+    }
+    if (!ev_done && blocks > 0) {
+        pdl_launch(k_ev_stencil<ST_JACOBI>, blocks, 128, 0, st, t, fl, x, b, y1, omega, uint8_t(F_ALL), kb);
+        check_launch("edge/vertex stencil");
+    }
+}
+
+void launch_jacobi2_finish(const LevelTables& t, const FlagTables& fl, const double* y1, const double* b, double* y2,
+                           double omega, cudaStream_t st) {
+    if (t.nfaces > 0 && t.n >= 4) {
+        pdl_launch(k_jacobi2_layer, dim3(unsigned((3 * (t.n - 2) + 127) / 128), unsigned(t.nfaces)), 128, 0, st, t,
+                   y1, b, y2, omega);
+        check_launch("two-sweep jacobi layer");
+    }
+    const int kb = kblocks_for(t.n);
+    const int blocks = t.nedges * kb + (t.nverts + 127) / 128;
+    if (blocks > 0) {
+        pdl_launch(k_ev_stencil<ST_JACOBI>, blocks, 128, 0, st, t, fl, y1, b, y2, omega, uint8_t(F_ALL), kb);
+        check_launch("edge/vertex stencil");
+    }
+}
+
 void launch_ghost_gather(const void* dst, const void* src, bool idx32, int64_t nlocal, int64_t ntotal, double* arena,
                          const double* recv, cudaStream_t st) {
     if (ntotal <= 0) return;

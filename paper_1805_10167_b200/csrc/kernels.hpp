@@ -86,7 +86,12 @@ enum StencilMode : int {
     ST_JACOBI = 2,
     ST_RESTRICT_RESIDUAL = 3,
     ST_JACOBI_ZERO = 4,
-    ST_JACOBI_PROLONG = 5
+    ST_JACOBI_PROLONG = 5,
+    // two weighted-Jacobi sweeps in one pass over the faces (temporal
+    // blocking): x1 = J(x0) is formed in registers, x2 = J(x1) is written at
+    // face points two or more away from every border, x1 at the one- and
+    // two-away layers (what the edges' second sweep and the layer pass read)
+    ST_JACOBI2 = 6
 };
 
 // ---- launchers (all asynchronous on `st`) ----
@@ -267,6 +272,15 @@ size_t coarse_minres_work_doubles(int64_t n);
 void launch_coarse_minres(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, double* b,
                           double* x, double* work, double tol, int max_iter, int64_t proj_begin, int64_t proj_end,
                           CoarseStatus* st, double* hist, cudaStream_t stream);
+/// ST_JACOBI2 pass (faces, plus the edges'/vertices' first sweep x -> y1 as
+/// trailing CTAs): y1 gets x1 on the face layers one and two away from the
+/// borders and on edges/vertices, y2 gets x2 at face points two or more away
+void launch_jacobi2(const LevelTables& t, const FlagTables& fl, const double* x, const double* b, double* y1,
+                    double* y2, double omega, cudaStream_t st);
+/// the second sweep where the pass above could not form it: face points one
+/// away from a border (from y1 with refreshed ghosts) and edges/vertices
+void launch_jacobi2_finish(const LevelTables& t, const FlagTables& fl, const double* y1, const double* b, double* y2,
+                           double omega, cudaStream_t st);
 /// host copy of the device hypot (glibc's), for the CPU pin
 double glibc_hypot_host(double x, double y);
 void launch_coarse_scatter_add(int64_t nloc, const int64_t* gidx, const int64_t* pos, const uint8_t* flag,

@@ -164,7 +164,7 @@ void residual(const Operator& A, Function& rhs, Function& x, Function& r, int le
     });
 }
 
-void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level, double* dotp) {
+void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, int level, double* dotp, int target) {
     check_op_function(A, rhs, level, "smooth_jacobi", true);
     check_op_function(A, x, level, "smooth_jacobi", true);
     if (&rhs == &x) throw InvalidArgument("smooth_jacobi: rhs and x must be distinct functions");
@@ -181,7 +181,7 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
     }
     check_diagonals(A, x, level, "smooth_jacobi");
     Domain& d = A.domain();
-    DevMem& next = d.jacobi_scratch(level);
+    DevMem& next = target == 2 ? d.jacobi_scratch2(level) : d.jacobi_scratch(level);
     // pending write-back of the reference (src/operators.cpp:435-468) is a
     // second buffer here: read x, write x', swap.
     const LevelTables t = A.tables(level);
@@ -190,6 +190,47 @@ void smooth_jacobi(const Operator& A, Function& rhs, Function& x, double omega, 
                        d.stream(), 3, dotp);
     });
     x.arena(level).swap(next);
+}
+
+namespace {
+// measured on config 2, L10 (one B200): the pass 2.95 ms against 2.10 ms for two
+// sweeps -- issue-bound (ncu: 2.5 IPC, 63% issue slots busy, ~480 instructions per
+// warp and row step for x1 at three columns and x2 at two, 96 registers with
+// spills), so it is off unless asked for (hyb_tuning("jacobi2_min_n", n))
+int g_jacobi2_min_n = 1 << 30;
+} // namespace
+
+int jacobi2_min_n() { return g_jacobi2_min_n; }
+void set_jacobi2_min_n(int n) { g_jacobi2_min_n = n; }
+
+// Two sweeps, x0 -> x1 -> x2: the face pass forms x1 in registers and writes x2
+// two or more away from every border plus x1 on the two layers next to the
+// borders; the edges' and vertices' first sweep runs as its trailing CTAs into
+// the scratch arena; after a ghost refresh of that arena the layer pass and the
+// edges' / vertices' second sweep complete x2. Every value is computed from the
+// same operands in the same order as by two smooth_jacobi calls: bitwise.
+void smooth_jacobi2(const Operator& A, Function& rhs, Function& x, double omega, int level) {
+    check_op_function(A, rhs, level, "smooth_jacobi", true);
+    check_op_function(A, x, level, "smooth_jacobi", true);
+    if (&rhs == &x) throw InvalidArgument("smooth_jacobi: rhs and x must be distinct functions");
+    Domain& d = A.domain();
+    if (A.kind() != KIND_P1 || (1 << level) < jacobi2_min_n()) {
+        smooth_jacobi(A, rhs, x, omega, level);
+        smooth_jacobi(A, rhs, x, omega, level, nullptr, 2); // lands where the pass would put it
+        d.swap_scratch(level);
+        return;
+    }
+    check_diagonals(A, x, level, "smooth_jacobi");
+    d.sync(x, level);
+    const LevelTables t = A.tables(level);
+    DevMem& y1 = d.jacobi_scratch(level);
+    DevMem& y2 = d.jacobi_scratch2(level);
+    d.timer_begin("jacobi2");
+    launch_jacobi2(t, x.flags(), x.data(level), rhs.data(level), y1.as<double>(), y2.as<double>(), omega, d.stream());
+    d.sync_arena(KIND_P1, level, y1.as<double>());
+    launch_jacobi2_finish(t, x.flags(), y1.as<double>(), rhs.data(level), y2.as<double>(), omega, d.stream());
+    d.timer_end();
+    x.arena(level).swap(y2);
 }
 
 namespace {
@@ -745,6 +786,7 @@ std::vector<const void*> Hierarchy::graph_key(Function& rhs, Function& x, int le
             k.push_back(e_.data(l));
         }
         if (l > a_.min_level()) k.push_back(dom_->jacobi_scratch(l).as<void>());
+        k.push_back(dom_->jacobi_scratch2_ptr(l));
     }
     return k;
 }
@@ -811,9 +853,19 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
         coarse_correct(rhs, x);
         return;
     }
-    for (int i = 0; i < nu_pre; ++i) {
-        if (i == 0 && zero_sweep) smooth_jacobi_zero(a_, rhs, x, omega_, level);
-        else smooth(rhs, x, level);
+    // the pre-smoothing pair as one two-sweep pass (x's arena goes to the second
+    // scratch arena); the post-smoothing's last sweep then writes the second scratch
+    // arena, and a final exchange of the two scratch arenas leaves every arena as
+    // the cycle found it (CUDA-graph replay)
+    const bool pair = smoother_ == SMOOTH_JACOBI && temporal_ && !zero_sweep && nu_pre == 2 && nu_post >= 2 &&
+                      (1 << level) >= jacobi2_min_n();
+    if (pair) {
+        smooth_jacobi2(a_, rhs, x, omega_, level);
+    } else {
+        for (int i = 0; i < nu_pre; ++i) {
+            if (i == 0 && zero_sweep) smooth_jacobi_zero(a_, rhs, x, omega_, level);
+            else smooth(rhs, x, level);
+        }
     }
     residual_restrict(a_, rhs, x, r_, b_, level - 1); // residual + restrict_to_coarse, fused
     fill_const(b_, 0.0, level - 1, kDirichletMask);
@@ -828,7 +880,13 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
     } else {
         prolongate(e_, x, level - 1, kSmoothMask, true);
     }
-    for (int i = i0; i < nu_post; ++i) smooth(rhs, x, level, dot_for(i));
+    for (int i = i0; i < nu_post; ++i) {
+        if (pair && i == nu_post - 1) smooth_jacobi(a_, rhs, x, omega_, level, dot_for(i), 2);
+        else smooth(rhs, x, level, dot_for(i));
+    }
+    // (x, s1, s2) went (X, Y, Z) -> (Z, Y, X) in the pass; nu_post - 1 exchanges with s1
+    // and one with s2 bring x back; the scratch pair is swapped when that count is odd
+    if (pair && (nu_post - 1) % 2 == 1) dom_->swap_scratch(level);
 }
 
 // reference src/solvers.cpp:430-442: residual, gather into the global coarse

@@ -521,6 +521,19 @@ def smooth_jacobi(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: S
     check(lib.hyb_smooth_jacobi(A._h, rhs._h, x._h, omega, level))
 
 
+def smooth_jacobi2(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: ScalarFunction,  # noqa: ARG001
+                   omega: float, level: int) -> None:
+    """Two smooth_jacobi sweeps, bitwise, in one pass over the faces (temporal blocking)."""
+    check(lib.hyb_smooth_jacobi2(A._h, rhs._h, x._h, omega, level))
+
+
+def tuning(name: str, value: int = -1) -> int:
+    """Set a measurement knob (value >= 0) and return its previous value."""
+    prev = C.c_int64()
+    check(lib.hyb_tuning(name.encode(), value, C.byref(prev)))
+    return prev.value
+
+
 def diagonal(A: StencilOperator, d: ScalarFunction, level: int) -> None:
     check(lib.hyb_diagonal(A._h, d._h, level))
 
@@ -640,6 +653,12 @@ class GridHierarchy:
         out = C.c_double()
         check(lib.hyb_hierarchy_residual_norm(self._h, rhs._h, x._h, level, C.byref(out)))
         return out.value
+
+    def use_temporal(self, enable: bool | None = None) -> bool:
+        """Toggle the two-sweep pre-smoothing pass of Jacobi V(2, >=2) cycles (default on)."""
+        st = C.c_int()
+        check(lib.hyb_hierarchy_temporal(self._h, -1 if enable is None else int(enable), C.byref(st)))
+        return bool(st.value)
 
     def solve(self, rhs: ScalarFunction, x: ScalarFunction, level: int, tol: float, max_cycles: int,
               nu_pre: int = 2, nu_post: int = 2) -> SolveReport:

@@ -27,8 +27,22 @@ pytestmark = pytest.mark.gpu
 
 
 def torch_sm_count():
-    import torch
-    return torch.cuda.get_device_properties(0).multi_processor_count
+    # from the CUDA runtime directly, not torch: once the library has loaded the system
+    # libnccl.so.2, torch's CUDA library cannot bind its newer NCCL symbols
+    import ctypes
+    rt = ctypes.CDLL("libcudart.so.12") if _has("libcudart.so.12") else ctypes.CDLL("libcudart.so")
+    v = ctypes.c_int()
+    assert rt.cudaDeviceGetAttribute(ctypes.byref(v), 16, 0) == 0  # cudaDevAttrMultiProcessorCount
+    return v.value
+
+
+def _has(name):
+    import ctypes
+    try:
+        ctypes.CDLL(name)
+        return True
+    except OSError:
+        return False
 
 
 def cfg3_mesh(segments=128, layers=32):
