@@ -106,6 +106,10 @@ int hyb_coarse_matrix_host(const char* mesh_text, int form, int level, const int
 typedef struct hyb_plan hyb_plan;
 int hyb_plan_create(const char* mesh_text, int world_ranks, const int32_t* assignment, const int32_t* local_ranks,
                     int n_local, int level, hyb_plan** out);
+/* the same for a function kind (HYB_P2: the P2 layout and exchange; owned_global / owner
+ * global indices in the level-(L+1) P1 numbering, the P2 owned set) */
+int hyb_plan_create_kind(const char* mesh_text, int world_ranks, const int32_t* assignment, const int32_t* local_ranks,
+                         int n_local, int level, int kind, hyb_plan** out);
 int hyb_plan_destroy(hyb_plan* p);
 int hyb_plan_sizes(hyb_plan* p, int64_t sizes[8]);
 int hyb_plan_array(hyb_plan* p, int which, int64_t* out, int64_t cap, int64_t* len);

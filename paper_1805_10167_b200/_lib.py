@@ -140,6 +140,7 @@ _SIGS = {
     "hyb_domain_overlap": (_i, [_p, _i, _pi64]),
     "hyb_smooth_jacobi2": (_i, [_p, _p, _p, _d, _i]),
     "hyb_tuning": (_i, [_cs, _i64, _pi64]),
+    "hyb_plan_create_kind": (_i, [_cs, _i, _pi32, _pi32, _i, _i, _i, C.POINTER(_p)]),
     "hyb_hierarchy_temporal": (_i, [_p, _i, C.POINTER(_i)]),
     "hyb_register_pack_info": (_i, [_p, C.c_uint32, _p, _p, _p]),
     "hyb_controller_sync": (_i, [_p, C.c_uint32, _i, C.POINTER(_i), _i]),

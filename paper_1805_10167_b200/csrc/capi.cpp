@@ -225,7 +225,13 @@ int hyb_coarse_matrix_host(const char* mesh_text, int form, int level, const int
 
 int hyb_plan_create(const char* mesh_text, int world_ranks, const int32_t* assignment, const int32_t* local_ranks,
                     int n_local, int level, hyb_plan** out) {
+    return hyb_plan_create_kind(mesh_text, world_ranks, assignment, local_ranks, n_local, level, HYB_P1, out);
+}
+
+int hyb_plan_create_kind(const char* mesh_text, int world_ranks, const int32_t* assignment, const int32_t* local_ranks,
+                         int n_local, int level, int kind, hyb_plan** out) {
     return guarded([&] {
+        if (kind != HYB_P1 && kind != HYB_P2) throw hyb::InvalidArgument("hyb_plan_create: unsupported kind");
         need(mesh_text, "hyb_plan_create");
         auto h = std::make_unique<hyb_plan>();
         h->g = hyb::build_macro_graph(hyb::parse_mesh_text(mesh_text));
@@ -239,8 +245,9 @@ int hyb_plan_create(const char* mesh_text, int world_ranks, const int32_t* assig
         if (level < 0 || level > 20) throw hyb::OutOfRange("hyb_plan_create: level");
         h->level = level;
         h->p = hyb::place(h->g, a, lr);
-        h->lay = hyb::plan_layout(h->g, h->p, level);
-        h->x = hyb::plan_exchange(h->g, a, lr, h->p, h->lay);
+        h->lay = kind == HYB_P2 ? hyb::plan_layout_p2(h->g, h->p, level) : hyb::plan_layout(h->g, h->p, level);
+        h->x = kind == HYB_P2 ? hyb::plan_exchange_p2(h->g, a, lr, h->p, h->lay)
+                              : hyb::plan_exchange(h->g, a, lr, h->p, h->lay);
         *out = h.release();
     });
 }
@@ -267,8 +274,11 @@ int hyb_plan_array(hyb_plan* p, int which, int64_t* out, int64_t cap, int64_t* l
             for (const auto& b : bs) v.insert(v.end(), {b.src_rank, b.dst_rank, b.send_off, b.recv_off, b.count});
         };
         switch (which) {
-        case 0: v = hyb::owned_positions(p->g, p->p, p->lay); break;
-        case 1: v = hyb::owned_global_index(p->g, p->p, p->level); break;
+        case 0: v = p->lay.p2 ? hyb::owned_global_p2(p->g, p->p, p->lay, true) : hyb::owned_positions(p->g, p->p, p->lay); break;
+        case 1:
+            v = p->lay.p2 ? hyb::owned_global_p2(p->g, p->p, p->lay, false)
+                          : hyb::owned_global_index(p->g, p->p, p->level);
+            break;
         case 2: v = p->x.dst; break;
         case 3: v = p->x.src; break;
         case 4: v = p->x.pack; break;

@@ -249,11 +249,6 @@ double to_host(Domain& d, const double* dev) {
     HYB_CUDA(cudaStreamSynchronize(d.stream()));
     return out;
 }
-double finish_dot(Domain& d, const LevelTables& t, const double* u, const double* v, const double* scratch, int slots,
-                  double* part) {
-    finish_dot_dev(d, t, u, v, scratch, slots, part, d.scalar_out());
-    return to_host(d, d.scalar_out());
-}
 } // namespace
 
 // dst = A src and src.dst in one pass over the faces (PCG's p.Ap): the face

@@ -384,10 +384,13 @@ HostExchange plan_exchange_p2(const MacroGraph& g, const std::vector<int>& rank_
     };
     HostExchange X;
     struct Lists {
-        std::vector<int64_t> send_src, recv_dst;
+        std::vector<int64_t> send_src, recv_dst, recv_gidx;
         int64_t count = 0;
     };
     std::map<std::pair<int, int>, Lists> blocks;
+    std::vector<int64_t> lgid;
+    // owners' global index in the level-(L+1) P1 numbering (the P2 owned set), for the tests
+    auto gidx_of = [&](const OwnerSlot& o) { return global_owned_index(g, o, n2); };
     auto emit = [&](uint64_t rcv, int64_t dst, const OwnerSlot& o) {
         const int rq = rank_of[size_t(rcv)], rs = rank_of[size_t(o.prim)];
         const bool rl = is_local(rq), sl = is_local(rs);
@@ -395,6 +398,7 @@ HostExchange plan_exchange_p2(const MacroGraph& g, const std::vector<int>& rank_
             if (rl) {
                 X.dst.push_back(dst);
                 X.src.push_back(pos_of(o));
+                lgid.push_back(gidx_of(o));
             }
             return;
         }
@@ -402,7 +406,10 @@ HostExchange plan_exchange_p2(const MacroGraph& g, const std::vector<int>& rank_
         Lists& b = blocks[{rs, rq}];
         ++b.count;
         if (sl) b.send_src.push_back(pos_of(o));
-        if (rl) b.recv_dst.push_back(dst);
+        if (rl) {
+            b.recv_dst.push_back(dst);
+            b.recv_gidx.push_back(gidx_of(o));
+        }
     };
     for (uint64_t id = 0; id < g.size(); ++id) {
         const int li = p.lidx[size_t(id)];
@@ -459,6 +466,7 @@ HostExchange plan_exchange_p2(const MacroGraph& g, const std::vector<int>& rank_
         }
     }
     X.nlocal = int64_t(X.dst.size());
+    X.owner_gidx = lgid;
     int64_t so = 0, ro = 0;
     for (auto& [key, b] : blocks) {
         const bool sl = is_local(key.first), rl = is_local(key.second);
@@ -469,6 +477,7 @@ HostExchange plan_exchange_p2(const MacroGraph& g, const std::vector<int>& rank_
         }
         if (rl) {
             X.dst.insert(X.dst.end(), b.recv_dst.begin(), b.recv_dst.end());
+            X.owner_gidx.insert(X.owner_gidx.end(), b.recv_gidx.begin(), b.recv_gidx.end());
             ro += b.count;
         }
         if (sl && rl) X.inproc.push_back(blk);
@@ -501,6 +510,23 @@ std::vector<int64_t> owned_positions_p2(const Placement& p, const HostLayout& la
         for (int r = 1; r <= n - 2; ++r) // interior vertices
             for (int c = 1; c + r <= n - 1; ++c) at(2 * c, 2 * r);
     }
+    return out;
+}
+
+// (slot, level-(L+1) P1 global index) of every local owned P2 DoF (tests)
+std::vector<int64_t> owned_global_p2(const MacroGraph& g, const Placement& p, const HostLayout& lay, bool slots) {
+    const int n2 = lay.n;
+    std::vector<int64_t> out;
+    for (size_t i = 0; i < p.verts.size(); ++i)
+        out.push_back(slots ? lay.vtx_off[i] : global_owned_index(g, {p.verts[i], 0, 0}, n2));
+    for (size_t i = 0; i < p.edges.size(); ++i)
+        for (int k = 1; k <= n2 - 1; ++k)
+            out.push_back(slots ? lay.edge_off[i] + k : global_owned_index(g, {p.edges[i], k, 0}, n2));
+    for (size_t i = 0; i < p.faces.size(); ++i)
+        for (int r = 1; r <= n2 - 2; ++r)
+            for (int c = 1; c + r <= n2 - 1; ++c)
+                out.push_back(slots ? int64_t(i) * lay.face_stride + lay.rowoff[size_t(r)] + c
+                                    : global_owned_index(g, {p.faces[i], c, r}, n2));
     return out;
 }
 

@@ -75,6 +75,9 @@ HostExchange plan_exchange_p2(const MacroGraph& g, const std::vector<int>& rank_
 /// order per primitive (vertex; edge line k = 1..n-1 then midline; face
 /// groups EH, ED, EV, V: for_each_owned, src/layout.cpp:176-237)
 std::vector<int64_t> owned_positions_p2(const Placement& p, const HostLayout& lay);
+/// every local owned P2 DoF as its arena slot (slots) or its global index in the
+/// level-(L+1) P1 numbering (the P2 owned set; the exchange's owner_gidx uses it)
+std::vector<int64_t> owned_global_p2(const MacroGraph& g, const Placement& p, const HostLayout& lay, bool slots);
 
 /// Arena slot / global index of each local owned DoF, in local packed order.
 std::vector<int64_t> owned_positions(const MacroGraph& g, const Placement& p, const HostLayout& lay);

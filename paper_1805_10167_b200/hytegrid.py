@@ -149,12 +149,12 @@ class ExchangePlan:
     ARRAYS = {"owned_slots": 0, "owned_global": 1, "gather_dst": 2, "gather_src": 3, "pack_src": 4,
               "owner_global": 5, "inproc": 6, "sends": 7, "recvs": 8}
 
-    def __init__(self, mesh_text: str, ranks: int, assignment, local_ranks, level: int):
+    def __init__(self, mesh_text: str, ranks: int, assignment, local_ranks, level: int, kind: int = 0):
         a = np.ascontiguousarray(assignment, dtype=np.int32)
         lr = (C.c_int32 * len(local_ranks))(*local_ranks)
         h = C.c_void_p()
-        check(lib.hyb_plan_create(mesh_text.encode(), ranks, a.ctypes.data_as(C.POINTER(C.c_int32)), lr,
-                                  len(local_ranks), level, C.byref(h)))
+        check(lib.hyb_plan_create_kind(mesh_text.encode(), ranks, a.ctypes.data_as(C.POINTER(C.c_int32)), lr,
+                                       len(local_ranks), level, kind, C.byref(h)))
         self._h = h
         s = (C.c_int64 * 8)()
         check(lib.hyb_plan_sizes(h, s))

@@ -48,7 +48,7 @@ def emulate_sync(plan, arena, rank):
     arena[dst[plan.nlocal:]] = recv
 
 
-def _worker(rank, world, port, mesh, level, partitioner, out):
+def _worker(rank, world, port, mesh, level, partitioner, out, kind=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -56,8 +56,9 @@ def _worker(rank, world, port, mesh, level, partitioner, out):
             assignment = H.partition_greedy_edgecut(mesh, world, max(level, 1))
         else:
             assignment = H.partition_round_robin(mesh, world)
-        plan = H.ExchangePlan(mesh, world, assignment, [rank], level)
-        glob = keyed_uniform(mesh, level, seed=17)
+        plan = H.ExchangePlan(mesh, world, assignment, [rank], level, kind)
+        # a P2 level's owned set is P1's at level + 1 (plan indices use that numbering)
+        glob = keyed_uniform(mesh, level + kind, seed=17)
         arena = np.full(plan.arena_size, np.nan)
         arena[plan.array("owned_slots")] = glob[plan.array("owned_global")]
         emulate_sync(plan, arena, rank)
@@ -90,6 +91,20 @@ def test_multiprocess_exchange_plan(world, partitioner, mesh_name, level):
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
     mp.start_processes(_worker, args=(world, _free_port(), mesh, level, partitioner, out), nprocs=world,
+                       join=True, start_method="spawn")
+    assert all(out[r] for r in range(world)), dict(out)
+
+
+@pytest.mark.parametrize("world,mesh_name,level", [(2, "ring8", 2), (3, "annulus", 1), (2, "square_rev", 0),
+                                                  (4, "channel44", 2)])
+def test_multiprocess_exchange_plan_p2(world, mesh_name, level):
+    """P2 plans (fine halo rows 1-2 per edge face, vertex ghosts per edge and face)
+    over gloo: every ghost holds its owner's value afterwards, blocks symmetric"""
+    mesh = {"ring8": H.meshgen.square_ring8(), "channel44": H.meshgen.channel(4, 4),
+            "annulus": H.meshgen.annulus(8, 2, 1.0, 2.0), "square_rev": H.meshgen.unit_square_reversed()}[mesh_name]
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker, args=(world, _free_port(), mesh, level, "rr", out, 1), nprocs=world,
                        join=True, start_method="spawn")
     assert all(out[r] for r in range(world)), dict(out)
 
