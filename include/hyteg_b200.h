@@ -339,6 +339,16 @@ int hyb_hierarchy_vcycle(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, i
  * enable < 0 leaves the setting unchanged; *replays = graph launches so far */
 int hyb_hierarchy_graphs(hyb_hierarchy* h, int enable, int64_t* replays);
 int hyb_hierarchy_residual_norm(hyb_hierarchy* h, hyb_function* rhs, hyb_function* x, int level, double* out);
+/* Weighted-Jacobi cycles run their coarse end -- every level with face size
+ * n = 2^level <= max_n, down to the min-level CG -- as ONE cooperative kernel
+ * (grid barriers between dependent steps; bitwise the launched cycle) when the
+ * domain is one process with one rank, the min-level system fits the one-CTA
+ * CG and each level sees an even number of sweeps. enable: 1 always, 0 never,
+ * 2 automatic (the default: domains of at most 16 faces, where it wins; with
+ * hundreds of faces the coarse rows are a few points long and the launched
+ * kernels are as fast); max_n default 64. enable < 0 / max_n <= 0 leave the
+ * settings; *launches counts such kernels. */
+int hyb_hierarchy_mega(hyb_hierarchy* h, int enable, int max_n, int64_t* launches);
 /* Jacobi V(2, nu2 >= 2) cycles smooth the finest pre-smoothing pair with one
  * two-sweep pass (hyb_smooth_jacobi2; bitwise the two sweeps); default on,
  * enable < 0 leaves the setting; *state = current setting */

@@ -142,6 +142,7 @@ _SIGS = {
     "hyb_tuning": (_i, [_cs, _i64, _pi64]),
     "hyb_plan_create_kind": (_i, [_cs, _i, _pi32, _pi32, _i, _i, _i, C.POINTER(_p)]),
     "hyb_hierarchy_temporal": (_i, [_p, _i, C.POINTER(_i)]),
+    "hyb_hierarchy_mega": (_i, [_p, _i, _i, _pi64]),
     "hyb_register_pack_info": (_i, [_p, C.c_uint32, _p, _p, _p]),
     "hyb_controller_sync": (_i, [_p, C.c_uint32, _i, C.POINTER(_i), _i]),
     "hyb_owned_coords_kind": (_i, [_p, _i, _i, _i, _pd, _i64]),

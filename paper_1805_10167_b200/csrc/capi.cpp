@@ -886,12 +886,24 @@ int hyb_tuning(const char* name, int64_t value, int64_t* previous) {
     return guarded([&] {
         need(name, "hyb_tuning");
         const std::string k(name);
-        if (k == "jacobi2_min_n") {
+        if (k == "mega_dofs_per_cta") { // applies to hierarchies created afterwards
+            if (previous) *previous = hyb::mega_dofs_per_cta_default();
+            if (value > 0) hyb::set_mega_dofs_per_cta_default(value);
+        } else if (k == "jacobi2_min_n") {
             if (previous) *previous = hyb::jacobi2_min_n();
             if (value >= 0) hyb::set_jacobi2_min_n(int(std::min<int64_t>(value, int64_t(1) << 30)));
         } else {
             throw hyb::InvalidArgument("hyb_tuning: unknown knob '" + k + "'");
         }
+    });
+}
+
+int hyb_hierarchy_mega(hyb_hierarchy* h, int enable, int max_n, int64_t* launches) {
+    return guarded([&] {
+        need(h, "hyb_hierarchy_mega");
+        if (enable >= 0) h->h->mega_ = enable > 1 ? -1 : enable; // 2: automatic
+        if (max_n > 0) h->h->mega_max_n = max_n;
+        if (launches) *launches = h->h->mega_launches;
     });
 }
 

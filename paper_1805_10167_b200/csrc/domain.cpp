@@ -47,6 +47,7 @@ template DevMem upload_vec(const std::vector<uint64_t>&, cudaStream_t);
 template DevMem upload_vec(const std::vector<int32_t>&, cudaStream_t);
 template DevMem upload_vec(const std::vector<int8_t>&, cudaStream_t);
 template DevMem upload_vec(const std::vector<uint8_t>&, cudaStream_t);
+template DevMem upload_vec(const std::vector<McLevel>&, cudaStream_t);
 
 // ---------------------------------------------------------------- NCCL (dlopen)
 namespace {

@@ -336,6 +336,8 @@ void smooth_jacobi2(const Operator& A, Function& rhs, Function& x, double omega,
 /// the smallest face size (n = 2^L) the two-sweep pass is used for (default: never)
 int jacobi2_min_n();
 void set_jacobi2_min_n(int n);
+int64_t mega_dofs_per_cta_default();
+void set_mega_dofs_per_cta_default(int64_t v);
 /// dst = A src (all flags) and returns src.dst, one pass over the faces
 double apply_dot(const Operator& A, Function& src, Function& dst, int level);
 /// the same with src.dst left on the device at *out (no host round trip)
@@ -411,6 +413,10 @@ class Hierarchy {
     void smooth(Function& rhs, Function& x, int level, double* dotp = nullptr);
     void check_coarse(); // throws if the last coarse solve did not converge
     void run_cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero = false);
+    bool mega_usable(int level, int nu_pre, int nu_post);
+    void run_mega(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero);
+    std::map<std::vector<const void*>, DevMem> mega_tables_;
+    DevMem mega_bar_;
     std::vector<const void*> graph_key(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero);
 
     // CUDA-graph replay of whole V-cycles: a cycle with an even number of
@@ -420,6 +426,15 @@ class Hierarchy {
     bool use_graphs = true;
     bool fuse_post_ = true; // prolongate_add fused with the first Jacobi post-sweep
     bool temporal_ = true;  // V(2, nu2 >= 2) Jacobi: the finest pre-smoothing pair as one two-sweep pass
+    // Jacobi cycles from levels with n <= mega_max_n down as one cooperative kernel: 1 always,
+    // 0 never, -1 (default) when the domain has at most mega_auto_faces faces (below that it
+    // wins: config 1 0.24 -> 0.14 ms per cycle; with hundreds of faces the coarse rows are a
+    // few points long and the launched kernels are as fast)
+    int mega_ = -1;
+    int mega_auto_faces = 16;
+    int mega_max_n = 64;
+    int64_t mega_dofs_per_cta = 16384; // CTAs of the coarse kernel: top-level DoFs / this
+    int64_t mega_launches = 0;
     int64_t graph_replays = 0;
 
   private:

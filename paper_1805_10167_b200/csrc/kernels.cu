@@ -94,12 +94,12 @@ template <int MODE>
 __device__ __forceinline__ void ev_stencil_block(const LevelTables& t, const FlagTables& fl,
                                                  const double* __restrict__ x, const double* __restrict__ b,
                                                  double* __restrict__ y, double omega, uint8_t mask, int kblocks,
-                                                 int ev_block) {
+                                                 int ev_block, int tid = int(threadIdx.x)) {
     const int n = t.n;
     const int eblocks = t.nedges * kblocks;
     if (ev_block < eblocks) {
         const int e = t.edge_list ? t.edge_list[ev_block / kblocks] : ev_block / kblocks;
-        const int k = 1 + (ev_block % kblocks) * 128 + int(threadIdx.x);
+        const int k = 1 + (ev_block % kblocks) * 128 + tid;
         if (k > n - 1) return;
         const uint8_t f = fl.edge_flag[e];
         if (!(f & mask)) return;
@@ -132,7 +132,7 @@ __device__ __forceinline__ void ev_stencil_block(const LevelTables& t, const Fla
         y[off + k] = o;
         return;
     }
-    const int vi = (ev_block - eblocks) * 128 + int(threadIdx.x);
+    const int vi = (ev_block - eblocks) * 128 + tid;
     if (vi >= t.nverts) return;
     const int v = t.vtx_list ? t.vtx_list[vi] : vi;
     const uint8_t f = fl.vtx_flag[v];
@@ -244,15 +244,15 @@ inline dim3 face_row_grid(int n_cols, int n_rows, int nfaces) {
 #include "transfer.cuh"
 #include "gauss_seidel.cuh"
 
-__global__ void __launch_bounds__(128) k_prolongate_ev(LevelTables tc, LevelTables tf, FlagTables ff,
-                                                       const double* __restrict__ xc, double* __restrict__ xf,
-                                                       uint8_t mask, int add, int kblocks) {
-    pdl_prologue();
+// one 128-thread logical block of the edge/vertex prolongation (blk: logical block, tid: 0..127)
+__device__ __forceinline__ void prolongate_ev_block(const LevelTables& tc, const LevelTables& tf, const FlagTables& ff,
+                                                    const double* __restrict__ xc, double* __restrict__ xf,
+                                                    uint8_t mask, int add, int kblocks, int blk, int tid) {
     const int nf = tf.n;
     const int eblocks = tf.nedges * kblocks;
-    if (int(blockIdx.x) < eblocks) {
-        const int e = blockIdx.x / kblocks;
-        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+    if (blk < eblocks) {
+        const int e = blk / kblocks;
+        const int k = 1 + (blk % kblocks) * 128 + tid;
         if (k > nf - 1 || !(ff.edge_flag[e] & mask)) return;
         const double* cl = xc + tc.edge_off[e];
         const double v = (k % 2 == 0) ? cl[k / 2] : 0.5 * (cl[(k - 1) / 2] + cl[(k + 1) / 2]);
@@ -260,26 +260,39 @@ __global__ void __launch_bounds__(128) k_prolongate_ev(LevelTables tc, LevelTabl
         *p = add ? *p + v : v;
         return;
     }
-    const int vtx = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+    const int vtx = (blk - eblocks) * 128 + tid;
     if (vtx >= tf.nverts || !(ff.vtx_flag[vtx] & mask)) return;
     const double v = xc[tc.vtx_off[vtx]];
     double* p = xf + tf.vtx_off[vtx];
     *p = add ? *p + v : v;
 }
 
+__global__ void __launch_bounds__(128) k_prolongate_ev(LevelTables tc, LevelTables tf, FlagTables ff,
+                                                       const double* __restrict__ xc, double* __restrict__ xf,
+                                                       uint8_t mask, int add, int kblocks) {
+    pdl_prologue();
+    prolongate_ev_block(tc, tf, ff, xc, xf, mask, add, kblocks, int(blockIdx.x), int(threadIdx.x));
+}
+
 // ---------------------------------------------------------------------------
 // K7: restriction (exact transpose of the prolongation).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_restrict_ev(LevelTables tc, LevelTables tf, FlagTables cf,
-                                                     const double* __restrict__ xf, double* __restrict__ xc,
-                                                     uint8_t mask, int kblocks) {
-    pdl_prologue();
+// one 128-thread logical block of the edge/vertex restriction; zero_dirichlet: coarse
+// DIRICHLET rows get 0.0 instead (the cycle's fill_const(b, 0, DIRICHLET) after it)
+__device__ __forceinline__ void restrict_ev_block(const LevelTables& tc, const LevelTables& tf, const FlagTables& cf,
+                                                  const double* __restrict__ xf, double* __restrict__ xc,
+                                                  uint8_t mask, int kblocks, int blk, int tid,
+                                                  bool zero_dirichlet = false) {
     const int nc = tc.n, nfn = tf.n;
     const int eblocks = tc.nedges * kblocks;
-    if (int(blockIdx.x) < eblocks) {
-        const int e = blockIdx.x / kblocks;
-        const int k = 1 + (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+    if (blk < eblocks) {
+        const int e = blk / kblocks;
+        const int k = 1 + (blk % kblocks) * 128 + tid;
         if (k > nc - 1 || !(cf.edge_flag[e] & mask)) return;
+        if (zero_dirichlet && (cf.edge_flag[e] & F_DIRICHLET)) {
+            xc[tc.edge_off[e] + k] = 0.0;
+            return;
+        }
         const double* fl = xf + tf.edge_off[e];
         double acc = fl[2 * k] + 0.5 * (fl[2 * k - 1] + fl[2 * k + 1]);
         const int nfc = tf.edge_nf[e];
@@ -290,13 +303,24 @@ __global__ void __launch_bounds__(128) k_restrict_ev(LevelTables tc, LevelTables
         xc[tc.edge_off[e] + k] = acc;
         return;
     }
-    const int v = (blockIdx.x - eblocks) * blockDim.x + threadIdx.x;
+    const int v = (blk - eblocks) * 128 + tid;
     if (v >= tc.nverts || !(cf.vtx_flag[v] & mask)) return;
+    if (zero_dirichlet && (cf.vtx_flag[v] & F_DIRICHLET)) {
+        xc[tc.vtx_off[v]] = 0.0;
+        return;
+    }
     const double* fv = xf + tf.vtx_off[v];
     double acc = fv[0];
     const int ne = tf.vtx_ne[v];
     for (int j = 1; j <= ne; ++j) acc += 0.5 * fv[j];
     xc[tc.vtx_off[v]] = acc;
+}
+
+__global__ void __launch_bounds__(128) k_restrict_ev(LevelTables tc, LevelTables tf, FlagTables cf,
+                                                     const double* __restrict__ xf, double* __restrict__ xc,
+                                                     uint8_t mask, int kblocks) {
+    pdl_prologue();
+    restrict_ev_block(tc, tf, cf, xf, xc, mask, kblocks, int(blockIdx.x), int(threadIdx.x));
 }
 
 // ---------------------------------------------------------------------------
@@ -626,6 +650,7 @@ __global__ void __launch_bounds__(1024) k_combine_tree(double* v, int64_t len, d
 }
 
 inline int kblocks_for(int n) { return n - 1 > 0 ? (n - 1 + 127) / 128 : 0; }
+__device__ __forceinline__ int kblocks_for_dev(int n) { return n - 1 > 0 ? (n - 1 + 127) / 128 : 0; }
 
 } // namespace
 
@@ -1372,15 +1397,12 @@ __device__ void cg_spmv(const int32_t* __restrict__ rowptr, const int32_t* __res
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(CG_THREADS) k_coarse_cg(int64_t n, const int32_t* __restrict__ rowptr,
-                                                          const int32_t* __restrict__ col,
-                                                          const double* __restrict__ val,
-                                                          const double* __restrict__ bg, double* xg, double* r,
-                                                          double* p, double* ap, double tol, int max_iter,
-                                                          CoarseStatus* st, int in_smem) {
-    pdl_prologue();
+// the single-CTA CG body (CG_THREADS threads): dsm holds the five vectors when in_smem
+__device__ void coarse_cg_body(int64_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                               const double* __restrict__ val, const double* __restrict__ bg, double* xg, double* r,
+                               double* p, double* ap, double tol, int max_iter, CoarseStatus* st, int in_smem,
+                               double* dsm) {
     __shared__ double red[33];
-    extern __shared__ double dsm[]; // small systems: all five vectors on chip
     const double* b = bg;
     double* x = xg;
     if (in_smem) {
@@ -1435,6 +1457,17 @@ __global__ void __launch_bounds__(CG_THREADS) k_coarse_cg(int64_t n, const int32
         st->target = target;
         st->residual = res;
     }
+}
+
+__global__ void __launch_bounds__(CG_THREADS) k_coarse_cg(int64_t n, const int32_t* __restrict__ rowptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ bg, double* xg, double* r,
+                                                          double* p, double* ap, double tol, int max_iter,
+                                                          CoarseStatus* st, int in_smem) {
+    pdl_prologue();
+    extern __shared__ double dsm[]; // small systems: all five vectors on chip
+    coarse_cg_body(n, rowptr, col, val, bg, xg, r, p, ap, tol, max_iter, st, in_smem, dsm);
 }
 
 // Large min-level systems (e.g. configuration 4: 66k DoFs at level 2 of a
@@ -1990,6 +2023,7 @@ void launch_coarse_minres(int64_t n, const int32_t* rowptr, const int32_t* col, 
     check_launch("coarse minres");
 }
 
+#include "mega.cuh"
 #include "p2_kernels.cuh"
 
 } // namespace hyb

@@ -281,6 +281,42 @@ void launch_jacobi2(const LevelTables& t, const FlagTables& fl, const double* x,
 /// away from a border (from y1 with refreshed ghosts) and edges/vertices
 void launch_jacobi2_finish(const LevelTables& t, const FlagTables& fl, const double* y1, const double* b, double* y2,
                            double omega, cudaStream_t st);
+// ---- the coarse end of a V-cycle as one cooperative kernel (mega.cuh) ----
+constexpr int MC_MAX_LEVELS = 16;
+struct McLevel { // one level of the sub-cycle (single process, one rank: all ghosts same-rank)
+    LevelTables t;         // geometry + the operator's coefficients
+    FlagTables fl;         // the cycle functions' flags (one set of BCs)
+    double* x;             // the iterate's arena (e below the top, the caller's x at the top)
+    double* s;             // Jacobi scratch arena
+    const double* rhs;     // b below the top, the caller's rhs at the top
+    double* r;             // residual arena
+    const void* gdst;      // ghost refresh lists (int32 when idx32)
+    const void* gsrc;
+    int64_t ng;
+    int idx32;
+};
+struct McCoarse { // the min-level CG (one CTA, coarse_cg_body)
+    int64_t n = 0, nloc = 0;
+    const int32_t *rowptr = nullptr, *col = nullptr;
+    const double* val = nullptr;
+    const int64_t *gidx = nullptr, *pos = nullptr;
+    const uint8_t* flag = nullptr;
+    double* vec = nullptr; // b, x, r, p, ap (n each)
+    CoarseStatus* st = nullptr;
+    double tol = 0;
+    int max_iter = 0;
+};
+struct McRun {
+    int top = 0, lmin = 0, nu_pre = 0, nu_post = 0, x_zero = 0;
+    int cg_smem = 0; // the CG's five vectors in dynamic shared memory (5 n doubles <= 200 KB)
+    double omega = 0;
+    McCoarse cg;
+    unsigned* bar = nullptr; // grid barrier words (2, zero-initialised once)
+};
+/// cycle(rhs, x, top, nu_pre, nu_post, x_zero) over levels top..lmin, weighted
+/// Jacobi, in one launch (lv: device array of top - lmin + 1 levels, lmin first)
+/// ctas: CTAs of the persistent grid (clamped to 1 .. #SMs; one CTA needs no grid barrier)
+void launch_vcycle_coarse(const McLevel* lv_dev, const McRun& run, int ctas, cudaStream_t st);
 /// host copy of the device hypot (glibc's), for the CPU pin
 double glibc_hypot_host(double x, double y);
 void launch_coarse_scatter_add(int64_t nloc, const int64_t* gidx, const int64_t* pos, const uint8_t* flag,

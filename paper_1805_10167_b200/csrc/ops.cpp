@@ -201,6 +201,11 @@ int g_jacobi2_min_n = 1 << 30;
 } // namespace
 
 int jacobi2_min_n() { return g_jacobi2_min_n; }
+namespace {
+int64_t g_mega_dofs_per_cta = 16384;
+}
+int64_t mega_dofs_per_cta_default() { return g_mega_dofs_per_cta; }
+void set_mega_dofs_per_cta_default(int64_t v) { g_mega_dofs_per_cta = v; }
 void set_jacobi2_min_n(int n) { g_jacobi2_min_n = n; }
 
 // Two sweeps, x0 -> x1 -> x2: the face pass forms x1 in registers and writes x2
@@ -718,6 +723,7 @@ Hierarchy::Hierarchy(Domain& d, Form form, int min_level, int max_level, Boundar
       omega_(omega), coarse_tol_(coarse_tol), coarse_max_iter_(coarse_max_iter) {
     if (min_level < 0 || min_level > max_level)
         throw InvalidArgument("GridHierarchy: need 0 <= min_level <= max_level");
+    mega_dofs_per_cta = mega_dofs_per_cta_default();
     if (smoother != SMOOTH_JACOBI && smoother != SMOOTH_GS && smoother != SMOOTH_CGS)
         throw InvalidArgument("GridHierarchy: unknown smoother");
     // min-level system: every rank holds the whole (small) constrained matrix
@@ -840,7 +846,92 @@ void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int
 // x_zero: x is known to be zero (a coarse correction, PCG's z); with Jacobi
 // pre-smoothing the zero-fill, the Dirichlet assign and the first sweep's read
 // of x are replaced by one zero-guess sweep (bitwise the same values).
+// The coarse end of the cycle in one cooperative kernel (mega.cuh): weighted
+// Jacobi, one process with one rank (every ghost same-rank), a one-CTA coarse
+// CG, an even number of sweeps per level (the iterate ends in its own arena),
+// no fused dot at these levels; bitwise the launched cycle.
+bool Hierarchy::mega_usable(int level, int nu_pre, int nu_post) {
+    Domain& d = *dom_;
+    const int lmin = a_.min_level();
+    if (mega_ == 0 || smoother_ != SMOOTH_JACOBI || d.profiling || (1 << level) > mega_max_n || level <= lmin)
+        return false;
+    if (mega_ < 0 && d.local_faces().size() > size_t(mega_auto_faces)) return false;
+    if (nu_pre < 1 || (nu_pre + nu_post) % 2 != 0 || level - lmin + 1 > MC_MAX_LEVELS) return false;
+    if (d.multi_process() || d.local_ranks().size() != 1 || coarse_.n >= coarse_grid_min_rows()) return false;
+    if (cycle_dot_ && cycle_dot_level_ >= lmin && cycle_dot_level_ <= level) return false;
+    for (int l = lmin; l <= level; ++l) {
+        const Exchange& X = d.level(l).xch;
+        if (X.ntotal != X.nlocal || X.npack) return false;
+    }
+    return true;
+}
+
+void Hierarchy::run_mega(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero) {
+    Domain& d = *dom_;
+    const int lmin = a_.min_level();
+    std::vector<McLevel> lv;
+    std::vector<const void*> key;
+    for (int l = lmin; l <= level; ++l) {
+        McLevel m{};
+        m.t = a_.tables(l);
+        Function& xf = l == level ? x : e_;
+        Function& bf = l == level ? rhs : b_;
+        m.fl = xf.flags();
+        m.x = xf.data(l);
+        m.s = d.jacobi_scratch(l).as<double>();
+        m.rhs = bf.data(l);
+        m.r = r_.data(l);
+        const Exchange& X = d.level(l).xch;
+        m.gdst = X.dst.as<void>();
+        m.gsrc = X.src.as<void>();
+        m.ng = X.nlocal;
+        m.idx32 = X.idx32 ? 1 : 0;
+        lv.push_back(m);
+        key.insert(key.end(), {m.x, m.s, m.rhs, m.r, m.fl.edge_flag, m.fl.vtx_flag});
+    }
+    auto it = mega_tables_.find(key);
+    if (it == mega_tables_.end()) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        HYB_CUDA(cudaStreamIsCapturing(d.stream(), &cs));
+        if (cs != cudaStreamCaptureStatusNone) throw LogicError("vcycle: coarse-cycle tables missing during capture");
+        it = mega_tables_.emplace(key, upload_vec(lv, d.stream())).first;
+    }
+    if (!mega_bar_.bytes()) {
+        mega_bar_ = DevMem(64);
+        HYB_CUDA(cudaMemsetAsync(mega_bar_.as<void>(), 0, 64, d.stream()));
+    }
+    McRun run;
+    run.top = level;
+    run.lmin = lmin;
+    run.nu_pre = nu_pre;
+    run.nu_post = nu_post;
+    run.x_zero = x_zero ? 1 : 0;
+    run.omega = omega_;
+    run.cg.n = coarse_.n;
+    run.cg.nloc = coarse_.nloc;
+    run.cg.rowptr = coarse_.rowptr.as<int32_t>();
+    run.cg.col = coarse_.col.as<int32_t>();
+    run.cg.val = coarse_.val.as<double>();
+    run.cg.gidx = coarse_.gidx.as<int64_t>();
+    run.cg.pos = coarse_.pos.as<int64_t>();
+    run.cg.flag = coarse_.flag.as<uint8_t>();
+    run.cg.vec = coarse_.vec.as<double>();
+    run.cg.st = coarse_.status.as<CoarseStatus>();
+    run.cg.tol = coarse_tol_;
+    run.cg.max_iter = coarse_max_iter_;
+    run.bar = mega_bar_.as<unsigned>();
+    run.cg_smem = size_t(5 * coarse_.n) * sizeof(double) <= 200 * 1024 ? 1 : 0;
+    const int64_t dofs = d.owned_local(level);
+    launch_vcycle_coarse(it->second.as<McLevel>(), run, int((dofs + mega_dofs_per_cta - 1) / mega_dofs_per_cta),
+                         d.stream());
+    ++mega_launches;
+}
+
 void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_post, bool x_zero) {
+    if (mega_usable(level, nu_pre, nu_post)) {
+        run_mega(rhs, x, level, nu_pre, nu_post, x_zero);
+        return;
+    }
     const bool zero_sweep = x_zero && level > a_.min_level() && nu_pre > 0 && smoother_ == SMOOTH_JACOBI;
     if (x_zero && !zero_sweep) fill_const(x, 0.0, level, ALL_FLAGS);
     if (!zero_sweep) assign(1.0, rhs, 0.0, rhs, x, level, kDirichletMask);

@@ -654,6 +654,14 @@ class GridHierarchy:
         check(lib.hyb_hierarchy_residual_norm(self._h, rhs._h, x._h, level, C.byref(out)))
         return out.value
 
+    def use_mega(self, enable: bool | str | None = None, max_n: int = 0) -> int:
+        """The one-kernel coarse end of Jacobi cycles (levels with 2^level <= max_n): True
+        always, False never, "auto" (default) on small domains; returns such launches so far."""
+        n = C.c_int64()
+        mode = -1 if enable is None else (2 if enable == "auto" else int(bool(enable)))
+        check(lib.hyb_hierarchy_mega(self._h, mode, max_n, C.byref(n)))
+        return n.value
+
     def use_temporal(self, enable: bool | None = None) -> bool:
         """Toggle the two-sweep pre-smoothing pass of Jacobi V(2, >=2) cycles (default on)."""
         st = C.c_int()
