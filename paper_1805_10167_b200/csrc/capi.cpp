@@ -734,6 +734,15 @@ int hyb_smooth_cgs(hyb_operator* A, hyb_function* rhs, hyb_function* x, int leve
     });
 }
 
+int hyb_smooth_cgs_n(hyb_operator* A, hyb_function* rhs, hyb_function* x, int level, int count) {
+    return guarded([&] {
+        need(A, "hyb_smooth_cgs_n");
+        need(rhs, "hyb_smooth_cgs_n");
+        need(x, "hyb_smooth_cgs_n");
+        hyb::smooth_cgs_n(*A->a, *rhs->f, *x->f, level, count);
+    });
+}
+
 int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level) {
     return guarded([&] {
         need(A, "hyb_smooth_jacobi");
@@ -889,6 +898,9 @@ int hyb_tuning(const char* name, int64_t value, int64_t* previous) {
         if (k == "mega_dofs_per_cta") { // applies to hierarchies created afterwards
             if (previous) *previous = hyb::mega_dofs_per_cta_default();
             if (value > 0) hyb::set_mega_dofs_per_cta_default(value);
+        } else if (k == "cgs_pair_min_n") {
+            if (previous) *previous = hyb::cgs_pair_min_n();
+            if (value >= 0) hyb::set_cgs_pair_min_n(int(std::min<int64_t>(value, int64_t(1) << 30)));
         } else if (k == "jacobi2_min_n") {
             if (previous) *previous = hyb::jacobi2_min_n();
             if (value >= 0) hyb::set_jacobi2_min_n(int(std::min<int64_t>(value, int64_t(1) << 30)));

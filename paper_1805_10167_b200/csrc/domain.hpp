@@ -349,6 +349,9 @@ void prolongate_add_jacobi(const Operator& A, Function& e, Function& rhs, Functi
 void smooth_jacobi_zero(const Operator& A, Function& rhs, Function& x, double omega, int level);
 void smooth_gs(const Operator& A, Function& rhs, Function& x, int level);
 void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level);
+void smooth_cgs_n(const Operator& A, Function& rhs, Function& x, int level, int count);
+int cgs_pair_min_n();
+void set_cgs_pair_min_n(int n);
 void diagonal(const Operator& A, Function& d, int level);
 /// some row x's flags leave to a smoother has a zero diagonal in A
 bool zero_diagonal_row(const Operator& A, const Function& x, int level);
@@ -444,6 +447,7 @@ class Hierarchy {
     };
     std::vector<CycleGraph> graphs_;
     std::vector<std::vector<const void*>> warm_;
+    std::vector<std::vector<const void*>> no_graph_; // cycles that leave an arena swapped: eager
 
   public:
     ~Hierarchy();

@@ -40,6 +40,13 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __global__ void __launch_bounds__(GS_WARPS * 32) k_gs_faces(LevelTables t, const double* __restrict__ b, double* x,
@@ -811,4 +818,222 @@ __global__ void __launch_bounds__(128) k_cgs_verts_oop(LevelTables t, FlagTables
     double acc = 0.0;
     for (int j = 0; j <= ne; ++j) acc += co[j] * x[off + j];
     y[off] = x[off] + 1.0 * (b[off] - acc) / co[ne + 1];
+}
+
+// ---------------------------------------------------------------------------
+// Two coloured sweeps in one pass (temporal blocking). The k_cgs_cols step
+// schedule with six consumer blocks instead of three: sweep 1's C0, C1, C2 on
+// rows [j, j+K), [j-S, ..), [j-2S, ..) and sweep 2's on [j-3S, ..), [j-4S, ..),
+// [j-5S, ..) (S = K+1). Sweep 2's C0 on row r reads rows r-1..r+1 only after
+// sweep 1's C2 finished them (a step earlier), and no block reads a row another
+// writes in the same step, so one consumer barrier per step still orders
+// everything. Each block computes one column fewer on each side than the one
+// before it: sweep 1's C0 on [c0-5, c1+5) ... sweep 2's C2 on [c0, c1), the kept
+// columns (recomputed halo values are bitwise the owner CTA's).
+// Between the sweeps the reference-order smoother syncs ghosts; here:
+//   * the face's boundary ghosts for sweep 2 (edge / vertex values after their
+//     sweep 1) come from `g` (a second arena whose face-boundary slots the caller
+//     filled); sweep-2 lanes patch them over the ring's stale copies;
+//   * every sweep-1 value of the layer next to the borders (row 1, column 1, the
+//     diagonal c + r = n-1) is stored into `g` at its own slot, so the caller can
+//     refresh the edges' halo rows with sweep-1 values before their sweep 2.
+// Bitwise two k_cgs_cols sweeps with the ghost refresh in between (og_cgs twice).
+constexpr int CGP_PF = 6; // steps of look-ahead for sweep 2's boundary ghosts
+template <int K, int D, int CB> struct CgpCfg {
+    static constexpr int S = K + 1;
+    static constexpr int RX = D * K + 6 * K + 6; // x ring rows: j-5S (pending write-back) .. j+(D+1)K
+    static constexpr int RB = D * K + 5 * K + 5; // b ring rows
+    static constexpr int NB = D + 1;
+    static constexpr int CW = 6 * K;
+    static constexpr int THREADS = (CW + 2) * 32;
+    static constexpr int H = 6;       // staged halo columns on each side
+    static constexpr int RS = CB + 2 * H;
+    static constexpr size_t SMEM = size_t(RX + RB) * RS * 8 + 16 * NB + 32 * CGP_PF * K; // + sweep-2 C0 slots
+};
+
+template <int K, int D, int CB, int MINB>
+__global__ void __launch_bounds__(CgpCfg<K, D, CB>::THREADS, MINB)
+    k_cgs_pair(LevelTables t, const double* __restrict__ b, const double* x, double* y, double* g) {
+    pdl_prologue();
+    using C = CgpCfg<K, D, CB>;
+    extern __shared__ __align__(16) double cp_ring[];
+    constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = C::S, RS = C::RS, H = C::H;
+    const int n = t.n, W = t.W;
+    const int c0 = int(blockIdx.x) * CB, c1 = c0 + CB;
+    const int last = min(n - 2, n - 1 - max(1, c0 - (H - 1))); // last row with a computed interior point
+    if (last < 1) return;                                         // CTA-uniform
+    double* xring = cp_ring;
+    double* bring = cp_ring + size_t(RX) * RS;
+    uint64_t* full = reinterpret_cast<uint64_t*>(cp_ring + size_t(RX + RB) * RS);
+    uint64_t* done = full + NB;
+    const int64_t base = int64_t(blockIdx.y) * t.face_stride;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nsteps = (last + 5 * S - 1) / K + 1;
+    const int a0 = max(0, c0 - H); // first staged column
+    const int so = a0 - (c0 - H);  // its ring index
+    const int64_t* __restrict__ ro = t.rowoff;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NB; ++i) {
+            mbar_init(&full[i], 2);
+            mbar_init(&done[i], C::CW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp >= C::CW) { // producers (k_cgs_cols' two warps)
+        if (lane != 0) return;
+        auto seg = [&](int q, int lo, int hi) {
+            const int e = min(hi, (W - q + 1) & ~1);
+            return e > lo ? uint32_t(e - lo) * 8u : 0u;
+        };
+        if (warp == C::CW) { // A: write-back of final rows, x rows
+            const double* xf = x + base;
+            double* yf = y + base;
+            const int xmax = last + 1;
+            int q_next = 0, slot_next = 0;
+            auto load_x = [&](int s_) {
+                const int qhi = min(xmax, 1 + (s_ + 1) * K);
+                uint32_t bytes = 0;
+                for (int q = q_next; q <= qhi; ++q) bytes += seg(q, a0, c1 + H);
+                mbar_arrive_expect_tx(&full[s_ % NB], bytes);
+                for (; q_next <= qhi; ++q_next) {
+                    const uint32_t nb_ = seg(q_next, a0, c1 + H);
+                    if (nb_) bulk_g2s(xring + size_t(slot_next) * RS + so, xf + ro[q_next] + a0, nb_, &full[s_ % NB]);
+                    slot_next = slot_next + 1 == RX ? 0 : slot_next + 1;
+                }
+            };
+            for (int s_ = 0; s_ < D && s_ < nsteps; ++s_) load_x(s_);
+            int q_st = 1 - 5 * S, slot_st = ((q_st % RX) + RX) % RX; // first row of step 0's sweep-2 C2 block
+            for (int i = 0; i < nsteps; ++i) {
+                mbar_wait(&done[i % NB], uint32_t((i / NB) & 1));
+                for (int k = 0; k < K; ++k) {
+                    const int q = q_st + k;
+                    const int sl = slot_st + k >= RX ? slot_st + k - RX : slot_st + k;
+                    if (q >= 1 && q <= last) {
+                        const uint32_t nb_ = seg(q, c0, c1);
+                        if (nb_) bulk_s2g(yf + ro[q] + c0, xring + size_t(sl) * RS + H, nb_);
+                    }
+                }
+                bulk_commit();
+                bulk_wait_read1();
+                q_st += K;
+                slot_st = slot_st + K >= RX ? slot_st + K - RX : slot_st + K;
+                if (i + D < nsteps) load_x(i + D);
+            }
+            bulk_wait_all();
+        } else { // B: b rows [1 + sK, (s+1)K]
+            const double* bf = b + base;
+            int q_next = 1, slot_next = 1 % RB;
+            auto load_b = [&](int s_) {
+                const int qhi = min(last, (s_ + 1) * K);
+                uint32_t bytes = 0;
+                for (int q = q_next; q <= qhi; ++q) bytes += seg(q, a0, c1 + H);
+                mbar_arrive_expect_tx(&full[s_ % NB], bytes);
+                for (; q_next <= qhi; ++q_next) {
+                    const uint32_t nb_ = seg(q_next, a0, c1 + H);
+                    if (nb_) bulk_g2s(bring + size_t(slot_next) * RS + so, bf + ro[q_next] + a0, nb_, &full[s_ % NB]);
+                    slot_next = slot_next + 1 == RB ? 0 : slot_next + 1;
+                }
+            };
+            for (int s_ = 0; s_ < D && s_ < nsteps; ++s_) load_b(s_);
+            for (int i = 0; i < nsteps; ++i) {
+                if (i + D >= nsteps) break;
+                mbar_wait(&done[i % NB], uint32_t((i / NB) & 1));
+                load_b(i + D);
+            }
+        }
+        return;
+    }
+    double co[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) co[i] = __ldg(t.face_coef + size_t(blockIdx.y) * 8 + i);
+    const double rd = 1.0 / co[7];
+    const int blk = warp / K; // 0..5: sweep 1 C0 C1 C2, sweep 2 C0 C1 C2
+    const int colour = blk % 3, roff = warp % K;
+    const bool second = blk >= 3;
+    const int clo = max(1, c0 - (H - 1) + blk), chi = c1 + (H - 2) - blk; // computed columns (inclusive)
+    int r = 1 - S * blk + roff;
+    auto wrap = [](int v, int m) { return ((v % m) + m) % m; };
+    int sxm = wrap(r - 1, RX), sx0 = wrap(r, RX), sxp = wrap(r + 1, RX), sb = wrap(r, RB);
+    int t3 = wrap(colour - 2 * r, 3);
+    constexpr int DT3 = (3 - (2 * K) % 3) % 3;
+    const int sh = H - c0; // ring index of column c
+    const double* gf = g + base;
+    double* gw = g + base;
+    // sweep 2's C0 block replaces the stale boundary ghosts of rows r and r+1 in the ring
+    // (column 0 and the diagonal) before it reads them; C1 and C2 read them after it. The
+    // four values are fetched CGP_PF steps ahead into per-warp shared slots (cp.async
+    // groups), so the global reads stay off the step chain. Both C0 warps touching a row
+    // write the same values.
+    double* bdv = reinterpret_cast<double*>(done + NB) + 4 * CGP_PF * (warp - 3 * K);
+    const bool patcher = blk == 3;
+    auto fetch_bd = [&](int rr, int buf) {
+        if (lane < 4 && rr >= 1 && rr <= last) {
+            const int q = rr + (lane & 1);
+            const int col = lane < 2 ? 0 : n - q; // lanes 0, 1: column 0 of rr, rr+1; 2, 3: their diagonals
+            cp_async8(bdv + 4 * buf + lane, gf + ro[q] + col);
+        }
+        cp_async_commit();
+    };
+    if (patcher)
+        for (int p = 0; p < CGP_PF; ++p) fetch_bd(r + p * K, p);
+#pragma unroll 1
+    for (int i = 0; i < nsteps; ++i) {
+        mbar_wait(&full[i % NB], uint32_t((i / NB) & 1));
+        if (patcher) {
+            cp_async_wait_group<CGP_PF - 1>(); // this step's group
+            __syncwarp();
+            if (lane < 4 && r >= 1 && r <= last) {
+                const int q = r + (lane & 1);
+                const int col = lane < 2 ? 0 : n - q;
+                const int ri = col - c0 + H; // ring index
+                if (ri >= 0 && ri < RS) xring[(lane & 1 ? sxp : sx0) * RS + ri] = bdv[4 * (i % CGP_PF) + lane];
+            }
+            if (r == 1) { // row 0, every staged column
+                const int s0 = wrap(0, RX), e0 = min(c1 + H, n + 1);
+                for (int col = a0 + lane; col < e0; col += 32) xring[s0 * RS + col - c0 + H] = gf[ro[0] + col];
+            }
+            __syncwarp();
+            fetch_bd(r + CGP_PF * K, i % CGP_PF); // the slot just consumed
+            __syncwarp();
+        }
+        if (r >= 1 && r <= last) {
+            const double* rm = xring + sxm * RS + sh;
+            double* r0 = xring + sx0 * RS + sh;
+            const double* rp = xring + sxp * RS + sh;
+            const double* br = bring + sb * RS + sh;
+            const int cmax = min(n - 1 - r, chi);
+            const int cs = clo + wrap(t3 - clo, 3);
+            const int cdiag = n - 1 - r;
+#pragma unroll 1
+            for (int c = cs + 3 * lane; c <= cmax; c += 192) {
+                const int c2 = c + 96;
+                double v[8], w[8];
+                v[0] = r0[c - 1], v[1] = rp[c - 1], v[2] = rm[c], v[3] = r0[c];
+                v[4] = rp[c], v[5] = rm[c + 1], v[6] = r0[c + 1], v[7] = br[c];
+                const bool two = c2 <= cmax;
+                if (two) {
+                    w[0] = r0[c2 - 1], w[1] = rp[c2 - 1], w[2] = rm[c2], w[3] = r0[c2];
+                    w[4] = rp[c2], w[5] = rm[c2 + 1], w[6] = r0[c2 + 1], w[7] = br[c2];
+                }
+                const double nv = cgs_point_update(v, co, rd);
+                r0[c] = nv;
+                double nw = 0.0;
+                if (two) r0[c2] = nw = cgs_point_update(w, co, rd);
+                if (!second) { // sweep-1 values of the border layer, for the edges' halo rows
+                    if ((r == 1 || c == 1 || c == cdiag) && c >= c0 && c < c1) gw[ro[r] + c] = nv;
+                    if (two && (r == 1 || c2 == cdiag) && c2 >= c0 && c2 < c1) gw[ro[r] + c2] = nw;
+                }
+            }
+        }
+        fence_proxy_async_smem();
+        consumer_sync<C::CW * 32>();
+        if (lane == 0) mbar_arrive(&done[i % NB]);
+        r += K;
+        sxm = sxm + K >= RX ? sxm + K - RX : sxm + K;
+        sx0 = sx0 + K >= RX ? sx0 + K - RX : sx0 + K;
+        sxp = sxp + K >= RX ? sxp + K - RX : sxp + K;
+        sb = sb + K >= RB ? sb + K - RB : sb + K;
+        t3 = t3 + DT3 >= 3 ? t3 + DT3 - 3 : t3 + DT3;
+    }
 }

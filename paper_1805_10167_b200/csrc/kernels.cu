@@ -997,6 +997,68 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
     return oop;
 }
 
+// two coloured sweeps per face pass (k_cgs_pair); returns false where no pair variant is tuned
+template <int K, int D, int CB, int MINB>
+void launch_cgs_pair_t(const LevelTables& t, const double* b, double* x, double* y, double* g, cudaStream_t st) {
+    using C = CgpCfg<K, D, CB>;
+    static const bool attr = cudaFuncSetAttribute(k_cgs_pair<K, D, CB, MINB>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)) ==
+                             cudaSuccess;
+    if (!attr) throw CudaError("coloured gauss-seidel pair: cannot reserve shared memory");
+    const int nb = (t.n - 1 + CB - 1) / CB;
+    pdl_launch(k_cgs_pair<K, D, CB, MINB>, dim3(unsigned(nb), unsigned(t.nfaces)), C::THREADS, C::SMEM, st, t, b, x,
+               nb == 1 ? x : y, g);
+}
+
+int cgs_pair_blocks(int n) {
+    if (n == 512) return 2; // 256-column blocks (the 512-column ring would leave one CTA per SM)
+    if (n == 256) return 1;
+    return 0;
+}
+
+bool launch_cgs_pair(const LevelTables& t, const double* b, double* x, double* y, double* g, cudaStream_t st) {
+    if (t.nfaces <= 0) return false;
+    // config 3 (8192 faces), per pair against two single sweeps: L9 12.81 ms vs 11.14 (K = 1,
+    // 3 CTAs per SM: 12.31), L8 3.76 vs 3.42 -- the sweep is issue- and step-chain-bound, not
+    // DRAM-bound, so halving the bytes does not pay
+    if (t.n == 512) launch_cgs_pair_t<2, 3, 256, 2>(t, b, x, y, g, st);
+    else if (t.n == 256) launch_cgs_pair_t<2, 3, 256, 2>(t, b, x, y, g, st);
+    else return false;
+    check_launch("coloured gauss-seidel pair");
+    return true;
+}
+
+// the ghost refreshes around a sweep pair (one arena per side of the faces' region [0, fend)):
+//   post = 0: face ghosts g[d] := y[s] (the face-boundary copies sweep 2 reads);
+//   post = 1: other ghosts y[d] := (s a face slot ? g : y)[s] (the edges' halo rows from the
+//             faces' sweep-1 layer in g, vertex/edge cross copies from y)
+template <class I>
+__global__ void __launch_bounds__(256) k_gather_split(const I* __restrict__ dst, const I* __restrict__ src, int64_t n,
+                                                      int64_t fend, int post, double* y, double* g) {
+    pdl_prologue();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t d = dst[i], s = src[i];
+        if (!post) {
+            if (d < fend) g[d] = y[s];
+        } else if (d >= fend) {
+            y[d] = s < fend ? g[s] : y[s];
+        }
+    }
+}
+
+void launch_gather_split(const void* dst, const void* src, bool idx32, int64_t n, int64_t fend, int post, double* y,
+                         double* g, cudaStream_t st) {
+    if (n <= 0) return;
+    const int blocks = grid_for(n, 256, 1 << 30);
+    if (idx32)
+        pdl_launch(k_gather_split<int32_t>, blocks, 256, 0, st, static_cast<const int32_t*>(dst),
+                   static_cast<const int32_t*>(src), n, fend, post, y, g);
+    else
+        pdl_launch(k_gather_split<int64_t>, blocks, 256, 0, st, static_cast<const int64_t*>(dst),
+                   static_cast<const int64_t*>(src), n, fend, post, y, g);
+    check_launch("ghost gather (sweep pair)");
+}
+
 void launch_cgs_ev_oop(const LevelTables& t, const FlagTables& fl, const double* b, const double* x, double* y,
                        cudaStream_t st) {
     if (t.nverts > 0) {

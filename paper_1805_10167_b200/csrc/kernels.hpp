@@ -149,6 +149,12 @@ void launch_gs_ev(const LevelTables& t, const FlagTables& fl, const double* b, d
 // odd/even k, vertices as in launch_gs_ev
 void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st);
 void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st);
+// two coloured face sweeps in one pass (see k_cgs_pair); cgs_pair_blocks: column blocks per face
+// of the tuned variant for face size n (0: none, 1: in place)
+int cgs_pair_blocks(int n);
+bool launch_cgs_pair(const LevelTables& t, const double* b, double* x, double* y, double* g, cudaStream_t st);
+void launch_gather_split(const void* dst, const void* src, bool idx32, int64_t n, int64_t fend, int post, double* y,
+                         double* g, cudaStream_t st);
 // column-blocked faces (k_cgs_cols): in place when a face is one block, else
 // out of place into y (returns true); bitwise the in-place sweep either way
 bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, double* y, cudaStream_t st);

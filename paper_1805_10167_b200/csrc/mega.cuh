@@ -27,6 +27,38 @@ __device__ __forceinline__ void mc_sync(const McCtx& c) {
     else grid_barrier(c.bar);
 }
 
+// interior point j (0 .. (n-1)(n-2)/2 - 1) of a face -> (c, r), counting from the apex row
+// (rows of 1, 2, ... points): thread per point, so short coarse rows keep every lane busy
+__device__ __forceinline__ void mc_point(int n, int64_t j, int& c, int& r) {
+    const int64_t P = int64_t(n - 1) * (n - 2) / 2;
+    const int64_t jr = P - 1 - j;
+    int t = int((sqrt(8.0 * double(jr) + 1.0) - 1.0) * 0.5);
+    while (int64_t(t) * (t + 1) / 2 > jr) --t;
+    while (int64_t(t + 1) * (t + 2) / 2 <= jr) ++t;
+    r = n - 2 - t;
+    c = t + 1 - int(jr - int64_t(t) * (t + 1) / 2);
+}
+
+// edge/vertex point u of a level -> the (logical block, thread) the 128-thread bodies take
+__device__ __forceinline__ bool mc_ev_point(const LevelTables& t, int64_t u, int& blk, int& tid) {
+    const int kb = kblocks_for_dev(t.n);
+    const int64_t ne = t.n > 1 ? int64_t(t.nedges) * (t.n - 1) : 0;
+    if (u < ne) {
+        const int e = int(u / (t.n - 1)), k1 = int(u % (t.n - 1));
+        blk = e * kb + k1 / 128;
+        tid = k1 % 128;
+        return true;
+    }
+    const int64_t v = u - ne;
+    if (v >= t.nverts) return false;
+    blk = t.nedges * kb + int(v / 128);
+    tid = int(v % 128);
+    return true;
+}
+__device__ __forceinline__ int64_t mc_ev_count(const LevelTables& t) {
+    return (t.n > 1 ? int64_t(t.nedges) * (t.n - 1) : 0) + t.nverts;
+}
+
 // every ghost slot of the arena from its same-rank owner (k_ghost_gather's local part)
 __device__ void mc_gather(const McLevel& L, double* arena, const McCtx& c) {
     for (int64_t i = c.gthread; i < L.ng; i += c.nthreads) {
@@ -43,33 +75,32 @@ __device__ void mc_face_rows(const LevelTables& t, const double* __restrict__ x,
                              double* __restrict__ y, double omega, const McCtx& c) {
     const int n = t.n;
     if (n < 3) return;
-    const int rows = n - 2;
-    const int64_t units = int64_t(t.nfaces) * rows;
-    for (int64_t u = c.gwarp; u < units; u += c.nwarps) {
-        const int face = int(u / rows), r = 1 + int(u % rows);
+    const int64_t P = int64_t(n - 1) * (n - 2) / 2;
+    const int64_t units = int64_t(t.nfaces) * P;
+    for (int64_t u = c.gthread; u < units; u += c.nthreads) {
+        const int face = int(u / P);
+        int col, r;
+        mc_point(n, u % P, col, r);
         const double* co = t.face_coef + size_t(face) * 8;
         const double dg = co[7], rdg = 1.0 / dg;
         const int64_t base = int64_t(face) * t.face_stride;
+        const int64_t i = base + t.rowoff[r] + col;
+        if (MODE == ST_JACOBI_ZERO) {
+            y[i] = 0.0 + div_by(omega * (b[i] - 0.0), dg, rdg);
+            continue;
+        }
         const double* xm = x + base + t.rowoff[r - 1];
         const double* x0 = x + base + t.rowoff[r];
         const double* xp = x + base + t.rowoff[r + 1];
-        const double* br = b + base + t.rowoff[r];
-        double* yr = y + base + t.rowoff[r];
-        for (int col = 1 + c.lane; col <= n - 1 - r; col += 32) {
-            if (MODE == ST_JACOBI_ZERO) {
-                yr[col] = 0.0 + div_by(omega * (br[col] - 0.0), dg, rdg);
-                continue;
-            }
-            double a = 0.0;
-            a += co[0] * x0[col - 1];
-            a += co[1] * xp[col - 1];
-            a += co[2] * xm[col];
-            a += co[3] * x0[col];
-            a += co[4] * xp[col];
-            a += co[5] * xm[col + 1];
-            a += co[6] * x0[col + 1];
-            yr[col] = MODE == ST_RESIDUAL ? br[col] - a : x0[col] + div_by(omega * (br[col] - a), dg, rdg);
-        }
+        double a = 0.0;
+        a += co[0] * x0[col - 1];
+        a += co[1] * xp[col - 1];
+        a += co[2] * xm[col];
+        a += co[3] * x0[col];
+        a += co[4] * xp[col];
+        a += co[5] * xm[col + 1];
+        a += co[6] * x0[col + 1];
+        y[i] = MODE == ST_RESIDUAL ? b[i] - a : x0[col] + div_by(omega * (b[i] - a), dg, rdg);
     }
 }
 
@@ -77,9 +108,11 @@ template <int MODE>
 __device__ void mc_ev_rows(const McLevel& L, const double* x, const double* b, double* y, double omega,
                            const McCtx& c) {
     const int kb = kblocks_for_dev(L.t.n);
-    const int blocks = L.t.nedges * kb + (L.t.nverts + 127) / 128;
-    for (int blk = c.ggroup; blk < blocks; blk += c.ngroups)
-        ev_stencil_block<MODE>(L.t, L.fl, x, b, y, omega, uint8_t(F_ALL), kb, blk, c.gtid);
+    const int64_t units = mc_ev_count(L.t);
+    for (int64_t u = c.gthread; u < units; u += c.nthreads) {
+        int blk, tid;
+        if (mc_ev_point(L.t, u, blk, tid)) ev_stencil_block<MODE>(L.t, L.fl, x, b, y, omega, uint8_t(F_ALL), kb, blk, tid);
+    }
 }
 
 // one smoothing step on faces + edges + vertices
@@ -97,26 +130,27 @@ __device__ void mc_restrict(const McLevel& C, const McLevel& F, const double* xf
     const LevelTables& tf = F.t;
     const int nc = tc.n;
     if (nc >= 3) {
-        const int rows = nc - 2;
-        const int64_t units = int64_t(tc.nfaces) * rows;
-        for (int64_t u = c.gwarp; u < units; u += c.nwarps) {
-            const int face = int(u / rows), r = 1 + int(u % rows);
+        const int64_t P = int64_t(nc - 1) * (nc - 2) / 2;
+        const int64_t units = int64_t(tc.nfaces) * P;
+        for (int64_t u = c.gthread; u < units; u += c.nthreads) {
+            const int face = int(u / P);
+            int col, r;
+            mc_point(nc, u % P, col, r);
             const double* fv = xf + int64_t(face) * tf.face_stride;
-            double* cv = xc + int64_t(face) * tc.face_stride;
             const int64_t* fro = tf.rowoff;
-            for (int col = 1 + c.lane; col <= nc - 1 - r; col += 32) {
-                const int fc = 2 * col, fr = 2 * r;
-                const double W = fv[fro[fr] + fc - 1], Cc = fv[fro[fr] + fc], E = fv[fro[fr] + fc + 1];
-                const double S = fv[fro[fr - 1] + fc], SE = fv[fro[fr - 1] + fc + 1];
-                const double N = fv[fro[fr + 1] + fc], NW = fv[fro[fr + 1] + fc - 1];
-                cv[tc.rowoff[r] + col] = Cc + 0.5 * (W + E + S + N + SE + NW);
-            }
+            const int fc = 2 * col, fr = 2 * r;
+            const double W = fv[fro[fr] + fc - 1], Cc = fv[fro[fr] + fc], E = fv[fro[fr] + fc + 1];
+            const double S = fv[fro[fr - 1] + fc], SE = fv[fro[fr - 1] + fc + 1];
+            const double N = fv[fro[fr + 1] + fc], NW = fv[fro[fr + 1] + fc - 1];
+            xc[int64_t(face) * tc.face_stride + tc.rowoff[r] + col] = Cc + 0.5 * (W + E + S + N + SE + NW);
         }
     }
     const int kb = kblocks_for_dev(nc);
-    const int blocks = tc.nedges * kb + (tc.nverts + 127) / 128;
-    for (int blk = c.ggroup; blk < blocks; blk += c.ngroups)
-        restrict_ev_block(tc, tf, C.fl, xf, xc, uint8_t(F_ALL), kb, blk, c.gtid, true);
+    const int64_t units = mc_ev_count(tc);
+    for (int64_t u = c.gthread; u < units; u += c.nthreads) {
+        int blk, tid;
+        if (mc_ev_point(tc, u, blk, tid)) restrict_ev_block(tc, tf, C.fl, xf, xc, uint8_t(F_ALL), kb, blk, tid, true);
+    }
 }
 
 // fine += P coarse on the smooth mask (k_prolongate_faces add mode, prolongate_ev_block)
@@ -125,49 +159,48 @@ __device__ void mc_prolongate_add(const McLevel& C, const McLevel& F, const doub
     const LevelTables& tf = F.t;
     const int nf = tf.n;
     if (nf >= 3) {
-        const int rows = nf - 2;
-        const int64_t units = int64_t(tf.nfaces) * rows;
-        for (int64_t u = c.gwarp; u < units; u += c.nwarps) {
-            const int face = int(u / rows), fr = 1 + int(u % rows);
+        const int64_t P = int64_t(nf - 1) * (nf - 2) / 2;
+        const int64_t units = int64_t(tf.nfaces) * P;
+        for (int64_t u = c.gthread; u < units; u += c.nthreads) {
+            const int face = int(u / P);
+            int fc, fr;
+            mc_point(nf, u % P, fc, fr);
             const double* cv = xc + int64_t(face) * tc.face_stride;
             double* fv = xf + int64_t(face) * tf.face_stride + tf.rowoff[fr];
             const int64_t* cro = tc.rowoff;
-            const int r = fr >> 1;
-            for (int fc = 1 + c.lane; fc <= nf - 1 - fr; fc += 32) {
-                const int col = fc >> 1;
-                double v;
-                if ((fr & 1) == 0) v = (fc & 1) == 0 ? cv[cro[r] + col] : 0.5 * (cv[cro[r] + col] + cv[cro[r] + col + 1]);
-                else if ((fc & 1) == 0) v = 0.5 * (cv[cro[r] + col] + cv[cro[r + 1] + col]);
-                else v = 0.5 * (cv[cro[r] + col + 1] + cv[cro[r + 1] + col]);
-                fv[fc] = fv[fc] + v;
-            }
+            const int r = fr >> 1, col = fc >> 1;
+            double v;
+            if ((fr & 1) == 0) v = (fc & 1) == 0 ? cv[cro[r] + col] : 0.5 * (cv[cro[r] + col] + cv[cro[r] + col + 1]);
+            else if ((fc & 1) == 0) v = 0.5 * (cv[cro[r] + col] + cv[cro[r + 1] + col]);
+            else v = 0.5 * (cv[cro[r] + col + 1] + cv[cro[r + 1] + col]);
+            fv[fc] = fv[fc] + v;
         }
     }
     const int kb = kblocks_for_dev(nf);
-    const int blocks = tf.nedges * kb + (tf.nverts + 127) / 128;
-    for (int blk = c.ggroup; blk < blocks; blk += c.ngroups)
-        prolongate_ev_block(tc, tf, F.fl, xc, xf, uint8_t(F_INNER | 4), 1, kb, blk, c.gtid);
+    const int64_t units = mc_ev_count(tf);
+    for (int64_t u = c.gthread; u < units; u += c.nthreads) {
+        int blk, tid;
+        if (mc_ev_point(tf, u, blk, tid)) prolongate_ev_block(tc, tf, F.fl, xc, xf, uint8_t(F_INNER | 4), 1, kb, blk, tid);
+    }
 }
 
 // x's DIRICHLET rows := 1 rhs + 0 rhs (the cycle's assign), edges and vertices
 __device__ void mc_dirichlet_from_rhs(const McLevel& L, double* x, const double* rhs, const McCtx& c) {
     const LevelTables& t = L.t;
-    const int kb = kblocks_for_dev(t.n);
-    const int eblocks = t.nedges * kb;
-    const int blocks = eblocks + (t.nverts + 127) / 128;
-    for (int blk = c.ggroup; blk < blocks; blk += c.ngroups) {
-        if (blk < eblocks) {
-            const int e = blk / kb;
-            const int k = 1 + (blk % kb) * 128 + c.gtid;
-            if (k > t.n - 1 || !(L.fl.edge_flag[e] & F_DIRICHLET)) continue;
-            const int64_t i = t.edge_off[e] + k;
-            x[i] = 1.0 * rhs[i] + 0.0 * rhs[i];
+    const int64_t ne = t.n > 1 ? int64_t(t.nedges) * (t.n - 1) : 0;
+    const int64_t units = mc_ev_count(t);
+    for (int64_t u = c.gthread; u < units; u += c.nthreads) {
+        int64_t i;
+        if (u < ne) {
+            const int e = int(u / (t.n - 1));
+            if (!(L.fl.edge_flag[e] & F_DIRICHLET)) continue;
+            i = t.edge_off[e] + 1 + u % (t.n - 1);
         } else {
-            const int v = (blk - eblocks) * 128 + c.gtid;
-            if (v >= t.nverts || !(L.fl.vtx_flag[v] & F_DIRICHLET)) continue;
-            const int64_t i = t.vtx_off[v];
-            x[i] = 1.0 * rhs[i] + 0.0 * rhs[i];
+            const int v = int(u - ne);
+            if (!(L.fl.vtx_flag[v] & F_DIRICHLET)) continue;
+            i = t.vtx_off[v];
         }
+        x[i] = 1.0 * rhs[i] + 0.0 * rhs[i];
     }
 }
 
@@ -175,19 +208,10 @@ __device__ void mc_dirichlet_from_rhs(const McLevel& L, double* x, const double*
 __device__ void mc_zero(const McLevel& L, double* x, const McCtx& c) {
     const LevelTables& t = L.t;
     for (int64_t i = c.gthread; i < t.faces_size; i += c.nthreads) x[i] = 0.0;
-    const int kb = kblocks_for_dev(t.n);
-    const int eblocks = t.nedges * kb;
-    const int blocks = eblocks + (t.nverts + 127) / 128;
-    for (int blk = c.ggroup; blk < blocks; blk += c.ngroups) {
-        if (blk < eblocks) {
-            const int e = blk / kb;
-            const int k = 1 + (blk % kb) * 128 + c.gtid;
-            if (k <= t.n - 1) x[t.edge_off[e] + k] = 0.0;
-        } else {
-            const int v = (blk - eblocks) * 128 + c.gtid;
-            if (v < t.nverts) x[t.vtx_off[v]] = 0.0;
-        }
-    }
+    const int64_t ne = t.n > 1 ? int64_t(t.nedges) * (t.n - 1) : 0;
+    const int64_t units = mc_ev_count(t);
+    for (int64_t u = c.gthread; u < units; u += c.nthreads)
+        x[u < ne ? t.edge_off[u / (t.n - 1)] + 1 + u % (t.n - 1) : t.vtx_off[u - ne]] = 0.0;
 }
 
 __global__ void __launch_bounds__(MC_THREADS, 1) k_vcycle_coarse(const McLevel* __restrict__ lv, McRun run) {

@@ -360,6 +360,61 @@ void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level) {
     if (oop) x.arena(level).swap(next);
 }
 
+// `count` coloured sweeps; consecutive pairs run the faces' two sweeps in one pass
+// (k_cgs_pair) where a tuned variant exists for the face size, every ghost is
+// same-process and same-rank, and n >= cgs_pair_min_n(). The pass reproduces the
+// ghost refresh between the two sweeps with two split gathers (face-boundary copies
+// into the second scratch arena before, the edges' halo rows from the faces' sweep-1
+// layer after), so the result is bitwise `count` smooth_cgs calls. Measured slower
+// than single sweeps (k_cgs_pair), so off unless asked for (hyb_tuning("cgs_pair_min_n")).
+int g_cgs_pair_min_n = 1 << 30;
+int cgs_pair_min_n() { return g_cgs_pair_min_n; }
+void set_cgs_pair_min_n(int n) { g_cgs_pair_min_n = n; }
+
+static bool cgs_pair_usable(const Operator& A, Function& x, int level) {
+    Domain& d = A.domain();
+    if (A.kind() != KIND_P1 || x.kind() != KIND_P1 || (1 << level) < cgs_pair_min_n()) return false;
+    if (cgs_pair_blocks(1 << level) == 0 || d.multi_process() || d.local_ranks().size() != 1) return false;
+    const Exchange& X = d.level(level).xch;
+    return X.ntotal == X.nlocal;
+}
+
+void smooth_cgs_n(const Operator& A, Function& rhs, Function& x, int level, int count) {
+    if (count < 0) throw InvalidArgument("smooth_cgs: negative sweep count");
+    check_op_function(A, rhs, level, "smooth_cgs", true);
+    check_op_function(A, x, level, "smooth_cgs", true);
+    if (&rhs == &x) throw InvalidArgument("smooth_cgs: rhs and x must be distinct functions");
+    require_p1(x, "smooth_cgs");
+    const bool pairs = count >= 2 && cgs_pair_usable(A, x, level);
+    for (; pairs && count >= 2; count -= 2) {
+        check_diagonals(A, x, level, "smooth_cgs");
+        Domain& d = A.domain();
+        d.sync(x, level);
+        const LevelTables t = A.tables(level);
+        const FlagTables fl = x.flags();
+        const Exchange& X = d.level(level).xch;
+        const bool oop = cgs_pair_blocks(t.n) > 1;
+        DevMem& next = d.jacobi_scratch(level);
+        double* xa = x.data(level);
+        double* y = oop ? next.as<double>() : xa;
+        double* g = d.jacobi_scratch2(level).as<double>();
+        const double* b = rhs.data(level);
+        // sweep 1 of the edges and vertices (their ghosts are the synced copies)
+        if (oop) launch_cgs_ev_oop(t, fl, b, xa, y, d.stream());
+        else launch_cgs_ev(t, fl, b, xa, d.stream());
+        // the faces' boundary ghosts as sweep 2 sees them
+        launch_gather_split(X.dst.as<void>(), X.src.as<void>(), X.idx32, X.nlocal, t.faces_size, 0, y, g, d.stream());
+        d.timer_begin("coloured_gs_pair");
+        launch_cgs_pair(t, b, xa, y, g, d.stream());
+        d.timer_end();
+        // the edges' halo rows (faces after sweep 1) and the vertex/edge cross copies
+        launch_gather_split(X.dst.as<void>(), X.src.as<void>(), X.idx32, X.nlocal, t.faces_size, 1, y, g, d.stream());
+        launch_cgs_ev(t, fl, b, y, d.stream()); // sweep 2 of the edges and vertices
+        if (oop) x.arena(level).swap(next);
+    }
+    for (; count > 0; --count) smooth_cgs(A, rhs, x, level);
+}
+
 void diagonal(const Operator& A, Function& dst, int level) {
     check_op_function(A, dst, level, "diagonal", true);
     Domain& d = A.domain();
@@ -804,6 +859,11 @@ void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int
         return;
     }
     const std::vector<const void*> key = graph_key(rhs, x, level, nu_pre, nu_post, x_zero);
+    if (std::find(no_graph_.begin(), no_graph_.end(), key) != no_graph_.end()) {
+        cycle(rhs, x, level, nu_pre, nu_post, x_zero);
+        check_coarse();
+        return;
+    }
     for (const auto& g : graphs_)
         if (g.key == key) {
             HYB_CUDA(cudaGraphLaunch(g.exec, d.stream()));
@@ -832,9 +892,15 @@ void Hierarchy::run_cycle(Function& rhs, Function& x, int level, int nu_pre, int
     const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     HYB_CUDA(ie);
-    if (graph_key(rhs, x, level, nu_pre, nu_post, x_zero) != key) { // capture ran no kernels, only host bookkeeping
+    if (graph_key(rhs, x, level, nu_pre, nu_post, x_zero) != key) {
+        // the cycle leaves some arena swapped (an odd number of out-of-place sweeps on a
+        // level): the captured kernels match the host state after this one call but no
+        // later call, so run them once and keep this cycle eager from now on
+        HYB_CUDA(cudaGraphLaunch(exec, d.stream()));
         cudaGraphExecDestroy(exec);
-        throw LogicError("vcycle: arena state not restored by the captured cycle");
+        no_graph_.push_back(key);
+        check_coarse();
+        return;
     }
     graphs_.push_back({key, exec});
     HYB_CUDA(cudaGraphLaunch(exec, d.stream()));
@@ -948,10 +1014,12 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
     if (pair) {
         smooth_jacobi2(a_, rhs, x, omega_, level);
     } else {
-        for (int i = 0; i < nu_pre; ++i) {
-            if (i == 0 && zero_sweep) smooth_jacobi_zero(a_, rhs, x, omega_, level);
-            else smooth(rhs, x, level);
-        }
+        if (smoother_ == SMOOTH_CGS) smooth_cgs_n(a_, rhs, x, level, nu_pre);
+        else
+            for (int i = 0; i < nu_pre; ++i) {
+                if (i == 0 && zero_sweep) smooth_jacobi_zero(a_, rhs, x, omega_, level);
+                else smooth(rhs, x, level);
+            }
     }
     residual_restrict(a_, rhs, x, r_, b_, level - 1); // residual + restrict_to_coarse, fused
     fill_const(b_, 0.0, level - 1, kDirichletMask);
@@ -965,6 +1033,10 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
         i0 = 1;
     } else {
         prolongate(e_, x, level - 1, kSmoothMask, true);
+    }
+    if (smoother_ == SMOOTH_CGS) {
+        smooth_cgs_n(a_, rhs, x, level, nu_post - i0);
+        i0 = nu_post;
     }
     for (int i = i0; i < nu_post; ++i) {
         if (pair && i == nu_post - 1) smooth_jacobi(a_, rhs, x, omega_, level, dot_for(i), 2);

@@ -511,9 +511,13 @@ def smooth_gs(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: Scala
 
 
 def smooth_colored_gs(A: StencilOperator, ctl: Controller, rhs: ScalarFunction,  # noqa: ARG001
-                      x: ScalarFunction, level: int) -> None:
-    """Coloured hybrid Gauss-Seidel: faces by (c + 2r) mod 3, edges odd/even k."""
-    check(lib.hyb_smooth_cgs(A._h, rhs._h, x._h, level))
+                      x: ScalarFunction, level: int, count: int = 1) -> None:
+    """Coloured hybrid Gauss-Seidel: faces by (c + 2r) mod 3, edges odd/even k. With count > 1,
+    `count` sweeps (consecutive pairs in one face pass where possible; bitwise the same)."""
+    if count == 1:
+        check(lib.hyb_smooth_cgs(A._h, rhs._h, x._h, level))
+    else:
+        check(lib.hyb_smooth_cgs_n(A._h, rhs._h, x._h, level, count))
 
 
 def smooth_jacobi(A: StencilOperator, ctl: Controller, rhs: ScalarFunction, x: ScalarFunction,  # noqa: ARG001
