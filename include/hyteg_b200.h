@@ -286,7 +286,7 @@ int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, doubl
  * instead of 48 bytes per DoF at the face interiors); measured issue-bound and
  * slower than two sweeps on B200, so the knob defaults to off. */
 int hyb_smooth_jacobi2(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level);
-/* measurement knobs: "jacobi2_min_n", "cgs_pair_min_n", "mega_dofs_per_cta"
+/* measurement knobs: "jacobi2_min_n", "cgs_pair_min_n", "cgs_prolong_fused", "mega_dofs_per_cta"
  * (value < 0: query only; *previous = old value) */
 int hyb_tuning(const char* name, int64_t value, int64_t* previous);
 /* smooth_gs(A, ctl, rhs, x, level): hybrid Gauss-Seidel, lexicographic inside
@@ -318,6 +318,12 @@ int hyb_residual_restrict(hyb_operator* A, hyb_function* rhs, hyb_function* x, h
  * Bitwise the two calls in sequence. */
 int hyb_prolongate_add_jacobi(hyb_operator* A, hyb_function* e, hyb_function* rhs, hyb_function* x, double omega,
                               int coarse_level);
+/* prolongate(ctl, e, x, coarse_level, smooth mask) + add, then one coloured GS
+ * sweep (hyb_smooth_cgs) at coarse_level + 1, fused on faces of n >= 256 (the
+ * correction is added as the sweep stages each face row) when the knob
+ * "cgs_prolong_fused" is set (default off: measured slower on B200);
+ * otherwise the two calls. Bitwise the two calls in sequence either way. */
+int hyb_prolongate_add_cgs(hyb_operator* A, hyb_function* e, hyb_function* rhs, hyb_function* x, int coarse_level);
 /* assign / add_scaled / dot / norm2 / max_abs     function.hpp:60-74 */
 int hyb_assign(double alpha, hyb_function* x1, double beta, hyb_function* x2, hyb_function* dst, int level,
                uint8_t mask);

@@ -122,6 +122,7 @@ _SIGS = {
     "hyb_restrict": (_i, [_p, _p, _i, _u8]),
     "hyb_residual_restrict": (_i, [_p, _p, _p, _p, _p, _i]),
     "hyb_prolongate_add_jacobi": (_i, [_p, _p, _p, _p, _d, _i]),
+    "hyb_prolongate_add_cgs": (_i, [_p, _p, _p, _p, _i]),
     "hyb_assign": (_i, [_d, _p, _d, _p, _p, _i, _u8]),
     "hyb_add_scaled": (_i, [_p, _d, _p, _i, _u8]),
     "hyb_dot": (_i, [_p, _p, _i, _pd]),

@@ -816,6 +816,16 @@ int hyb_prolongate_add_jacobi(hyb_operator* A, hyb_function* e, hyb_function* rh
     });
 }
 
+int hyb_prolongate_add_cgs(hyb_operator* A, hyb_function* e, hyb_function* rhs, hyb_function* x, int coarse_level) {
+    return guarded([&] {
+        need(A, "hyb_prolongate_add_cgs");
+        need(e, "hyb_prolongate_add_cgs");
+        need(rhs, "hyb_prolongate_add_cgs");
+        need(x, "hyb_prolongate_add_cgs");
+        hyb::prolongate_add_cgs(*A->a, *e->f, *rhs->f, *x->f, coarse_level);
+    });
+}
+
 int hyb_assign(double alpha, hyb_function* x1, double beta, hyb_function* x2, hyb_function* dst, int level,
                uint8_t mask) {
     return guarded([&] {
@@ -898,6 +908,9 @@ int hyb_tuning(const char* name, int64_t value, int64_t* previous) {
         if (k == "mega_dofs_per_cta") { // applies to hierarchies created afterwards
             if (previous) *previous = hyb::mega_dofs_per_cta_default();
             if (value > 0) hyb::set_mega_dofs_per_cta_default(value);
+        } else if (k == "cgs_prolong_fused") {
+            if (previous) *previous = hyb::cgs_prolong_fused() ? 1 : 0;
+            if (value >= 0) hyb::set_cgs_prolong_fused(value != 0);
         } else if (k == "cgs_pair_min_n") {
             if (previous) *previous = hyb::cgs_pair_min_n();
             if (value >= 0) hyb::set_cgs_pair_min_n(int(std::min<int64_t>(value, int64_t(1) << 30)));

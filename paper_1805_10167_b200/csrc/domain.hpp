@@ -350,6 +350,9 @@ void smooth_jacobi_zero(const Operator& A, Function& rhs, Function& x, double om
 void smooth_gs(const Operator& A, Function& rhs, Function& x, int level);
 void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level);
 void smooth_cgs_n(const Operator& A, Function& rhs, Function& x, int level, int count);
+void prolongate_add_cgs(const Operator& A, Function& e, Function& rhs, Function& x, int lc);
+bool cgs_prolong_fused();
+void set_cgs_prolong_fused(bool on);
 int cgs_pair_min_n();
 void set_cgs_pair_min_n(int n);
 void diagonal(const Operator& A, Function& d, int level);
@@ -427,7 +430,7 @@ class Hierarchy {
     // captured kernel/NCCL sequence can be replayed while the pointers match.
   public:
     bool use_graphs = true;
-    bool fuse_post_ = true; // prolongate_add fused with the first Jacobi post-sweep
+    bool fuse_post_ = true; // prolongate_add fused with the first post-sweep (Jacobi, coloured GS)
     bool temporal_ = true;  // V(2, nu2 >= 2) Jacobi: the finest pre-smoothing pair as one two-sweep pass
     // Jacobi cycles from levels with n <= mega_max_n down as one cooperative kernel: 1 always,
     // 0 never, -1 (default) when the domain has at most mega_auto_faces faces (below that it

@@ -36,6 +36,34 @@ void Domain::build_exchange(LevelGeom& lg, const HostLayout& lay) {
     lg.recv_size = h.recv_size;
     if (int64_t(sendbuf_.bytes() / 8) < h.send_size) sendbuf_ = DevMem(size_t(h.send_size) * 8);
     if (int64_t(recvbuf_.bytes() / 8) < h.recv_size) recvbuf_ = DevMem(size_t(h.recv_size) * 8);
+    // The same-rank ghosts in face-address order (each dst is written once, so the order
+    // is free): a face's boundary ghosts (column 0, diagonal) and the edges' halo sources
+    // next to them (column 1, diagonal - 1) share DRAM sectors -- row r's diagonal, row
+    // r+1's columns 0 and 1 are adjacent slots -- and are now touched together instead of
+    // once per side (config 3, level 9: 1.7 GB of DRAM traffic per refresh for 0.6 GB of
+    // copies in plan order)
+    {
+        const int64_t fend = lay.faces_size;
+        auto key = [&](int64_t i) {
+            const int64_t d = h.dst[size_t(i)], s = h.src[size_t(i)];
+            return d < fend ? d : (s < fend ? s : fend + d);
+        };
+        std::vector<int64_t> perm(size_t(h.nlocal));
+        for (int64_t i = 0; i < h.nlocal; ++i) perm[size_t(i)] = i;
+        std::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return key(a) < key(b); });
+        std::vector<int64_t> d2(size_t(h.nlocal)), s2(size_t(h.nlocal));
+        for (int64_t i = 0; i < h.nlocal; ++i) {
+            d2[size_t(i)] = h.dst[size_t(perm[size_t(i)])];
+            s2[size_t(i)] = h.src[size_t(perm[size_t(i)])];
+        }
+        std::copy(d2.begin(), d2.end(), h.dst.begin());
+        std::copy(s2.begin(), s2.end(), h.src.begin());
+        if (h.owner_gidx.size() >= size_t(h.nlocal)) {
+            std::vector<int64_t> g2(size_t(h.nlocal));
+            for (int64_t i = 0; i < h.nlocal; ++i) g2[size_t(i)] = h.owner_gidx[size_t(perm[size_t(i)])];
+            std::copy(g2.begin(), g2.end(), h.owner_gidx.begin());
+        }
+    }
     fill_exchange(lg.xch, std::move(h), lay.arena_size, stream_);
 }
 

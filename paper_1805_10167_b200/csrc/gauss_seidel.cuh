@@ -615,21 +615,33 @@ __global__ void __launch_bounds__(NT) k_cgs_smem(LevelTables t, const double* __
 // producer's instruction stream bounded the step rate (ncu: consumers 33% in
 // the full-barrier wait, the producer warp never waiting).
 // Bitwise the in-place sweep, og_cgs.
-template <int K, int D, int CB, int WPR> struct CgcCfg {
+template <int K, int D, int CB, int WPR, bool PRO = false> struct CgcCfg {
     static constexpr int RX = D * K + 3 * K + 3; // x ring rows (see k_cgs_tma)
     static constexpr int RB = D * K + 2 * K + 2; // b ring rows
     static constexpr int NB = D + 1;
     static constexpr int CW = 3 * K * WPR;
-    static constexpr int THREADS = (CW + 2) * 32;
+    static constexpr int NCOR = PRO ? K : 0;  // corrector warps (prolongation fused in, one per entering row)
+    static constexpr int THREADS = (CW + 2 + NCOR) * 32;
     static constexpr int RS = CB + 8; // ring row: columns [c0-4, c0+CB+4)
-    static constexpr size_t SMEM = size_t(RX + RB) * RS * 8 + 16 * NB;
+    static constexpr int RC = PRO ? (D * K) / 2 + 3 : 0; // coarse ring rows
+    static constexpr int RCS = CB / 2 + 12;                // coarse columns [ca0, ca0 + RCS)
+    static constexpr size_t SMEM = size_t(RX + RB) * RS * 8 + size_t(RC) * RCS * 8 + 16 * NB;
 };
 
-template <int K, int D, int CB, int MINB, int WPR>
-__global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR>::THREADS, MINB)
-    k_cgs_cols(LevelTables t, const double* __restrict__ b, const double* x, double* y) {
+// PRO: prolongate + add fused in: the coarse correction xc (level L-1: coarse row
+// offsets cro, face stride cstride) is added to every staged face point off the border
+// layer (c, r >= 2, c + r <= n-2) as its x row enters the ring, by NCOR corrector warps
+// working one step ahead of the C0 block (rows first read at step i+1 are corrected
+// during step i, before its consumer barrier); producer B stages the coarse rows. The
+// caller has corrected edges, vertices and the layer in place and synced, as for
+// ST_JACOBI_PROLONG. Bitwise prolongate(add) followed by the sweep.
+template <int K, int D, int CB, int MINB, int WPR, bool PRO = false>
+__global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR, PRO>::THREADS, MINB)
+    k_cgs_cols(LevelTables t, const double* __restrict__ b, const double* x, double* y,
+               const double* __restrict__ xc = nullptr, const int64_t* __restrict__ cro = nullptr,
+               int64_t cstride = 0) {
     pdl_prologue();
-    using C = CgcCfg<K, D, CB, WPR>;
+    using C = CgcCfg<K, D, CB, WPR, PRO>;
     extern __shared__ __align__(16) double cc_ring[];
     constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = K + 1, RS = C::RS;
     const int n = t.n, W = t.W;
@@ -639,13 +651,15 @@ __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR>::THREADS, MINB)
     if (last < 1) return; // CTA-uniform
     double* xring = cc_ring;
     double* bring = cc_ring + size_t(RX) * RS;
-    uint64_t* full = reinterpret_cast<uint64_t*>(cc_ring + size_t(RX + RB) * RS);
+    double* cring = cc_ring + size_t(RX + RB) * RS; // PRO: coarse rows
+    uint64_t* full = reinterpret_cast<uint64_t*>(cring + size_t(C::RC) * C::RCS);
     uint64_t* done = full + NB;
     const int64_t base = int64_t(blockIdx.y) * t.face_stride;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nsteps = (last + 2 * S - 1) / K + 1;
     const int a0 = max(0, c0 - 4); // first staged column
     const int so = a0 - (c0 - 4);  // its ring index
+    const int ca0 = (a0 >> 1) & ~1; // PRO: first staged coarse column (even: 16-byte copies)
     if (threadIdx.x == 0) {
         for (int i = 0; i < NB; ++i) {
             mbar_init(&full[i], 2);
@@ -654,6 +668,44 @@ __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR>::THREADS, MINB)
         fence_mbar_init();
     }
     __syncthreads();
+    if constexpr (PRO) {
+        if (warp >= C::CW + 2) { // correctors: rows first read at step i+1, during step i
+            const int w = warp - (C::CW + 2);
+            const int64_t* __restrict__ ro = t.rowoff;
+            auto correct = [&](int q) {
+                if (q < 2 || q > n - 4) return; // rows with points off the layer
+                double* xr = xring + size_t(q % RX) * RS + 4 - c0;
+                const int cr = q >> 1;
+                const double* ca = cring + size_t(cr % C::RC) * C::RCS - ca0;
+                const double* cb = cring + size_t((cr + 1) % C::RC) * C::RCS - ca0;
+                const bool odd = q & 1;
+                const int chi_ = min(n - 2 - q, c1 + 3);
+#pragma unroll 4
+                for (int c = max(2, a0) + lane; c <= chi_; c += 32) {
+                    const int cc = c >> 1;
+                    double v;
+                    if (!odd) v = (c & 1) == 0 ? ca[cc] : 0.5 * (ca[cc] + ca[cc + 1]);
+                    else if ((c & 1) == 0) v = 0.5 * (ca[cc] + cb[cc]);
+                    else v = 0.5 * (ca[cc + 1] + cb[cc]);
+                    xr[c] = xr[c] + v;
+                }
+            };
+            (void)ro;
+            mbar_wait(&full[0], 0u);
+            correct(2 + w); // rows 2 .. K+1, read at step 0
+            fence_proxy_async_smem();
+            consumer_sync<(C::CW + C::NCOR) * 32>();
+            for (int i = 0; i < nsteps; ++i) {
+                if (i + 1 < nsteps) {
+                    mbar_wait(&full[(i + 1) % NB], uint32_t(((i + 1) / NB) & 1));
+                    correct((i + 1) * K + 2 + w);
+                    fence_proxy_async_smem();
+                }
+                consumer_sync<(C::CW + C::NCOR) * 32>();
+            }
+            return;
+        }
+    }
     if (warp >= C::CW) { // producers
         if (lane != 0) return;
         const int64_t* __restrict__ ro = t.rowoff;
@@ -697,18 +749,34 @@ __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR>::THREADS, MINB)
                 if (i + D < nsteps) load_x(i + D);
             }
             bulk_wait_all();
-        } else { // B: b rows [1 + sK, (s+1)K]
+        } else { // B: b rows [1 + sK, (s+1)K] (PRO: and the coarse rows of the fine rows read at step s)
             const double* bf = b + base;
             int q_next = 1, slot_next = 1 % RB;
+            int cq_next = 0;
+            const int nc = n >> 1;
+            // coarse row cq: columns [ca0, min(ca0 + RCS, row end rounded up to 2))
+            auto cseg = [&](int cq) {
+                const int e = min(ca0 + C::RCS, (nc + 2 - cq) & ~1);
+                return e > ca0 ? uint32_t(e - ca0) * 8u : 0u;
+            };
             auto load_b = [&](int s_) {
                 const int qhi = min(last, (s_ + 1) * K);
+                // PRO: coarse rows of fine rows <= 1 + (s_+1)K (corrected at step s_-1)
+                const int cqhi = PRO ? min(nc - 1, ((1 + (s_ + 1) * K) >> 1) + 1) : -1;
                 uint32_t bytes = 0;
                 for (int q = q_next; q <= qhi; ++q) bytes += seg(q, a0, c1 + 2);
+                for (int cq = cq_next; cq <= cqhi; ++cq) bytes += cseg(cq);
                 mbar_arrive_expect_tx(&full[s_ % NB], bytes);
                 for (; q_next <= qhi; ++q_next) {
                     const uint32_t nb_ = seg(q_next, a0, c1 + 2);
                     if (nb_) bulk_g2s(bring + size_t(slot_next) * RS + so, bf + ro[q_next] + a0, nb_, &full[s_ % NB]);
                     slot_next = slot_next + 1 == RB ? 0 : slot_next + 1;
+                }
+                for (; cq_next <= cqhi; ++cq_next) { // PRO only (cqhi < 0 otherwise)
+                    const uint32_t nb_ = cseg(cq_next);
+                    if (nb_)
+                        bulk_g2s(cring + size_t(cq_next % C::RC) * C::RCS,
+                                 xc + int64_t(blockIdx.y) * cstride + cro[cq_next] + ca0, nb_, &full[s_ % NB]);
                 }
             };
             for (int s_ = 0; s_ < D && s_ < nsteps; ++s_) load_b(s_);
@@ -734,6 +802,7 @@ __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR>::THREADS, MINB)
     int t3 = wrap(colour - 2 * r, 3);
     constexpr int DT3 = (3 - (2 * K) % 3) % 3;
     const int sh = 4 - c0; // ring index of column c
+    if constexpr (PRO) consumer_sync<(C::CW + C::NCOR) * 32>(); // the correctors' rows of step 0
 #pragma unroll 1
     for (int i = 0; i < nsteps; ++i) {
         mbar_wait(&full[i % NB], uint32_t((i / NB) & 1));
@@ -760,7 +829,7 @@ __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR>::THREADS, MINB)
             }
         }
         fence_proxy_async_smem();
-        consumer_sync<C::CW * 32>();
+        consumer_sync<(C::CW + C::NCOR) * 32>();
         if (lane == 0) mbar_arrive(&done[i % NB]);
         r += K;
         sxm = sxm + K >= RX ? sxm + K - RX : sxm + K;

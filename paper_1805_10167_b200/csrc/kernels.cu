@@ -933,7 +933,9 @@ bool launch_cgs_cols(const LevelTables& t, const double* b, double* x, double* y
     if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
     const int nb = (t.n - 1 + CB - 1) / CB; // blocks over columns [0, n-1)
     double* out = nb == 1 ? x : y;          // one block per face: in place
-    pdl_launch(k_cgs_cols<K, D, CB, MINB, WPR>, dim3(unsigned(nb), unsigned(t.nfaces)), C::THREADS, C::SMEM, st, t, b, x, out);
+    pdl_launch(k_cgs_cols<K, D, CB, MINB, WPR>, dim3(unsigned(nb), unsigned(t.nfaces)), C::THREADS, C::SMEM, st, t, b,
+               static_cast<const double*>(x), out, static_cast<const double*>(nullptr), static_cast<const int64_t*>(nullptr),
+               int64_t(0));
     return nb > 1;
 }
 
@@ -995,6 +997,25 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
     }
     check_launch("coloured gauss-seidel faces (column blocks)");
     return oop;
+}
+
+// prolongate(add) + one coloured sweep, fused on the faces (k_cgs_cols<PRO>): 256-column
+// blocks (in place at n = 256, out of place above). Returns -1 where no fused variant
+// exists (n < 256: the whole-face shared-memory sweep), else whether it swept out of place.
+int launch_cgs_prolong(const LevelTables& tc, const LevelTables& t, const double* b, double* x, double* y,
+                       const double* xc, cudaStream_t st) {
+    if (t.nfaces <= 0 || t.n < 256) return -1;
+    using C = CgcCfg<2, 3, 256, 1, true>;
+    static const bool attr = cudaFuncSetAttribute(k_cgs_cols<2, 3, 256, 3, 1, true>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)) ==
+                             cudaSuccess;
+    if (!attr) throw CudaError("coloured gauss-seidel (prolongation fused): cannot reserve shared memory");
+    const int nb = (t.n - 1 + 255) / 256;
+    double* out = nb == 1 ? x : y;
+    pdl_launch(k_cgs_cols<2, 3, 256, 3, 1, true>, dim3(unsigned(nb), unsigned(t.nfaces)), C::THREADS, C::SMEM, st,
+               t, b, static_cast<const double*>(x), out, xc, static_cast<const int64_t*>(tc.rowoff), tc.face_stride);
+    check_launch("coloured gauss-seidel faces (prolongation fused)");
+    return nb > 1 ? 1 : 0;
 }
 
 // two coloured sweeps per face pass (k_cgs_pair); returns false where no pair variant is tuned

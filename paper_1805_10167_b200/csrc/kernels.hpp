@@ -149,6 +149,10 @@ void launch_gs_ev(const LevelTables& t, const FlagTables& fl, const double* b, d
 // odd/even k, vertices as in launch_gs_ev
 void launch_cgs_faces(const LevelTables& t, const double* b, double* x, cudaStream_t st);
 void launch_cgs_ev(const LevelTables& t, const FlagTables& fl, const double* b, double* x, cudaStream_t st);
+// prolongate(add) fused into one coloured face sweep (k_cgs_cols<PRO>): -1 if no variant
+// for the face size, else 1 when it swept out of place (into y)
+int launch_cgs_prolong(const LevelTables& tc, const LevelTables& t, const double* b, double* x, double* y,
+                       const double* xc, cudaStream_t st);
 // two coloured face sweeps in one pass (see k_cgs_pair); cgs_pair_blocks: column blocks per face
 // of the tuned variant for face size n (0: none, 1: in place)
 int cgs_pair_blocks(int n);

@@ -521,6 +521,51 @@ void prolongate_add_jacobi(const Operator& A, Function& e, Function& rhs, Functi
     x.arena(level).swap(next);
 }
 
+// prolongate(e -> x, smooth mask, add) followed by smooth_cgs(A, rhs, x, lc+1), fused
+// on the faces where a variant exists (k_cgs_cols<PRO>, faces of n >= 256): edges,
+// vertices and the face layer next to the borders take the correction in place, a sync
+// refreshes the ghosts, and the sweep adds the correction to the other face points as
+// their rows enter its ring, so the corrected faces are never stored before the sweep.
+// Bitwise the two calls in sequence. Measured slower than the two calls on B200
+// (config 3, per level with the syncs: L9 10.59 vs 9.62 ms, L8 3.36 vs 2.99): the
+// fused sweep needs 256-column blocks and corrector warps (9.57 ms, 6.3 G instructions,
+// against 5.56 ms + 3.38 ms for the 512-column sweep and the prolongation), so the
+// fusion is off unless asked for (hyb_tuning("cgs_prolong_fused", 1)).
+bool g_cgs_prolong_fused = false;
+bool cgs_prolong_fused() { return g_cgs_prolong_fused; }
+void set_cgs_prolong_fused(bool on) { g_cgs_prolong_fused = on; }
+
+void prolongate_add_cgs(const Operator& A, Function& e, Function& rhs, Function& x, int lc) {
+    const int level = lc + 1;
+    check_transfer(e, x, lc, "prolongate");
+    check_op_function(A, rhs, level, "smooth_cgs", true);
+    check_op_function(A, x, level, "smooth_cgs", true);
+    if (&rhs == &x) throw InvalidArgument("smooth_cgs: rhs and x must be distinct functions");
+    require_p1(x, "smooth_cgs");
+    const LevelTables t = A.tables(level);
+    if (!cgs_prolong_fused() || t.n < 256) {
+        prolongate(e, x, lc, kSmoothMask, true);
+        smooth_cgs(A, rhs, x, level);
+        return;
+    }
+    check_diagonals(A, x, level, "smooth_cgs");
+    Domain& d = A.domain();
+    d.sync(e, lc);
+    const LevelTables& tc = d.level(lc).t;
+    launch_prolongate(tc, t, x.flags(), e.data(lc), x.data(level), kSmoothMask, true, d.stream(), false);
+    launch_prolongate_layer(tc, t, e.data(lc), x.data(level), d.stream());
+    d.sync(x, level);
+    DevMem& next = d.jacobi_scratch(level);
+    d.timer_begin("coloured_gs_prolong");
+    const int oop = launch_cgs_prolong(tc, t, rhs.data(level), x.data(level), next.as<double>(), e.data(lc), d.stream());
+    d.timer_end();
+    d.fork();
+    if (oop) launch_cgs_ev_oop(t, x.flags(), rhs.data(level), x.data(level), next.as<double>(), d.aux_stream());
+    else launch_cgs_ev(t, x.flags(), rhs.data(level), x.data(level), d.aux_stream());
+    d.join();
+    if (oop) x.arena(level).swap(next);
+}
+
 void restrict_to_coarse(Function& fine, Function& coarse, int lc, uint8_t mask) {
     check_transfer(coarse, fine, lc, "restrict_to_coarse");
     Domain& d = fine.domain();
@@ -1030,6 +1075,9 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
     int i0 = 0;
     if (nu_post > 0 && smoother_ == SMOOTH_JACOBI && fuse_post_) {
         prolongate_add_jacobi(a_, e_, rhs, x, omega_, level - 1, dot_for(0));
+        i0 = 1;
+    } else if (nu_post > 0 && smoother_ == SMOOTH_CGS && fuse_post_) {
+        prolongate_add_cgs(a_, e_, rhs, x, level - 1);
         i0 = 1;
     } else {
         prolongate(e_, x, level - 1, kSmoothMask, true);

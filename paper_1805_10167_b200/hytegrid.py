@@ -571,6 +571,13 @@ def prolongate_add_jacobi(A: StencilOperator, ctl: Controller, e: ScalarFunction
     check(lib.hyb_prolongate_add_jacobi(A._h, e._h, rhs._h, x._h, omega, coarse_level))
 
 
+def prolongate_add_colored_gs(A: StencilOperator, ctl: Controller, e: ScalarFunction,  # noqa: ARG001
+                              rhs: ScalarFunction, x: ScalarFunction, coarse_level: int) -> None:
+    """prolongate_add(e -> x, smooth mask) then smooth_colored_gs(rhs, x), fused on faces of
+    n >= 256 (the V-cycle's correction and first coloured post-sweep); bitwise the two calls."""
+    check(lib.hyb_prolongate_add_cgs(A._h, e._h, rhs._h, x._h, coarse_level))
+
+
 def assign(alpha: float, x1: ScalarFunction, beta: float, x2: ScalarFunction, dst: ScalarFunction, level: int,
            flag_mask: int = ALL_DOF_FLAGS) -> None:
     check(lib.hyb_assign(alpha, x1._h, beta, x2._h, dst._h, level, flag_mask))

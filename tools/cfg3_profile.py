@@ -7,6 +7,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1805_10167_b200 import hytegrid as H  # noqa: E402
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 9
+if "HYB_CGS_PROLONG" in os.environ:
+    H.tuning("cgs_prolong_fused", int(os.environ["HYB_CGS_PROLONG"]))
 if "HYB_CGS_PAIR_MIN_N" in os.environ:
     H.tuning("cgs_pair_min_n", int(os.environ["HYB_CGS_PAIR_MIN_N"]))
 cyc = 3
@@ -34,7 +36,7 @@ dom.synchronize()
 tot = dom.event_elapsed(0, 1) / cyc
 print(f"profiled: {tot:.2f} ms per cycle")
 acc = 0.0
-for name in ("coloured_gs_pair", "coloured_gs", "residual_restrict", "restrict", "prolongate_add", "prolongate", "coarse_cg", "apply"):
+for name in ("coloured_gs_pair", "coloured_gs_prolong", "coloured_gs", "residual_restrict", "restrict", "prolongate_add", "prolongate", "coarse_cg", "apply"):
     ms, n = dom.timer(name)
     if n:
         acc += ms / cyc
