@@ -840,6 +840,176 @@ __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR, PRO>::THREADS, MINB)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Coloured face sweep on two faces per CTA (faces whose n - 1 columns fit one
+// ring row, in place). The k_cgs_cols step schedule, but each ring row holds
+// row v of face A (W - v entries) followed by row n-1-v of face B (v + 2
+// entries): A is swept upwards in row index and B downwards, so every ring row
+// is full, every step moves the same n + 3 entries per row, and the per-step
+// cost (barrier waits, slot arithmetic, the consumer barrier, the producers'
+// scalar issue) is paid once for two faces. A colour class is an independent
+// set and the skewed blocks (C0 on virtual rows [j, j+K), C1 on [j-S, ..), C2
+// on [j-2S, ..), S = K+1) order the classes the same way in either direction,
+// so B's updates see exactly the operands of the three full-face passes:
+// bitwise og_cgs. Lanes 0 and 1 of the two producer warps serve faces A and B
+// (x loads + write-back, b loads); the last CTA of an odd face count runs A
+// alone. The 7+1 coefficients and 1/diag of both faces sit in shared memory
+// (registers hold one face's at a time).
+template <int K, int D, int NMAX> struct CgdCfg {
+    static constexpr int RX = D * K + 3 * K + 3; // x ring rows (see k_cgs_tma)
+    static constexpr int RB = D * K + 2 * K + 2; // b ring rows
+    static constexpr int NB = D + 1;
+    static constexpr int CW = 3 * K;             // consumer warps: one per row of a step
+    static constexpr int THREADS = (CW + 2) * 32;
+    static constexpr int RS = NMAX + 8; // A: [0, W-v), B from round_up(W-v, 4): <= W + 6 entries
+    static constexpr size_t SMEM = size_t(RX + RB) * RS * 8 + 16 * NB + 2 * 10 * 8;
+};
+
+template <int K, int D, int NMAX, int MINB>
+__global__ void __launch_bounds__(CgdCfg<K, D, NMAX>::THREADS, MINB)
+    k_cgs_duo(LevelTables t, const double* __restrict__ b, double* x) {
+    pdl_prologue();
+    using C = CgdCfg<K, D, NMAX>;
+    extern __shared__ __align__(16) double cd_ring[];
+    constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = K + 1, RS = C::RS;
+    const int n = t.n, W = t.W, last = n - 2;
+    const int fa = 2 * int(blockIdx.x);
+    const bool hasB = fa + 1 < t.nfaces;
+    double* xring = cd_ring;
+    double* bring = cd_ring + size_t(RX) * RS;
+    uint64_t* full = reinterpret_cast<uint64_t*>(cd_ring + size_t(RX + RB) * RS);
+    uint64_t* done = full + NB;
+    double* cosm = reinterpret_cast<double*>(done + NB); // [2][10]: 7 terms, diag, 1/diag
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nsteps = (last + 2 * S - 1) / K + 1;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NB; ++i) {
+            mbar_init(&full[i], hasB ? 4 : 2);
+            mbar_init(&done[i], C::CW);
+        }
+        fence_mbar_init();
+    }
+    if (threadIdx.x < 16 && (threadIdx.x < 8 || hasB)) {
+        const int sd = threadIdx.x >> 3, i = threadIdx.x & 7;
+        const double v = __ldg(t.face_coef + size_t(fa + sd) * 8 + i);
+        cosm[sd * 10 + i] = v;
+        if (i == 7) cosm[sd * 10 + 8] = 1.0 / v;
+    }
+    __syncthreads();
+    if (warp >= C::CW) { // producers: lane 0 face A, lane 1 face B
+        if (lane > (hasB ? 1 : 0)) return;
+        const int side = lane;
+        const int64_t* __restrict__ ro = t.rowoff;
+        const int64_t base = int64_t(fa + side) * t.face_stride;
+        // virtual row v: face row, its ring offset and its copied bytes (entries rounded up to 2)
+        auto real = [&](int v) { return side ? n - 1 - v : v; };
+        auto off = [&](int v) { return side ? (W - v + 3) & ~3 : 0; };
+        auto nbytes = [&](int v) { return uint32_t((W - real(v) + 1) & ~1) * 8u; };
+        if (warp == C::CW) { // write-back of final rows, x rows
+            double* xf = x + base;
+            const int xmax = last + 1;
+            int q_next = 0, slot_next = 0;
+            auto load_x = [&](int s_) { // rows first read at step s_: up to 1 + (s_+1)K
+                const int qhi = min(xmax, 1 + (s_ + 1) * K);
+                uint32_t bytes = 0;
+                for (int q = q_next; q <= qhi; ++q) bytes += nbytes(q);
+                mbar_arrive_expect_tx(&full[s_ % NB], bytes);
+                for (; q_next <= qhi; ++q_next) {
+                    bulk_g2s(xring + size_t(slot_next) * RS + off(q_next), xf + ro[real(q_next)], nbytes(q_next),
+                             &full[s_ % NB]);
+                    slot_next = slot_next + 1 == RX ? 0 : slot_next + 1;
+                }
+            };
+            for (int s_ = 0; s_ < D && s_ < nsteps; ++s_) load_x(s_);
+            int q_st = 1 - 2 * S, slot_st = ((q_st % RX) + RX) % RX; // first row of step 0's C2 block
+            for (int i = 0; i < nsteps; ++i) {
+                mbar_wait(&done[i % NB], uint32_t((i / NB) & 1));
+                for (int k = 0; k < K; ++k) { // rows q_st .. q_st + K - 1 are final after step i
+                    const int q = q_st + k;
+                    const int sl = slot_st + k >= RX ? slot_st + k - RX : slot_st + k;
+                    if (q >= 1 && q <= last) bulk_s2g(xf + ro[real(q)], xring + size_t(sl) * RS + off(q), nbytes(q));
+                }
+                bulk_commit();
+                bulk_wait_read1();
+                q_st += K;
+                slot_st = slot_st + K >= RX ? slot_st + K - RX : slot_st + K;
+                if (i + D < nsteps) load_x(i + D);
+            }
+            bulk_wait_all();
+        } else { // b rows [1 + sK, (s+1)K]
+            const double* bf = b + base;
+            int q_next = 1, slot_next = 1 % RB;
+            auto load_b = [&](int s_) {
+                const int qhi = min(last, (s_ + 1) * K);
+                uint32_t bytes = 0;
+                for (int q = q_next; q <= qhi; ++q) bytes += nbytes(q);
+                mbar_arrive_expect_tx(&full[s_ % NB], bytes);
+                for (; q_next <= qhi; ++q_next) {
+                    bulk_g2s(bring + size_t(slot_next) * RS + off(q_next), bf + ro[real(q_next)], nbytes(q_next),
+                             &full[s_ % NB]);
+                    slot_next = slot_next + 1 == RB ? 0 : slot_next + 1;
+                }
+            };
+            for (int s_ = 0; s_ < D && s_ < nsteps; ++s_) load_b(s_);
+            for (int i = 0; i + D < nsteps; ++i) {
+                mbar_wait(&done[i % NB], uint32_t((i / NB) & 1));
+                load_b(i + D);
+            }
+        }
+        return;
+    }
+    const int colour = warp / K, roff = warp % K;
+    int r = 1 - S * colour + roff; // virtual row
+    auto wrap = [](int v, int m) { return ((v % m) + m) % m; };
+    int sxm = wrap(r - 1, RX), sx0 = wrap(r, RX), sxp = wrap(r + 1, RX), sb = wrap(r, RB);
+    const int nsides = hasB ? 2 : 1;
+#pragma unroll 1
+    for (int i = 0; i < nsteps; ++i) {
+        mbar_wait(&full[i % NB], uint32_t((i / NB) & 1));
+        if (r >= 1 && r <= last) {
+#pragma unroll 1
+            for (int side = 0; side < nsides; ++side) {
+                // face row rr; rows rr-1 / rr+1 are virtual r-1 / r+1 for A, r+1 / r-1 for B
+                const int rr = side ? n - 1 - r : r;
+                const int o0 = side ? (W - r + 3) & ~3 : 0;
+                const double* rm = xring + (side ? sxp * RS + ((W - r + 2) & ~3) : sxm * RS);
+                double* r0 = xring + sx0 * RS + o0;
+                const double* rp = xring + (side ? sxm * RS + ((W - r + 4) & ~3) : sxp * RS);
+                const double* br = bring + sb * RS + o0;
+                double co[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) co[k] = cosm[side * 10 + k];
+                const double rd = cosm[side * 10 + 8];
+                const int cmax = n - 1 - rr;
+                const int t3 = wrap(colour - 2 * rr, 3);
+                const int cs = t3 == 0 ? 3 : t3; // first column >= 1 of this colour
+#pragma unroll 1
+                for (int c = cs + 3 * lane; c <= cmax; c += 192) {
+                    const int c2 = c + 96;
+                    double v[8], w[8];
+                    v[0] = r0[c - 1], v[1] = rp[c - 1], v[2] = rm[c], v[3] = r0[c];
+                    v[4] = rp[c], v[5] = rm[c + 1], v[6] = r0[c + 1], v[7] = br[c];
+                    const bool two = c2 <= cmax;
+                    if (two) {
+                        w[0] = r0[c2 - 1], w[1] = rp[c2 - 1], w[2] = rm[c2], w[3] = r0[c2];
+                        w[4] = rp[c2], w[5] = rm[c2 + 1], w[6] = r0[c2 + 1], w[7] = br[c2];
+                    }
+                    r0[c] = cgs_point_update(v, co, rd);
+                    if (two) r0[c2] = cgs_point_update(w, co, rd);
+                }
+            }
+        }
+        fence_proxy_async_smem();
+        consumer_sync<C::CW * 32>();
+        if (lane == 0) mbar_arrive(&done[i % NB]);
+        r += K;
+        sxm = sxm + K >= RX ? sxm + K - RX : sxm + K;
+        sx0 = sx0 + K >= RX ? sx0 + K - RX : sx0 + K;
+        sxp = sxp + K >= RX ? sxp + K - RX : sxp + K;
+        sb = sb + K >= RB ? sb + K - RB : sb + K;
+    }
+}
+
 // edges out of place: odd k from x, then even k reading the new odd values
 // from y (the in-place sweep's operands); DIRICHLET lines are copied
 __global__ void __launch_bounds__(128) k_cgs_edges_oop(LevelTables t, FlagTables fl, const double* __restrict__ b,

@@ -939,6 +939,17 @@ bool launch_cgs_cols(const LevelTables& t, const double* b, double* x, double* y
     return nb > 1;
 }
 
+// two faces per CTA (k_cgs_duo): in place
+template <int K, int D, int NMAX, int MINB>
+void launch_cgs_duo(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
+    using C = CgdCfg<K, D, NMAX>;
+    static const bool attr = cudaFuncSetAttribute(k_cgs_duo<K, D, NMAX, MINB>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)) ==
+                             cudaSuccess;
+    if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
+    pdl_launch(k_cgs_duo<K, D, NMAX, MINB>, unsigned((t.nfaces + 1) / 2), C::THREADS, C::SMEM, st, t, b, x);
+}
+
 template <int NT>
 void launch_cgs_smem(const LevelTables& t, const double* b, double* x, size_t smem, cudaStream_t st) {
     static const bool attr =
@@ -983,6 +994,15 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
         const size_t smem = size_t(face_rowoff(t.W, t.n)) * 8; // rows 0..n-1
         if (n == 128) launch_cgs_smem<512>(t, b, x, smem, st);
         else launch_cgs_smem<256>(t, b, x, smem, st);
+    } else if (n == 256 && v != 20 && !t.face_list) {
+        // two faces per CTA (k_cgs_duo), config 3 L8: 1.450 ms per sweep against 1.700 one face per CTA
+        // (HYB_CGS_CFG=20); 4 CTAs per SM (64 registers) 1.598, K = 4 1.548, D = 2 1.636, D = 4 1.452;
+        // at n = 128 the whole-face kernel stays ahead (0.429 ms against 0.670)
+        launch_cgs_duo<2, 3, 256, 3>(t, b, x, st);
+    } else if (n == 512 && v != 20 && !t.face_list) {
+        // config 3 L9: 4.744 ms per sweep (0.83 of the copy peak) against 5.545; K = 4 (one CTA per SM)
+        // 5.078, D = 2 5.248, K = 3 / D = 1 7.435
+        launch_cgs_duo<2, 3, 512, 2>(t, b, x, st);
     } else if (n == 256) {
         // config 3 L8: 4 CTAs per SM (64 registers) 1.705 ms per sweep; 3 CTAs 1.828, D = 2 1.884,
         // 128-column blocks out of place 2.42-2.44

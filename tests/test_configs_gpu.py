@@ -92,6 +92,28 @@ def test_colored_gs_bitwise_large_faces(mesh_name, ranks):
             assert np.array_equal(x.download(level), o.get(1, level)), (mesh_name, ranks, level, sweep)
 
 
+@pytest.mark.parametrize("ranks", [1, 3])
+def test_colored_gs_two_faces_per_cta(ranks):
+    """Faces of n = 256 and 512 are swept two per CTA (k_cgs_duo: face A upwards, face B downwards in
+    one ring; an odd local face count leaves the last CTA with one face). ring8 on 3 ranks has 3 + 3 + 2
+    local faces, channel(3,1) 6 faces of mixed orientation; bitwise the restatement, three sweeps."""
+    for mesh, levels in ((FIXTURES["ring8"](), (8, 9)), (H.meshgen.channel(3, 1), (8,))):
+        for level in levels:
+            dom = H.DistributedDomain(mesh, ranks)
+            ctl = H.Controller(dom)
+            A = H.StencilOperator(dom, H.LAPLACE, level, level)
+            rhs, x = H.ScalarFunction("rhs", dom, level, level), H.ScalarFunction("x", dom, level, level)
+            o = O.Session(mesh, level, level, 2)
+            for f, i, seed in ((rhs, 0, 71), (x, 1, 72)):
+                v = keyed_uniform(mesh, level, seed)
+                f.upload(level, v)
+                o.set(i, level, v)
+            for sweep in range(3):
+                H.smooth_colored_gs(A, ctl, rhs, x, level)
+                o.cgs(0, 1, level)
+                assert np.array_equal(x.download(level), o.get(1, level)), (ranks, level, sweep)
+
+
 def test_cfg3_reduced_vcycle_history():
     """Config 3 shape at reduced size: perturbed annulus(32, 8) levels 5 -> 0,
     V(3,3) coloured GS, rhs U[-1,1] (seed 2) on INNER, x0 = 0, 5 cycles."""
