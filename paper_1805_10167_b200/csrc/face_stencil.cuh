@@ -311,11 +311,11 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
             p1 = (c + 1 >= 2 && c + 1 <= lim) ? p1 + v1 : p1;
             pr = (c + 2 >= 2 && c + 2 <= lim) ? pr + vr : pr;
         }
-        // a warp whose first column lies past the row's end has nothing to restrict on this or any
-        // later row of the band (rows only get shorter): skip the arithmetic, warp-uniformly
-        if (RR && i >= 2 && c0 + 2 * (31 * warp - 1) <= n - (r_lo + i - 2) + 2) {
+        if (RR && i >= 2) {
             // residual of fine row q at c, c+1, same operations as
-            // ST_RESIDUAL; every lane of a live warp computes (the shuffle follows)
+            // ST_RESIDUAL; every lane computes (the shuffle follows). Skipping the warps whose
+            // columns lie past the row's end (warp-uniform) was measured slower on config 3's
+            // 8192 faces: level 9 4.47 ms against 3.98, level 8 1.48 against 1.34
             const int q = r_lo + i - 2;
             double a0 = 0.0;
             a0 += cW * zl;

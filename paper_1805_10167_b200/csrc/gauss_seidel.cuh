@@ -855,55 +855,59 @@ __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR, PRO>::THREADS, MINB)
 // (x loads + write-back, b loads); the last CTA of an odd face count runs A
 // alone. The 7+1 coefficients and 1/diag of both faces sit in shared memory
 // (registers hold one face's at a time).
-template <int K, int D, int NMAX> struct CgdCfg {
+template <int K, int D, int NMAX, int NP = 1> struct CgdCfg {
     static constexpr int RX = D * K + 3 * K + 3; // x ring rows (see k_cgs_tma)
     static constexpr int RB = D * K + 2 * K + 2; // b ring rows
     static constexpr int NB = D + 1;
     static constexpr int CW = 3 * K;             // consumer warps: one per row of a step
     static constexpr int THREADS = (CW + 2) * 32;
-    static constexpr int RS = NMAX + 8; // A: [0, W-v), B from round_up(W-v, 4): <= W + 6 entries
-    static constexpr size_t SMEM = size_t(RX + RB) * RS * 8 + 16 * NB + 2 * 10 * 8;
+    static constexpr int PS = NMAX + 8; // one pair: A [0, W-v), B from round_up(W-v, 4): <= W + 6 entries
+    static constexpr int RS = NP * PS;  // ring row: NP face pairs side by side
+    static constexpr size_t SMEM = size_t(RX + RB) * RS * 8 + 16 * NB + 2 * NP * 10 * 8;
 };
 
-template <int K, int D, int NMAX, int MINB>
-__global__ void __launch_bounds__(CgdCfg<K, D, NMAX>::THREADS, MINB)
+// NP: face pairs per CTA (faces 2 NP blockIdx.x ...; the per-step cost is then shared by 2 NP
+// faces, which pays on smaller faces whose rows are short). NPT = 0: two points per lane and
+// iteration, the second skipped by a branch; NPT >= 1: NPT points, branch-free (see below).
+template <int K, int D, int NMAX, int MINB, int NPT = 0, int NP = 1>
+__global__ void __launch_bounds__(CgdCfg<K, D, NMAX, NP>::THREADS, MINB)
     k_cgs_duo(LevelTables t, const double* __restrict__ b, double* x) {
     pdl_prologue();
-    using C = CgdCfg<K, D, NMAX>;
+    using C = CgdCfg<K, D, NMAX, NP>;
     extern __shared__ __align__(16) double cd_ring[];
-    constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = K + 1, RS = C::RS;
+    constexpr int RX = C::RX, RB = C::RB, NB = C::NB, S = K + 1, RS = C::RS, PS = C::PS;
     const int n = t.n, W = t.W, last = n - 2;
-    const int fa = 2 * int(blockIdx.x);
-    const bool hasB = fa + 1 < t.nfaces;
+    const int f0 = 2 * NP * int(blockIdx.x);
+    const int nf = min(2 * NP, t.nfaces - f0); // faces of this CTA (>= 1)
     double* xring = cd_ring;
     double* bring = cd_ring + size_t(RX) * RS;
     uint64_t* full = reinterpret_cast<uint64_t*>(cd_ring + size_t(RX + RB) * RS);
     uint64_t* done = full + NB;
-    double* cosm = reinterpret_cast<double*>(done + NB); // [2][10]: 7 terms, diag, 1/diag
+    double* cosm = reinterpret_cast<double*>(done + NB); // [2 NP][10]: 7 terms, diag, 1/diag
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nsteps = (last + 2 * S - 1) / K + 1;
     if (threadIdx.x == 0) {
         for (int i = 0; i < NB; ++i) {
-            mbar_init(&full[i], hasB ? 4 : 2);
+            mbar_init(&full[i], 2 * nf);
             mbar_init(&done[i], C::CW);
         }
         fence_mbar_init();
     }
-    if (threadIdx.x < 16 && (threadIdx.x < 8 || hasB)) {
+    if (threadIdx.x < 16 * NP && int(threadIdx.x >> 3) < nf) {
         const int sd = threadIdx.x >> 3, i = threadIdx.x & 7;
-        const double v = __ldg(t.face_coef + size_t(fa + sd) * 8 + i);
+        const double v = __ldg(t.face_coef + size_t(f0 + sd) * 8 + i);
         cosm[sd * 10 + i] = v;
         if (i == 7) cosm[sd * 10 + 8] = 1.0 / v;
     }
     __syncthreads();
-    if (warp >= C::CW) { // producers: lane 0 face A, lane 1 face B
-        if (lane > (hasB ? 1 : 0)) return;
-        const int side = lane;
+    if (warp >= C::CW) { // producers: lane s serves face f0 + s (even s: side A, odd s: side B)
+        if (lane >= nf) return;
+        const int side = lane & 1, pbase = (lane >> 1) * PS;
         const int64_t* __restrict__ ro = t.rowoff;
-        const int64_t base = int64_t(fa + side) * t.face_stride;
+        const int64_t base = int64_t(f0 + lane) * t.face_stride;
         // virtual row v: face row, its ring offset and its copied bytes (entries rounded up to 2)
         auto real = [&](int v) { return side ? n - 1 - v : v; };
-        auto off = [&](int v) { return side ? (W - v + 3) & ~3 : 0; };
+        auto off = [&](int v) { return pbase + (side ? (W - v + 3) & ~3 : 0); };
         auto nbytes = [&](int v) { return uint32_t((W - real(v) + 1) & ~1) * 8u; };
         if (warp == C::CW) { // write-back of final rows, x rows
             double* xf = x + base;
@@ -962,40 +966,66 @@ __global__ void __launch_bounds__(CgdCfg<K, D, NMAX>::THREADS, MINB)
     int r = 1 - S * colour + roff; // virtual row
     auto wrap = [](int v, int m) { return ((v % m) + m) % m; };
     int sxm = wrap(r - 1, RX), sx0 = wrap(r, RX), sxp = wrap(r + 1, RX), sb = wrap(r, RB);
-    const int nsides = hasB ? 2 : 1;
 #pragma unroll 1
     for (int i = 0; i < nsteps; ++i) {
         mbar_wait(&full[i % NB], uint32_t((i / NB) & 1));
         if (r >= 1 && r <= last) {
 #pragma unroll 1
-            for (int side = 0; side < nsides; ++side) {
+            for (int s = 0; s < nf; ++s) {
                 // face row rr; rows rr-1 / rr+1 are virtual r-1 / r+1 for A, r+1 / r-1 for B
+                const int side = s & 1, pbase = (s >> 1) * PS;
                 const int rr = side ? n - 1 - r : r;
-                const int o0 = side ? (W - r + 3) & ~3 : 0;
-                const double* rm = xring + (side ? sxp * RS + ((W - r + 2) & ~3) : sxm * RS);
+                const int o0 = pbase + (side ? (W - r + 3) & ~3 : 0);
+                const double* rm = xring + pbase + (side ? sxp * RS + ((W - r + 2) & ~3) : sxm * RS);
                 double* r0 = xring + sx0 * RS + o0;
-                const double* rp = xring + (side ? sxm * RS + ((W - r + 4) & ~3) : sxp * RS);
+                const double* rp = xring + pbase + (side ? sxm * RS + ((W - r + 4) & ~3) : sxp * RS);
                 const double* br = bring + sb * RS + o0;
                 double co[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) co[k] = cosm[side * 10 + k];
-                const double rd = cosm[side * 10 + 8];
+                for (int k = 0; k < 8; ++k) co[k] = cosm[s * 10 + k];
+                const double rd = cosm[s * 10 + 8];
                 const int cmax = n - 1 - rr;
                 const int t3 = wrap(colour - 2 * rr, 3);
                 const int cs = t3 == 0 ? 3 : t3; // first column >= 1 of this colour
+                if constexpr (NPT > 0) {
+                    // NPT points per lane and iteration, branch-free: a lane past the row's end
+                    // recomputes the row's last point of this colour (clamped column) and only its
+                    // store is predicated. Config 3 (8192 faces): one point (32-point granularity on
+                    // the short rows) level 8 1.351 ms against 1.450, level 9 4.83 against 4.70; more
+                    // points per lane are slower (level 9: 4.88, 5.21, 5.62 for 2, 3, 4): the sweep is
+                    // bound by instructions issued, not by the latency of the dependent fp64 chain
+                    const int clast = cmax - (cmax - cs) % 3; // last column of this colour (>= cs when any)
 #pragma unroll 1
-                for (int c = cs + 3 * lane; c <= cmax; c += 192) {
-                    const int c2 = c + 96;
-                    double v[8], w[8];
-                    v[0] = r0[c - 1], v[1] = rp[c - 1], v[2] = rm[c], v[3] = r0[c];
-                    v[4] = rp[c], v[5] = rm[c + 1], v[6] = r0[c + 1], v[7] = br[c];
-                    const bool two = c2 <= cmax;
-                    if (two) {
-                        w[0] = r0[c2 - 1], w[1] = rp[c2 - 1], w[2] = rm[c2], w[3] = r0[c2];
-                        w[4] = rp[c2], w[5] = rm[c2 + 1], w[6] = r0[c2 + 1], w[7] = br[c2];
+                    for (int c = cs + 3 * lane; c <= cmax; c += 96 * NPT) {
+                        double v[NPT][8];
+#pragma unroll
+                        for (int q = 0; q < NPT; ++q) {
+                            const int cq = min(c + 96 * q, clast);
+                            v[q][0] = r0[cq - 1], v[q][1] = rp[cq - 1], v[q][2] = rm[cq], v[q][3] = r0[cq];
+                            v[q][4] = rp[cq], v[q][5] = rm[cq + 1], v[q][6] = r0[cq + 1], v[q][7] = br[cq];
+                        }
+                        double u[NPT];
+#pragma unroll
+                        for (int q = 0; q < NPT; ++q) u[q] = cgs_point_update(v[q], co, rd);
+#pragma unroll
+                        for (int q = 0; q < NPT; ++q)
+                            if (c + 96 * q <= cmax) r0[c + 96 * q] = u[q];
                     }
-                    r0[c] = cgs_point_update(v, co, rd);
-                    if (two) r0[c2] = cgs_point_update(w, co, rd);
+                } else {
+#pragma unroll 1
+                    for (int c = cs + 3 * lane; c <= cmax; c += 192) {
+                        const int c2 = c + 96;
+                        double v[8], w[8];
+                        v[0] = r0[c - 1], v[1] = rp[c - 1], v[2] = rm[c], v[3] = r0[c];
+                        v[4] = rp[c], v[5] = rm[c + 1], v[6] = r0[c + 1], v[7] = br[c];
+                        const bool two = c2 <= cmax;
+                        if (two) {
+                            w[0] = r0[c2 - 1], w[1] = rp[c2 - 1], w[2] = rm[c2], w[3] = r0[c2];
+                            w[4] = rp[c2], w[5] = rm[c2 + 1], w[6] = r0[c2 + 1], w[7] = br[c2];
+                        }
+                        r0[c] = cgs_point_update(v, co, rd);
+                        if (two) r0[c2] = cgs_point_update(w, co, rd);
+                    }
                 }
             }
         }

@@ -939,15 +939,16 @@ bool launch_cgs_cols(const LevelTables& t, const double* b, double* x, double* y
     return nb > 1;
 }
 
-// two faces per CTA (k_cgs_duo): in place
-template <int K, int D, int NMAX, int MINB>
+// two faces (NP pairs of faces) per CTA (k_cgs_duo): in place
+template <int K, int D, int NMAX, int MINB, int NPT = 0, int NP = 1>
 void launch_cgs_duo(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
-    using C = CgdCfg<K, D, NMAX>;
-    static const bool attr = cudaFuncSetAttribute(k_cgs_duo<K, D, NMAX, MINB>,
+    using C = CgdCfg<K, D, NMAX, NP>;
+    static const bool attr = cudaFuncSetAttribute(k_cgs_duo<K, D, NMAX, MINB, NPT, NP>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)) ==
                              cudaSuccess;
     if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
-    pdl_launch(k_cgs_duo<K, D, NMAX, MINB>, unsigned((t.nfaces + 1) / 2), C::THREADS, C::SMEM, st, t, b, x);
+    pdl_launch(k_cgs_duo<K, D, NMAX, MINB, NPT, NP>, unsigned((t.nfaces + 2 * NP - 1) / (2 * NP)), C::THREADS, C::SMEM,
+               st, t, b, x);
 }
 
 template <int NT>
@@ -983,6 +984,8 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
         oop = launch_cgs_cols<2, 2, 256, 4, 1>(t, b, x, y, st);
     } else if (v == 8 && n <= 128) {
         oop = launch_cgs_cols<2, 3, 128, 4, 1>(t, b, x, y, st);
+    } else if (n == 128 && v == 32 && !t.face_list) {
+        launch_cgs_duo<2, 3, 128, 3, 1, 2>(t, b, x, st); // four faces per CTA: 0.558 ms (k_cgs_smem 0.430)
     } else if (n <= 128 && v == 12) {
         // small faces: two warps per face, 8-row blocks through L1/L2 (config 3, 8192 faces: L7
         // 0.67 ms, L6 0.29, L5 0.15; the ring kernel: L7 0.80)
@@ -994,14 +997,23 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
         const size_t smem = size_t(face_rowoff(t.W, t.n)) * 8; // rows 0..n-1
         if (n == 128) launch_cgs_smem<512>(t, b, x, smem, st);
         else launch_cgs_smem<256>(t, b, x, smem, st);
+    } else if (n == 256 && v >= 31 && v <= 33 && !t.face_list) { // measured variants, see below
+        if (v == 31) launch_cgs_duo<2, 3, 256, 3, 0>(t, b, x, st);
+        else if (v == 32) launch_cgs_duo<2, 3, 256, 2, 1, 2>(t, b, x, st);
+        else launch_cgs_duo<2, 3, 256, 2, 0, 2>(t, b, x, st);
+    } else if (n == 512 && v == 31 && !t.face_list) {
+        launch_cgs_duo<2, 3, 512, 2, 1>(t, b, x, st);
     } else if (n == 256 && v != 20 && !t.face_list) {
-        // two faces per CTA (k_cgs_duo), config 3 L8: 1.450 ms per sweep against 1.700 one face per CTA
-        // (HYB_CGS_CFG=20); 4 CTAs per SM (64 registers) 1.598, K = 4 1.548, D = 2 1.636, D = 4 1.452;
-        // at n = 128 the whole-face kernel stays ahead (0.429 ms against 0.670)
-        launch_cgs_duo<2, 3, 256, 3>(t, b, x, st);
+        // two faces per CTA (k_cgs_duo), config 3 L8: 1.351-1.376 ms per sweep with one point per lane
+        // and iteration (branch-free); two points, the second skipped by a branch (HYB_CGS_CFG=31) 1.450;
+        // one face per CTA (k_cgs_cols, HYB_CGS_CFG=20) 1.700; four faces per CTA (two CTAs per SM) 1.622 /
+        // 1.538; 4 CTAs per SM (64 registers) 1.598, K = 4 1.548, D = 2 1.636, D = 4 1.452;
+        // at n = 128 the whole-face kernel stays ahead (0.430 ms against 0.54-0.67)
+        launch_cgs_duo<2, 3, 256, 3, 1>(t, b, x, st);
     } else if (n == 512 && v != 20 && !t.face_list) {
-        // config 3 L9: 4.744 ms per sweep (0.83 of the copy peak) against 5.545; K = 4 (one CTA per SM)
-        // 5.078, D = 2 5.248, K = 3 / D = 1 7.435
+        // config 3 L9: 4.70-4.74 ms per sweep (0.83 of the copy peak) against 5.545 one face per CTA;
+        // one point per lane (HYB_CGS_CFG=31) 4.83, 2 / 3 / 4 points branch-free 4.88 / 5.21 / 5.62;
+        // K = 4 (one CTA per SM) 5.078, D = 2 5.248, K = 3 / D = 1 7.435
         launch_cgs_duo<2, 3, 512, 2>(t, b, x, st);
     } else if (n == 256) {
         // config 3 L8: 4 CTAs per SM (64 registers) 1.705 ms per sweep; 3 CTAs 1.828, D = 2 1.884,

@@ -21,7 +21,7 @@ if timeout 300 python tools/kernels_once.py 10 > "$out/kernels_once.log" 2>&1; t
     python tools/kernels_once.py 10 > "$out/ncu_kernels.log" 2>&1
 fi
 if timeout 300 python tools/smoother_time.py cgs 9 1 > "$out/cgs_once.log" 2>&1; then
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_cgs_cols -s 1 -c 1 -o "$out/cgs_L9" \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_cgs_duo -s 1 -c 1 -o "$out/cgs_L9" \
     python tools/smoother_time.py cgs 9 1 > "$out/ncu_cgs.log" 2>&1
 fi
 # the reports stay on the box; their tables come back (gpurun copies <= 64 MiB)
