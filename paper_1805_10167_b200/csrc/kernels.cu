@@ -1003,6 +1003,8 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
         else launch_cgs_duo<2, 3, 256, 2, 0, 2>(t, b, x, st);
     } else if (n == 512 && v == 31 && !t.face_list) {
         launch_cgs_duo<2, 3, 512, 2, 1>(t, b, x, st);
+    } else if (n == 512 && v == 32 && !t.face_list) {
+        launch_cgs_duo<2, 3, 512, 2, 2>(t, b, x, st);
     } else if (n == 256 && v != 20 && !t.face_list) {
         // two faces per CTA (k_cgs_duo), config 3 L8: 1.351-1.376 ms per sweep with one point per lane
         // and iteration (branch-free); two points, the second skipped by a branch (HYB_CGS_CFG=31) 1.450;
