@@ -475,7 +475,8 @@ def cfg3_leg(c: Ctx):
     rhs, x = H.ScalarFunction("rhs", dom, 0, L), H.ScalarFunction("x", dom, 0, L)
     H.interpolate_random(rhs, L, seed=2, flag_mask=H.INNER)
     mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="colored_gs", coarse_tol=1e-12)
-    mg.vcycle(rhs, x, L, 3, 3)
+    for _ in range(3):  # warm-up: eager (allocations, plans), graph capture, first replay
+        mg.vcycle(rhs, x, L, 3, 3)
     H.interpolate(x, 0.0, L)
     # the 5 cycles alone (the 240 B/DoF roofline is a cycle's), then the solve with its residual history
     _, ms, clk = c.timed(dom, lambda: [mg.vcycle(rhs, x, L, 3, 3) for _ in range(5)])

@@ -286,7 +286,9 @@ int hyb_smooth_jacobi(hyb_operator* A, hyb_function* rhs, hyb_function* x, doubl
  * instead of 48 bytes per DoF at the face interiors); measured issue-bound and
  * slower than two sweeps on B200, so the knob defaults to off. */
 int hyb_smooth_jacobi2(hyb_operator* A, hyb_function* rhs, hyb_function* x, double omega, int level);
-/* measurement knobs: "jacobi2_min_n", "cgs_pair_min_n", "cgs_prolong_fused", "mega_dofs_per_cta"
+/* measurement knobs: "jacobi2_min_n", "cgs_pair_min_n", "cgs_prolong_fused", "mega_dofs_per_cta",
+ * "cgs_zero_sweep" (default 1: a coloured-GS correction's first sweep starts from x = 0 without the
+ * fill, the ghost refresh and the read of x; 0: fill and sweep -- bitwise the same)
  * (value < 0: query only; *previous = old value) */
 int hyb_tuning(const char* name, int64_t value, int64_t* previous);
 /* smooth_gs(A, ctl, rhs, x, level): hybrid Gauss-Seidel, lexicographic inside

@@ -911,6 +911,9 @@ int hyb_tuning(const char* name, int64_t value, int64_t* previous) {
         } else if (k == "cgs_prolong_fused") {
             if (previous) *previous = hyb::cgs_prolong_fused() ? 1 : 0;
             if (value >= 0) hyb::set_cgs_prolong_fused(value != 0);
+        } else if (k == "cgs_zero_sweep") {
+            if (previous) *previous = hyb::cgs_zero_sweep() ? 1 : 0;
+            if (value >= 0) hyb::set_cgs_zero_sweep(value != 0);
         } else if (k == "cgs_pair_min_n") {
             if (previous) *previous = hyb::cgs_pair_min_n();
             if (value >= 0) hyb::set_cgs_pair_min_n(int(std::min<int64_t>(value, int64_t(1) << 30)));

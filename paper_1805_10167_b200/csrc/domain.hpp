@@ -351,6 +351,10 @@ void smooth_gs(const Operator& A, Function& rhs, Function& x, int level);
 void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level);
 void smooth_cgs_n(const Operator& A, Function& rhs, Function& x, int level, int count);
 void prolongate_add_cgs(const Operator& A, Function& e, Function& rhs, Function& x, int lc);
+/// the first coloured sweep of a coarse-grid correction from x = 0 without fill, refresh or read of x
+bool smooth_cgs_zero(const Operator& A, Function& rhs, Function& x, int level);
+bool cgs_zero_sweep();
+void set_cgs_zero_sweep(bool on);
 bool cgs_prolong_fused();
 void set_cgs_prolong_fused(bool on);
 int cgs_pair_min_n();

@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(128) k_gs_ev(LevelTables t, FlagTables fl, con
 // 1..n-2 go back with bulk stores. Same operands and term order as the
 // in-place sweep: bitwise og_cgs.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_cgs_smem(LevelTables t, const double* __restrict__ b, double* x) {
+__global__ void __launch_bounds__(NT) k_cgs_smem(LevelTables t, const double* __restrict__ b, double* x, int zero) {
     pdl_prologue();
     extern __shared__ __align__(128) double cs_face[];
     __shared__ int64_t ro[130];
@@ -539,10 +539,14 @@ __global__ void __launch_bounds__(NT) k_cgs_smem(LevelTables t, const double* __
     const int n = t.n;
     const int64_t base = int64_t(blockIdx.x) * t.face_stride;
     constexpr uint32_t CHUNK = 32768;
+    if (zero) { // the sweep starts from x = 0: nothing to load
+        const int cnt = int(face_rowoff(t.W, n));
+        for (int i = threadIdx.x; i < cnt; i += NT) cs_face[i] = 0.0;
+    }
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         fence_mbar_init();
-        const uint32_t bytes = uint32_t(face_rowoff(t.W, n)) * 8u; // rows 0..n-1
+        const uint32_t bytes = zero ? 0u : uint32_t(face_rowoff(t.W, n)) * 8u; // rows 0..n-1
         mbar_arrive_expect_tx(&bar, bytes);
         for (uint32_t o = 0; o < bytes; o += CHUNK)
             bulk_g2s(reinterpret_cast<char*>(cs_face) + o, reinterpret_cast<const char*>(x + base) + o,
@@ -854,7 +858,9 @@ __global__ void __launch_bounds__(CgcCfg<K, D, CB, WPR, PRO>::THREADS, MINB)
 // bitwise og_cgs. Lanes 0 and 1 of the two producer warps serve faces A and B
 // (x loads + write-back, b loads); the last CTA of an odd face count runs A
 // alone. The 7+1 coefficients and 1/diag of both faces sit in shared memory
-// (registers hold one face's at a time).
+// (registers hold one face's at a time). With zsrc set the x rows are not read: every ring
+// row is loaded from a row of zeros (the first sweep of a coarse-grid correction, whose
+// iterate is zero on entry -- faces, ghosts and all), bitwise the sweep of a zero-filled x.
 template <int K, int D, int NMAX, int NP = 1> struct CgdCfg {
     static constexpr int RX = D * K + 3 * K + 3; // x ring rows (see k_cgs_tma)
     static constexpr int RB = D * K + 2 * K + 2; // b ring rows
@@ -871,7 +877,7 @@ template <int K, int D, int NMAX, int NP = 1> struct CgdCfg {
 // iteration, the second skipped by a branch; NPT >= 1: NPT points, branch-free (see below).
 template <int K, int D, int NMAX, int MINB, int NPT = 0, int NP = 1>
 __global__ void __launch_bounds__(CgdCfg<K, D, NMAX, NP>::THREADS, MINB)
-    k_cgs_duo(LevelTables t, const double* __restrict__ b, double* x) {
+    k_cgs_duo(LevelTables t, const double* __restrict__ b, double* x, const double* __restrict__ zsrc) {
     pdl_prologue();
     using C = CgdCfg<K, D, NMAX, NP>;
     extern __shared__ __align__(16) double cd_ring[];
@@ -919,8 +925,9 @@ __global__ void __launch_bounds__(CgdCfg<K, D, NMAX, NP>::THREADS, MINB)
                 for (int q = q_next; q <= qhi; ++q) bytes += nbytes(q);
                 mbar_arrive_expect_tx(&full[s_ % NB], bytes);
                 for (; q_next <= qhi; ++q_next) {
-                    bulk_g2s(xring + size_t(slot_next) * RS + off(q_next), xf + ro[real(q_next)], nbytes(q_next),
-                             &full[s_ % NB]);
+                    // zsrc: the sweep starts from x = 0 (a row of zeros stands in for every x row)
+                    bulk_g2s(xring + size_t(slot_next) * RS + off(q_next), zsrc ? zsrc : xf + ro[real(q_next)],
+                             nbytes(q_next), &full[s_ % NB]);
                     slot_next = slot_next + 1 == RX ? 0 : slot_next + 1;
                 }
             };

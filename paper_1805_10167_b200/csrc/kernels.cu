@@ -941,22 +941,22 @@ bool launch_cgs_cols(const LevelTables& t, const double* b, double* x, double* y
 
 // two faces (NP pairs of faces) per CTA (k_cgs_duo): in place
 template <int K, int D, int NMAX, int MINB, int NPT = 0, int NP = 1>
-void launch_cgs_duo(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
+void launch_cgs_duo(const LevelTables& t, const double* b, double* x, cudaStream_t st, const double* zsrc = nullptr) {
     using C = CgdCfg<K, D, NMAX, NP>;
     static const bool attr = cudaFuncSetAttribute(k_cgs_duo<K, D, NMAX, MINB, NPT, NP>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)) ==
                              cudaSuccess;
     if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
     pdl_launch(k_cgs_duo<K, D, NMAX, MINB, NPT, NP>, unsigned((t.nfaces + 2 * NP - 1) / (2 * NP)), C::THREADS, C::SMEM,
-               st, t, b, x);
+               st, t, b, x, zsrc);
 }
 
 template <int NT>
-void launch_cgs_smem(const LevelTables& t, const double* b, double* x, size_t smem, cudaStream_t st) {
+void launch_cgs_smem(const LevelTables& t, const double* b, double* x, size_t smem, cudaStream_t st, int zero = 0) {
     static const bool attr =
         cudaFuncSetAttribute(k_cgs_smem<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024) == cudaSuccess;
     if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
-    pdl_launch(k_cgs_smem<NT>, unsigned(t.nfaces), NT, smem, st, t, b, x);
+    pdl_launch(k_cgs_smem<NT>, unsigned(t.nfaces), NT, smem, st, t, b, x, zero);
 }
 
 // tuning knob for measurements (HYB_CGS_CFG); the default is the measured best
@@ -996,7 +996,9 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
         // L5 0.099 vs 0.119; V(3,3) cycle 76.7 -> 75.9 ms
         const size_t smem = size_t(face_rowoff(t.W, t.n)) * 8; // rows 0..n-1
         if (n == 128) launch_cgs_smem<512>(t, b, x, smem, st);
-        else launch_cgs_smem<256>(t, b, x, smem, st);
+        else if (n == 64 || v == 41) launch_cgs_smem<256>(t, b, x, smem, st);
+        else if (n == 32 || v == 42) launch_cgs_smem<128>(t, b, x, smem, st);
+        else launch_cgs_smem<64>(t, b, x, smem, st);
     } else if (n == 256 && v >= 31 && v <= 33 && !t.face_list) { // measured variants, see below
         if (v == 31) launch_cgs_duo<2, 3, 256, 3, 0>(t, b, x, st);
         else if (v == 32) launch_cgs_duo<2, 3, 256, 2, 1, 2>(t, b, x, st);
@@ -1031,6 +1033,35 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
     }
     check_launch("coloured gauss-seidel faces (column blocks)");
     return oop;
+}
+
+// a row of zeros for sweeps that start from x = 0 (k_cgs_duo's zsrc)
+__device__ __align__(128) double g_zero_row[1056];
+
+bool cgs_zero_supported(const LevelTables& t) {
+    return t.nfaces > 0 && t.n >= 4 && t.n <= 512 && !t.face_list && cgs_cfg() == 0;
+}
+
+// the coloured face sweep of x = 0 (x's face blocks are not read; rows 1..n-2 are written)
+void launch_cgs_faces_zero(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
+    if (!cgs_zero_supported(t)) throw CudaError("coloured gauss-seidel from zero: unsupported face size");
+    const int n = t.n;
+    if (n <= 128) {
+        const size_t smem = size_t(face_rowoff(t.W, t.n)) * 8;
+        if (n == 128) launch_cgs_smem<512>(t, b, x, smem, st, 1);
+        else if (n == 64) launch_cgs_smem<256>(t, b, x, smem, st, 1);
+        else if (n == 32) launch_cgs_smem<128>(t, b, x, smem, st, 1);
+        else launch_cgs_smem<64>(t, b, x, smem, st, 1);
+    } else {
+        static const double* zrow = [] {
+            void* p = nullptr;
+            if (cudaGetSymbolAddress(&p, g_zero_row) != cudaSuccess) throw CudaError("coloured gauss-seidel: no zero row");
+            return static_cast<const double*>(p);
+        }();
+        if (n == 256) launch_cgs_duo<2, 3, 256, 3, 1>(t, b, x, st, zrow);
+        else launch_cgs_duo<2, 3, 512, 2>(t, b, x, st, zrow);
+    }
+    check_launch("coloured gauss-seidel faces (from zero)");
 }
 
 // prolongate(add) + one coloured sweep, fused on the faces (k_cgs_cols<PRO>): 256-column

@@ -162,6 +162,9 @@ void launch_gather_split(const void* dst, const void* src, bool idx32, int64_t n
 // column-blocked faces (k_cgs_cols): in place when a face is one block, else
 // out of place into y (returns true); bitwise the in-place sweep either way
 bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, double* y, cudaStream_t st);
+// one coloured face sweep of x = 0 without reading x's face blocks (n <= 512, full launches)
+bool cgs_zero_supported(const LevelTables& t);
+void launch_cgs_faces_zero(const LevelTables& t, const double* b, double* x, cudaStream_t st);
 void launch_cgs_ev_oop(const LevelTables& t, const FlagTables& fl, const double* b, const double* x, double* y,
                        cudaStream_t st);
 // dst := alpha*x1 + beta*x2 (op 0), dst += alpha*x1 (op 1), dst := alpha (op 2)

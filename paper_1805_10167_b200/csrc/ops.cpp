@@ -379,6 +379,39 @@ static bool cgs_pair_usable(const Operator& A, Function& x, int level) {
     return X.ntotal == X.nlocal;
 }
 
+// One coloured sweep of x = 0 (a coarse-grid correction's first pre-smoothing sweep: the
+// iterate and every ghost of it are zero on entry, and its Dirichlet rows -- x := rhs -- are
+// zero because the cycle zeroes the coarse rhs there). x's face blocks are neither filled
+// nor read (the face kernels sweep rows of zeros and write rows 1..n-2), the edge/vertex
+// part of the arena, halos included, is zeroed with one memset, and no ghost refresh is
+// needed: bitwise fill_const(x, 0) + smooth_cgs. Face rows 0, n-1 and n hold only ghosts;
+// the next operation's refresh rewrites them. False where no variant exists (the caller
+// then fills and sweeps).
+bool g_cgs_zero_sweep = true; // hyb_tuning("cgs_zero_sweep", 0) fills and sweeps instead
+bool cgs_zero_sweep() { return g_cgs_zero_sweep; }
+void set_cgs_zero_sweep(bool on) { g_cgs_zero_sweep = on; }
+
+bool smooth_cgs_zero(const Operator& A, Function& rhs, Function& x, int level) {
+    check_op_function(A, rhs, level, "smooth_cgs", true);
+    check_op_function(A, x, level, "smooth_cgs", true);
+    if (&rhs == &x) throw InvalidArgument("smooth_cgs: rhs and x must be distinct functions");
+    require_p1(x, "smooth_cgs");
+    const LevelTables t = A.tables(level);
+    if (!cgs_zero_supported(t) || (1 << level) >= cgs_pair_min_n()) return false;
+    check_diagonals(A, x, level, "smooth_cgs");
+    Domain& d = A.domain();
+    double* xa = x.data(level);
+    if (t.arena_size > t.faces_size)
+        HYB_CUDA(cudaMemsetAsync(xa + t.faces_size, 0, size_t(t.arena_size - t.faces_size) * 8, d.stream()));
+    d.timer_begin("coloured_gs");
+    launch_cgs_faces_zero(t, rhs.data(level), xa, d.stream());
+    d.timer_end();
+    d.fork();
+    launch_cgs_ev(t, x.flags(), rhs.data(level), xa, d.aux_stream());
+    d.join();
+    return true;
+}
+
 void smooth_cgs_n(const Operator& A, Function& rhs, Function& x, int level, int count) {
     if (count < 0) throw InvalidArgument("smooth_cgs: negative sweep count");
     check_op_function(A, rhs, level, "smooth_cgs", true);
@@ -1044,8 +1077,14 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
         return;
     }
     const bool zero_sweep = x_zero && level > a_.min_level() && nu_pre > 0 && smoother_ == SMOOTH_JACOBI;
-    if (x_zero && !zero_sweep) fill_const(x, 0.0, level, ALL_FLAGS);
-    if (!zero_sweep) assign(1.0, rhs, 0.0, rhs, x, level, kDirichletMask);
+    // coloured GS: the first sweep of a correction (x = 0, Dirichlet rows of the coarse rhs
+    // zeroed by the caller below) without the fill, the ghost refresh and the read of x
+    int cgs_done = 0;
+    if (x_zero && &rhs == &b_ && &x == &e_ && level > a_.min_level() && nu_pre > 0 && smoother_ == SMOOTH_CGS &&
+        cgs_zero_sweep() && smooth_cgs_zero(a_, rhs, x, level))
+        cgs_done = 1;
+    if (x_zero && !zero_sweep && !cgs_done) fill_const(x, 0.0, level, ALL_FLAGS);
+    if (!zero_sweep && !cgs_done) assign(1.0, rhs, 0.0, rhs, x, level, kDirichletMask);
     if (level == a_.min_level()) {
         coarse_correct(rhs, x);
         return;
@@ -1059,7 +1098,7 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
     if (pair) {
         smooth_jacobi2(a_, rhs, x, omega_, level);
     } else {
-        if (smoother_ == SMOOTH_CGS) smooth_cgs_n(a_, rhs, x, level, nu_pre);
+        if (smoother_ == SMOOTH_CGS) smooth_cgs_n(a_, rhs, x, level, nu_pre - cgs_done);
         else
             for (int i = 0; i < nu_pre; ++i) {
                 if (i == 0 && zero_sweep) smooth_jacobi_zero(a_, rhs, x, omega_, level);

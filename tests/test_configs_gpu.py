@@ -114,6 +114,32 @@ def test_colored_gs_two_faces_per_cta(ranks):
                 assert np.array_equal(x.download(level), o.get(1, level)), (ranks, level, sweep)
 
 
+@pytest.mark.parametrize("mesh_name,L", [("annulus", 9), ("square", 10), ("ring8", 7)])
+def test_colored_gs_zero_sweep_bitwise(mesh_name, L):
+    """A correction's first coloured sweep from x = 0 (no fill, no ghost refresh, x's face blocks not
+    read: k_cgs_smem / k_cgs_duo fed with zeros) against fill + sweep: V(2,1) and V(1,2) cycles bitwise,
+    with coarse faces of n = 512 (top level 10), 256 (9) and <= 128 (7)."""
+    mesh = cfg3_mesh(4, 2) if mesh_name == "annulus" else FIXTURES[mesh_name]()
+    got = []
+    for knob in (1, 0):
+        prev = H.tuning("cgs_zero_sweep", knob)
+        try:
+            dom = H.DistributedDomain(mesh, 2 if mesh_name != "square" else 1)
+            ctl = H.Controller(dom)
+            rhs, x = H.ScalarFunction("rhs", dom, 0, L), H.ScalarFunction("x", dom, 0, L)
+            b = keyed_uniform(mesh, L, seed=81)
+            b[rhs.flags(L) != H.INNER] = 0.0
+            rhs.upload(L, b)
+            mg = H.GridHierarchy(dom, ctl, H.LAPLACE, 0, L, smoother="colored_gs", coarse_tol=1e-12)
+            mg.vcycle(rhs, x, L, 2, 1)
+            mg.vcycle(rhs, x, L, 1, 2)
+            got.append(x.download(L))
+        finally:
+            H.tuning("cgs_zero_sweep", prev)
+    assert np.array_equal(got[0], got[1])
+    assert np.abs(got[0]).max() > 0
+
+
 def test_cfg3_reduced_vcycle_history():
     """Config 3 shape at reduced size: perturbed annulus(32, 8) levels 5 -> 0,
     V(3,3) coloured GS, rhs U[-1,1] (seed 2) on INNER, x0 = 0, 5 cycles."""

@@ -1,5 +1,6 @@
 """Time the fused prolongate-add + Jacobi (hyb_prolongate_add_jacobi) and a plain Jacobi sweep at
-level L on the config-2 mesh (CUDA events, after a warm-up)."""
+level L on the config-2 mesh, or with a second argument cfg3 on config 3's perturbed annulus (CUDA
+events, after a warm-up)."""
 import os
 import sys
 
@@ -7,7 +8,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1805_10167_b200 import hytegrid as H  # noqa: E402
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-dom = H.DistributedDomain(H.meshgen.channel(16, 16), 1)
+which = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
+mesh = (H.meshgen.perturb(H.meshgen.annulus(128, 32, 1.0, 2.0), 0.1, 2) if which == "cfg3"
+        else H.meshgen.channel(16, 16))
+dom = H.DistributedDomain(mesh, 1)
 ctl = H.Controller(dom)
 A = H.StencilOperator(dom, H.LAPLACE, L - 1, L)
 x, b = H.ScalarFunction("x", dom, L, L), H.ScalarFunction("b", dom, L, L)
