@@ -995,6 +995,10 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
         // kernel per sweep against the row-block kernel: L7 0.429 vs 0.555 ms, L6 0.183 vs 0.243,
         // L5 0.099 vs 0.119; V(3,3) cycle 76.7 -> 75.9 ms
         const size_t smem = size_t(face_rowoff(t.W, t.n)) * 8; // rows 0..n-1
+        // CTA sizes per face size, config 3 per sweep: n = 128 with 512 threads 0.429 ms (256: 0.588,
+        // 1024: 0.637); n = 64 with 256 threads 0.179 (128: 0.177, 512: 0.193); n = 32 with 128 threads
+        // 0.089 (256: 0.099); n = 16 / 8 / 4 with 64 threads 0.047 / 0.026 / 0.018 (256: 0.056 / 0.037 /
+        // 0.033)
         if (n == 128) launch_cgs_smem<512>(t, b, x, smem, st);
         else if (n == 64 || v == 41) launch_cgs_smem<256>(t, b, x, smem, st);
         else if (n == 32 || v == 42) launch_cgs_smem<128>(t, b, x, smem, st);
