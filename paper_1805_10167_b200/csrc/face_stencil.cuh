@@ -263,10 +263,22 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     double sl = 0, s0 = 0, s1 = 0, hl = 0, h0 = 0, h1 = 0;
     const int nc = n / 2;
     const int C = c / 2; // coarse column of this lane (RR, JP)
+    // JP: columns c-1 .. c+2 take the correction where 2 <= column <= lim(row): a column below 2 never does
+    constexpr int JP_NEVER = 0x7fffffff;
+    const int jp_e0 = c - 1 >= 2 ? c - 1 : JP_NEVER, jp_e1 = c >= 2 ? c : JP_NEVER;
+    const int jp_e2 = c + 1 >= 2 ? c + 1 : JP_NEVER, jp_e3 = c + 2 >= 2 ? c + 2 : JP_NEVER;
 
     // optional dot partials (dotp): APPLY x.(Ax), JACOBI b.x_new, per lane for
     // its two columns over the band's rows, then a fixed tree over the CTA
     double d0 = 0.0, d1 = 0.0;
+    // the fused restriction's loop unrolled by 6 (its row window and residual rows rotate with period
+    // 3, its row parity with period 2): config 2 L10 879 -> 858 us, config 3 L9 3.98 -> 3.87 ms, L8
+    // 1.34 -> 1.29; the fused prolongation got slower unrolled (L10 1.37 -> 1.47 ms) and stays rolled.
+    // Rotating three row structs through three instantiations of the stage body (no register moves at
+    // all) was measured too: apply 687 -> 699 us, the fused restriction 877, the fused prolongation 1.34
+    // ms against 1.30, Jacobi on config 3's faces 4.10 -> 4.26 ms -- not kept
+    constexpr int UNR = RR ? 6 : 1;
+#pragma unroll UNR
     for (int i = 0; i < nstage; ++i) {
         const int s = i % NS;
         mbar_wait(&sm.full[s], (i / NS) & 1);
@@ -306,10 +318,10 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
             }
             // points two or more away from every border take the correction here
             const int lim = q >= 2 ? n - 2 - q : -1; // deep columns 2 .. lim
-            pl = (c - 1 >= 2 && c - 1 <= lim) ? pl + vl : pl;
-            p0 = (c >= 2 && c <= lim) ? p0 + v0 : p0;
-            p1 = (c + 1 >= 2 && c + 1 <= lim) ? p1 + v1 : p1;
-            pr = (c + 2 >= 2 && c + 2 <= lim) ? pr + vr : pr;
+            if (jp_e0 <= lim) pl = pl + vl; // (the columns' lower bound is folded into jp_e*)
+            if (jp_e1 <= lim) p0 = p0 + v0;
+            if (jp_e2 <= lim) p1 = p1 + v1;
+            if (jp_e3 <= lim) pr = pr + vr;
         }
         if (RR && i >= 2) {
             // residual of fine row q at c, c+1, same operations as
