@@ -277,7 +277,9 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     // Rotating three row structs through three instantiations of the stage body (no register moves at
     // all) was measured too: apply 687 -> 699 us, the fused restriction 877, the fused prolongation 1.34
     // ms against 1.30, Jacobi on config 3's faces 4.10 -> 4.26 ms -- not kept
-    constexpr int UNR = RR ? 6 : 1;
+    // the other modes: by 2, the compiler's own choice when left alone (rolled, apply ran 687 -> 693 us);
+    // the fused prolongation rolled (1.30 ms; by 2: more registers)
+    constexpr int UNR = RR ? 6 : (JP ? 1 : 2);
 #pragma unroll UNR
     for (int i = 0; i < nstage; ++i) {
         const int s = i % NS;

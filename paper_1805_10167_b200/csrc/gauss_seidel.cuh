@@ -530,8 +530,15 @@ __global__ void __launch_bounds__(128) k_gs_ev(LevelTables t, FlagTables fl, con
 // colour is one parallel step; b is read from L2, each value once), and rows
 // 1..n-2 go back with bulk stores. Same operands and term order as the
 // in-place sweep: bitwise og_cgs.
+// tab (optional): the face's interior points by colour, {position in the face block, row strides
+// (r+1 in the high half, r-1 in the low half)}, cnt.x / .y / .z points of colour 0 / 1 / 2: a thread
+// per point instead of a warp per row. Rows of a small face hold few points of one colour (42 at most
+// at n = 128, 10 at n = 32), so the row loop leaves most lanes idle (54% of the lane slots used at
+// n = 128, a third at n = 64) and the sweep is bound by instructions issued; any order inside a
+// colour gives the same values.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_cgs_smem(LevelTables t, const double* __restrict__ b, double* x, int zero) {
+__global__ void __launch_bounds__(NT) k_cgs_smem(LevelTables t, const double* __restrict__ b, double* x, int zero,
+                                                 const int2* __restrict__ tab, int3 cnt) {
     pdl_prologue();
     extern __shared__ __align__(128) double cs_face[];
     __shared__ int64_t ro[130];
@@ -565,6 +572,27 @@ __global__ void __launch_bounds__(NT) k_cgs_smem(LevelTables t, const double* __
     constexpr int NW = NT / 32;
     __syncthreads(); // ro[] and the barrier's initialisation
     mbar_wait(&bar, 0);
+    if (tab) {
+        int first = 0;
+#pragma unroll 1
+        for (int colour = 0; colour < 3; ++colour) {
+            const int count = colour == 0 ? cnt.x : (colour == 1 ? cnt.y : cnt.z);
+#pragma unroll 1
+            for (int i = threadIdx.x; i < count; i += NT) {
+                const int2 e = __ldg(tab + first + i);
+                const int up = e.y >> 16, dn = e.y & 0xffff;
+                double* r0 = cs_face + e.x;
+                const double* rm = r0 - dn;
+                const double* rp = r0 + up;
+                double v[8];
+                v[0] = r0[-1], v[1] = rp[-1], v[2] = rm[0], v[3] = r0[0];
+                v[4] = rp[0], v[5] = rm[1], v[6] = r0[1], v[7] = __ldg(bf + e.x);
+                r0[0] = cgs_point_update(v, co, rd);
+            }
+            first += count;
+            __syncthreads();
+        }
+    } else
 #pragma unroll 1
     for (int colour = 0; colour < 3; ++colour) {
 #pragma unroll 1

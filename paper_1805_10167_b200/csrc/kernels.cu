@@ -16,6 +16,10 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <vector>
 
 namespace hyb {
 
@@ -951,14 +955,6 @@ void launch_cgs_duo(const LevelTables& t, const double* b, double* x, cudaStream
                st, t, b, x, zsrc);
 }
 
-template <int NT>
-void launch_cgs_smem(const LevelTables& t, const double* b, double* x, size_t smem, cudaStream_t st, int zero = 0) {
-    static const bool attr =
-        cudaFuncSetAttribute(k_cgs_smem<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024) == cudaSuccess;
-    if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
-    pdl_launch(k_cgs_smem<NT>, unsigned(t.nfaces), NT, smem, st, t, b, x, zero);
-}
-
 // tuning knob for measurements (HYB_CGS_CFG); the default is the measured best
 static int cgs_cfg() {
     static const int v = [] {
@@ -966,6 +962,58 @@ static int cgs_cfg() {
         return e ? std::atoi(e) : 0;
     }();
     return v;
+}
+
+// the per-colour point table of a face of size n (k_cgs_smem's tab), built once per size and kept
+struct CgsPointTable {
+    int2* dev = nullptr;
+    int3 cnt{0, 0, 0};
+};
+static const CgsPointTable& cgs_point_table(int n, int W, cudaStream_t st) {
+    static std::map<int, CgsPointTable> cache;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(n);
+    if (it != cache.end()) return it->second;
+    std::vector<int2> host;
+    CgsPointTable tb;
+    int counts[3] = {0, 0, 0};
+    for (int colour = 0; colour < 3; ++colour)
+        for (int r = 1; r <= n - 2; ++r) {
+            const int up = int(face_rowoff(W, r + 1) - face_rowoff(W, r));
+            const int dn = int(face_rowoff(W, r) - face_rowoff(W, r - 1));
+            for (int c = 1; c <= n - 1 - r; ++c)
+                if ((c + 2 * r) % 3 == colour) {
+                    host.push_back(make_int2(int(face_rowoff(W, r)) + c, (up << 16) | dn));
+                    ++counts[colour];
+                }
+        }
+    tb.cnt = make_int3(counts[0], counts[1], counts[2]);
+    if (cudaMalloc(&tb.dev, std::max<size_t>(host.size(), 1) * sizeof(int2)) != cudaSuccess)
+        throw CudaError("coloured gauss-seidel: cannot allocate the point table");
+    if (!host.empty()) {
+        // a blocking copy (pageable source): the table must not depend on `host` after return; a
+        // stream being captured cannot take it, so the caller builds the tables before any capture
+        if (cudaMemcpy(tb.dev, host.data(), host.size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess)
+            throw CudaError("coloured gauss-seidel: cannot upload the point table");
+    }
+    (void)st;
+    return cache.emplace(n, tb).first->second;
+}
+
+template <int NT>
+void launch_cgs_smem(const LevelTables& t, const double* b, double* x, size_t smem, cudaStream_t st, int zero = 0) {
+    static const bool attr =
+        cudaFuncSetAttribute(k_cgs_smem<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024) == cudaSuccess;
+    if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
+    const int2* tab = nullptr;
+    int3 cnt = make_int3(0, 0, 0);
+    if (cgs_cfg() != 47) { // HYB_CGS_CFG=47: the row loop
+        const CgsPointTable& tb = cgs_point_table(t.n, t.W, st);
+        tab = tb.dev;
+        cnt = tb.cnt;
+    }
+    pdl_launch(k_cgs_smem<NT>, unsigned(t.nfaces), NT, smem, st, t, b, x, zero, tab, cnt);
 }
 
 // coloured face sweep: true if the faces went out of place into y
