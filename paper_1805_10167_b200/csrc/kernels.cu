@@ -970,10 +970,13 @@ struct CgsPointTable {
     int3 cnt{0, 0, 0};
 };
 static const CgsPointTable& cgs_point_table(int n, int W, cudaStream_t st) {
-    static std::map<int, CgsPointTable> cache;
+    static std::map<std::pair<int, int>, CgsPointTable> cache; // (device, n)
     static std::mutex mu;
     std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find(n);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::pair<int, int> key(dev, n);
+    auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     std::vector<int2> host;
     CgsPointTable tb;
@@ -998,7 +1001,7 @@ static const CgsPointTable& cgs_point_table(int n, int W, cudaStream_t st) {
             throw CudaError("coloured gauss-seidel: cannot upload the point table");
     }
     (void)st;
-    return cache.emplace(n, tb).first->second;
+    return cache.emplace(key, tb).first->second;
 }
 
 template <int NT>
@@ -1091,13 +1094,13 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
 // a row of zeros for sweeps that start from x = 0 (k_cgs_duo's zsrc)
 __device__ __align__(128) double g_zero_row[1056];
 
-bool cgs_zero_supported(const LevelTables& t) {
-    return t.nfaces > 0 && t.n >= 4 && t.n <= 512 && !t.face_list && cgs_cfg() == 0;
-}
+// (a property of the level, not of this process's share of it: every process takes the same path)
+bool cgs_zero_supported(const LevelTables& t) { return t.n >= 4 && t.n <= 512 && !t.face_list && cgs_cfg() == 0; }
 
 // the coloured face sweep of x = 0 (x's face blocks are not read; rows 1..n-2 are written)
 void launch_cgs_faces_zero(const LevelTables& t, const double* b, double* x, cudaStream_t st) {
     if (!cgs_zero_supported(t)) throw CudaError("coloured gauss-seidel from zero: unsupported face size");
+    if (t.nfaces <= 0) return;
     const int n = t.n;
     if (n <= 128) {
         const size_t smem = size_t(face_rowoff(t.W, t.n)) * 8;
@@ -1106,11 +1109,9 @@ void launch_cgs_faces_zero(const LevelTables& t, const double* b, double* x, cud
         else if (n == 32) launch_cgs_smem<128>(t, b, x, smem, st, 1);
         else launch_cgs_smem<64>(t, b, x, smem, st, 1);
     } else {
-        static const double* zrow = [] {
-            void* p = nullptr;
-            if (cudaGetSymbolAddress(&p, g_zero_row) != cudaSuccess) throw CudaError("coloured gauss-seidel: no zero row");
-            return static_cast<const double*>(p);
-        }();
+        void* zp = nullptr; // (the symbol's address on the current device)
+        if (cudaGetSymbolAddress(&zp, g_zero_row) != cudaSuccess) throw CudaError("coloured gauss-seidel: no zero row");
+        const double* zrow = static_cast<const double*>(zp);
         if (n == 256) launch_cgs_duo<2, 3, 256, 3, 1>(t, b, x, st, zrow);
         else launch_cgs_duo<2, 3, 512, 2>(t, b, x, st, zrow);
     }
