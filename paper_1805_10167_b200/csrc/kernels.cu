@@ -1839,6 +1839,54 @@ void launch_coarse_gather(int64_t nloc, const int64_t* gidx, const int64_t* pos,
     check_launch("coarse gather");
 }
 
+// A grid barrier with one atomic on the critical path (k_coarse_cg_reg, whose iteration is two
+// barriers and little else): arrivals count up for the whole launch in cnt and barrier k is passed
+// once cnt reaches (k + 1) gridDim.x -- no reset between barriers, so the last arrival's atomic
+// releases everyone (grid_barrier: arrive, reset, bump the generation, three dependent L2 round
+// trips). The words are zero at launch: after its last barrier every CTA checks out through `out`,
+// and the last one to do so zeroes both (everyone has left the polling loops by then).
+struct CountingGridSync {
+    unsigned* cnt;
+    unsigned* out;
+    unsigned k = 0;
+    __device__ __forceinline__ void sync() {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(cnt, 1u);
+            const unsigned target = (k + 1u) * gridDim.x;
+            unsigned seen;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+            } while (seen < target);
+            __threadfence();
+        }
+        ++k;
+        __syncthreads();
+    }
+    __device__ __forceinline__ void finish() {
+        if (threadIdx.x == 0 && atomicAdd(out, 1u) == gridDim.x - 1) {
+            atomicExch(cnt, 0u);
+            atomicExch(out, 0u);
+        }
+    }
+};
+
+__device__ double2 grid_sum2(double2 s, double* red, double* part, CountingGridSync& gs) {
+    const double2 bsum = block_sum2(s, red);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = bsum.x;
+        part[2 * blockIdx.x + 1] = bsum.y;
+    }
+    gs.sync();
+    double2 t = make_double2(0.0, 0.0);
+    for (int i = threadIdx.x; i < int(gridDim.x); i += CGG_THREADS) {
+        t.x += __ldcg(part + 2 * i);
+        t.y += __ldcg(part + 2 * i + 1);
+    }
+    return block_sum2(t, red);
+}
+
 // Register-resident variant (at most one row per thread, at most NZ entries
 // per row): the row's matrix entries and its x, r, p, s = Ap, w = Ar stay in
 // registers for the whole solve; per iteration r is exchanged through L2 for
@@ -1855,6 +1903,7 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const 
                                                                double* part, unsigned* bar) {
     pdl_prologue();
     __shared__ double red[66];
+    CountingGridSync gs{bar + 4, bar + 5}; // (words 0 and 1 are grid_barrier's)
     const int64_t i = blockIdx.x * int64_t(CGG_THREADS) + threadIdx.x;
     const bool own = i < n;
     double* part0 = part;                  // 2 x gridDim.x
@@ -1889,14 +1938,14 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const 
     if (own) R[i] = ri;
     double2 sb = make_double2(0.0, 0.0);
     if (own) sb.x += bi * bi;
-    const double target = tol * sqrt(grid_sum2(sb, red, part0, bar).x); // also publishes R
+    const double target = tol * sqrt(grid_sum2(sb, red, part0, gs).x); // also publishes R
     double wi = spmv(R);
     double2 gd = make_double2(0.0, 0.0);
     if (own) {
         gd.x += ri * ri;
         gd.y += wi * ri;
     }
-    double2 g = grid_sum2(gd, red, part1, bar);
+    double2 g = grid_sum2(gd, red, part1, gs);
     double gamma = g.x;
     double alpha = g.y > 0.0 ? gamma / g.y : 0.0;
     double pi = ri, si = wi;
@@ -1906,14 +1955,14 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const 
         xi += alpha * pi;
         ri -= alpha * si;
         if (own) R[i] = ri;
-        grid_barrier(bar); // r published
+        gs.sync(); // r published
         wi = spmv(R);
         gd = make_double2(0.0, 0.0);
         if (own) {
             gd.x += ri * ri;
             gd.y += wi * ri;
         }
-        g = grid_sum2(gd, red, flip ? part1 : part0, bar);
+        g = grid_sum2(gd, red, flip ? part1 : part0, gs);
         flip ^= 1;
         const double gamma_new = g.x;
         const double beta = gamma_new / gamma;
@@ -1931,11 +1980,11 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const 
         ++it;
     }
     if (own) x[i] = xi;
-    grid_barrier(bar); // x complete
+    gs.sync(); // x complete
     const double ti = bi - spmv(x);
     double2 tr = make_double2(0.0, 0.0);
     if (own) tr.x += ti * ti;
-    const double res = sqrt(grid_sum2(tr, red, flip ? part1 : part0, bar).x);
+    const double res = sqrt(grid_sum2(tr, red, flip ? part1 : part0, gs).x);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->iterations = it;
         st->breakdown = breakdown;
@@ -1943,6 +1992,7 @@ __global__ void __launch_bounds__(CGG_THREADS) k_coarse_cg_reg(int64_t n, const 
         st->target = target;
         st->residual = res;
     }
+    gs.finish();
 }
 
 int64_t coarse_grid_min_rows() {
