@@ -340,6 +340,8 @@ int64_t mega_dofs_per_cta_default();
 void set_mega_dofs_per_cta_default(int64_t v);
 /// dst = A src (all flags) and returns src.dst, one pass over the faces
 double apply_dot(const Operator& A, Function& src, Function& dst, int level);
+/// r = rhs - A x and r.r in one pass over the faces (face partials from the stencil kernel's CTAs)
+double residual_dot(const Operator& A, Function& rhs, Function& x, Function& r, int level);
 /// the same with src.dst left on the device at *out (no host round trip)
 void apply_dot_dev(const Operator& A, Function& src, Function& dst, int level, double* out);
 /// prolongate_add(e -> x) then one weighted-Jacobi sweep, fused on the faces
@@ -435,6 +437,7 @@ class Hierarchy {
   public:
     bool use_graphs = true;
     bool fuse_post_ = true; // prolongate_add fused with the first post-sweep (Jacobi, coloured GS)
+    bool fuse_norm_ = true; // residual_norm: r.r from the residual kernel's own CTAs
     bool temporal_ = true;  // V(2, nu2 >= 2) Jacobi: the finest pre-smoothing pair as one two-sweep pass
     // Jacobi cycles from levels with n <= mega_max_n down as one cooperative kernel: 1 always,
     // 0 never, -1 (default) when the domain has at most mega_auto_faces faces (below that it

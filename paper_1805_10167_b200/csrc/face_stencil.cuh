@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
     const int jp_e0 = c - 1 >= 2 ? c - 1 : JP_NEVER, jp_e1 = c >= 2 ? c : JP_NEVER;
     const int jp_e2 = c + 1 >= 2 ? c + 1 : JP_NEVER, jp_e3 = c + 2 >= 2 ? c + 2 : JP_NEVER;
 
-    // optional dot partials (dotp): APPLY x.(Ax), JACOBI b.x_new, per lane for
+    // optional dot partials (dotp): APPLY x.(Ax), JACOBI b.x_new, RESIDUAL r.r, per lane for
     // its two columns over the band's rows, then a fixed tree over the CTA
     double d0 = 0.0, d1 = 0.0;
     // the fused restriction's loop unrolled by 6 (its row window and residual rows rotate with period
@@ -477,6 +477,9 @@ __global__ void __launch_bounds__(FS_THREADS, 4) k_face_stencil(LevelTables t, c
                     } else if (MODE == ST_JACOBI || JP) {
                         if (v0) d0 = d0 + bb.x * o0;
                         if (v1) d1 = d1 + bb.y * o1;
+                    } else if (MODE == ST_RESIDUAL) { // r.r (a solve's residual norm)
+                        if (v0) d0 = d0 + o0 * o0;
+                        if (v1) d1 = d1 + o1 * o1;
                     }
                 }
                 double* yrow = yf + ro[r];

@@ -737,7 +737,8 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
             else pdl_launch(k_face_stencil<ST_APPLY>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
             break;
         case ST_RESIDUAL:
-            pdl_launch(k_face_stencil<ST_RESIDUAL>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
+            if (dotp) pdl_launch(k_face_stencil<ST_RESIDUAL, true>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, dotp, nullptr, ev);
+            else pdl_launch(k_face_stencil<ST_RESIDUAL>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
             break;
         default:
             if (dotp) pdl_launch(k_face_stencil<ST_JACOBI, true>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, dotp, nullptr, ev);

@@ -99,7 +99,7 @@ enum StencilMode : int {
 void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const double* x, const double* b,
                     double* y, double omega, uint8_t mask, cudaStream_t st, int parts = 3,
                     double* dotp = nullptr);
-// dotp (APPLY: x.(Ax); JACOBI: b.x_new): one partial per face-kernel CTA,
+// dotp (APPLY: x.(Ax); JACOBI: b.x_new; RESIDUAL: r.r): one partial per face-kernel CTA,
 // face_dot_slots(t) per face, folded per face by launch_partials_finish
 int face_dot_slots(const LevelTables& t);
 void launch_partials_finish(const LevelTables& t, const double* u, const double* v, const double* scratch, int bands,

@@ -284,6 +284,31 @@ void apply_dot_dev(const Operator& A, Function& src, Function& dst, int level, d
     finish_dot_dev(d, t, src.data(level), dst.data(level), scratch, slots, part, out);
 }
 
+// r = rhs - A x and r.r in one pass over the faces (a solve's residual norm after each cycle):
+// the face partials come from the stencil kernel's CTAs, as apply_dot's do
+double residual_dot(const Operator& A, Function& rhs, Function& x, Function& r, int level) {
+    check_op_function(A, rhs, level, "residual", false);
+    check_op_function(A, x, level, "residual", false);
+    check_op_function(A, r, level, "residual", true);
+    if (&x == &r || &rhs == &r) throw InvalidArgument("residual: r must be distinct from x and rhs");
+    require_p1(x, "residual (fused)");
+    Domain& d = A.domain();
+    d.sync(x, level);
+    const LevelTables t = A.tables(level);
+    const int slots = face_dot_slots(t);
+    const int64_t np = int64_t(d.graph().size());
+    double* buf = d.partials(np + int64_t(t.nfaces) * slots + 1);
+    double* part = buf;
+    double* scratch = buf + np;
+    HYB_CUDA(cudaMemsetAsync(part, 0, size_t(np) * 8, d.stream()));
+    d.timer_begin("residual");
+    launch_stencil(ST_RESIDUAL, t, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
+                   d.stream(), 3, scratch);
+    d.timer_end();
+    finish_dot_dev(d, t, r.data(level), r.data(level), scratch, slots, part, d.scalar_out());
+    return to_host(d, d.scalar_out());
+}
+
 // the first weighted-Jacobi sweep of a cycle whose x starts at zero (see
 // ST_JACOBI_ZERO): x is neither synced nor read; Dirichlet rows take rhs,
 // exactly what the cycle's assign would have put there
@@ -1171,6 +1196,7 @@ void Hierarchy::check_coarse() {
 }
 
 double Hierarchy::residual_norm(Function& rhs, Function& x, int level) {
+    if (a_.kind() == KIND_P1 && fuse_norm_) return std::sqrt(residual_dot(a_, rhs, x, r_, level));
     residual(a_, rhs, x, r_, level);
     return std::sqrt(dot(r_, r_, level));
 }
