@@ -696,6 +696,55 @@ void launch_partials_finish(const LevelTables& t, const double* u, const double*
     }
 }
 
+// faces up to this size sweep through k_jacobi_dense (HYB_JACOBI_DENSE_MAX_N; 0: never)
+static int jacobi_dense_max_n() {
+    static const int v = [] {
+        const char* e = std::getenv("HYB_JACOBI_DENSE_MAX_N");
+        return e ? std::atoi(e) : 128;
+    }();
+    return v;
+}
+
+// Weighted Jacobi on small faces (n <= 128), a thread per interior point from the face's point
+// table (position in the face block, the two row strides; row-major, so a warp's loads and its
+// store are contiguous): x's seven values come through L1/L2 (a face is at most 67 KB). The tiled
+// ring kernel spends a pipeline stage per row however short the row is: on 8192 faces a level-7 sweep
+// took 651 us (0.38 of its bytes), level 6 381 us, level 5 246 us. Same term order and division as
+// k_face_stencil<ST_JACOBI>: bitwise.
+__global__ void __launch_bounds__(256) k_jacobi_dense(LevelTables t, const double* __restrict__ x,
+                                                      const double* __restrict__ b, double* __restrict__ y,
+                                                      double omega, const int2* __restrict__ tab, int count) {
+    pdl_prologue();
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= count) return;
+    const int face = blockIdx.y;
+    const double* co = t.face_coef + size_t(face) * 8;
+    const double cW = __ldg(co), cNW = __ldg(co + 1), cS = __ldg(co + 2), cC = __ldg(co + 3), cN = __ldg(co + 4),
+                 cSE = __ldg(co + 5), cE = __ldg(co + 6), dg = __ldg(co + 7);
+    const double rdg = 1.0 / dg;
+    const int2 e = __ldg(tab + i);
+    const int up = e.y >> 16, dn = e.y & 0xffff;
+    const int64_t base = int64_t(face) * t.face_stride + e.x;
+    const double* r0 = x + base;
+    const double* rm = r0 - dn;
+    const double* rp = r0 + up;
+    const double z0 = r0[0];
+    double a0 = 0.0; // reference term order W NW S C N SE E
+    a0 += cW * r0[-1];
+    a0 += cNW * rp[-1];
+    a0 += cS * rm[0];
+    a0 += cC * z0;
+    a0 += cN * rp[0];
+    a0 += cSE * rm[1];
+    a0 += cE * r0[1];
+    y[base] = z0 + div_by(omega * (__ldg(b + base) - a0), dg, rdg);
+}
+struct FacePointTable {
+    int2* dev = nullptr;
+    int count = 0;
+};
+static const FacePointTable& face_point_table(int n, int W); // every interior point, row-major
+
 void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const double* x, const double* b, double* y,
                     double omega, uint8_t mask, cudaStream_t st, int parts, double* dotp) {
     if (mode == ST_JACOBI_ZERO) {
@@ -721,9 +770,18 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
         dim3 grid = face_stencil_grid(t);
         EvTail ev;
         const unsigned ev_z = unsigned((blocks + int(grid.x * grid.y) - 1) / int(grid.x * grid.y));
+        // small faces, plain Jacobi: a thread per point (k_jacobi_dense); edges/vertices in their own launch
+        const bool dense = mode == ST_JACOBI && !dotp && !t.face_list && t.n >= 4 && t.n <= jacobi_dense_max_n() &&
+                           t.nfaces <= 65535;
+        if (dense) {
+            const FacePointTable& tb = face_point_table(t.n, t.W);
+            pdl_launch(k_jacobi_dense, dim3(unsigned((tb.count + 255) / 256), unsigned(t.nfaces)), 256, 0, st, t, x, b, y,
+                       omega, static_cast<const int2*>(tb.dev), tb.count);
+            check_launch("face stencil (dense jacobi)");
+        }
         // edge/vertex rows as trailing CTAs of the same launch, while grid.z stays
         // within its 65535 limit (else a separate k_ev_stencil launch below)
-        if ((parts & 2) && blocks > 0 && grid.z + ev_z <= 65535u) {
+        if (!dense && (parts & 2) && blocks > 0 && grid.z + ev_z <= 65535u) {
             ev.fl = fl;
             ev.mask = mask;
             ev.kblocks = kb;
@@ -731,7 +789,7 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
             grid.z += ev_z;
             ev_done = true;
         }
-        switch (mode) {
+        if (!dense) switch (mode) {
         case ST_APPLY:
             if (dotp) pdl_launch(k_face_stencil<ST_APPLY, true>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, dotp, nullptr, ev);
             else pdl_launch(k_face_stencil<ST_APPLY>, grid, FS_THREADS, 0, st, t, x, b, y, omega, nullptr, 0, nullptr, nullptr, ev);
@@ -1002,6 +1060,31 @@ static const CgsPointTable& cgs_point_table(int n, int W, cudaStream_t st) {
             throw CudaError("coloured gauss-seidel: cannot upload the point table");
     }
     (void)st;
+    return cache.emplace(key, tb).first->second;
+}
+
+static const FacePointTable& face_point_table(int n, int W) {
+    static std::map<std::pair<int, int>, FacePointTable> cache; // (device, n)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::pair<int, int> key(dev, n);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    std::vector<int2> host;
+    for (int r = 1; r <= n - 2; ++r) {
+        const int up = int(face_rowoff(W, r + 1) - face_rowoff(W, r));
+        const int dn = int(face_rowoff(W, r) - face_rowoff(W, r - 1));
+        for (int c = 1; c <= n - 1 - r; ++c) host.push_back(make_int2(int(face_rowoff(W, r)) + c, (up << 16) | dn));
+    }
+    FacePointTable tb;
+    tb.count = int(host.size());
+    if (cudaMalloc(&tb.dev, std::max<size_t>(host.size(), 1) * sizeof(int2)) != cudaSuccess)
+        throw CudaError("jacobi: cannot allocate the point table");
+    if (!host.empty() &&
+        cudaMemcpy(tb.dev, host.data(), host.size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess)
+        throw CudaError("jacobi: cannot upload the point table");
     return cache.emplace(key, tb).first->second;
 }
 

@@ -1,6 +1,7 @@
 // Operations on device-resident functions, with the reference's argument
 // checks and exception types (reference src/operators.cpp:322-505,
 // src/solvers.cpp:22-204, 385-465, src/function.cpp:11-241).
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -1137,7 +1138,13 @@ void Hierarchy::cycle(Function& rhs, Function& x, int level, int nu_pre, int nu_
     // Jacobi post-smoothing also fused with the first sweep
     auto dot_for = [&](int i) { return (level == cycle_dot_level_ && i == nu_post - 1) ? cycle_dot_ : nullptr; };
     int i0 = 0;
-    if (nu_post > 0 && smoother_ == SMOOTH_JACOBI && fuse_post_) {
+    // (on small faces the correction and the sweep run apart: the sweep is then the thread-per-point
+    // kernel, HYB_JP_UNFUSED_MAX_N)
+    static const int jp_unfused_max_n = [] {
+        const char* e = std::getenv("HYB_JP_UNFUSED_MAX_N");
+        return e ? std::atoi(e) : 128;
+    }();
+    if (nu_post > 0 && smoother_ == SMOOTH_JACOBI && fuse_post_ && (1 << level) > jp_unfused_max_n) {
         prolongate_add_jacobi(a_, e_, rhs, x, omega_, level - 1, dot_for(0));
         i0 = 1;
     } else if (nu_post > 0 && smoother_ == SMOOTH_CGS && fuse_post_) {
