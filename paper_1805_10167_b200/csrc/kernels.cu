@@ -705,12 +705,13 @@ static int jacobi_dense_max_n() {
     return v;
 }
 
-// Weighted Jacobi on small faces (n <= 128), a thread per interior point from the face's point
+// Apply, residual and weighted Jacobi on small faces (n <= 128), a thread per interior point from the face's point
 // table (position in the face block, the two row strides; row-major, so a warp's loads and its
 // store are contiguous): x's seven values come through L1/L2 (a face is at most 67 KB). The tiled
 // ring kernel spends a pipeline stage per row however short the row is: on 8192 faces a level-7 sweep
 // took 651 us (0.38 of its bytes), level 6 381 us, level 5 246 us. Same term order and division as
-// k_face_stencil<ST_JACOBI>: bitwise.
+// k_face_stencil's modes: bitwise.
+template <int MODE> // ST_APPLY, ST_RESIDUAL or ST_JACOBI, as k_face_stencil's
 __global__ void __launch_bounds__(256) k_jacobi_dense(LevelTables t, const double* __restrict__ x,
                                                       const double* __restrict__ b, double* __restrict__ y,
                                                       double omega, const int2* __restrict__ tab, int count) {
@@ -737,7 +738,9 @@ __global__ void __launch_bounds__(256) k_jacobi_dense(LevelTables t, const doubl
     a0 += cN * rp[0];
     a0 += cSE * rm[1];
     a0 += cE * r0[1];
-    y[base] = z0 + div_by(omega * (__ldg(b + base) - a0), dg, rdg);
+    if (MODE == ST_APPLY) y[base] = a0;
+    else if (MODE == ST_RESIDUAL) y[base] = __ldg(b + base) - a0;
+    else y[base] = z0 + div_by(omega * (__ldg(b + base) - a0), dg, rdg);
 }
 struct FacePointTable {
     int2* dev = nullptr;
@@ -771,13 +774,16 @@ void launch_stencil(int mode, const LevelTables& t, const FlagTables& fl, const 
         EvTail ev;
         const unsigned ev_z = unsigned((blocks + int(grid.x * grid.y) - 1) / int(grid.x * grid.y));
         // small faces, plain Jacobi: a thread per point (k_jacobi_dense); edges/vertices in their own launch
-        const bool dense = mode == ST_JACOBI && !dotp && !t.face_list && t.n >= 4 && t.n <= jacobi_dense_max_n() &&
-                           t.nfaces <= 65535;
+        const bool dense = (mode == ST_JACOBI || mode == ST_RESIDUAL || mode == ST_APPLY) && !dotp && !t.face_list &&
+                           t.n >= 4 && t.n <= jacobi_dense_max_n() && t.nfaces <= 65535;
         if (dense) {
             const FacePointTable& tb = face_point_table(t.n, t.W);
-            pdl_launch(k_jacobi_dense, dim3(unsigned((tb.count + 255) / 256), unsigned(t.nfaces)), 256, 0, st, t, x, b, y,
-                       omega, static_cast<const int2*>(tb.dev), tb.count);
-            check_launch("face stencil (dense jacobi)");
+            const dim3 dg(unsigned((tb.count + 255) / 256), unsigned(t.nfaces));
+            const int2* tab = tb.dev;
+            if (mode == ST_APPLY) pdl_launch(k_jacobi_dense<ST_APPLY>, dg, 256, 0, st, t, x, b, y, omega, tab, tb.count);
+            else if (mode == ST_RESIDUAL) pdl_launch(k_jacobi_dense<ST_RESIDUAL>, dg, 256, 0, st, t, x, b, y, omega, tab, tb.count);
+            else pdl_launch(k_jacobi_dense<ST_JACOBI>, dg, 256, 0, st, t, x, b, y, omega, tab, tb.count);
+            check_launch("face stencil (thread per point)");
         }
         // edge/vertex rows as trailing CTAs of the same launch, while grid.z stays
         // within its 65535 limit (else a separate k_ev_stencil launch below)
