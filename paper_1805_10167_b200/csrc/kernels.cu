@@ -1418,7 +1418,7 @@ void launch_jacobi_prolong_faces(const LevelTables& tc, const LevelTables& tf, c
 }
 
 void launch_residual_restrict_faces(const LevelTables& tc, const LevelTables& tf, const double* x, const double* b,
-                                    double* r, double* xc, cudaStream_t st) {
+                                    double* r, double* xc, cudaStream_t st, cudaStream_t st_layer) {
     if (tf.nfaces <= 0 || tf.n < 3) return;
     if (tc.n >= 3) {
         pdl_launch(k_face_stencil<ST_RESTRICT_RESIDUAL>, face_rr_grid(tf), FS_THREADS, 0, st, tf, x, b, xc, 0.0, tc.rowoff,
@@ -1426,7 +1426,8 @@ void launch_residual_restrict_faces(const LevelTables& tc, const LevelTables& tf
         check_launch("residual+restrict faces");
     }
     const dim3 grid(unsigned((tf.n - 2 + 127) / 128), 3u, unsigned(tf.nfaces));
-    pdl_launch(k_residual_layer, grid, 128, 0, st, tf, x, b, r);
+    // (the layer reads x and b and writes r's layer points only: independent of the face kernel)
+    pdl_launch(k_residual_layer, grid, 128, 0, st_layer ? st_layer : st, tf, x, b, r);
     check_launch("residual border layer");
 }
 

@@ -135,8 +135,10 @@ void launch_prolongate_layer(const LevelTables& coarse, const LevelTables& fine,
 void launch_jacobi_prolong_faces(const LevelTables& coarse, const LevelTables& fine, const double* x, const double* xc,
                                  const double* b, double* y, double omega, double* dotp, cudaStream_t st,
                                  const FlagTables* ev_flags = nullptr);
+// st_layer (optional): the stream of the border-layer kernel, which is independent of the face kernel
 void launch_residual_restrict_faces(const LevelTables& coarse, const LevelTables& fine, const double* x,
-                                    const double* b, double* r, double* xc, cudaStream_t st);
+                                    const double* b, double* r, double* xc, cudaStream_t st,
+                                    cudaStream_t st_layer = nullptr);
 // hybrid Gauss-Seidel: face tiles (face, I, J, dependency bits) over skewed
 // coordinates (t = c + 2r in GS_TILE_COLS-wide slabs, rows in GS_TILE_ROWS),
 // queue ordered by I + J; per-tile done flags and the queue counter zeroed by

@@ -664,11 +664,16 @@ void residual_restrict(const Operator& A, Function& rhs, Function& x, Function& 
     d.sync(x, level);
     const LevelTables t = A.tables(level);
     const LevelTables& tc = d.level(lc).t;
+    // the faces' border layer and the edge/vertex rows of r on the side stream, beside the face kernel
+    // (all three read x and rhs only and write disjoint parts of r / coarse)
+    d.fork();
     d.timer_begin("residual_restrict");
-    launch_residual_restrict_faces(tc, t, x.data(level), rhs.data(level), r.data(level), coarse.data(lc), d.stream());
+    launch_residual_restrict_faces(tc, t, x.data(level), rhs.data(level), r.data(level), coarse.data(lc), d.stream(),
+                                   d.aux_stream());
     d.timer_end();
     launch_stencil(ST_RESIDUAL, t, r.flags(), x.data(level), rhs.data(level), r.data(level), 0.0, ALL_FLAGS,
-                   d.stream(), 2);
+                   d.aux_stream(), 2);
+    d.join();
     d.sync(r, level);
     launch_restrict_ev(tc, t, coarse.flags(), r.data(level), coarse.data(lc), ALL_FLAGS, d.stream());
 }
