@@ -12,6 +12,9 @@ timeout 1200 python -m pytest tests -m gpu -q > "$out/pytest_gpu.log" 2>&1; echo
 timeout 900 python bench.py > "$out/bench.json" 2> "$out/bench.err"; echo "bench_exit=$?" >> "$out/bench.err"
 timeout 900 python bench.py --impl reference > "$out/bench_ref.json" 2> "$out/bench_ref.err"
 timeout 900 python tools/configs_time.py > "$out/configs_time.jsonl" 2> "$out/configs_time.err"
+# graph-replayed cycles (five after three warm-ups) and config 3's cycle by operation
+{ timeout 300 python tools/cfg3_cycles.py 9; timeout 300 python tools/jac_cycles.py cfg2; timeout 300 python tools/jac_cycles.py faces8192; } > "$out/cycles.txt" 2>&1
+timeout 300 python tools/cfg3_profile.py > "$out/cfg3_profile.txt" 2>&1
 if timeout 600 python bench.py --steps 2 --warmup 1 > "$out/bench_short.json" 2>&1; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
     --log-file "$out/bench_launches.csv" python bench.py --steps 2 --warmup 1 > "$out/ncu_launches.log" 2>&1
