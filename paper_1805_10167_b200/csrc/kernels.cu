@@ -1156,7 +1156,7 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
         // two faces per CTA (k_cgs_duo), config 3 L8: 1.351-1.376 ms per sweep with one point per lane
         // and iteration (branch-free); two points, the second skipped by a branch (HYB_CGS_CFG=31) 1.450;
         // one face per CTA (k_cgs_cols, HYB_CGS_CFG=20) 1.700; four faces per CTA (two CTAs per SM) 1.622 /
-        // 1.538; 4 CTAs per SM (64 registers) 1.598 (1.405 with one point per lane), K = 4 1.548, D = 2 1.636,
+        // 1.538; 4 CTAs per SM (64 registers) 1.598 (1.405 with one point per lane), K = 4 1.548 (1.709 with one point per lane; K = 3: 1.714-1.889), D = 2 1.636,
         // D = 4 1.452;
         // at n = 128 the whole-face kernel stays ahead (0.430 ms against 0.54-0.67)
         launch_cgs_duo<2, 3, 256, 3, 1>(t, b, x, st);
