@@ -1001,12 +1001,17 @@ __global__ void __launch_bounds__(CgdCfg<K, D, NMAX, NP>::THREADS, MINB)
     int r = 1 - S * colour + roff; // virtual row
     auto wrap = [](int v, int m) { return ((v % m) + m) % m; };
     int sxm = wrap(r - 1, RX), sx0 = wrap(r, RX), sxp = wrap(r + 1, RX), sb = wrap(r, RB);
+    // first column's residue of this colour on face A's row r and face B's row n-1-r, kept up to date
+    // per step (r += K) instead of two divisions per step
+    int t3a = wrap(colour - 2 * r, 3), t3b = wrap(colour - 2 * (n - 1 - r), 3);
+    constexpr int DT3A = (3 - (2 * K) % 3) % 3, DT3B = (2 * K) % 3;
 #pragma unroll 1
     for (int i = 0; i < nsteps; ++i) {
         mbar_wait(&full[i % NB], uint32_t((i / NB) & 1));
         if (r >= 1 && r <= last) {
-#pragma unroll 1
-            for (int s = 0; s < nf; ++s) {
+#pragma unroll
+            for (int s = 0; s < 2 * NP; ++s) { // unrolled: the side and the pair are constants in each copy
+                if (s >= nf) break;
                 // face row rr; rows rr-1 / rr+1 are virtual r-1 / r+1 for A, r+1 / r-1 for B
                 const int side = s & 1, pbase = (s >> 1) * PS;
                 const int rr = side ? n - 1 - r : r;
@@ -1020,7 +1025,7 @@ __global__ void __launch_bounds__(CgdCfg<K, D, NMAX, NP>::THREADS, MINB)
                 for (int k = 0; k < 8; ++k) co[k] = cosm[s * 10 + k];
                 const double rd = cosm[s * 10 + 8];
                 const int cmax = n - 1 - rr;
-                const int t3 = wrap(colour - 2 * rr, 3);
+                const int t3 = side ? t3b : t3a;
                 const int cs = t3 == 0 ? 3 : t3; // first column >= 1 of this colour
                 if constexpr (NPT > 0) {
                     // NPT points per lane and iteration, branch-free: a lane past the row's end
@@ -1072,6 +1077,8 @@ __global__ void __launch_bounds__(CgdCfg<K, D, NMAX, NP>::THREADS, MINB)
         sx0 = sx0 + K >= RX ? sx0 + K - RX : sx0 + K;
         sxp = sxp + K >= RX ? sxp + K - RX : sxp + K;
         sb = sb + K >= RB ? sb + K - RB : sb + K;
+        t3a = t3a + DT3A >= 3 ? t3a + DT3A - 3 : t3a + DT3A;
+        t3b = t3b + DT3B >= 3 ? t3b + DT3B - 3 : t3b + DT3B;
     }
 }
 
