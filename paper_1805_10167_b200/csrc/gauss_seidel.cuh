@@ -903,7 +903,7 @@ template <int K, int D, int NMAX, int NP = 1> struct CgdCfg {
 // NP: face pairs per CTA (faces 2 NP blockIdx.x ...; the per-step cost is then shared by 2 NP
 // faces, which pays on smaller faces whose rows are short). NPT = 0: two points per lane and
 // iteration, the second skipped by a branch; NPT >= 1: NPT points, branch-free (see below).
-template <int K, int D, int NMAX, int MINB, int NPT = 0, int NP = 1>
+template <int K, int D, int NMAX, int MINB, int NPT = 0, int NP = 1, int COR = 0>
 __global__ void __launch_bounds__(CgdCfg<K, D, NMAX, NP>::THREADS, MINB)
     k_cgs_duo(LevelTables t, const double* __restrict__ b, double* x, const double* __restrict__ zsrc) {
     pdl_prologue();
@@ -1005,6 +1005,13 @@ __global__ void __launch_bounds__(CgdCfg<K, D, NMAX, NP>::THREADS, MINB)
     // per step (r += K) instead of two divisions per step
     int t3a = wrap(colour - 2 * r, 3), t3b = wrap(colour - 2 * (n - 1 - r), 3);
     constexpr int DT3A = (3 - (2 * K) % 3) % 3, DT3B = (2 * K) % 3;
+    // COR: the first COR faces' coefficients stay in registers for the whole sweep (the others are read
+    // from shared memory at every step)
+    double cor[COR > 0 ? COR : 1][9];
+#pragma unroll
+    for (int s = 0; s < COR; ++s)
+#pragma unroll
+        for (int k = 0; k < 9; ++k) cor[s][k] = s < nf ? cosm[s * 10 + k] : 0.0;
 #pragma unroll 1
     for (int i = 0; i < nsteps; ++i) {
         mbar_wait(&full[i % NB], uint32_t((i / NB) & 1));
@@ -1022,8 +1029,8 @@ __global__ void __launch_bounds__(CgdCfg<K, D, NMAX, NP>::THREADS, MINB)
                 const double* br = bring + sb * RS + o0;
                 double co[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) co[k] = cosm[s * 10 + k];
-                const double rd = cosm[s * 10 + 8];
+                for (int k = 0; k < 8; ++k) co[k] = s < COR ? cor[s < COR ? s : 0][k] : cosm[s * 10 + k];
+                const double rd = s < COR ? cor[s < COR ? s : 0][8] : cosm[s * 10 + 8];
                 const int cmax = n - 1 - rr;
                 const int t3 = side ? t3b : t3a;
                 const int cs = t3 == 0 ? 3 : t3; // first column >= 1 of this colour

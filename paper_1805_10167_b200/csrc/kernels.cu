@@ -1009,14 +1009,14 @@ bool launch_cgs_cols(const LevelTables& t, const double* b, double* x, double* y
 }
 
 // two faces (NP pairs of faces) per CTA (k_cgs_duo): in place
-template <int K, int D, int NMAX, int MINB, int NPT = 0, int NP = 1>
+template <int K, int D, int NMAX, int MINB, int NPT = 0, int NP = 1, int COR = 0>
 void launch_cgs_duo(const LevelTables& t, const double* b, double* x, cudaStream_t st, const double* zsrc = nullptr) {
     using C = CgdCfg<K, D, NMAX, NP>;
-    static const bool attr = cudaFuncSetAttribute(k_cgs_duo<K, D, NMAX, MINB, NPT, NP>,
+    static const bool attr = cudaFuncSetAttribute(k_cgs_duo<K, D, NMAX, MINB, NPT, NP, COR>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)) ==
                              cudaSuccess;
     if (!attr) throw CudaError("coloured gauss-seidel: cannot reserve shared memory");
-    pdl_launch(k_cgs_duo<K, D, NMAX, MINB, NPT, NP>, unsigned((t.nfaces + 2 * NP - 1) / (2 * NP)), C::THREADS, C::SMEM,
+    pdl_launch(k_cgs_duo<K, D, NMAX, MINB, NPT, NP, COR>, unsigned((t.nfaces + 2 * NP - 1) / (2 * NP)), C::THREADS, C::SMEM,
                st, t, b, x, zsrc);
 }
 
@@ -1148,6 +1148,14 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
         if (v == 31) launch_cgs_duo<2, 3, 256, 3, 0>(t, b, x, st);
         else if (v == 32) launch_cgs_duo<2, 3, 256, 2, 1, 2>(t, b, x, st);
         else launch_cgs_duo<2, 3, 256, 2, 0, 2>(t, b, x, st);
+    } else if (n == 256 && v == 38 && !t.face_list) {
+        launch_cgs_duo<2, 3, 256, 3, 1, 1, 1>(t, b, x, st);
+    } else if (n == 256 && v == 39 && !t.face_list) {
+        launch_cgs_duo<2, 3, 256, 3, 1, 1, 2>(t, b, x, st);
+    } else if (n == 512 && v == 38 && !t.face_list) {
+        launch_cgs_duo<2, 3, 512, 2, 0, 1, 1>(t, b, x, st);
+    } else if (n == 512 && v == 39 && !t.face_list) {
+        launch_cgs_duo<2, 3, 512, 2>(t, b, x, st); // COR = 0: the default before COR
     } else if (n == 512 && v == 31 && !t.face_list) {
         launch_cgs_duo<2, 3, 512, 2, 1>(t, b, x, st);
     } else if (n == 512 && v == 32 && !t.face_list) {
@@ -1163,8 +1171,11 @@ bool launch_cgs_faces_cols(const LevelTables& t, const double* b, double* x, dou
     } else if (n == 512 && v != 20 && !t.face_list) {
         // config 3 L9: 4.70-4.74 ms per sweep (0.83 of the copy peak) against 5.545 one face per CTA;
         // one point per lane (HYB_CGS_CFG=31) 4.83, 2 / 3 / 4 points branch-free 4.88 / 5.21 / 5.62;
-        // K = 4 (one CTA per SM) 5.078, D = 2 5.248, K = 3 / D = 1 7.435
-        launch_cgs_duo<2, 3, 512, 2>(t, b, x, st);
+        // K = 4 (one CTA per SM) 5.078, D = 2 5.248, K = 3 / D = 1 7.435;
+        // after the side loop was unrolled: face kernel 4.349 ms, with the first face's coefficients in
+        // registers (COR = 1, HYB_CGS_CFG=38) 4.244, the first two (COR = 2) 4.186 -- at n = 256 COR
+        // costs (1.242 -> 1.32), so it stays off there
+        launch_cgs_duo<2, 3, 512, 2, 0, 1, 2>(t, b, x, st);
     } else if (n == 256) {
         // config 3 L8: 4 CTAs per SM (64 registers) 1.705 ms per sweep; 3 CTAs 1.828, D = 2 1.884,
         // 128-column blocks out of place 2.42-2.44
