@@ -376,10 +376,12 @@ void smooth_cgs(const Operator& A, Function& rhs, Function& x, int level) {
     // several blocks per face sweep out of place into the Jacobi scratch arena,
     // with the edges and vertices, and the scratch is swapped in
     DevMem& next = d.jacobi_scratch(level);
+    // the edges and vertices read only their own rows and their halo copies (frozen by the sync
+    // above) and the faces only theirs, so the two run side by side, as in smooth_gs
+    d.fork();
     d.timer_begin("coloured_gs");
     const bool oop = launch_cgs_faces_cols(t, rhs.data(level), x.data(level), next.as<double>(), d.stream());
     d.timer_end();
-    d.fork();
     if (oop) launch_cgs_ev_oop(t, x.flags(), rhs.data(level), x.data(level), next.as<double>(), d.aux_stream());
     else launch_cgs_ev(t, x.flags(), rhs.data(level), x.data(level), d.aux_stream());
     d.join();
