@@ -431,10 +431,10 @@ bool smooth_cgs_zero(const Operator& A, Function& rhs, Function& x, int level) {
     double* xa = x.data(level);
     if (t.arena_size > t.faces_size)
         HYB_CUDA(cudaMemsetAsync(xa + t.faces_size, 0, size_t(t.arena_size - t.faces_size) * 8, d.stream()));
+    d.fork(); // after the memset; edges/vertices beside the faces, as in smooth_cgs
     d.timer_begin("coloured_gs");
     launch_cgs_faces_zero(t, rhs.data(level), xa, d.stream());
     d.timer_end();
-    d.fork();
     launch_cgs_ev(t, x.flags(), rhs.data(level), xa, d.aux_stream());
     d.join();
     return true;
@@ -617,10 +617,10 @@ void prolongate_add_cgs(const Operator& A, Function& e, Function& rhs, Function&
     launch_prolongate_layer(tc, t, e.data(lc), x.data(level), d.stream());
     d.sync(x, level);
     DevMem& next = d.jacobi_scratch(level);
+    d.fork(); // edges/vertices beside the faces, as in smooth_cgs
     d.timer_begin("coloured_gs_prolong");
     const int oop = launch_cgs_prolong(tc, t, rhs.data(level), x.data(level), next.as<double>(), e.data(lc), d.stream());
     d.timer_end();
-    d.fork();
     if (oop) launch_cgs_ev_oop(t, x.flags(), rhs.data(level), x.data(level), next.as<double>(), d.aux_stream());
     else launch_cgs_ev(t, x.flags(), rhs.data(level), x.data(level), d.aux_stream());
     d.join();
